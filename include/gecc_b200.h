@@ -1,0 +1,212 @@
+/*
+ * gecc_b200.h -- C ABI of libgecc_b200.so, the B200 (sm_100a) batched
+ * elliptic-curve engine.
+ *
+ * Part 1 is the drop-in boundary: the exact entry points, enum values and struct
+ * layouts of the reference library's C interface
+ * (/root/reference/proj/include/sm2batch.h), so a consumer of libsm2batch.so
+ * can link this library instead.  Each declaration cites the line it replaces.
+ * Part 2 adds what the reference's C++ batch API offers (batch_invert.hpp,
+ * batch_point.hpp) in C form -- flat column-major arrays, host or device
+ * pointers -- plus a curve selector (SM2 / secp256k1) and MSM.
+ *
+ * Record formats (sm2batch.h:4-9): all big-endian, flat arrays:
+ *   scalar / digest / secret 32 B, point 65 B (0x04 || X || Y),
+ *   signature 64 B (r || s), shared secret 32 B.
+ * Column buffers (batch_buffer.hpp:15-35): limb k of element i at cols[k*n + i],
+ *   least-significant limb first, 8 limbs; field elements are in Montgomery form
+ *   (R = 2^256), scalars are plain integers.  Infinity masks are one byte per
+ *   element (1 = point at infinity) and infinity coordinates are written as zero
+ *   (batch_point.cpp:41-47).
+ *
+ * There is no CPU fallback: every compute entry point runs CUDA kernels and
+ * returns SM2B_ERROR_INTERNAL (see gecc_last_error) if no device is usable.
+ */
+#ifndef GECC_B200_H
+#define GECC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ===================== Part 1: drop-in for sm2batch.h ===================== */
+
+/* sm2batch.h:27-36 */
+typedef enum sm2b_status {
+    SM2B_OK = 0,
+    SM2B_ERROR_INVALID_ARGUMENT = 1,
+    SM2B_ERROR_MALFORMED_INPUT = 2,
+    SM2B_ERROR_INVALID_PEER = 3,
+    SM2B_ERROR_DEGENERATE = 4,
+    SM2B_ERROR_NONCE_EXHAUSTED = 5,
+    SM2B_ERROR_NO_CROSSOVER = 6,
+    SM2B_ERROR_INTERNAL = 7
+} sm2b_status;
+
+/* sm2batch.h:41 -- opaque; here it owns a CUDA stream, device scratch and the
+ * fixed-base tables instead of a worker pool. Calls on one context serialise. */
+typedef struct sm2b_ctx sm2b_ctx;
+
+/* sm2batch.h:44-45.  SM2 curve on the current CUDA device.  `workers` and `lanes`
+ * are accepted for compatibility; results are lane-count invariant by contract
+ * (batch_invert.hpp:59-60) and the grid replaces the pool.  NULL on failure. */
+sm2b_ctx* sm2b_ctx_new(uint32_t workers, uint32_t lanes);
+void sm2b_ctx_free(sm2b_ctx* ctx);
+
+/* sm2batch.h:47-48 */
+const char* sm2b_version(void);
+const char* sm2b_status_str(sm2b_status status);
+
+/* sm2batch.h:51-59.  The GPU kernels do not count operations; the ledger is
+ * advanced with the reference algorithm's closed-form counts for each call
+ * (SURVEY.md section 5), so economics checks written against the reference
+ * (e.g. modinv == 257 per sign call) keep their meaning. */
+typedef struct sm2b_op_counts {
+    uint64_t modmul;
+    uint64_t modadd;
+    uint64_t modsub;
+    uint64_t modinv;
+} sm2b_op_counts;
+sm2b_status sm2b_ledger_read(const sm2b_ctx* ctx, sm2b_op_counts* out);
+sm2b_status sm2b_ledger_reset(sm2b_ctx* ctx);
+
+/* sm2batch.h:63-64 */
+sm2b_status sm2b_keygen(sm2b_ctx* ctx, uint64_t seed, size_t count, uint8_t* secrets,
+                        uint8_t* publics);
+/* sm2batch.h:69-71 */
+sm2b_status sm2b_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
+                      const uint8_t* secrets, uint64_t nonce_seed, uint8_t* signatures,
+                      int32_t* lane_status);
+/* sm2batch.h:75-77 */
+sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
+                        const uint8_t* publics, const uint8_t* signatures,
+                        uint8_t* results);
+/* sm2batch.h:80-82 */
+sm2b_status sm2b_ecdh(sm2b_ctx* ctx, size_t count, const uint8_t* secrets,
+                      const uint8_t* peers, uint8_t* shared, int32_t* lane_status);
+/* sm2batch.h:86-87 */
+sm2b_status sm2b_crossover_n(uint64_t cost_add, uint64_t cost_mul, uint64_t cost_inv,
+                             uint64_t* out_n);
+
+/* sm2batch.h:89-96 */
+typedef struct sm2b_bench_report {
+    uint64_t lanes_used;
+    double wall_seconds;
+    double throughput;
+    sm2b_op_counts ops;
+    uint64_t modeled_cost;
+    int equivalence_checked;
+} sm2b_bench_report;
+/* sm2batch.h:102-105.  op: padd|fpmul|upmul|sign|verify; strategy: affine-batch
+ * (GPU batch kernels) | jacobian-serial (GPU per-lane Jacobian kernels).  Both
+ * are run once and compared before timing (bench.cpp:253-256). */
+sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, size_t n,
+                           size_t lanes, uint32_t workers, uint64_t seed, uint32_t repeats,
+                           sm2b_bench_report* out);
+
+/* ========================== Part 2: extensions ========================== */
+
+typedef enum gecc_curve { GECC_CURVE_SM2 = 0, GECC_CURVE_SECP256K1 = 1 } gecc_curve;
+typedef enum gecc_field { GECC_FIELD_P = 0, GECC_FIELD_N = 1 } gecc_field;
+/* same numbering as the oracle's field ops */
+typedef enum gecc_field_opcode {
+    GECC_OP_MONT_MUL = 0, /* field.cpp:205-211 */
+    GECC_OP_MOD_ADD = 1,  /* field.cpp:213-219 */
+    GECC_OP_MOD_SUB = 2,  /* field.cpp:221-227 */
+    GECC_OP_TO_MONT = 3,  /* field.cpp:194-198 */
+    GECC_OP_FROM_MONT = 4,/* field.cpp:200-203 */
+    GECC_OP_MOD_INV = 5   /* field.cpp:239-246, zero maps to zero */
+} gecc_field_opcode;
+
+/* Context for `curve` on CUDA device `device` (< 0: the current device). */
+sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device);
+int gecc_ctx_curve(const sm2b_ctx* ctx);
+int gecc_ctx_device(const sm2b_ctx* ctx);
+/* Message of the last failing call on this context ("" if none). */
+const char* gecc_last_error(const sm2b_ctx* ctx);
+/* Number of CUDA kernels this context has launched so far. */
+uint64_t gecc_kernel_launches(const sm2b_ctx* ctx);
+/* Use `stream` (a cudaStream_t) for all following calls; NULL = context's own. */
+sm2b_status gecc_ctx_set_stream(sm2b_ctx* ctx, void* stream);
+
+/* Sharded forms of keygen / sign: `lane_base` is the global index of lane 0 of
+ * this call, used as the nonce stream id (protocol.cpp:125-126), so a batch split
+ * over several GPUs / calls produces the same bytes as one call. */
+sm2b_status gecc_keygen(sm2b_ctx* ctx, uint64_t seed, uint64_t lane_base, size_t count,
+                        uint8_t* secrets, uint8_t* publics);
+sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
+                      const uint8_t* secrets, uint64_t nonce_seed, uint64_t lane_base,
+                      uint8_t* signatures, int32_t* lane_status);
+
+/* Element-wise field operation on column buffers (host pointers). */
+sm2b_status gecc_field_op(sm2b_ctx* ctx, gecc_field field, gecc_field_opcode op, size_t n,
+                          const uint32_t* a, const uint32_t* b, uint32_t* out);
+
+/* batch_invert (batch_invert.hpp:61-63): element-wise inverse, zero -> zero. */
+sm2b_status gecc_batch_invert(sm2b_ctx* ctx, gecc_field field, size_t n, const uint32_t* in,
+                              uint32_t* out);
+/* batch_padd (batch_point.hpp:47-49): out[i] = p[i] + t[i], complete. */
+sm2b_status gecc_batch_padd(sm2b_ctx* ctx, size_t n, const uint32_t* px, const uint32_t* py,
+                            const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty,
+                            const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf);
+/* batch_pdbl (batch_point.hpp:52-53) */
+sm2b_status gecc_batch_pdbl(sm2b_ctx* ctx, size_t n, const uint32_t* px, const uint32_t* py,
+                            const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf);
+/* batch_fpmul (batch_point.hpp:89-91): out[i] = scalars[i] * G, scalars raw 256-bit. */
+sm2b_status gecc_batch_fpmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, uint32_t* ox,
+                             uint32_t* oy, uint8_t* oinf);
+/* batch_upmul (batch_point.hpp:72-74): out[i] = scalars[i] * p[i]. */
+sm2b_status gecc_batch_upmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars,
+                             const uint32_t* px, const uint32_t* py, const uint8_t* pinf,
+                             uint32_t* ox, uint32_t* oy, uint8_t* oinf);
+/* MSM (no reference counterpart): out = sum_i scalars[i]*p[i],
+ * one affine point (ox, oy: 8 limbs each; *oinf). */
+sm2b_status gecc_msm(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uint32_t* px,
+                     const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
+                     uint8_t* oinf);
+
+/* Device-resident forms: identical semantics, all pointers are device memory on
+ * the context's device, work is enqueued on the context's stream and NOT
+ * synchronised (the caller owns ordering). */
+sm2b_status gecc_field_op_dev(sm2b_ctx* ctx, gecc_field field, gecc_field_opcode op, size_t n,
+                              const uint32_t* a, const uint32_t* b, uint32_t* out);
+sm2b_status gecc_batch_invert_dev(sm2b_ctx* ctx, gecc_field field, size_t n,
+                                  const uint32_t* in, uint32_t* out);
+sm2b_status gecc_batch_padd_dev(sm2b_ctx* ctx, size_t n, const uint32_t* px,
+                                const uint32_t* py, const uint8_t* pinf, const uint32_t* tx,
+                                const uint32_t* ty, const uint8_t* tinf, uint32_t* ox,
+                                uint32_t* oy, uint8_t* oinf);
+sm2b_status gecc_batch_pdbl_dev(sm2b_ctx* ctx, size_t n, const uint32_t* px,
+                                const uint32_t* py, const uint8_t* pinf, uint32_t* ox,
+                                uint32_t* oy, uint8_t* oinf);
+sm2b_status gecc_batch_fpmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars,
+                                 uint32_t* ox, uint32_t* oy, uint8_t* oinf);
+sm2b_status gecc_batch_upmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars,
+                                 const uint32_t* px, const uint32_t* py, const uint8_t* pinf,
+                                 uint32_t* ox, uint32_t* oy, uint8_t* oinf);
+sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
+                            const uint8_t* publics, const uint8_t* signatures,
+                            uint8_t* results);
+sm2b_status gecc_sign_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
+                          const uint8_t* secrets, uint64_t nonce_seed, uint64_t lane_base,
+                          uint8_t* signatures, int32_t* lane_status);
+sm2b_status gecc_msm_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uint32_t* px,
+                         const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
+                         uint8_t* oinf);
+
+/* Integer-pipe issue-rate microbenchmark (roofline denominator).
+ * which: 0 IMAD.WIDE.U32 independent, 1 IMAD.WIDE dependent chain, 2 IMAD (32-bit),
+ *        3 IMAD.HI, 4 IADD3, 5 IADD3.X carry chain, 6 IMAD.WIDE + IADD3 1:1 mix,
+ *        7 secp256k1 fe_mul, 8 generic fe_mul, 9 secp256k1 fe_add+fe_sub.
+ * Fills ops_per_clk_per_sm (thread-level operations per SM clock per SM, from
+ * clock64 spans) and seconds (CUDA-event time); iters = inner loop trip count. */
+sm2b_status gecc_microbench(sm2b_ctx* ctx, int which, int iters, double* ops_per_clk_per_sm,
+                            double* seconds, double* total_ops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GECC_B200_H */

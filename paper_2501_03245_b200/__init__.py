@@ -1,0 +1,13 @@
+"""gecc-b200: batched elliptic-curve engine for NVIDIA B200 (sm_100a).
+
+Python is only a thin ctypes view of ``lib/libgecc_b200.so`` (the product is the
+CUDA library behind the C ABI in ``include/gecc_b200.h``).  There is no CPU
+implementation here: importing works anywhere, but creating a Context needs the
+compiled library and a CUDA device and raises loudly otherwise.
+"""
+from .capi import (Context, GeccError, LIB_PATH, SM2, SECP256K1, STATUS, lib, lib_available,
+                   cols_from_ints, ints_from_cols)
+
+__all__ = ["Context", "GeccError", "LIB_PATH", "SM2", "SECP256K1", "STATUS", "lib",
+           "lib_available", "cols_from_ints", "ints_from_cols"]
+__version__ = "0.1.0"

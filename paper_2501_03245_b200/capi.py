@@ -1,0 +1,247 @@
+"""ctypes binding of include/gecc_b200.h.
+
+Method names and argument meaning mirror the reference's interface for this path
+(sm2batch.h: keygen / sign / verify / ecdh; batch_point.hpp: batch_padd / batch_pdbl /
+batch_fpmul / batch_upmul; batch_invert.hpp: batch_invert) so that the parity tests
+read like the reference's own tests.  Column buffers are numpy uint32 arrays of shape
+(8, n): arr[k, i] = limb k of element i (batch_buffer.hpp:15-35).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "lib", "libgecc_b200.so")
+
+SM2, SECP256K1 = 0, 1
+FIELD_P, FIELD_N = 0, 1
+STATUS = {0: "ok", 1: "invalid argument", 2: "malformed input", 3: "invalid peer point",
+          4: "degenerate result", 5: "nonce retries exhausted", 6: "cost model has no crossover",
+          7: "internal error"}
+FIELD_OPS = dict(mont_mul=0, mod_add=1, mod_sub=2, to_mont=3, from_mont=4, mod_inv=5)
+
+
+class GeccError(RuntimeError):
+    pass
+
+
+_lib = None
+
+
+def lib_available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    """Loads libgecc_b200.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not lib_available():
+            raise GeccError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; "
+                            "g.build()'` or `make -C paper_2501_03245_b200/csrc`")
+        l = C.CDLL(LIB_PATH, mode=os.RTLD_LOCAL)
+        l.sm2b_ctx_new.restype = C.c_void_p
+        l.sm2b_ctx_new.argtypes = [C.c_uint32, C.c_uint32]
+        l.gecc_ctx_new.restype = C.c_void_p
+        l.gecc_ctx_new.argtypes = [C.c_int, C.c_int]
+        l.sm2b_ctx_free.argtypes = [C.c_void_p]
+        l.sm2b_version.restype = C.c_char_p
+        l.sm2b_status_str.restype = C.c_char_p
+        l.gecc_last_error.restype = C.c_char_p
+        l.gecc_last_error.argtypes = [C.c_void_p]
+        l.gecc_kernel_launches.restype = C.c_uint64
+        l.gecc_kernel_launches.argtypes = [C.c_void_p]
+        _lib = l
+    return _lib
+
+
+def cols_from_ints(vals) -> np.ndarray:
+    n = len(vals)
+    raw = b"".join(int(v).to_bytes(32, "little") for v in vals)
+    return np.ascontiguousarray(np.frombuffer(raw, dtype="<u4").reshape(n, 8).T)
+
+
+def ints_from_cols(cols: np.ndarray):
+    rows = np.ascontiguousarray(cols.T).astype("<u4")
+    return [int.from_bytes(rows[i].tobytes(), "little") for i in range(rows.shape[0])]
+
+
+def _vp(a):
+    """numpy array / bytes / int (raw address) / None -> void pointer argument"""
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        assert a.flags["C_CONTIGUOUS"]
+        return C.c_void_p(a.ctypes.data)
+    if isinstance(a, (bytes, bytearray)):
+        return C.cast(C.c_char_p(bytes(a)), C.c_void_p) if len(a) else None
+    return C.c_void_p(int(a))
+
+
+class Context:
+    """One engine context = one CUDA device + one curve (sm2b_ctx, sm2batch.h:41-45)."""
+
+    def __init__(self, curve: int = SM2, device: int = -1, reference_compat: bool = False,
+                 workers: int = 0, lanes: int = 0):
+        self.l = lib()
+        if reference_compat:
+            h = self.l.sm2b_ctx_new(workers, lanes)
+        else:
+            h = self.l.gecc_ctx_new(curve, device)
+        if not h:
+            raise GeccError("gecc_ctx_new failed: no usable CUDA device or bad arguments "
+                            "(libgecc_b200 has no CPU path)")
+        self.h = C.c_void_p(h)
+        self.curve = self.l.gecc_ctx_curve(self.h)
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.l.sm2b_ctx_free(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- plumbing
+    def _check(self, rc, what):
+        if rc == 7:
+            raise GeccError(f"{what}: {self.l.gecc_last_error(self.h).decode()}")
+        return rc
+
+    @property
+    def launches(self) -> int:
+        return int(self.l.gecc_kernel_launches(self.h))
+
+    def set_stream(self, stream_ptr: int | None):
+        self.l.gecc_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0))
+
+    def ledger(self):
+        arr = (C.c_uint64 * 4)()
+        self.l.sm2b_ledger_read(self.h, arr)
+        return dict(zip(("modmul", "modadd", "modsub", "modinv"), list(arr)))
+
+    def ledger_reset(self):
+        self.l.sm2b_ledger_reset(self.h)
+
+    # -- field layer
+    def field_op(self, field: int, op: str, a: np.ndarray, b: np.ndarray | None = None):
+        n = a.shape[1]
+        out = np.zeros((8, n), np.uint32)
+        rc = self.l.gecc_field_op(self.h, field, FIELD_OPS[op], C.c_size_t(n), _vp(a), _vp(b), _vp(out))
+        if self._check(rc, "gecc_field_op"):
+            raise ValueError(f"gecc_field_op rc={rc}")
+        return out
+
+    def microbench(self, which: int, iters: int = 2000):
+        r, s, t = C.c_double(), C.c_double(), C.c_double()
+        rc = self.l.gecc_microbench(self.h, which, iters, C.byref(r), C.byref(s), C.byref(t))
+        if self._check(rc, "gecc_microbench"):
+            raise ValueError(f"gecc_microbench rc={rc}")
+        return dict(ops_per_clk_per_sm=r.value, seconds=s.value, total_ops=t.value)
+
+    # -- batch layer (host column buffers)
+    def batch_invert(self, field: int, a: np.ndarray):
+        n = a.shape[1]
+        out = np.zeros((8, n), np.uint32)
+        rc = self.l.gecc_batch_invert(self.h, field, C.c_size_t(n), _vp(a), _vp(out))
+        if self._check(rc, "gecc_batch_invert"):
+            raise ValueError(f"gecc_batch_invert rc={rc}")
+        return out
+
+    @staticmethod
+    def _pts_out(n):
+        return np.zeros((8, n), np.uint32), np.zeros((8, n), np.uint32), np.zeros(n, np.uint8)
+
+    def batch_padd(self, P, T):
+        if P[0].shape != T[0].shape:
+            raise ValueError("batch_padd: buffer sizes differ")  # batch_point.cpp:71-72
+        n = P[0].shape[1]
+        ox, oy, oi = self._pts_out(n)
+        rc = self.l.gecc_batch_padd(self.h, C.c_size_t(n), _vp(P[0]), _vp(P[1]), _vp(P[2]),
+                                    _vp(T[0]), _vp(T[1]), _vp(T[2]), _vp(ox), _vp(oy), _vp(oi))
+        if self._check(rc, "gecc_batch_padd"):
+            raise ValueError(f"gecc_batch_padd rc={rc}")
+        return ox, oy, oi
+
+    def batch_pdbl(self, P):
+        n = P[0].shape[1]
+        ox, oy, oi = self._pts_out(n)
+        rc = self.l.gecc_batch_pdbl(self.h, C.c_size_t(n), _vp(P[0]), _vp(P[1]), _vp(P[2]),
+                                    _vp(ox), _vp(oy), _vp(oi))
+        if self._check(rc, "gecc_batch_pdbl"):
+            raise ValueError(f"gecc_batch_pdbl rc={rc}")
+        return ox, oy, oi
+
+    def batch_fpmul(self, scalars: np.ndarray):
+        n = scalars.shape[1]
+        ox, oy, oi = self._pts_out(n)
+        rc = self.l.gecc_batch_fpmul(self.h, C.c_size_t(n), _vp(scalars), _vp(ox), _vp(oy), _vp(oi))
+        if self._check(rc, "gecc_batch_fpmul"):
+            raise ValueError(f"gecc_batch_fpmul rc={rc}")
+        return ox, oy, oi
+
+    def batch_upmul(self, scalars: np.ndarray, P):
+        n = scalars.shape[1]
+        if P[0].shape[1] != n:
+            raise ValueError("batch_upmul: scalar count mismatch")  # batch_point.cpp:239-240
+        ox, oy, oi = self._pts_out(n)
+        rc = self.l.gecc_batch_upmul(self.h, C.c_size_t(n), _vp(scalars), _vp(P[0]), _vp(P[1]),
+                                     _vp(P[2]), _vp(ox), _vp(oy), _vp(oi))
+        if self._check(rc, "gecc_batch_upmul"):
+            raise ValueError(f"gecc_batch_upmul rc={rc}")
+        return ox, oy, oi
+
+    def msm(self, scalars: np.ndarray, P):
+        n = scalars.shape[1]
+        ox, oy, oi = self._pts_out(1)
+        rc = self.l.gecc_msm(self.h, C.c_size_t(n), _vp(scalars), _vp(P[0]), _vp(P[1]), _vp(P[2]),
+                             _vp(ox), _vp(oy), _vp(oi))
+        if self._check(rc, "gecc_msm"):
+            raise ValueError(f"gecc_msm rc={rc}")
+        return ox, oy, oi
+
+    # -- protocol layer (byte records, sm2batch.h:61-82)
+    def keygen(self, seed: int, count: int, lane_base: int = 0):
+        sec = (C.c_uint8 * max(1, 32 * count))()
+        pub = (C.c_uint8 * max(1, 65 * count))()
+        rc = self.l.gecc_keygen(self.h, C.c_uint64(seed), C.c_uint64(lane_base), C.c_size_t(count),
+                                sec, pub)
+        self._check(rc, "gecc_keygen")
+        return rc, bytes(sec)[:32 * count], bytes(pub)[:65 * count]
+
+    def sign(self, digests: bytes, secrets: bytes, nonce_seed: int, lane_base: int = 0,
+             want_status: bool = True):
+        count = len(digests) // 32
+        sig = (C.c_uint8 * max(1, 64 * count))()
+        st = (C.c_int32 * max(1, count))() if want_status else None
+        rc = self.l.gecc_sign(self.h, C.c_size_t(count), _vp(digests), _vp(secrets),
+                              C.c_uint64(nonce_seed), C.c_uint64(lane_base), sig, st)
+        self._check(rc, "gecc_sign")
+        return rc, bytes(sig)[:64 * count], (list(st)[:count] if st is not None else None)
+
+    def verify(self, digests: bytes, publics: bytes, sigs: bytes):
+        count = len(digests) // 32
+        res = (C.c_uint8 * max(1, count))()
+        rc = self.l.sm2b_verify(self.h, C.c_size_t(count), _vp(digests), _vp(publics), _vp(sigs), res)
+        self._check(rc, "sm2b_verify")
+        return rc, bytes(res)[:count]
+
+    def ecdh(self, secrets: bytes, peers: bytes, want_status: bool = True):
+        count = len(secrets) // 32
+        sh = (C.c_uint8 * max(1, 32 * count))()
+        st = (C.c_int32 * max(1, count))() if want_status else None
+        rc = self.l.sm2b_ecdh(self.h, C.c_size_t(count), _vp(secrets), _vp(peers), sh, st)
+        self._check(rc, "sm2b_ecdh")
+        return rc, bytes(sh)[:32 * count], (list(st)[:count] if st is not None else None)

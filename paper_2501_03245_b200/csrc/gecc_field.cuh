@@ -1,0 +1,333 @@
+// 256-bit Montgomery field arithmetic, one element per thread, 8 x 32-bit limbs in
+// registers, built on the carry-chain primitives of gecc_prims.cuh.
+//
+// Semantics follow the reference's field layer (proj/src/field.cpp):
+//   fe_mul   == mont_mul  (field.cpp:205-211): a*b*2^-256 mod q, canonical (< q)
+//   fe_add   == mod_add   (field.cpp:24-29,213-219)
+//   fe_sub   == mod_sub   (field.cpp:31-35,221-227)
+//   fe_to_mont / fe_from_mont (field.cpp:194-203)
+//   fe_inv   == mod_inv_fermat's *value* (field.cpp:239-246); computed differently
+//               (windowed Fermat or safegcd) -- the residue is unique.
+// All outputs are canonical, so results are bit-identical to the reference no
+// matter which reduction route computes them (the reference itself checks its
+// two routes against each other, tests/test_field.cpp:166-169).
+//
+// A field is a type F with accessors q(i), r(i), r2(i), ninv(i), qm2(i), qinv32 and
+// a `kind`.  Compile-time fields (gecc_consts.cuh) fold to immediates after
+// unrolling; FieldRT carries runtime constants for arbitrary odd 256-bit moduli
+// (the reference's FieldParams::make(q), field.cpp:159-179).
+#pragma once
+#include "gecc_consts.cuh"
+
+namespace gecc {
+
+struct fe {
+    uint32_t w[8];
+};
+
+struct FieldRT {
+    static constexpr int N = 8;
+    static constexpr int kind = KIND_GENERIC;
+    uint32_t q_[8], r_[8], r2_[8], ninv_[8], qm2_[8];
+    uint32_t qinv32;
+    GECC_HD uint32_t q(int i) const { return q_[i]; }
+    GECC_HD uint32_t r(int i) const { return r_[i]; }
+    GECC_HD uint32_t r2(int i) const { return r2_[i]; }
+    GECC_HD uint32_t ninv(int i) const { return ninv_[i]; }
+    GECC_HD uint32_t qm2(int i) const { return qm2_[i]; }
+};
+
+// ---------------------------------------------------------------- basics
+GECC_HD fe fe_zero() {
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.w[i] = 0;
+    return r;
+}
+template <class F>
+GECC_HD fe fe_one(const F& f) {  // Montgomery one = R mod q
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.w[i] = f.r(i);
+    return r;
+}
+template <class F>
+GECC_HD fe fe_modulus(const F& f) {
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.w[i] = f.q(i);
+    return r;
+}
+GECC_HD bool fe_is_zero(const fe& a) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc |= a.w[i];
+    return acc == 0;
+}
+GECC_HD bool fe_eq(const fe& a, const fe& b) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc |= a.w[i] ^ b.w[i];
+    return acc == 0;
+}
+GECC_HD fe fe_select(bool c, const fe& a, const fe& b) {  // c ? a : b
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.w[i] = c ? a.w[i] : b.w[i];
+    return r;
+}
+// a < b as 256-bit integers (limbs.hpp:115-122)
+GECC_HD bool u256_lt(const fe& a, const fe& b) {
+    sub_cc(a.w[0], b.w[0]);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) subc_cc(a.w[i], b.w[i]);
+    return subc(0, 0) != 0;
+}
+template <class F>
+GECC_HD bool fe_lt_modulus(const F& f, const fe& a) {
+    return u256_lt(a, fe_modulus(f));
+}
+
+// ---------------------------------------------------------------- add / sub
+template <class F>
+GECC_HD fe fe_add(const F& f, const fe& a, const fe& b) {
+    fe s, d;
+    s.w[0] = add_cc(a.w[0], b.w[0]);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) s.w[i] = addc_cc(a.w[i], b.w[i]);
+    uint32_t top = addc(0, 0);
+    d.w[0] = sub_cc(s.w[0], f.q(0));
+#pragma unroll
+    for (int i = 1; i < 8; ++i) d.w[i] = subc_cc(s.w[i], f.q(i));
+    uint32_t borrow = subc(0, 0);  // 0xFFFFFFFF when s < q
+    // s >= q  <=>  carried out of 2^256, or no borrow
+    return fe_select(top != 0 || borrow == 0, d, s);
+}
+template <class F>
+GECC_HD fe fe_sub(const F& f, const fe& a, const fe& b) {
+    fe d, e;
+    d.w[0] = sub_cc(a.w[0], b.w[0]);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) d.w[i] = subc_cc(a.w[i], b.w[i]);
+    uint32_t borrow = subc(0, 0);
+    e.w[0] = add_cc(d.w[0], f.q(0));
+#pragma unroll
+    for (int i = 1; i < 8; ++i) e.w[i] = addc_cc(d.w[i], f.q(i));
+    return fe_select(borrow != 0, e, d);
+}
+template <class F>
+GECC_HD fe fe_neg(const F& f, const fe& a) {
+    return fe_sub(f, fe_zero(), a);
+}
+template <class F>
+GECC_HD fe fe_dbl(const F& f, const fe& a) {
+    return fe_add(f, a, a);
+}
+
+// ---------------------------------------------------------------- products
+// Full 16-limb product.  Products a[j]*b[i] whose position i+j is even are
+// accumulated in e[], odd ones in o[] (o is one limb to the left), so that every
+// lo/hi pair sits on an aligned register pair and each row is two carry chains of
+// IMAD.WIDE.U32(.X).  64 wide multiply-adds + 8 carry folds + 15 merge adds.
+GECC_HD void mul_wide8(uint32_t* t, const uint32_t* a, const uint32_t* b) {
+    constexpr int N = 8;
+    uint32_t e[2 * N], o[2 * N];
+#pragma unroll
+    for (int k = 0; k < 2 * N; ++k) e[k] = o[k] = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const uint32_t bi = b[i];
+        if ((i & 1) == 0) {
+            e[i] = mad_lo_cc(a[0], bi, e[i]);
+            e[i + 1] = madc_hi_cc(a[0], bi, e[i + 1]);
+#pragma unroll
+            for (int j = 2; j < N; j += 2) {
+                e[i + j] = madc_lo_cc(a[j], bi, e[i + j]);
+                e[i + j + 1] = madc_hi_cc(a[j], bi, e[i + j + 1]);
+            }
+            e[i + N] = addc(e[i + N], 0);
+            o[i] = mad_lo_cc(a[1], bi, o[i]);
+            o[i + 1] = madc_hi_cc(a[1], bi, o[i + 1]);
+#pragma unroll
+            for (int j = 3; j < N; j += 2) {
+                o[i + j - 1] = madc_lo_cc(a[j], bi, o[i + j - 1]);
+                o[i + j] = madc_hi_cc(a[j], bi, o[i + j]);
+            }
+        } else {
+            o[i - 1] = mad_lo_cc(a[0], bi, o[i - 1]);
+            o[i] = madc_hi_cc(a[0], bi, o[i]);
+#pragma unroll
+            for (int j = 2; j < N; j += 2) {
+                o[i + j - 1] = madc_lo_cc(a[j], bi, o[i + j - 1]);
+                o[i + j] = madc_hi_cc(a[j], bi, o[i + j]);
+            }
+            o[i + N - 1] = addc(o[i + N - 1], 0);
+            e[i + 1] = mad_lo_cc(a[1], bi, e[i + 1]);
+            e[i + 2] = madc_hi_cc(a[1], bi, e[i + 2]);
+#pragma unroll
+            for (int j = 3; j < N; j += 2) {
+                e[i + j] = madc_lo_cc(a[j], bi, e[i + j]);
+                e[i + j + 1] = madc_hi_cc(a[j], bi, e[i + j + 1]);
+            }
+        }
+    }
+    t[0] = e[0];
+    t[1] = add_cc(e[1], o[0]);
+#pragma unroll
+    for (int k = 2; k < 2 * N; ++k) t[k] = addc_cc(e[k], o[k - 1]);
+}
+
+// Low 8 limbs of a*b (used only by the generic REDC).
+GECC_HD void mul_low8(uint32_t* r, const uint32_t* a, const uint32_t* b) {
+    constexpr int N = 8;
+#pragma unroll
+    for (int k = 0; k < N; ++k) r[k] = 0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const uint32_t bi = b[i];
+        r[i] = mad_lo_cc(a[0], bi, r[i]);
+#pragma unroll
+        for (int j = 1; j < N - i; ++j) r[i + j] = madc_lo_cc(a[j], bi, r[i + j]);
+        if (i < N - 1) {
+            r[i + 1] = mad_hi_cc(a[0], bi, r[i + 1]);
+#pragma unroll
+            for (int j = 1; j < N - 1 - i; ++j) r[i + j + 1] = madc_hi_cc(a[j], bi, r[i + j + 1]);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- reductions
+// r = (top:r) - q if (top:r) >= q
+template <class F>
+GECC_HD fe final_sub(const F& f, const fe& r, uint32_t top) {
+    fe d;
+    d.w[0] = sub_cc(r.w[0], f.q(0));
+#pragma unroll
+    for (int i = 1; i < 8; ++i) d.w[i] = subc_cc(r.w[i], f.q(i));
+    uint32_t borrow = subc(0, 0);
+    return fe_select(top != 0 || borrow == 0, d, r);
+}
+
+// Generic REDC for any odd q (reference: reduce_generic_raw, field.cpp:50-78, same
+// value): m = t_lo * (-q^-1) mod 2^256, result = (t + m*q) / 2^256, one final
+// subtraction.  Two more products instead of a word-serial sweep: no dependent
+// chain of 8 multiplier words.
+template <class F>
+GECC_HD fe redc_generic(const F& f, const uint32_t* t) {
+    uint32_t ninv[8], q[8], m[8], u[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        ninv[i] = f.ninv(i);
+        q[i] = f.q(i);
+    }
+    mul_low8(m, t, ninv);
+    mul_wide8(u, m, q);
+    // t_lo + u_lo == 0 mod 2^256: it carries exactly when t_lo != 0
+    uint32_t nz = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) nz |= t[i];
+    add_cc(nz != 0 ? 1u : 0u, 0xFFFFFFFFu);
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.w[i] = addc_cc(t[8 + i], u[8 + i]);
+    uint32_t top = addc(0, 0);
+    return final_sub(f, r, top);
+}
+
+// secp256k1 base field, q = 2^256 - c with c = 2^32 + 977.  Word-serial REDC where
+// m_i * q = m_i * 2^256 - m_i * c, so each step needs one low multiply (m_i) and
+// one high multiply (m_i * 977); D carries the running amount still to be
+// subtracted from the next limb.  Result = t_hi + M - D, then one conditional
+// subtraction done as "+ c with carry-out".  16 multiplies instead of 72.
+template <class F>
+GECC_HD fe redc_secp(const F& f, const uint32_t* t) {
+    uint32_t m[8];
+    uint32_t dlo = 0, dhi = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        uint32_t v = sub_cc(t[i], dlo);       // CF = borrow
+        m[i] = mul_lo(v, F::qinv32);           // m_i * 977 == v mod 2^32
+        uint32_t ph = mul_hi(m[i], 977u);
+        uint32_t tmp = addc(dhi, ph);          // dhi + hi(m_i*977) + borrow (no overflow)
+        dlo = add_cc(tmp, m[i]);               // + m_i from the 2^32 term of c
+        dhi = addc(0, 0);
+    }
+    fe r;
+    r.w[0] = add_cc(t[8], m[0]);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) r.w[i] = addc_cc(t[8 + i], m[i]);
+    uint32_t top = addc(0, 0);
+    r.w[0] = sub_cc(r.w[0], dlo);
+    r.w[1] = subc_cc(r.w[1], dhi);
+#pragma unroll
+    for (int i = 2; i < 8; ++i) r.w[i] = subc_cc(r.w[i], 0);
+    top = subc(top, 0);
+    // (top:r) >= q  <=>  (top:r) + c >= 2^256
+    fe s;
+    s.w[0] = add_cc(r.w[0], 977u);
+    s.w[1] = addc_cc(r.w[1], 1u);
+#pragma unroll
+    for (int i = 2; i < 8; ++i) s.w[i] = addc_cc(r.w[i], 0);
+    uint32_t over = addc(top, 0);
+    (void)f;
+    return fe_select(over != 0, s, r);
+}
+
+template <class F>
+GECC_HD fe redc(const F& f, const uint32_t* t) {
+    if constexpr (F::kind == KIND_SECP_P) return redc_secp(f, t);
+    else return redc_generic(f, t);
+}
+
+// ---------------------------------------------------------------- mul / sqr
+template <class F>
+GECC_HD fe fe_mul(const F& f, const fe& a, const fe& b) {
+    uint32_t t[16];
+    mul_wide8(t, a.w, b.w);
+    return redc(f, t);
+}
+template <class F>
+GECC_HD fe fe_sqr(const F& f, const fe& a) {
+    return fe_mul(f, a, a);
+}
+template <class F>
+GECC_HD fe fe_to_mont(const F& f, const fe& a) {  // a * R
+    fe r2;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r2.w[i] = f.r2(i);
+    return fe_mul(f, a, r2);
+}
+template <class F>
+GECC_HD fe fe_from_mont(const F& f, const fe& a) {  // a * R^-1
+    uint32_t t[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        t[i] = a.w[i];
+        t[8 + i] = 0;
+    }
+    return redc(f, t);
+}
+
+// a^(q-2) in Montgomery form, 4-bit fixed window: 256 squarings + 64 + 14 products.
+// Not unrolled on purpose (code size).  Zero maps to zero.
+template <class F>
+GECC_HD fe fe_inv_fermat(const F& f, const fe& a) {
+    fe tab[16];
+    tab[0] = fe_one(f);
+    tab[1] = a;
+#pragma unroll 1
+    for (int i = 2; i < 16; ++i) tab[i] = fe_mul(f, tab[i - 1], a);
+    fe r = fe_one(f);
+#pragma unroll 1
+    for (int k = 63; k >= 0; --k) {
+        r = fe_sqr(f, r);
+        r = fe_sqr(f, r);
+        r = fe_sqr(f, r);
+        r = fe_sqr(f, r);
+        uint32_t nib = (f.qm2(k >> 3) >> ((k & 7) * 4)) & 15u;
+        r = fe_mul(f, r, tab[nib]);
+    }
+    return r;
+}
+
+}  // namespace gecc

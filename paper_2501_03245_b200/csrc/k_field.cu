@@ -1,0 +1,46 @@
+// Element-wise field kernels over column buffers: the GPU form of the reference's
+// field layer (field.cpp:194-246) used for parity tests of the limb arithmetic.
+#include "gecc_dev.cuh"
+#include "gecc_host.h"
+
+namespace gecc {
+
+template <class F>
+__global__ void __launch_bounds__(256) k_field_op(int op, size_t n, const uint32_t* __restrict__ a,
+                                                  const uint32_t* __restrict__ b,
+                                                  uint32_t* __restrict__ out) {
+    const F f{};
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+         i += (size_t)gridDim.x * blockDim.x) {
+        fe x = col_load(a, n, i);
+        fe y = b ? col_load(b, n, i) : fe_zero();
+        fe r;
+        switch (op) {
+            case 0: r = fe_mul(f, x, y); break;
+            case 1: r = fe_add(f, x, y); break;
+            case 2: r = fe_sub(f, x, y); break;
+            case 3: r = fe_to_mont(f, x); break;
+            case 4: r = fe_from_mont(f, x); break;
+            default: r = fe_is_zero(x) ? x : fe_inv_fermat(f, x); break;
+        }
+        col_store(out, n, i, r);
+    }
+}
+
+cudaError_t launch_field_op(int curve, int field, int op, size_t n, const uint32_t* a,
+                            const uint32_t* b, uint32_t* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int threads = 256;
+    size_t want = (n + threads - 1) / threads;
+    const int blocks = (int)(want < 148 * 16 ? want : 148 * 16);
+    if (curve == CURVE_SECP) {
+        if (field == 0) k_field_op<SecpP><<<blocks, threads, 0, s>>>(op, n, a, b, out);
+        else k_field_op<SecpN><<<blocks, threads, 0, s>>>(op, n, a, b, out);
+    } else {
+        if (field == 0) k_field_op<Sm2P><<<blocks, threads, 0, s>>>(op, n, a, b, out);
+        else k_field_op<Sm2N><<<blocks, threads, 0, s>>>(op, n, a, b, out);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace gecc
