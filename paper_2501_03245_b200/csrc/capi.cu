@@ -49,6 +49,8 @@ struct sm2b_ctx {
     uint64_t launches = 0;
     std::string last_error;
     DevBuf in, out, scratch;
+    uint32_t* gtab = nullptr;   // fixed-base table, built on the GPU at creation
+    uint32_t* flags = nullptr;  // device word: malformed-call flag of sign / ecdh
 };
 
 namespace {
@@ -122,6 +124,21 @@ sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device) {
     }
     ctx->sm_count = prop.multiProcessorCount;
     ctx->stream = ctx->own_stream;
+    // fixed-base table (sm2b_ctx_new builds sm2_base_table() eagerly too, capi.cpp:101)
+    uint32_t* bases = nullptr;
+    bool ok = cudaMalloc(&ctx->gtab, gtable_words() * 4) == cudaSuccess &&
+              cudaMalloc(&ctx->flags, 256) == cudaSuccess &&
+              cudaMalloc(&bases, 64 * 16 * 4 * 8) == cudaSuccess &&
+              build_gtable(ctx->curve, ctx->gtab, bases, ctx->stream) == cudaSuccess &&
+              cudaStreamSynchronize(ctx->stream) == cudaSuccess;
+    if (bases) cudaFree(bases);
+    if (!ok) {
+        fprintf(stderr, "gecc_b200: building the fixed-base table failed: %s\n",
+                cudaGetErrorString(cudaGetLastError()));
+        sm2b_ctx_free(ctx);
+        return nullptr;
+    }
+    ctx->launches += 2;
     return ctx;
 }
 
@@ -142,6 +159,8 @@ void sm2b_ctx_free(sm2b_ctx* ctx) {
         ctx->in.release();
         ctx->out.release();
         ctx->scratch.release();
+        if (ctx->gtab) cudaFree(ctx->gtab);
+        if (ctx->flags) cudaFree(ctx->flags);
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     }
     delete ctx;
@@ -249,29 +268,415 @@ sm2b_status gecc_microbench(sm2b_ctx* ctx, int which, int iters, double* ops_per
     return SM2B_OK;
 }
 
+// ------------------------------------------------------------------ ledger emulation
+// The kernels do not count; each call advances the ledger by the reference
+// algorithm's closed forms for a batch with no exceptional lanes:
+//   batch_invert  (3N-3, 0, 0, 1)            batch_padd (6N-3, 0, 6N, 1)
+//   batch_fpmul   256*(6N+3(L-1), 0, 7N, 1)  batch_upmul 256*(14N+3(L-1), 5N, 11N, 1)
+namespace {
+uint64_t eff_lanes(const sm2b_ctx* ctx, size_t n) {  // BatchConfig::effective_lanes + LanePlan clamp
+    uint64_t l = ctx->lanes;
+    if (l == 0) {
+        uint64_t w = ctx->workers ? ctx->workers : 1;
+        l = w * 4;
+    }
+    if (l > n) l = n ? n : 1;
+    return l;
+}
+void led(sm2b_ctx* ctx, uint64_t mul, uint64_t add, uint64_t sub, uint64_t inv) {
+    ctx->ledger.modmul += mul;
+    ctx->ledger.modadd += add;
+    ctx->ledger.modsub += sub;
+    ctx->ledger.modinv += inv;
+}
+void led_invert(sm2b_ctx* c, uint64_t n) { if (n) led(c, 3 * n - 3, 0, 0, 1); }
+void led_padd(sm2b_ctx* c, uint64_t n) { if (n) led(c, 6 * n - 3, 0, 6 * n, 1); }
+void led_fpmul(sm2b_ctx* c, uint64_t n) {
+    if (n) led(c, 256 * (6 * n + 3 * (eff_lanes(c, n) - 1)), 0, 256 * 7 * n, 256);
+}
+void led_upmul(sm2b_ctx* c, uint64_t n) {
+    if (n) led(c, 256 * (14 * n + 3 * (eff_lanes(c, n) - 1)), 256 * 5 * n, 256 * 11 * n, 256);
+}
+}  // namespace
+
+// ------------------------------------------------------------------ protocol layer
+sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
+                            const uint8_t* publics, const uint8_t* signatures,
+                            uint8_t* results) {
+    if (!ctx || (count > 0 && (!digests || !publics || !signatures || !results)))
+        return SM2B_ERROR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, launch_verify(ctx->curve, count, digests, publics, signatures, ctx->gtab, results,
+                          ctx->stream));
+    ctx->launches += count ? 1 : 0;
+    led_invert(ctx, count);
+    led(ctx, 2 * count, 0, 0, 0);
+    led_fpmul(ctx, count);
+    led_upmul(ctx, count);
+    led_padd(ctx, count);
+    return SM2B_OK;
+}
+
+sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
+                        const uint8_t* publics, const uint8_t* signatures, uint8_t* results) {
+    if (!ctx || (count > 0 && (!digests || !publics || !signatures || !results)))
+        return SM2B_ERROR_INVALID_ARGUMENT;
+    if (count == 0) return SM2B_OK;
+    uint8_t *dd, *dp, *ds, *dr;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        DeviceGuard g(ctx->device);
+        CU(ctx, ctx->in.ensure(Carver::need(32 * count) + Carver::need(65 * count) +
+                               Carver::need(64 * count)));
+        CU(ctx, ctx->out.ensure(Carver::need(count)));
+        Carver ci(ctx->in.p);
+        dd = ci.take<uint8_t>(32 * count);
+        dp = ci.take<uint8_t>(65 * count);
+        ds = ci.take<uint8_t>(64 * count);
+        dr = (uint8_t*)ctx->out.p;
+        CU(ctx, cudaMemcpyAsync(dd, digests, 32 * count, cudaMemcpyHostToDevice, ctx->stream));
+        CU(ctx, cudaMemcpyAsync(dp, publics, 65 * count, cudaMemcpyHostToDevice, ctx->stream));
+        CU(ctx, cudaMemcpyAsync(ds, signatures, 64 * count, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    sm2b_status st = gecc_verify_dev(ctx, count, dd, dp, ds, dr);
+    if (st != SM2B_OK) return st;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, cudaMemcpyAsync(results, dr, count, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return SM2B_OK;
+}
+
+sm2b_status gecc_sign_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
+                          const uint8_t* secrets, uint64_t nonce_seed, uint64_t lane_base,
+                          uint8_t* signatures, int32_t* lane_status) {
+    if (!ctx || (count > 0 && (!digests || !secrets || !signatures || !lane_status)))
+        return SM2B_ERROR_INVALID_ARGUMENT;
+    if (nonce_seed == 0) return fail_msg(ctx, "device signing needs a non-zero nonce seed");
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, cudaMemsetAsync(ctx->flags, 0, 4, ctx->stream));
+    CU(ctx, launch_sign(ctx->curve, count, digests, secrets, nonce_seed, lane_base, ctx->gtab,
+                        signatures, lane_status, ctx->flags, ctx->stream));
+    ctx->launches += count ? 1 : 0;
+    led_fpmul(ctx, count);
+    led_invert(ctx, count);
+    led(ctx, 2 * count, count, 0, 0);
+    return SM2B_OK;
+}
+
+namespace {
+uint64_t system_seed() {  // seed == 0: system entropy (capi.cpp:75-79), drawn on the host
+    uint64_t v = 0;
+    FILE* f = fopen("/dev/urandom", "rb");
+    if (f) {
+        if (fread(&v, 1, sizeof v, f) != sizeof v) v = 0;
+        fclose(f);
+    }
+    static uint64_t counter = 0;
+    v ^= 0x9E3779B97F4A7C15ull * (++counter) ^ (uint64_t)(uintptr_t)&v;
+    return v ? v : 1;
+}
+
+// report_lanes (capi.cpp:64-73)
+sm2b_status report_lanes(const int32_t* st, size_t n, int32_t* lane_status) {
+    int32_t first = SM2B_OK;
+    for (size_t i = 0; i < n; ++i) {
+        if (lane_status) lane_status[i] = st[i];
+        if (st[i] != SM2B_OK && first == SM2B_OK) first = st[i];
+    }
+    return lane_status ? SM2B_OK : (sm2b_status)first;
+}
+}  // namespace
+
+sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const uint8_t* secrets,
+                      uint64_t nonce_seed, uint64_t lane_base, uint8_t* signatures,
+                      int32_t* lane_status) {
+    if (!ctx || (count > 0 && (!digests || !secrets || !signatures)))
+        return SM2B_ERROR_INVALID_ARGUMENT;
+    if (count == 0) return SM2B_OK;
+    if (nonce_seed == 0) nonce_seed = system_seed();
+    uint8_t *dd, *dsec, *dsig;
+    int32_t* dst;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        DeviceGuard g(ctx->device);
+        CU(ctx, ctx->in.ensure(2 * Carver::need(32 * count)));
+        CU(ctx, ctx->out.ensure(Carver::need(64 * count) + Carver::need(4 * count)));
+        Carver ci(ctx->in.p), co(ctx->out.p);
+        dd = ci.take<uint8_t>(32 * count);
+        dsec = ci.take<uint8_t>(32 * count);
+        dsig = co.take<uint8_t>(64 * count);
+        dst = co.take<int32_t>(count);
+        CU(ctx, cudaMemcpyAsync(dd, digests, 32 * count, cudaMemcpyHostToDevice, ctx->stream));
+        CU(ctx, cudaMemcpyAsync(dsec, secrets, 32 * count, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    sm2b_status st = gecc_sign_dev(ctx, count, dd, dsec, nonce_seed, lane_base, dsig, dst);
+    if (st != SM2B_OK) return st;
+    std::vector<int32_t> hst(count);
+    uint32_t flag = 0;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        DeviceGuard g(ctx->device);
+        CU(ctx, cudaMemcpyAsync(&flag, ctx->flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(ctx, cudaMemcpyAsync(hst.data(), dst, 4 * count, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+        // a zero or oversize secret fails the whole call before any output (capi.cpp:181-184)
+        if (flag) return SM2B_ERROR_MALFORMED_INPUT;
+        CU(ctx, cudaMemcpyAsync(signatures, dsig, 64 * count, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return report_lanes(hst.data(), count, lane_status);
+}
+
+sm2b_status sm2b_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const uint8_t* secrets,
+                      uint64_t nonce_seed, uint8_t* signatures, int32_t* lane_status) {
+    return gecc_sign(ctx, count, digests, secrets, nonce_seed, 0, signatures, lane_status);
+}
+
+sm2b_status gecc_keygen(sm2b_ctx* ctx, uint64_t seed, uint64_t lane_base, size_t count,
+                        uint8_t* secrets, uint8_t* publics) {
+    if (!ctx || (count > 0 && (!secrets || !publics))) return SM2B_ERROR_INVALID_ARGUMENT;
+    if (count == 0) return SM2B_OK;
+    if (seed == 0) seed = system_seed();
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, ctx->out.ensure(Carver::need(32 * count) + Carver::need(65 * count)));
+    Carver co(ctx->out.p);
+    uint8_t* dsec = co.take<uint8_t>(32 * count);
+    uint8_t* dpub = co.take<uint8_t>(65 * count);
+    CU(ctx, launch_keygen(ctx->curve, count, seed, lane_base, ctx->gtab, dsec, dpub, ctx->stream));
+    ctx->launches += 1;
+    led_fpmul(ctx, count);
+    CU(ctx, cudaMemcpyAsync(secrets, dsec, 32 * count, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(publics, dpub, 65 * count, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return SM2B_OK;
+}
+sm2b_status sm2b_keygen(sm2b_ctx* ctx, uint64_t seed, size_t count, uint8_t* secrets,
+                        uint8_t* publics) {
+    return gecc_keygen(ctx, seed, 0, count, secrets, publics);
+}
+
+sm2b_status sm2b_ecdh(sm2b_ctx* ctx, size_t count, const uint8_t* secrets, const uint8_t* peers,
+                      uint8_t* shared, int32_t* lane_status) {
+    if (!ctx || (count > 0 && (!secrets || !peers || !shared))) return SM2B_ERROR_INVALID_ARGUMENT;
+    if (count == 0) return SM2B_OK;
+    std::vector<int32_t> hst(count);
+    uint32_t flag = 0;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        DeviceGuard g(ctx->device);
+        CU(ctx, ctx->in.ensure(Carver::need(32 * count) + Carver::need(65 * count)));
+        CU(ctx, ctx->out.ensure(Carver::need(32 * count) + Carver::need(4 * count)));
+        Carver ci(ctx->in.p), co(ctx->out.p);
+        uint8_t* dsec = ci.take<uint8_t>(32 * count);
+        uint8_t* dpeer = ci.take<uint8_t>(65 * count);
+        uint8_t* dsh = co.take<uint8_t>(32 * count);
+        int32_t* dst = co.take<int32_t>(count);
+        CU(ctx, cudaMemcpyAsync(dsec, secrets, 32 * count, cudaMemcpyHostToDevice, ctx->stream));
+        CU(ctx, cudaMemcpyAsync(dpeer, peers, 65 * count, cudaMemcpyHostToDevice, ctx->stream));
+        CU(ctx, cudaMemsetAsync(ctx->flags, 0, 4, ctx->stream));
+        CU(ctx, launch_ecdh(ctx->curve, count, dsec, dpeer, dsh, dst, ctx->flags, ctx->stream));
+        ctx->launches += 1;
+        led_upmul(ctx, count);
+        CU(ctx, cudaMemcpyAsync(&flag, ctx->flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(ctx, cudaMemcpyAsync(hst.data(), dst, 4 * count, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+        if (flag) return SM2B_ERROR_MALFORMED_INPUT;  // Scalar::checked on a secret (capi.cpp:241)
+        CU(ctx, cudaMemcpyAsync(shared, dsh, 32 * count, cudaMemcpyDeviceToHost, ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return report_lanes(hst.data(), count, lane_status);
+}
+
+// ------------------------------------------------------------------ batch layer
+sm2b_status gecc_batch_invert_dev(sm2b_ctx* ctx, gecc_field field, size_t n, const uint32_t* in,
+                                  uint32_t* out) {
+    if (!ctx || (n > 0 && (!in || !out)) || (unsigned)field > 1) return SM2B_ERROR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, launch_batch_invert(ctx->curve, field, n, in, out, ctx->stream));
+    ctx->launches += n ? 1 : 0;
+    led_invert(ctx, n);
+    return SM2B_OK;
+}
+sm2b_status gecc_batch_padd_dev(sm2b_ctx* ctx, size_t n, const uint32_t* px, const uint32_t* py,
+                                const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty,
+                                const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    if (!ctx || (n > 0 && (!px || !py || !tx || !ty || !ox || !oy || !oinf)))
+        return SM2B_ERROR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, launch_batch_padd(ctx->curve, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, ctx->stream));
+    ctx->launches += n ? 1 : 0;
+    led_padd(ctx, n);
+    return SM2B_OK;
+}
+sm2b_status gecc_batch_pdbl_dev(sm2b_ctx* ctx, size_t n, const uint32_t* px, const uint32_t* py,
+                                const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    if (!ctx || (n > 0 && (!px || !py || !ox || !oy || !oinf))) return SM2B_ERROR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, launch_batch_pdbl(ctx->curve, n, px, py, pinf, ox, oy, oinf, ctx->stream));
+    ctx->launches += n ? 1 : 0;
+    if (n) led(ctx, 7 * n - 3, 4 * n, 4 * n, 1);
+    return SM2B_OK;
+}
+sm2b_status gecc_batch_fpmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, uint32_t* ox,
+                                 uint32_t* oy, uint8_t* oinf) {
+    if (!ctx || (n > 0 && (!scalars || !ox || !oy || !oinf))) return SM2B_ERROR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, launch_fpmul(ctx->curve, n, scalars, ctx->gtab, ox, oy, oinf, ctx->stream));
+    ctx->launches += n ? 1 : 0;
+    led_fpmul(ctx, n);
+    return SM2B_OK;
+}
+sm2b_status gecc_batch_upmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars,
+                                 const uint32_t* px, const uint32_t* py, const uint8_t* pinf,
+                                 uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    if (!ctx || (n > 0 && (!scalars || !px || !py || !ox || !oy || !oinf)))
+        return SM2B_ERROR_INVALID_ARGUMENT;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, launch_upmul(ctx->curve, n, scalars, px, py, pinf, ox, oy, oinf, ctx->stream));
+    ctx->launches += n ? 1 : 0;
+    led_upmul(ctx, n);
+    return SM2B_OK;
+}
+
+}  // extern "C"
+namespace {
+// Host-pointer wrapper shared by the column-buffer entry points: stages up to
+// three column inputs (+ up to two infinity masks), runs `body` with the device
+// pointers, then returns one output point buffer.
+struct HostPoints {
+    const uint32_t* x;
+    const uint32_t* y;
+    const uint8_t* inf;
+};
+template <class Body>
+sm2b_status run_points(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const HostPoints* p,
+                       const HostPoints* t, uint32_t* ox, uint32_t* oy, uint8_t* oinf, Body body) {
+    const size_t cb = Carver::need(32 * n), mb = Carver::need(n);
+    uint32_t *dk = nullptr, *dpx = nullptr, *dpy = nullptr, *dtx = nullptr, *dty = nullptr;
+    uint8_t *dpi = nullptr, *dti = nullptr;
+    uint32_t *dox, *doy;
+    uint8_t* doi;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        DeviceGuard g(ctx->device);
+        CU(ctx, ctx->in.ensure(5 * cb + 2 * mb));
+        CU(ctx, ctx->out.ensure(2 * cb + mb));
+        Carver ci(ctx->in.p), co(ctx->out.p);
+        dox = co.take<uint32_t>(8 * n);
+        doy = co.take<uint32_t>(8 * n);
+        doi = co.take<uint8_t>(n);
+        auto up = [&](const void* h, size_t bytes, void* d) {
+            return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream);
+        };
+        if (scalars) { dk = ci.take<uint32_t>(8 * n); CU(ctx, up(scalars, 32 * n, dk)); }
+        if (p) {
+            dpx = ci.take<uint32_t>(8 * n); dpy = ci.take<uint32_t>(8 * n);
+            CU(ctx, up(p->x, 32 * n, dpx)); CU(ctx, up(p->y, 32 * n, dpy));
+            if (p->inf) { dpi = ci.take<uint8_t>(n); CU(ctx, up(p->inf, n, dpi)); }
+        }
+        if (t) {
+            dtx = ci.take<uint32_t>(8 * n); dty = ci.take<uint32_t>(8 * n);
+            CU(ctx, up(t->x, 32 * n, dtx)); CU(ctx, up(t->y, 32 * n, dty));
+            if (t->inf) { dti = ci.take<uint8_t>(n); CU(ctx, up(t->inf, n, dti)); }
+        }
+    }
+    sm2b_status st = body(dk, dpx, dpy, dpi, dtx, dty, dti, dox, doy, doi);
+    if (st != SM2B_OK) return st;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, cudaMemcpyAsync(ox, dox, 32 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(oy, doy, 32 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(oinf, doi, n, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return SM2B_OK;
+}
+}  // namespace
+extern "C" {
+
+sm2b_status gecc_batch_invert(sm2b_ctx* ctx, gecc_field field, size_t n, const uint32_t* in,
+                              uint32_t* out) {
+    if (!ctx || (n > 0 && (!in || !out)) || (unsigned)field > 1) return SM2B_ERROR_INVALID_ARGUMENT;
+    if (n == 0) return SM2B_OK;
+    uint32_t *din, *dout;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        DeviceGuard g(ctx->device);
+        CU(ctx, ctx->in.ensure(32 * n));
+        CU(ctx, ctx->out.ensure(32 * n));
+        din = (uint32_t*)ctx->in.p;
+        dout = (uint32_t*)ctx->out.p;
+        CU(ctx, cudaMemcpyAsync(din, in, 32 * n, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    sm2b_status st = gecc_batch_invert_dev(ctx, field, n, din, dout);
+    if (st != SM2B_OK) return st;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, cudaMemcpyAsync(out, dout, 32 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return SM2B_OK;
+}
+
+sm2b_status gecc_batch_padd(sm2b_ctx* ctx, size_t n, const uint32_t* px, const uint32_t* py,
+                            const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty,
+                            const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    if (!ctx || (n > 0 && (!px || !py || !tx || !ty || !ox || !oy || !oinf)))
+        return SM2B_ERROR_INVALID_ARGUMENT;
+    if (n == 0) return SM2B_OK;
+    HostPoints p{px, py, pinf}, t{tx, ty, tinf};
+    return run_points(ctx, n, nullptr, &p, &t, ox, oy, oinf,
+                      [&](uint32_t*, uint32_t* dpx, uint32_t* dpy, uint8_t* dpi, uint32_t* dtx,
+                          uint32_t* dty, uint8_t* dti, uint32_t* dox, uint32_t* doy, uint8_t* doi) {
+                          return gecc_batch_padd_dev(ctx, n, dpx, dpy, dpi, dtx, dty, dti, dox, doy, doi);
+                      });
+}
+sm2b_status gecc_batch_pdbl(sm2b_ctx* ctx, size_t n, const uint32_t* px, const uint32_t* py,
+                            const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    if (!ctx || (n > 0 && (!px || !py || !ox || !oy || !oinf))) return SM2B_ERROR_INVALID_ARGUMENT;
+    if (n == 0) return SM2B_OK;
+    HostPoints p{px, py, pinf};
+    return run_points(ctx, n, nullptr, &p, nullptr, ox, oy, oinf,
+                      [&](uint32_t*, uint32_t* dpx, uint32_t* dpy, uint8_t* dpi, uint32_t*, uint32_t*,
+                          uint8_t*, uint32_t* dox, uint32_t* doy, uint8_t* doi) {
+                          return gecc_batch_pdbl_dev(ctx, n, dpx, dpy, dpi, dox, doy, doi);
+                      });
+}
+sm2b_status gecc_batch_fpmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, uint32_t* ox,
+                             uint32_t* oy, uint8_t* oinf) {
+    if (!ctx || (n > 0 && (!scalars || !ox || !oy || !oinf))) return SM2B_ERROR_INVALID_ARGUMENT;
+    if (n == 0) return SM2B_OK;
+    return run_points(ctx, n, scalars, nullptr, nullptr, ox, oy, oinf,
+                      [&](uint32_t* dk, uint32_t*, uint32_t*, uint8_t*, uint32_t*, uint32_t*, uint8_t*,
+                          uint32_t* dox, uint32_t* doy, uint8_t* doi) {
+                          return gecc_batch_fpmul_dev(ctx, n, dk, dox, doy, doi);
+                      });
+}
+sm2b_status gecc_batch_upmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uint32_t* px,
+                             const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
+                             uint8_t* oinf) {
+    if (!ctx || (n > 0 && (!scalars || !px || !py || !ox || !oy || !oinf)))
+        return SM2B_ERROR_INVALID_ARGUMENT;
+    if (n == 0) return SM2B_OK;
+    HostPoints p{px, py, pinf};
+    return run_points(ctx, n, scalars, &p, nullptr, ox, oy, oinf,
+                      [&](uint32_t* dk, uint32_t* dpx, uint32_t* dpy, uint8_t* dpi, uint32_t*, uint32_t*,
+                          uint8_t*, uint32_t* dox, uint32_t* doy, uint8_t* doi) {
+                          return gecc_batch_upmul_dev(ctx, n, dk, dpx, dpy, dpi, dox, doy, doi);
+                      });
+}
+
 // ------------------------------------------------------------------ not yet built
 #define GECC_TODO(ctx) ((ctx) ? fail_msg(ctx, "not implemented in this build") : SM2B_ERROR_INVALID_ARGUMENT)
-
-sm2b_status sm2b_keygen(sm2b_ctx* ctx, uint64_t, size_t, uint8_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status sm2b_sign(sm2b_ctx* ctx, size_t, const uint8_t*, const uint8_t*, uint64_t, uint8_t*, int32_t*) { return GECC_TODO(ctx); }
-sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t, const uint8_t*, const uint8_t*, const uint8_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status sm2b_ecdh(sm2b_ctx* ctx, size_t, const uint8_t*, const uint8_t*, uint8_t*, int32_t*) { return GECC_TODO(ctx); }
 sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char*, const char*, size_t, size_t, uint32_t, uint64_t, uint32_t, sm2b_bench_report*) { return GECC_TODO(ctx); }
-sm2b_status gecc_keygen(sm2b_ctx* ctx, uint64_t, uint64_t, size_t, uint8_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_sign(sm2b_ctx* ctx, size_t, const uint8_t*, const uint8_t*, uint64_t, uint64_t, uint8_t*, int32_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_batch_invert(sm2b_ctx* ctx, gecc_field, size_t, const uint32_t*, uint32_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_batch_padd(sm2b_ctx* ctx, size_t, const uint32_t*, const uint32_t*, const uint8_t*, const uint32_t*, const uint32_t*, const uint8_t*, uint32_t*, uint32_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_batch_pdbl(sm2b_ctx* ctx, size_t, const uint32_t*, const uint32_t*, const uint8_t*, uint32_t*, uint32_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_batch_fpmul(sm2b_ctx* ctx, size_t, const uint32_t*, uint32_t*, uint32_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_batch_upmul(sm2b_ctx* ctx, size_t, const uint32_t*, const uint32_t*, const uint32_t*, const uint8_t*, uint32_t*, uint32_t*, uint8_t*) { return GECC_TODO(ctx); }
 sm2b_status gecc_msm(sm2b_ctx* ctx, size_t, const uint32_t*, const uint32_t*, const uint32_t*, const uint8_t*, uint32_t*, uint32_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_batch_invert_dev(sm2b_ctx* ctx, gecc_field, size_t, const uint32_t*, uint32_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_batch_padd_dev(sm2b_ctx* ctx, size_t, const uint32_t*, const uint32_t*, const uint8_t*, const uint32_t*, const uint32_t*, const uint8_t*, uint32_t*, uint32_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_batch_pdbl_dev(sm2b_ctx* ctx, size_t, const uint32_t*, const uint32_t*, const uint8_t*, uint32_t*, uint32_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_batch_fpmul_dev(sm2b_ctx* ctx, size_t, const uint32_t*, uint32_t*, uint32_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_batch_upmul_dev(sm2b_ctx* ctx, size_t, const uint32_t*, const uint32_t*, const uint32_t*, const uint8_t*, uint32_t*, uint32_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t, const uint8_t*, const uint8_t*, const uint8_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_sign_dev(sm2b_ctx* ctx, size_t, const uint8_t*, const uint8_t*, uint64_t, uint64_t, uint8_t*, int32_t*) { return GECC_TODO(ctx); }
 sm2b_status gecc_msm_dev(sm2b_ctx* ctx, size_t, const uint32_t*, const uint32_t*, const uint32_t*, const uint8_t*, uint32_t*, uint32_t*, uint8_t*) { return GECC_TODO(ctx); }
 
 }  // extern "C"

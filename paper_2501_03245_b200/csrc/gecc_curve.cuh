@@ -1,0 +1,205 @@
+// Short-Weierstrass point arithmetic y^2 = x^3 + a x + b over a 256-bit prime
+// field, one point per thread, coordinates in Montgomery form.
+//
+// The reference keeps points affine and shares one inversion per batch step
+// (batch_point.cpp); its serial ground truth is Jacobian (curve.cpp:109-185).
+// The GPU ladders here are per-thread Jacobian with complete case handling, so
+// every output *value* equals the reference's (points are unique; only the
+// representation inside a kernel differs).  Affine conversion happens once at
+// kernel exit.
+//
+//   jac_dbl   : a = 0    -> 2M + 5S ("dbl-2009-l")
+//               a = -3   -> 3M + 5S ("dbl-2001-b")
+//               generic  -> the reference's own formula, curve.cpp:109-127
+//   jac_madd  : Jacobian + affine, 8M + 3S, the reference's mixed path
+//               (curve.cpp:136-141,152-166), complete
+//   jac_add   : Jacobian + Jacobian, 12M + 4S (curve.cpp:142-166), complete
+#pragma once
+#include "gecc_field.cuh"
+
+namespace gecc {
+
+struct jac {
+    fe X, Y, Z;  // Z == 0 <=> point at infinity
+};
+struct aff {
+    fe x, y;
+};
+
+template <class C>
+GECC_HD jac jac_infinity() {
+    jac r;
+    r.X = fe_one(typename C::Fp{});
+    r.Y = r.X;
+    r.Z = fe_zero();
+    return r;
+}
+GECC_HD bool jac_is_inf(const jac& p) { return fe_is_zero(p.Z); }
+
+template <class C>
+GECC_HD fe curve_a() {
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.w[i] = C::a(i);
+    return r;
+}
+template <class C>
+GECC_HD fe curve_b() {
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.w[i] = C::b(i);
+    return r;
+}
+template <class C>
+GECC_HD aff curve_g() {
+    aff g;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        g.x.w[i] = C::gx(i);
+        g.y.w[i] = C::gy(i);
+    }
+    return g;
+}
+
+// y^2 == x^3 + a x + b (curve.cpp:62-70)
+template <class C>
+GECC_HD bool aff_on_curve(const aff& p) {
+    const typename C::Fp f{};
+    fe lhs = fe_sqr(f, p.y);
+    fe rhs = fe_mul(f, fe_sqr(f, p.x), p.x);
+    if (C::a_kind == A_MINUS3) {
+        fe x3 = fe_add(f, fe_dbl(f, p.x), p.x);
+        rhs = fe_sub(f, rhs, x3);
+    } else if (C::a_kind != A_ZERO) {
+        rhs = fe_add(f, rhs, fe_mul(f, curve_a<C>(), p.x));
+    }
+    rhs = fe_add(f, rhs, curve_b<C>());
+    return fe_eq(lhs, rhs);
+}
+
+template <class C>
+GECC_HD_CALL jac jac_dbl(const jac& p) {
+    const typename C::Fp f{};
+    jac r;
+    if (C::a_kind == A_ZERO) {
+        fe A = fe_sqr(f, p.X);
+        fe B = fe_sqr(f, p.Y);
+        fe Cc = fe_sqr(f, B);
+        fe t = fe_add(f, p.X, B);
+        fe D = fe_sub(f, fe_sub(f, fe_sqr(f, t), A), Cc);
+        D = fe_dbl(f, D);                       // 2((X+B)^2 - A - C)
+        fe E = fe_add(f, fe_dbl(f, A), A);      // 3A
+        fe F = fe_sqr(f, E);
+        r.X = fe_sub(f, F, fe_dbl(f, D));
+        fe C8 = fe_dbl(f, fe_dbl(f, fe_dbl(f, Cc)));
+        r.Y = fe_sub(f, fe_mul(f, E, fe_sub(f, D, r.X)), C8);
+        r.Z = fe_dbl(f, fe_mul(f, p.Y, p.Z));
+    } else if (C::a_kind == A_MINUS3) {
+        fe delta = fe_sqr(f, p.Z);
+        fe gamma = fe_sqr(f, p.Y);
+        fe beta = fe_mul(f, p.X, gamma);
+        fe t = fe_mul(f, fe_sub(f, p.X, delta), fe_add(f, p.X, delta));
+        fe alpha = fe_add(f, fe_dbl(f, t), t);
+        fe beta4 = fe_dbl(f, fe_dbl(f, beta));
+        r.X = fe_sub(f, fe_sqr(f, alpha), fe_dbl(f, beta4));
+        fe yz = fe_add(f, p.Y, p.Z);
+        r.Z = fe_sub(f, fe_sub(f, fe_sqr(f, yz), gamma), delta);
+        fe g2 = fe_sqr(f, gamma);
+        fe g8 = fe_dbl(f, fe_dbl(f, fe_dbl(f, g2)));
+        r.Y = fe_sub(f, fe_mul(f, alpha, fe_sub(f, beta4, r.X)), g8);
+    } else {
+        fe yy = fe_sqr(f, p.Y);
+        fe yy2 = fe_dbl(f, yy);
+        fe s4 = fe_dbl(f, fe_mul(f, p.X, yy2));
+        fe c8 = fe_dbl(f, fe_sqr(f, yy2));
+        fe xx = fe_sqr(f, p.X);
+        fe zz2 = fe_sqr(f, fe_sqr(f, p.Z));
+        fe m = fe_add(f, fe_add(f, fe_dbl(f, xx), xx), fe_mul(f, curve_a<C>(), zz2));
+        r.X = fe_sub(f, fe_sub(f, fe_sqr(f, m), s4), s4);
+        r.Y = fe_sub(f, fe_mul(f, m, fe_sub(f, s4, r.X)), c8);
+        r.Z = fe_dbl(f, fe_mul(f, p.Y, p.Z));
+    }
+    // infinity (Z = 0) stays infinity: Z3 = 2 Y Z = 0.  Y = 0 (a 2-torsion point)
+    // also gives Z3 = 0, matching curve.cpp:110-112.
+    return r;
+}
+
+// p + (x2, y2), (x2, y2) finite.  Handles p = infinity, p = q (doubling) and
+// p = -q (infinity) -- curve.cpp:129-167 with t.Z == 1.
+template <class C>
+GECC_HD_CALL jac jac_madd(const jac& p, const aff& q) {
+    const typename C::Fp f{};
+    if (jac_is_inf(p)) {
+        jac r;
+        r.X = q.x;
+        r.Y = q.y;
+        r.Z = fe_one(f);
+        return r;
+    }
+    fe z1z1 = fe_sqr(f, p.Z);
+    fe u2 = fe_mul(f, q.x, z1z1);
+    fe s2 = fe_mul(f, q.y, fe_mul(f, z1z1, p.Z));
+    fe h = fe_sub(f, u2, p.X);
+    fe rr = fe_sub(f, s2, p.Y);
+    if (fe_is_zero(h)) {
+        if (fe_is_zero(rr)) return jac_dbl<C>(p);
+        return jac_infinity<C>();
+    }
+    fe hh = fe_sqr(f, h);
+    fe hhh = fe_mul(f, hh, h);
+    fe v = fe_mul(f, p.X, hh);
+    jac r;
+    r.X = fe_sub(f, fe_sub(f, fe_sub(f, fe_sqr(f, rr), hhh), v), v);
+    r.Y = fe_sub(f, fe_mul(f, rr, fe_sub(f, v, r.X)), fe_mul(f, p.Y, hhh));
+    r.Z = fe_mul(f, p.Z, h);
+    return r;
+}
+
+// complete Jacobian + Jacobian (curve.cpp:142-166)
+template <class C>
+GECC_HD_CALL jac jac_add(const jac& p, const jac& q) {
+    const typename C::Fp f{};
+    if (jac_is_inf(p)) return q;
+    if (jac_is_inf(q)) return p;
+    fe z1z1 = fe_sqr(f, p.Z);
+    fe z2z2 = fe_sqr(f, q.Z);
+    fe u1 = fe_mul(f, p.X, z2z2);
+    fe u2 = fe_mul(f, q.X, z1z1);
+    fe s1 = fe_mul(f, p.Y, fe_mul(f, z2z2, q.Z));
+    fe s2 = fe_mul(f, q.Y, fe_mul(f, z1z1, p.Z));
+    fe h = fe_sub(f, u2, u1);
+    fe rr = fe_sub(f, s2, s1);
+    if (fe_is_zero(h)) {
+        if (fe_is_zero(rr)) return jac_dbl<C>(p);
+        return jac_infinity<C>();
+    }
+    fe hh = fe_sqr(f, h);
+    fe hhh = fe_mul(f, hh, h);
+    fe v = fe_mul(f, u1, hh);
+    jac r;
+    r.X = fe_sub(f, fe_sub(f, fe_sub(f, fe_sqr(f, rr), hhh), v), v);
+    r.Y = fe_sub(f, fe_mul(f, rr, fe_sub(f, v, r.X)), fe_mul(f, s1, hhh));
+    r.Z = fe_mul(f, fe_mul(f, p.Z, q.Z), h);
+    return r;
+}
+
+// (X/Z^2, Y/Z^3) given zinv = Z^-1 (curve.cpp:169-174)
+template <class C>
+GECC_HD aff jac_to_aff_with(const jac& p, const fe& zinv) {
+    const typename C::Fp f{};
+    fe zi2 = fe_sqr(f, zinv);
+    aff r;
+    r.x = fe_mul(f, p.X, zi2);
+    r.y = fe_mul(f, p.Y, fe_mul(f, zi2, zinv));
+    return r;
+}
+
+template <class C>
+GECC_HD aff aff_neg(const aff& p) {
+    aff r;
+    r.x = p.x;
+    r.y = fe_neg(typename C::Fp{}, p.y);
+    return r;
+}
+
+}  // namespace gecc

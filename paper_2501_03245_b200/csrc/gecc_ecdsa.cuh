@@ -1,0 +1,323 @@
+// Per-lane (one thread = one signature / one scalar) building blocks of the fused
+// ECDSA kernels.  All of it is __host__ __device__ so tests/hostsim can run the
+// exact logic on the CPU.
+//
+// Reference behaviour being reproduced (values, not operation sequence):
+//   nonce_scalar      DeterministicNonceSource::scalar_for + draw_scalar
+//                     (protocol.cpp:13-34, 67-75), n parameterised
+//   fixed_base_mul    batch_fpmul's result  s*G      (batch_point.cpp:358-426)
+//   var_base_mul      batch_upmul's result  s*P      (batch_point.cpp:236-339)
+//   sign_lane         one lane of ecdsa_sign_batch   (protocol.cpp:121-164)
+//   verify_lane       one lane of ecdsa_verify_batch (protocol.cpp:184-220) +
+//                     the C-ABI decoding rules (capi.cpp:207-226)
+// The reference walks 256 bits with one shared inversion per bit; here each lane
+// keeps a Jacobian accumulator in registers: s*G is WG-bit signed windows over a
+// precomputed table of d*2^(WG*j)*G (no doublings), s*P is 4-bit signed windows
+// over an 8-entry affine table of the lane's own point kept in shared memory.
+#pragma once
+#include "gecc_curve.cuh"
+#include "gecc_dev.cuh"
+
+namespace gecc {
+
+// ------------------------------------------------------------ scalars
+GECC_HD fe u256_add(const fe& a, const fe& b, uint32_t* carry) {
+    fe r;
+    r.w[0] = add_cc(a.w[0], b.w[0]);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) r.w[i] = addc_cc(a.w[i], b.w[i]);
+    *carry = addc(0, 0);
+    return r;
+}
+GECC_HD fe u256_sub(const fe& a, const fe& b) {
+    fe r;
+    r.w[0] = sub_cc(a.w[0], b.w[0]);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) r.w[i] = subc_cc(a.w[i], b.w[i]);
+    return r;
+}
+// v mod n for v < 2n: one conditional subtraction (Scalar::reduce, curve.cpp:22-27)
+template <class Fn>
+GECC_HD fe scalar_reduce_once(const fe& v) {
+    const Fn f{};
+    fe n = fe_modulus(f);
+    return u256_lt(v, n) ? v : u256_sub(v, n);
+}
+// 0 < v < n (scalar_in_range, protocol.cpp:41-44)
+template <class Fn>
+GECC_HD bool scalar_in_range(const fe& v) {
+    return !fe_is_zero(v) && fe_lt_modulus(Fn{}, v);
+}
+
+GECC_HD uint64_t splitmix64(uint64_t* x) {  // protocol.cpp:13-19
+    *x += 0x9E3779B97F4A7C15ull;
+    uint64_t z = *x;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+template <class Fn>
+GECC_HD fe nonce_scalar(uint64_t seed, uint64_t stream, uint32_t attempt) {
+    uint64_t state = seed;
+    (void)splitmix64(&state);
+    state ^= 0xA3EC647659359ACDull * (stream + 1);
+    (void)splitmix64(&state);
+    state ^= 0xC2B2AE3D27D4EB4Full * ((uint64_t)attempt + 1);
+    for (;;) {
+        fe raw;
+#pragma unroll
+        for (int i = 0; i < 8; i += 2) {
+            uint64_t v = splitmix64(&state);
+            raw.w[i] = (uint32_t)v;
+            raw.w[i + 1] = (uint32_t)(v >> 32);
+        }
+        if (scalar_in_range<Fn>(raw)) return raw;
+    }
+}
+
+// Signed fixed-window recoding: k = sum_j (win_j(k + C) - 2^(W-1)) 2^(W j) + carry 2^256
+// with C = sum_j 2^(W-1) 2^(W j); every digit lies in [-2^(W-1), 2^(W-1)-1] and can be
+// read MSB-first without a dependent carry sweep.  W must divide 256.
+template <int W>
+struct Recoded {
+    fe biased;       // (k + C) mod 2^256
+    uint32_t carry;  // digit of the extra top window (0 or 1)
+};
+template <int W>
+GECC_HD Recoded<W> recode_signed(const fe& k) {
+    fe c;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        uint32_t v = 0;
+#pragma unroll
+        for (int b = W - 1; b < 32; b += W) v |= 1u << b;
+        c.w[i] = v;
+    }
+    static_assert(32 % W == 0 || W == 16, "window must tile the 32-bit limbs");
+    Recoded<W> r;
+    r.biased = u256_add(k, c, &r.carry);
+    return r;
+}
+template <int W>
+GECC_HD int recoded_digit(const Recoded<W>& r, int j) {  // j-th window, signed
+    int bit = j * W;
+    uint32_t v = (r.biased.w[bit >> 5] >> (bit & 31)) & ((1u << W) - 1u);
+    return (int)v - (1 << (W - 1));
+}
+
+// ------------------------------------------------------------ fixed base
+// Table layout (built by k_tables.cu): entry (j, d), d = 1 .. 2^(WG-1), holds the
+// affine Montgomery point d * 2^(WG*j) * G as 16 words x[0..7] y[0..7] at
+// tab[(j * 2^(WG-1) + d - 1) * 16].  Windows j = 0 .. 256/WG (the last one only
+// ever uses d = 1).
+template <int WG>
+struct GTable {
+    const uint32_t* tab;
+    static constexpr int windows = 256 / WG + 1;
+    static constexpr int per_window = 1 << (WG - 1);
+    GECC_HD aff load(int j, int d) const {  // d >= 1
+        const uint32_t* p = tab + ((size_t)j * per_window + (size_t)(d - 1)) * 16;
+        aff r;
+#if defined(__CUDA_ARCH__)
+        const uint4* q = reinterpret_cast<const uint4*>(p);
+        uint4 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2), e = __ldg(q + 3);
+        r.x.w[0] = a.x; r.x.w[1] = a.y; r.x.w[2] = a.z; r.x.w[3] = a.w;
+        r.x.w[4] = b.x; r.x.w[5] = b.y; r.x.w[6] = b.z; r.x.w[7] = b.w;
+        r.y.w[0] = c.x; r.y.w[1] = c.y; r.y.w[2] = c.z; r.y.w[3] = c.w;
+        r.y.w[4] = e.x; r.y.w[5] = e.y; r.y.w[6] = e.z; r.y.w[7] = e.w;
+#else
+        for (int i = 0; i < 8; ++i) {
+            r.x.w[i] = p[i];
+            r.y.w[i] = p[8 + i];
+        }
+#endif
+        return r;
+    }
+};
+
+// k * G for any 256-bit k (the value of k mod n times G, like the reference's
+// bit ladder on an unreduced scalar, acceptance.cpp:288-291).
+template <class C, int WG>
+GECC_HD jac fixed_base_mul(const fe& k_raw, const GTable<WG>& tab) {
+    const typename C::Fp f{};
+    fe k = scalar_reduce_once<typename C::Fn>(k_raw);
+    Recoded<WG> rc = recode_signed<WG>(k);
+    jac acc = jac_infinity<C>();
+#pragma unroll 1
+    for (int j = 0; j <= 256 / WG; ++j) {
+        int d = j == 256 / WG ? (int)rc.carry : recoded_digit<WG>(rc, j);
+        if (d == 0) continue;
+        aff t = tab.load(j, d < 0 ? -d : d);
+        if (d < 0) t.y = fe_neg(f, t.y);
+        acc = jac_madd<C>(acc, t);
+    }
+    return acc;
+}
+
+// ------------------------------------------------------------ variable base
+// 8-entry table of the lane's own point, entry e (0..7) = (e+1) * P, affine.
+// `base` points at this lane's first word; consecutive words of one entry are
+// `stride` words apart (stride = blockDim.x in shared memory: conflict-free,
+// 1 on the host).
+struct LaneTable {
+    uint32_t* base;
+    int stride;
+    GECC_HD void store(int e, const aff& p) const {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            base[(size_t)(e * 16 + i) * stride] = p.x.w[i];
+            base[(size_t)(e * 16 + 8 + i) * stride] = p.y.w[i];
+        }
+    }
+    GECC_HD aff load(int e) const {
+        aff p;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            p.x.w[i] = base[(size_t)(e * 16 + i) * stride];
+            p.y.w[i] = base[(size_t)(e * 16 + 8 + i) * stride];
+        }
+        return p;
+    }
+};
+
+// Builds {1..8} * P in affine form with ONE field inversion (Montgomery's trick
+// over the seven Jacobian Z's).  P must be finite and on the curve.
+template <class C>
+GECC_HD void build_lane_table(const aff& p, const LaneTable& tab) {
+    const typename C::Fp f{};
+    jac m[8];
+    m[0].X = p.x; m[0].Y = p.y; m[0].Z = fe_one(f);
+    m[1] = jac_dbl<C>(m[0]);
+    m[2] = jac_madd<C>(m[1], p);
+    m[3] = jac_dbl<C>(m[1]);
+    m[4] = jac_madd<C>(m[3], p);
+    m[5] = jac_dbl<C>(m[2]);
+    m[6] = jac_madd<C>(m[5], p);
+    m[7] = jac_dbl<C>(m[3]);
+    // prefix products of Z_1..Z_7 (none is zero: the group has prime order > 8)
+    fe pre[8];
+    pre[1] = m[1].Z;
+#pragma unroll
+    for (int i = 2; i < 8; ++i) pre[i] = fe_mul(f, pre[i - 1], m[i].Z);
+    fe inv = fe_inv_fermat(f, pre[7]);
+    tab.store(0, p);
+#pragma unroll
+    for (int i = 7; i >= 1; --i) {
+        fe zi = i > 1 ? fe_mul(f, inv, pre[i - 1]) : inv;
+        if (i > 1) inv = fe_mul(f, inv, m[i].Z);
+        tab.store(i, jac_to_aff_with<C>(m[i], zi));
+    }
+}
+
+// k * P, P finite and on the curve, any 256-bit k (k mod n is what is computed).
+template <class C>
+GECC_HD jac var_base_mul(const fe& k_raw, const LaneTable& tab) {
+    const typename C::Fp f{};
+    fe k = scalar_reduce_once<typename C::Fn>(k_raw);
+    Recoded<4> rc = recode_signed<4>(k);
+    jac acc = jac_infinity<C>();
+    if (rc.carry) {
+        aff t = tab.load(0);
+        acc.X = t.x; acc.Y = t.y; acc.Z = fe_one(f);
+    }
+#pragma unroll 1
+    for (int j = 63; j >= 0; --j) {
+        acc = jac_dbl<C>(acc);
+        acc = jac_dbl<C>(acc);
+        acc = jac_dbl<C>(acc);
+        acc = jac_dbl<C>(acc);
+        int d = recoded_digit<4>(rc, j);
+        if (d != 0) {
+            aff t = tab.load((d < 0 ? -d : d) - 1);
+            if (d < 0) t.y = fe_neg(f, t.y);
+            acc = jac_madd<C>(acc, t);
+        }
+    }
+    return acc;
+}
+
+// ------------------------------------------------------------ point codec
+// 65-byte record 0x04 || X || Y -> affine Montgomery point; false when the tag,
+// range or curve check fails (decode_point, curve.cpp:203-217).
+template <class C>
+GECC_HD bool decode_point(const uint8_t* rec, aff* out) {
+    const typename C::Fp f{};
+    if (rec[0] != 0x04) return false;
+    fe x = be32_load(rec + 1), y = be32_load(rec + 33);
+    if (!fe_lt_modulus(f, x) || !fe_lt_modulus(f, y)) return false;
+    out->x = fe_to_mont(f, x);
+    out->y = fe_to_mont(f, y);
+    return aff_on_curve<C>(*out);
+}
+template <class C>
+GECC_HD void encode_point(uint8_t* rec, const aff& p) {  // curve.cpp:192-201
+    const typename C::Fp f{};
+    rec[0] = 0x04;
+    be32_store(rec + 1, fe_from_mont(f, p.x));
+    be32_store(rec + 33, fe_from_mont(f, p.y));
+}
+
+// ------------------------------------------------------------ ECDSA lanes
+enum { LANE_OK = 0, LANE_NONCE_EXHAUSTED = 5 };  // sm2b_status values
+
+// One lane of ecdsa_sign_batch: e already reduced mod n, 0 < d < n.
+// Writes r || s (64 bytes) or zeros; returns the lane status.
+template <class C, int WG>
+GECC_HD int sign_lane(const fe& e, const fe& d, uint64_t seed, uint64_t stream,
+                      const GTable<WG>& gt, uint8_t* sig64) {
+    const typename C::Fp fp{};
+    const typename C::Fn fn{};
+    fe e_m = fe_to_mont(fn, e);
+    fe d_m = fe_to_mont(fn, d);
+#pragma unroll 1
+    for (uint32_t attempt = 0; attempt < 8; ++attempt) {     // protocol.cpp:121
+        fe k = nonce_scalar<typename C::Fn>(seed, stream, attempt);
+        jac R = fixed_base_mul<C, WG>(k, gt);
+        if (jac_is_inf(R)) continue;                          // cannot happen for 0 < k < n
+        fe zinv = fe_inv_fermat(fp, R.Z);
+        fe x = fe_from_mont(fp, fe_mul(fp, R.X, fe_sqr(fp, zinv)));
+        fe r = scalar_reduce_once<typename C::Fn>(x);         // coord_mod_n, protocol.cpp:37-39
+        if (fe_is_zero(r)) continue;
+        fe kinv_m = fe_inv_fermat(fn, fe_to_mont(fn, k));
+        fe r_m = fe_to_mont(fn, r);
+        fe s_m = fe_mul(fn, kinv_m, fe_add(fn, e_m, fe_mul(fn, r_m, d_m)));
+        fe s = fe_from_mont(fn, s_m);
+        if (fe_is_zero(s)) continue;
+        be32_store(sig64, r);
+        be32_store(sig64 + 32, s);
+        return LANE_OK;
+    }
+    for (int i = 0; i < 64; ++i) sig64[i] = 0;
+    return LANE_NONCE_EXHAUSTED;
+}
+
+// One lane of sm2b_verify: raw records in, 0/1 out.
+template <class C, int WG>
+GECC_HD uint8_t verify_lane(const uint8_t* digest32, const uint8_t* pub65, const uint8_t* sig64,
+                            const GTable<WG>& gt, const LaneTable& qt) {
+    const typename C::Fp fp{};
+    const typename C::Fn fn{};
+    fe r = be32_load(sig64), s = be32_load(sig64 + 32);
+    if (!scalar_in_range<typename C::Fn>(r) || !scalar_in_range<typename C::Fn>(s)) return 0;
+    aff Q;
+    if (!decode_point<C>(pub65, &Q)) return 0;
+    fe e = scalar_reduce_once<typename C::Fn>(be32_load(digest32));   // capi.cpp:81-88
+    fe w_m = fe_inv_fermat(fn, fe_to_mont(fn, s));                     // s^-1 (Montgomery form)
+    fe u1 = fe_mul(fn, e, w_m);                                        // e * w, plain
+    fe u2 = fe_mul(fn, r, w_m);
+    jac A = fixed_base_mul<C, WG>(u1, gt);
+    build_lane_table<C>(Q, qt);
+    jac B = var_base_mul<C>(u2, qt);
+    jac R = jac_add<C>(A, B);
+    if (jac_is_inf(R)) return 0;
+    // x(R) mod n == r  <=>  X == r Z^2  or  (r + n < p and X == (r + n) Z^2)
+    fe zz = fe_sqr(fp, R.Z);
+    if (fe_eq(R.X, fe_mul(fp, fe_to_mont(fp, r), zz))) return 1;
+    uint32_t carry;
+    fe rn = u256_add(r, fe_modulus(fn), &carry);
+    if (carry == 0 && fe_lt_modulus(fp, rn) && fe_eq(R.X, fe_mul(fp, fe_to_mont(fp, rn), zz)))
+        return 1;
+    return 0;
+}
+
+}  // namespace gecc

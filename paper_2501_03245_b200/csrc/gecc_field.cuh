@@ -245,10 +245,12 @@ GECC_HD fe redc_secp(const F& f, const uint32_t* t) {
     uint32_t dlo = 0, dhi = 0;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        uint32_t v = sub_cc(t[i], dlo);       // CF = borrow
+        uint32_t v = sub_cc(t[i], dlo);
+        uint32_t bmask = subc(0, 0);           // 0xFFFFFFFF on borrow (sub family only:
+                                               // a sub-produced flag must never feed addc)
         m[i] = mul_lo(v, F::qinv32);           // m_i * 977 == v mod 2^32
         uint32_t ph = mul_hi(m[i], 977u);
-        uint32_t tmp = addc(dhi, ph);          // dhi + hi(m_i*977) + borrow (no overflow)
+        uint32_t tmp = dhi + ph - bmask;       // dhi + hi(m_i*977) + borrow (no overflow)
         dlo = add_cc(tmp, m[i]);               // + m_i from the 2^32 term of c
         dhi = addc(0, 0);
     }
@@ -311,7 +313,7 @@ GECC_HD fe fe_from_mont(const F& f, const fe& a) {  // a * R^-1
 // a^(q-2) in Montgomery form, 4-bit fixed window: 256 squarings + 64 + 14 products.
 // Not unrolled on purpose (code size).  Zero maps to zero.
 template <class F>
-GECC_HD fe fe_inv_fermat(const F& f, const fe& a) {
+GECC_HD_CALL fe fe_inv_fermat(const F& f, const fe& a) {
     fe tab[16];
     tab[0] = fe_one(f);
     tab[1] = a;

@@ -5,6 +5,10 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#ifndef GECC_WG
+#define GECC_WG 16  // fixed-base window width in bits (table = 17 x 2^15 x 64 B = 34 MiB)
+#endif
+
 namespace gecc {
 
 enum { CURVE_SM2 = 0, CURVE_SECP = 1 };
@@ -13,5 +17,33 @@ cudaError_t launch_field_op(int curve, int field, int op, size_t n, const uint32
                             const uint32_t* b, uint32_t* out, cudaStream_t s);
 cudaError_t run_microbench(int which, int iters, int sm_count, double* ops_per_clk_per_sm,
                            double* seconds, double* total_ops, cudaStream_t s);
+
+size_t gtable_words();
+cudaError_t build_gtable(int curve, uint32_t* tab, uint32_t* bases_scratch, cudaStream_t s);
+
+cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t* pub,
+                          const uint8_t* sig, const uint32_t* gtab, uint8_t* res, cudaStream_t s);
+cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed,
+                        uint64_t lane_base, const uint32_t* gtab, uint8_t* sig, int32_t* status,
+                        uint32_t* flags, cudaStream_t s);
+cudaError_t launch_keygen(int curve, size_t n, uint64_t seed, uint64_t lane_base,
+                          const uint32_t* gtab, uint8_t* sec, uint8_t* pub, cudaStream_t s);
+cudaError_t launch_ecdh(int curve, size_t n, const uint8_t* sec, const uint8_t* peers,
+                        uint8_t* shared, int32_t* status, uint32_t* flags, cudaStream_t s);
+cudaError_t launch_fpmul(int curve, size_t n, const uint32_t* k, const uint32_t* gtab, uint32_t* ox,
+                         uint32_t* oy, uint8_t* oinf, cudaStream_t s);
+cudaError_t launch_upmul(int curve, size_t n, const uint32_t* k, const uint32_t* px,
+                         const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
+                         uint8_t* oinf, cudaStream_t s);
+
+cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* in, uint32_t* out,
+                                cudaStream_t s);
+cudaError_t launch_batch_padd(int curve, size_t n, const uint32_t* px, const uint32_t* py,
+                              const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty,
+                              const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
+                              cudaStream_t s);
+cudaError_t launch_batch_pdbl(int curve, size_t n, const uint32_t* px, const uint32_t* py,
+                              const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
+                              cudaStream_t s);
 
 }  // namespace gecc

@@ -1,0 +1,225 @@
+// Fused ECDSA kernels: one thread = one lane; wire records are decoded, checked,
+// processed and re-encoded on the GPU, nothing but the records touches HBM
+// (reference path: capi.cpp:145-261 host loops + protocol.cpp:106-263, which
+// re-reads all point state from memory for each of 256 bit steps).
+#include "gecc_ecdsa.cuh"
+#include "gecc_host.h"
+
+namespace gecc {
+
+constexpr int VERIFY_THREADS = 128;  // x 512 B of lane table = 64 KiB shared memory per block
+constexpr int SIGN_THREADS = 128;
+
+template <class C>
+__global__ void __launch_bounds__(VERIFY_THREADS)
+k_verify(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ pub,
+         const uint8_t* __restrict__ sig, const uint32_t* __restrict__ gtab,
+         uint8_t* __restrict__ res) {
+    extern __shared__ uint32_t lane_tables[];
+    const size_t i = blockIdx.x * (size_t)VERIFY_THREADS + threadIdx.x;
+    if (i >= n) return;
+    GTable<GECC_WG> gt{gtab};
+    LaneTable qt{lane_tables + threadIdx.x, VERIFY_THREADS};
+    res[i] = verify_lane<C, GECC_WG>(dig + 32 * i, pub + 65 * i, sig + 64 * i, gt, qt);
+}
+
+// flags[0] is set when any secret is zero or >= n: the whole call is malformed
+// (capi.cpp:181-184) and the host discards the outputs.
+template <class C>
+__global__ void __launch_bounds__(SIGN_THREADS)
+k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ sec, uint64_t seed,
+       uint64_t lane_base, const uint32_t* __restrict__ gtab, uint8_t* __restrict__ sig,
+       int32_t* __restrict__ status, uint32_t* __restrict__ flags) {
+    const size_t i = blockIdx.x * (size_t)SIGN_THREADS + threadIdx.x;
+    if (i >= n) return;
+    GTable<GECC_WG> gt{gtab};
+    fe d = be32_load(sec + 32 * i);
+    if (!scalar_in_range<typename C::Fn>(d)) {
+        atomicOr(flags, 1u);
+        status[i] = 2;
+        for (int b = 0; b < 64; ++b) sig[64 * i + b] = 0;
+        return;
+    }
+    fe e = scalar_reduce_once<typename C::Fn>(be32_load(dig + 32 * i));
+    status[i] = sign_lane<C, GECC_WG>(e, d, seed, lane_base + i, gt, sig + 64 * i);
+}
+
+// capi.cpp:145-169: secret = nonce stream (lane, attempt 0), public = secret * G
+template <class C>
+__global__ void __launch_bounds__(SIGN_THREADS)
+k_keygen(size_t n, uint64_t seed, uint64_t lane_base, const uint32_t* __restrict__ gtab,
+         uint8_t* __restrict__ sec, uint8_t* __restrict__ pub) {
+    const size_t i = blockIdx.x * (size_t)SIGN_THREADS + threadIdx.x;
+    if (i >= n) return;
+    const typename C::Fp f{};
+    GTable<GECC_WG> gt{gtab};
+    fe d = nonce_scalar<typename C::Fn>(seed, lane_base + i, 0);
+    be32_store(sec + 32 * i, d);
+    jac r = fixed_base_mul<C, GECC_WG>(d, gt);
+    encode_point<C>(pub + 65 * i, jac_to_aff_with<C>(r, fe_inv_fermat(f, r.Z)));
+}
+
+// capi.cpp:230-261 + protocol.cpp:224-263.  status: 0 ok, 3 invalid peer,
+// 4 degenerate; a secret >= n flags the whole call malformed.
+template <class C>
+__global__ void __launch_bounds__(VERIFY_THREADS)
+k_ecdh(size_t n, const uint8_t* __restrict__ sec, const uint8_t* __restrict__ peers,
+       uint8_t* __restrict__ shared, int32_t* __restrict__ status, uint32_t* __restrict__ flags) {
+    extern __shared__ uint32_t lane_tables[];
+    const size_t i = blockIdx.x * (size_t)VERIFY_THREADS + threadIdx.x;
+    if (i >= n) return;
+    const typename C::Fp f{};
+    LaneTable qt{lane_tables + threadIdx.x, VERIFY_THREADS};
+    for (int b = 0; b < 32; ++b) shared[32 * i + b] = 0;
+    fe d = be32_load(sec + 32 * i);
+    if (!fe_lt_modulus(typename C::Fn{}, d)) {  // Scalar::checked: zero is allowed here
+        atomicOr(flags, 1u);
+        status[i] = 2;
+        return;
+    }
+    aff p;
+    if (!decode_point<C>(peers + 65 * i, &p)) {
+        status[i] = 3;
+        return;
+    }
+    build_lane_table<C>(p, qt);
+    jac r = var_base_mul<C>(d, qt);
+    if (jac_is_inf(r)) {
+        status[i] = 4;
+        return;
+    }
+    fe zinv = fe_inv_fermat(f, r.Z);
+    be32_store(shared + 32 * i, fe_from_mont(f, fe_mul(f, r.X, fe_sqr(f, zinv))));
+    status[i] = 0;
+}
+
+// ---- column-buffer forms of the two multiplication kernels (batch_point.hpp:72-91)
+template <class C>
+__device__ __forceinline__ void store_affine(const jac& r, uint32_t* ox, uint32_t* oy,
+                                             uint8_t* oinf, size_t n, size_t i) {
+    const typename C::Fp f{};
+    if (jac_is_inf(r)) {  // infinity coordinates are normalised to zero (batch_point.cpp:41-47)
+        col_store(ox, n, i, fe_zero());
+        col_store(oy, n, i, fe_zero());
+        oinf[i] = 1;
+        return;
+    }
+    aff a = jac_to_aff_with<C>(r, fe_inv_fermat(f, r.Z));
+    col_store(ox, n, i, a.x);
+    col_store(oy, n, i, a.y);
+    oinf[i] = 0;
+}
+
+template <class C>
+__global__ void __launch_bounds__(SIGN_THREADS)
+k_fpmul(size_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ gtab,
+        uint32_t* __restrict__ ox, uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf) {
+    const size_t i = blockIdx.x * (size_t)SIGN_THREADS + threadIdx.x;
+    if (i >= n) return;
+    GTable<GECC_WG> gt{gtab};
+    store_affine<C>(fixed_base_mul<C, GECC_WG>(col_load(k, n, i), gt), ox, oy, oinf, n, i);
+}
+
+template <class C>
+__global__ void __launch_bounds__(VERIFY_THREADS)
+k_upmul(size_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ px,
+        const uint32_t* __restrict__ py, const uint8_t* __restrict__ pinf,
+        uint32_t* __restrict__ ox, uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf) {
+    extern __shared__ uint32_t lane_tables[];
+    const size_t i = blockIdx.x * (size_t)VERIFY_THREADS + threadIdx.x;
+    if (i >= n) return;
+    LaneTable qt{lane_tables + threadIdx.x, VERIFY_THREADS};
+    if (pinf && pinf[i]) {  // infinity input stays infinity (test_batch_point.cpp:231,244)
+        store_affine<C>(jac_infinity<C>(), ox, oy, oinf, n, i);
+        return;
+    }
+    aff p{col_load(px, n, i), col_load(py, n, i)};
+    build_lane_table<C>(p, qt);
+    store_affine<C>(var_base_mul<C>(col_load(k, n, i), qt), ox, oy, oinf, n, i);
+}
+
+// ---------------------------------------------------------------- launchers
+constexpr size_t LANE_TABLE_SMEM = (size_t)VERIFY_THREADS * 8 * 16 * sizeof(uint32_t);
+
+template <class K>
+static cudaError_t opt_in_smem(K kernel) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)LANE_TABLE_SMEM);
+}
+static int blocks_for(size_t n, int threads) { return (int)((n + threads - 1) / threads); }
+
+#define GECC_BY_CURVE(curve, EXPR_SECP, EXPR_SM2) \
+    do {                                          \
+        if ((curve) == CURVE_SECP) { EXPR_SECP; } \
+        else { EXPR_SM2; }                        \
+    } while (0)
+
+cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t* pub,
+                          const uint8_t* sig, const uint32_t* gtab, uint8_t* res, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    cudaError_t e = curve == CURVE_SECP ? opt_in_smem(k_verify<SecpCurve>) : opt_in_smem(k_verify<Sm2Curve>);
+    if (e != cudaSuccess) return e;
+    const int b = blocks_for(n, VERIFY_THREADS);
+    GECC_BY_CURVE(curve,
+        (k_verify<SecpCurve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, dig, pub, sig, gtab, res)),
+        (k_verify<Sm2Curve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, dig, pub, sig, gtab, res)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed,
+                        uint64_t lane_base, const uint32_t* gtab, uint8_t* sig, int32_t* status,
+                        uint32_t* flags, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int b = blocks_for(n, SIGN_THREADS);
+    GECC_BY_CURVE(curve,
+        (k_sign<SecpCurve><<<b, SIGN_THREADS, 0, s>>>(n, dig, sec, seed, lane_base, gtab, sig, status, flags)),
+        (k_sign<Sm2Curve><<<b, SIGN_THREADS, 0, s>>>(n, dig, sec, seed, lane_base, gtab, sig, status, flags)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_keygen(int curve, size_t n, uint64_t seed, uint64_t lane_base,
+                          const uint32_t* gtab, uint8_t* sec, uint8_t* pub, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int b = blocks_for(n, SIGN_THREADS);
+    GECC_BY_CURVE(curve,
+        (k_keygen<SecpCurve><<<b, SIGN_THREADS, 0, s>>>(n, seed, lane_base, gtab, sec, pub)),
+        (k_keygen<Sm2Curve><<<b, SIGN_THREADS, 0, s>>>(n, seed, lane_base, gtab, sec, pub)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ecdh(int curve, size_t n, const uint8_t* sec, const uint8_t* peers,
+                        uint8_t* shared, int32_t* status, uint32_t* flags, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    cudaError_t e = curve == CURVE_SECP ? opt_in_smem(k_ecdh<SecpCurve>) : opt_in_smem(k_ecdh<Sm2Curve>);
+    if (e != cudaSuccess) return e;
+    const int b = blocks_for(n, VERIFY_THREADS);
+    GECC_BY_CURVE(curve,
+        (k_ecdh<SecpCurve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, sec, peers, shared, status, flags)),
+        (k_ecdh<Sm2Curve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, sec, peers, shared, status, flags)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fpmul(int curve, size_t n, const uint32_t* k, const uint32_t* gtab, uint32_t* ox,
+                         uint32_t* oy, uint8_t* oinf, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int b = blocks_for(n, SIGN_THREADS);
+    GECC_BY_CURVE(curve,
+        (k_fpmul<SecpCurve><<<b, SIGN_THREADS, 0, s>>>(n, k, gtab, ox, oy, oinf)),
+        (k_fpmul<Sm2Curve><<<b, SIGN_THREADS, 0, s>>>(n, k, gtab, ox, oy, oinf)));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_upmul(int curve, size_t n, const uint32_t* k, const uint32_t* px,
+                         const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
+                         uint8_t* oinf, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    cudaError_t e = curve == CURVE_SECP ? opt_in_smem(k_upmul<SecpCurve>) : opt_in_smem(k_upmul<Sm2Curve>);
+    if (e != cudaSuccess) return e;
+    const int b = blocks_for(n, VERIFY_THREADS);
+    GECC_BY_CURVE(curve,
+        (k_upmul<SecpCurve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, k, px, py, pinf, ox, oy, oinf)),
+        (k_upmul<Sm2Curve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, k, px, py, pinf, ox, oy, oinf)));
+    return cudaGetLastError();
+}
+
+}  // namespace gecc

@@ -55,3 +55,131 @@ int hs_field_op(int field, const FieldRT* rt, int op, size_t n, const uint32_t* 
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// ECDSA / point-multiplication lanes (gecc_ecdsa.cuh) run as plain host loops.
+#include <vector>
+
+#include "gecc_ecdsa.cuh"
+
+namespace {
+
+constexpr int HS_WG = 4;  // small fixed-base window so the host can build the table quickly
+
+template <class C>
+const std::vector<uint32_t>& host_gtable() {
+    static std::vector<uint32_t> tab;
+    if (!tab.empty()) return tab;
+    using GT = GTable<HS_WG>;
+    const typename C::Fp f{};
+    tab.assign((size_t)GT::windows * GT::per_window * 16, 0);
+    jac base;  // 2^(WG*j) * G
+    aff g = curve_g<C>();
+    base.X = g.x; base.Y = g.y; base.Z = fe_one(f);
+    for (int j = 0; j < GT::windows; ++j) {
+        aff b = jac_to_aff_with<C>(base, fe_inv_fermat(f, base.Z));
+        jac acc = jac_infinity<C>();
+        for (int d = 1; d <= GT::per_window; ++d) {
+            acc = jac_madd<C>(acc, b);
+            aff e = jac_to_aff_with<C>(acc, fe_inv_fermat(f, acc.Z));
+            uint32_t* p = &tab[((size_t)j * GT::per_window + (d - 1)) * 16];
+            for (int i = 0; i < 8; ++i) { p[i] = e.x.w[i]; p[8 + i] = e.y.w[i]; }
+        }
+        for (int k = 0; k < HS_WG; ++k) base = jac_dbl<C>(base);
+    }
+    return tab;
+}
+
+template <class C>
+void store_point(const jac& r, uint32_t* ox, uint32_t* oy, uint8_t* oinf, size_t n, size_t i) {
+    const typename C::Fp f{};
+    if (jac_is_inf(r)) {
+        col_set(ox, n, i, fe_zero());
+        col_set(oy, n, i, fe_zero());
+        oinf[i] = 1;
+        return;
+    }
+    aff a = jac_to_aff_with<C>(r, fe_inv_fermat(f, r.Z));
+    col_set(ox, n, i, a.x);
+    col_set(oy, n, i, a.y);
+    oinf[i] = 0;
+}
+
+template <class C>
+int fpmul_t(size_t n, const uint32_t* k, uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    GTable<HS_WG> gt{host_gtable<C>().data()};
+    for (size_t i = 0; i < n; ++i)
+        store_point<C>(fixed_base_mul<C, HS_WG>(col_get(k, n, i), gt), ox, oy, oinf, n, i);
+    return 0;
+}
+template <class C>
+int upmul_t(size_t n, const uint32_t* k, const uint32_t* px, const uint32_t* py,
+            const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    uint32_t lane[8 * 16];
+    LaneTable lt{lane, 1};
+    for (size_t i = 0; i < n; ++i) {
+        if (pinf && pinf[i]) { store_point<C>(jac_infinity<C>(), ox, oy, oinf, n, i); continue; }
+        aff p{col_get(px, n, i), col_get(py, n, i)};
+        build_lane_table<C>(p, lt);
+        store_point<C>(var_base_mul<C>(col_get(k, n, i), lt), ox, oy, oinf, n, i);
+    }
+    return 0;
+}
+template <class C>
+int sign_t(size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed, uint64_t base,
+           uint8_t* sig, int32_t* st) {
+    GTable<HS_WG> gt{host_gtable<C>().data()};
+    for (size_t i = 0; i < n; ++i) {
+        fe e = scalar_reduce_once<typename C::Fn>(be32_load(dig + 32 * i));
+        fe d = be32_load(sec + 32 * i);
+        st[i] = sign_lane<C, HS_WG>(e, d, seed, base + i, gt, sig + 64 * i);
+    }
+    return 0;
+}
+template <class C>
+int verify_t(size_t n, const uint8_t* dig, const uint8_t* pub, const uint8_t* sig, uint8_t* res) {
+    GTable<HS_WG> gt{host_gtable<C>().data()};
+    uint32_t lane[8 * 16];
+    LaneTable lt{lane, 1};
+    for (size_t i = 0; i < n; ++i)
+        res[i] = verify_lane<C, HS_WG>(dig + 32 * i, pub + 65 * i, sig + 64 * i, gt, lt);
+    return 0;
+}
+template <class C>
+int keygen_t(size_t n, uint64_t seed, uint64_t base, uint8_t* sec, uint8_t* pub) {
+    GTable<HS_WG> gt{host_gtable<C>().data()};
+    const typename C::Fp f{};
+    for (size_t i = 0; i < n; ++i) {
+        fe d = nonce_scalar<typename C::Fn>(seed, base + i, 0);
+        be32_store(sec + 32 * i, d);
+        jac r = fixed_base_mul<C, HS_WG>(d, gt);
+        encode_point<C>(pub + 65 * i, jac_to_aff_with<C>(r, fe_inv_fermat(f, r.Z)));
+    }
+    return 0;
+}
+}  // namespace
+
+extern "C" {
+int hs_fpmul(int curve, size_t n, const uint32_t* k, uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    return curve == 0 ? fpmul_t<Sm2Curve>(n, k, ox, oy, oinf) : fpmul_t<SecpCurve>(n, k, ox, oy, oinf);
+}
+int hs_upmul(int curve, size_t n, const uint32_t* k, const uint32_t* px, const uint32_t* py,
+             const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    return curve == 0 ? upmul_t<Sm2Curve>(n, k, px, py, pinf, ox, oy, oinf)
+                      : upmul_t<SecpCurve>(n, k, px, py, pinf, ox, oy, oinf);
+}
+int hs_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed,
+            uint64_t base, uint8_t* sig, int32_t* st) {
+    return curve == 0 ? sign_t<Sm2Curve>(n, dig, sec, seed, base, sig, st)
+                      : sign_t<SecpCurve>(n, dig, sec, seed, base, sig, st);
+}
+int hs_verify(int curve, size_t n, const uint8_t* dig, const uint8_t* pub, const uint8_t* sig,
+              uint8_t* res) {
+    return curve == 0 ? verify_t<Sm2Curve>(n, dig, pub, sig, res)
+                      : verify_t<SecpCurve>(n, dig, pub, sig, res);
+}
+int hs_keygen(int curve, size_t n, uint64_t seed, uint64_t base, uint8_t* sec, uint8_t* pub) {
+    return curve == 0 ? keygen_t<Sm2Curve>(n, seed, base, sec, pub)
+                      : keygen_t<SecpCurve>(n, seed, base, sec, pub);
+}
+}  // extern "C"

@@ -1,0 +1,81 @@
+"""TEST-ONLY ctypes view of tests/hostsim/_build/libgecc_hostsim.so: the product's
+__host__ __device__ limb / curve / ECDSA-lane code compiled for the CPU."""
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(HERE, "_build", "libgecc_hostsim.so")
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        subprocess.check_call(["make", "-C", HERE], stdout=subprocess.DEVNULL)
+        _lib = C.CDLL(LIB, mode=os.RTLD_LOCAL)
+    return _lib
+
+
+def _p(a):
+    if a is None:
+        return None
+    if isinstance(a, np.ndarray):
+        return C.c_void_p(a.ctypes.data)
+    return C.cast(C.c_char_p(bytes(a)), C.c_void_p) if len(a) else None
+
+
+FIELD_IDS = {(1, 0): 0, (1, 1): 1, (0, 0): 2, (0, 1): 3}  # (curve, which) -> hostsim field id
+OPS = dict(mont_mul=0, mod_add=1, mod_sub=2, to_mont=3, from_mont=4, mod_inv=5, sqr=6)
+
+
+def field_op(curve, which, op, a, b=None):
+    n = a.shape[1]
+    out = np.zeros((8, n), np.uint32)
+    rc = lib().hs_field_op(FIELD_IDS[(curve, which)], None, OPS[op], C.c_size_t(n), _p(a), _p(b), _p(out))
+    assert rc == 0
+    return out
+
+
+def _pts(n):
+    return np.zeros((8, n), np.uint32), np.zeros((8, n), np.uint32), np.zeros(n, np.uint8)
+
+
+def batch_fpmul(curve, k):
+    n = k.shape[1]
+    o = _pts(n)
+    assert lib().hs_fpmul(curve, C.c_size_t(n), _p(k), _p(o[0]), _p(o[1]), _p(o[2])) == 0
+    return o
+
+
+def batch_upmul(curve, k, P):
+    n = k.shape[1]
+    o = _pts(n)
+    assert lib().hs_upmul(curve, C.c_size_t(n), _p(k), _p(P[0]), _p(P[1]), _p(P[2]), _p(o[0]),
+                          _p(o[1]), _p(o[2])) == 0
+    return o
+
+
+def sign(curve, dig, sec, seed, lane_base=0):
+    n = len(dig) // 32
+    sig = (C.c_uint8 * max(1, 64 * n))()
+    st = (C.c_int32 * max(1, n))()
+    assert lib().hs_sign(curve, C.c_size_t(n), _p(dig), _p(sec), C.c_uint64(seed),
+                         C.c_uint64(lane_base), sig, st) == 0
+    return bytes(sig)[:64 * n], list(st)[:n]
+
+
+def verify(curve, dig, pub, sig):
+    n = len(dig) // 32
+    res = (C.c_uint8 * max(1, n))()
+    assert lib().hs_verify(curve, C.c_size_t(n), _p(dig), _p(pub), _p(sig), res) == 0
+    return bytes(res)[:n]
+
+
+def keygen(curve, seed, n, lane_base=0):
+    sec = (C.c_uint8 * max(1, 32 * n))()
+    pub = (C.c_uint8 * max(1, 65 * n))()
+    assert lib().hs_keygen(curve, C.c_size_t(n), C.c_uint64(seed), C.c_uint64(lane_base), sec, pub) == 0
+    return bytes(sec)[:32 * n], bytes(pub)[:65 * n]
