@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark: secp256k1 ECDSA verify, batch 2^20 per GPU.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload verify|sign|padd] [--log2n 20]
+
+One JSON line on stdout (rank 0).  A "step" is one pass of the hot path over one
+batch of synthetic records (BASELINE.json configs[1]: 2^20 signatures per GPU).
+
+  value     whole-job throughput with the records already resident in HBM
+            (CUDA events on the stream the kernel is launched on, max over ranks)
+  e2e       the same metric through the reference-facing C ABI (sm2b_verify on a
+            secp256k1 context): pinned HOST buffers in, host results out, the
+            host<->device copies inside the timed region
+  roofline  integer-multiply (IMAD) pipe: executed field multiplications x
+            multiply-issue slots each, against the pipe peak measured live by
+            the library's own microbenchmark in the same process
+  cpu_baseline  the reference's CPU path on this box's host cores on a bounded
+            sample of the same records (oracle/_ref, else the C port)
+
+N > 1: launched by torchrun, one rank per GPU; lanes are sharded by range with
+the global lane index as nonce stream, no data-path collective (scaling: weak).
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SECP = 1
+METRIC = {"verify": "ecdsa_verify_throughput", "sign": "ecdsa_sign_throughput",
+          "padd": "batch_padd_throughput"}
+UNIT = {"verify": "verifications/s", "sign": "signatures/s", "padd": "point additions/s"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="verify", choices=["verify", "sign", "padd"])
+    ap.add_argument("--log2n", type=int, default=20)
+    ap.add_argument("--cpu-sample-log2", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.rows, self.proc = [], None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for nm, v in zip(names, r[3:7]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# ----------------------------------------------------------------------------- CPU arm
+def cpu_verify_runner():
+    """Returns (kind, cores, fn(dig, pub, sig) -> results) for the CPU reference path."""
+    from oracle import refshim as R
+    if R.available():
+        cores = os.cpu_count() or 1
+        return "reference", cores, lambda d, p, s: R.ecdsa_verify(SECP, d, p, s, workers=0)[1]
+    from oracle import coracle as O
+    return "port", 1, lambda d, p, s: O.ecdsa_verify(SECP, d, p, s)[1]
+
+
+def cpu_sign_runner():
+    from oracle import refshim as R
+    if R.available():
+        cores = os.cpu_count() or 1
+        return "reference", cores, lambda d, s, seed: R.ecdsa_sign(SECP, d, s, seed, workers=0)[1]
+    from oracle import coracle as O
+    return "port", 1, lambda d, s, seed: O.ecdsa_sign(SECP, d, s, seed)[1]
+
+
+def make_records_cpu(n, seed=1):
+    """Synthetic keys/digests/signatures for the reference arm, made by the CPU path itself."""
+    from oracle import refshim as R
+    from oracle import coracle as O
+    import numpy as np
+    src = R if R.available() else O
+    kw = {"workers": 0} if R.available() else {}
+    rc, sec, pub = src.keygen(SECP, seed, n, **kw)
+    dig = np.random.RandomState(seed).bytes(32 * n)
+    rc, sig, st = src.ecdsa_sign(SECP, dig, sec, seed + 1, **kw)
+    return dig, sec, pub, sig
+
+
+def run_reference_arm(args, rank):
+    if rank != 0:
+        return
+    wl = args.workload if args.workload != "padd" else "verify"
+    log2 = args.cpu_sample_log2 or (13 if wl == "verify" else 14)
+    n = 1 << log2
+    dig, sec, pub, sig = make_records_cpu(n)
+    if wl == "verify":
+        kind, cores, fn = cpu_verify_runner()
+        step = lambda: fn(dig, pub, sig)
+    else:
+        kind, cores, fn = cpu_sign_runner()
+        step = lambda: fn(dig, sec, 7)
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        out = step()
+    dt = time.perf_counter() - t0
+    if wl == "verify":
+        assert out == b"\x01" * n
+    value = n * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC[wl], "value": value, "unit": UNIT[wl],
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32 limbs (256-bit modular integer)", "data": "synthetic",
+        "config": {"workload": f"secp256k1 ECDSA {wl}, batch 2^{args.log2n} per GPU",
+                   "curve": "secp256k1", "cpu_sample_lanes_per_step": n},
+        "cpu_baseline": {"value": value, "unit": UNIT[wl], "cores": cores, "kind": kind,
+                         "sample": f"2^{log2} lanes per step of the same synthetic recipe; "
+                                   "reference batch kernels (batch_fpmul/upmul/padd/invert) "
+                                   "driven by the restated secp256k1 protocol glue"},
+        "e2e": {"value": value, "unit": UNIT[wl], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+# Executed field multiplications per lane of OUR kernels (analytic, from the code in
+# gecc_ecdsa.cuh) and FMA-pipe issue slots per
+# multiplication in IMAD.WIDE units (IMAD.WIDE / IMAD.HI = 1, 32-bit IMAD = 1/2; measured
+# issue rates 32 and 64 per clk per SM).
+MAD_SECP_P = 64 + 8 + 8 * 0.5          # product + 8 IMAD.HI + 8 IMAD of the word-serial REDC
+MAD_GENERIC = 64 + (28 + 36 * 0.5) + 64  # product + low product + m*q product
+
+
+def verify_work_per_lane():
+    fp = dict(decode=5, gmul=17 * 11, table=4 * 7 + 3 * 11 + 6 + 334 + 6 * 2 + 7 * 4,
+              ladder=256 * 7 + 64 * (15 / 16) * 11, final=16 + 3)
+    fn = dict(inv=334 + 1, u=2)
+    return sum(fp.values()), sum(fn.values())
+
+
+def sign_work_per_lane():
+    return 17 * 11 + 334 + 3, 2 + 334 + 1 + 4 + 1
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl == "reference":
+        run_reference_arm(args, rank)
+        return
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2501_03245_b200 as gecc
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device; the product has no CPU path "
+                         "(use --impl reference for the CPU arm)")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    n = 1 << args.log2n
+    lane_base = rank * n
+    wl = args.workload
+    ctx = gecc.Context(gecc.SECP256K1, local_rank)
+    l = gecc.lib()
+    stream = torch.cuda.Stream()          # all timed work and its events share this stream
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    vp = lambda t: C.c_void_p(t.data_ptr())
+
+    # ---- synthetic records, generated on the GPU by our own keygen/sign (not timed)
+    u8 = lambda m: torch.empty(m, dtype=torch.uint8, device="cuda")
+    h_sec, h_pub = np.empty(32 * n, np.uint8), np.empty(65 * n, np.uint8)
+    rc = l.gecc_keygen(ctx.h, C.c_uint64(1), C.c_uint64(lane_base), C.c_size_t(n),
+                       C.c_void_p(h_sec.ctypes.data), C.c_void_p(h_pub.ctypes.data))
+    assert rc == 0, ctx.l.gecc_last_error(ctx.h)
+    h_dig = np.frombuffer(np.random.RandomState(1234 + rank).bytes(32 * n), np.uint8).copy()
+    d_dig, d_sec, d_pub = (torch.from_numpy(a).cuda() for a in (h_dig, h_sec, h_pub))
+    d_sig, d_res = u8(64 * n), u8(n)
+    d_st = torch.empty(n, dtype=torch.int32, device="cuda")
+    rc = l.gecc_sign_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_sec), C.c_uint64(7),
+                         C.c_uint64(lane_base), vp(d_sig), vp(d_st))
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert int(d_st.abs().sum()) == 0
+    h_sig = d_sig.cpu().numpy()
+
+    # ---- equivalence gate before timing (bench.cpp:253-256): spot lanes vs the oracle
+    from oracle import coracle as O
+    rs = np.random.RandomState(99)
+    idx = [int(i) for i in rs.choice(n, 24, replace=False)]
+    pick = lambda a, w: b"".join(a[w * i:w * i + w].tobytes() for i in idx)
+    for i in idx[:8]:
+        want = O.ecdsa_sign(SECP, h_dig[32 * i:32 * i + 32].tobytes(), h_sec[32 * i:32 * i + 32].tobytes(),
+                            7, lane_base=lane_base + i)[1]
+        assert want == h_sig[64 * i:64 * i + 64].tobytes(), "sign parity gate failed"
+    bad = bytearray(pick(h_sig, 64))
+    bad[64 * 3 + 9] ^= 4
+    want = O.ecdsa_verify(SECP, pick(h_dig, 32), pick(h_pub, 65), bytes(bad))[1]
+    got = ctx.verify(pick(h_dig, 32), pick(h_pub, 65), bytes(bad))[1]
+    assert want == got and sum(want) == 23, "verify parity gate failed"
+
+    if wl == "padd":
+        k1 = torch.from_numpy(rs.randint(0, 2**32, size=(8, n), dtype=np.uint64).astype(np.uint32)).cuda()
+        k2 = torch.from_numpy(rs.randint(0, 2**32, size=(8, n), dtype=np.uint64).astype(np.uint32)).cuda()
+        col = lambda: torch.empty((8, n), dtype=torch.int32, device="cuda")
+        P = (col(), col(), u8(n)); T = (col(), col(), u8(n)); S = (col(), col(), u8(n))
+        l.gecc_batch_fpmul_dev(ctx.h, C.c_size_t(n), vp(k1), vp(P[0]), vp(P[1]), vp(P[2]))
+        l.gecc_batch_fpmul_dev(ctx.h, C.c_size_t(n), vp(k2), vp(T[0]), vp(T[1]), vp(T[2]))
+        torch.cuda.synchronize()
+
+    def step_dev():
+        if wl == "verify":
+            return l.gecc_verify_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_pub), vp(d_sig), vp(d_res))
+        if wl == "sign":
+            return l.gecc_sign_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_sec), C.c_uint64(7),
+                                   C.c_uint64(lane_base), vp(d_sig), vp(d_st))
+        return l.gecc_batch_padd_dev(ctx.h, C.c_size_t(n), vp(P[0]), vp(P[1]), vp(P[2]), vp(T[0]),
+                                     vp(T[1]), vp(T[2]), vp(S[0]), vp(S[1]), vp(S[2]))
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- integer-pipe peak, measured live (rank 0's device is representative)
+    peak = ctx.microbench(1, 3000)  # dependent IMAD.WIDE chain, 8 warps/scheduler
+    peak_mad_per_s = peak["total_ops"] / peak["seconds"]
+
+    # ---- value: device-resident
+    for _ in range(args.warmup):
+        assert step_dev() == 0
+    barrier()
+    sampler = ClockSampler(local_rank)
+    launches0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        assert step_dev() == 0
+    ev1.record(stream)
+    barrier()
+    launches = ctx.launches - launches0
+    dev_s = max_over_ranks(ev0.elapsed_time(ev1) * 1e-3)
+    clocks = sampler.stop()
+    if wl == "verify":
+        assert int(d_res.sum()) == n, "timed verify produced rejects"
+    value = world * n * args.steps / dev_s
+
+    # ---- e2e: reference-facing C ABI, pinned host buffers, copies inside the timed region
+    pin = lambda a: torch.from_numpy(a).pin_memory()
+    e2e = None
+    if wl in ("verify", "sign"):
+        p_dig, p_pub, p_sig, p_sec = pin(h_dig), pin(h_pub), pin(h_sig.copy()), pin(h_sec)
+        p_res = torch.empty(n, dtype=torch.uint8).pin_memory()
+        p_out = torch.empty(64 * n, dtype=torch.uint8).pin_memory()
+        p_st = torch.empty(n, dtype=torch.int32).pin_memory()
+        if wl == "verify":
+            call = lambda: l.sm2b_verify(ctx.h, C.c_size_t(n), vp(p_dig), vp(p_pub), vp(p_sig), vp(p_res))
+            h2d, d2h = 161 * n, n
+        else:
+            call = lambda: l.gecc_sign(ctx.h, C.c_size_t(n), vp(p_dig), vp(p_sec), C.c_uint64(7),
+                                       C.c_uint64(lane_base), vp(p_out), vp(p_st))
+            h2d, d2h = 64 * n, 68 * n
+        for _ in range(max(1, args.warmup // 2)):
+            assert call() == 0
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            assert call() == 0  # synchronous: returns after the D2H copy completed
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        if wl == "verify":
+            assert int(p_res.sum()) == n
+        e2e = {"value": world * n * args.steps / e2e_s, "unit": UNIT[wl],
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": e2e_s / args.steps * 1e3,
+               "api": "sm2b_verify" if wl == "verify" else "gecc_sign", "host_buffers": "pinned"}
+
+    # ---- roofline of the dominant kernel (the only kernel in the step)
+    per_launch_s = dev_s / args.steps
+    if wl == "verify":
+        m_p, m_n = verify_work_per_lane()
+    elif wl == "sign":
+        m_p, m_n = sign_work_per_lane()
+    else:
+        m_p, m_n = 6 + 334 / 16, 0
+    mads = n * (m_p * MAD_SECP_P + m_n * MAD_GENERIC)
+    achieved = mads / per_launch_s
+    io_bytes = {"verify": 162, "sign": 132, "padd": 194}[wl] * n
+    roofline = {
+        "bound": "imad", "kernel": {"verify": "k_verify", "sign": "k_sign", "padd": "k_batch_padd"}[wl],
+        "achieved": achieved / 1e12, "peak": peak_mad_per_s / 1e12, "unit": "T IMAD.WIDE-slot/s",
+        "frac": achieved / peak_mad_per_s,
+        "peak_source": "measured live: gecc_microbench(dependent IMAD.WIDE.U32), "
+                       f"{peak['ops_per_clk_per_sm']:.1f} per clk per SM",
+        "work_per_lane": {"fp_mul": m_p, "fn_mul": m_n, "mad_per_fp_mul": MAD_SECP_P,
+                          "mad_per_fn_mul": MAD_GENERIC},
+        "modmul_per_s": n * (m_p + m_n) / per_launch_s,
+        "hbm": {"algorithmic_bytes_per_launch": io_bytes, "achieved_gbs": io_bytes / per_launch_s / 1e9,
+                "peak_gbs": _measured_peaks().get("hbm_gbs"), "note": "records only; not the bound"},
+        "traffic": None,
+    }
+
+    # ---- CPU baseline on this box's host cores (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and wl in ("verify", "sign"):
+        log2 = args.cpu_sample_log2 or (16 if wl == "verify" else 17)
+        m = min(n, 1 << log2)
+        if wl == "verify":
+            kind, cores, fn = cpu_verify_runner()
+            if kind == "port":
+                m = min(m, 1 << 12)
+            t0 = time.perf_counter()
+            out = fn(h_dig[:32 * m].tobytes(), h_pub[:65 * m].tobytes(), h_sig[:64 * m].tobytes())
+            dt = time.perf_counter() - t0
+            assert out == b"\x01" * m, "CPU reference rejected GPU-made signatures"
+        else:
+            kind, cores, fn = cpu_sign_runner()
+            if kind == "port":
+                m = min(m, 1 << 13)
+            t0 = time.perf_counter()
+            out = fn(h_dig[:32 * m].tobytes(), h_sec[:32 * m].tobytes(), 7)
+            dt = time.perf_counter() - t0
+            assert out == h_sig[:64 * m].tobytes(), "CPU reference signatures differ from the GPU's"
+        cpu = {"value": m / dt, "unit": UNIT[wl], "cores": cores, "kind": kind,
+               "sample": f"first {m} lanes of the timed batch, one call, outputs compared with the GPU's",
+               "seconds": dt}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC[wl], "value": value, "unit": UNIT[wl], "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_launch_s * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "u32 limbs (256-bit modular integer)", "data": "synthetic",
+            "config": {"workload": f"secp256k1 ECDSA {wl}, batch 2^{args.log2n} per GPU"
+                       if wl != "padd" else f"secp256k1 batched affine point addition, 2^{args.log2n} pairs per GPU",
+                       "curve": "secp256k1", "lanes_per_gpu": n, "sharding": f"lane ranges x{world}, no collective",
+                       "l2": "inputs larger than L2 (records 161 B/lane x 2^20 = 169 MB > 126 MB)"
+                       if wl == "verify" and args.log2n >= 20 else "no L2 flush; kernel is IMAD-bound, records read once"},
+            "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+if __name__ == "__main__":
+    main()

@@ -200,7 +200,8 @@ sm2b_status gecc_msm_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const
 /* Integer-pipe issue-rate microbenchmark (roofline denominator).
  * which: 0 IMAD.WIDE.U32 independent, 1 IMAD.WIDE dependent chain, 2 IMAD (32-bit),
  *        3 IMAD.HI, 4 IADD3, 5 IADD3.X carry chain, 6 IMAD.WIDE + IADD3 1:1 mix,
- *        7 secp256k1 fe_mul, 8 generic fe_mul, 9 secp256k1 fe_add+fe_sub.
+ *        7 secp256k1 fe_mul (inlined), 8 generic fe_mul, 9 secp256k1 fe_add+fe_sub,
+ *        10 secp256k1 fe_mul (by-value call), 11 fe_sqr (inlined), 12 fe_sqr (call).
  * Fills ops_per_clk_per_sm (thread-level operations per SM clock per SM, from
  * clock64 spans) and seconds (CUDA-event time); iters = inner loop trip count. */
 sm2b_status gecc_microbench(sm2b_ctx* ctx, int which, int iters, double* ops_per_clk_per_sm,

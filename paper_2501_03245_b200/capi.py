@@ -125,7 +125,13 @@ class Context:
         return int(self.l.gecc_kernel_launches(self.h))
 
     def set_stream(self, stream_ptr: int | None):
-        self.l.gecc_ctx_set_stream(self.h, C.c_void_p(stream_ptr or 0))
+        """None -> the context's own stream; 0 -> the CUDA legacy default stream
+        (cudaStreamLegacy), anything else is taken as a cudaStream_t."""
+        if stream_ptr is None:
+            ptr = 0
+        else:
+            ptr = 1 if int(stream_ptr) == 0 else int(stream_ptr)  # 0x1 == cudaStreamLegacy
+        self.l.gecc_ctx_set_stream(self.h, C.c_void_p(ptr))
 
     def ledger(self):
         arr = (C.c_uint64 * 4)()

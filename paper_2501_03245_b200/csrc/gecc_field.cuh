@@ -17,6 +17,8 @@
 // unrolling; FieldRT carries runtime constants for arbitrary odd 256-bit moduli
 // (the reference's FieldParams::make(q), field.cpp:159-179).
 #pragma once
+#include <type_traits>
+
 #include "gecc_consts.cuh"
 
 namespace gecc {
@@ -196,6 +198,63 @@ GECC_HD void mul_low8(uint32_t* r, const uint32_t* a, const uint32_t* b) {
     }
 }
 
+// Full 16-limb square: the 28 off-diagonal products once (same even/odd carry-chain
+// layout as mul_wide8), doubled by a one-bit funnel shift, plus the 8 diagonal
+// squares in one chain: 36 wide multiply-adds instead of 64.
+GECC_HD void sqr_wide8(uint32_t* t, const uint32_t* a) {
+    constexpr int N = 8;
+    uint32_t e[2 * N], o[2 * N];
+#pragma unroll
+    for (int k = 0; k < 2 * N; ++k) e[k] = o[k] = 0;
+#pragma unroll
+    for (int i = 0; i < N - 1; ++i) {
+        const uint32_t ai = a[i];
+        // s = i + j even: j = i+2, i+4, ...  -> e[s], e[s+1]
+        if (i + 2 < N) {
+            e[2 * i + 2] = mad_lo_cc(a[i + 2], ai, e[2 * i + 2]);
+            e[2 * i + 3] = madc_hi_cc(a[i + 2], ai, e[2 * i + 3]);
+#pragma unroll
+            for (int j = i + 4; j < N; j += 2) {
+                e[i + j] = madc_lo_cc(a[j], ai, e[i + j]);
+                e[i + j + 1] = madc_hi_cc(a[j], ai, e[i + j + 1]);
+            }
+            // chain ended at index i + jl + 1 with jl the last j used; fold the carry
+            const int jl = ((N - 1 - i) % 2 == 0) ? N - 1 : N - 2;  // last j with i + j even
+            if (i + jl + 2 < 2 * N) e[i + jl + 2] = addc(e[i + jl + 2], 0);
+        }
+        // s = i + j odd: j = i+1, i+3, ...  -> o[s-1], o[s]
+        o[2 * i] = mad_lo_cc(a[i + 1], ai, o[2 * i]);
+        o[2 * i + 1] = madc_hi_cc(a[i + 1], ai, o[2 * i + 1]);
+#pragma unroll
+        for (int j = i + 3; j < N; j += 2) {
+            o[i + j - 1] = madc_lo_cc(a[j], ai, o[i + j - 1]);
+            o[i + j] = madc_hi_cc(a[j], ai, o[i + j]);
+        }
+        {
+            const int jl = ((N - 1 - i) % 2 == 1) ? N - 1 : N - 2;  // last j with i + j odd
+            if (i + jl + 1 < 2 * N) o[i + jl + 1] = addc(o[i + jl + 1], 0);
+        }
+    }
+    // off-diagonal sum S = e + (o << 32)
+    uint32_t sd[2 * N];
+    sd[0] = e[0];
+    sd[1] = add_cc(e[1], o[0]);
+#pragma unroll
+    for (int k = 2; k < 2 * N; ++k) sd[k] = addc_cc(e[k], o[k - 1]);
+    // 2S, then + diagonal squares
+    uint32_t dbl[2 * N];
+    dbl[0] = sd[0] << 1;
+#pragma unroll
+    for (int k = 1; k < 2 * N; ++k) dbl[k] = (sd[k] << 1) | (sd[k - 1] >> 31);
+    t[0] = mad_lo_cc(a[0], a[0], dbl[0]);
+    t[1] = madc_hi_cc(a[0], a[0], dbl[1]);
+#pragma unroll
+    for (int i = 1; i < N; ++i) {
+        t[2 * i] = madc_lo_cc(a[i], a[i], dbl[2 * i]);
+        t[2 * i + 1] = madc_hi_cc(a[i], a[i], dbl[2 * i + 1]);
+    }
+}
+
 // ---------------------------------------------------------------- reductions
 // r = (top:r) - q if (top:r) >= q
 template <class F>
@@ -283,15 +342,51 @@ GECC_HD fe redc(const F& f, const uint32_t* t) {
 
 // ---------------------------------------------------------------- mul / sqr
 template <class F>
-GECC_HD fe fe_mul(const F& f, const fe& a, const fe& b) {
+GECC_HD fe fe_mul_inl(const F& f, const fe& a, const fe& b) {
     uint32_t t[16];
     mul_wide8(t, a.w, b.w);
     return redc(f, t);
 }
 template <class F>
-GECC_HD fe fe_sqr(const F& f, const fe& a) {
-    return fe_mul(f, a, a);
+GECC_HD fe fe_sqr_inl(const F& f, const fe& a) {
+    uint32_t t[16];
+    sqr_wide8(t, a.w);
+    return redc(f, t);
 }
+// On the device the two products are real functions with by-value arguments: the
+// ABI passes the 16 + 8 limbs in registers (no stack traffic), and the hot code
+// of a whole ECDSA kernel shrinks to these two bodies plus glue, which is what
+// keeps it inside the instruction caches (round-1 ncu: with everything inlined the
+// top stall of k_verify was no_instruction).  Runtime fields stay inline.
+#if defined(__CUDA_ARCH__) && !defined(GECC_INLINE_FIELD)
+template <class F>
+__device__ __noinline__ fe fe_mul_call(fe a, fe b) {
+    return fe_mul_inl(F{}, a, b);
+}
+template <class F>
+__device__ __noinline__ fe fe_sqr_call(fe a) {
+    return fe_sqr_inl(F{}, a);
+}
+template <class F>
+GECC_HD fe fe_mul(const F& f, const fe& a, const fe& b) {
+    if constexpr (std::is_empty<F>::value) return fe_mul_call<F>(a, b);
+    else return fe_mul_inl(f, a, b);
+}
+template <class F>
+GECC_HD fe fe_sqr(const F& f, const fe& a) {
+    if constexpr (std::is_empty<F>::value) return fe_sqr_call<F>(a);
+    else return fe_sqr_inl(f, a);
+}
+#else
+template <class F>
+GECC_HD fe fe_mul(const F& f, const fe& a, const fe& b) {
+    return fe_mul_inl(f, a, b);
+}
+template <class F>
+GECC_HD fe fe_sqr(const F& f, const fe& a) {
+    return fe_sqr_inl(f, a);
+}
+#endif
 template <class F>
 GECC_HD fe fe_to_mont(const F& f, const fe& a) {  // a * R
     fe r2;

@@ -11,7 +11,7 @@ constexpr int VERIFY_THREADS = 128;  // x 512 B of lane table = 64 KiB shared me
 constexpr int SIGN_THREADS = 128;
 
 template <class C>
-__global__ void __launch_bounds__(VERIFY_THREADS)
+__global__ void __launch_bounds__(VERIFY_THREADS, 3)
 k_verify(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ pub,
          const uint8_t* __restrict__ sig, const uint32_t* __restrict__ gtab,
          uint8_t* __restrict__ res) {
@@ -62,7 +62,7 @@ k_keygen(size_t n, uint64_t seed, uint64_t lane_base, const uint32_t* __restrict
 // capi.cpp:230-261 + protocol.cpp:224-263.  status: 0 ok, 3 invalid peer,
 // 4 degenerate; a secret >= n flags the whole call malformed.
 template <class C>
-__global__ void __launch_bounds__(VERIFY_THREADS)
+__global__ void __launch_bounds__(VERIFY_THREADS, 3)
 k_ecdh(size_t n, const uint8_t* __restrict__ sec, const uint8_t* __restrict__ peers,
        uint8_t* __restrict__ shared, int32_t* __restrict__ status, uint32_t* __restrict__ flags) {
     extern __shared__ uint32_t lane_tables[];
@@ -121,7 +121,7 @@ k_fpmul(size_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ g
 }
 
 template <class C>
-__global__ void __launch_bounds__(VERIFY_THREADS)
+__global__ void __launch_bounds__(VERIFY_THREADS, 3)
 k_upmul(size_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ px,
         const uint32_t* __restrict__ py, const uint8_t* __restrict__ pinf,
         uint32_t* __restrict__ ox, uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf) {

@@ -102,12 +102,21 @@ __global__ void __launch_bounds__(1024) k_rate_fe(int iters, uint32_t seed, uint
     long long t0 = clock64();
 #pragma unroll 1
     for (int it = 0; it < iters; ++it) {
-        if (WHICH == 0) {
-            x = fe_mul(f, x, y);
-            y = fe_mul(f, y, x);
-        } else {
+        if (WHICH == 0) {         // inlined product + reduction
+            x = fe_mul_inl(f, x, y);
+            y = fe_mul_inl(f, y, x);
+        } else if (WHICH == 1) {
             x = fe_add(f, x, y);
             y = fe_sub(f, y, x);
+        } else if (WHICH == 2) {  // the by-value function the kernels call
+            x = fe_mul(f, x, y);
+            y = fe_mul(f, y, x);
+        } else if (WHICH == 3) {
+            x = fe_sqr_inl(f, x);
+            y = fe_sqr_inl(f, y);
+        } else {
+            x = fe_sqr(f, x);
+            y = fe_sqr(f, y);
         }
     }
     long long t1 = clock64();
@@ -146,6 +155,12 @@ cudaError_t run_microbench(int which, int iters, int sm_count, double* ops_per_c
             case 8: k_rate_fe<SecpN, 0><<<sm_count, 1024, 0, s>>>(iters, 17, d_cycles, d_sink);
                 ops_per_thread_iter = 2.0; break;
             case 9: k_rate_fe<SecpP, 1><<<sm_count, 1024, 0, s>>>(iters, 17, d_cycles, d_sink);
+                ops_per_thread_iter = 2.0; break;
+            case 10: k_rate_fe<SecpP, 2><<<sm_count, 1024, 0, s>>>(iters, 17, d_cycles, d_sink);
+                ops_per_thread_iter = 2.0; break;
+            case 11: k_rate_fe<SecpP, 3><<<sm_count, 1024, 0, s>>>(iters, 17, d_cycles, d_sink);
+                ops_per_thread_iter = 2.0; break;
+            case 12: k_rate_fe<SecpP, 4><<<sm_count, 1024, 0, s>>>(iters, 17, d_cycles, d_sink);
                 ops_per_thread_iter = 2.0; break;
             default: cudaFree(d_cycles); cudaFree(d_sink); return cudaErrorInvalidValue;
         }

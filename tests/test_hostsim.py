@@ -35,8 +35,9 @@ def test_hostsim_field_golden(key):
 def test_hostsim_field_random(cid, which):
     q = O.field_params(cid, which)["q"]
     rng = random.Random(50 + 2 * cid + which)
-    a = O.ints_to_cols([rng.randrange(q) for _ in range(4000)])
-    b = O.ints_to_cols([rng.randrange(q) for _ in range(4000)])
+    edge = [0, 1, 2, q - 1, q - 2, (1 << 255) % q, (1 << 224) - 1, q >> 1, 0xFFFFFFFF, ((q - 1) ^ 0xFFFFFFFF) % q]
+    a = O.ints_to_cols(edge + [rng.randrange(q) for _ in range(4000)])
+    b = O.ints_to_cols(edge[::-1] + [rng.randrange(q) for _ in range(4000)])
     for op in ("mont_mul", "mod_add", "mod_sub", "to_mont", "from_mont"):
         assert (H.field_op(cid, which, op, a, b) == O.field_op(cid, which, op, a, b)).all(), op
     assert (H.field_op(cid, which, "sqr", a) == O.field_op(cid, which, "mont_mul", a, a)).all()

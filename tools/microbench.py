@@ -9,7 +9,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2501_03245_b200 as gecc  # noqa: E402
 
 NAMES = ["imad_wide_indep", "imad_wide_dep", "imad32", "imad_hi", "iadd3", "iadd3x_chain",
-         "imad_wide+iadd_mix", "fe_mul_secp_p", "fe_mul_generic", "fe_addsub_secp_p"]
+         "imad_wide+iadd_mix", "fe_mul_secp_p", "fe_mul_generic", "fe_addsub_secp_p",
+         "fe_mul_secp_p_call", "fe_sqr_secp_p", "fe_sqr_secp_p_call"]
 
 
 def main():
