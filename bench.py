@@ -171,23 +171,31 @@ def run_reference_arm(args, rank):
 
 
 # ----------------------------------------------------------------------------- GPU arm
-# Executed field multiplications per lane of OUR kernels (analytic, from the code in
-# gecc_ecdsa.cuh) and FMA-pipe issue slots per
-# multiplication in IMAD.WIDE units (IMAD.WIDE / IMAD.HI = 1, 32-bit IMAD = 1/2; measured
-# issue rates 32 and 64 per clk per SM).
-MAD_SECP_P = 64 + 8 + 8 * 0.5          # product + 8 IMAD.HI + 8 IMAD of the word-serial REDC
-MAD_GENERIC = 64 + (28 + 36 * 0.5) + 64  # product + low product + m*q product
+# Executed field products per lane of OUR kernels: counted by running the product's own
+# lane code on the host with instrumented multiply / square / safegcd
+# (tools/count_ops.py -> tools/op_counts.json; method in DESIGN.md "work per lane").
+# Multiply-pipe issue slots per product, in IMAD.WIDE units (IMAD.WIDE and IMAD.HI = 1,
+# 32-bit IMAD = 1/2: measured issue rates are 32 and 64 per clk per SM):
+SLOTS = {
+    "mul_special": 64 + 8 + 8 * 0.5,            # product + word-serial secp256k1 REDC
+    "sqr_special": 36 + 8 + 8 * 0.5,
+    "mul_generic": 64 + (28 + 36 * 0.5) + 64,   # product + low product + m*q product
+    "sqr_generic": 36 + (28 + 36 * 0.5) + 64,
+    "safegcd_special": 20 * (36 + 54),          # 20 rounds of two 2x2 matrix updates
+    "safegcd_generic": 20 * (36 + 54),
+}
 
 
-def verify_work_per_lane():
-    fp = dict(decode=5, gmul=17 * 11, table=4 * 7 + 3 * 11 + 6 + 334 + 6 * 2 + 7 * 4,
-              ladder=256 * 7 + 64 * (15 / 16) * 11, final=16 + 3)
-    fn = dict(inv=334 + 1, u=2)
-    return sum(fp.values()), sum(fn.values())
-
-
-def sign_work_per_lane():
-    return 17 * 11 + 334 + 3, 2 + 334 + 1 + 4 + 1
+def work_per_lane(workload):
+    with open(os.path.join(ROOT, "tools", "op_counts.json")) as f:
+        counts = json.load(f)["secp256k1"]
+    if workload == "padd":   # compress 1 + scatter 2 + chord 3 (one a square) + inversion share
+        c = {"mul_special": 5 + 2 / 16, "sqr_special": 1, "safegcd_special": 1 / 16}
+    else:
+        c = counts[workload]
+    slots = sum(SLOTS[k] * v for k, v in c.items())
+    products = sum(v for k, v in c.items() if not k.startswith("safegcd"))
+    return c, slots, products
 
 
 def main():
@@ -338,13 +346,8 @@ def main():
 
     # ---- roofline of the dominant kernel (the only kernel in the step)
     per_launch_s = dev_s / args.steps
-    if wl == "verify":
-        m_p, m_n = verify_work_per_lane()
-    elif wl == "sign":
-        m_p, m_n = sign_work_per_lane()
-    else:
-        m_p, m_n = 6 + 334 / 16, 0
-    mads = n * (m_p * MAD_SECP_P + m_n * MAD_GENERIC)
+    counts, slots_per_lane, products_per_lane = work_per_lane(wl)
+    mads = n * slots_per_lane
     achieved = mads / per_launch_s
     io_bytes = {"verify": 162, "sign": 132, "padd": 194}[wl] * n
     roofline = {
@@ -353,9 +356,9 @@ def main():
         "frac": achieved / peak_mad_per_s,
         "peak_source": "measured live: gecc_microbench(dependent IMAD.WIDE.U32), "
                        f"{peak['ops_per_clk_per_sm']:.1f} per clk per SM",
-        "work_per_lane": {"fp_mul": m_p, "fn_mul": m_n, "mad_per_fp_mul": MAD_SECP_P,
-                          "mad_per_fn_mul": MAD_GENERIC},
-        "modmul_per_s": n * (m_p + m_n) / per_launch_s,
+        "work_per_lane": {"executed": counts, "imad_wide_slots": slots_per_lane,
+                          "slots_per_op": SLOTS, "source": "tools/op_counts.json"},
+        "modmul_per_s": n * products_per_lane / per_launch_s,
         "hbm": {"algorithmic_bytes_per_launch": io_bytes, "achieved_gbs": io_bytes / per_launch_s / 1e9,
                 "peak_gbs": _measured_peaks().get("hbm_gbs"), "note": "records only; not the bound"},
         "traffic": None,

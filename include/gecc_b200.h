@@ -118,7 +118,8 @@ typedef enum gecc_field_opcode {
     GECC_OP_MOD_SUB = 2,  /* field.cpp:221-227 */
     GECC_OP_TO_MONT = 3,  /* field.cpp:194-198 */
     GECC_OP_FROM_MONT = 4,/* field.cpp:200-203 */
-    GECC_OP_MOD_INV = 5   /* field.cpp:239-246, zero maps to zero */
+    GECC_OP_MOD_INV = 5,  /* field.cpp:239-246's value via safegcd, zero maps to zero */
+    GECC_OP_MOD_INV_FERMAT = 6 /* same value by a^(q-2), kept as a cross-check */
 } gecc_field_opcode;
 
 /* Context for `curve` on CUDA device `device` (< 0: the current device). */

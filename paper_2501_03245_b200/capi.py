@@ -21,7 +21,7 @@ FIELD_P, FIELD_N = 0, 1
 STATUS = {0: "ok", 1: "invalid argument", 2: "malformed input", 3: "invalid peer point",
           4: "degenerate result", 5: "nonce retries exhausted", 6: "cost model has no crossover",
           7: "internal error"}
-FIELD_OPS = dict(mont_mul=0, mod_add=1, mod_sub=2, to_mont=3, from_mont=4, mod_inv=5)
+FIELD_OPS = dict(mont_mul=0, mod_add=1, mod_sub=2, to_mont=3, from_mont=4, mod_inv=5, mod_inv_fermat=6)
 
 
 class GeccError(RuntimeError):

@@ -217,7 +217,7 @@ sm2b_status gecc_ctx_set_stream(sm2b_ctx* ctx, void* stream) {
 // ------------------------------------------------------------------ field ops
 sm2b_status gecc_field_op_dev(sm2b_ctx* ctx, gecc_field field, gecc_field_opcode op, size_t n,
                               const uint32_t* a, const uint32_t* b, uint32_t* out) {
-    if (!ctx || (n > 0 && (!a || !out)) || (unsigned)op > 5 || (unsigned)field > 1)
+    if (!ctx || (n > 0 && (!a || !out)) || (unsigned)op > 6 || (unsigned)field > 1)
         return SM2B_ERROR_INVALID_ARGUMENT;
     if (n > 0 && op <= GECC_OP_MOD_SUB && !b) return SM2B_ERROR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -229,7 +229,7 @@ sm2b_status gecc_field_op_dev(sm2b_ctx* ctx, gecc_field field, gecc_field_opcode
 
 sm2b_status gecc_field_op(sm2b_ctx* ctx, gecc_field field, gecc_field_opcode op, size_t n,
                           const uint32_t* a, const uint32_t* b, uint32_t* out) {
-    if (!ctx || (n > 0 && (!a || !out)) || (unsigned)op > 5 || (unsigned)field > 1)
+    if (!ctx || (n > 0 && (!a || !out)) || (unsigned)op > 6 || (unsigned)field > 1)
         return SM2B_ERROR_INVALID_ARGUMENT;
     if (n > 0 && op <= GECC_OP_MOD_SUB && !b) return SM2B_ERROR_INVALID_ARGUMENT;
     if (n == 0) return SM2B_OK;

@@ -17,6 +17,7 @@
 #pragma once
 #include "gecc_curve.cuh"
 #include "gecc_dev.cuh"
+#include "gecc_modinv.cuh"
 
 namespace gecc {
 
@@ -199,7 +200,7 @@ GECC_HD void build_lane_table(const aff& p, const LaneTable& tab) {
     pre[1] = m[1].Z;
 #pragma unroll
     for (int i = 2; i < 8; ++i) pre[i] = fe_mul(f, pre[i - 1], m[i].Z);
-    fe inv = fe_inv_fermat(f, pre[7]);
+    fe inv = fe_inv(f, pre[7]);
     tab.store(0, p);
 #pragma unroll
     for (int i = 7; i >= 1; --i) {
@@ -209,31 +210,161 @@ GECC_HD void build_lane_table(const aff& p, const LaneTable& tab) {
     }
 }
 
+// ---- GLV split for curves with the endomorphism phi(x, y) = (beta x, y) = lambda (x, y)
+// (secp256k1; Gallant-Lambert-Vanstone 2001).  k = k1 + k2 lambda (mod n) with
+// |k1|, |k2| < 2^129, by rounding k onto the lattice basis (a1, b1), (a2, b2):
+//   c1 = round(k g1 / 2^384), c2 = round(k g2 / 2^384)
+//   k1 = k - c1 a1 - c2 a2,   k2 = c1 (-b1) - c2 b2        (exact integers)
+// The ladder then needs 132 doublings instead of 256.
+struct GlvSplit {
+    fe m1, m2;        // magnitudes (upper limbs zero)
+    bool neg1, neg2;  // signs
+};
+
+// out[na+nb] = a[na] * b[nb], small schoolbook on 64-bit accumulators
+template <int NA, int NB>
+GECC_HD void mul_small(uint32_t* out, const uint32_t* a, const uint32_t* b) {
+#pragma unroll
+    for (int i = 0; i < NA + NB; ++i) out[i] = 0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+        uint64_t carry = 0;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            uint64_t t = (uint64_t)a[i] * b[j] + out[i + j] + carry;
+            out[i + j] = (uint32_t)t;
+            carry = t >> 32;
+        }
+        out[i + NB] = (uint32_t)carry;
+    }
+}
+// r[N] = a[N] - b[N]; returns true when the result is negative, in which case r = b - a
+template <int N>
+GECC_HD bool sub_abs(uint32_t* r, const uint32_t* a, const uint32_t* b) {
+    r[0] = sub_cc(a[0], b[0]);
+#pragma unroll
+    for (int i = 1; i < N; ++i) r[i] = subc_cc(a[i], b[i]);
+    const bool neg = subc(0, 0) != 0;
+    if (neg) {
+        r[0] = sub_cc(b[0], a[0]);
+#pragma unroll
+        for (int i = 1; i < N; ++i) r[i] = subc_cc(b[i], a[i]);
+    }
+    return neg;
+}
+
+template <class C>
+GECC_HD GlvSplit glv_split(const fe& k) {
+    uint32_t g[8], t[16], c1[5], c2[5];
+    // c = (k g + 2^383) >> 384
+#pragma unroll
+    for (int i = 0; i < 8; ++i) g[i] = C::glv_g1(i);
+    mul_wide8(t, k.w, g);
+    c1[0] = add_cc(t[12], t[11] >> 31);
+    c1[1] = addc_cc(t[13], 0);
+    c1[2] = addc_cc(t[14], 0);
+    c1[3] = addc_cc(t[15], 0);
+    c1[4] = addc(0, 0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) g[i] = C::glv_g2(i);
+    mul_wide8(t, k.w, g);
+    c2[0] = add_cc(t[12], t[11] >> 31);
+    c2[1] = addc_cc(t[13], 0);
+    c2[2] = addc_cc(t[14], 0);
+    c2[3] = addc_cc(t[15], 0);
+    c2[4] = addc(0, 0);
+    uint32_t a1[4], a2[5], mb1[4], b2[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        a1[i] = C::glv_a1(i);
+        mb1[i] = C::glv_minus_b1(i);
+        b2[i] = C::glv_b2(i);
+    }
+#pragma unroll
+    for (int i = 0; i < 5; ++i) a2[i] = C::glv_a2(i);
+    // k1 = k - (c1 a1 + c2 a2), 10-limb arithmetic
+    uint32_t p1[10], p2[10], s[10], kk[10], d[10];
+    mul_small<5, 4>(p1, c1, a1);
+    p1[9] = 0;
+    mul_small<5, 5>(p2, c2, a2);
+    s[0] = add_cc(p1[0], p2[0]);
+#pragma unroll
+    for (int i = 1; i < 10; ++i) s[i] = addc_cc(p1[i], p2[i]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) kk[i] = k.w[i];
+    kk[8] = kk[9] = 0;
+    GlvSplit r;
+    r.neg1 = sub_abs<10>(d, kk, s);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.m1.w[i] = d[i];
+    // k2 = c1 (-b1) - c2 b2, 9-limb arithmetic
+    uint32_t u1[9], u2[9], e[9];
+    mul_small<5, 4>(u1, c1, mb1);
+    mul_small<5, 4>(u2, c2, b2);
+    r.neg2 = sub_abs<9>(e, u1, u2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.m2.w[i] = e[i];
+    return r;
+}
+
 // k * P, P finite and on the curve, any 256-bit k (k mod n is what is computed).
 template <class C>
 GECC_HD jac var_base_mul(const fe& k_raw, const LaneTable& tab) {
     const typename C::Fp f{};
     fe k = scalar_reduce_once<typename C::Fn>(k_raw);
-    Recoded<4> rc = recode_signed<4>(k);
     jac acc = jac_infinity<C>();
-    if (rc.carry) {
-        aff t = tab.load(0);
-        acc.X = t.x; acc.Y = t.y; acc.Z = fe_one(f);
-    }
+    if constexpr (C::has_glv) {
+        const GlvSplit sp = glv_split<C>(k);
+        const Recoded<4> r1 = recode_signed<4>(sp.m1), r2 = recode_signed<4>(sp.m2);
+        fe beta;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) beta.w[i] = C::beta(i);
+        // magnitudes are below 2^129: windows 0..32 plus the recoding carry in window 33
 #pragma unroll 1
-    for (int j = 63; j >= 0; --j) {
-        acc = jac_dbl<C>(acc);
-        acc = jac_dbl<C>(acc);
-        acc = jac_dbl<C>(acc);
-        acc = jac_dbl<C>(acc);
-        int d = recoded_digit<4>(rc, j);
-        if (d != 0) {
-            aff t = tab.load((d < 0 ? -d : d) - 1);
-            if (d < 0) t.y = fe_neg(f, t.y);
-            acc = jac_madd<C>(acc, t);
+        for (int j = 33; j >= 0; --j) {
+            if (j != 33) {
+                acc = jac_dbl<C>(acc);
+                acc = jac_dbl<C>(acc);
+                acc = jac_dbl<C>(acc);
+                acc = jac_dbl<C>(acc);
+            }
+            int d1 = recoded_digit<4>(r1, j), d2 = recoded_digit<4>(r2, j);
+            if (sp.neg1) d1 = -d1;
+            if (sp.neg2) d2 = -d2;
+            if (d1 != 0) {
+                aff t = tab.load((d1 < 0 ? -d1 : d1) - 1);
+                if (d1 < 0) t.y = fe_neg(f, t.y);
+                acc = jac_madd<C>(acc, t);
+            }
+            if (d2 != 0) {  // phi(d P) = (beta x, y)
+                aff t = tab.load((d2 < 0 ? -d2 : d2) - 1);
+                t.x = fe_mul(f, t.x, beta);
+                if (d2 < 0) t.y = fe_neg(f, t.y);
+                acc = jac_madd<C>(acc, t);
+            }
         }
+        return acc;
+    } else {
+        Recoded<4> rc = recode_signed<4>(k);
+        if (rc.carry) {
+            aff t = tab.load(0);
+            acc.X = t.x; acc.Y = t.y; acc.Z = fe_one(f);
+        }
+#pragma unroll 1
+        for (int j = 63; j >= 0; --j) {
+            acc = jac_dbl<C>(acc);
+            acc = jac_dbl<C>(acc);
+            acc = jac_dbl<C>(acc);
+            acc = jac_dbl<C>(acc);
+            int d = recoded_digit<4>(rc, j);
+            if (d != 0) {
+                aff t = tab.load((d < 0 ? -d : d) - 1);
+                if (d < 0) t.y = fe_neg(f, t.y);
+                acc = jac_madd<C>(acc, t);
+            }
+        }
+        return acc;
     }
-    return acc;
 }
 
 // ------------------------------------------------------------ point codec
@@ -274,11 +405,11 @@ GECC_HD int sign_lane(const fe& e, const fe& d, uint64_t seed, uint64_t stream,
         fe k = nonce_scalar<typename C::Fn>(seed, stream, attempt);
         jac R = fixed_base_mul<C, WG>(k, gt);
         if (jac_is_inf(R)) continue;                          // cannot happen for 0 < k < n
-        fe zinv = fe_inv_fermat(fp, R.Z);
+        fe zinv = fe_inv(fp, R.Z);
         fe x = fe_from_mont(fp, fe_mul(fp, R.X, fe_sqr(fp, zinv)));
         fe r = scalar_reduce_once<typename C::Fn>(x);         // coord_mod_n, protocol.cpp:37-39
         if (fe_is_zero(r)) continue;
-        fe kinv_m = fe_inv_fermat(fn, fe_to_mont(fn, k));
+        fe kinv_m = fe_to_mont(fn, safegcd_inverse(fn, k));
         fe r_m = fe_to_mont(fn, r);
         fe s_m = fe_mul(fn, kinv_m, fe_add(fn, e_m, fe_mul(fn, r_m, d_m)));
         fe s = fe_from_mont(fn, s_m);
@@ -302,7 +433,7 @@ GECC_HD uint8_t verify_lane(const uint8_t* digest32, const uint8_t* pub65, const
     aff Q;
     if (!decode_point<C>(pub65, &Q)) return 0;
     fe e = scalar_reduce_once<typename C::Fn>(be32_load(digest32));   // capi.cpp:81-88
-    fe w_m = fe_inv_fermat(fn, fe_to_mont(fn, s));                     // s^-1 (Montgomery form)
+    fe w_m = fe_to_mont(fn, safegcd_inverse(fn, s));                   // s^-1 (Montgomery form)
     fe u1 = fe_mul(fn, e, w_m);                                        // e * w, plain
     fe u2 = fe_mul(fn, r, w_m);
     jac A = fixed_base_mul<C, WG>(u1, gt);

@@ -30,13 +30,16 @@ struct fe {
 struct FieldRT {
     static constexpr int N = 8;
     static constexpr int kind = KIND_GENERIC;
-    uint32_t q_[8], r_[8], r2_[8], ninv_[8], qm2_[8];
-    uint32_t qinv32;
+    uint32_t q_[8], r_[8], r2_[8], ninv_[8], qm2_[8], r3_[8], q30_[9];
+    uint32_t qinv32, qinv30_;
     GECC_HD uint32_t q(int i) const { return q_[i]; }
     GECC_HD uint32_t r(int i) const { return r_[i]; }
     GECC_HD uint32_t r2(int i) const { return r2_[i]; }
     GECC_HD uint32_t ninv(int i) const { return ninv_[i]; }
     GECC_HD uint32_t qm2(int i) const { return qm2_[i]; }
+    GECC_HD uint32_t r3(int i) const { return r3_[i]; }
+    GECC_HD uint32_t q30(int i) const { return q30_[i]; }
+    GECC_HD uint32_t qinv30() const { return qinv30_; }
 };
 
 // ---------------------------------------------------------------- basics
@@ -341,14 +344,31 @@ GECC_HD fe redc(const F& f, const uint32_t* t) {
 }
 
 // ---------------------------------------------------------------- mul / sqr
+#if defined(GECC_COUNT_OPS) && !defined(__CUDA_ARCH__)
+// test-only instrumentation (tests/hostsim): executed products per field kind,
+// used to derive the analytic work-per-lane figures quoted in DESIGN.md / bench.py
+struct OpCounters {
+    unsigned long long mul[3], sqr[3], safegcd[3];
+};
+inline OpCounters& op_counters() {
+    static OpCounters c = {};
+    return c;
+}
+#define GECC_COUNT(what, F) (op_counters().what[F::kind == KIND_GENERIC ? 0 : 1]++)
+#else
+#define GECC_COUNT(what, F) ((void)0)
+#endif
+
 template <class F>
 GECC_HD fe fe_mul_inl(const F& f, const fe& a, const fe& b) {
+    GECC_COUNT(mul, F);
     uint32_t t[16];
     mul_wide8(t, a.w, b.w);
     return redc(f, t);
 }
 template <class F>
 GECC_HD fe fe_sqr_inl(const F& f, const fe& a) {
+    GECC_COUNT(sqr, F);
     uint32_t t[16];
     sqr_wide8(t, a.w);
     return redc(f, t);

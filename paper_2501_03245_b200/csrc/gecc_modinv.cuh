@@ -1,0 +1,202 @@
+// Modular inversion by Bernstein-Yang division steps ("safegcd", Bernstein & Yang,
+// "Fast constant-time gcd computation and modular inversion", TCHES 2019), in the
+// signed 30-bit-limb organisation that is common for 32-bit targets: 20 rounds of 30
+// branch-free divsteps on the low limbs, each followed by one 2x2 matrix update of
+// (f, g) and, modulo q, of (d, e).  Every lane of a warp executes the identical
+// instruction sequence (no data-dependent branches), which is what a SIMT machine
+// needs; a Fermat exponentiation costs 256 squarings + ~80 products instead.
+//
+// The reference inverts by Fermat (mod_inv_fermat, field.cpp:239-246) and checks it
+// against an extended-Euclid oracle (tests/test_field.cpp:203-225): the residue is
+// unique, so the result bits are identical whichever way it is computed.
+//
+//   safegcd_inverse(f, x)  : x^-1 mod q for a plain residue 0 < x < q (0 -> 0)
+//   fe_inv(f, a)           : Montgomery-form inverse of a Montgomery-form element:
+//                            (aR)^-1 * R^3 * R^-1 = a^-1 R
+#pragma once
+#include "gecc_field.cuh"
+
+namespace gecc {
+
+struct s30 {
+    int32_t v[9];  // value = sum v[i] 2^(30 i); limbs in (-2^30, 2^30) except v[8]
+};
+struct trans2x2 {
+    int32_t u, v, q, r;
+};
+
+GECC_HD s30 s30_from_u256(const uint32_t* w) {
+    s30 r;
+    const uint32_t M30 = 0x3FFFFFFFu;
+    r.v[0] = (int32_t)(w[0] & M30);
+    r.v[1] = (int32_t)(((w[0] >> 30) | (w[1] << 2)) & M30);
+    r.v[2] = (int32_t)(((w[1] >> 28) | (w[2] << 4)) & M30);
+    r.v[3] = (int32_t)(((w[2] >> 26) | (w[3] << 6)) & M30);
+    r.v[4] = (int32_t)(((w[3] >> 24) | (w[4] << 8)) & M30);
+    r.v[5] = (int32_t)(((w[4] >> 22) | (w[5] << 10)) & M30);
+    r.v[6] = (int32_t)(((w[5] >> 20) | (w[6] << 12)) & M30);
+    r.v[7] = (int32_t)(((w[6] >> 18) | (w[7] << 14)) & M30);
+    r.v[8] = (int32_t)(w[7] >> 16);
+    return r;
+}
+GECC_HD void s30_to_u256(uint32_t* w, const s30& a) {  // a normalised: limbs in [0, 2^30)
+    const uint32_t* v = reinterpret_cast<const uint32_t*>(a.v);
+    w[0] = v[0] | (v[1] << 30);
+    w[1] = (v[1] >> 2) | (v[2] << 28);
+    w[2] = (v[2] >> 4) | (v[3] << 26);
+    w[3] = (v[3] >> 6) | (v[4] << 24);
+    w[4] = (v[4] >> 8) | (v[5] << 22);
+    w[5] = (v[5] >> 10) | (v[6] << 20);
+    w[6] = (v[6] >> 12) | (v[7] << 18);
+    w[7] = (v[7] >> 14) | (v[8] << 16);
+}
+
+// 30 division steps on the low limbs; zeta = -(delta + 1/2).  Returns the new zeta
+// and the transition matrix t with t * [f, g] = 2^30 * [f', g'].
+GECC_HD int32_t divsteps_30(int32_t zeta, uint32_t f0, uint32_t g0, trans2x2* t) {
+    uint32_t u = 1, v = 0, q = 0, r = 1;
+    uint32_t f = f0, g = g0;
+#pragma unroll 6
+    for (int i = 0; i < 30; ++i) {
+        uint32_t c1 = (uint32_t)(zeta >> 31);  // all ones when zeta < 0
+        uint32_t c2 = 0u - (g & 1u);           // all ones when g is odd
+        uint32_t x = (f ^ c1) - c1;            // +-f
+        uint32_t y = (u ^ c1) - c1;
+        uint32_t z = (v ^ c1) - c1;
+        g += x & c2;
+        q += y & c2;
+        r += z & c2;
+        c1 &= c2;                              // swap happens when zeta < 0 and g odd
+        zeta = (int32_t)(((uint32_t)zeta ^ c1) - 1u);
+        f += g & c1;
+        u += q & c1;
+        v += r & c1;
+        g >>= 1;
+        u <<= 1;
+        v <<= 1;
+    }
+    t->u = (int32_t)u;
+    t->v = (int32_t)v;
+    t->q = (int32_t)q;
+    t->r = (int32_t)r;
+    return zeta;
+}
+
+// (f, g) <- t * (f, g) / 2^30 (exact)
+GECC_HD void update_fg_30(s30* f, s30* g, const trans2x2& t) {
+    const int32_t M30 = 0x3FFFFFFF;
+    const int64_t u = t.u, v = t.v, q = t.q, r = t.r;
+    int64_t cf = u * f->v[0] + v * g->v[0];
+    int64_t cg = q * f->v[0] + r * g->v[0];
+    cf >>= 30;
+    cg >>= 30;
+#pragma unroll
+    for (int i = 1; i < 9; ++i) {
+        const int32_t fi = f->v[i], gi = g->v[i];
+        cf += u * fi + v * gi;
+        cg += q * fi + r * gi;
+        f->v[i - 1] = (int32_t)cf & M30;
+        cf >>= 30;
+        g->v[i - 1] = (int32_t)cg & M30;
+        cg >>= 30;
+    }
+    f->v[8] = (int32_t)cf;
+    g->v[8] = (int32_t)cg;
+}
+
+// (d, e) <- t * (d, e) / 2^30 mod q: a multiple of q is added first so that the
+// low 30 bits vanish and the division is exact.  d, e stay in (-2q, q).
+template <class F>
+GECC_HD void update_de_30(const F& f, s30* d, s30* e, const trans2x2& t) {
+    const int32_t M30 = 0x3FFFFFFF;
+    const int64_t u = t.u, v = t.v, q = t.q, r = t.r;
+    const int32_t sd = d->v[8] >> 31, se = e->v[8] >> 31;
+    int32_t md = (t.u & sd) + (t.v & se);
+    int32_t me = (t.q & sd) + (t.r & se);
+    int64_t cd = u * d->v[0] + v * e->v[0];
+    int64_t ce = q * d->v[0] + r * e->v[0];
+    md -= (int32_t)((f.qinv30() * (uint32_t)cd + (uint32_t)md) & (uint32_t)M30);
+    me -= (int32_t)((f.qinv30() * (uint32_t)ce + (uint32_t)me) & (uint32_t)M30);
+    cd += (int64_t)f.q30(0) * md;
+    ce += (int64_t)f.q30(0) * me;
+    cd >>= 30;
+    ce >>= 30;
+#pragma unroll
+    for (int i = 1; i < 9; ++i) {
+        const int32_t di = d->v[i], ei = e->v[i];
+        cd += u * di + v * ei;
+        ce += q * di + r * ei;
+        cd += (int64_t)f.q30(i) * md;
+        ce += (int64_t)f.q30(i) * me;
+        d->v[i - 1] = (int32_t)cd & M30;
+        cd >>= 30;
+        e->v[i - 1] = (int32_t)ce & M30;
+        ce >>= 30;
+    }
+    d->v[8] = (int32_t)cd;
+    e->v[8] = (int32_t)ce;
+}
+
+// r in (-2q, q) -> [0, q), negated first when sign < 0
+template <class F>
+GECC_HD void normalize_30(const F& f, s30* r, int32_t sign) {
+    const int32_t M30 = 0x3FFFFFFF;
+    int32_t cond_add = r->v[8] >> 31;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) r->v[i] += (int32_t)f.q30(i) & cond_add;
+    const int32_t cond_negate = sign >> 31;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) r->v[i] = (r->v[i] ^ cond_negate) - cond_negate;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        r->v[i + 1] += r->v[i] >> 30;
+        r->v[i] &= M30;
+    }
+    cond_add = r->v[8] >> 31;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) r->v[i] += (int32_t)f.q30(i) & cond_add;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        r->v[i + 1] += r->v[i] >> 30;
+        r->v[i] &= M30;
+    }
+}
+
+// x^-1 mod q, x a plain residue in [0, q); 0 -> 0.
+template <class F>
+GECC_HD_CALL fe safegcd_inverse(const F& fld, const fe& x) {
+    GECC_COUNT(safegcd, F);
+    s30 d, e, f, g;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+        d.v[i] = 0;
+        e.v[i] = 0;
+        f.v[i] = (int32_t)fld.q30(i);
+    }
+    e.v[0] = 1;
+    g = s30_from_u256(x.w);
+    int32_t zeta = -1;
+#pragma unroll 1
+    for (int round = 0; round < 20; ++round) {  // 600 divsteps >= 590 needed for 256 bits
+        trans2x2 t;
+        zeta = divsteps_30(zeta, (uint32_t)f.v[0], (uint32_t)g.v[0], &t);
+        update_de_30(fld, &d, &e, t);
+        update_fg_30(&f, &g, t);
+    }
+    // g == 0 now and f == +-gcd == +-1 (or f == +-q when x == 0, where d == 0)
+    normalize_30(fld, &d, f.v[8]);
+    fe r;
+    s30_to_u256(r.w, d);
+    return r;
+}
+
+// Montgomery-form inverse of a Montgomery-form element (zero -> zero).
+template <class F>
+GECC_HD fe fe_inv(const F& f, const fe& a) {
+    fe r3;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r3.w[i] = f.r3(i);
+    return fe_mul(f, safegcd_inverse(f, a), r3);
+}
+
+}  // namespace gecc

@@ -12,6 +12,7 @@
 // reference's for any LanePlan.
 #include "gecc_curve.cuh"
 #include "gecc_dev.cuh"
+#include "gecc_modinv.cuh"
 #include "gecc_host.h"
 
 namespace gecc {
@@ -34,7 +35,7 @@ k_batch_invert(size_t n, size_t T, const uint32_t* __restrict__ in, uint32_t* __
         col_store(out, n, i, acc);  // prefix product through element i
         last = i;
     }
-    fe inv = fe_inv_fermat(f, acc);
+    fe inv = fe_inv(f, acc);
 #pragma unroll 1
     for (size_t i = last;; i -= T) {
         fe v = col_load(in, n, i);
@@ -111,7 +112,7 @@ k_batch_padd(size_t n, size_t T, const uint32_t* __restrict__ px, const uint32_t
         col_store(ox, n, i, acc);
         last = i;
     }
-    fe inv = fe_inv_fermat(f, acc);
+    fe inv = fe_inv(f, acc);
     // scatter + DCWPA: recover each inverse and finish the formulas (batch_point.cpp:124-170)
 #pragma unroll 1
     for (size_t i = last;; i -= T) {
@@ -163,7 +164,7 @@ k_batch_pdbl(size_t n, size_t T, const uint32_t* __restrict__ px, const uint32_t
         col_store(ox, n, i, acc);
         last = i;
     }
-    fe inv = fe_inv_fermat(f, acc);
+    fe inv = fe_inv(f, acc);
 #pragma unroll 1
     for (size_t i = last;; i -= T) {
         fe ax = col_load(px, n, i), ay = col_load(py, n, i);

@@ -56,7 +56,7 @@ k_keygen(size_t n, uint64_t seed, uint64_t lane_base, const uint32_t* __restrict
     fe d = nonce_scalar<typename C::Fn>(seed, lane_base + i, 0);
     be32_store(sec + 32 * i, d);
     jac r = fixed_base_mul<C, GECC_WG>(d, gt);
-    encode_point<C>(pub + 65 * i, jac_to_aff_with<C>(r, fe_inv_fermat(f, r.Z)));
+    encode_point<C>(pub + 65 * i, jac_to_aff_with<C>(r, fe_inv(f, r.Z)));
 }
 
 // capi.cpp:230-261 + protocol.cpp:224-263.  status: 0 ok, 3 invalid peer,
@@ -88,7 +88,7 @@ k_ecdh(size_t n, const uint8_t* __restrict__ sec, const uint8_t* __restrict__ pe
         status[i] = 4;
         return;
     }
-    fe zinv = fe_inv_fermat(f, r.Z);
+    fe zinv = fe_inv(f, r.Z);
     be32_store(shared + 32 * i, fe_from_mont(f, fe_mul(f, r.X, fe_sqr(f, zinv))));
     status[i] = 0;
 }
@@ -104,7 +104,7 @@ __device__ __forceinline__ void store_affine(const jac& r, uint32_t* ox, uint32_
         oinf[i] = 1;
         return;
     }
-    aff a = jac_to_aff_with<C>(r, fe_inv_fermat(f, r.Z));
+    aff a = jac_to_aff_with<C>(r, fe_inv(f, r.Z));
     col_store(ox, n, i, a.x);
     col_store(oy, n, i, a.y);
     oinf[i] = 0;

@@ -1,6 +1,7 @@
 // Element-wise field kernels over column buffers: the GPU form of the reference's
 // field layer (field.cpp:194-246) used for parity tests of the limb arithmetic.
 #include "gecc_dev.cuh"
+#include "gecc_modinv.cuh"
 #include "gecc_host.h"
 
 namespace gecc {
@@ -21,7 +22,8 @@ __global__ void __launch_bounds__(256) k_field_op(int op, size_t n, const uint32
             case 2: r = fe_sub(f, x, y); break;
             case 3: r = fe_to_mont(f, x); break;
             case 4: r = fe_from_mont(f, x); break;
-            default: r = fe_is_zero(x) ? x : fe_inv_fermat(f, x); break;
+            case 5: r = fe_inv(f, x); break;  // safegcd; zero -> zero
+            default: r = fe_is_zero(x) ? x : fe_inv_fermat(f, x); break;  // 6: Fermat cross-check
         }
         col_store(out, n, i, r);
     }

@@ -18,7 +18,7 @@ __global__ void k_gtable_bases(uint32_t* __restrict__ bases) {
     b.X = g.x; b.Y = g.y; b.Z = fe_one(f);
 #pragma unroll 1
     for (int k = 0; k < WG * j; ++k) b = jac_dbl<C>(b);
-    aff a = jac_to_aff_with<C>(b, fe_inv_fermat(f, b.Z));
+    aff a = jac_to_aff_with<C>(b, fe_inv(f, b.Z));
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         bases[j * 16 + i] = a.x.w[i];
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(128) k_gtable_fill(const uint32_t* __restrict_
         acc = jac_dbl<C>(acc);
         if ((d >> bit) & 1u) acc = jac_madd<C>(acc, b);
     }
-    aff a = jac_to_aff_with<C>(acc, fe_inv_fermat(f, acc.Z));
+    aff a = jac_to_aff_with<C>(acc, fe_inv(f, acc.Z));
     uint4* out = reinterpret_cast<uint4*>(tab + idx * 16);
     out[0] = make_uint4(a.x.w[0], a.x.w[1], a.x.w[2], a.x.w[3]);
     out[1] = make_uint4(a.x.w[4], a.x.w[5], a.x.w[6], a.x.w[7]);

@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "gecc_field.cuh"
+#include "gecc_modinv.cuh"
 
 using namespace gecc;
 
@@ -31,6 +32,8 @@ int field_op_t(const F& f, int op, size_t n, const uint32_t* a, const uint32_t* 
             case 4: r = fe_from_mont(f, x); break;
             case 5: r = fe_is_zero(x) ? x : fe_inv_fermat(f, x); break;
             case 6: r = fe_sqr(f, x); break;
+            case 7: r = fe_inv(f, x); break;            // safegcd, Montgomery in/out
+            case 8: r = safegcd_inverse(f, x); break;   // safegcd, plain in/out
             default: return 1;
         }
         col_set(out, n, i, r);
@@ -64,7 +67,9 @@ int hs_field_op(int field, const FieldRT* rt, int op, size_t n, const uint32_t* 
 
 namespace {
 
-constexpr int HS_WG = 4;  // small fixed-base window so the host can build the table quickly
+#ifndef HS_WG
+#define HS_WG 4  // small fixed-base window so the host can build the table quickly
+#endif
 
 template <class C>
 const std::vector<uint32_t>& host_gtable() {
@@ -77,11 +82,11 @@ const std::vector<uint32_t>& host_gtable() {
     aff g = curve_g<C>();
     base.X = g.x; base.Y = g.y; base.Z = fe_one(f);
     for (int j = 0; j < GT::windows; ++j) {
-        aff b = jac_to_aff_with<C>(base, fe_inv_fermat(f, base.Z));
+        aff b = jac_to_aff_with<C>(base, fe_inv(f, base.Z));
         jac acc = jac_infinity<C>();
         for (int d = 1; d <= GT::per_window; ++d) {
             acc = jac_madd<C>(acc, b);
-            aff e = jac_to_aff_with<C>(acc, fe_inv_fermat(f, acc.Z));
+            aff e = jac_to_aff_with<C>(acc, fe_inv(f, acc.Z));
             uint32_t* p = &tab[((size_t)j * GT::per_window + (d - 1)) * 16];
             for (int i = 0; i < 8; ++i) { p[i] = e.x.w[i]; p[8 + i] = e.y.w[i]; }
         }
@@ -99,7 +104,7 @@ void store_point(const jac& r, uint32_t* ox, uint32_t* oy, uint8_t* oinf, size_t
         oinf[i] = 1;
         return;
     }
-    aff a = jac_to_aff_with<C>(r, fe_inv_fermat(f, r.Z));
+    aff a = jac_to_aff_with<C>(r, fe_inv(f, r.Z));
     col_set(ox, n, i, a.x);
     col_set(oy, n, i, a.y);
     oinf[i] = 0;
@@ -153,7 +158,7 @@ int keygen_t(size_t n, uint64_t seed, uint64_t base, uint8_t* sec, uint8_t* pub)
         fe d = nonce_scalar<typename C::Fn>(seed, base + i, 0);
         be32_store(sec + 32 * i, d);
         jac r = fixed_base_mul<C, HS_WG>(d, gt);
-        encode_point<C>(pub + 65 * i, jac_to_aff_with<C>(r, fe_inv_fermat(f, r.Z)));
+        encode_point<C>(pub + 65 * i, jac_to_aff_with<C>(r, fe_inv(f, r.Z)));
     }
     return 0;
 }
@@ -183,3 +188,29 @@ int hs_keygen(int curve, size_t n, uint64_t seed, uint64_t base, uint8_t* sec, u
                       : keygen_t<SecpCurve>(n, seed, base, sec, pub);
 }
 }  // extern "C"
+
+// GLV split of secp256k1 scalars: out = m1 (8 limbs) | m2 (8 limbs) per element, signs in sg[2*i..]
+extern "C" int hs_glv_split(size_t n, const uint32_t* k, uint32_t* m1, uint32_t* m2, uint8_t* sg) {
+    for (size_t i = 0; i < n; ++i) {
+        GlvSplit s = glv_split<SecpCurve>(col_get(k, n, i));
+        col_set(m1, n, i, s.m1);
+        col_set(m2, n, i, s.m2);
+        sg[2 * i] = s.neg1;
+        sg[2 * i + 1] = s.neg2;
+    }
+    return 0;
+}
+
+// executed-product counters: [mul_generic, mul_special, sqr_generic, sqr_special, safegcd_generic, safegcd_special]
+extern "C" void hs_op_counts(unsigned long long* out, int reset) {
+#if defined(GECC_COUNT_OPS)
+    OpCounters& c = op_counters();
+    out[0] = c.mul[0]; out[1] = c.mul[1]; out[2] = c.sqr[0]; out[3] = c.sqr[1];
+    out[4] = c.safegcd[0]; out[5] = c.safegcd[1];
+    if (reset) c = OpCounters{};
+#else
+    for (int i = 0; i < 6; ++i) out[i] = 0;
+    (void)reset;
+#endif
+}
+extern "C" int hs_window_bits(void) { return HS_WG; }
