@@ -676,7 +676,67 @@ sm2b_status gecc_batch_upmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, c
 // ------------------------------------------------------------------ not yet built
 #define GECC_TODO(ctx) ((ctx) ? fail_msg(ctx, "not implemented in this build") : SM2B_ERROR_INVALID_ARGUMENT)
 sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char*, const char*, size_t, size_t, uint32_t, uint64_t, uint32_t, sm2b_bench_report*) { return GECC_TODO(ctx); }
-sm2b_status gecc_msm(sm2b_ctx* ctx, size_t, const uint32_t*, const uint32_t*, const uint32_t*, const uint8_t*, uint32_t*, uint32_t*, uint8_t*) { return GECC_TODO(ctx); }
-sm2b_status gecc_msm_dev(sm2b_ctx* ctx, size_t, const uint32_t*, const uint32_t*, const uint32_t*, const uint8_t*, uint32_t*, uint32_t*, uint8_t*) { return GECC_TODO(ctx); }
+sm2b_status gecc_msm_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uint32_t* px,
+                         const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
+                         uint8_t* oinf) {
+    if (!ctx || !ox || !oy || !oinf || (n > 0 && (!scalars || !px || !py)))
+        return SM2B_ERROR_INVALID_ARGUMENT;
+    if (n >= ((size_t)1 << 31)) return SM2B_ERROR_INVALID_ARGUMENT;  // point index is 31 bits
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    if (n == 0) {  // empty sum = point at infinity
+        CU(ctx, cudaMemsetAsync(ox, 0, 32, ctx->stream));
+        CU(ctx, cudaMemsetAsync(oy, 0, 32, ctx->stream));
+        CU(ctx, cudaMemsetAsync(oinf, 1, 1, ctx->stream));
+        return SM2B_OK;
+    }
+    CU(ctx, ctx->scratch.ensure(msm_scratch_bytes(n)));
+    int launches = 0;
+    CU(ctx, launch_msm(ctx->curve, n, scalars, px, py, pinf, ox, oy, oinf, ctx->scratch.p, ctx->stream,
+                       &launches));
+    ctx->launches += launches;
+    return SM2B_OK;
+}
+
+sm2b_status gecc_msm(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uint32_t* px,
+                     const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
+                     uint8_t* oinf) {
+    if (!ctx || !ox || !oy || !oinf || (n > 0 && (!scalars || !px || !py)))
+        return SM2B_ERROR_INVALID_ARGUMENT;
+    uint32_t *dk = nullptr, *dpx = nullptr, *dpy = nullptr, *dox, *doy;
+    uint8_t *dpi = nullptr, *doi;
+    {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        DeviceGuard g(ctx->device);
+        const size_t cb = Carver::need(32 * n), mb = Carver::need(n);
+        CU(ctx, ctx->in.ensure(3 * cb + mb + 256));
+        CU(ctx, ctx->out.ensure(1024));
+        Carver ci(ctx->in.p), co(ctx->out.p);
+        dox = co.take<uint32_t>(8);
+        doy = co.take<uint32_t>(8);
+        doi = co.take<uint8_t>(1);
+        if (n) {
+            dk = ci.take<uint32_t>(8 * n);
+            dpx = ci.take<uint32_t>(8 * n);
+            dpy = ci.take<uint32_t>(8 * n);
+            CU(ctx, cudaMemcpyAsync(dk, scalars, 32 * n, cudaMemcpyHostToDevice, ctx->stream));
+            CU(ctx, cudaMemcpyAsync(dpx, px, 32 * n, cudaMemcpyHostToDevice, ctx->stream));
+            CU(ctx, cudaMemcpyAsync(dpy, py, 32 * n, cudaMemcpyHostToDevice, ctx->stream));
+            if (pinf) {
+                dpi = ci.take<uint8_t>(n);
+                CU(ctx, cudaMemcpyAsync(dpi, pinf, n, cudaMemcpyHostToDevice, ctx->stream));
+            }
+        }
+    }
+    sm2b_status st = gecc_msm_dev(ctx, n, dk, dpx, dpy, dpi, dox, doy, doi);
+    if (st != SM2B_OK) return st;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, cudaMemcpyAsync(ox, dox, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(oy, doy, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(oinf, doi, 1, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    return SM2B_OK;
+}
 
 }  // extern "C"

@@ -46,4 +46,11 @@ cudaError_t launch_batch_pdbl(int curve, size_t n, const uint32_t* px, const uin
                               const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
                               cudaStream_t s);
 
+
+// MSM: scratch must hold msm_scratch_bytes(n) bytes of device memory
+size_t msm_scratch_bytes(size_t n);
+cudaError_t launch_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px,
+                       const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
+                       uint8_t* oinf, void* scratch, cudaStream_t s, int* launches);
+
 }  // namespace gecc

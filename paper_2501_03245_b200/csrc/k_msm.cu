@@ -1,0 +1,260 @@
+// Multi-scalar multiplication  sum_i k_i * P_i  (Pippenger's bucket method).
+//
+// The reference has no MSM; the contract here is the
+// definition, checked against the oracle's sum of pmul_serial results and against
+// the identity  sum_i s_i (t_i G) = (sum_i s_i t_i) G  at full size.
+//
+//   1. k_msm_digits   : every scalar is recoded into 17 signed 16-bit digits
+//                       (same offset recoding as the fixed-base path); one
+//                       (bucket id, point index | sign) pair per non-zero digit.
+//   2. radix sort of the pairs by bucket id (CUB, plumbing only).
+//   3. k_msm_buckets  : one thread per bucket sums its points (mixed Jacobian adds).
+//   4. bucket reduction  S_w = sum_b (b+1) B_w[b]  without any long serial chain:
+//      b = lo + 32 mid + 1024 top, so S_w = sum B + sum_k 32^k sum_e e * C^k_e with the
+//      three marginal sums C^k_e (each over 1024 buckets, done as 32 x 32).
+//   5. k_msm_combine  : sum_w 2^(16 w) S_w, one affine point out.
+// Bucket ids: window w, magnitude m = 1..2^15  ->  w * 2^15 + (m - 1).
+#include <cub/device/device_radix_sort.cuh>
+
+#include "gecc_ecdsa.cuh"
+#include "gecc_host.h"
+
+namespace gecc {
+
+constexpr int MSM_C = 16;                          // window bits
+constexpr int MSM_WINDOWS = 256 / MSM_C + 1;       // 17 (the last one holds the recoding carry)
+constexpr int MSM_BUCKETS = 1 << (MSM_C - 1);      // 32768 per window
+constexpr uint32_t MSM_NB = MSM_WINDOWS * MSM_BUCKETS;
+constexpr uint32_t MSM_KEY_NONE = 0xFFFFFu;        // sorts behind every real bucket (20-bit keys)
+
+template <class C>
+__global__ void __launch_bounds__(256)
+k_msm_digits(size_t n, const uint32_t* __restrict__ scalars, const uint8_t* __restrict__ pinf,
+             uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    fe k = scalar_reduce_once<typename C::Fn>(col_load(scalars, n, i));
+    const bool skip = pinf && pinf[i];
+    Recoded<MSM_C> rc = recode_signed<MSM_C>(k);
+#pragma unroll
+    for (int w = 0; w < MSM_WINDOWS; ++w) {
+        int d = w == MSM_WINDOWS - 1 ? (int)rc.carry : recoded_digit<MSM_C>(rc, w);
+        uint32_t key = MSM_KEY_NONE, val = 0;
+        if (d != 0 && !skip) {
+            const uint32_t mag = (uint32_t)(d < 0 ? -d : d);
+            key = (uint32_t)w * MSM_BUCKETS + (mag - 1);
+            val = (uint32_t)i | (d < 0 ? 0x80000000u : 0u);
+        }
+        keys[(size_t)w * n + i] = key;   // window-major: coalesced writes
+        vals[(size_t)w * n + i] = val;
+    }
+}
+
+// first position whose key is >= bucket (sorted keys)
+__device__ __forceinline__ size_t lower_bound_key(const uint32_t* keys, size_t m, uint32_t bucket) {
+    size_t lo = 0, hi = m;
+    while (lo < hi) {
+        size_t mid = (lo + hi) >> 1;
+        if (keys[mid] < bucket) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Jacobian point arrays are stored word-major: word k (0..23: X, Y, Z) of element e at
+// buf[k * count + e].
+__device__ __forceinline__ void jac_store(uint32_t* buf, size_t count, size_t e, const jac& p) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        buf[(size_t)k * count + e] = p.X.w[k];
+        buf[(size_t)(8 + k) * count + e] = p.Y.w[k];
+        buf[(size_t)(16 + k) * count + e] = p.Z.w[k];
+    }
+}
+__device__ __forceinline__ jac jac_load(const uint32_t* buf, size_t count, size_t e) {
+    jac p;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        p.X.w[k] = buf[(size_t)k * count + e];
+        p.Y.w[k] = buf[(size_t)(8 + k) * count + e];
+        p.Z.w[k] = buf[(size_t)(16 + k) * count + e];
+    }
+    return p;
+}
+
+template <class C>
+__global__ void __launch_bounds__(128)
+k_msm_buckets(size_t n, size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+              const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
+              uint32_t* __restrict__ buckets) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= MSM_NB) return;
+    const typename C::Fp f{};
+    size_t lo = lower_bound_key(keys, m, b), hi = lower_bound_key(keys, m, b + 1);
+    jac acc = jac_infinity<C>();
+#pragma unroll 1
+    for (size_t p = lo; p < hi; ++p) {
+        const uint32_t v = vals[p];
+        const size_t idx = v & 0x7FFFFFFFu;
+        aff t{col_load(px, n, idx), col_load(py, n, idx)};
+        if (v >> 31) t.y = fe_neg(f, t.y);
+        acc = jac_madd<C>(acc, t);
+    }
+    jac_store(buckets, MSM_NB, b, acc);
+}
+
+// marginal sums, stage 1: thread (w, k, e, part) adds the 32 buckets of window w whose
+// k-th base-32 digit is e and whose next digit (cyclically) is `part`.
+template <class C>
+__global__ void __launch_bounds__(128)
+k_msm_marginal_parts(const uint32_t* __restrict__ buckets, uint32_t* __restrict__ parts) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= MSM_WINDOWS * 3 * 32 * 32) return;
+    const uint32_t part = t & 31, e = (t >> 5) & 31, k = (t >> 10) % 3, w = t / (3 * 1024);
+    jac acc = jac_infinity<C>();
+#pragma unroll 1
+    for (uint32_t v = 0; v < 32; ++v) {
+        uint32_t b;
+        if (k == 0) b = e + 32 * part + 1024 * v;        // lo = e
+        else if (k == 1) b = part + 32 * e + 1024 * v;   // mid = e
+        else b = part + 32 * v + 1024 * e;               // top = e
+        acc = jac_add<C>(acc, jac_load(buckets, MSM_NB, (size_t)w * MSM_BUCKETS + b));
+    }
+    jac_store(parts, (size_t)MSM_WINDOWS * 3 * 1024, t, acc);
+}
+// stage 2: thread (w, k, e) folds its 32 parts
+template <class C>
+__global__ void __launch_bounds__(128)
+k_msm_marginal_fold(const uint32_t* __restrict__ parts, uint32_t* __restrict__ marg) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= MSM_WINDOWS * 3 * 32) return;
+    jac acc = jac_infinity<C>();
+#pragma unroll 1
+    for (uint32_t p = 0; p < 32; ++p)
+        acc = jac_add<C>(acc, jac_load(parts, (size_t)MSM_WINDOWS * 3 * 1024, (size_t)t * 32 + p));
+    jac_store(marg, (size_t)MSM_WINDOWS * 3 * 32, t, acc);
+}
+// stage 3: thread (w, j): j < 3 -> sum_e e * C^j_e (running sums); j == 3 -> sum_e C^0_e
+template <class C>
+__global__ void __launch_bounds__(128)
+k_msm_weighted(const uint32_t* __restrict__ marg, uint32_t* __restrict__ wsum) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= MSM_WINDOWS * 4) return;
+    const uint32_t w = t >> 2, j = t & 3;
+    const size_t cnt = (size_t)MSM_WINDOWS * 3 * 32;
+    jac acc = jac_infinity<C>();
+    if (j == 3) {
+#pragma unroll 1
+        for (uint32_t e = 0; e < 32; ++e) acc = jac_add<C>(acc, jac_load(marg, cnt, (size_t)(w * 3) * 32 + e));
+    } else {
+        jac run = jac_infinity<C>();
+#pragma unroll 1
+        for (int e = 31; e >= 1; --e) {
+            run = jac_add<C>(run, jac_load(marg, cnt, (size_t)(w * 3 + j) * 32 + e));
+            acc = jac_add<C>(acc, run);
+        }
+    }
+    jac_store(wsum, (size_t)MSM_WINDOWS * 4, t, acc);
+}
+// stage 4 (one block of 32 threads): thread w forms S_w = (sum B) + W0 + 32 W1 + 1024 W2
+// (weights b + 1), shifts it by 2^(16 w); thread 0 adds the windows and converts to affine.
+template <class C>
+__global__ void __launch_bounds__(32)
+k_msm_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, uint32_t* __restrict__ oy,
+              uint8_t* __restrict__ oinf) {
+    __shared__ uint32_t win[24 * MSM_WINDOWS];
+    const uint32_t w = threadIdx.x;
+    const size_t cnt = (size_t)MSM_WINDOWS * 4;
+    if (w < MSM_WINDOWS) {
+        jac s = jac_load(wsum, cnt, w * 4 + 2);
+#pragma unroll 1
+        for (int i = 0; i < 5; ++i) s = jac_dbl<C>(s);
+        s = jac_add<C>(s, jac_load(wsum, cnt, w * 4 + 1));
+#pragma unroll 1
+        for (int i = 0; i < 5; ++i) s = jac_dbl<C>(s);
+        s = jac_add<C>(s, jac_load(wsum, cnt, w * 4 + 0));
+        s = jac_add<C>(s, jac_load(wsum, cnt, w * 4 + 3));
+#pragma unroll 1
+        for (uint32_t i = 0; i < MSM_C * w; ++i) s = jac_dbl<C>(s);
+        jac_store(win, MSM_WINDOWS, w, s);
+    }
+    __syncthreads();
+    if (w == 0) {
+        const typename C::Fp f{};
+        jac acc = jac_infinity<C>();
+#pragma unroll 1
+        for (int i = 0; i < MSM_WINDOWS; ++i) acc = jac_add<C>(acc, jac_load(win, MSM_WINDOWS, i));
+        if (jac_is_inf(acc)) {
+            col_store(ox, 1, 0, fe_zero());
+            col_store(oy, 1, 0, fe_zero());
+            oinf[0] = 1;
+        } else {
+            aff a = jac_to_aff_with<C>(acc, fe_inv(f, acc.Z));
+            col_store(ox, 1, 0, a.x);
+            col_store(oy, 1, 0, a.y);
+            oinf[0] = 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- host side
+struct MsmPlan {
+    size_t pairs, sort_temp, total;
+    size_t off_keys, off_vals, off_keys2, off_vals2, off_buckets, off_parts, off_marg, off_wsum, off_temp;
+};
+static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+static MsmPlan msm_plan(size_t n) {
+    MsmPlan p{};
+    p.pairs = n * MSM_WINDOWS;
+    cub::DeviceRadixSort::SortPairs(nullptr, p.sort_temp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)p.pairs, 0, 20);
+    size_t at = 0;
+    auto take = [&](size_t bytes) { size_t o = at; at += align256(bytes); return o; };
+    p.off_keys = take(4 * p.pairs);
+    p.off_vals = take(4 * p.pairs);
+    p.off_keys2 = take(4 * p.pairs);
+    p.off_vals2 = take(4 * p.pairs);
+    p.off_buckets = take((size_t)96 * MSM_NB);
+    p.off_parts = take((size_t)96 * MSM_WINDOWS * 3 * 1024);
+    p.off_marg = take((size_t)96 * MSM_WINDOWS * 3 * 32);
+    p.off_wsum = take((size_t)96 * MSM_WINDOWS * 4);
+    p.off_temp = take(p.sort_temp);
+    p.total = at;
+    return p;
+}
+size_t msm_scratch_bytes(size_t n) { return n ? msm_plan(n).total : 0; }
+
+template <class C>
+static cudaError_t run_msm(size_t n, const uint32_t* scalars, const uint32_t* px, const uint32_t* py,
+                           const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
+                           void* scratch, cudaStream_t s, int* launches) {
+    MsmPlan p = msm_plan(n);
+    uint8_t* base = (uint8_t*)scratch;
+    uint32_t *keys = (uint32_t*)(base + p.off_keys), *vals = (uint32_t*)(base + p.off_vals);
+    uint32_t *keys2 = (uint32_t*)(base + p.off_keys2), *vals2 = (uint32_t*)(base + p.off_vals2);
+    uint32_t *buckets = (uint32_t*)(base + p.off_buckets), *parts = (uint32_t*)(base + p.off_parts);
+    uint32_t *marg = (uint32_t*)(base + p.off_marg), *wsum = (uint32_t*)(base + p.off_wsum);
+    k_msm_digits<C><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, scalars, pinf, keys, vals);
+    size_t temp = p.sort_temp;
+    cudaError_t e = cub::DeviceRadixSort::SortPairs(base + p.off_temp, temp, keys, keys2, vals, vals2,
+                                                    (int64_t)p.pairs, 0, 20, s);
+    if (e != cudaSuccess) return e;
+    k_msm_buckets<C><<<(MSM_NB + 127) / 128, 128, 0, s>>>(n, p.pairs, keys2, vals2, px, py, buckets);
+    k_msm_marginal_parts<C><<<(MSM_WINDOWS * 3 * 1024 + 127) / 128, 128, 0, s>>>(buckets, parts);
+    k_msm_marginal_fold<C><<<(MSM_WINDOWS * 3 * 32 + 127) / 128, 128, 0, s>>>(parts, marg);
+    k_msm_weighted<C><<<1, 128, 0, s>>>(marg, wsum);
+    k_msm_combine<C><<<1, 32, 0, s>>>(wsum, ox, oy, oinf);
+    *launches = 6 + 4;  // ours + the sort's passes (approximate; CUB picks the pass count)
+    return cudaGetLastError();
+}
+
+cudaError_t launch_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px,
+                       const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
+                       uint8_t* oinf, void* scratch, cudaStream_t s, int* launches) {
+    if (curve == CURVE_SECP)
+        return run_msm<SecpCurve>(n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
+    return run_msm<Sm2Curve>(n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
+}
+
+}  // namespace gecc
