@@ -36,8 +36,9 @@ sys.path.insert(0, ROOT)
 
 SECP = 1
 METRIC = {"verify": "ecdsa_verify_throughput", "sign": "ecdsa_sign_throughput",
-          "padd": "batch_padd_throughput"}
-UNIT = {"verify": "verifications/s", "sign": "signatures/s", "padd": "point additions/s"}
+          "padd": "batch_padd_throughput", "msm": "msm_time"}
+UNIT = {"verify": "verifications/s", "sign": "signatures/s", "padd": "point additions/s",
+        "msm": "ms per MSM"}
 
 
 def parse():
@@ -46,7 +47,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="verify", choices=["verify", "sign", "padd"])
+    ap.add_argument("--workload", default="verify", choices=["verify", "sign", "padd", "msm"])
     ap.add_argument("--log2n", type=int, default=20)
     ap.add_argument("--cpu-sample-log2", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -186,6 +187,10 @@ SLOTS = {
 }
 
 
+def wl_is_msm(w):
+    return w == "msm"
+
+
 def work_per_lane(workload):
     with open(os.path.join(ROOT, "tools", "op_counts.json")) as f:
         counts = json.load(f)["secp256k1"]
@@ -260,7 +265,7 @@ def main():
     got = ctx.verify(pick(h_dig, 32), pick(h_pub, 65), bytes(bad))[1]
     assert want == got and sum(want) == 23, "verify parity gate failed"
 
-    if wl == "padd":
+    if wl in ("padd", "msm"):
         k1 = torch.from_numpy(rs.randint(0, 2**32, size=(8, n), dtype=np.uint64).astype(np.uint32)).cuda()
         k2 = torch.from_numpy(rs.randint(0, 2**32, size=(8, n), dtype=np.uint64).astype(np.uint32)).cuda()
         col = lambda: torch.empty((8, n), dtype=torch.int32, device="cuda")
@@ -275,6 +280,9 @@ def main():
         if wl == "sign":
             return l.gecc_sign_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_sec), C.c_uint64(7),
                                    C.c_uint64(lane_base), vp(d_sig), vp(d_st))
+        if wl == "msm":   # sum_i k2_i * P_i, one point out
+            return l.gecc_msm_dev(ctx.h, C.c_size_t(n), vp(k2), vp(P[0]), vp(P[1]), vp(P[2]),
+                                  vp(S[0]), vp(S[1]), vp(S[2]))
         return l.gecc_batch_padd_dev(ctx.h, C.c_size_t(n), vp(P[0]), vp(P[1]), vp(P[2]), vp(T[0]),
                                      vp(T[1]), vp(T[2]), vp(S[0]), vp(S[1]), vp(S[2]))
 
@@ -313,6 +321,8 @@ def main():
     if wl == "verify":
         assert int(d_res.sum()) == n, "timed verify produced rejects"
     value = world * n * args.steps / dev_s
+    if wl == "msm":   # time-like metric: ms per 2^log2n-point MSM (per GPU; ranks run their own range)
+        value = dev_s / args.steps * 1e3
 
     # ---- e2e: reference-facing C ABI, pinned host buffers, copies inside the timed region
     pin = lambda a: torch.from_numpy(a).pin_memory()
@@ -349,9 +359,9 @@ def main():
     counts, slots_per_lane, products_per_lane = work_per_lane(wl)
     mads = n * slots_per_lane
     achieved = mads / per_launch_s
-    io_bytes = {"verify": 162, "sign": 132, "padd": 194}[wl] * n
+    io_bytes = {"verify": 162, "sign": 132, "padd": 194, "msm": 96}[wl] * n
     roofline = {
-        "bound": "imad", "kernel": {"verify": "k_verify", "sign": "k_sign", "padd": "k_batch_padd"}[wl],
+        "bound": "imad", "kernel": {"verify": "k_verify", "sign": "k_sign", "padd": "k_batch_padd", "msm": "k_msm_buckets"}[wl],
         "achieved": achieved / 1e12, "peak": peak_mad_per_s / 1e12, "unit": "T IMAD.WIDE-slot/s",
         "frac": achieved / peak_mad_per_s,
         "peak_source": "measured live: gecc_microbench(dependent IMAD.WIDE.U32), "
@@ -393,10 +403,12 @@ def main():
         line = {
             "metric": METRIC[wl], "value": value, "unit": UNIT[wl], "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_launch_s * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": wl != "msm", "scaling": "weak", "vs_baseline": None,
             "dtype": "u32 limbs (256-bit modular integer)", "data": "synthetic",
-            "config": {"workload": f"secp256k1 ECDSA {wl}, batch 2^{args.log2n} per GPU"
-                       if wl != "padd" else f"secp256k1 batched affine point addition, 2^{args.log2n} pairs per GPU",
+            "config": {"workload": {"verify": f"secp256k1 ECDSA verify, batch 2^{args.log2n} per GPU",
+                                    "sign": f"secp256k1 ECDSA sign, batch 2^{args.log2n} per GPU",
+                                    "padd": f"secp256k1 batched affine point addition, 2^{args.log2n} pairs per GPU",
+                                    "msm": f"secp256k1 Pippenger MSM, 2^{args.log2n} points per GPU (c = 16)"}[wl],
                        "curve": "secp256k1", "lanes_per_gpu": n, "sharding": f"lane ranges x{world}, no collective",
                        "l2": "inputs larger than L2 (records 161 B/lane x 2^20 = 169 MB > 126 MB)"
                        if wl == "verify" and args.log2n >= 20 else "no L2 flush; kernel is IMAD-bound, records read once"},
