@@ -187,15 +187,13 @@ SLOTS = {
 }
 
 
-def wl_is_msm(w):
-    return w == "msm"
-
-
 def work_per_lane(workload):
     with open(os.path.join(ROOT, "tools", "op_counts.json")) as f:
         counts = json.load(f)["secp256k1"]
     if workload == "padd":   # compress 1 + scatter 2 + chord 3 (one a square) + inversion share
         c = {"mul_special": 5 + 2 / 16, "sqr_special": 1, "safegcd_special": 1 / 16}
+    elif workload == "msm":  # 16 signed windows: one mixed addition (8M + 3S) per window and point
+        c = {"mul_special": 16 * 8.0, "sqr_special": 16 * 3.0}
     else:
         c = counts[workload]
     slots = sum(SLOTS[k] * v for k, v in c.items())

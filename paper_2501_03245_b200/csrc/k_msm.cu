@@ -4,7 +4,7 @@
 // definition, checked against the oracle's sum of pmul_serial results and against
 // the identity  sum_i s_i (t_i G) = (sum_i s_i t_i) G  at full size.
 //
-//   1. k_msm_digits   : every scalar is recoded into 17 signed 16-bit digits
+//   1. k_msm_digits   : every scalar (folded below 2^255) is recoded into 16 signed 16-bit digits
 //                       (same offset recoding as the fixed-base path); one
 //                       (bucket id, point index | sign) pair per non-zero digit.
 //   2. radix sort of the pairs by bucket id (CUB, plumbing only).
@@ -22,7 +22,8 @@
 namespace gecc {
 
 constexpr int MSM_C = 16;                          // window bits
-constexpr int MSM_WINDOWS = 256 / MSM_C + 1;       // 17 (the last one holds the recoding carry)
+constexpr int MSM_WINDOWS = 256 / MSM_C;           // 16: scalars are folded below 2^255 first, so the
+                                                   // signed recoding never carries into a 17th window
 constexpr int MSM_BUCKETS = 1 << (MSM_C - 1);      // 32768 per window
 constexpr uint32_t MSM_NB = MSM_WINDOWS * MSM_BUCKETS;
 constexpr uint32_t MSM_KEY_NONE = 0xFFFFFu;        // sorts behind every real bucket (20-bit keys)
@@ -35,15 +36,19 @@ k_msm_digits(size_t n, const uint32_t* __restrict__ scalars, const uint8_t* __re
     if (i >= n) return;
     fe k = scalar_reduce_once<typename C::Fn>(col_load(scalars, n, i));
     const bool skip = pinf && pinf[i];
-    Recoded<MSM_C> rc = recode_signed<MSM_C>(k);
+    // k >= 2^255: use (n - k) * (-P).  A carry window would otherwise collect ~n/2 points in
+    // ONE bucket (a single thread adding half a million points).
+    const bool flip = (k.w[7] >> 31) != 0;
+    if (flip) k = u256_sub(fe_modulus(typename C::Fn{}), k);
+    Recoded<MSM_C> rc = recode_signed<MSM_C>(k);  // k < 2^255: rc.carry == 0
 #pragma unroll
     for (int w = 0; w < MSM_WINDOWS; ++w) {
-        int d = w == MSM_WINDOWS - 1 ? (int)rc.carry : recoded_digit<MSM_C>(rc, w);
+        int d = recoded_digit<MSM_C>(rc, w);
         uint32_t key = MSM_KEY_NONE, val = 0;
         if (d != 0 && !skip) {
             const uint32_t mag = (uint32_t)(d < 0 ? -d : d);
             key = (uint32_t)w * MSM_BUCKETS + (mag - 1);
-            val = (uint32_t)i | (d < 0 ? 0x80000000u : 0u);
+            val = (uint32_t)i | (((d < 0) != flip) ? 0x80000000u : 0u);
         }
         keys[(size_t)w * n + i] = key;   // window-major: coalesced writes
         vals[(size_t)w * n + i] = val;
