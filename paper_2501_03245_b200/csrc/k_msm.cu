@@ -5,6 +5,7 @@
 // the identity  sum_i s_i (t_i G) = (sum_i s_i t_i) G  at full size.
 //
 //   1. k_msm_digits   : every scalar (folded below 2^255) is recoded into 16 signed 16-bit digits
+//                       plus a rarely non-zero carry digit
 //                       (same offset recoding as the fixed-base path); one
 //                       (bucket id, point index | sign) pair per non-zero digit.
 //   2. radix sort of the pairs by bucket id (CUB, plumbing only).
@@ -22,8 +23,9 @@
 namespace gecc {
 
 constexpr int MSM_C = 16;                          // window bits
-constexpr int MSM_WINDOWS = 256 / MSM_C;           // 16: scalars are folded below 2^255 first, so the
-                                                   // signed recoding never carries into a 17th window
+constexpr int MSM_WINDOWS = 256 / MSM_C + 1;       // 17: scalars are folded below 2^255 first, so the
+                                                   // 17th (recoding-carry) window is hit with probability
+                                                   // ~2^-16 only -- it must exist, but stays almost empty
 constexpr int MSM_BUCKETS = 1 << (MSM_C - 1);      // 32768 per window
 constexpr uint32_t MSM_NB = MSM_WINDOWS * MSM_BUCKETS;
 constexpr uint32_t MSM_KEY_NONE = 0xFFFFFu;        // sorts behind every real bucket (20-bit keys)
@@ -40,10 +42,10 @@ k_msm_digits(size_t n, const uint32_t* __restrict__ scalars, const uint8_t* __re
     // ONE bucket (a single thread adding half a million points).
     const bool flip = (k.w[7] >> 31) != 0;
     if (flip) k = u256_sub(fe_modulus(typename C::Fn{}), k);
-    Recoded<MSM_C> rc = recode_signed<MSM_C>(k);  // k < 2^255: rc.carry == 0
+    Recoded<MSM_C> rc = recode_signed<MSM_C>(k);  // k < 2^255: rc.carry is 1 only for 0x7FFF8... tops
 #pragma unroll
     for (int w = 0; w < MSM_WINDOWS; ++w) {
-        int d = recoded_digit<MSM_C>(rc, w);
+        int d = w == MSM_WINDOWS - 1 ? (int)rc.carry : recoded_digit<MSM_C>(rc, w);
         uint32_t key = MSM_KEY_NONE, val = 0;
         if (d != 0 && !skip) {
             const uint32_t mag = (uint32_t)(d < 0 ? -d : d);

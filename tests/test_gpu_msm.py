@@ -45,6 +45,7 @@ def test_msm_small_vs_oracle(ctxs, cid):
     for i in range(8, 24):
         ks[i] = 5
     ks[30], ks[31] = 77, c.n - 77
+    ks[5], ks[6], ks[7] = (0x7FFF << 240) | (0x9000 << 224), (1 << 255) - 1, 1 << 255  # recoding-carry window
     for a in (0, 1):
         P[a][:, 31] = P[a][:, 30]
     P[2][40] = 1
