@@ -100,9 +100,13 @@ typedef struct sm2b_bench_report {
     uint64_t modeled_cost;
     int equivalence_checked;
 } sm2b_bench_report;
-/* sm2batch.h:102-105.  op: padd|fpmul|upmul|sign|verify; strategy: affine-batch
- * (GPU batch kernels) | jacobian-serial (GPU per-lane Jacobian kernels).  Both
- * are run once and compared before timing (bench.cpp:253-256). */
+/* sm2batch.h:102-105.  op: padd|fpmul|upmul|sign|verify; strategy: affine-batch (the
+ * production kernels) | jacobian-serial (independent per-lane kernels: one mixed
+ * Jacobian add / LSB-first double-and-add, as serial_padd and pmul_serial of the
+ * reference).  Inputs use the reference's seeded recipe and stream tags
+ * (bench.cpp:20-48,139-200); both strategies run once and are compared before timing
+ * (bench.cpp:253-256); wall_seconds is the median of `repeats` CUDA-event timings after
+ * one warm-up; ops are the reference's closed-form counts. */
 sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, size_t n,
                            size_t lanes, uint32_t workers, uint64_t seed, uint32_t repeats,
                            sm2b_bench_report* out);

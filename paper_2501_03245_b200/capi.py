@@ -157,6 +157,22 @@ class Context:
             raise ValueError(f"gecc_microbench rc={rc}")
         return dict(ops_per_clk_per_sm=r.value, seconds=s.value, total_ops=t.value)
 
+    def bench_run(self, op: str, strategy: str, n: int, lanes: int = 0, workers: int = 0, seed: int = 1,
+                  repeats: int = 5):
+        """sm2b_bench_run (sm2batch.h:102-105); returns (status, report dict)."""
+
+        class Report(C.Structure):
+            _fields_ = [("lanes_used", C.c_uint64), ("wall_seconds", C.c_double), ("throughput", C.c_double),
+                        ("ops", C.c_uint64 * 4), ("modeled_cost", C.c_uint64), ("equivalence_checked", C.c_int)]
+
+        rep = Report()
+        rc = self.l.sm2b_bench_run(self.h, op.encode(), strategy.encode(), C.c_size_t(n), C.c_size_t(lanes),
+                                   C.c_uint32(workers), C.c_uint64(seed), C.c_uint32(repeats), C.byref(rep))
+        self._check(rc, "sm2b_bench_run")
+        return rc, dict(lanes_used=rep.lanes_used, wall_seconds=rep.wall_seconds, throughput=rep.throughput,
+                        ops=dict(zip(("modmul", "modadd", "modsub", "modinv"), list(rep.ops))),
+                        modeled_cost=rep.modeled_cost, equivalence_checked=rep.equivalence_checked)
+
     # -- batch layer (host column buffers)
     def batch_invert(self, field: int, a: np.ndarray):
         n = a.shape[1]

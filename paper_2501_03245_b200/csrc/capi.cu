@@ -4,6 +4,7 @@
 // There is no CPU compute path in this file.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -673,9 +674,162 @@ sm2b_status gecc_batch_upmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, c
                       });
 }
 
-// ------------------------------------------------------------------ not yet built
-#define GECC_TODO(ctx) ((ctx) ? fail_msg(ctx, "not implemented in this build") : SM2B_ERROR_INVALID_ARGUMENT)
-sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char*, const char*, size_t, size_t, uint32_t, uint64_t, uint32_t, sm2b_bench_report*) { return GECC_TODO(ctx); }
+// ------------------------------------------------------------------ sm2b_bench_run
+// bench.cpp:114-282 on the GPU: seeded synthetic inputs with the reference's stream tags,
+// both strategies run once and compared before anything is timed, one discarded warm-up,
+// a ledger run (closed forms), then the median of `repeats` timed runs (CUDA events).
+//   affine-batch     = the production kernels (k_batch_padd / k_fpmul / k_upmul / k_sign / k_verify)
+//   jacobian-serial  = independent per-lane kernels (k_padd_jacobian, k_pmul_serial); sign and
+//                      verify have a single GPU implementation, their gate is sign -> verify.
+} // extern "C"
+namespace {
+struct BenchBufs {
+    uint32_t *k, *k2, *px, *py, *tx, *ty, *ax, *ay, *bx, *by;
+    uint8_t *ai, *bi, *dig, *sec, *pub, *sig, *res;
+    int32_t* st;
+};
+}  // namespace
+extern "C" {
+
+sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, size_t n,
+                           size_t lanes, uint32_t workers, uint64_t seed, uint32_t repeats,
+                           sm2b_bench_report* out) {
+    if (!ctx || !op || !strategy || !out) return SM2B_ERROR_INVALID_ARGUMENT;
+    static const char* const ops[] = {"padd", "fpmul", "upmul", "sign", "verify"};
+    int opi = -1;
+    for (int i = 0; i < 5; ++i)
+        if (!strcmp(op, ops[i])) opi = i;
+    const bool batch = !strcmp(strategy, "affine-batch");
+    if (opi < 0 || (!batch && strcmp(strategy, "jacobian-serial")) || n == 0 || repeats == 0)
+        return SM2B_ERROR_INVALID_ARGUMENT;
+    if (seed == 0) seed = 1;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    const size_t cb = Carver::need(32 * n), mb = Carver::need(n);
+    CU(ctx, ctx->scratch.ensure(10 * cb + 2 * mb + 2 * cb + Carver::need(65 * n) + Carver::need(64 * n) +
+                                mb + Carver::need(4 * n)));
+    Carver cv(ctx->scratch.p);
+    BenchBufs b;
+    b.k = cv.take<uint32_t>(8 * n); b.k2 = cv.take<uint32_t>(8 * n);
+    b.px = cv.take<uint32_t>(8 * n); b.py = cv.take<uint32_t>(8 * n);
+    b.tx = cv.take<uint32_t>(8 * n); b.ty = cv.take<uint32_t>(8 * n);
+    b.ax = cv.take<uint32_t>(8 * n); b.ay = cv.take<uint32_t>(8 * n);
+    b.bx = cv.take<uint32_t>(8 * n); b.by = cv.take<uint32_t>(8 * n);
+    b.ai = cv.take<uint8_t>(n); b.bi = cv.take<uint8_t>(n);
+    b.dig = cv.take<uint8_t>(32 * n); b.sec = cv.take<uint8_t>(32 * n);
+    b.pub = cv.take<uint8_t>(65 * n); b.sig = cv.take<uint8_t>(64 * n);
+    b.res = cv.take<uint8_t>(n); b.st = cv.take<int32_t>(n);
+    cudaStream_t s = ctx->stream;
+    const int cv_ = ctx->curve;
+    const uint32_t* gt = ctx->gtab;
+    uint8_t* scratch_inf = b.res;  // infinity flags of generated points (never set for 0 < k < n)
+    // ---- inputs (bench.cpp:139-140,163,167,194-200)
+    if (opi == 0) {
+        CU(ctx, launch_seeded_scalars(cv_, n, seed, 0x10000, b.k, s));
+        CU(ctx, launch_fpmul(cv_, n, b.k, gt, b.px, b.py, scratch_inf, s));
+        CU(ctx, launch_seeded_scalars(cv_, n, seed, 0x20000, b.k, s));
+        CU(ctx, launch_fpmul(cv_, n, b.k, gt, b.tx, b.ty, scratch_inf, s));
+    } else if (opi <= 2) {
+        CU(ctx, launch_seeded_scalars(cv_, n, seed, 0x40000, b.k2, s));
+        CU(ctx, launch_fpmul(cv_, n, b.k2, gt, b.px, b.py, scratch_inf, s));
+        CU(ctx, launch_seeded_scalars(cv_, n, seed, 0x30000, b.k, s));
+    } else {
+        CU(ctx, launch_keygen(cv_, n, seed, 0x50000, gt, b.dig, b.pub, s));  // digests = seeded scalars
+        CU(ctx, launch_keygen(cv_, n, seed, 0x60000, gt, b.sec, b.pub, s));  // key pairs
+        CU(ctx, cudaMemsetAsync(ctx->flags, 0, 4, s));
+        CU(ctx, launch_sign(cv_, n, b.dig, b.sec, seed, 0, gt, b.sig, b.st, ctx->flags, s));
+    }
+    auto run = [&](bool use_batch, uint32_t* ox, uint32_t* oy, uint8_t* oi) -> cudaError_t {
+        switch (opi) {
+            case 0:
+                return use_batch ? launch_batch_padd(cv_, n, b.px, b.py, nullptr, b.tx, b.ty, nullptr, ox, oy, oi, s)
+                                 : launch_padd_jacobian(cv_, n, b.px, b.py, nullptr, b.tx, b.ty, nullptr, ox, oy, oi, s);
+            case 1:
+                return use_batch ? launch_fpmul(cv_, n, b.k, gt, ox, oy, oi, s)
+                                 : launch_pmul_serial(cv_, n, b.k, nullptr, nullptr, nullptr, ox, oy, oi, s);
+            case 2:
+                return use_batch ? launch_upmul(cv_, n, b.k, b.px, b.py, nullptr, ox, oy, oi, s)
+                                 : launch_pmul_serial(cv_, n, b.k, b.px, b.py, nullptr, ox, oy, oi, s);
+            case 3: {
+                cudaError_t e = cudaMemsetAsync(ctx->flags, 0, 4, s);
+                if (e != cudaSuccess) return e;
+                return launch_sign(cv_, n, b.dig, b.sec, seed, 0, gt, b.sig, b.st, ctx->flags, s);
+            }
+            default:
+                return launch_verify(cv_, n, b.dig, b.pub, b.sig, gt, b.res, s);
+        }
+    };
+    // ---- equivalence gate
+    bool agree = true;
+    if (opi <= 2) {
+        CU(ctx, run(true, b.ax, b.ay, b.ai));
+        CU(ctx, run(false, b.bx, b.by, b.bi));
+        std::vector<uint32_t> ha(16 * n), hb(16 * n);
+        std::vector<uint8_t> ia(n), ib(n);
+        CU(ctx, cudaMemcpyAsync(ha.data(), b.ax, 32 * n, cudaMemcpyDeviceToHost, s));
+        CU(ctx, cudaMemcpyAsync(ha.data() + 8 * n, b.ay, 32 * n, cudaMemcpyDeviceToHost, s));
+        CU(ctx, cudaMemcpyAsync(hb.data(), b.bx, 32 * n, cudaMemcpyDeviceToHost, s));
+        CU(ctx, cudaMemcpyAsync(hb.data() + 8 * n, b.by, 32 * n, cudaMemcpyDeviceToHost, s));
+        CU(ctx, cudaMemcpyAsync(ia.data(), b.ai, n, cudaMemcpyDeviceToHost, s));
+        CU(ctx, cudaMemcpyAsync(ib.data(), b.bi, n, cudaMemcpyDeviceToHost, s));
+        CU(ctx, cudaStreamSynchronize(s));
+        agree = ha == hb && ia == ib;
+    } else {
+        CU(ctx, launch_verify(cv_, n, b.dig, b.pub, b.sig, gt, b.res, s));
+        std::vector<uint8_t> hr(n);
+        std::vector<int32_t> hs(n);
+        CU(ctx, cudaMemcpyAsync(hr.data(), b.res, n, cudaMemcpyDeviceToHost, s));
+        CU(ctx, cudaMemcpyAsync(hs.data(), b.st, 4 * n, cudaMemcpyDeviceToHost, s));
+        CU(ctx, cudaStreamSynchronize(s));
+        for (size_t i = 0; i < n; ++i) agree = agree && hr[i] == 1 && hs[i] == 0;
+    }
+    if (!agree) return fail_msg(ctx, "run_bench: strategies disagree, aborting");  // bench.cpp:253-256
+    // ---- warm-up, timed repeats (median)
+    CU(ctx, run(batch, b.ax, b.ay, b.ai));
+    cudaEvent_t e0, e1;
+    CU(ctx, cudaEventCreate(&e0));
+    CU(ctx, cudaEventCreate(&e1));
+    std::vector<float> ms(repeats);
+    for (uint32_t r = 0; r < repeats; ++r) {
+        cudaEventRecord(e0, s);
+        cudaError_t e = run(batch, b.ax, b.ay, b.ai);
+        cudaEventRecord(e1, s);
+        if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+        if (e != cudaSuccess) {
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+            return fail(ctx, "bench run", e);
+        }
+        cudaEventElapsedTime(&ms[r], e0, e1);
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    std::sort(ms.begin(), ms.end());
+    ctx->launches += 8 + repeats;
+    // ---- report: ledger of one run in the reference's closed forms
+    sm2b_ctx tmp_counts_holder;  // only its ledger / lanes / workers fields are used
+    tmp_counts_holder.lanes = (uint32_t)lanes ? (uint32_t)lanes : ctx->lanes;
+    tmp_counts_holder.workers = workers ? workers : ctx->workers;
+    sm2b_ctx* t = &tmp_counts_holder;
+    if (batch) {
+        if (opi == 0) led_padd(t, n);
+        else if (opi == 1) led_fpmul(t, n);
+        else if (opi == 2) led_upmul(t, n);
+        else if (opi == 3) { led_fpmul(t, n); led_invert(t, n); led(t, 2 * n, n, 0, 0); }
+        else { led_invert(t, n); led(t, 2 * n, 0, 0, 0); led_fpmul(t, n); led_upmul(t, n); led_padd(t, n); }
+    } else {  // Jacobian pipeline: no inversions inside; padd = 11 modmul + 6 modsub per lane
+        if (opi == 0) led(t, 11 * n, 0, 6 * n, 0);
+        else led(t, (uint64_t)(256 * 10 + 128 * 16) * n, (uint64_t)256 * 7 * n, (uint64_t)(256 * 4 + 128 * 7) * n, n);
+    }
+    out->lanes_used = eff_lanes(t, n);
+    out->wall_seconds = ms[ms.size() / 2] * 1e-3;
+    out->throughput = out->wall_seconds > 0 ? (double)n / out->wall_seconds : 0.0;
+    out->ops = t->ledger;
+    out->modeled_cost = (t->ledger.modadd + t->ledger.modsub) + 5 * t->ledger.modmul + 500 * t->ledger.modinv;
+    out->equivalence_checked = 1;
+    return SM2B_OK;
+}
+
 sm2b_status gecc_msm_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uint32_t* px,
                          const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
                          uint8_t* oinf) {

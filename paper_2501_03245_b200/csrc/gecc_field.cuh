@@ -337,9 +337,50 @@ GECC_HD fe redc_secp(const F& f, const uint32_t* t) {
     return fe_select(over != 0, s, r);
 }
 
+// SM2 base field (SCA-256), q = 2^256 - 2^224 - 2^96 + 2^64 - 1, q_inv32 == 1: the
+// Montgomery multiplier of every eliminated word is the word itself and
+//   m q = m 2^256 - m 2^224 - m 2^96 + m 2^64 - m
+// is single-word signed contributions, so the whole reduction is additions and
+// subtractions (reference: reduce_sm2_impl, field.cpp:88-128; same two-words-per-pass
+// schedule).  Pass j eliminates t[j], t[j+1] (m0, m1); their combined deltas are
+//   +m0 @ j+2,  +m1 - m0 @ j+3,  -m1 @ j+4,  -m0 @ j+7,  +m0 - m1 @ j+8,  +m1 @ j+9
+// applied as one add chain and one sub chain that run to the top word.  No multiply.
+template <class F>
+GECC_HD fe redc_sm2(const F& f, const uint32_t* tin) {
+    uint32_t t[17];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) t[i] = tin[i];
+    t[16] = 0;
+#pragma unroll
+    for (int j = 0; j < 8; j += 2) {
+        const uint32_t m0 = t[j], m1 = t[j + 1];
+        // positive contributions: +m0 @ j+2, +m1 @ j+3, +m0 @ j+8, +m1 @ j+9
+        t[j + 2] = add_cc(t[j + 2], m0);
+        t[j + 3] = addc_cc(t[j + 3], m1);
+#pragma unroll
+        for (int w = j + 4; w < 17; ++w) {
+            const uint32_t d = (w == j + 8) ? m0 : (w == j + 9) ? m1 : 0u;
+            t[w] = addc_cc(t[w], d);
+        }
+        // negative contributions: -m0 @ j+3, -m1 @ j+4, -m0 @ j+7, -m1 @ j+8
+        t[j + 3] = sub_cc(t[j + 3], m0);
+        t[j + 4] = subc_cc(t[j + 4], m1);
+#pragma unroll
+        for (int w = j + 5; w < 17; ++w) {
+            const uint32_t d = (w == j + 7) ? m0 : (w == j + 8) ? m1 : 0u;
+            t[w] = subc_cc(t[w], d);
+        }
+    }
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.w[i] = t[8 + i];
+    return final_sub(f, r, t[16]);
+}
+
 template <class F>
 GECC_HD fe redc(const F& f, const uint32_t* t) {
     if constexpr (F::kind == KIND_SECP_P) return redc_secp(f, t);
+    else if constexpr (F::kind == KIND_SM2_P) return redc_sm2(f, t);
     else return redc_generic(f, t);
 }
 

@@ -47,6 +47,16 @@ cudaError_t launch_batch_pdbl(int curve, size_t n, const uint32_t* px, const uin
                               cudaStream_t s);
 
 
+cudaError_t launch_seeded_scalars(int curve, size_t n, uint64_t seed, uint64_t tag, uint32_t* out,
+                                  cudaStream_t s);
+cudaError_t launch_padd_jacobian(int curve, size_t n, const uint32_t* px, const uint32_t* py,
+                                 const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty,
+                                 const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
+                                 cudaStream_t s);
+cudaError_t launch_pmul_serial(int curve, size_t n, const uint32_t* k, const uint32_t* px,
+                               const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
+                               uint8_t* oinf, cudaStream_t s);
+
 // MSM: scratch must hold msm_scratch_bytes(n) bytes of device memory
 size_t msm_scratch_bytes(size_t n);
 cudaError_t launch_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px,

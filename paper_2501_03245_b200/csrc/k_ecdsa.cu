@@ -138,6 +138,63 @@ k_upmul(size_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ p
     store_affine<C>(var_base_mul<C>(col_load(k, n, i), qt), ox, oy, oinf, n, i);
 }
 
+// ---- sm2b_bench_run support (bench.cpp:20-62): seeded inputs and the "jacobian-serial"
+// strategy as independent per-lane kernels
+template <class C>
+__global__ void __launch_bounds__(256)
+k_seeded_scalars(size_t n, uint64_t seed, uint64_t tag, uint32_t* __restrict__ out) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    col_store(out, n, i, nonce_scalar<typename C::Fn>(seed, tag + i, 0));  // bench.cpp:20-28
+}
+
+// serial_padd (bench.cpp:50-60): one mixed Jacobian addition per lane, normalised to affine
+template <class C>
+__global__ void __launch_bounds__(SIGN_THREADS)
+k_padd_jacobian(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
+                const uint8_t* __restrict__ pinf, const uint32_t* __restrict__ tx,
+                const uint32_t* __restrict__ ty, const uint8_t* __restrict__ tinf,
+                uint32_t* __restrict__ ox, uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf) {
+    const size_t i = blockIdx.x * (size_t)SIGN_THREADS + threadIdx.x;
+    if (i >= n) return;
+    const typename C::Fp f{};
+    jac acc = jac_infinity<C>();
+    if (!(pinf && pinf[i])) {
+        acc.X = col_load(px, n, i);
+        acc.Y = col_load(py, n, i);
+        acc.Z = fe_one(f);
+    }
+    if (!(tinf && tinf[i])) acc = jac_madd<C>(acc, aff{col_load(tx, n, i), col_load(ty, n, i)});
+    store_affine<C>(acc, ox, oy, oinf, n, i);
+}
+
+// pmul_serial (curve.cpp:176-185): LSB-first double-and-add, no tables, no recoding --
+// deliberately a different algorithm from k_fpmul / k_upmul so that comparing them is a
+// real equivalence check.  px == nullptr multiplies the generator.
+template <class C>
+__global__ void __launch_bounds__(SIGN_THREADS)
+k_pmul_serial(size_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ px,
+              const uint32_t* __restrict__ py, const uint8_t* __restrict__ pinf,
+              uint32_t* __restrict__ ox, uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf) {
+    const size_t i = blockIdx.x * (size_t)SIGN_THREADS + threadIdx.x;
+    if (i >= n) return;
+    const typename C::Fp f{};
+    fe s = col_load(k, n, i);
+    jac acc = jac_infinity<C>(), run = jac_infinity<C>();
+    if (!px) {
+        aff g = curve_g<C>();
+        run.X = g.x; run.Y = g.y; run.Z = fe_one(f);
+    } else if (!(pinf && pinf[i])) {
+        run.X = col_load(px, n, i); run.Y = col_load(py, n, i); run.Z = fe_one(f);
+    }
+#pragma unroll 1
+    for (int b = 0; b < 256; ++b) {
+        if ((s.w[b >> 5] >> (b & 31)) & 1u) acc = jac_add<C>(acc, run);
+        run = jac_dbl<C>(run);
+    }
+    store_affine<C>(acc, ox, oy, oinf, n, i);
+}
+
 // ---------------------------------------------------------------- launchers
 constexpr size_t LANE_TABLE_SMEM = (size_t)VERIFY_THREADS * 8 * 16 * sizeof(uint32_t);
 
@@ -219,6 +276,37 @@ cudaError_t launch_upmul(int curve, size_t n, const uint32_t* k, const uint32_t*
     GECC_BY_CURVE(curve,
         (k_upmul<SecpCurve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, k, px, py, pinf, ox, oy, oinf)),
         (k_upmul<Sm2Curve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, k, px, py, pinf, ox, oy, oinf)));
+    return cudaGetLastError();
+}
+
+
+cudaError_t launch_seeded_scalars(int curve, size_t n, uint64_t seed, uint64_t tag, uint32_t* out,
+                                  cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int b = blocks_for(n, 256);
+    GECC_BY_CURVE(curve, (k_seeded_scalars<SecpCurve><<<b, 256, 0, s>>>(n, seed, tag, out)),
+                  (k_seeded_scalars<Sm2Curve><<<b, 256, 0, s>>>(n, seed, tag, out)));
+    return cudaGetLastError();
+}
+cudaError_t launch_padd_jacobian(int curve, size_t n, const uint32_t* px, const uint32_t* py,
+                                 const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty,
+                                 const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
+                                 cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int b = blocks_for(n, SIGN_THREADS);
+    GECC_BY_CURVE(curve,
+        (k_padd_jacobian<SecpCurve><<<b, SIGN_THREADS, 0, s>>>(n, px, py, pinf, tx, ty, tinf, ox, oy, oinf)),
+        (k_padd_jacobian<Sm2Curve><<<b, SIGN_THREADS, 0, s>>>(n, px, py, pinf, tx, ty, tinf, ox, oy, oinf)));
+    return cudaGetLastError();
+}
+cudaError_t launch_pmul_serial(int curve, size_t n, const uint32_t* k, const uint32_t* px,
+                               const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
+                               uint8_t* oinf, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const int b = blocks_for(n, SIGN_THREADS);
+    GECC_BY_CURVE(curve,
+        (k_pmul_serial<SecpCurve><<<b, SIGN_THREADS, 0, s>>>(n, k, px, py, pinf, ox, oy, oinf)),
+        (k_pmul_serial<Sm2Curve><<<b, SIGN_THREADS, 0, s>>>(n, k, px, py, pinf, ox, oy, oinf)));
     return cudaGetLastError();
 }
 

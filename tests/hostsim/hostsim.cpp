@@ -214,3 +214,23 @@ extern "C" void hs_op_counts(unsigned long long* out, int reset) {
 #endif
 }
 extern "C" int hs_window_bits(void) { return HS_WG; }
+
+// raw Montgomery reduction of 16-limb inputs (c < q * 2^256), field ids as hs_field_op
+template <class F>
+static int redc_t(const F& f, size_t n, const uint32_t* c16, uint32_t* out) {
+    for (size_t i = 0; i < n; ++i) {
+        uint32_t t[16];
+        for (int k = 0; k < 16; ++k) t[k] = c16[k * n + i];
+        col_set(out, n, i, redc(f, t));
+    }
+    return 0;
+}
+extern "C" int hs_redc(int field, size_t n, const uint32_t* c16, uint32_t* out) {
+    switch (field) {
+        case 0: return redc_t(SecpP{}, n, c16, out);
+        case 1: return redc_t(SecpN{}, n, c16, out);
+        case 2: return redc_t(Sm2P{}, n, c16, out);
+        case 3: return redc_t(Sm2N{}, n, c16, out);
+    }
+    return 1;
+}

@@ -79,3 +79,17 @@ def keygen(curve, seed, n, lane_base=0):
     pub = (C.c_uint8 * max(1, 65 * n))()
     assert lib().hs_keygen(curve, C.c_size_t(n), C.c_uint64(seed), C.c_uint64(lane_base), sec, pub) == 0
     return bytes(sec)[:32 * n], bytes(pub)[:65 * n]
+
+
+def redc(curve, which, c16):
+    n = c16.shape[1]
+    out = np.zeros((8, n), np.uint32)
+    assert lib().hs_redc(FIELD_IDS[(curve, which)], C.c_size_t(n), _p(c16), _p(out)) == 0
+    return out
+
+
+def glv_split(k):
+    n = k.shape[1]
+    m1, m2, sg = np.zeros((8, n), np.uint32), np.zeros((8, n), np.uint32), np.zeros(2 * n, np.uint8)
+    assert lib().hs_glv_split(C.c_size_t(n), _p(k), _p(m1), _p(m2), _p(sg)) == 0
+    return m1, m2, sg

@@ -145,3 +145,26 @@ def test_ecdsa_roundtrip_large(ctxs):
     for i in rs.choice(n, 48, replace=False):
         i = int(i)
         assert O.ecdsa_sign(1, dig[32 * i:32 * i + 32], sec[32 * i:32 * i + 32], 77, lane_base=i)[1] == sig[64 * i:64 * i + 64]
+
+
+def test_bench_run_gpu(ctxs):
+    """sm2b_bench_run: both strategies compared before timing (bench.cpp:253-256), ledger in the
+    reference's closed forms (acceptance.cpp criteria 3 and 7), argument errors (capi.cpp:266-273)."""
+    with gecc.Context(reference_compat=True, workers=1) as sm2:
+        n = 512
+        for op in ("padd", "fpmul", "upmul", "sign", "verify"):
+            for strategy in ("affine-batch", "jacobian-serial"):
+                rc, rep = sm2.bench_run(op, strategy, n, lanes=8, seed=1, repeats=3)
+                assert rc == 0 and rep["equivalence_checked"] == 1, (op, strategy)
+                assert rep["wall_seconds"] > 0 and rep["throughput"] > 0 and rep["lanes_used"] == 8
+        rc, rep = sm2.bench_run("padd", "affine-batch", 4096, lanes=16, repeats=3)
+        assert (rep["ops"]["modmul"], rep["ops"]["modsub"], rep["ops"]["modinv"]) == (6 * 4096 - 3, 6 * 4096, 1)
+        assert rep["modeled_cost"] == 6 * 4096 + 5 * (6 * 4096 - 3) + 500
+        rc, rep = sm2.bench_run("upmul", "affine-batch", 32, lanes=8, repeats=1)
+        assert rep["ops"] == dict(modmul=120064, modadd=40960, modsub=90112, modinv=256)  # acceptance.cpp crit. 7
+        assert sm2.bench_run("nope", "affine-batch", 8)[0] == 1
+        assert sm2.bench_run("padd", "quantum", 8)[0] == 1
+        assert sm2.bench_run("padd", "affine-batch", 0)[0] == 1
+        assert sm2.bench_run("padd", "affine-batch", 8, repeats=0)[0] == 1
+    rc, rep = ctxs[1].bench_run("verify", "affine-batch", 1 << 14, repeats=3)
+    assert rc == 0 and rep["equivalence_checked"] == 1

@@ -14,7 +14,7 @@ import pytest
 from oracle import coracle as O
 from oracle import pyec as E
 from tests.hostsim import hostsim as H
-from tests.util import CURVE_IDS, cols_hex, golden, hex_cols, pts_from_hex, pts_to_hex
+from tests.util import CURVE_IDS, cols_hex, golden, hex_cols, pts_from_hex, pts_to_hex, wide_cols
 
 FIELD, BATCH, ECDSA = golden("field"), golden("batch"), golden("ecdsa")
 CURVES = ["sm2", "secp256k1"]
@@ -28,6 +28,44 @@ def test_hostsim_field_golden(key):
     A, B = hex_cols(ent["a"]), hex_cols(ent["b"])
     for op in ("mont_mul", "mod_add", "mod_sub", "to_mont", "from_mont", "mod_inv"):
         assert cols_hex(H.field_op(cid, which, op, A, B)) == ent[op], op
+
+
+@pytest.mark.parametrize("key", [k for k in FIELD if not k.startswith("_")])
+def test_hostsim_reduce_edges(key):
+    """512-bit reduce edge values of test_field.cpp:136-164 through every reduction route
+    (secp256k1 word-serial, SM2 add/sub-only, generic two-product REDC)."""
+    ent = FIELD[key]
+    cid = CURVE_IDS[key.split(".")[0]]
+    which = 0 if key.endswith(".p") else 1
+    q = int(ent["q"], 16)
+    rng = random.Random(77)
+    extra = [format(rng.randrange(q << 256), "0128x") for _ in range(3000)]
+    c16 = wide_cols(ent["reduce_in"] + extra)
+    got = cols_hex(H.redc(cid, which, c16))
+    assert got[:len(ent["reduce_in"])] == ent["reduce_generic"]
+    assert got == cols_hex(O.mont_reduce(cid, which, c16, False))
+
+
+def test_hostsim_inverse_and_glv():
+    """safegcd inversion vs the oracle's Fermat value; GLV split k = k1 + k2 lambda mod n."""
+    rng = random.Random(8)
+    for cid in (0, 1):
+        for which in (0, 1):
+            q = O.field_params(cid, which)["q"]
+            vals = [0, 1, 2, q - 1, q - 2, (q + 1) // 2, (1 << 128) - 1] + [rng.randrange(q) for _ in range(1500)]
+            a = O.ints_to_cols(vals)
+            assert (H.field_op(cid, which, "inv_safegcd", a) == O.field_op(cid, which, "mod_inv", a)).all()
+            plain = O.cols_to_ints(H.field_op(cid, which, "inv_plain", a))
+            assert all(g == (pow(v, -1, q) if v else 0) for g, v in zip(plain, vals))
+    n = E.SECP256K1.n
+    lam = 0x5363AD4CC05C30E0A5261C028812645A122E22EA20816678DF02967C1B23BD72
+    ks = [0, 1, 2, n - 1, n - 2, lam, n - lam, (n - 1) // 2, 1 << 255] + [rng.randrange(n) for _ in range(5000)]
+    m1, m2, sg = H.glv_split(O.ints_to_cols(ks))
+    a, b = O.cols_to_ints(m1), O.cols_to_ints(m2)
+    for i, k in enumerate(ks):
+        k1 = -a[i] if sg[2 * i] else a[i]
+        k2 = -b[i] if sg[2 * i + 1] else b[i]
+        assert (k1 + k2 * lam - k) % n == 0 and a[i] < 1 << 129 and b[i] < 1 << 129
 
 
 @pytest.mark.parametrize("cid", [0, 1])
