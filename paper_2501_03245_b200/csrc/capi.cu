@@ -46,6 +46,7 @@ struct sm2b_ctx {
     std::mutex mu;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;  // copy engines of the pipelined host API
     sm2b_op_counts ledger{0, 0, 0, 0};
     uint64_t launches = 0;
     std::string last_error;
@@ -119,7 +120,9 @@ sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device) {
     DeviceGuard g(device);
     cudaDeviceProp prop;
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete ctx;
         return nullptr;
     }
@@ -163,6 +166,8 @@ void sm2b_ctx_free(sm2b_ctx* ctx) {
         if (ctx->gtab) cudaFree(ctx->gtab);
         if (ctx->flags) cudaFree(ctx->flags);
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+        if (ctx->h2d_stream) cudaStreamDestroy(ctx->h2d_stream);
+        if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
     }
     delete ctx;
 }
@@ -300,6 +305,45 @@ void led_upmul(sm2b_ctx* c, uint64_t n) {
 }
 }  // namespace
 
+// ------------------------------------------------------------------ host-API pipeline
+// The byte-record entry points split a large batch into chunks and run three streams:
+// H2D of chunk c+1, the kernel of chunk c and D2H of chunk c-1 overlap (events order
+// them).  With pinned caller buffers the copies are truly asynchronous; with pageable
+// buffers CUDA stages them and the result is the same, only less overlapped.
+} // extern "C"
+namespace {
+constexpr size_t PIPE_MIN_CHUNK = (size_t)1 << 14;
+constexpr int PIPE_MAX_CHUNKS = 16;
+
+struct Chunks {
+    size_t count, size;
+    int n;
+    explicit Chunks(size_t total) : count(total) {
+        n = (int)(total / PIPE_MIN_CHUNK);
+        if (n < 1) n = 1;
+        if (n > PIPE_MAX_CHUNKS) n = PIPE_MAX_CHUNKS;
+        size = (total + n - 1) / n;
+        n = (int)((total + size - 1) / size);
+    }
+    size_t begin(int c) const { return (size_t)c * size; }
+    size_t len(int c) const { return begin(c) + size <= count ? size : count - begin(c); }
+};
+
+struct EventPool {  // events of one pipelined call; destroyed at scope exit
+    std::vector<cudaEvent_t> ev;
+    cudaEvent_t get() {
+        cudaEvent_t e = nullptr;
+        cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        ev.push_back(e);
+        return e;
+    }
+    ~EventPool() {
+        for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    }
+};
+}  // namespace
+extern "C" {
+
 // ------------------------------------------------------------------ protocol layer
 sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
                             const uint8_t* publics, const uint8_t* signatures,
@@ -324,27 +368,41 @@ sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
     if (!ctx || (count > 0 && (!digests || !publics || !signatures || !results)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     if (count == 0) return SM2B_OK;
-    uint8_t *dd, *dp, *ds, *dr;
-    {
-        std::lock_guard<std::mutex> lk(ctx->mu);
-        DeviceGuard g(ctx->device);
-        CU(ctx, ctx->in.ensure(Carver::need(32 * count) + Carver::need(65 * count) +
-                               Carver::need(64 * count)));
-        CU(ctx, ctx->out.ensure(Carver::need(count)));
-        Carver ci(ctx->in.p);
-        dd = ci.take<uint8_t>(32 * count);
-        dp = ci.take<uint8_t>(65 * count);
-        ds = ci.take<uint8_t>(64 * count);
-        dr = (uint8_t*)ctx->out.p;
-        CU(ctx, cudaMemcpyAsync(dd, digests, 32 * count, cudaMemcpyHostToDevice, ctx->stream));
-        CU(ctx, cudaMemcpyAsync(dp, publics, 65 * count, cudaMemcpyHostToDevice, ctx->stream));
-        CU(ctx, cudaMemcpyAsync(ds, signatures, 64 * count, cudaMemcpyHostToDevice, ctx->stream));
-    }
-    sm2b_status st = gecc_verify_dev(ctx, count, dd, dp, ds, dr);
-    if (st != SM2B_OK) return st;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
-    CU(ctx, cudaMemcpyAsync(results, dr, count, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, ctx->in.ensure(Carver::need(32 * count) + Carver::need(65 * count) + Carver::need(64 * count)));
+    CU(ctx, ctx->out.ensure(Carver::need(count)));
+    Carver ci(ctx->in.p);
+    uint8_t* dd = ci.take<uint8_t>(32 * count);
+    uint8_t* dp = ci.take<uint8_t>(65 * count);
+    uint8_t* ds = ci.take<uint8_t>(64 * count);
+    uint8_t* dr = (uint8_t*)ctx->out.p;
+    const Chunks ch(count);
+    EventPool pool;
+    // the arenas may still be in use by earlier work on the compute stream
+    cudaEvent_t idle = pool.get();
+    CU(ctx, cudaEventRecord(idle, ctx->stream));
+    CU(ctx, cudaStreamWaitEvent(ctx->h2d_stream, idle, 0));
+    for (int c = 0; c < ch.n; ++c) {
+        const size_t b = ch.begin(c), m = ch.len(c);
+        CU(ctx, cudaMemcpyAsync(dd + 32 * b, digests + 32 * b, 32 * m, cudaMemcpyHostToDevice, ctx->h2d_stream));
+        CU(ctx, cudaMemcpyAsync(dp + 65 * b, publics + 65 * b, 65 * m, cudaMemcpyHostToDevice, ctx->h2d_stream));
+        CU(ctx, cudaMemcpyAsync(ds + 64 * b, signatures + 64 * b, 64 * m, cudaMemcpyHostToDevice, ctx->h2d_stream));
+        cudaEvent_t up = pool.get(), done = pool.get();
+        CU(ctx, cudaEventRecord(up, ctx->h2d_stream));
+        CU(ctx, cudaStreamWaitEvent(ctx->stream, up, 0));
+        CU(ctx, launch_verify(ctx->curve, m, dd + 32 * b, dp + 65 * b, ds + 64 * b, ctx->gtab, dr + b, ctx->stream));
+        CU(ctx, cudaEventRecord(done, ctx->stream));
+        CU(ctx, cudaStreamWaitEvent(ctx->d2h_stream, done, 0));
+        CU(ctx, cudaMemcpyAsync(results + b, dr + b, m, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    }
+    ctx->launches += ch.n;
+    led_invert(ctx, count);
+    led(ctx, 2 * count, 0, 0, 0);
+    led_fpmul(ctx, count);
+    led_upmul(ctx, count);
+    led_padd(ctx, count);
+    CU(ctx, cudaStreamSynchronize(ctx->d2h_stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     return SM2B_OK;
 }
@@ -398,36 +456,51 @@ sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const
         return SM2B_ERROR_INVALID_ARGUMENT;
     if (count == 0) return SM2B_OK;
     if (nonce_seed == 0) nonce_seed = system_seed();
-    uint8_t *dd, *dsec, *dsig;
-    int32_t* dst;
-    {
-        std::lock_guard<std::mutex> lk(ctx->mu);
-        DeviceGuard g(ctx->device);
-        CU(ctx, ctx->in.ensure(2 * Carver::need(32 * count)));
-        CU(ctx, ctx->out.ensure(Carver::need(64 * count) + Carver::need(4 * count)));
-        Carver ci(ctx->in.p), co(ctx->out.p);
-        dd = ci.take<uint8_t>(32 * count);
-        dsec = ci.take<uint8_t>(32 * count);
-        dsig = co.take<uint8_t>(64 * count);
-        dst = co.take<int32_t>(count);
-        CU(ctx, cudaMemcpyAsync(dd, digests, 32 * count, cudaMemcpyHostToDevice, ctx->stream));
-        CU(ctx, cudaMemcpyAsync(dsec, secrets, 32 * count, cudaMemcpyHostToDevice, ctx->stream));
-    }
-    sm2b_status st = gecc_sign_dev(ctx, count, dd, dsec, nonce_seed, lane_base, dsig, dst);
-    if (st != SM2B_OK) return st;
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    DeviceGuard g(ctx->device);
+    CU(ctx, ctx->in.ensure(2 * Carver::need(32 * count)));
+    CU(ctx, ctx->out.ensure(Carver::need(64 * count) + Carver::need(4 * count)));
+    Carver ci(ctx->in.p), co(ctx->out.p);
+    uint8_t* dd = ci.take<uint8_t>(32 * count);
+    uint8_t* dsec = ci.take<uint8_t>(32 * count);
+    uint8_t* dsig = co.take<uint8_t>(64 * count);
+    int32_t* dst = co.take<int32_t>(count);
     std::vector<int32_t> hst(count);
-    uint32_t flag = 0;
-    {
-        std::lock_guard<std::mutex> lk(ctx->mu);
-        DeviceGuard g(ctx->device);
-        CU(ctx, cudaMemcpyAsync(&flag, ctx->flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
-        CU(ctx, cudaMemcpyAsync(hst.data(), dst, 4 * count, cudaMemcpyDeviceToHost, ctx->stream));
-        CU(ctx, cudaStreamSynchronize(ctx->stream));
-        // a zero or oversize secret fails the whole call before any output (capi.cpp:181-184)
-        if (flag) return SM2B_ERROR_MALFORMED_INPUT;
-        CU(ctx, cudaMemcpyAsync(signatures, dsig, 64 * count, cudaMemcpyDeviceToHost, ctx->stream));
-        CU(ctx, cudaStreamSynchronize(ctx->stream));
+    const Chunks ch(count);
+    EventPool pool;
+    cudaEvent_t idle = pool.get();
+    CU(ctx, cudaEventRecord(idle, ctx->stream));
+    CU(ctx, cudaStreamWaitEvent(ctx->h2d_stream, idle, 0));
+    CU(ctx, cudaMemsetAsync(ctx->flags, 0, 4, ctx->h2d_stream));
+    // A zero or oversize secret must fail the whole call before any output is written
+    // (capi.cpp:181-184), so signatures are only copied out after every chunk's kernel has
+    // run and the flag is known; the uploads and kernels still overlap chunk by chunk.
+    for (int c = 0; c < ch.n; ++c) {
+        const size_t b = ch.begin(c), m = ch.len(c);
+        CU(ctx, cudaMemcpyAsync(dsec + 32 * b, secrets + 32 * b, 32 * m, cudaMemcpyHostToDevice, ctx->h2d_stream));
+        CU(ctx, cudaMemcpyAsync(dd + 32 * b, digests + 32 * b, 32 * m, cudaMemcpyHostToDevice, ctx->h2d_stream));
+        cudaEvent_t up = pool.get();
+        CU(ctx, cudaEventRecord(up, ctx->h2d_stream));
+        CU(ctx, cudaStreamWaitEvent(ctx->stream, up, 0));
+        CU(ctx, launch_sign(ctx->curve, m, dd + 32 * b, dsec + 32 * b, nonce_seed, lane_base + b, ctx->gtab,
+                            dsig + 64 * b, dst + b, ctx->flags, ctx->stream));
     }
+    ctx->launches += ch.n;
+    led_fpmul(ctx, count);
+    led_invert(ctx, count);
+    led(ctx, 2 * count, count, 0, 0);
+    uint32_t flag = 0;
+    CU(ctx, cudaMemcpyAsync(&flag, ctx->flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(hst.data(), dst, 4 * count, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    if (flag) return SM2B_ERROR_MALFORMED_INPUT;
+    // two copy streams keep the D2H engine busy with large transfers
+    const size_t half = count / 2;
+    CU(ctx, cudaMemcpyAsync(signatures, dsig, 64 * half, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    CU(ctx, cudaMemcpyAsync(signatures + 64 * half, dsig + 64 * half, 64 * (count - half), cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    CU(ctx, cudaStreamSynchronize(ctx->d2h_stream));
+    CU(ctx, cudaStreamSynchronize(ctx->stream));
     return report_lanes(hst.data(), count, lane_status);
 }
 

@@ -2,6 +2,9 @@
 // processed and re-encoded on the GPU, nothing but the records touches HBM
 // (reference path: capi.cpp:145-261 host loops + protocol.cpp:106-263, which
 // re-reads all point state from memory for each of 256 bit steps).
+#include <cstdlib>
+#include <cstring>
+
 #include "gecc_ecdsa.cuh"
 #include "gecc_host.h"
 
@@ -10,16 +13,18 @@ namespace gecc {
 constexpr int VERIFY_THREADS = 128;  // x 512 B of lane table = 64 KiB shared memory per block
 constexpr int SIGN_THREADS = 128;
 
-template <class C>
-__global__ void __launch_bounds__(VERIFY_THREADS, 3)
+// THREADS x BLOCKS_PER_SM is the occupancy knob: the lane tables need 512 B of shared
+// memory per lane, so at most 454 lanes (14 warps) fit an SM whatever the block shape.
+template <class C, int THREADS, int BLOCKS_PER_SM>
+__global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM)
 k_verify(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ pub,
          const uint8_t* __restrict__ sig, const uint32_t* __restrict__ gtab,
          uint8_t* __restrict__ res) {
     extern __shared__ uint32_t lane_tables[];
-    const size_t i = blockIdx.x * (size_t)VERIFY_THREADS + threadIdx.x;
+    const size_t i = blockIdx.x * (size_t)THREADS + threadIdx.x;
     if (i >= n) return;
     GTable<GECC_WG> gt{gtab};
-    LaneTable qt{lane_tables + threadIdx.x, VERIFY_THREADS};
+    LaneTable qt{lane_tables + threadIdx.x, THREADS};
     res[i] = verify_lane<C, GECC_WG>(dig + 32 * i, pub + 65 * i, sig + 64 * i, gt, qt);
 }
 
@@ -211,16 +216,30 @@ static int blocks_for(size_t n, int threads) { return (int)((n + threads - 1) / 
         else { EXPR_SM2; }                        \
     } while (0)
 
+template <class C, int THREADS, int BLOCKS_PER_SM>
+static cudaError_t launch_verify_t(size_t n, const uint8_t* dig, const uint8_t* pub, const uint8_t* sig,
+                                   const uint32_t* gtab, uint8_t* res, cudaStream_t s) {
+    const size_t smem = (size_t)THREADS * 8 * 16 * sizeof(uint32_t);
+    cudaError_t e = cudaFuncSetAttribute(k_verify<C, THREADS, BLOCKS_PER_SM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    k_verify<C, THREADS, BLOCKS_PER_SM><<<blocks_for(n, THREADS), THREADS, smem, s>>>(n, dig, pub, sig, gtab, res);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t* pub,
                           const uint8_t* sig, const uint32_t* gtab, uint8_t* res, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    cudaError_t e = curve == CURVE_SECP ? opt_in_smem(k_verify<SecpCurve>) : opt_in_smem(k_verify<Sm2Curve>);
-    if (e != cudaSuccess) return e;
-    const int b = blocks_for(n, VERIFY_THREADS);
-    GECC_BY_CURVE(curve,
-        (k_verify<SecpCurve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, dig, pub, sig, gtab, res)),
-        (k_verify<Sm2Curve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, dig, pub, sig, gtab, res)));
-    return cudaGetLastError();
+    // GECC_VERIFY_SHAPE=128x3 selects the alternative launch shape (tuning experiments only)
+    static const bool wide = [] {
+        const char* v = getenv("GECC_VERIFY_SHAPE");
+        return v && !strcmp(v, "128x3");
+    }();
+    if (curve == CURVE_SECP)
+        return wide ? launch_verify_t<SecpCurve, 128, 3>(n, dig, pub, sig, gtab, res, s)
+                    : launch_verify_t<SecpCurve, 64, 7>(n, dig, pub, sig, gtab, res, s);
+    return wide ? launch_verify_t<Sm2Curve, 128, 3>(n, dig, pub, sig, gtab, res, s)
+                : launch_verify_t<Sm2Curve, 64, 7>(n, dig, pub, sig, gtab, res, s);
 }
 
 cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed,
