@@ -51,7 +51,8 @@ struct sm2b_ctx {
     uint64_t launches = 0;
     std::string last_error;
     DevBuf in, out, scratch;
-    uint32_t* gtab = nullptr;   // fixed-base table, built on the GPU at creation
+    uint32_t* gtab = nullptr;   // fixed-base table (Montgomery form), built on the GPU at creation
+    uint32_t* gtab_rec = nullptr;  // table of the byte-record kernels (== gtab on SM2, plain form on secp256k1)
     uint32_t* flags = nullptr;  // device word: malformed-call flag of sign / ecdh
 };
 
@@ -133,8 +134,12 @@ sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device) {
     bool ok = cudaMalloc(&ctx->gtab, gtable_words() * 4) == cudaSuccess &&
               cudaMalloc(&ctx->flags, 256) == cudaSuccess &&
               cudaMalloc(&bases, 64 * 16 * 4 * 8) == cudaSuccess &&
-              build_gtable(ctx->curve, ctx->gtab, bases, ctx->stream) == cudaSuccess &&
-              cudaStreamSynchronize(ctx->stream) == cudaSuccess;
+              build_gtable(ctx->curve, false, ctx->gtab, bases, ctx->stream) == cudaSuccess;
+    ctx->gtab_rec = ctx->gtab;
+    if (ok && ctx->curve == CURVE_SECP)
+        ok = cudaMalloc(&ctx->gtab_rec, gtable_words() * 4) == cudaSuccess &&
+             build_gtable(ctx->curve, true, ctx->gtab_rec, bases, ctx->stream) == cudaSuccess;
+    ok = ok && cudaStreamSynchronize(ctx->stream) == cudaSuccess;
     if (bases) cudaFree(bases);
     if (!ok) {
         fprintf(stderr, "gecc_b200: building the fixed-base table failed: %s\n",
@@ -163,6 +168,7 @@ void sm2b_ctx_free(sm2b_ctx* ctx) {
         ctx->in.release();
         ctx->out.release();
         ctx->scratch.release();
+        if (ctx->gtab_rec && ctx->gtab_rec != ctx->gtab) cudaFree(ctx->gtab_rec);
         if (ctx->gtab) cudaFree(ctx->gtab);
         if (ctx->flags) cudaFree(ctx->flags);
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -312,8 +318,8 @@ void led_upmul(sm2b_ctx* c, uint64_t n) {
 // buffers CUDA stages them and the result is the same, only less overlapped.
 } // extern "C"
 namespace {
-constexpr size_t PIPE_MIN_CHUNK = (size_t)1 << 14;
-constexpr int PIPE_MAX_CHUNKS = 16;
+constexpr size_t PIPE_MIN_CHUNK = (size_t)1 << 17;
+constexpr int PIPE_MAX_CHUNKS = 4;
 
 struct Chunks {
     size_t count, size;
@@ -352,7 +358,7 @@ sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
         return SM2B_ERROR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
-    CU(ctx, launch_verify(ctx->curve, count, digests, publics, signatures, ctx->gtab, results,
+    CU(ctx, launch_verify(ctx->curve, count, digests, publics, signatures, ctx->gtab_rec, results,
                           ctx->stream));
     ctx->launches += count ? 1 : 0;
     led_invert(ctx, count);
@@ -391,7 +397,7 @@ sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
         cudaEvent_t up = pool.get(), done = pool.get();
         CU(ctx, cudaEventRecord(up, ctx->h2d_stream));
         CU(ctx, cudaStreamWaitEvent(ctx->stream, up, 0));
-        CU(ctx, launch_verify(ctx->curve, m, dd + 32 * b, dp + 65 * b, ds + 64 * b, ctx->gtab, dr + b, ctx->stream));
+        CU(ctx, launch_verify(ctx->curve, m, dd + 32 * b, dp + 65 * b, ds + 64 * b, ctx->gtab_rec, dr + b, ctx->stream));
         CU(ctx, cudaEventRecord(done, ctx->stream));
         CU(ctx, cudaStreamWaitEvent(ctx->d2h_stream, done, 0));
         CU(ctx, cudaMemcpyAsync(results + b, dr + b, m, cudaMemcpyDeviceToHost, ctx->d2h_stream));
@@ -416,7 +422,7 @@ sm2b_status gecc_sign_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
     CU(ctx, cudaMemsetAsync(ctx->flags, 0, 4, ctx->stream));
-    CU(ctx, launch_sign(ctx->curve, count, digests, secrets, nonce_seed, lane_base, ctx->gtab,
+    CU(ctx, launch_sign(ctx->curve, count, digests, secrets, nonce_seed, lane_base, ctx->gtab_rec,
                         signatures, lane_status, ctx->flags, ctx->stream));
     ctx->launches += count ? 1 : 0;
     led_fpmul(ctx, count);
@@ -465,7 +471,6 @@ sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const
     uint8_t* dsec = ci.take<uint8_t>(32 * count);
     uint8_t* dsig = co.take<uint8_t>(64 * count);
     int32_t* dst = co.take<int32_t>(count);
-    std::vector<int32_t> hst(count);
     const Chunks ch(count);
     EventPool pool;
     cudaEvent_t idle = pool.get();
@@ -482,7 +487,7 @@ sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const
         cudaEvent_t up = pool.get();
         CU(ctx, cudaEventRecord(up, ctx->h2d_stream));
         CU(ctx, cudaStreamWaitEvent(ctx->stream, up, 0));
-        CU(ctx, launch_sign(ctx->curve, m, dd + 32 * b, dsec + 32 * b, nonce_seed, lane_base + b, ctx->gtab,
+        CU(ctx, launch_sign(ctx->curve, m, dd + 32 * b, dsec + 32 * b, nonce_seed, lane_base + b, ctx->gtab_rec,
                             dsig + 64 * b, dst + b, ctx->flags, ctx->stream));
     }
     ctx->launches += ch.n;
@@ -491,17 +496,25 @@ sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const
     led(ctx, 2 * count, count, 0, 0);
     uint32_t flag = 0;
     CU(ctx, cudaMemcpyAsync(&flag, ctx->flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaMemcpyAsync(hst.data(), dst, 4 * count, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     if (flag) return SM2B_ERROR_MALFORMED_INPUT;
-    // two copy streams keep the D2H engine busy with large transfers
+    // two copy streams keep the D2H engine busy with large transfers; per-lane statuses go
+    // straight into the caller's array (no host-side pass over the lanes)
     const size_t half = count / 2;
+    std::vector<int32_t> hst;
+    int32_t* st_dst = lane_status;
+    if (!st_dst) {
+        hst.resize(count);
+        st_dst = hst.data();
+    }
     CU(ctx, cudaMemcpyAsync(signatures, dsig, 64 * half, cudaMemcpyDeviceToHost, ctx->d2h_stream));
     CU(ctx, cudaMemcpyAsync(signatures + 64 * half, dsig + 64 * half, 64 * (count - half), cudaMemcpyDeviceToHost,
                             ctx->stream));
+    CU(ctx, cudaMemcpyAsync(st_dst, dst, 4 * count, cudaMemcpyDeviceToHost, ctx->d2h_stream));
     CU(ctx, cudaStreamSynchronize(ctx->d2h_stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
-    return report_lanes(hst.data(), count, lane_status);
+    if (lane_status) return SM2B_OK;  // report_lanes (capi.cpp:64-73): statuses delivered, call is OK
+    return report_lanes(hst.data(), count, nullptr);
 }
 
 sm2b_status sm2b_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const uint8_t* secrets,
@@ -520,7 +533,7 @@ sm2b_status gecc_keygen(sm2b_ctx* ctx, uint64_t seed, uint64_t lane_base, size_t
     Carver co(ctx->out.p);
     uint8_t* dsec = co.take<uint8_t>(32 * count);
     uint8_t* dpub = co.take<uint8_t>(65 * count);
-    CU(ctx, launch_keygen(ctx->curve, count, seed, lane_base, ctx->gtab, dsec, dpub, ctx->stream));
+    CU(ctx, launch_keygen(ctx->curve, count, seed, lane_base, ctx->gtab_rec, dsec, dpub, ctx->stream));
     ctx->launches += 1;
     led_fpmul(ctx, count);
     CU(ctx, cudaMemcpyAsync(secrets, dsec, 32 * count, cudaMemcpyDeviceToHost, ctx->stream));
@@ -794,7 +807,8 @@ sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, 
     b.res = cv.take<uint8_t>(n); b.st = cv.take<int32_t>(n);
     cudaStream_t s = ctx->stream;
     const int cv_ = ctx->curve;
-    const uint32_t* gt = ctx->gtab;
+    const uint32_t* gt = ctx->gtab;          // column-buffer kernels
+    const uint32_t* gr = ctx->gtab_rec;      // byte-record kernels
     uint8_t* scratch_inf = b.res;  // infinity flags of generated points (never set for 0 < k < n)
     // ---- inputs (bench.cpp:139-140,163,167,194-200)
     if (opi == 0) {
@@ -807,10 +821,10 @@ sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, 
         CU(ctx, launch_fpmul(cv_, n, b.k2, gt, b.px, b.py, scratch_inf, s));
         CU(ctx, launch_seeded_scalars(cv_, n, seed, 0x30000, b.k, s));
     } else {
-        CU(ctx, launch_keygen(cv_, n, seed, 0x50000, gt, b.dig, b.pub, s));  // digests = seeded scalars
-        CU(ctx, launch_keygen(cv_, n, seed, 0x60000, gt, b.sec, b.pub, s));  // key pairs
+        CU(ctx, launch_keygen(cv_, n, seed, 0x50000, gr, b.dig, b.pub, s));  // digests = seeded scalars
+        CU(ctx, launch_keygen(cv_, n, seed, 0x60000, gr, b.sec, b.pub, s));  // key pairs
         CU(ctx, cudaMemsetAsync(ctx->flags, 0, 4, s));
-        CU(ctx, launch_sign(cv_, n, b.dig, b.sec, seed, 0, gt, b.sig, b.st, ctx->flags, s));
+        CU(ctx, launch_sign(cv_, n, b.dig, b.sec, seed, 0, gr, b.sig, b.st, ctx->flags, s));
     }
     auto run = [&](bool use_batch, uint32_t* ox, uint32_t* oy, uint8_t* oi) -> cudaError_t {
         switch (opi) {
@@ -826,10 +840,10 @@ sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, 
             case 3: {
                 cudaError_t e = cudaMemsetAsync(ctx->flags, 0, 4, s);
                 if (e != cudaSuccess) return e;
-                return launch_sign(cv_, n, b.dig, b.sec, seed, 0, gt, b.sig, b.st, ctx->flags, s);
+                return launch_sign(cv_, n, b.dig, b.sec, seed, 0, gr, b.sig, b.st, ctx->flags, s);
             }
             default:
-                return launch_verify(cv_, n, b.dig, b.pub, b.sig, gt, b.res, s);
+                return launch_verify(cv_, n, b.dig, b.pub, b.sig, gr, b.res, s);
         }
     };
     // ---- equivalence gate
@@ -848,7 +862,7 @@ sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, 
         CU(ctx, cudaStreamSynchronize(s));
         agree = ha == hb && ia == ib;
     } else {
-        CU(ctx, launch_verify(cv_, n, b.dig, b.pub, b.sig, gt, b.res, s));
+        CU(ctx, launch_verify(cv_, n, b.dig, b.pub, b.sig, gr, b.res, s));
         std::vector<uint8_t> hr(n);
         std::vector<int32_t> hs(n);
         CU(ctx, cudaMemcpyAsync(hr.data(), b.res, n, cudaMemcpyDeviceToHost, s));

@@ -34,7 +34,12 @@ GECC_HD jac jac_infinity() {
     r.Z = fe_zero();
     return r;
 }
-GECC_HD bool jac_is_inf(const jac& p) { return fe_is_zero(p.Z); }
+// Z == 0 (mod q).  Infinity is always *written* as the exact zero, but a weakly reduced
+// field may also hold q itself, so the test is the field's own.
+template <class C>
+GECC_HD bool jac_is_inf(const jac& p) {
+    return fe_is_zero(typename C::Fp{}, p.Z);
+}
 
 template <class C>
 GECC_HD fe curve_a() {
@@ -74,7 +79,7 @@ GECC_HD bool aff_on_curve(const aff& p) {
         rhs = fe_add(f, rhs, fe_mul(f, curve_a<C>(), p.x));
     }
     rhs = fe_add(f, rhs, curve_b<C>());
-    return fe_eq(lhs, rhs);
+    return fe_eq(f, lhs, rhs);
 }
 
 template <class C>
@@ -129,7 +134,7 @@ GECC_HD_CALL jac jac_dbl(const jac& p) {
 template <class C>
 GECC_HD_CALL jac jac_madd(const jac& p, const aff& q) {
     const typename C::Fp f{};
-    if (jac_is_inf(p)) {
+    if (jac_is_inf<C>(p)) {
         jac r;
         r.X = q.x;
         r.Y = q.y;
@@ -141,8 +146,8 @@ GECC_HD_CALL jac jac_madd(const jac& p, const aff& q) {
     fe s2 = fe_mul(f, q.y, fe_mul(f, z1z1, p.Z));
     fe h = fe_sub(f, u2, p.X);
     fe rr = fe_sub(f, s2, p.Y);
-    if (fe_is_zero(h)) {
-        if (fe_is_zero(rr)) return jac_dbl<C>(p);
+    if (fe_is_zero(f, h)) {
+        if (fe_is_zero(f, rr)) return jac_dbl<C>(p);
         return jac_infinity<C>();
     }
     fe hh = fe_sqr(f, h);
@@ -159,8 +164,8 @@ GECC_HD_CALL jac jac_madd(const jac& p, const aff& q) {
 template <class C>
 GECC_HD_CALL jac jac_add(const jac& p, const jac& q) {
     const typename C::Fp f{};
-    if (jac_is_inf(p)) return q;
-    if (jac_is_inf(q)) return p;
+    if (jac_is_inf<C>(p)) return q;
+    if (jac_is_inf<C>(q)) return p;
     fe z1z1 = fe_sqr(f, p.Z);
     fe z2z2 = fe_sqr(f, q.Z);
     fe u1 = fe_mul(f, p.X, z2z2);
@@ -169,8 +174,8 @@ GECC_HD_CALL jac jac_add(const jac& p, const jac& q) {
     fe s2 = fe_mul(f, q.Y, fe_mul(f, z1z1, p.Z));
     fe h = fe_sub(f, u2, u1);
     fe rr = fe_sub(f, s2, s1);
-    if (fe_is_zero(h)) {
-        if (fe_is_zero(rr)) return jac_dbl<C>(p);
+    if (fe_is_zero(f, h)) {
+        if (fe_is_zero(f, rr)) return jac_dbl<C>(p);
         return jac_infinity<C>();
     }
     fe hh = fe_sqr(f, h);

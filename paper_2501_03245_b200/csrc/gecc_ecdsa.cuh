@@ -404,7 +404,7 @@ GECC_HD int sign_lane(const fe& e, const fe& d, uint64_t seed, uint64_t stream,
     for (uint32_t attempt = 0; attempt < 8; ++attempt) {     // protocol.cpp:121
         fe k = nonce_scalar<typename C::Fn>(seed, stream, attempt);
         jac R = fixed_base_mul<C, WG>(k, gt);
-        if (jac_is_inf(R)) continue;                          // cannot happen for 0 < k < n
+        if (jac_is_inf<C>(R)) continue;                       // cannot happen for 0 < k < n
         fe zinv = fe_inv(fp, R.Z);
         fe x = fe_from_mont(fp, fe_mul(fp, R.X, fe_sqr(fp, zinv)));
         fe r = scalar_reduce_once<typename C::Fn>(x);         // coord_mod_n, protocol.cpp:37-39
@@ -440,13 +440,13 @@ GECC_HD uint8_t verify_lane(const uint8_t* digest32, const uint8_t* pub65, const
     build_lane_table<C>(Q, qt);
     jac B = var_base_mul<C>(u2, qt);
     jac R = jac_add<C>(A, B);
-    if (jac_is_inf(R)) return 0;
+    if (jac_is_inf<C>(R)) return 0;
     // x(R) mod n == r  <=>  X == r Z^2  or  (r + n < p and X == (r + n) Z^2)
     fe zz = fe_sqr(fp, R.Z);
-    if (fe_eq(R.X, fe_mul(fp, fe_to_mont(fp, r), zz))) return 1;
+    if (fe_eq(fp, R.X, fe_mul(fp, fe_to_mont(fp, r), zz))) return 1;
     uint32_t carry;
     fe rn = u256_add(r, fe_modulus(fn), &carry);
-    if (carry == 0 && fe_lt_modulus(fp, rn) && fe_eq(R.X, fe_mul(fp, fe_to_mont(fp, rn), zz)))
+    if (carry == 0 && fe_lt_modulus(fp, rn) && fe_eq(fp, R.X, fe_mul(fp, fe_to_mont(fp, rn), zz)))
         return 1;
     return 0;
 }

@@ -93,9 +93,128 @@ GECC_HD bool fe_lt_modulus(const F& f, const fe& a) {
     return u256_lt(a, fe_modulus(f));
 }
 
+// ---------------------------------------------------------------- lazy secp256k1 field
+// KIND_SECP_LAZY: elements are plain residues (no Montgomery factor) that are only
+// WEAKLY reduced -- any 256-bit value, congruent mod q = 2^256 - c, c = 2^32 + 977.
+// 2^256 == c (mod q), so an overflow of 2^256 is folded back by adding c and a borrow by
+// subtracting c; there is no compare-and-select.  Canonical form is produced only where a
+// value leaves the field layer (bytes, equality with a canonical constant, inversion).
+template <class F>
+GECC_HD fe lazy_canon(const F&, const fe& a) {  // a -> a mod q in [0, q)
+    fe s;
+    s.w[0] = add_cc(a.w[0], 977u);
+    s.w[1] = addc_cc(a.w[1], 1u);
+#pragma unroll
+    for (int i = 2; i < 8; ++i) s.w[i] = addc_cc(a.w[i], 0);
+    const uint32_t over = addc(0, 0);  // a + c >= 2^256  <=>  a >= q
+    return fe_select(over != 0, s, a);
+}
+// a == 0 (mod q) for a weakly reduced a: a is 0 or q
+template <class F>
+GECC_HD bool lazy_is_zero(const F& f, const fe& a) {
+    uint32_t z = 0, e = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        z |= a.w[i];
+        e |= a.w[i] ^ f.q(i);
+    }
+    return z == 0 || e == 0;
+}
+// r = (carry : a) folded once more: a + carry * c, with the (rare) second wrap handled
+GECC_HD fe lazy_fold_carry(const fe& a, uint32_t carry) {
+    fe r;
+    r.w[0] = add_cc(a.w[0], carry * 977u);
+    r.w[1] = addc_cc(a.w[1], carry);
+#pragma unroll
+    for (int i = 2; i < 8; ++i) r.w[i] = addc_cc(a.w[i], 0);
+    const uint32_t again = addc(0, 0);
+    if (again) {  // only when a >= 2^256 - c: the wrapped value is below c, adding c cannot wrap
+        r.w[0] = add_cc(r.w[0], 977u);
+        r.w[1] = addc_cc(r.w[1], 1u);
+#pragma unroll
+        for (int i = 2; i < 8; ++i) r.w[i] = addc_cc(r.w[i], 0);
+    }
+    return r;
+}
+GECC_HD fe lazy_add(const fe& a, const fe& b) {
+    fe s;
+    s.w[0] = add_cc(a.w[0], b.w[0]);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) s.w[i] = addc_cc(a.w[i], b.w[i]);
+    return lazy_fold_carry(s, addc(0, 0));
+}
+GECC_HD fe lazy_sub(const fe& a, const fe& b) {
+    fe d;
+    d.w[0] = sub_cc(a.w[0], b.w[0]);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) d.w[i] = subc_cc(a.w[i], b.w[i]);
+    const uint32_t k = subc(0, 0) & 1u;  // borrowed: d = a - b + 2^256 == a - b + c, so take c off
+    fe r;
+    r.w[0] = sub_cc(d.w[0], k * 977u);
+    r.w[1] = subc_cc(d.w[1], k);
+#pragma unroll
+    for (int i = 2; i < 8; ++i) r.w[i] = subc_cc(d.w[i], 0);
+    const uint32_t again = subc(0, 0);
+    if (again) {  // only when d < c: wrapped once more, take c off again (cannot wrap a third time)
+        r.w[0] = sub_cc(r.w[0], 977u);
+        r.w[1] = subc_cc(r.w[1], 1u);
+#pragma unroll
+        for (int i = 2; i < 8; ++i) r.w[i] = subc_cc(r.w[i], 0);
+    }
+    return r;
+}
+// 512-bit t -> weakly reduced 256-bit value == t (mod q):
+//   v = t_lo + t_hi * 977 + (t_hi << 32)          (10 limbs, top part V < 2^33 + 2^10)
+//   w = v_lo + V * 977 + (V << 32)                 (carry <= 1)
+//   r = w + carry * c
+// 8 IMAD + 8 IMAD.HI + 2, everything else carry chains; no dependent multiplier sequence.
+GECC_HD fe redc_secp_lazy(const uint32_t* t) {
+    uint32_t s[10];
+    s[0] = mad_lo_cc(t[8], 977u, t[0]);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) s[i] = madc_lo_cc(t[8 + i], 977u, t[i]);
+    s[8] = addc(0, 0);
+    s[1] = mad_hi_cc(t[8], 977u, s[1]);
+#pragma unroll
+    for (int i = 1; i < 7; ++i) s[i + 1] = madc_hi_cc(t[8 + i], 977u, s[i + 1]);
+    s[8] = madc_hi(t[15], 977u, s[8]);  // <= 1 + 976 + 1: no carry out
+    s[1] = add_cc(s[1], t[8]);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) s[i + 1] = addc_cc(s[i + 1], t[8 + i]);
+    s[9] = addc(0, 0);
+    // fold V = s[9] : s[8]
+    const uint32_t lo977 = mul_lo(s[8], 977u);
+    const uint32_t hi977 = mul_hi(s[8], 977u) + s[9] * 977u;
+    fe r;
+    r.w[0] = add_cc(s[0], lo977);
+    r.w[1] = addc_cc(s[1], hi977);
+    r.w[2] = addc_cc(s[2], s[9]);
+#pragma unroll
+    for (int i = 3; i < 8; ++i) r.w[i] = addc_cc(s[i], 0);
+    uint32_t carry = addc(0, 0);
+    r.w[1] = add_cc(r.w[1], s[8]);
+#pragma unroll
+    for (int i = 2; i < 8; ++i) r.w[i] = addc_cc(r.w[i], 0);
+    carry = addc(carry, 0);  // total carry is 0 or 1 (w < 2^256 + 2^67)
+    // w >= 2^256 leaves a tiny remainder, so adding c cannot wrap again
+    r.w[0] = add_cc(r.w[0], carry * 977u);
+    r.w[1] = addc_cc(r.w[1], carry);
+#pragma unroll
+    for (int i = 2; i < 8; ++i) r.w[i] = addc_cc(r.w[i], 0);
+    return r;
+}
+
+// field-aware predicates: canonical fields compare limbs, the lazy field compares mod q
+template <class F>
+GECC_HD bool fe_is_zero(const F& f, const fe& a) {
+    if constexpr (F::kind == KIND_SECP_LAZY) return lazy_is_zero(f, a);
+    else return fe_is_zero(a);
+}
+
 // ---------------------------------------------------------------- add / sub
 template <class F>
 GECC_HD fe fe_add(const F& f, const fe& a, const fe& b) {
+    if constexpr (F::kind == KIND_SECP_LAZY) return lazy_add(a, b);
     fe s, d;
     s.w[0] = add_cc(a.w[0], b.w[0]);
 #pragma unroll
@@ -110,6 +229,7 @@ GECC_HD fe fe_add(const F& f, const fe& a, const fe& b) {
 }
 template <class F>
 GECC_HD fe fe_sub(const F& f, const fe& a, const fe& b) {
+    if constexpr (F::kind == KIND_SECP_LAZY) return lazy_sub(a, b);
     fe d, e;
     d.w[0] = sub_cc(a.w[0], b.w[0]);
 #pragma unroll
@@ -119,6 +239,11 @@ GECC_HD fe fe_sub(const F& f, const fe& a, const fe& b) {
 #pragma unroll
     for (int i = 1; i < 8; ++i) e.w[i] = addc_cc(d.w[i], f.q(i));
     return fe_select(borrow != 0, e, d);
+}
+template <class F>
+GECC_HD bool fe_eq(const F& f, const fe& a, const fe& b) {
+    if constexpr (F::kind == KIND_SECP_LAZY) return lazy_is_zero(f, lazy_sub(a, b));
+    else return fe_eq(a, b);
 }
 template <class F>
 GECC_HD fe fe_neg(const F& f, const fe& a) {
@@ -380,6 +505,7 @@ GECC_HD fe redc_sm2(const F& f, const uint32_t* tin) {
 template <class F>
 GECC_HD fe redc(const F& f, const uint32_t* t) {
     if constexpr (F::kind == KIND_SECP_P) return redc_secp(f, t);
+    else if constexpr (F::kind == KIND_SECP_LAZY) return redc_secp_lazy(t);
     else if constexpr (F::kind == KIND_SM2_P) return redc_sm2(f, t);
     else return redc_generic(f, t);
 }
@@ -450,6 +576,7 @@ GECC_HD fe fe_sqr(const F& f, const fe& a) {
 #endif
 template <class F>
 GECC_HD fe fe_to_mont(const F& f, const fe& a) {  // a * R
+    if constexpr (F::kind == KIND_SECP_LAZY) return a;  // plain representation: R = 1
     fe r2;
 #pragma unroll
     for (int i = 0; i < 8; ++i) r2.w[i] = f.r2(i);
@@ -457,6 +584,7 @@ GECC_HD fe fe_to_mont(const F& f, const fe& a) {  // a * R
 }
 template <class F>
 GECC_HD fe fe_from_mont(const F& f, const fe& a) {  // a * R^-1
+    if constexpr (F::kind == KIND_SECP_LAZY) return lazy_canon(f, a);  // leaves the field layer: canonical
     uint32_t t[16];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {

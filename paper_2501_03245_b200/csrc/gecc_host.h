@@ -19,7 +19,10 @@ cudaError_t run_microbench(int which, int iters, int sm_count, double* ops_per_c
                            double* seconds, double* total_ops, cudaStream_t s);
 
 size_t gtable_words();
-cudaError_t build_gtable(int curve, uint32_t* tab, uint32_t* bases_scratch, cudaStream_t s);
+// lazy_plain: the table of the byte-record kernels on secp256k1 (plain coordinates);
+// otherwise Montgomery-form coordinates (column-buffer kernels; SM2 uses it for both)
+cudaError_t build_gtable(int curve, bool lazy_plain, uint32_t* tab, uint32_t* bases_scratch,
+                         cudaStream_t s);
 
 cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t* pub,
                           const uint8_t* sig, const uint32_t* gtab, uint8_t* res, cudaStream_t s);

@@ -193,6 +193,7 @@ GECC_HD_CALL fe safegcd_inverse(const F& fld, const fe& x) {
 // Montgomery-form inverse of a Montgomery-form element (zero -> zero).
 template <class F>
 GECC_HD fe fe_inv(const F& f, const fe& a) {
+    if constexpr (F::kind == KIND_SECP_LAZY) return safegcd_inverse(f, lazy_canon(f, a));  // plain in, plain out
     fe r3;
 #pragma unroll
     for (int i = 0; i < 8; ++i) r3.w[i] = f.r3(i);

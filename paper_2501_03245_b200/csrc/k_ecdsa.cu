@@ -89,7 +89,7 @@ k_ecdh(size_t n, const uint8_t* __restrict__ sec, const uint8_t* __restrict__ pe
     }
     build_lane_table<C>(p, qt);
     jac r = var_base_mul<C>(d, qt);
-    if (jac_is_inf(r)) {
+    if (jac_is_inf<C>(r)) {
         status[i] = 4;
         return;
     }
@@ -103,7 +103,7 @@ template <class C>
 __device__ __forceinline__ void store_affine(const jac& r, uint32_t* ox, uint32_t* oy,
                                              uint8_t* oinf, size_t n, size_t i) {
     const typename C::Fp f{};
-    if (jac_is_inf(r)) {  // infinity coordinates are normalised to zero (batch_point.cpp:41-47)
+    if (jac_is_inf<C>(r)) {  // infinity coordinates are normalised to zero (batch_point.cpp:41-47)
         col_store(ox, n, i, fe_zero());
         col_store(oy, n, i, fe_zero());
         oinf[i] = 1;
@@ -215,6 +215,10 @@ static int blocks_for(size_t n, int threads) { return (int)((n + threads - 1) / 
         if ((curve) == CURVE_SECP) { EXPR_SECP; } \
         else { EXPR_SM2; }                        \
     } while (0)
+// The byte-record (ECDSA / keygen / ECDH) kernels run secp256k1 in the lazy plain
+// representation (SecpLCurve, its own fixed-base table); the column-buffer kernels keep
+// the reference's Montgomery form (SecpCurve) because that is their I/O contract.
+using SecpEcdsaCurve = SecpLCurve;
 
 template <class C, int THREADS, int BLOCKS_PER_SM>
 static cudaError_t launch_verify_t(size_t n, const uint8_t* dig, const uint8_t* pub, const uint8_t* sig,
@@ -230,14 +234,14 @@ static cudaError_t launch_verify_t(size_t n, const uint8_t* dig, const uint8_t* 
 cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t* pub,
                           const uint8_t* sig, const uint32_t* gtab, uint8_t* res, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    // GECC_VERIFY_SHAPE=128x3 selects the alternative launch shape (tuning experiments only)
+    // GECC_VERIFY_SHAPE=64x7 selects the alternative launch shape (14 warps per SM, measured slower) (tuning experiments only)
     static const bool wide = [] {
         const char* v = getenv("GECC_VERIFY_SHAPE");
-        return v && !strcmp(v, "128x3");
+        return !(v && !strcmp(v, "64x7"));
     }();
     if (curve == CURVE_SECP)
-        return wide ? launch_verify_t<SecpCurve, 128, 3>(n, dig, pub, sig, gtab, res, s)
-                    : launch_verify_t<SecpCurve, 64, 7>(n, dig, pub, sig, gtab, res, s);
+        return wide ? launch_verify_t<SecpEcdsaCurve, 128, 3>(n, dig, pub, sig, gtab, res, s)
+                    : launch_verify_t<SecpEcdsaCurve, 64, 7>(n, dig, pub, sig, gtab, res, s);
     return wide ? launch_verify_t<Sm2Curve, 128, 3>(n, dig, pub, sig, gtab, res, s)
                 : launch_verify_t<Sm2Curve, 64, 7>(n, dig, pub, sig, gtab, res, s);
 }
@@ -248,7 +252,7 @@ cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* 
     if (n == 0) return cudaSuccess;
     const int b = blocks_for(n, SIGN_THREADS);
     GECC_BY_CURVE(curve,
-        (k_sign<SecpCurve><<<b, SIGN_THREADS, 0, s>>>(n, dig, sec, seed, lane_base, gtab, sig, status, flags)),
+        (k_sign<SecpEcdsaCurve><<<b, SIGN_THREADS, 0, s>>>(n, dig, sec, seed, lane_base, gtab, sig, status, flags)),
         (k_sign<Sm2Curve><<<b, SIGN_THREADS, 0, s>>>(n, dig, sec, seed, lane_base, gtab, sig, status, flags)));
     return cudaGetLastError();
 }
@@ -258,7 +262,7 @@ cudaError_t launch_keygen(int curve, size_t n, uint64_t seed, uint64_t lane_base
     if (n == 0) return cudaSuccess;
     const int b = blocks_for(n, SIGN_THREADS);
     GECC_BY_CURVE(curve,
-        (k_keygen<SecpCurve><<<b, SIGN_THREADS, 0, s>>>(n, seed, lane_base, gtab, sec, pub)),
+        (k_keygen<SecpEcdsaCurve><<<b, SIGN_THREADS, 0, s>>>(n, seed, lane_base, gtab, sec, pub)),
         (k_keygen<Sm2Curve><<<b, SIGN_THREADS, 0, s>>>(n, seed, lane_base, gtab, sec, pub)));
     return cudaGetLastError();
 }
@@ -266,11 +270,11 @@ cudaError_t launch_keygen(int curve, size_t n, uint64_t seed, uint64_t lane_base
 cudaError_t launch_ecdh(int curve, size_t n, const uint8_t* sec, const uint8_t* peers,
                         uint8_t* shared, int32_t* status, uint32_t* flags, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    cudaError_t e = curve == CURVE_SECP ? opt_in_smem(k_ecdh<SecpCurve>) : opt_in_smem(k_ecdh<Sm2Curve>);
+    cudaError_t e = curve == CURVE_SECP ? opt_in_smem(k_ecdh<SecpEcdsaCurve>) : opt_in_smem(k_ecdh<Sm2Curve>);
     if (e != cudaSuccess) return e;
     const int b = blocks_for(n, VERIFY_THREADS);
     GECC_BY_CURVE(curve,
-        (k_ecdh<SecpCurve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, sec, peers, shared, status, flags)),
+        (k_ecdh<SecpEcdsaCurve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, sec, peers, shared, status, flags)),
         (k_ecdh<Sm2Curve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, sec, peers, shared, status, flags)));
     return cudaGetLastError();
 }

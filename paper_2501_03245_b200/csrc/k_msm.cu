@@ -191,7 +191,7 @@ k_msm_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, uint
         jac acc = jac_infinity<C>();
 #pragma unroll 1
         for (int i = 0; i < MSM_WINDOWS; ++i) acc = jac_add<C>(acc, jac_load(win, MSM_WINDOWS, i));
-        if (jac_is_inf(acc)) {
+        if (jac_is_inf<C>(acc)) {
             col_store(ox, 1, 0, fe_zero());
             col_store(oy, 1, 0, fe_zero());
             oinf[0] = 1;

@@ -57,11 +57,15 @@ __global__ void __launch_bounds__(128) k_gtable_fill(const uint32_t* __restrict_
 
 size_t gtable_words() { return (size_t)GTable<GECC_WG>::windows * GTable<GECC_WG>::per_window * 16; }
 
-cudaError_t build_gtable(int curve, uint32_t* tab, uint32_t* bases_scratch, cudaStream_t s) {
+cudaError_t build_gtable(int curve, bool lazy_plain, uint32_t* tab, uint32_t* bases_scratch,
+                         cudaStream_t s) {
     using GT = GTable<GECC_WG>;
     const size_t entries = (size_t)GT::windows * GT::per_window;
     const int blocks = (int)((entries + 127) / 128);
-    if (curve == CURVE_SECP) {
+    if (curve == CURVE_SECP && lazy_plain) {  // table of the fused ECDSA kernels (plain coordinates)
+        k_gtable_bases<SecpLCurve, GECC_WG><<<1, 32, 0, s>>>(bases_scratch);
+        k_gtable_fill<SecpLCurve, GECC_WG><<<blocks, 128, 0, s>>>(bases_scratch, tab);
+    } else if (curve == CURVE_SECP) {
         k_gtable_bases<SecpCurve, GECC_WG><<<1, 32, 0, s>>>(bases_scratch);
         k_gtable_fill<SecpCurve, GECC_WG><<<blocks, 128, 0, s>>>(bases_scratch, tab);
     } else {

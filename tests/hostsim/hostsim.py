@@ -31,10 +31,15 @@ FIELD_IDS = {(1, 0): 0, (1, 1): 1, (0, 0): 2, (0, 1): 3}  # (curve, which) -> ho
 OPS = dict(mont_mul=0, mod_add=1, mod_sub=2, to_mont=3, from_mont=4, mod_inv=5, sqr=6, inv_safegcd=7, inv_plain=8)
 
 
-def field_op(curve, which, op, a, b=None):
+SECP_LAZY_CURVE = 2   # secp256k1 in the lazy plain representation (ECDSA kernels)
+SECP_LAZY_FIELD = 5
+
+
+def field_op(curve, which, op, a, b=None, field_id=None):
     n = a.shape[1]
     out = np.zeros((8, n), np.uint32)
-    rc = lib().hs_field_op(FIELD_IDS[(curve, which)], None, OPS[op], C.c_size_t(n), _p(a), _p(b), _p(out))
+    fid = FIELD_IDS[(curve, which)] if field_id is None else field_id
+    rc = lib().hs_field_op(fid, None, OPS[op], C.c_size_t(n), _p(a), _p(b), _p(out))
     assert rc == 0
     return out
 

@@ -113,3 +113,36 @@ def test_hostsim_ecdsa_golden(name):
     rt = ent["retry"]
     s, st = H.sign(cid, bytes.fromhex(rt["digests"]), bytes.fromhex(rt["secrets"]), rt["nonce_seed"])
     assert (s.hex(), st) == (rt["sigs"], [0, 0])
+
+
+def test_hostsim_lazy_secp_field():
+    """The lazy plain secp256k1 field of the fused ECDSA kernels: weakly reduced 256-bit values,
+    including NON-canonical inputs (q, q+1, 2^256-1 ...), against Python integers mod q."""
+    p = E.SECP256K1.p
+    rng = random.Random(11)
+    special = [0, 1, p - 1, p, p + 1, 2**256 - 1, 2**256 - 2, p + 977, 2**255, 2**256 - 2**32, 2**256 - 977, 5]
+    a = special + [rng.randrange(1 << 256) for _ in range(5000)]
+    b = special[::-1] + [rng.randrange(1 << 256) for _ in range(5000)]
+    A, B = O.ints_to_cols(a), O.ints_to_cols(b)
+    for op, fn in (("mont_mul", lambda x, y: x * y), ("mod_add", lambda x, y: x + y),
+                   ("mod_sub", lambda x, y: x - y), ("sqr", lambda x, y: x * x)):
+        got = O.cols_to_ints(H.field_op(1, 0, op, A, B, field_id=H.SECP_LAZY_FIELD))
+        assert all(g % p == fn(x, y) % p for g, x, y in zip(got, a, b)), op
+    canon = O.cols_to_ints(H.field_op(1, 0, "from_mont", A, field_id=H.SECP_LAZY_FIELD))
+    assert canon == [x % p for x in a]
+    inv = O.cols_to_ints(H.field_op(1, 0, "inv_safegcd", np.ascontiguousarray(A[:, :400]), field_id=H.SECP_LAZY_FIELD))
+    assert all((g * x) % p == 1 if x % p else g == 0 for g, x in zip(inv, a[:400]))
+
+
+def test_hostsim_lazy_curve_ecdsa_golden():
+    ent = ECDSA["secp256k1"]
+    cid, n = H.SECP_LAZY_CURVE, ent["n"]
+    sec, pub = bytes.fromhex(ent["secrets"]), bytes.fromhex(ent["publics"])
+    dig, sig = bytes.fromhex(ent["digests"]), bytes.fromhex(ent["sigs"])
+    assert H.keygen(cid, ent["keygen_seed"], n) == (sec, pub)
+    assert H.sign(cid, dig, sec, ent["nonce_seed"]) == (sig, [0] * n)
+    for case in ent["verify_cases"]:
+        d, p, sg = (bytes.fromhex(case[k]) for k in ("digests", "publics", "sigs"))
+        assert list(H.verify(cid, d, p, sg)) == case["results"], case["name"]
+    rt = ent["retry"]
+    assert H.sign(cid, bytes.fromhex(rt["digests"]), bytes.fromhex(rt["secrets"]), rt["nonce_seed"])[0].hex() == rt["sigs"]
