@@ -38,7 +38,7 @@ def main():
             name = vals[hdr.index("Kernel Name")] if "Kernel Name" in hdr else "?"
             for h, u, v in zip(hdr, units, vals):
                 if h in KEEP or h.startswith("smsp__average_warps_issue_stalled"):
-                    w.writerow([name[:60], h, u, v])
+                    w.writerow([name.split("(")[0].replace("void ", "")[:60], h, u, v])
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(src.splitlines()))
     hdr = rows[1]
