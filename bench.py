@@ -369,7 +369,7 @@ def main():
         "modmul_per_s": n * products_per_lane / per_launch_s,
         "hbm": {"algorithmic_bytes_per_launch": io_bytes, "achieved_gbs": io_bytes / per_launch_s / 1e9,
                 "peak_gbs": _measured_peaks().get("hbm_gbs"), "note": "records only; not the bound"},
-        "traffic": None,
+        "traffic": _ncu_traffic(wl),
     }
 
     # ---- CPU baseline on this box's host cores (rank 0, N = 1 only)
@@ -417,6 +417,27 @@ def main():
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def _ncu_traffic(wl):
+    """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per launch, from the
+    committed `ncu --set full` capture of this same command (profiles/, tools/ncu_summary.py).
+    For k_verify it is well above the 170 MB of records: the excess is per-thread stack
+    (2 KB x 2^20 lanes of local memory written back from L1), not re-reads of the inputs."""
+    import csv
+    name = {"verify": "r01d_verify_lazyfield", "padd": "r01_padd", "msm": "r01_msm"}.get(wl)
+    if not name:
+        return None
+    try:
+        tot = 0.0
+        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        with open(os.path.join(ROOT, "profiles", name + "_metrics.csv")) as f:
+            for r in csv.reader(f):
+                if len(r) >= 4 and r[1] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    tot += float(r[3]) * scale.get(r[2], 1)
+        return {"bytes_per_launch": tot, "source": f"profiles/{name}_metrics.csv"} if tot else None
+    except OSError:
+        return None
 
 
 def _measured_peaks():
