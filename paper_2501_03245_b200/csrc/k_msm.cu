@@ -89,25 +89,85 @@ __device__ __forceinline__ jac jac_load(const uint32_t* buf, size_t count, size_
     return p;
 }
 
+// Bucket accumulation, load-balanced: thread t owns the fixed-size slice
+// [t * MSM_SLICE, (t+1) * MSM_SLICE) of the SORTED pairs, whatever buckets it crosses (a
+// thread per bucket makes every warp wait for its largest bucket: sizes are Poisson(32)).
+// A run of equal keys that starts and ends strictly inside the slice is a complete bucket
+// and is stored directly.  The first and the last run of a slice may continue in the
+// neighbouring slices: those sums go to edge[2t] / edge[2t+1] with their bucket ids, and
+// k_msm_bucket_edges adds, for every bucket, the edge partials that belong to it.
+// Buckets that receive nothing are pre-set to infinity (Z = 0) by a memset.
+constexpr int MSM_SLICE = 32;
+
 template <class C>
 __global__ void __launch_bounds__(128)
 k_msm_buckets(size_t n, size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
               const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
-              uint32_t* __restrict__ buckets) {
-    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= MSM_NB) return;
+              uint32_t* __restrict__ buckets, uint32_t* __restrict__ edge, uint32_t* __restrict__ edge_key,
+              size_t slices) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (t >= slices) return;
     const typename C::Fp f{};
-    size_t lo = lower_bound_key(keys, m, b), hi = lower_bound_key(keys, m, b + 1);
+    const size_t lo = t * MSM_SLICE, hi = lo + MSM_SLICE < m ? lo + MSM_SLICE : m;
+    const uint32_t prev_key = lo > 0 ? keys[lo - 1] : 0xFFFFFFFFu;
+    const uint32_t next_key = hi < m ? keys[hi] : 0xFFFFFFFFu;
+    edge_key[2 * t] = edge_key[2 * t + 1] = MSM_KEY_NONE;
     jac acc = jac_infinity<C>();
+    uint32_t cur = keys[lo];
+    bool first_run = true;
 #pragma unroll 1
-    for (size_t p = lo; p < hi; ++p) {
-        const uint32_t v = vals[p];
-        const size_t idx = v & 0x7FFFFFFFu;
-        aff t{col_load(px, n, idx), col_load(py, n, idx)};
-        if (v >> 31) t.y = fe_neg(f, t.y);
-        acc = jac_madd<C>(acc, t);
+    for (size_t p = lo; p <= hi; ++p) {
+        const uint32_t key = p < hi ? keys[p] : 0xFFFFFFFEu;  // sentinel closes the last run
+        if (key != cur) {
+            if (cur < MSM_NB) {  // close the run of bucket `cur`
+                const bool open_left = first_run && cur == prev_key;
+                const bool open_right = p == hi && cur == next_key;
+                if (open_left) {
+                    jac_store(edge, 2 * slices, 2 * t, acc);
+                    edge_key[2 * t] = cur;
+                    // the whole slice lies inside one bucket: mark "continues to the right"
+                    // (no point is stored in the right edge; the high bit says so)
+                    if (open_right) edge_key[2 * t + 1] = cur | 0x80000000u;
+                } else if (open_right) {
+                    jac_store(edge, 2 * slices, 2 * t + 1, acc);
+                    edge_key[2 * t + 1] = cur;
+                } else {
+                    jac_store(buckets, MSM_NB, cur, acc);
+                }
+            }
+            first_run = false;
+            acc = jac_infinity<C>();
+            cur = key;
+        }
+        if (p < hi && key < MSM_NB) {
+            const uint32_t v = vals[p];
+            const size_t idx = v & 0x7FFFFFFFu;
+            aff q{col_load(px, n, idx), col_load(py, n, idx)};
+            if (v >> 31) q.y = fe_neg(f, q.y);
+            acc = jac_madd<C>(acc, q);
+        }
     }
-    jac_store(buckets, MSM_NB, b, acc);
+}
+
+// one thread per slice edge that opens a bucket from the left side of a chain: a bucket
+// spanning slices t0 < ... < t1 has partials right(t0), left(t0+1) [whole slices in between
+// are left edges too], ..., left(t1).  The thread holding right(t0) walks to the right and
+// adds every following left edge with the same key, then stores the bucket.
+template <class C>
+__global__ void __launch_bounds__(128)
+k_msm_bucket_edges(uint32_t* __restrict__ buckets, const uint32_t* __restrict__ edge,
+                   const uint32_t* __restrict__ edge_key, size_t slices) {
+    const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (t >= slices) return;
+    const uint32_t key = edge_key[2 * t + 1];
+    if (key >= MSM_NB) return;  // this slice's last run does not continue to the right
+    jac acc = jac_load(edge, 2 * slices, 2 * t + 1);
+#pragma unroll 1
+    for (size_t u = t + 1; u < slices && edge_key[2 * u] == key; ++u) {
+        acc = jac_add<C>(acc, jac_load(edge, 2 * slices, 2 * u));
+        if (edge_key[2 * u + 1] != (key | 0x80000000u)) break;  // the run ended inside slice u
+    }
+    jac_store(buckets, MSM_NB, key, acc);
 }
 
 // marginal sums, stage 1: thread (w, k, e, part) adds the 32 buckets of window w whose
@@ -207,7 +267,8 @@ k_msm_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, uint
 // ---------------------------------------------------------------- host side
 struct MsmPlan {
     size_t pairs, sort_temp, total;
-    size_t off_keys, off_vals, off_keys2, off_vals2, off_buckets, off_parts, off_marg, off_wsum, off_temp;
+    size_t slices;
+    size_t off_keys, off_vals, off_keys2, off_vals2, off_buckets, off_edge, off_edge_key, off_parts, off_marg, off_wsum, off_temp;
 };
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
@@ -222,7 +283,10 @@ static MsmPlan msm_plan(size_t n) {
     p.off_vals = take(4 * p.pairs);
     p.off_keys2 = take(4 * p.pairs);
     p.off_vals2 = take(4 * p.pairs);
+    p.slices = (p.pairs + MSM_SLICE - 1) / MSM_SLICE;
     p.off_buckets = take((size_t)96 * MSM_NB);
+    p.off_edge = take((size_t)96 * 2 * p.slices);
+    p.off_edge_key = take((size_t)4 * 2 * p.slices);
     p.off_parts = take((size_t)96 * MSM_WINDOWS * 3 * 1024);
     p.off_marg = take((size_t)96 * MSM_WINDOWS * 3 * 32);
     p.off_wsum = take((size_t)96 * MSM_WINDOWS * 4);
@@ -247,12 +311,17 @@ static cudaError_t run_msm(size_t n, const uint32_t* scalars, const uint32_t* px
     cudaError_t e = cub::DeviceRadixSort::SortPairs(base + p.off_temp, temp, keys, keys2, vals, vals2,
                                                     (int64_t)p.pairs, 0, 20, s);
     if (e != cudaSuccess) return e;
-    k_msm_buckets<C><<<(MSM_NB + 127) / 128, 128, 0, s>>>(n, p.pairs, keys2, vals2, px, py, buckets);
+    uint32_t *edge = (uint32_t*)(base + p.off_edge), *edge_key = (uint32_t*)(base + p.off_edge_key);
+    e = cudaMemsetAsync(buckets, 0, (size_t)96 * MSM_NB, s);  // empty buckets = infinity (Z = 0)
+    if (e != cudaSuccess) return e;
+    const unsigned sb = (unsigned)((p.slices + 127) / 128);
+    k_msm_buckets<C><<<sb, 128, 0, s>>>(n, p.pairs, keys2, vals2, px, py, buckets, edge, edge_key, p.slices);
+    k_msm_bucket_edges<C><<<sb, 128, 0, s>>>(buckets, edge, edge_key, p.slices);
     k_msm_marginal_parts<C><<<(MSM_WINDOWS * 3 * 1024 + 127) / 128, 128, 0, s>>>(buckets, parts);
     k_msm_marginal_fold<C><<<(MSM_WINDOWS * 3 * 32 + 127) / 128, 128, 0, s>>>(parts, marg);
     k_msm_weighted<C><<<1, 128, 0, s>>>(marg, wsum);
     k_msm_combine<C><<<1, 32, 0, s>>>(wsum, ox, oy, oinf);
-    *launches = 6 + 4;  // ours + the sort's passes (approximate; CUB picks the pass count)
+    *launches = 7 + 4;  // ours + the sort's passes (approximate; CUB picks the pass count)
     return cudaGetLastError();
 }
 
