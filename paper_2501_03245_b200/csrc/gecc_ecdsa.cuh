@@ -395,13 +395,13 @@ enum { LANE_OK = 0, LANE_NONCE_EXHAUSTED = 5 };  // sm2b_status values
 // Writes r || s (64 bytes) or zeros; returns the lane status.
 template <class C, int WG>
 GECC_HD int sign_lane(const fe& e, const fe& d, uint64_t seed, uint64_t stream,
-                      const GTable<WG>& gt, uint8_t* sig64) {
+                      const GTable<WG>& gt, uint8_t* sig64, uint32_t first_attempt = 0) {
     const typename C::Fp fp{};
     const typename C::Fn fn{};
     fe e_m = fe_to_mont(fn, e);
     fe d_m = fe_to_mont(fn, d);
 #pragma unroll 1
-    for (uint32_t attempt = 0; attempt < 8; ++attempt) {     // protocol.cpp:121
+    for (uint32_t attempt = first_attempt; attempt < 8; ++attempt) {  // protocol.cpp:121
         fe k = nonce_scalar<typename C::Fn>(seed, stream, attempt);
         jac R = fixed_base_mul<C, WG>(k, gt);
         if (jac_is_inf<C>(R)) continue;                       // cannot happen for 0 < k < n
@@ -420,6 +420,58 @@ GECC_HD int sign_lane(const fe& e, const fe& d, uint64_t seed, uint64_t stream,
     }
     for (int i = 0; i < 64; ++i) sig64[i] = 0;
     return LANE_NONCE_EXHAUSTED;
+}
+
+// K lanes signed by one thread: the K nonce points are computed first, then ONE inversion
+// mod p (for the K Jacobian Z's) and ONE inversion mod n (for the K nonces) are shared by
+// Montgomery's trick -- the same idea the reference applies across a whole batch
+// (protocol.cpp:133-136 + batch_invert), applied here inside a thread so that no
+// cross-thread traffic is needed.  A lane that has to retry (r == 0 or s == 0, probability
+// ~2^-255 unless forced) falls back to sign_lane from attempt 1, which reproduces the
+// reference's per-lane retry sequence exactly.
+template <class C, int WG, int K>
+GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream0,
+                        const GTable<WG>& gt, uint8_t* sig64, int* status) {
+    const typename C::Fp fp{};
+    const typename C::Fn fn{};
+    fe X[K], Z[K], km[K], pz[K], pk[K];
+#pragma unroll 1
+    for (int j = 0; j < K; ++j) {
+        fe k = nonce_scalar<typename C::Fn>(seed, stream0 + j, 0);
+        jac R = fixed_base_mul<C, WG>(k, gt);
+        X[j] = R.X;
+        Z[j] = R.Z;  // never zero for 0 < k < n
+        km[j] = fe_to_mont(fn, k);
+        pz[j] = j ? fe_mul(fp, pz[j - 1], Z[j]) : Z[j];
+        pk[j] = j ? fe_mul(fn, pk[j - 1], km[j]) : km[j];
+    }
+    fe iz = fe_inv(fp, pz[K - 1]);                                   // (Z_0 ... Z_{K-1})^-1
+    fe ik = fe_to_mont(fn, safegcd_inverse(fn, fe_from_mont(fn, pk[K - 1])));  // Montgomery form
+#pragma unroll 1
+    for (int j = K - 1; j >= 0; --j) {
+        fe zinv = j ? fe_mul(fp, iz, pz[j - 1]) : iz;
+        fe kinv_m = j ? fe_mul(fn, ik, pk[j - 1]) : ik;
+        if (j) {
+            iz = fe_mul(fp, iz, Z[j]);
+            ik = fe_mul(fn, ik, km[j]);
+        }
+        uint8_t* out = sig64 + 64 * j;
+        fe x = fe_from_mont(fp, fe_mul(fp, X[j], fe_sqr(fp, zinv)));
+        fe r = scalar_reduce_once<typename C::Fn>(x);
+        fe s = fe_zero();
+        if (!fe_is_zero(r)) {
+            fe s_m = fe_mul(fn, kinv_m, fe_add(fn, fe_to_mont(fn, e[j]),
+                                               fe_mul(fn, fe_to_mont(fn, r), fe_to_mont(fn, d[j]))));
+            s = fe_from_mont(fn, s_m);
+        }
+        if (fe_is_zero(r) || fe_is_zero(s)) {  // retry with fresh nonces (protocol.cpp:142-160)
+            status[j] = sign_lane<C, WG>(e[j], d[j], seed, stream0 + j, gt, out, 1);
+            continue;
+        }
+        be32_store(out, r);
+        be32_store(out + 32, s);
+        status[j] = LANE_OK;
+    }
 }
 
 // One lane of sm2b_verify: raw records in, 0/1 out.

@@ -29,24 +29,45 @@ k_verify(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ 
 }
 
 // flags[0] is set when any secret is zero or >= n: the whole call is malformed
-// (capi.cpp:181-184) and the host discards the outputs.
+// (capi.cpp:181-184) and the host discards the outputs.  Each thread signs SIGN_K
+// consecutive lanes and shares the two inversions among them (sign_lanes).
+constexpr int SIGN_K = 4;
+
 template <class C>
 __global__ void __launch_bounds__(SIGN_THREADS)
 k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ sec, uint64_t seed,
        uint64_t lane_base, const uint32_t* __restrict__ gtab, uint8_t* __restrict__ sig,
        int32_t* __restrict__ status, uint32_t* __restrict__ flags) {
-    const size_t i = blockIdx.x * (size_t)SIGN_THREADS + threadIdx.x;
-    if (i >= n) return;
+    const size_t i0 = (blockIdx.x * (size_t)SIGN_THREADS + threadIdx.x) * SIGN_K;
+    if (i0 >= n) return;
     GTable<GECC_WG> gt{gtab};
-    fe d = be32_load(sec + 32 * i);
-    if (!scalar_in_range<typename C::Fn>(d)) {
-        atomicOr(flags, 1u);
-        status[i] = 2;
-        for (int b = 0; b < 64; ++b) sig[64 * i + b] = 0;
+    fe e[SIGN_K], d[SIGN_K];
+    bool all_ok = i0 + SIGN_K <= n;
+#pragma unroll 1
+    for (int j = 0; j < SIGN_K && i0 + j < n; ++j) {
+        d[j] = be32_load(sec + 32 * (i0 + j));
+        e[j] = scalar_reduce_once<typename C::Fn>(be32_load(dig + 32 * (i0 + j)));
+        if (!scalar_in_range<typename C::Fn>(d[j])) all_ok = false;
+    }
+    if (all_ok) {
+        int st[SIGN_K];
+        sign_lanes<C, GECC_WG, SIGN_K>(e, d, seed, lane_base + i0, gt, sig + 64 * i0, st);
+#pragma unroll
+        for (int j = 0; j < SIGN_K; ++j) status[i0 + j] = st[j];
         return;
     }
-    fe e = scalar_reduce_once<typename C::Fn>(be32_load(dig + 32 * i));
-    status[i] = sign_lane<C, GECC_WG>(e, d, seed, lane_base + i, gt, sig + 64 * i);
+    // ragged tail or a malformed secret in this group: lane by lane
+#pragma unroll 1
+    for (int j = 0; j < SIGN_K && i0 + j < n; ++j) {
+        const size_t i = i0 + j;
+        if (!scalar_in_range<typename C::Fn>(d[j])) {
+            atomicOr(flags, 1u);
+            status[i] = 2;
+            for (int b = 0; b < 64; ++b) sig[64 * i + b] = 0;
+            continue;
+        }
+        status[i] = sign_lane<C, GECC_WG>(e[j], d[j], seed, lane_base + i, gt, sig + 64 * i);
+    }
 }
 
 // capi.cpp:145-169: secret = nonce stream (lane, attempt 0), public = secret * G
@@ -250,7 +271,7 @@ cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* 
                         uint64_t lane_base, const uint32_t* gtab, uint8_t* sig, int32_t* status,
                         uint32_t* flags, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const int b = blocks_for(n, SIGN_THREADS);
+    const int b = blocks_for((n + SIGN_K - 1) / SIGN_K, SIGN_THREADS);
     GECC_BY_CURVE(curve,
         (k_sign<SecpEcdsaCurve><<<b, SIGN_THREADS, 0, s>>>(n, dig, sec, seed, lane_base, gtab, sig, status, flags)),
         (k_sign<Sm2Curve><<<b, SIGN_THREADS, 0, s>>>(n, dig, sec, seed, lane_base, gtab, sig, status, flags)));

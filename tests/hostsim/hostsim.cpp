@@ -135,7 +135,19 @@ template <class C>
 int sign_t(size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed, uint64_t base,
            uint8_t* sig, int32_t* st) {
     GTable<HS_WG> gt{host_gtable<C>().data()};
-    for (size_t i = 0; i < n; ++i) {
+    constexpr int K = 4;  // same grouping as k_sign: shared inversions inside a group
+    size_t i = 0;
+    for (; i + K <= n; i += K) {
+        fe e[K], d[K];
+        int s4[K];
+        for (int j = 0; j < K; ++j) {
+            e[j] = scalar_reduce_once<typename C::Fn>(be32_load(dig + 32 * (i + j)));
+            d[j] = be32_load(sec + 32 * (i + j));
+        }
+        sign_lanes<C, HS_WG, K>(e, d, seed, base + i, gt, sig + 64 * i, s4);
+        for (int j = 0; j < K; ++j) st[i + j] = s4[j];
+    }
+    for (; i < n; ++i) {
         fe e = scalar_reduce_once<typename C::Fn>(be32_load(dig + 32 * i));
         fe d = be32_load(sec + 32 * i);
         st[i] = sign_lane<C, HS_WG>(e, d, seed, base + i, gt, sig + 64 * i);

@@ -168,3 +168,24 @@ def test_bench_run_gpu(ctxs):
         assert sm2.bench_run("padd", "affine-batch", 8, repeats=0)[0] == 1
     rc, rep = ctxs[1].bench_run("verify", "affine-batch", 1 << 14, repeats=3)
     assert rc == 0 and rep["equivalence_checked"] == 1
+
+
+@pytest.mark.parametrize("cid", [0, 1])
+def test_sign_group_retry_and_ragged_gpu(ctxs, cid):
+    """k_sign signs 4 lanes per thread with shared inversions: forced retry inside a group,
+    ragged batch sizes (tail lanes), and a malformed secret inside a group."""
+    c, ctx = E.CURVES[cid], ctxs[cid]
+    rng = random.Random(199 + cid)
+    n, seed, rig = 11, 13, 5
+    sec = b"".join(E.be32(rng.randrange(1, c.n)) for _ in range(n))
+    dig = bytearray(rng.randrange(256) for _ in range(32 * n))
+    d = int.from_bytes(sec[32 * rig:32 * rig + 32], "big")
+    r0 = E.ec_mul(c, E.nonce(c, seed, rig, 0), c.G)[0] % c.n
+    dig[32 * rig:32 * rig + 32] = E.be32((-r0 * d) % c.n)
+    want = O.ecdsa_sign(cid, bytes(dig), sec, seed)
+    assert ctx.sign(bytes(dig), sec, seed) == want
+    for m in (1, 2, 3, 4, 5, 7, 9):
+        assert ctx.sign(bytes(dig[:32 * m]), sec[:32 * m], seed) == O.ecdsa_sign(cid, bytes(dig[:32 * m]), sec[:32 * m], seed)
+    bad = bytearray(sec)
+    bad[32 * 6:32 * 7] = bytes(32)
+    assert ctx.sign(bytes(dig), bytes(bad), seed)[0] == 2

@@ -146,3 +146,23 @@ def test_hostsim_lazy_curve_ecdsa_golden():
         assert list(H.verify(cid, d, p, sg)) == case["results"], case["name"]
     rt = ent["retry"]
     assert H.sign(cid, bytes.fromhex(rt["digests"]), bytes.fromhex(rt["secrets"]), rt["nonce_seed"])[0].hex() == rt["sigs"]
+
+
+@pytest.mark.parametrize("cid,hs_curve", [(0, 0), (1, 1), (1, 2)])
+def test_hostsim_sign_group_retry(cid, hs_curve):
+    """A forced s == 0 on attempt 0 INSIDE a 4-lane group (shared inversions) must retry that
+    lane with a fresh nonce exactly as the reference does (test_protocol.cpp:196-228)."""
+    c = E.CURVES[cid]
+    rng = random.Random(99 + cid)
+    n, seed, rig = 8, 13, 5
+    sec = b"".join(E.be32(rng.randrange(1, c.n)) for _ in range(n))
+    dig = bytearray(rng.randrange(256) for _ in range(32 * n))
+    d = int.from_bytes(sec[32 * rig:32 * rig + 32], "big")
+    k0 = E.nonce(c, seed, rig, 0)
+    r0 = E.ec_mul(c, k0, c.G)[0] % c.n
+    dig[32 * rig:32 * rig + 32] = E.be32((-r0 * d) % c.n)      # e + r d == 0  ->  s == 0
+    want = O.ecdsa_sign(cid, bytes(dig), sec, seed)
+    assert want[2] == [0] * n
+    k1 = E.nonce(c, seed, rig, 1)
+    assert want[1][64 * rig:64 * rig + 32] == E.be32(E.ec_mul(c, k1, c.G)[0] % c.n)  # really retried
+    assert H.sign(hs_curve, bytes(dig), sec, seed) == (want[1], want[2])
