@@ -286,29 +286,35 @@ sm2b_status gecc_microbench(sm2b_ctx* ctx, int which, int iters, double* ops_per
 //   batch_invert  (3N-3, 0, 0, 1)            batch_padd (6N-3, 0, 6N, 1)
 //   batch_fpmul   256*(6N+3(L-1), 0, 7N, 1)  batch_upmul 256*(14N+3(L-1), 5N, 11N, 1)
 namespace {
-uint64_t eff_lanes(const sm2b_ctx* ctx, size_t n) {  // BatchConfig::effective_lanes + LanePlan clamp
-    uint64_t l = ctx->lanes;
+// lane policy + counters; sm2b_ctx derives its own, sm2b_bench_run builds a scratch one
+struct Ledger {
+    sm2b_op_counts* ops;
+    uint32_t lanes, workers;
+};
+uint64_t eff_lanes(const Ledger& L, size_t n) {  // BatchConfig::effective_lanes + LanePlan clamp
+    uint64_t l = L.lanes;
     if (l == 0) {
-        uint64_t w = ctx->workers ? ctx->workers : 1;
+        uint64_t w = L.workers ? L.workers : 1;
         l = w * 4;
     }
     if (l > n) l = n ? n : 1;
     return l;
 }
-void led(sm2b_ctx* ctx, uint64_t mul, uint64_t add, uint64_t sub, uint64_t inv) {
-    ctx->ledger.modmul += mul;
-    ctx->ledger.modadd += add;
-    ctx->ledger.modsub += sub;
-    ctx->ledger.modinv += inv;
+void led(const Ledger& L, uint64_t mul, uint64_t add, uint64_t sub, uint64_t inv) {
+    L.ops->modmul += mul;
+    L.ops->modadd += add;
+    L.ops->modsub += sub;
+    L.ops->modinv += inv;
 }
-void led_invert(sm2b_ctx* c, uint64_t n) { if (n) led(c, 3 * n - 3, 0, 0, 1); }
-void led_padd(sm2b_ctx* c, uint64_t n) { if (n) led(c, 6 * n - 3, 0, 6 * n, 1); }
-void led_fpmul(sm2b_ctx* c, uint64_t n) {
-    if (n) led(c, 256 * (6 * n + 3 * (eff_lanes(c, n) - 1)), 0, 256 * 7 * n, 256);
+void led_invert(const Ledger& L, uint64_t n) { if (n) led(L, 3 * n - 3, 0, 0, 1); }
+void led_padd(const Ledger& L, uint64_t n) { if (n) led(L, 6 * n - 3, 0, 6 * n, 1); }
+void led_fpmul(const Ledger& L, uint64_t n) {
+    if (n) led(L, 256 * (6 * n + 3 * (eff_lanes(L, n) - 1)), 0, 256 * 7 * n, 256);
 }
-void led_upmul(sm2b_ctx* c, uint64_t n) {
-    if (n) led(c, 256 * (14 * n + 3 * (eff_lanes(c, n) - 1)), 256 * 5 * n, 256 * 11 * n, 256);
+void led_upmul(const Ledger& L, uint64_t n) {
+    if (n) led(L, 256 * (14 * n + 3 * (eff_lanes(L, n) - 1)), 256 * 5 * n, 256 * 11 * n, 256);
 }
+Ledger ledger_of(sm2b_ctx* ctx) { return Ledger{&ctx->ledger, ctx->lanes, ctx->workers}; }
 }  // namespace
 
 // ------------------------------------------------------------------ host-API pipeline
@@ -361,11 +367,11 @@ sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
     CU(ctx, launch_verify(ctx->curve, count, digests, publics, signatures, ctx->gtab_rec, results,
                           ctx->stream));
     ctx->launches += count ? 1 : 0;
-    led_invert(ctx, count);
-    led(ctx, 2 * count, 0, 0, 0);
-    led_fpmul(ctx, count);
-    led_upmul(ctx, count);
-    led_padd(ctx, count);
+    led_invert(ledger_of(ctx), count);
+    led(ledger_of(ctx), 2 * count, 0, 0, 0);
+    led_fpmul(ledger_of(ctx), count);
+    led_upmul(ledger_of(ctx), count);
+    led_padd(ledger_of(ctx), count);
     return SM2B_OK;
 }
 
@@ -403,11 +409,11 @@ sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
         CU(ctx, cudaMemcpyAsync(results + b, dr + b, m, cudaMemcpyDeviceToHost, ctx->d2h_stream));
     }
     ctx->launches += ch.n;
-    led_invert(ctx, count);
-    led(ctx, 2 * count, 0, 0, 0);
-    led_fpmul(ctx, count);
-    led_upmul(ctx, count);
-    led_padd(ctx, count);
+    led_invert(ledger_of(ctx), count);
+    led(ledger_of(ctx), 2 * count, 0, 0, 0);
+    led_fpmul(ledger_of(ctx), count);
+    led_upmul(ledger_of(ctx), count);
+    led_padd(ledger_of(ctx), count);
     CU(ctx, cudaStreamSynchronize(ctx->d2h_stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     return SM2B_OK;
@@ -425,9 +431,9 @@ sm2b_status gecc_sign_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
     CU(ctx, launch_sign(ctx->curve, count, digests, secrets, nonce_seed, lane_base, ctx->gtab_rec,
                         signatures, lane_status, ctx->flags, ctx->stream));
     ctx->launches += count ? 1 : 0;
-    led_fpmul(ctx, count);
-    led_invert(ctx, count);
-    led(ctx, 2 * count, count, 0, 0);
+    led_fpmul(ledger_of(ctx), count);
+    led_invert(ledger_of(ctx), count);
+    led(ledger_of(ctx), 2 * count, count, 0, 0);
     return SM2B_OK;
 }
 
@@ -491,9 +497,9 @@ sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const
                             dsig + 64 * b, dst + b, ctx->flags, ctx->stream));
     }
     ctx->launches += ch.n;
-    led_fpmul(ctx, count);
-    led_invert(ctx, count);
-    led(ctx, 2 * count, count, 0, 0);
+    led_fpmul(ledger_of(ctx), count);
+    led_invert(ledger_of(ctx), count);
+    led(ledger_of(ctx), 2 * count, count, 0, 0);
     uint32_t flag = 0;
     CU(ctx, cudaMemcpyAsync(&flag, ctx->flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
@@ -535,7 +541,7 @@ sm2b_status gecc_keygen(sm2b_ctx* ctx, uint64_t seed, uint64_t lane_base, size_t
     uint8_t* dpub = co.take<uint8_t>(65 * count);
     CU(ctx, launch_keygen(ctx->curve, count, seed, lane_base, ctx->gtab_rec, dsec, dpub, ctx->stream));
     ctx->launches += 1;
-    led_fpmul(ctx, count);
+    led_fpmul(ledger_of(ctx), count);
     CU(ctx, cudaMemcpyAsync(secrets, dsec, 32 * count, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaMemcpyAsync(publics, dpub, 65 * count, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
@@ -567,7 +573,7 @@ sm2b_status sm2b_ecdh(sm2b_ctx* ctx, size_t count, const uint8_t* secrets, const
         CU(ctx, cudaMemsetAsync(ctx->flags, 0, 4, ctx->stream));
         CU(ctx, launch_ecdh(ctx->curve, count, dsec, dpeer, dsh, dst, ctx->flags, ctx->stream));
         ctx->launches += 1;
-        led_upmul(ctx, count);
+        led_upmul(ledger_of(ctx), count);
         CU(ctx, cudaMemcpyAsync(&flag, ctx->flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
         CU(ctx, cudaMemcpyAsync(hst.data(), dst, 4 * count, cudaMemcpyDeviceToHost, ctx->stream));
         CU(ctx, cudaStreamSynchronize(ctx->stream));
@@ -586,7 +592,7 @@ sm2b_status gecc_batch_invert_dev(sm2b_ctx* ctx, gecc_field field, size_t n, con
     DeviceGuard g(ctx->device);
     CU(ctx, launch_batch_invert(ctx->curve, field, n, in, out, ctx->stream));
     ctx->launches += n ? 1 : 0;
-    led_invert(ctx, n);
+    led_invert(ledger_of(ctx), n);
     return SM2B_OK;
 }
 sm2b_status gecc_batch_padd_dev(sm2b_ctx* ctx, size_t n, const uint32_t* px, const uint32_t* py,
@@ -598,7 +604,7 @@ sm2b_status gecc_batch_padd_dev(sm2b_ctx* ctx, size_t n, const uint32_t* px, con
     DeviceGuard g(ctx->device);
     CU(ctx, launch_batch_padd(ctx->curve, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, ctx->stream));
     ctx->launches += n ? 1 : 0;
-    led_padd(ctx, n);
+    led_padd(ledger_of(ctx), n);
     return SM2B_OK;
 }
 sm2b_status gecc_batch_pdbl_dev(sm2b_ctx* ctx, size_t n, const uint32_t* px, const uint32_t* py,
@@ -608,7 +614,7 @@ sm2b_status gecc_batch_pdbl_dev(sm2b_ctx* ctx, size_t n, const uint32_t* px, con
     DeviceGuard g(ctx->device);
     CU(ctx, launch_batch_pdbl(ctx->curve, n, px, py, pinf, ox, oy, oinf, ctx->stream));
     ctx->launches += n ? 1 : 0;
-    if (n) led(ctx, 7 * n - 3, 4 * n, 4 * n, 1);
+    if (n) led(ledger_of(ctx), 7 * n - 3, 4 * n, 4 * n, 1);
     return SM2B_OK;
 }
 sm2b_status gecc_batch_fpmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, uint32_t* ox,
@@ -618,7 +624,7 @@ sm2b_status gecc_batch_fpmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalar
     DeviceGuard g(ctx->device);
     CU(ctx, launch_fpmul(ctx->curve, n, scalars, ctx->gtab, ox, oy, oinf, ctx->stream));
     ctx->launches += n ? 1 : 0;
-    led_fpmul(ctx, n);
+    led_fpmul(ledger_of(ctx), n);
     return SM2B_OK;
 }
 sm2b_status gecc_batch_upmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars,
@@ -630,7 +636,7 @@ sm2b_status gecc_batch_upmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalar
     DeviceGuard g(ctx->device);
     CU(ctx, launch_upmul(ctx->curve, n, scalars, px, py, pinf, ox, oy, oinf, ctx->stream));
     ctx->launches += n ? 1 : 0;
-    led_upmul(ctx, n);
+    led_upmul(ledger_of(ctx), n);
     return SM2B_OK;
 }
 
@@ -894,10 +900,8 @@ sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, 
     std::sort(ms.begin(), ms.end());
     ctx->launches += 8 + repeats;
     // ---- report: ledger of one run in the reference's closed forms
-    sm2b_ctx tmp_counts_holder;  // only its ledger / lanes / workers fields are used
-    tmp_counts_holder.lanes = (uint32_t)lanes ? (uint32_t)lanes : ctx->lanes;
-    tmp_counts_holder.workers = workers ? workers : ctx->workers;
-    sm2b_ctx* t = &tmp_counts_holder;
+    sm2b_op_counts run_ops{0, 0, 0, 0};
+    const Ledger t{&run_ops, (uint32_t)lanes ? (uint32_t)lanes : ctx->lanes, workers ? workers : ctx->workers};
     if (batch) {
         if (opi == 0) led_padd(t, n);
         else if (opi == 1) led_fpmul(t, n);
@@ -911,8 +915,8 @@ sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, 
     out->lanes_used = eff_lanes(t, n);
     out->wall_seconds = ms[ms.size() / 2] * 1e-3;
     out->throughput = out->wall_seconds > 0 ? (double)n / out->wall_seconds : 0.0;
-    out->ops = t->ledger;
-    out->modeled_cost = (t->ledger.modadd + t->ledger.modsub) + 5 * t->ledger.modmul + 500 * t->ledger.modinv;
+    out->ops = run_ops;
+    out->modeled_cost = (run_ops.modadd + run_ops.modsub) + 5 * run_ops.modmul + 500 * run_ops.modinv;
     out->equivalence_checked = 1;
     return SM2B_OK;
 }
