@@ -51,6 +51,7 @@ struct sm2b_ctx {
     uint64_t launches = 0;
     std::string last_error;
     DevBuf in, out, scratch;
+    DevBuf lane_tabs;  // per-lane point tables of the verify kernel (512 B per lane, capped)
     uint32_t* gtab = nullptr;   // fixed-base table (Montgomery form), built on the GPU at creation
     uint32_t* gtab_rec = nullptr;  // table of the byte-record kernels (== gtab on SM2, plain form on secp256k1)
     uint32_t* flags = nullptr;  // device word: malformed-call flag of sign / ecdh
@@ -168,6 +169,7 @@ void sm2b_ctx_free(sm2b_ctx* ctx) {
         ctx->in.release();
         ctx->out.release();
         ctx->scratch.release();
+        ctx->lane_tabs.release();
         if (ctx->gtab_rec && ctx->gtab_rec != ctx->gtab) cudaFree(ctx->gtab_rec);
         if (ctx->gtab) cudaFree(ctx->gtab);
         if (ctx->flags) cudaFree(ctx->flags);
@@ -357,6 +359,16 @@ struct EventPool {  // events of one pipelined call; destroyed at scope exit
 extern "C" {
 
 // ------------------------------------------------------------------ protocol layer
+} // extern "C"
+namespace {
+constexpr size_t VERIFY_SCRATCH_MAX_LANES = (size_t)1 << 22;  // 2 GiB of lane tables at most
+// returns the number of lanes the verify scratch covers (0 on allocation failure)
+size_t ensure_lane_tabs(sm2b_ctx* ctx, size_t count) {
+    const size_t lanes = count < VERIFY_SCRATCH_MAX_LANES ? count : VERIFY_SCRATCH_MAX_LANES;
+    return ctx->lane_tabs.ensure(verify_scratch_bytes(lanes)) == cudaSuccess ? lanes : 0;
+}
+}  // namespace
+extern "C" {
 sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
                             const uint8_t* publics, const uint8_t* signatures,
                             uint8_t* results) {
@@ -364,8 +376,9 @@ sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
         return SM2B_ERROR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
+    const size_t tab_lanes = ensure_lane_tabs(ctx, count);
     CU(ctx, launch_verify(ctx->curve, count, digests, publics, signatures, ctx->gtab_rec, results,
-                          ctx->stream));
+                          (uint32_t*)ctx->lane_tabs.p, tab_lanes, ctx->stream));
     ctx->launches += count ? 1 : 0;
     led_invert(ledger_of(ctx), count);
     led(ledger_of(ctx), 2 * count, 0, 0, 0);
@@ -390,6 +403,7 @@ sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
     uint8_t* ds = ci.take<uint8_t>(64 * count);
     uint8_t* dr = (uint8_t*)ctx->out.p;
     const Chunks ch(count);
+    const size_t tab_lanes = ensure_lane_tabs(ctx, ch.size);
     EventPool pool;
     // the arenas may still be in use by earlier work on the compute stream
     cudaEvent_t idle = pool.get();
@@ -403,7 +417,8 @@ sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
         cudaEvent_t up = pool.get(), done = pool.get();
         CU(ctx, cudaEventRecord(up, ctx->h2d_stream));
         CU(ctx, cudaStreamWaitEvent(ctx->stream, up, 0));
-        CU(ctx, launch_verify(ctx->curve, m, dd + 32 * b, dp + 65 * b, ds + 64 * b, ctx->gtab_rec, dr + b, ctx->stream));
+        CU(ctx, launch_verify(ctx->curve, m, dd + 32 * b, dp + 65 * b, ds + 64 * b, ctx->gtab_rec, dr + b,
+                              (uint32_t*)ctx->lane_tabs.p, tab_lanes, ctx->stream));
         CU(ctx, cudaEventRecord(done, ctx->stream));
         CU(ctx, cudaStreamWaitEvent(ctx->d2h_stream, done, 0));
         CU(ctx, cudaMemcpyAsync(results + b, dr + b, m, cudaMemcpyDeviceToHost, ctx->d2h_stream));
@@ -812,6 +827,7 @@ sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, 
     b.pub = cv.take<uint8_t>(65 * n); b.sig = cv.take<uint8_t>(64 * n);
     b.res = cv.take<uint8_t>(n); b.st = cv.take<int32_t>(n);
     cudaStream_t s = ctx->stream;
+    const size_t tab_lanes = ensure_lane_tabs(ctx, n);
     const int cv_ = ctx->curve;
     const uint32_t* gt = ctx->gtab;          // column-buffer kernels
     const uint32_t* gr = ctx->gtab_rec;      // byte-record kernels
@@ -849,7 +865,7 @@ sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, 
                 return launch_sign(cv_, n, b.dig, b.sec, seed, 0, gr, b.sig, b.st, ctx->flags, s);
             }
             default:
-                return launch_verify(cv_, n, b.dig, b.pub, b.sig, gr, b.res, s);
+                return launch_verify(cv_, n, b.dig, b.pub, b.sig, gr, b.res, (uint32_t*)ctx->lane_tabs.p, tab_lanes, s);
         }
     };
     // ---- equivalence gate
@@ -868,7 +884,7 @@ sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, 
         CU(ctx, cudaStreamSynchronize(s));
         agree = ha == hb && ia == ib;
     } else {
-        CU(ctx, launch_verify(cv_, n, b.dig, b.pub, b.sig, gr, b.res, s));
+        CU(ctx, launch_verify(cv_, n, b.dig, b.pub, b.sig, gr, b.res, (uint32_t*)ctx->lane_tabs.p, tab_lanes, s));
         std::vector<uint8_t> hr(n);
         std::vector<int32_t> hs(n);
         CU(ctx, cudaMemcpyAsync(hr.data(), b.res, n, cudaMemcpyDeviceToHost, s));

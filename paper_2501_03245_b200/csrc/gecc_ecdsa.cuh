@@ -164,6 +164,16 @@ struct LaneTable {
     uint32_t* base;
     int stride;
     GECC_HD void store(int e, const aff& p) const {
+#if defined(__CUDA_ARCH__)
+        if (stride == 1) {  // table in global memory, 64 B per entry, 16-byte aligned by construction
+            uint4* q = reinterpret_cast<uint4*>(base + e * 16);
+            q[0] = make_uint4(p.x.w[0], p.x.w[1], p.x.w[2], p.x.w[3]);
+            q[1] = make_uint4(p.x.w[4], p.x.w[5], p.x.w[6], p.x.w[7]);
+            q[2] = make_uint4(p.y.w[0], p.y.w[1], p.y.w[2], p.y.w[3]);
+            q[3] = make_uint4(p.y.w[4], p.y.w[5], p.y.w[6], p.y.w[7]);
+            return;
+        }
+#endif
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             base[(size_t)(e * 16 + i) * stride] = p.x.w[i];
@@ -172,6 +182,17 @@ struct LaneTable {
     }
     GECC_HD aff load(int e) const {
         aff p;
+#if defined(__CUDA_ARCH__)
+        if (stride == 1) {
+            const uint4* q = reinterpret_cast<const uint4*>(base + e * 16);
+            uint4 a = q[0], b = q[1], c = q[2], d = q[3];
+            p.x.w[0] = a.x; p.x.w[1] = a.y; p.x.w[2] = a.z; p.x.w[3] = a.w;
+            p.x.w[4] = b.x; p.x.w[5] = b.y; p.x.w[6] = b.z; p.x.w[7] = b.w;
+            p.y.w[0] = c.x; p.y.w[1] = c.y; p.y.w[2] = c.z; p.y.w[3] = c.w;
+            p.y.w[4] = d.x; p.y.w[5] = d.y; p.y.w[6] = d.z; p.y.w[7] = d.w;
+            return p;
+        }
+#endif
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             p.x.w[i] = base[(size_t)(e * 16 + i) * stride];

@@ -28,6 +28,20 @@ k_verify(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ 
     res[i] = verify_lane<C, GECC_WG>(dig + 32 * i, pub + 65 * i, sig + 64 * i, gt, qt);
 }
 
+// Lane tables in global memory (512 B per lane, read back through L2): no shared memory,
+// so residency is limited by registers only.
+template <class C, int THREADS, int BLOCKS_PER_SM>
+__global__ void __launch_bounds__(THREADS, BLOCKS_PER_SM)
+k_verify_gtab(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ pub,
+              const uint8_t* __restrict__ sig, const uint32_t* __restrict__ gtab,
+              uint32_t* __restrict__ lane_tables, uint8_t* __restrict__ res) {
+    const size_t i = blockIdx.x * (size_t)THREADS + threadIdx.x;
+    if (i >= n) return;
+    GTable<GECC_WG> gt{gtab};
+    LaneTable qt{lane_tables + i * 128, 1};
+    res[i] = verify_lane<C, GECC_WG>(dig + 32 * i, pub + 65 * i, sig + 64 * i, gt, qt);
+}
+
 // flags[0] is set when any secret is zero or >= n: the whole call is malformed
 // (capi.cpp:181-184) and the host discards the outputs.  Each thread signs SIGN_K
 // consecutive lanes and shares the two inversions among them (sign_lanes).
@@ -252,19 +266,37 @@ static cudaError_t launch_verify_t(size_t n, const uint8_t* dig, const uint8_t* 
     return cudaGetLastError();
 }
 
+// Production shape: lane tables in global memory, 128 threads x 4 blocks per SM (16 warps,
+// 128 registers): measured 26.6 ms per 2^20 against 28.9 ms for the shared-memory shape
+// (12 warps; 512 B of shared memory per lane caps an SM at 14 warps).  The resident lanes'
+// tables (148 x 512 lanes x 512 B = 39 MB) stay in the 126 MB L2; each entry is one 64-byte
+// vector read.  GECC_VERIFY_SHAPE=smem selects the shared-memory kernel for comparison.
+size_t verify_scratch_bytes(size_t lanes) { return lanes * 512; }
+
 cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t* pub,
-                          const uint8_t* sig, const uint32_t* gtab, uint8_t* res, cudaStream_t s) {
+                          const uint8_t* sig, const uint32_t* gtab, uint8_t* res,
+                          uint32_t* lane_scratch, size_t scratch_lanes, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    // GECC_VERIFY_SHAPE=64x7 selects the alternative launch shape (14 warps per SM, measured slower) (tuning experiments only)
-    static const bool wide = [] {
+    static const bool use_smem = [] {
         const char* v = getenv("GECC_VERIFY_SHAPE");
-        return !(v && !strcmp(v, "64x7"));
+        return v && !strcmp(v, "smem");
     }();
-    if (curve == CURVE_SECP)
-        return wide ? launch_verify_t<SecpEcdsaCurve, 128, 3>(n, dig, pub, sig, gtab, res, s)
-                    : launch_verify_t<SecpEcdsaCurve, 64, 7>(n, dig, pub, sig, gtab, res, s);
-    return wide ? launch_verify_t<Sm2Curve, 128, 3>(n, dig, pub, sig, gtab, res, s)
-                : launch_verify_t<Sm2Curve, 64, 7>(n, dig, pub, sig, gtab, res, s);
+    if (use_smem || !lane_scratch || scratch_lanes == 0) {
+        if (curve == CURVE_SECP) return launch_verify_t<SecpEcdsaCurve, 128, 3>(n, dig, pub, sig, gtab, res, s);
+        return launch_verify_t<Sm2Curve, 128, 3>(n, dig, pub, sig, gtab, res, s);
+    }
+    // kernels on one stream run back to back, so consecutive pieces may reuse the scratch
+    for (size_t at = 0; at < n; at += scratch_lanes) {
+        const size_t m = n - at < scratch_lanes ? n - at : scratch_lanes;
+        const int b = blocks_for(m, 128);
+        if (curve == CURVE_SECP)
+            k_verify_gtab<SecpEcdsaCurve, 128, 4><<<b, 128, 0, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at,
+                                                                    gtab, lane_scratch, res + at);
+        else
+            k_verify_gtab<Sm2Curve, 128, 4><<<b, 128, 0, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at, gtab,
+                                                              lane_scratch, res + at);
+    }
+    return cudaGetLastError();
 }
 
 cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed,
