@@ -586,7 +586,9 @@ sm2b_status sm2b_ecdh(sm2b_ctx* ctx, size_t count, const uint8_t* secrets, const
         CU(ctx, cudaMemcpyAsync(dsec, secrets, 32 * count, cudaMemcpyHostToDevice, ctx->stream));
         CU(ctx, cudaMemcpyAsync(dpeer, peers, 65 * count, cudaMemcpyHostToDevice, ctx->stream));
         CU(ctx, cudaMemsetAsync(ctx->flags, 0, 4, ctx->stream));
-        CU(ctx, launch_ecdh(ctx->curve, count, dsec, dpeer, dsh, dst, ctx->flags, ctx->stream));
+        const size_t tab_lanes = ensure_lane_tabs(ctx, count);
+        CU(ctx, launch_ecdh(ctx->curve, count, dsec, dpeer, dsh, dst, ctx->flags, (uint32_t*)ctx->lane_tabs.p,
+                            tab_lanes, ctx->stream));
         ctx->launches += 1;
         led_upmul(ledger_of(ctx), count);
         CU(ctx, cudaMemcpyAsync(&flag, ctx->flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
@@ -649,7 +651,9 @@ sm2b_status gecc_batch_upmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalar
         return SM2B_ERROR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
-    CU(ctx, launch_upmul(ctx->curve, n, scalars, px, py, pinf, ox, oy, oinf, ctx->stream));
+    CU(ctx, ctx->lane_tabs.ensure(verify_scratch_bytes(n)));
+    CU(ctx, launch_upmul(ctx->curve, n, scalars, px, py, pinf, ox, oy, oinf, (uint32_t*)ctx->lane_tabs.p,
+                         ctx->stream));
     ctx->launches += n ? 1 : 0;
     led_upmul(ledger_of(ctx), n);
     return SM2B_OK;
@@ -827,7 +831,8 @@ sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, 
     b.pub = cv.take<uint8_t>(65 * n); b.sig = cv.take<uint8_t>(64 * n);
     b.res = cv.take<uint8_t>(n); b.st = cv.take<int32_t>(n);
     cudaStream_t s = ctx->stream;
-    const size_t tab_lanes = ensure_lane_tabs(ctx, n);
+    CU(ctx, ctx->lane_tabs.ensure(verify_scratch_bytes(n)));  // upmul needs all n lanes covered
+    const size_t tab_lanes = n;
     const int cv_ = ctx->curve;
     const uint32_t* gt = ctx->gtab;          // column-buffer kernels
     const uint32_t* gr = ctx->gtab_rec;      // byte-record kernels
@@ -857,7 +862,7 @@ sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, 
                 return use_batch ? launch_fpmul(cv_, n, b.k, gt, ox, oy, oi, s)
                                  : launch_pmul_serial(cv_, n, b.k, nullptr, nullptr, nullptr, ox, oy, oi, s);
             case 2:
-                return use_batch ? launch_upmul(cv_, n, b.k, b.px, b.py, nullptr, ox, oy, oi, s)
+                return use_batch ? launch_upmul(cv_, n, b.k, b.px, b.py, nullptr, ox, oy, oi, (uint32_t*)ctx->lane_tabs.p, s)
                                  : launch_pmul_serial(cv_, n, b.k, b.px, b.py, nullptr, ox, oy, oi, s);
             case 3: {
                 cudaError_t e = cudaMemsetAsync(ctx->flags, 0, 4, s);

@@ -36,12 +36,14 @@ cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* 
 cudaError_t launch_keygen(int curve, size_t n, uint64_t seed, uint64_t lane_base,
                           const uint32_t* gtab, uint8_t* sec, uint8_t* pub, cudaStream_t s);
 cudaError_t launch_ecdh(int curve, size_t n, const uint8_t* sec, const uint8_t* peers,
-                        uint8_t* shared, int32_t* status, uint32_t* flags, cudaStream_t s);
+                        uint8_t* shared, int32_t* status, uint32_t* flags, uint32_t* lane_scratch,
+                        size_t scratch_lanes, cudaStream_t s);
 cudaError_t launch_fpmul(int curve, size_t n, const uint32_t* k, const uint32_t* gtab, uint32_t* ox,
                          uint32_t* oy, uint8_t* oinf, cudaStream_t s);
+// lane_scratch must cover all n lanes (verify_scratch_bytes(n))
 cudaError_t launch_upmul(int curve, size_t n, const uint32_t* k, const uint32_t* px,
                          const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
-                         uint8_t* oinf, cudaStream_t s);
+                         uint8_t* oinf, uint32_t* lane_scratch, cudaStream_t s);
 
 cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* in, uint32_t* out,
                                 cudaStream_t s);

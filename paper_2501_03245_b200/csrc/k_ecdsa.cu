@@ -102,14 +102,14 @@ k_keygen(size_t n, uint64_t seed, uint64_t lane_base, const uint32_t* __restrict
 // capi.cpp:230-261 + protocol.cpp:224-263.  status: 0 ok, 3 invalid peer,
 // 4 degenerate; a secret >= n flags the whole call malformed.
 template <class C>
-__global__ void __launch_bounds__(VERIFY_THREADS, 3)
+__global__ void __launch_bounds__(VERIFY_THREADS, 4)
 k_ecdh(size_t n, const uint8_t* __restrict__ sec, const uint8_t* __restrict__ peers,
-       uint8_t* __restrict__ shared, int32_t* __restrict__ status, uint32_t* __restrict__ flags) {
-    extern __shared__ uint32_t lane_tables[];
+       uint8_t* __restrict__ shared, int32_t* __restrict__ status, uint32_t* __restrict__ flags,
+       uint32_t* __restrict__ lane_tables) {
     const size_t i = blockIdx.x * (size_t)VERIFY_THREADS + threadIdx.x;
     if (i >= n) return;
     const typename C::Fp f{};
-    LaneTable qt{lane_tables + threadIdx.x, VERIFY_THREADS};
+    LaneTable qt{lane_tables + i * 128, 1};
     for (int b = 0; b < 32; ++b) shared[32 * i + b] = 0;
     fe d = be32_load(sec + 32 * i);
     if (!fe_lt_modulus(typename C::Fn{}, d)) {  // Scalar::checked: zero is allowed here
@@ -161,14 +161,14 @@ k_fpmul(size_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ g
 }
 
 template <class C>
-__global__ void __launch_bounds__(VERIFY_THREADS, 3)
+__global__ void __launch_bounds__(VERIFY_THREADS, 4)
 k_upmul(size_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ px,
         const uint32_t* __restrict__ py, const uint8_t* __restrict__ pinf,
-        uint32_t* __restrict__ ox, uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf) {
-    extern __shared__ uint32_t lane_tables[];
+        uint32_t* __restrict__ ox, uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf,
+        uint32_t* __restrict__ lane_tables) {
     const size_t i = blockIdx.x * (size_t)VERIFY_THREADS + threadIdx.x;
     if (i >= n) return;
-    LaneTable qt{lane_tables + threadIdx.x, VERIFY_THREADS};
+    LaneTable qt{lane_tables + i * 128, 1};
     if (pinf && pinf[i]) {  // infinity input stays infinity (test_batch_point.cpp:231,244)
         store_affine<C>(jac_infinity<C>(), ox, oy, oinf, n, i);
         return;
@@ -236,13 +236,6 @@ k_pmul_serial(size_t n, const uint32_t* __restrict__ k, const uint32_t* __restri
 }
 
 // ---------------------------------------------------------------- launchers
-constexpr size_t LANE_TABLE_SMEM = (size_t)VERIFY_THREADS * 8 * 16 * sizeof(uint32_t);
-
-template <class K>
-static cudaError_t opt_in_smem(K kernel) {
-    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)LANE_TABLE_SMEM);
-}
 static int blocks_for(size_t n, int threads) { return (int)((n + threads - 1) / threads); }
 
 #define GECC_BY_CURVE(curve, EXPR_SECP, EXPR_SM2) \
@@ -321,14 +314,19 @@ cudaError_t launch_keygen(int curve, size_t n, uint64_t seed, uint64_t lane_base
 }
 
 cudaError_t launch_ecdh(int curve, size_t n, const uint8_t* sec, const uint8_t* peers,
-                        uint8_t* shared, int32_t* status, uint32_t* flags, cudaStream_t s) {
+                        uint8_t* shared, int32_t* status, uint32_t* flags, uint32_t* lane_scratch,
+                        size_t scratch_lanes, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    cudaError_t e = curve == CURVE_SECP ? opt_in_smem(k_ecdh<SecpEcdsaCurve>) : opt_in_smem(k_ecdh<Sm2Curve>);
-    if (e != cudaSuccess) return e;
-    const int b = blocks_for(n, VERIFY_THREADS);
-    GECC_BY_CURVE(curve,
-        (k_ecdh<SecpEcdsaCurve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, sec, peers, shared, status, flags)),
-        (k_ecdh<Sm2Curve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, sec, peers, shared, status, flags)));
+    if (!lane_scratch || scratch_lanes == 0) return cudaErrorInvalidValue;
+    for (size_t at = 0; at < n; at += scratch_lanes) {
+        const size_t m = n - at < scratch_lanes ? n - at : scratch_lanes;
+        const int b = blocks_for(m, VERIFY_THREADS);
+        GECC_BY_CURVE(curve,
+            (k_ecdh<SecpEcdsaCurve><<<b, VERIFY_THREADS, 0, s>>>(m, sec + 32 * at, peers + 65 * at, shared + 32 * at,
+                                                                 status + at, flags, lane_scratch)),
+            (k_ecdh<Sm2Curve><<<b, VERIFY_THREADS, 0, s>>>(m, sec + 32 * at, peers + 65 * at, shared + 32 * at,
+                                                           status + at, flags, lane_scratch)));
+    }
     return cudaGetLastError();
 }
 
@@ -342,19 +340,18 @@ cudaError_t launch_fpmul(int curve, size_t n, const uint32_t* k, const uint32_t*
     return cudaGetLastError();
 }
 
+// column buffers are indexed k*n + i, so pieces are not contiguous: the scratch must cover n
 cudaError_t launch_upmul(int curve, size_t n, const uint32_t* k, const uint32_t* px,
                          const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
-                         uint8_t* oinf, cudaStream_t s) {
+                         uint8_t* oinf, uint32_t* lane_scratch, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    cudaError_t e = curve == CURVE_SECP ? opt_in_smem(k_upmul<SecpCurve>) : opt_in_smem(k_upmul<Sm2Curve>);
-    if (e != cudaSuccess) return e;
+    if (!lane_scratch) return cudaErrorInvalidValue;
     const int b = blocks_for(n, VERIFY_THREADS);
     GECC_BY_CURVE(curve,
-        (k_upmul<SecpCurve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, k, px, py, pinf, ox, oy, oinf)),
-        (k_upmul<Sm2Curve><<<b, VERIFY_THREADS, LANE_TABLE_SMEM, s>>>(n, k, px, py, pinf, ox, oy, oinf)));
+        (k_upmul<SecpCurve><<<b, VERIFY_THREADS, 0, s>>>(n, k, px, py, pinf, ox, oy, oinf, lane_scratch)),
+        (k_upmul<Sm2Curve><<<b, VERIFY_THREADS, 0, s>>>(n, k, px, py, pinf, ox, oy, oinf, lane_scratch)));
     return cudaGetLastError();
 }
-
 
 cudaError_t launch_seeded_scalars(int curve, size_t n, uint64_t seed, uint64_t tag, uint32_t* out,
                                   cudaStream_t s) {
