@@ -425,7 +425,7 @@ def _ncu_traffic(wl):
     For k_verify it is well above the 170 MB of records: the excess is per-thread stack
     (2 KB x 2^20 lanes of local memory written back from L1), not re-reads of the inputs."""
     import csv
-    name = {"verify": "r01d_verify_lazyfield", "padd": "r01_padd", "msm": "r01_msm"}.get(wl)
+    name = {"verify": "r01e_verify_globaltab", "padd": "r01_padd", "msm": "r01_msm"}.get(wl)
     if not name:
         return None
     try:
