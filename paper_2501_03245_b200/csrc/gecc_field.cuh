@@ -167,17 +167,28 @@ GECC_HD fe lazy_sub(const fe& a, const fe& b) {
 //   v = t_lo + t_hi * 977 + (t_hi << 32)          (10 limbs, top part V < 2^33 + 2^10)
 //   w = v_lo + V * 977 + (V << 32)                 (carry <= 1)
 //   r = w + carry * c
-// 8 IMAD + 8 IMAD.HI + 2, everything else carry chains; no dependent multiplier sequence.
+// 8 wide multiplies + 2, everything else carry chains; no dependent multiplier sequence.
 GECC_HD fe redc_secp_lazy(const uint32_t* t) {
-    uint32_t s[10];
+    uint32_t s[10], o[8];
+    // even limbs of t_hi: products sit on aligned pairs of s -> one chain of four IMAD.WIDE
     s[0] = mad_lo_cc(t[8], 977u, t[0]);
+    s[1] = madc_hi_cc(t[8], 977u, t[1]);
 #pragma unroll
-    for (int i = 1; i < 8; ++i) s[i] = madc_lo_cc(t[8 + i], 977u, t[i]);
+    for (int i = 2; i < 8; i += 2) {
+        s[i] = madc_lo_cc(t[8 + i], 977u, t[i]);
+        s[i + 1] = madc_hi_cc(t[8 + i], 977u, t[i + 1]);
+    }
     s[8] = addc(0, 0);
-    s[1] = mad_hi_cc(t[8], 977u, s[1]);
+    // odd limbs: four independent wide products, one limb to the left
 #pragma unroll
-    for (int i = 1; i < 7; ++i) s[i + 1] = madc_hi_cc(t[8 + i], 977u, s[i + 1]);
-    s[8] = madc_hi(t[15], 977u, s[8]);  // <= 1 + 976 + 1: no carry out
+    for (int i = 1; i < 8; i += 2) {
+        o[i - 1] = mul_lo(t[8 + i], 977u);
+        o[i] = mul_hi(t[8 + i], 977u);
+    }
+    s[1] = add_cc(s[1], o[0]);
+#pragma unroll
+    for (int i = 1; i < 7; ++i) s[i + 1] = addc_cc(s[i + 1], o[i]);
+    s[8] = addc(s[8], o[7]);  // <= 1 + 976 + 1: no carry out
     s[1] = add_cc(s[1], t[8]);
 #pragma unroll
     for (int i = 1; i < 8; ++i) s[i + 1] = addc_cc(s[i + 1], t[8 + i]);
