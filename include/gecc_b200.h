@@ -202,6 +202,12 @@ sm2b_status gecc_msm_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const
                          const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
                          uint8_t* oinf);
 
+/* Form of the batch_invert / batch_padd / batch_pdbl kernels (process-wide; results are
+ * identical, batch_invert.hpp:59-60): 0 = by batch size (default), 1 = chunked (every thread
+ * runs Montgomery's trick over its own 16 elements), 2 = cooperative (one inversion per thread
+ * block: warp-shuffle scans + shared memory). */
+void gecc_set_batch_form(int form);
+
 /* Integer-pipe issue-rate microbenchmark (roofline denominator).
  * which: 0 IMAD.WIDE.U32 independent, 1 IMAD.WIDE dependent chain, 2 IMAD (32-bit),
  *        3 IMAD.HI, 4 IADD3, 5 IADD3.X carry chain, 6 IMAD.WIDE + IADD3 1:1 mix,

@@ -54,8 +54,18 @@ def lib():
         l.gecc_last_error.argtypes = [C.c_void_p]
         l.gecc_kernel_launches.restype = C.c_uint64
         l.gecc_kernel_launches.argtypes = [C.c_void_p]
+        l.gecc_set_batch_form.argtypes = [C.c_int]
+        l.gecc_set_batch_form.restype = None
         _lib = l
     return _lib
+
+
+BATCH_FORMS = {"auto": 0, "chunked": 1, "coop": 2, "chunked8": 3, "coop128": 4, "coop32": 5, "tiled8": 6, "tiled4": 7}
+
+
+def set_batch_form(form: str):
+    """Pins the batch kernels' form (gecc_set_batch_form): auto | chunked | coop."""
+    lib().gecc_set_batch_form(BATCH_FORMS[form])
 
 
 def cols_from_ints(vals) -> np.ndarray:

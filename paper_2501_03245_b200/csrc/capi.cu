@@ -51,6 +51,7 @@ struct sm2b_ctx {
     uint64_t launches = 0;
     std::string last_error;
     DevBuf in, out, scratch;
+    DevBuf batch_tmp;  // tile totals of the tiled batch_padd form
     DevBuf lane_tabs;  // per-lane point tables of the verify kernel (512 B per lane, capped)
     uint32_t* gtab = nullptr;   // fixed-base table (Montgomery form), built on the GPU at creation
     uint32_t* gtab_rec = nullptr;  // table of the byte-record kernels (== gtab on SM2, plain form on secp256k1)
@@ -169,6 +170,7 @@ void sm2b_ctx_free(sm2b_ctx* ctx) {
         ctx->in.release();
         ctx->out.release();
         ctx->scratch.release();
+        ctx->batch_tmp.release();
         ctx->lane_tabs.release();
         if (ctx->gtab_rec && ctx->gtab_rec != ctx->gtab) cudaFree(ctx->gtab_rec);
         if (ctx->gtab) cudaFree(ctx->gtab);
@@ -269,6 +271,8 @@ sm2b_status gecc_field_op(sm2b_ctx* ctx, gecc_field field, gecc_field_opcode op,
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     return SM2B_OK;
 }
+
+void gecc_set_batch_form(int form) { set_batch_form(form < 0 || form > 7 ? 0 : form); }
 
 sm2b_status gecc_microbench(sm2b_ctx* ctx, int which, int iters, double* ops_per_clk_per_sm,
                             double* seconds, double* total_ops) {
@@ -619,7 +623,9 @@ sm2b_status gecc_batch_padd_dev(sm2b_ctx* ctx, size_t n, const uint32_t* px, con
         return SM2B_ERROR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
-    CU(ctx, launch_batch_padd(ctx->curve, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, ctx->stream));
+    CU(ctx, ctx->batch_tmp.ensure(batch_padd_scratch_bytes(n)));
+    CU(ctx, launch_batch_padd(ctx->curve, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, ctx->stream,
+                              ctx->batch_tmp.p));
     ctx->launches += n ? 1 : 0;
     led_padd(ledger_of(ctx), n);
     return SM2B_OK;

@@ -45,12 +45,16 @@ cudaError_t launch_upmul(int curve, size_t n, const uint32_t* k, const uint32_t*
                          const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
                          uint8_t* oinf, uint32_t* lane_scratch, cudaStream_t s);
 
+// 0 auto (by batch size), 1 chunked (one inversion per thread), 2 cooperative (one per block)
+void set_batch_form(int form);
 cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* in, uint32_t* out,
                                 cudaStream_t s);
 cudaError_t launch_batch_padd(int curve, size_t n, const uint32_t* px, const uint32_t* py,
                               const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty,
                               const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
-                              cudaStream_t s);
+                              cudaStream_t s, void* scratch = nullptr);
+// scratch of the tiled batch_padd form (tile totals); without it the single-launch forms run
+size_t batch_padd_scratch_bytes(size_t n);
 cudaError_t launch_batch_pdbl(int curve, size_t n, const uint32_t* px, const uint32_t* py,
                               const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
                               cudaStream_t s);

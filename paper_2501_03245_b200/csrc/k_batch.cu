@@ -85,8 +85,8 @@ __device__ __forceinline__ fe tangent_numerator(const fe& x) {  // 3x^2 + a
     return fe_add(f, num, curve_a<C>());
 }
 
-template <class C>
-__global__ void __launch_bounds__(BATCH_THREADS)
+template <class C, int MINB>
+__global__ void __launch_bounds__(BATCH_THREADS, MINB)
 k_batch_padd(size_t n, size_t T, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
              const uint8_t* __restrict__ pinf, const uint32_t* __restrict__ tx,
              const uint32_t* __restrict__ ty, const uint8_t* __restrict__ tinf,
@@ -96,10 +96,16 @@ k_batch_padd(size_t n, size_t T, const uint32_t* __restrict__ px, const uint32_t
     if (t >= T || t >= n) return;
     fe acc = fe_one(f);
     size_t last = t;
-    // compress: running product of the denominators, parked in ox
+    // compress: running product of the denominators, parked in ox.  The next pair's x
+    // coordinates are requested before the current product so the loads overlap the multiply.
+    fe ax = col_load(px, n, t), bx = col_load(tx, n, t);
 #pragma unroll 1
     for (size_t i = t; i < n; i += T) {
-        fe ax = col_load(px, n, i), bx = col_load(tx, n, i);
+        fe nax = ax, nbx = bx;
+        if (i + T < n) {
+            nax = col_load(px, n, i + T);
+            nbx = col_load(tx, n, i + T);
+        }
         const bool ai = pinf && pinf[i], bi = tinf && tinf[i];
         fe d = fe_one(f);
         if (!ai && !bi && fe_eq(ax, bx)) {  // y is only needed when the x's collide
@@ -111,6 +117,8 @@ k_batch_padd(size_t n, size_t T, const uint32_t* __restrict__ px, const uint32_t
         acc = fe_mul(f, acc, d);
         col_store(ox, n, i, acc);
         last = i;
+        ax = nax;
+        bx = nbx;
     }
     fe inv = fe_inv(f, acc);
     // scatter + DCWPA: recover each inverse and finish the formulas (batch_point.cpp:124-170)
@@ -184,19 +192,428 @@ k_batch_pdbl(size_t n, size_t T, const uint32_t* __restrict__ px, const uint32_t
     }
 }
 
+// ---------------------------------------------------------------- block-cooperative form
+// Montgomery's trick with ONE inversion per thread block (section 3.3's prefix-product
+// tree, mapped to the SM): a thread folds the denominators of its COOP_K elements into a local
+// prefix product (registers); the per-thread totals are scanned inside each warp with shuffles
+// (inclusive prefix and inclusive suffix, 5 steps each); the 8 warp totals meet in shared
+// memory, warp 0 scans them the same way, inverts the block product once and hands every warp
+// the inverse of its own total; thread j then gets the inverse of its total as
+//     winv[warp] * (exclusive prefix)_j * (exclusive suffix)_j
+// and unwinds its local prefix products.  Elements of a tile are interleaved (element
+// tile + k * COOP_THREADS + tid), so every limb load of a warp is one 128-byte line.
+// Compared with the chunked kernels above this exposes n / COOP_K threads instead of n / 16:
+// it is the form used while the batch is too small to fill the chip with 16-element chunks.
+constexpr int COOP_K = 4;
+
+__device__ __forceinline__ fe fe_shfl_up(const fe& v, int d) {
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.w[i] = __shfl_up_sync(0xFFFFFFFFu, v.w[i], d);
+    return r;
+}
+__device__ __forceinline__ fe fe_shfl_down(const fe& v, int d) {
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.w[i] = __shfl_down_sync(0xFFFFFFFFu, v.w[i], d);
+    return r;
+}
+// inclusive prefix product P and inclusive suffix product Q of t over the 32 lanes of a warp
+template <class F>
+__device__ __forceinline__ void warp_scan_products(const F& f, const fe& t, int lane, int width,
+                                                   fe* P, fe* Q) {
+    *P = t;
+    *Q = t;
+#pragma unroll 1
+    for (int d = 1; d < width; d <<= 1) {
+        fe m = fe_mul(f, *P, fe_shfl_up(*P, d));
+        *P = fe_select(lane >= d, m, *P);
+        fe m2 = fe_mul(f, *Q, fe_shfl_down(*Q, d));
+        *Q = fe_select(lane + d < 32, m2, *Q);
+    }
+}
+// t != 0 on every thread of the block (all COOP_THREADS threads must call).  Returns t^-1.
+// sm: 2 * (COOP_THREADS / 32) field elements of shared memory, word-major.
+template <class F, int COOP_THREADS>
+__device__ fe coop_block_inverse(const F& f, const fe& t, uint32_t* sm) {
+    constexpr int NW = COOP_THREADS / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const fe one = fe_one(f);
+    fe P, Q;
+    warp_scan_products(f, t, lane, 32, &P, &Q);
+    fe E = fe_select(lane == 0, one, fe_shfl_up(P, 1));    // exclusive prefix
+    fe S = fe_select(lane == 31, one, fe_shfl_down(Q, 1)); // exclusive suffix
+    if constexpr (NW == 1) {  // a block of one warp: the warp total is inverted directly
+        fe total;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) total.w[i] = __shfl_sync(0xFFFFFFFFu, P.w[i], 31);
+        return fe_mul(f, fe_mul(f, fe_inv(f, total), E), S);
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sm[i * NW + warp] = P.w[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        fe w = one;
+        if (lane < NW) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w.w[i] = sm[i * NW + lane];
+        }
+        fe PP, QQ;
+        warp_scan_products(f, w, lane, NW, &PP, &QQ);  // lanes >= NW hold one
+        fe total;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) total.w[i] = __shfl_sync(0xFFFFFFFFu, PP.w[i], NW - 1);
+        const fe inv = fe_inv(f, total);  // the block's single inversion
+        fe EE = fe_select(lane == 0, one, fe_shfl_up(PP, 1));
+        fe SS = fe_select(lane == 31, one, fe_shfl_down(QQ, 1));
+        fe wi = fe_mul(f, fe_mul(f, inv, EE), SS);
+        if (lane < NW) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) sm[(8 + i) * NW + lane] = wi.w[i];
+        }
+    }
+    __syncthreads();
+    fe wi;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) wi.w[i] = sm[(8 + i) * NW + warp];
+    return fe_mul(f, fe_mul(f, wi, E), S);
+}
+
+template <class F, int COOP_THREADS>
+__global__ void __launch_bounds__(COOP_THREADS)
+k_batch_invert_coop(size_t n, const uint32_t* __restrict__ in, uint32_t* __restrict__ out) {
+    __shared__ uint32_t sm[16 * (COOP_THREADS / 32)];
+    const F f{};
+    const size_t tile = (size_t)blockIdx.x * (COOP_THREADS * COOP_K) + threadIdx.x;
+    fe lp[COOP_K];
+    fe acc = fe_one(f);
+#pragma unroll
+    for (int k = 0; k < COOP_K; ++k) {
+        const size_t i = tile + (size_t)k * COOP_THREADS;
+        if (i < n) {
+            fe v = col_load(in, n, i);
+            if (!fe_is_zero(v)) acc = fe_mul(f, acc, v);
+        }
+        lp[k] = acc;
+    }
+    fe inv = coop_block_inverse<decltype(f), COOP_THREADS>(f, acc, sm);
+#pragma unroll
+    for (int k = COOP_K - 1; k >= 0; --k) {
+        const size_t i = tile + (size_t)k * COOP_THREADS;
+        if (i < n) {
+            fe v = col_load(in, n, i);
+            const bool zero = fe_is_zero(v);
+            fe r = k > 0 ? fe_mul(f, inv, lp[k > 0 ? k - 1 : 0]) : inv;
+            if (!zero && k > 0) inv = fe_mul(f, inv, v);
+            col_store(out, n, i, zero ? fe_zero() : r);
+        }
+    }
+}
+
+template <class C, int COOP_THREADS>
+__global__ void __launch_bounds__(COOP_THREADS)
+k_batch_padd_coop(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
+                  const uint8_t* __restrict__ pinf, const uint32_t* __restrict__ tx,
+                  const uint32_t* __restrict__ ty, const uint8_t* __restrict__ tinf,
+                  uint32_t* __restrict__ ox, uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf) {
+    __shared__ uint32_t sm[16 * (COOP_THREADS / 32)];
+    const typename C::Fp f{};
+    const size_t tile = (size_t)blockIdx.x * (COOP_THREADS * COOP_K) + threadIdx.x;
+    fe lp[COOP_K];
+    fe acc = fe_one(f);
+#pragma unroll
+    for (int k = 0; k < COOP_K; ++k) {
+        const size_t i = tile + (size_t)k * COOP_THREADS;
+        if (i < n) {
+            fe ax = col_load(px, n, i), bx = col_load(tx, n, i);
+            const bool ai = pinf && pinf[i], bi = tinf && tinf[i];
+            fe d = fe_one(f);
+            if (!ai && !bi && fe_eq(ax, bx)) {
+                fe ay = col_load(py, n, i), by = col_load(ty, n, i);
+                classify_pair<C>(ax, ay, ai, bx, by, bi, &d);
+            } else if (!ai && !bi) {
+                d = fe_sub(f, ax, bx);
+            }
+            acc = fe_mul(f, acc, d);
+        }
+        lp[k] = acc;
+    }
+    fe inv = coop_block_inverse<decltype(f), COOP_THREADS>(f, acc, sm);
+#pragma unroll
+    for (int k = COOP_K - 1; k >= 0; --k) {
+        const size_t i = tile + (size_t)k * COOP_THREADS;
+        if (i < n) {
+            fe ax = col_load(px, n, i), ay = col_load(py, n, i);
+            fe bx = col_load(tx, n, i), by = col_load(ty, n, i);
+            const bool ai = pinf && pinf[i], bi = tinf && tinf[i];
+            fe d = fe_one(f);
+            const uint32_t kind = classify_pair<C>(ax, ay, ai, bx, by, bi, &d);
+            fe dinv = k > 0 ? fe_mul(f, inv, lp[k > 0 ? k - 1 : 0]) : inv;
+            if (k > 0) inv = fe_mul(f, inv, d);
+            fe xr = fe_zero(), yr = fe_zero();
+            uint8_t rinf = 0;
+            if (kind == K_GENERIC) {
+                fe lam = fe_mul(f, fe_sub(f, ay, by), dinv);
+                finish_lambda<C>(lam, ax, bx, ay, &xr, &yr);
+            } else if (kind == K_TANGENT) {
+                fe lam = fe_mul(f, tangent_numerator<C>(ax), dinv);
+                finish_lambda<C>(lam, ax, ax, ay, &xr, &yr);
+            } else if (kind == K_COPY_LEFT) {
+                xr = ax; yr = ay;
+            } else if (kind == K_COPY_RIGHT) {
+                xr = bx; yr = by;
+            } else {
+                rinf = 1;
+            }
+            col_store(ox, n, i, xr);
+            col_store(oy, n, i, yr);
+            oinf[i] = rinf;
+        }
+    }
+}
+
+template <class C, int COOP_THREADS>
+__global__ void __launch_bounds__(COOP_THREADS)
+k_batch_pdbl_coop(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
+                  const uint8_t* __restrict__ pinf, uint32_t* __restrict__ ox,
+                  uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf) {
+    __shared__ uint32_t sm[16 * (COOP_THREADS / 32)];
+    const typename C::Fp f{};
+    const size_t tile = (size_t)blockIdx.x * (COOP_THREADS * COOP_K) + threadIdx.x;
+    fe lp[COOP_K];
+    fe acc = fe_one(f);
+#pragma unroll
+    for (int k = 0; k < COOP_K; ++k) {
+        const size_t i = tile + (size_t)k * COOP_THREADS;
+        if (i < n) {
+            fe ay = col_load(py, n, i);
+            const bool degenerate = (pinf && pinf[i]) || fe_is_zero(ay);
+            if (!degenerate) acc = fe_mul(f, acc, fe_dbl(f, ay));
+        }
+        lp[k] = acc;
+    }
+    fe inv = coop_block_inverse<decltype(f), COOP_THREADS>(f, acc, sm);
+#pragma unroll
+    for (int k = COOP_K - 1; k >= 0; --k) {
+        const size_t i = tile + (size_t)k * COOP_THREADS;
+        if (i < n) {
+            fe ax = col_load(px, n, i), ay = col_load(py, n, i);
+            const bool degenerate = (pinf && pinf[i]) || fe_is_zero(ay);
+            fe dinv = k > 0 ? fe_mul(f, inv, lp[k > 0 ? k - 1 : 0]) : inv;
+            fe xr = fe_zero(), yr = fe_zero();
+            if (!degenerate) {
+                if (k > 0) inv = fe_mul(f, inv, fe_dbl(f, ay));
+                fe lam = fe_mul(f, tangent_numerator<C>(ax), dinv);
+                finish_lambda<C>(lam, ax, ax, ay, &xr, &yr);
+            }
+            col_store(ox, n, i, xr);
+            col_store(oy, n, i, yr);
+            oinf[i] = degenerate ? 1 : 0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- tiled form (three launches)
+// The single-launch cooperative kernels make a whole block wait for one warp's inversion
+// (~36 us of dependent divsteps), which only pays while the batch is small.  The tiled form
+// splits the same block-level trick at the inversion:
+//   k_padd_fwd  : per tile of TILED_THREADS * K pairs -- local prefix products (parked in ox,
+//                 which is free until the last launch), warp-shuffle scans, cross-warp scan in
+//                 shared memory; every thread keeps the product of ALL OTHER totals of its tile
+//                 (parked in oy at its first element) and the tile total goes to `totals`;
+//   batch_invert: the n / tile totals are inverted by the kernels above (a batch 1000x smaller);
+//   k_padd_bwd  : thread total^-1 = tile total^-1 * others, unwind, chord / tangent formulas.
+// Per pair: (6K + 8)/K products (K = 8: 7) and no inversion work to speak of; the chunked form
+// spends ~875 of its ~2000 instructions per pair inside safegcd at 16 pairs per thread.
+constexpr int TILED_THREADS = 256;
+
+// product of every other thread's t in the block (returned) and the block total (*total, valid
+// on thread 0 only).  sm: 16 * (TILED_THREADS / 32) words.
+template <class F>
+__device__ fe block_others_product(const F& f, const fe& t, uint32_t* sm, fe* total) {
+    constexpr int NW = TILED_THREADS / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const fe one = fe_one(f);
+    fe P, Q;
+    warp_scan_products(f, t, lane, 32, &P, &Q);
+    fe E = fe_select(lane == 0, one, fe_shfl_up(P, 1));
+    fe S = fe_select(lane == 31, one, fe_shfl_down(Q, 1));
+    if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sm[i * NW + warp] = P.w[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        fe w = one;
+        if (lane < NW) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w.w[i] = sm[i * NW + lane];
+        }
+        fe PP, QQ;
+        warp_scan_products(f, w, lane, NW, &PP, &QQ);
+        fe EE = fe_select(lane == 0, one, fe_shfl_up(PP, 1));
+        fe SS = fe_select(lane == 31, one, fe_shfl_down(QQ, 1));
+        fe ab = fe_mul(f, EE, SS);  // product of the other warps' totals
+        if (lane < NW) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) sm[(8 + i) * NW + lane] = ab.w[i];
+        }
+        if (lane == 0) *total = QQ;  // lane 0's inclusive suffix = all warps
+    }
+    __syncthreads();
+    fe ab;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ab.w[i] = sm[(8 + i) * NW + warp];
+    return fe_mul(f, fe_mul(f, ab, E), S);
+}
+
+template <class C, int K>
+__global__ void __launch_bounds__(TILED_THREADS)
+k_padd_fwd(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
+           const uint8_t* __restrict__ pinf, const uint32_t* __restrict__ tx,
+           const uint32_t* __restrict__ ty, const uint8_t* __restrict__ tinf,
+           uint32_t* __restrict__ ox, uint32_t* __restrict__ oy, uint32_t* __restrict__ totals,
+           size_t tiles) {
+    __shared__ uint32_t sm[16 * (TILED_THREADS / 32)];
+    const typename C::Fp f{};
+    const size_t first = (size_t)blockIdx.x * (TILED_THREADS * K) + threadIdx.x;
+    fe acc = fe_one(f);
+#pragma unroll 2
+    for (int k = 0; k < K; ++k) {
+        const size_t i = first + (size_t)k * TILED_THREADS;
+        if (i < n) {
+            fe ax = col_load(px, n, i), bx = col_load(tx, n, i);
+            const bool ai = pinf && pinf[i], bi = tinf && tinf[i];
+            fe d = fe_one(f);
+            if (!ai && !bi && fe_eq(ax, bx)) {
+                fe ay = col_load(py, n, i), by = col_load(ty, n, i);
+                classify_pair<C>(ax, ay, ai, bx, by, bi, &d);
+            } else if (!ai && !bi) {
+                d = fe_sub(f, ax, bx);
+            }
+            acc = fe_mul(f, acc, d);
+            col_store(ox, n, i, acc);  // local prefix product through element k
+        }
+    }
+    fe total;
+    fe others = block_others_product(f, acc, sm, &total);
+    if (first < n) col_store(oy, n, first, others);
+    if (threadIdx.x == 0) col_store(totals, tiles, blockIdx.x, total);
+}
+
+template <class C, int K>
+__global__ void __launch_bounds__(TILED_THREADS, 2)
+k_padd_bwd(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
+           const uint8_t* __restrict__ pinf, const uint32_t* __restrict__ tx,
+           const uint32_t* __restrict__ ty, const uint8_t* __restrict__ tinf,
+           uint32_t* __restrict__ ox, uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf,
+           const uint32_t* __restrict__ total_inv, size_t tiles) {
+    const typename C::Fp f{};
+    const size_t first = (size_t)blockIdx.x * (TILED_THREADS * K) + threadIdx.x;
+    if (first >= n) return;
+    fe inv = fe_mul(f, col_load(total_inv, tiles, blockIdx.x), col_load(oy, n, first));
+    int last = K - 1;
+    while (first + (size_t)last * TILED_THREADS >= n) --last;
+#pragma unroll 1
+    for (int k = last; k >= 0; --k) {
+        const size_t i = first + (size_t)k * TILED_THREADS;
+        fe ax = col_load(px, n, i), ay = col_load(py, n, i);
+        fe bx = col_load(tx, n, i), by = col_load(ty, n, i);
+        const bool ai = pinf && pinf[i], bi = tinf && tinf[i];
+        fe d = fe_one(f);
+        const uint32_t kind = classify_pair<C>(ax, ay, ai, bx, by, bi, &d);
+        fe dinv = inv;
+        if (k > 0) {
+            dinv = fe_mul(f, inv, col_load(ox, n, i - TILED_THREADS));
+            inv = fe_mul(f, inv, d);
+        }
+        fe xr = fe_zero(), yr = fe_zero();
+        uint8_t rinf = 0;
+        if (kind == K_GENERIC) {
+            fe lam = fe_mul(f, fe_sub(f, ay, by), dinv);
+            finish_lambda<C>(lam, ax, bx, ay, &xr, &yr);
+        } else if (kind == K_TANGENT) {
+            fe lam = fe_mul(f, tangent_numerator<C>(ax), dinv);
+            finish_lambda<C>(lam, ax, ax, ay, &xr, &yr);
+        } else if (kind == K_COPY_LEFT) {
+            xr = ax; yr = ay;
+        } else if (kind == K_COPY_RIGHT) {
+            xr = bx; yr = by;
+        } else {
+            rinf = 1;
+        }
+        col_store(ox, n, i, xr);
+        col_store(oy, n, i, yr);
+        oinf[i] = rinf;
+    }
+}
+
+// Form selection: the cooperative kernels while 16-element chunks would leave the chip
+// under-filled, the chunked kernels beyond.  gecc_set_batch_form pins one form (tests, sweeps):
+// 0 auto, 1 chunked (16 per thread), 2 cooperative 256 threads, 3 chunked at 6 blocks per SM,
+// 4 cooperative 128 threads, 5 cooperative 32 threads (one inversion per warp),
+// 6 / 7 tiled with 8 / 4 pairs per thread (batch_padd only; needs the context's scratch).
+static size_t g_coop_max_n = (size_t)1 << 18;
+static int g_batch_form = 0;
+void set_batch_form(int form) { g_batch_form = form; }
+static int pick_form(size_t n, bool tiled_ok = false) {
+    if (g_batch_form >= 6) return tiled_ok ? g_batch_form : (n <= g_coop_max_n ? 4 : 1);
+    if (g_batch_form) return g_batch_form;
+    // measured on B200 (profiles/r01f_sweep.json): cooperative/128 wins up to 2^18 pairs
+    // (0.054 ms vs 0.083 ms), chunked and tiled are within 7 % of each other beyond
+    return n <= g_coop_max_n ? 4 : 1;
+}
+size_t batch_padd_scratch_bytes(size_t n) {  // tile totals and their inverses (K = 4 is the larger)
+    const size_t tiles = (n + (size_t)TILED_THREADS * 4 - 1) / ((size_t)TILED_THREADS * 4);
+    return 2 * tiles * 32 + 512;
+}
+static int coop_threads(int form) { return form == 2 ? 256 : form == 4 ? 128 : form == 5 ? 32 : 0; }
+static unsigned coop_blocks(size_t n, int threads) {
+    return (unsigned)((n + (size_t)threads * COOP_K - 1) / ((size_t)threads * COOP_K));
+}
 // threads: enough to fill the chip, at most one element short of ~CHUNK per thread
-static size_t pick_threads(size_t n) {
-    const size_t CHUNK = 16, cap = (size_t)148 * 16 * BATCH_THREADS;
+static size_t pick_threads(size_t n, int form) {
+    const size_t CHUNK = 16, cap = (size_t)148 * (form == 3 ? 24 : 16) * BATCH_THREADS;
     size_t T = (n + CHUNK - 1) / CHUNK;
     if (T > cap) T = cap;
     if (T < 1) T = 1;
     return (T + BATCH_THREADS - 1) / BATCH_THREADS * BATCH_THREADS;
 }
+#define COOP_DISPATCH(threads, KERNEL, ...)                                             \
+    do {                                                                                \
+        const unsigned cb__ = coop_blocks(n, threads);                                  \
+        if (threads == 256) KERNEL(256)<<<cb__, 256, 0, s>>>(__VA_ARGS__);              \
+        else if (threads == 128) KERNEL(128)<<<cb__, 128, 0, s>>>(__VA_ARGS__);         \
+        else KERNEL(32)<<<cb__, 32, 0, s>>>(__VA_ARGS__);                               \
+    } while (0)
 
 cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* in, uint32_t* out,
                                 cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const size_t T = pick_threads(n);
+    const int form = pick_form(n);
+    if (const int ct = coop_threads(form)) {
+        if (curve == CURVE_SECP && field == 0) {
+#define KT_(t) k_batch_invert_coop<SecpP, t>
+            COOP_DISPATCH(ct, KT_, n, in, out);
+#undef KT_
+        } else if (curve == CURVE_SECP) {
+#define KT_(t) k_batch_invert_coop<SecpN, t>
+            COOP_DISPATCH(ct, KT_, n, in, out);
+#undef KT_
+        } else if (field == 0) {
+#define KT_(t) k_batch_invert_coop<Sm2P, t>
+            COOP_DISPATCH(ct, KT_, n, in, out);
+#undef KT_
+        } else {
+#define KT_(t) k_batch_invert_coop<Sm2N, t>
+            COOP_DISPATCH(ct, KT_, n, in, out);
+#undef KT_
+        }
+        return cudaGetLastError();
+    }
+    const size_t T = pick_threads(n, form);
     const int b = (int)(T / BATCH_THREADS);
     if (curve == CURVE_SECP) {
         if (field == 0) k_batch_invert<SecpP><<<b, BATCH_THREADS, 0, s>>>(n, T, in, out);
@@ -211,14 +628,50 @@ cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* 
 cudaError_t launch_batch_padd(int curve, size_t n, const uint32_t* px, const uint32_t* py,
                               const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty,
                               const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
-                              cudaStream_t s) {
+                              cudaStream_t s, void* scratch) {
     if (n == 0) return cudaSuccess;
-    const size_t T = pick_threads(n);
+    const int form = pick_form(n, scratch != nullptr);
+    if (form >= 6) {
+        const int K = form == 6 ? 8 : 4;
+        const size_t tiles = (n + (size_t)TILED_THREADS * K - 1) / ((size_t)TILED_THREADS * K);
+        uint32_t* totals = (uint32_t*)scratch;
+        uint32_t* total_inv = totals + ((tiles * 8 + 63) & ~(size_t)63);
+        const unsigned b = (unsigned)tiles;
+#define TILED_(CURVE, KK)                                                                              \
+    k_padd_fwd<CURVE, KK><<<b, TILED_THREADS, 0, s>>>(n, px, py, pinf, tx, ty, tinf, ox, oy, totals, tiles); \
+    if (cudaError_t e = launch_batch_invert(curve, 0, tiles, totals, total_inv, s)) return e;           \
+    k_padd_bwd<CURVE, KK><<<b, TILED_THREADS, 0, s>>>(n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, total_inv, tiles)
+        if (curve == CURVE_SECP) {
+            if (K == 8) { TILED_(SecpCurve, 8); } else { TILED_(SecpCurve, 4); }
+        } else {
+            if (K == 8) { TILED_(Sm2Curve, 8); } else { TILED_(Sm2Curve, 4); }
+        }
+#undef TILED_
+        return cudaGetLastError();
+    }
+    if (const int ct = coop_threads(form)) {
+        if (curve == CURVE_SECP) {
+#define KT_(t) k_batch_padd_coop<SecpCurve, t>
+            COOP_DISPATCH(ct, KT_, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
+#undef KT_
+        } else {
+#define KT_(t) k_batch_padd_coop<Sm2Curve, t>
+            COOP_DISPATCH(ct, KT_, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
+#undef KT_
+        }
+        return cudaGetLastError();
+    }
+    const size_t T = pick_threads(n, form);
     const int b = (int)(T / BATCH_THREADS);
-    if (curve == CURVE_SECP)
-        k_batch_padd<SecpCurve><<<b, BATCH_THREADS, 0, s>>>(n, T, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
+    if (form == 3) {  // experimental: 6 blocks per SM (80 registers)
+        if (curve == CURVE_SECP)
+            k_batch_padd<SecpCurve, 6><<<b, BATCH_THREADS, 0, s>>>(n, T, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
+        else
+            k_batch_padd<Sm2Curve, 6><<<b, BATCH_THREADS, 0, s>>>(n, T, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
+    } else if (curve == CURVE_SECP)
+        k_batch_padd<SecpCurve, 4><<<b, BATCH_THREADS, 0, s>>>(n, T, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
     else
-        k_batch_padd<Sm2Curve><<<b, BATCH_THREADS, 0, s>>>(n, T, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
+        k_batch_padd<Sm2Curve, 4><<<b, BATCH_THREADS, 0, s>>>(n, T, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
     return cudaGetLastError();
 }
 
@@ -226,7 +679,20 @@ cudaError_t launch_batch_pdbl(int curve, size_t n, const uint32_t* px, const uin
                               const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
                               cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    const size_t T = pick_threads(n);
+    const int form = pick_form(n);
+    if (const int ct = coop_threads(form)) {
+        if (curve == CURVE_SECP) {
+#define KT_(t) k_batch_pdbl_coop<SecpCurve, t>
+            COOP_DISPATCH(ct, KT_, n, px, py, pinf, ox, oy, oinf);
+#undef KT_
+        } else {
+#define KT_(t) k_batch_pdbl_coop<Sm2Curve, t>
+            COOP_DISPATCH(ct, KT_, n, px, py, pinf, ox, oy, oinf);
+#undef KT_
+        }
+        return cudaGetLastError();
+    }
+    const size_t T = pick_threads(n, form);
     const int b = (int)(T / BATCH_THREADS);
     if (curve == CURVE_SECP)
         k_batch_pdbl<SecpCurve><<<b, BATCH_THREADS, 0, s>>>(n, T, px, py, pinf, ox, oy, oinf);

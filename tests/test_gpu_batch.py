@@ -24,12 +24,21 @@ def ctxs():
         x.close()
 
 
+@pytest.fixture(params=["chunked", "coop", "coop32", "tiled8", "tiled4"])
+def form(request):
+    """Both forms of the batch kernels (one inversion per thread / one per block) must agree
+    with the reference bit for bit (results are grouping-invariant, batch_invert.hpp:59-60)."""
+    gecc.set_batch_form(request.param)
+    yield request.param
+    gecc.set_batch_form("auto")
+
+
 def same(A, B):
     return all((a == b).all() for a, b in zip(A, B))
 
 
 @pytest.mark.parametrize("name", CURVES)
-def test_batch_golden_gpu(ctxs, name):
+def test_batch_golden_gpu(ctxs, name, form):
     ent, cid = BATCH[name], CURVE_IDS[name]
     ctx = ctxs[cid]
     P, T = pts_from_hex(ent["P"]), pts_from_hex(ent["T"])
@@ -45,7 +54,7 @@ def test_batch_golden_gpu(ctxs, name):
 
 
 @pytest.mark.parametrize("cid", [0, 1])
-def test_batch_random_vs_oracle(ctxs, cid):
+def test_batch_random_vs_oracle(ctxs, cid, form):
     c, ctx = E.CURVES[cid], ctxs[cid]
     rng = random.Random(300 + cid)
     n = 1500
@@ -65,7 +74,7 @@ def test_batch_random_vs_oracle(ctxs, cid):
         assert (ctx.batch_invert(which, a) == O.batch_invert(cid, which, a, lanes=9)).all()
 
 
-def test_batch_sizes_and_errors(ctxs):
+def test_batch_sizes_and_errors(ctxs, form):
     ctx = ctxs[1]
     empty = (np.zeros((8, 0), np.uint32), np.zeros((8, 0), np.uint32), np.zeros(0, np.uint8))
     assert ctx.batch_padd(empty, empty)[0].shape == (8, 0)  # empty batches are fine
@@ -75,7 +84,7 @@ def test_batch_sizes_and_errors(ctxs):
         ctx.batch_padd(one, empty)
     # ragged sizes around the chunking boundaries: all-infinity + t = infinity returns p
     rng = random.Random(4)
-    for n in (1, 2, 127, 128, 129, 2049):
+    for n in (1, 2, 127, 128, 129, 1023, 1024, 1025, 2049):
         k = gecc.cols_from_ints([rng.randrange(1, E.SECP256K1.n) for _ in range(n)])
         P = ctx.batch_fpmul(k)
         inf = (np.zeros((8, n), np.uint32), np.zeros((8, n), np.uint32), np.ones(n, np.uint8))
@@ -87,7 +96,7 @@ def test_batch_sizes_and_errors(ctxs):
         assert same(ctx.batch_padd(P, P), ctx.batch_pdbl(P))
 
 
-def test_padd_properties_large(ctxs):
+def test_padd_properties_large(ctxs, form):
     """2^20 pairs: commutativity and (P+T)+(-T) == P, plus a CPU spot check."""
     ctx, c = ctxs[1], E.SECP256K1
     n = 1 << 20

@@ -73,10 +73,17 @@ def main():
         Pn, Tn, Sn = sub(P), sub(T), sub(S)
         ms_v = timed(lambda: l.gecc_verify_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_pub), vp(d_sig), vp(d_res)), stream)
         assert int(d_res[:n].sum()) == n
-        ms_p = timed(lambda: l.gecc_batch_padd_dev(ctx.h, C.c_size_t(n), vp(Pn[0]), vp(Pn[1]), vp(Pn[2]), vp(Tn[0]),
-                                                    vp(Tn[1]), vp(Tn[2]), vp(Sn[0]), vp(Sn[1]), vp(Sn[2])), stream)
-        rows.append(dict(log2n=lg, verify_ms=ms_v, verify_per_s=n / ms_v * 1e3, padd_ms=ms_p, padd_per_s=n / ms_p * 1e3))
-        print(f"2^{lg:2d}  verify {ms_v:9.3f} ms  {n / ms_v / 1e3:8.2f} M/s   padd {ms_p:8.4f} ms  {n / ms_p / 1e6:7.3f} G/s", flush=True)
+        padd = lambda: l.gecc_batch_padd_dev(ctx.h, C.c_size_t(n), vp(Pn[0]), vp(Pn[1]), vp(Pn[2]), vp(Tn[0]),
+                                             vp(Tn[1]), vp(Tn[2]), vp(Sn[0]), vp(Sn[1]), vp(Sn[2]))
+        forms = {}
+        for name in ("chunked", "chunked8", "coop", "coop128", "tiled8", "tiled4", "auto"):  # one inversion per thread / per block / library's pick
+            gecc.set_batch_form(name)
+            forms[name] = timed(padd, stream)
+        ms_p = forms["auto"]
+        rows.append(dict(log2n=lg, verify_ms=ms_v, verify_per_s=n / ms_v * 1e3, padd_ms=ms_p, padd_per_s=n / ms_p * 1e3,
+                         padd_ms_by_form=forms))
+        print(f"2^{lg:2d}  verify {ms_v:9.3f} ms  {n / ms_v / 1e3:8.2f} M/s   padd {ms_p:8.4f} ms  {n / ms_p / 1e6:7.3f} G/s"
+              "  (" + ", ".join(f"{k} {v:.4f}" for k, v in forms.items()) + ")", flush=True)
     # CPU reference at 2^12, 2^14, 2^16
     cpu = []
     from oracle import refshim as R
