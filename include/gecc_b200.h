@@ -208,6 +208,12 @@ sm2b_status gecc_msm_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const
  * block: warp-shuffle scans + shared memory). */
 void gecc_set_batch_form(int form);
 
+/* Bucket accumulation of gecc_msm (process-wide; results are identical): 0 = default
+ * (batch-affine), 1 = mixed Jacobian additions over fixed slices of the sorted pairs,
+ * 2 = batch-affine: segmented pairwise tree, affine additions sharing one inversion per
+ * thread block, three launches per tree level, 3 = the same with one launch per level. */
+void gecc_set_msm_form(int form);
+
 /* Integer-pipe issue-rate microbenchmark (roofline denominator).
  * which: 0 IMAD.WIDE.U32 independent, 1 IMAD.WIDE dependent chain, 2 IMAD (32-bit),
  *        3 IMAD.HI, 4 IADD3, 5 IADD3.X carry chain, 6 IMAD.WIDE + IADD3 1:1 mix,

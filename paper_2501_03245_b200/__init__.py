@@ -6,8 +6,8 @@ implementation here: importing works anywhere, but creating a Context needs the
 compiled library and a CUDA device and raises loudly otherwise.
 """
 from .capi import (Context, GeccError, LIB_PATH, SM2, SECP256K1, STATUS, lib, lib_available,
-                   cols_from_ints, ints_from_cols, set_batch_form)
+                   cols_from_ints, ints_from_cols, set_batch_form, set_msm_form)
 
 __all__ = ["Context", "GeccError", "LIB_PATH", "SM2", "SECP256K1", "STATUS", "lib",
-           "lib_available", "cols_from_ints", "ints_from_cols", "set_batch_form"]
+           "lib_available", "cols_from_ints", "ints_from_cols", "set_batch_form", "set_msm_form"]
 __version__ = "0.1.0"

@@ -56,6 +56,8 @@ def lib():
         l.gecc_kernel_launches.argtypes = [C.c_void_p]
         l.gecc_set_batch_form.argtypes = [C.c_int]
         l.gecc_set_batch_form.restype = None
+        l.gecc_set_msm_form.argtypes = [C.c_int]
+        l.gecc_set_msm_form.restype = None
         _lib = l
     return _lib
 
@@ -66,6 +68,14 @@ BATCH_FORMS = {"auto": 0, "chunked": 1, "coop": 2, "chunked8": 3, "coop128": 4, 
 def set_batch_form(form: str):
     """Pins the batch kernels' form (gecc_set_batch_form): auto | chunked | coop."""
     lib().gecc_set_batch_form(BATCH_FORMS[form])
+
+
+MSM_FORMS = {"auto": 0, "jacobian": 1, "affine": 2, "affine1": 3}
+
+
+def set_msm_form(form: str):
+    """Pins gecc_msm's bucket accumulation (gecc_set_msm_form): auto | jacobian | affine."""
+    lib().gecc_set_msm_form(MSM_FORMS[form])
 
 
 def cols_from_ints(vals) -> np.ndarray:

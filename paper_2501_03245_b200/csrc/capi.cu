@@ -273,6 +273,7 @@ sm2b_status gecc_field_op(sm2b_ctx* ctx, gecc_field field, gecc_field_opcode op,
 }
 
 void gecc_set_batch_form(int form) { set_batch_form(form < 0 || form > 7 ? 0 : form); }
+void gecc_set_msm_form(int form) { set_msm_form(form < 0 || form > 3 ? 0 : form); }
 
 sm2b_status gecc_microbench(sm2b_ctx* ctx, int which, int iters, double* ops_per_clk_per_sm,
                             double* seconds, double* total_ops) {

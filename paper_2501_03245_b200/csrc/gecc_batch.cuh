@@ -1,0 +1,164 @@
+// Shared device helpers of the batched-affine kernels (k_batch.cu, k_msm.cu):
+// the complete pair classification of batch_padd (batch_point.cpp:91-111), the
+// chord / tangent finish (batch_point.cpp:124-170) and the block-level Montgomery
+// trick (warp-shuffle scans + shared memory, one inversion per thread block).
+#pragma once
+#include "gecc_curve.cuh"
+#include "gecc_dev.cuh"
+#include "gecc_modinv.cuh"
+
+namespace gecc {
+
+enum : uint32_t { K_GENERIC = 0, K_TANGENT, K_INFINITY, K_COPY_LEFT, K_COPY_RIGHT };
+
+// classification + denominator of one pair (batch_point.cpp:91-111)
+template <class C>
+__device__ __forceinline__ uint32_t classify_pair(const fe& px, const fe& py, bool pinf,
+                                                  const fe& tx, const fe& ty, bool tinf, fe* d) {
+    const typename C::Fp f{};
+    if (pinf && tinf) return K_INFINITY;
+    if (pinf) return K_COPY_RIGHT;
+    if (tinf) return K_COPY_LEFT;
+    if (fe_eq(px, tx)) {
+        if (fe_eq(py, ty) && !fe_is_zero(py)) {
+            *d = fe_dbl(f, py);
+            return K_TANGENT;
+        }
+        return K_INFINITY;  // inverse pair (covers y == 0)
+    }
+    *d = fe_sub(f, px, tx);
+    return K_GENERIC;
+}
+
+template <class C>
+__device__ __forceinline__ void finish_lambda(const fe& lam, const fe& x1, const fe& x2,
+                                              const fe& y1, fe* xr, fe* yr) {
+    const typename C::Fp f{};
+    *xr = fe_sub(f, fe_sub(f, fe_sqr(f, lam), x1), x2);
+    *yr = fe_sub(f, fe_mul(f, lam, fe_sub(f, x1, *xr)), y1);
+}
+template <class C>
+__device__ __forceinline__ fe tangent_numerator(const fe& x) {  // 3x^2 + a
+    const typename C::Fp f{};
+    fe x2 = fe_sqr(f, x);
+    fe num = fe_add(f, fe_dbl(f, x2), x2);
+    if (C::a_kind == A_ZERO) return num;
+    return fe_add(f, num, curve_a<C>());
+}
+
+__device__ __forceinline__ fe fe_shfl_up(const fe& v, int d) {
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.w[i] = __shfl_up_sync(0xFFFFFFFFu, v.w[i], d);
+    return r;
+}
+__device__ __forceinline__ fe fe_shfl_down(const fe& v, int d) {
+    fe r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r.w[i] = __shfl_down_sync(0xFFFFFFFFu, v.w[i], d);
+    return r;
+}
+// inclusive prefix product P and inclusive suffix product Q of t over the 32 lanes of a warp
+template <class F>
+__device__ __forceinline__ void warp_scan_products(const F& f, const fe& t, int lane, int width,
+                                                   fe* P, fe* Q) {
+    *P = t;
+    *Q = t;
+#pragma unroll 1
+    for (int d = 1; d < width; d <<= 1) {
+        fe m = fe_mul(f, *P, fe_shfl_up(*P, d));
+        *P = fe_select(lane >= d, m, *P);
+        fe m2 = fe_mul(f, *Q, fe_shfl_down(*Q, d));
+        *Q = fe_select(lane + d < 32, m2, *Q);
+    }
+}
+// t != 0 on every thread of the block (all COOP_THREADS threads must call).  Returns t^-1.
+// sm: 2 * (COOP_THREADS / 32) field elements of shared memory, word-major.
+template <class F, int COOP_THREADS>
+__device__ fe coop_block_inverse(const F& f, const fe& t, uint32_t* sm) {
+    constexpr int NW = COOP_THREADS / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const fe one = fe_one(f);
+    fe P, Q;
+    warp_scan_products(f, t, lane, 32, &P, &Q);
+    fe E = fe_select(lane == 0, one, fe_shfl_up(P, 1));    // exclusive prefix
+    fe S = fe_select(lane == 31, one, fe_shfl_down(Q, 1)); // exclusive suffix
+    if constexpr (NW == 1) {  // a block of one warp: the warp total is inverted directly
+        fe total;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) total.w[i] = __shfl_sync(0xFFFFFFFFu, P.w[i], 31);
+        return fe_mul(f, fe_mul(f, fe_inv(f, total), E), S);
+    }
+    if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sm[i * NW + warp] = P.w[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        fe w = one;
+        if (lane < NW) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w.w[i] = sm[i * NW + lane];
+        }
+        fe PP, QQ;
+        warp_scan_products(f, w, lane, NW, &PP, &QQ);  // lanes >= NW hold one
+        fe total;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) total.w[i] = __shfl_sync(0xFFFFFFFFu, PP.w[i], NW - 1);
+        const fe inv = fe_inv(f, total);  // the block's single inversion
+        fe EE = fe_select(lane == 0, one, fe_shfl_up(PP, 1));
+        fe SS = fe_select(lane == 31, one, fe_shfl_down(QQ, 1));
+        fe wi = fe_mul(f, fe_mul(f, inv, EE), SS);
+        if (lane < NW) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) sm[(8 + i) * NW + lane] = wi.w[i];
+        }
+    }
+    __syncthreads();
+    fe wi;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) wi.w[i] = sm[(8 + i) * NW + warp];
+    return fe_mul(f, fe_mul(f, wi, E), S);
+}
+
+// product of every other thread's t in the block (returned) and the block total (*total, valid
+// on thread 0 only).  sm: 16 * (THREADS / 32) words.
+template <class F, int THREADS>
+__device__ fe block_others_product(const F& f, const fe& t, uint32_t* sm, fe* total) {
+    constexpr int NW = THREADS / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const fe one = fe_one(f);
+    fe P, Q;
+    warp_scan_products(f, t, lane, 32, &P, &Q);
+    fe E = fe_select(lane == 0, one, fe_shfl_up(P, 1));
+    fe S = fe_select(lane == 31, one, fe_shfl_down(Q, 1));
+    if (lane == 31) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sm[i * NW + warp] = P.w[i];
+    }
+    __syncthreads();
+    if (warp == 0) {
+        fe w = one;
+        if (lane < NW) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) w.w[i] = sm[i * NW + lane];
+        }
+        fe PP, QQ;
+        warp_scan_products(f, w, lane, NW, &PP, &QQ);
+        fe EE = fe_select(lane == 0, one, fe_shfl_up(PP, 1));
+        fe SS = fe_select(lane == 31, one, fe_shfl_down(QQ, 1));
+        fe ab = fe_mul(f, EE, SS);  // product of the other warps' totals
+        if (lane < NW) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) sm[(8 + i) * NW + lane] = ab.w[i];
+        }
+        if (lane == 0) *total = QQ;  // lane 0's inclusive suffix = all warps
+    }
+    __syncthreads();
+    fe ab;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) ab.w[i] = sm[(8 + i) * NW + warp];
+    return fe_mul(f, fe_mul(f, ab, E), S);
+}
+
+}  // namespace gecc

@@ -17,6 +17,7 @@
 // Bucket ids: window w, magnitude m = 1..2^15  ->  w * 2^15 + (m - 1).
 #include <cub/device/device_radix_sort.cuh>
 
+#include "gecc_batch.cuh"
 #include "gecc_ecdsa.cuh"
 #include "gecc_host.h"
 
@@ -170,6 +171,342 @@ k_msm_bucket_edges(uint32_t* __restrict__ buckets, const uint32_t* __restrict__ 
     jac_store(buckets, MSM_NB, key, acc);
 }
 
+// ---------------------------------------------------------------- batch-affine bucket accumulation
+// The bucket sums are formed with AFFINE additions that share their inversions (Montgomery's
+// trick across a thread block), 5M + 1S + the scan share per addition instead of the 8M + 3S
+// of a mixed Jacobian addition.  Independent additions come from a segmented pairwise tree
+// over the SORTED pair list (positions 0 .. m-1):
+//   invariant after level l: inside every aligned node [a, a + 2^l) the partial sum of key k
+//   over the node's entries sits in slot max(a, runstart(k));
+//   level l joins the two halves of every node of size 2^(l+1): only the key that straddles
+//   the middle c needs work,  slot[max(a, runstart)] += slot[c]  -- all joins of one level are
+//   independent, and a consumed slot is never read again.
+// Level 0 reads the points themselves (64-byte AoS records, gathered by index, sign applied)
+// and fills the slots.  After MSM_TREE_LEVELS levels a bucket whose run is [s, e) has its sum
+// spread over slot s and the slots at multiples of 2^MSM_TREE_LEVELS inside (s, e): the tail
+// kernel (one thread per bucket) adds those few (mean run length is 32) with mixed Jacobian
+// additions and writes the bucket in the layout the reduction kernels read.
+// All formulas are complete: slots carry an infinity flag; equal points take the tangent,
+// opposite points give infinity (classification as batch_padd, batch_point.cpp:91-111).
+constexpr int MSM_TREE_LEVELS = 6;
+constexpr int MSM_TREE_THREADS = 128;
+
+struct rec4 {
+    uint4 a, b, c, d;  // x limbs 0-3, 4-7, y limbs 0-3, 4-7
+};
+__device__ __forceinline__ fe fe_from_u4(const uint4& lo, const uint4& hi) {
+    fe r;
+    r.w[0] = lo.x; r.w[1] = lo.y; r.w[2] = lo.z; r.w[3] = lo.w;
+    r.w[4] = hi.x; r.w[5] = hi.y; r.w[6] = hi.z; r.w[7] = hi.w;
+    return r;
+}
+__device__ __forceinline__ void rec_store(uint4* rec, size_t i, const fe& x, const fe& y) {
+    uint4* p = rec + 4 * i;
+    p[0] = make_uint4(x.w[0], x.w[1], x.w[2], x.w[3]);
+    p[1] = make_uint4(x.w[4], x.w[5], x.w[6], x.w[7]);
+    p[2] = make_uint4(y.w[0], y.w[1], y.w[2], y.w[3]);
+    p[3] = make_uint4(y.w[4], y.w[5], y.w[6], y.w[7]);
+}
+__device__ __forceinline__ fe rec_x(const uint4* rec, size_t i) {
+    return fe_from_u4(rec[4 * i], rec[4 * i + 1]);
+}
+__device__ __forceinline__ fe rec_y(const uint4* rec, size_t i) {
+    return fe_from_u4(rec[4 * i + 2], rec[4 * i + 3]);
+}
+
+// column-major coordinates -> 64-byte records (one gather of a point = two 32-byte sectors
+// instead of sixteen)
+__global__ void __launch_bounds__(256)
+k_msm_aos(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
+          uint4* __restrict__ rec) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    rec_store(rec, i, col_load(px, n, i), col_load(py, n, i));
+}
+
+// first position of every bucket's run in the sorted keys (0xFFFFFFFF: empty bucket; memset)
+__global__ void __launch_bounds__(256)
+k_msm_starts(size_t m, const uint32_t* __restrict__ keys, uint32_t* __restrict__ starts) {
+    const size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (p >= m) return;
+    const uint32_t k = keys[p];
+    if (k < MSM_NB && (p == 0 || keys[p - 1] != k)) starts[k] = (uint32_t)p;
+}
+
+// One join (see above).  LEVEL0: the operands are input points fetched through vals.
+template <class C, bool LEVEL0>
+struct TreeJoin {
+    size_t dst, src;
+    bool active;      // an addition happens
+    bool copy2;       // level 0 only: keys differ, both points pass through
+    uint32_t v0, v1;  // level 0: vals of the two entries
+};
+
+template <class C, bool LEVEL0>
+__device__ __forceinline__ TreeJoin<C, LEVEL0> tree_locate(size_t j, int level, size_t m,
+                                                           const uint32_t* __restrict__ keys,
+                                                           const uint32_t* __restrict__ vals) {
+    TreeJoin<C, LEVEL0> t;
+    t.active = t.copy2 = false;
+    t.dst = t.src = 0;
+    t.v0 = t.v1 = 0;
+    if (LEVEL0) {
+        const size_t a = 2 * j;
+        if (a >= m) return t;
+        const uint32_t k0 = keys[a], k1 = a + 1 < m ? keys[a + 1] : 0xFFFFFFFFu;
+        if (k0 >= MSM_NB) return t;  // sorted: k1 is not a bucket either
+        t.dst = a;
+        t.src = a + 1;
+        t.v0 = vals[a];
+        if (k1 == k0) {
+            t.active = true;
+            t.v1 = vals[a + 1];
+        } else {
+            t.copy2 = true;          // dst gets entry a; src gets entry a + 1 when it is a bucket
+            if (k1 < MSM_NB) t.v1 = vals[a + 1];
+            else t.src = (size_t)-1;
+        }
+        return t;
+    }
+    const size_t half = (size_t)1 << level;
+    const size_t c = (2 * j + 1) * half;
+    if (c >= m) return t;
+    const uint32_t k = keys[c];
+    if (k >= MSM_NB || keys[c - 1] != k) return t;
+    size_t lo = c - half, hi = c - 1;  // first position of key k inside the left half
+    while (lo < hi) {
+        const size_t mid = (lo + hi) >> 1;
+        if (keys[mid] < k) lo = mid + 1;
+        else hi = mid;
+    }
+    t.dst = lo;
+    t.src = c;
+    t.active = true;
+    return t;
+}
+
+template <class C>
+__device__ __forceinline__ aff msm_point(const uint4* __restrict__ rec, uint32_t v) {
+    const size_t idx = v & 0x7FFFFFFFu;
+    aff q{rec_x(rec, idx), rec_y(rec, idx)};
+    if (v >> 31) q.y = fe_neg(typename C::Fp{}, q.y);
+    return q;
+}
+
+// denominator of a join (one when nothing is inverted for it)
+template <class C, bool LEVEL0>
+__device__ __forceinline__ fe tree_denominator(const TreeJoin<C, LEVEL0>& t, const uint4* __restrict__ rec,
+                                               const uint4* slots, const uint8_t* sinf) {
+    const typename C::Fp f{};
+    fe d = fe_one(f);
+    if (!t.active) return d;
+    fe ax, bx;
+    bool ai = false, bi = false;
+    if (LEVEL0) {
+        ax = rec_x(rec, t.v0 & 0x7FFFFFFFu);
+        bx = rec_x(rec, t.v1 & 0x7FFFFFFFu);
+    } else {
+        ax = rec_x(slots, t.dst);
+        bx = rec_x(slots, t.src);
+        ai = sinf[t.dst] != 0;
+        bi = sinf[t.src] != 0;
+    }
+    if (ai || bi) return d;
+    if (fe_eq(ax, bx)) {  // y is only needed when the x's collide
+        fe ay, by;
+        if (LEVEL0) {
+            ay = msm_point<C>(rec, t.v0).y;
+            by = msm_point<C>(rec, t.v1).y;
+        } else {
+            ay = rec_y(slots, t.dst);
+            by = rec_y(slots, t.src);
+        }
+        classify_pair<C>(ax, ay, false, bx, by, false, &d);
+        return d;
+    }
+    return fe_sub(f, ax, bx);
+}
+
+// backward step of Montgomery's trick for one join: inv holds the inverse of the product of
+// the denominators up to and including this join's; prev the product before it.
+template <class C, bool LEVEL0>
+__device__ __forceinline__ void tree_apply(const TreeJoin<C, LEVEL0>& t, fe& inv, const fe& prev, bool first,
+                                           const uint4* __restrict__ rec, uint4* slots, uint8_t* sinf) {
+    const typename C::Fp f{};
+    if (LEVEL0 && t.copy2) {
+        const aff p0 = msm_point<C>(rec, t.v0);
+        rec_store(slots, t.dst, p0.x, p0.y);
+        sinf[t.dst] = 0;
+        if (t.src != (size_t)-1) {
+            const aff p1 = msm_point<C>(rec, t.v1);
+            rec_store(slots, t.src, p1.x, p1.y);
+            sinf[t.src] = 0;
+        }
+        return;
+    }
+    if (!t.active) return;
+    aff A, B;
+    bool ai = false, bi = false;
+    if (LEVEL0) {
+        A = msm_point<C>(rec, t.v0);
+        B = msm_point<C>(rec, t.v1);
+    } else {
+        A.x = rec_x(slots, t.dst); A.y = rec_y(slots, t.dst);
+        B.x = rec_x(slots, t.src); B.y = rec_y(slots, t.src);
+        ai = sinf[t.dst] != 0;
+        bi = sinf[t.src] != 0;
+    }
+    fe d = fe_one(f);
+    const uint32_t kind = classify_pair<C>(A.x, A.y, ai, B.x, B.y, bi, &d);
+    fe dinv = inv;
+    if (!first) {
+        dinv = fe_mul(f, inv, prev);
+        inv = fe_mul(f, inv, d);
+    }
+    fe xr = fe_zero(), yr = fe_zero();
+    uint8_t rinf = 0;
+    if (kind == K_GENERIC) {
+        fe lam = fe_mul(f, fe_sub(f, A.y, B.y), dinv);
+        finish_lambda<C>(lam, A.x, B.x, A.y, &xr, &yr);
+    } else if (kind == K_TANGENT) {
+        fe lam = fe_mul(f, tangent_numerator<C>(A.x), dinv);
+        finish_lambda<C>(lam, A.x, A.x, A.y, &xr, &yr);
+    } else if (kind == K_COPY_LEFT) {
+        xr = A.x; yr = A.y;
+    } else if (kind == K_COPY_RIGHT) {
+        xr = B.x; yr = B.y;
+    } else {
+        rinf = 1;
+    }
+    rec_store(slots, t.dst, xr, yr);
+    sinf[t.dst] = rinf;
+}
+
+// Single-launch form of one level: the block's one inversion happens inside the kernel
+// (prefix products in shared memory; the other warps wait while warp 0 inverts).
+template <class C, int K, bool LEVEL0>
+__global__ void __launch_bounds__(MSM_TREE_THREADS)
+k_msm_tree(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
+           const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
+           uint4* slots, uint8_t* sinf) {
+    __shared__ uint32_t sm_scan[16 * (MSM_TREE_THREADS / 32)];
+    __shared__ uint32_t sm_pref[K * 8 * MSM_TREE_THREADS];
+    const typename C::Fp f{};
+    const size_t j0 = (size_t)blockIdx.x * (MSM_TREE_THREADS * K) + threadIdx.x;
+    fe acc = fe_one(f);
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+        const size_t j = j0 + (size_t)k * MSM_TREE_THREADS;
+        if (j < joins) {
+            const TreeJoin<C, LEVEL0> t = tree_locate<C, LEVEL0>(j, level, m, keys, vals);
+            if (t.active) acc = fe_mul(f, acc, tree_denominator<C, LEVEL0>(t, rec, slots, sinf));
+        }
+#pragma unroll
+        for (int w = 0; w < 8; ++w) sm_pref[(k * 8 + w) * MSM_TREE_THREADS + threadIdx.x] = acc.w[w];
+    }
+    fe inv = coop_block_inverse<decltype(f), MSM_TREE_THREADS>(f, acc, sm_scan);
+#pragma unroll 1
+    for (int k = K - 1; k >= 0; --k) {
+        const size_t j = j0 + (size_t)k * MSM_TREE_THREADS;
+        if (j >= joins) continue;
+        const TreeJoin<C, LEVEL0> t = tree_locate<C, LEVEL0>(j, level, m, keys, vals);
+        fe prev = fe_one(f);
+        if (k > 0) {
+#pragma unroll
+            for (int w = 0; w < 8; ++w) prev.w[w] = sm_pref[((k - 1) * 8 + w) * MSM_TREE_THREADS + threadIdx.x];
+        }
+        tree_apply<C, LEVEL0>(t, inv, prev, k == 0, rec, slots, sinf);
+    }
+}
+
+// Three-launch form of one level (no warp ever waits for an inversion):
+//   k_msm_tree_fwd : running products of the denominators, parked in `pref` (32 B per join);
+//                    every thread keeps the product of ALL OTHER thread totals of its block
+//                    (`others`), the block total goes to `totals` (column buffer);
+//   batch_invert   : the block totals (a batch MSM_TREE_THREADS * K times smaller);
+//   k_msm_tree_bwd : thread total^-1 = block total^-1 * others, unwind, chord / tangent.
+// (6K + 8) / K products per addition.
+template <class C, int K, bool LEVEL0>
+__global__ void __launch_bounds__(MSM_TREE_THREADS)
+k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
+               const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
+               const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
+               uint4* __restrict__ pref, uint4* __restrict__ others, uint32_t* __restrict__ totals,
+               size_t tiles) {
+    __shared__ uint32_t sm_scan[16 * (MSM_TREE_THREADS / 32)];
+    const typename C::Fp f{};
+    const size_t j0 = (size_t)blockIdx.x * (MSM_TREE_THREADS * K) + threadIdx.x;
+    fe acc = fe_one(f);
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+        const size_t j = j0 + (size_t)k * MSM_TREE_THREADS;
+        if (j >= joins) break;
+        const TreeJoin<C, LEVEL0> t = tree_locate<C, LEVEL0>(j, level, m, keys, vals);
+        if (t.active) acc = fe_mul(f, acc, tree_denominator<C, LEVEL0>(t, rec, slots, sinf));
+        pref[2 * j] = make_uint4(acc.w[0], acc.w[1], acc.w[2], acc.w[3]);
+        pref[2 * j + 1] = make_uint4(acc.w[4], acc.w[5], acc.w[6], acc.w[7]);
+    }
+    fe total;
+    const fe oth = block_others_product<decltype(f), MSM_TREE_THREADS>(f, acc, sm_scan, &total);
+    const size_t tid = (size_t)blockIdx.x * MSM_TREE_THREADS + threadIdx.x;
+    others[2 * tid] = make_uint4(oth.w[0], oth.w[1], oth.w[2], oth.w[3]);
+    others[2 * tid + 1] = make_uint4(oth.w[4], oth.w[5], oth.w[6], oth.w[7]);
+    if (threadIdx.x == 0) col_store(totals, tiles, blockIdx.x, total);
+}
+
+template <class C, int K, bool LEVEL0>
+__global__ void __launch_bounds__(MSM_TREE_THREADS)
+k_msm_tree_bwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
+               const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
+               uint4* slots, uint8_t* sinf, const uint4* __restrict__ pref,
+               const uint4* __restrict__ others, const uint32_t* __restrict__ total_inv, size_t tiles) {
+    const typename C::Fp f{};
+    const size_t j0 = (size_t)blockIdx.x * (MSM_TREE_THREADS * K) + threadIdx.x;
+    if (j0 >= joins) return;
+    const size_t tid = (size_t)blockIdx.x * MSM_TREE_THREADS + threadIdx.x;
+    fe inv = fe_mul(f, col_load(total_inv, tiles, blockIdx.x), fe_from_u4(others[2 * tid], others[2 * tid + 1]));
+#pragma unroll 1
+    for (int k = K - 1; k >= 0; --k) {
+        const size_t j = j0 + (size_t)k * MSM_TREE_THREADS;
+        if (j >= joins) continue;
+        const TreeJoin<C, LEVEL0> t = tree_locate<C, LEVEL0>(j, level, m, keys, vals);
+        fe prev = fe_one(f);
+        if (k > 0) {
+            const size_t jp = j - MSM_TREE_THREADS;
+            prev = fe_from_u4(pref[2 * jp], pref[2 * jp + 1]);
+        }
+        tree_apply<C, LEVEL0>(t, inv, prev, k == 0, rec, slots, sinf);
+    }
+}
+
+// one thread per bucket: slot[start] + the slots at multiples of 2^MSM_TREE_LEVELS inside the run
+template <class C>
+__global__ void __launch_bounds__(128)
+k_msm_tail(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ starts,
+           const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
+           uint32_t* __restrict__ buckets) {
+    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= MSM_NB) return;
+    const typename C::Fp f{};
+    jac acc = jac_infinity<C>();
+    const size_t s = starts[b];
+    if (s != 0xFFFFFFFFu) {
+        if (!sinf[s]) {
+            acc.X = rec_x(slots, s);
+            acc.Y = rec_y(slots, s);
+            acc.Z = fe_one(f);
+        }
+        const size_t step = (size_t)1 << MSM_TREE_LEVELS;
+#pragma unroll 1
+        for (size_t a = (s / step + 1) * step; a < m && keys[a] == b; a += step) {
+            if (sinf[a]) continue;
+            aff q{rec_x(slots, a), rec_y(slots, a)};
+            acc = jac_madd<C>(acc, q);
+        }
+    }
+    jac_store(buckets, MSM_NB, b, acc);
+}
+
 // marginal sums, stage 1: thread (w, k, e, part) adds the 32 buckets of window w whose
 // k-th base-32 digit is e and whose next digit (cyclically) is `part`.
 template <class C>
@@ -264,13 +601,151 @@ k_msm_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, uint
     }
 }
 
+// ---------------------------------------------------------------- bucket reduction, second form
+// Used after the batch-affine tree.  Same decomposition as above (three base-32 marginal sums
+// per window), arranged so that no thread runs a long serial chain -- the chip is nearly empty
+// at this stage, so depth, not work, is the cost:
+//   k_msm_red_parts    : thread (w, k, e, part, sub) adds 8 buckets.  A bucket is read straight
+//                        from the tree's slots (slot[start] and the slots at multiples of
+//                        2^MSM_TREE_LEVELS inside its run), all AFFINE operands: mixed additions.
+//   k_msm_red_fold     : warp (w, k, e): 4 partials per lane, then a 5-step shuffle tree.
+//   k_msm_red_weighted : warp (w, k): lane e holds C_e; inclusive suffix scan S_e = sum_{e' >= e} C_e'
+//                        (5 steps), then sum_e e C_e = sum_{e >= 1} S_e (5-step tree); S_0 is the
+//                        plain total.
+//   k_msm_red_combine  : lane w forms S_w, shifts it by 2^(16 w); shuffle tree over the windows.
+constexpr uint32_t MSM_RED_PARTS = MSM_WINDOWS * 3 * 32 * 32 * 4;
+
+__device__ __forceinline__ jac jac_shfl_down(const jac& p, int d) {
+    jac r;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        r.X.w[i] = __shfl_down_sync(0xFFFFFFFFu, p.X.w[i], d);
+        r.Y.w[i] = __shfl_down_sync(0xFFFFFFFFu, p.Y.w[i], d);
+        r.Z.w[i] = __shfl_down_sync(0xFFFFFFFFu, p.Z.w[i], d);
+    }
+    return r;
+}
+// lane 0 ends with the sum of all 32 lanes' points
+template <class C>
+__device__ __forceinline__ jac warp_sum_points(jac acc, int lane) {
+#pragma unroll 1
+    for (int d = 16; d >= 1; d >>= 1) {
+        const jac other = jac_shfl_down(acc, d);
+        if (lane < d) acc = jac_add<C>(acc, other);
+    }
+    return acc;
+}
+
+template <class C>
+__global__ void __launch_bounds__(128)
+k_msm_red_parts(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ starts,
+                const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
+                uint32_t* __restrict__ parts) {
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= MSM_RED_PARTS) return;
+    const uint32_t sub = t & 3, part = (t >> 2) & 31, e = (t >> 7) & 31, k = (t >> 12) % 3, w = t / (3 * 4096);
+    const size_t step = (size_t)1 << MSM_TREE_LEVELS;
+    jac acc = jac_infinity<C>();
+#pragma unroll 1
+    for (uint32_t v = sub * 8; v < sub * 8 + 8; ++v) {
+        uint32_t b;
+        if (k == 0) b = e + 32 * part + 1024 * v;        // lo = e
+        else if (k == 1) b = part + 32 * e + 1024 * v;   // mid = e
+        else b = part + 32 * v + 1024 * e;               // top = e
+        const uint32_t id = w * MSM_BUCKETS + b;
+        const size_t s = starts[id];
+        if (s == 0xFFFFFFFFu) continue;
+        if (!sinf[s]) acc = jac_madd<C>(acc, aff{rec_x(slots, s), rec_y(slots, s)});
+#pragma unroll 1
+        for (size_t a = (s / step + 1) * step; a < m && keys[a] == id; a += step)
+            if (!sinf[a]) acc = jac_madd<C>(acc, aff{rec_x(slots, a), rec_y(slots, a)});
+    }
+    jac_store(parts, MSM_RED_PARTS, t, acc);
+}
+
+template <class C>
+__global__ void __launch_bounds__(128)
+k_msm_red_fold(const uint32_t* __restrict__ parts, uint32_t* __restrict__ marg) {
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (gw >= MSM_WINDOWS * 3 * 32) return;  // whole warps leave together
+    const size_t base = ((size_t)gw * 32 + lane) * 4;
+    jac acc = jac_load(parts, MSM_RED_PARTS, base);
+#pragma unroll 1
+    for (int sub = 1; sub < 4; ++sub) acc = jac_add<C>(acc, jac_load(parts, MSM_RED_PARTS, base + sub));
+    acc = warp_sum_points<C>(acc, lane);
+    if (lane == 0) jac_store(marg, (size_t)MSM_WINDOWS * 3 * 32, gw, acc);
+}
+
+template <class C>
+__global__ void __launch_bounds__(128)
+k_msm_red_weighted(const uint32_t* __restrict__ marg, uint32_t* __restrict__ wsum) {
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (gw >= MSM_WINDOWS * 3) return;
+    const uint32_t w = gw / 3, k = gw % 3;
+    jac S = jac_load(marg, (size_t)MSM_WINDOWS * 3 * 32, (size_t)gw * 32 + lane);
+#pragma unroll 1
+    for (int d = 1; d < 32; d <<= 1) {  // inclusive suffix sums
+        const jac other = jac_shfl_down(S, d);
+        if (lane + d < 32) S = jac_add<C>(S, other);
+    }
+    const size_t cnt = (size_t)MSM_WINDOWS * 4;
+    if (lane == 0 && k == 0) jac_store(wsum, cnt, w * 4 + 3, S);  // S_0 = sum_e C_e
+    jac R = lane == 0 ? jac_infinity<C>() : S;
+    R = warp_sum_points<C>(R, lane);                              // sum_{e >= 1} S_e = sum_e e C_e
+    if (lane == 0) jac_store(wsum, cnt, w * 4 + k, R);
+}
+
+template <class C>
+__global__ void __launch_bounds__(32)
+k_msm_red_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, uint32_t* __restrict__ oy,
+                  uint8_t* __restrict__ oinf) {
+    const uint32_t w = threadIdx.x;
+    const size_t cnt = (size_t)MSM_WINDOWS * 4;
+    jac s = jac_infinity<C>();
+    if (w < MSM_WINDOWS) {
+        s = jac_load(wsum, cnt, w * 4 + 2);
+#pragma unroll 1
+        for (int i = 0; i < 5; ++i) s = jac_dbl<C>(s);
+        s = jac_add<C>(s, jac_load(wsum, cnt, w * 4 + 1));
+#pragma unroll 1
+        for (int i = 0; i < 5; ++i) s = jac_dbl<C>(s);
+        s = jac_add<C>(s, jac_load(wsum, cnt, w * 4 + 0));
+        s = jac_add<C>(s, jac_load(wsum, cnt, w * 4 + 3));
+#pragma unroll 1
+        for (uint32_t i = 0; i < MSM_C * w; ++i) s = jac_dbl<C>(s);
+    }
+    s = warp_sum_points<C>(s, (int)w);
+    if (w == 0) {
+        const typename C::Fp f{};
+        if (jac_is_inf<C>(s)) {
+            col_store(ox, 1, 0, fe_zero());
+            col_store(oy, 1, 0, fe_zero());
+            oinf[0] = 1;
+        } else {
+            aff a = jac_to_aff_with<C>(s, fe_inv(f, s.Z));
+            col_store(ox, 1, 0, a.x);
+            col_store(oy, 1, 0, a.y);
+            oinf[0] = 0;
+        }
+    }
+}
+
 // ---------------------------------------------------------------- host side
 struct MsmPlan {
     size_t pairs, sort_temp, total;
     size_t slices;
     size_t off_keys, off_vals, off_keys2, off_vals2, off_buckets, off_edge, off_edge_key, off_parts, off_marg, off_wsum, off_temp;
+    size_t off_rec, off_slots, off_sinf, off_starts, off_pref, off_others, off_totals;
+    size_t max_tiles;
 };
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+// 0 auto (= 2), 1 mixed-Jacobian slices, 2 batch-affine tree with three launches per level,
+// 3 batch-affine tree with one launch per level (inversion inside the block)
+static int g_msm_form = 0;
+void set_msm_form(int form) { g_msm_form = form; }
+static bool msm_affine() { return g_msm_form != 1; }
+constexpr int MSM_TREE_KMIN = 2;  // fewest joins per thread any level uses
 
 static MsmPlan msm_plan(size_t n) {
     MsmPlan p{};
@@ -285,19 +760,63 @@ static MsmPlan msm_plan(size_t n) {
     p.off_vals2 = take(4 * p.pairs);
     p.slices = (p.pairs + MSM_SLICE - 1) / MSM_SLICE;
     p.off_buckets = take((size_t)96 * MSM_NB);
-    p.off_edge = take((size_t)96 * 2 * p.slices);
-    p.off_edge_key = take((size_t)4 * 2 * p.slices);
-    p.off_parts = take((size_t)96 * MSM_WINDOWS * 3 * 1024);
+    p.off_parts = take((size_t)96 * MSM_RED_PARTS);
     p.off_marg = take((size_t)96 * MSM_WINDOWS * 3 * 32);
     p.off_wsum = take((size_t)96 * MSM_WINDOWS * 4);
     p.off_temp = take(p.sort_temp);
-    p.total = at;
+    // the two accumulation forms never run in the same call: their scratch overlaps
+    const size_t fork = at;
+    p.off_edge = take((size_t)96 * 2 * p.slices);
+    p.off_edge_key = take((size_t)4 * 2 * p.slices);
+    const size_t end_jac = at;
+    at = fork;
+    p.off_rec = take((size_t)64 * n);
+    p.off_slots = take((size_t)64 * p.pairs);
+    p.off_sinf = take(p.pairs);
+    p.off_starts = take((size_t)4 * MSM_NB);
+    const size_t joins0 = (p.pairs + 1) / 2;
+    p.off_pref = take((size_t)32 * joins0);
+    p.max_tiles = (joins0 + (size_t)MSM_TREE_THREADS * MSM_TREE_KMIN - 1) / ((size_t)MSM_TREE_THREADS * MSM_TREE_KMIN);
+    p.off_others = take((size_t)32 * MSM_TREE_THREADS * p.max_tiles);
+    p.off_totals = take((size_t)2 * 32 * (p.max_tiles + 64));
+    p.total = at > end_jac ? at : end_jac;
     return p;
 }
 size_t msm_scratch_bytes(size_t n) { return n ? msm_plan(n).total : 0; }
 
+struct TreeBufs {
+    const uint32_t *keys, *vals;
+    const uint4* rec;
+    uint4* slots;
+    uint8_t* sinf;
+    uint4 *pref, *others;
+    uint32_t* totals;
+    size_t max_tiles;
+};
+template <class C, int K, bool LEVEL0>
+static cudaError_t launch_tree(int curve, size_t m, int level, const TreeBufs& b, bool split, cudaStream_t s) {
+    const size_t span = (size_t)2 << level;
+    const size_t joins = (m + span - 1) / span;  // nodes of size 2^(level+1) that have a left half
+    const size_t per_block = (size_t)MSM_TREE_THREADS * K;
+    const size_t tiles = (joins + per_block - 1) / per_block;
+    const unsigned blocks = (unsigned)tiles;
+    if constexpr (K <= 8) {
+        if (!split) {
+            k_msm_tree<C, K, LEVEL0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots, b.sinf);
+            return cudaGetLastError();
+        }
+    }
+    uint32_t* total_inv = b.totals + 8 * (b.max_tiles + 64);
+    k_msm_tree_fwd<C, K, LEVEL0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots,
+                                                                      b.sinf, b.pref, b.others, b.totals, tiles);
+    if (cudaError_t e = launch_batch_invert(curve, 0, tiles, b.totals, total_inv, s)) return e;
+    k_msm_tree_bwd<C, K, LEVEL0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots,
+                                                                      b.sinf, b.pref, b.others, total_inv, tiles);
+    return cudaGetLastError();
+}
+
 template <class C>
-static cudaError_t run_msm(size_t n, const uint32_t* scalars, const uint32_t* px, const uint32_t* py,
+static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px, const uint32_t* py,
                            const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
                            void* scratch, cudaStream_t s, int* launches) {
     MsmPlan p = msm_plan(n);
@@ -311,17 +830,54 @@ static cudaError_t run_msm(size_t n, const uint32_t* scalars, const uint32_t* px
     cudaError_t e = cub::DeviceRadixSort::SortPairs(base + p.off_temp, temp, keys, keys2, vals, vals2,
                                                     (int64_t)p.pairs, 0, 20, s);
     if (e != cudaSuccess) return e;
-    uint32_t *edge = (uint32_t*)(base + p.off_edge), *edge_key = (uint32_t*)(base + p.off_edge_key);
-    e = cudaMemsetAsync(buckets, 0, (size_t)96 * MSM_NB, s);  // empty buckets = infinity (Z = 0)
-    if (e != cudaSuccess) return e;
-    const unsigned sb = (unsigned)((p.slices + 127) / 128);
-    k_msm_buckets<C><<<sb, 128, 0, s>>>(n, p.pairs, keys2, vals2, px, py, buckets, edge, edge_key, p.slices);
-    k_msm_bucket_edges<C><<<sb, 128, 0, s>>>(buckets, edge, edge_key, p.slices);
+    if (msm_affine()) {
+        uint4 *rec = (uint4*)(base + p.off_rec), *slots = (uint4*)(base + p.off_slots);
+        uint8_t* sinf = base + p.off_sinf;
+        uint32_t* starts = (uint32_t*)(base + p.off_starts);
+        const size_t m = p.pairs;
+        e = cudaMemsetAsync(starts, 0xFF, (size_t)4 * MSM_NB, s);
+        if (e != cudaSuccess) return e;
+        k_msm_starts<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, keys2, starts);
+        k_msm_aos<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, px, py, rec);
+        // K joins per thread; thin levels take fewer per thread so that the chip stays filled
+        const bool split = g_msm_form != 3;
+        TreeBufs tb{keys2, vals2, rec, slots, sinf, (uint4*)(base + p.off_pref), (uint4*)(base + p.off_others),
+                    (uint32_t*)(base + p.off_totals), p.max_tiles};
+        // joins per thread: as many as keep >= ~8 blocks per SM in flight (the scan share is 14 / K
+        // products per join).  The single-launch form parks prefixes in shared memory: K <= 8.
+        const size_t fill = (size_t)148 * 8 * MSM_TREE_THREADS;
+        const size_t joins0 = (m + 1) / 2;
+        if (split && joins0 >= 16 * fill) e = launch_tree<C, 16, true>(curve, m, 0, tb, split, s);
+        else e = launch_tree<C, 8, true>(curve, m, 0, tb, split, s);
+        if (e != cudaSuccess) return e;
+        for (int l = 1; l < MSM_TREE_LEVELS; ++l) {
+            const size_t joins = (m + ((size_t)2 << l) - 1) / ((size_t)2 << l);
+            if (split && joins >= 16 * fill) e = launch_tree<C, 16, false>(curve, m, l, tb, split, s);
+            else if (joins >= 8 * fill) e = launch_tree<C, 8, false>(curve, m, l, tb, split, s);
+            else if (joins >= 4 * fill) e = launch_tree<C, 4, false>(curve, m, l, tb, split, s);
+            else e = launch_tree<C, MSM_TREE_KMIN, false>(curve, m, l, tb, split, s);
+            if (e != cudaSuccess) return e;
+        }
+        k_msm_red_parts<C><<<(MSM_RED_PARTS + 127) / 128, 128, 0, s>>>(m, keys2, starts, slots, sinf, parts);
+        k_msm_red_fold<C><<<(MSM_WINDOWS * 3 * 32 * 32 + 127) / 128, 128, 0, s>>>(parts, marg);
+        k_msm_red_weighted<C><<<(MSM_WINDOWS * 3 * 32 + 127) / 128, 128, 0, s>>>(marg, wsum);
+        k_msm_red_combine<C><<<1, 32, 0, s>>>(wsum, ox, oy, oinf);
+        *launches = 3 + (split ? 3 : 1) * MSM_TREE_LEVELS + 4 + 4;  // + the sort's passes
+        return cudaGetLastError();
+    } else {
+        uint32_t *edge = (uint32_t*)(base + p.off_edge), *edge_key = (uint32_t*)(base + p.off_edge_key);
+        e = cudaMemsetAsync(buckets, 0, (size_t)96 * MSM_NB, s);  // empty buckets = infinity (Z = 0)
+        if (e != cudaSuccess) return e;
+        const unsigned sb = (unsigned)((p.slices + 127) / 128);
+        k_msm_buckets<C><<<sb, 128, 0, s>>>(n, p.pairs, keys2, vals2, px, py, buckets, edge, edge_key, p.slices);
+        k_msm_bucket_edges<C><<<sb, 128, 0, s>>>(buckets, edge, edge_key, p.slices);
+        *launches = 3;
+    }
     k_msm_marginal_parts<C><<<(MSM_WINDOWS * 3 * 1024 + 127) / 128, 128, 0, s>>>(buckets, parts);
     k_msm_marginal_fold<C><<<(MSM_WINDOWS * 3 * 32 + 127) / 128, 128, 0, s>>>(parts, marg);
     k_msm_weighted<C><<<1, 128, 0, s>>>(marg, wsum);
     k_msm_combine<C><<<1, 32, 0, s>>>(wsum, ox, oy, oinf);
-    *launches = 7 + 4;  // ours + the sort's passes (approximate; CUB picks the pass count)
+    *launches += 4 + 4;  // reduction + the sort's passes (approximate; CUB picks the pass count)
     return cudaGetLastError();
 }
 
@@ -329,8 +885,8 @@ cudaError_t launch_msm(int curve, size_t n, const uint32_t* scalars, const uint3
                        const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
                        uint8_t* oinf, void* scratch, cudaStream_t s, int* launches) {
     if (curve == CURVE_SECP)
-        return run_msm<SecpCurve>(n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
-    return run_msm<Sm2Curve>(n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
+        return run_msm<SecpCurve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
+    return run_msm<Sm2Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
 }
 
 }  // namespace gecc

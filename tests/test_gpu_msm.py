@@ -21,6 +21,14 @@ def ctxs():
         x.close()
 
 
+@pytest.fixture(params=["affine", "affine1", "jacobian"], autouse=True)
+def msm_form(request):
+    """every test runs with both bucket-accumulation forms (results must be identical)"""
+    gecc.set_msm_form(request.param)
+    yield request.param
+    gecc.set_msm_form("auto")
+
+
 def same(A, B):
     return all((np.asarray(a) == np.asarray(b)).all() for a, b in zip(A, B))
 
@@ -80,3 +88,27 @@ def test_msm_identity_2_20(ctxs):
     a = ctx.msm(cut(s, 0, h), tuple(cut(x, 0, h) for x in P))
     b = ctx.msm(cut(s, h, n), tuple(cut(x, h, n) for x in P))
     assert same(ctx.batch_padd(a, b), got)
+
+
+@pytest.mark.parametrize("cid", [0, 1])
+def test_msm_skewed_buckets(ctxs, cid):
+    """Runs far longer than a tree node: one scalar for every point (17 runs of n entries),
+    a handful of distinct scalars, the same point everywhere (tangent joins at every level),
+    and alternating P / -P (every join cancels)."""
+    ctx, c = ctxs[cid], E.CURVES[cid]
+    rng = random.Random(50 + cid)
+    n = 1500
+    P = ctx.batch_fpmul(gecc.cols_from_ints([rng.randrange(1, c.n) for _ in range(n)]))
+    k = rng.randrange(1, c.n)
+    for ks in ([k] * n, [rng.choice([k, 3, c.n - 3, 1 << 200]) for _ in range(n)]):
+        s = gecc.cols_from_ints(ks)
+        assert same(ctx.msm(s, P), O.msm(cid, s, P))
+    Q = tuple(np.ascontiguousarray(np.repeat(a[..., :1], n, axis=-1)) for a in P)
+    s = gecc.cols_from_ints([k] * n)
+    assert same(ctx.msm(s, Q), O.msm(cid, s, Q))
+    s = gecc.cols_from_ints([k if i % 2 == 0 else c.n - k for i in range(n)])
+    assert ctx.msm(s, Q)[2][0] == 1
+    s = gecc.cols_from_ints([k if i % 2 == 0 else c.n - k for i in range(n - 1)] + [0])
+    got = ctx.msm(s, Q)
+    one = tuple(np.ascontiguousarray(a[..., :1]) for a in Q)
+    assert same(got, O.msm(cid, gecc.cols_from_ints([k]), one))
