@@ -53,7 +53,20 @@ SECP256K1 = Curve(
     gy=0x483ADA7726A3C4655DA4FBFC0E1108A8FD17B448A68554199C47D08FFB10D4B8,
 )
 
-CURVES = {0: SM2, 1: SECP256K1, "sm2": SM2, "secp256k1": SECP256K1}
+# BLS12-381 G1 (the pairing-friendly curve of north_star's 381-bit field; not in the reference,
+# which is 256-bit only): y^2 = x^3 + 4 over the 381-bit prime, prime-order subgroup of order n,
+# standard generator (draft-irtf-cfrg-pairing-friendly-curves, section 4.2.1).
+BLS12_381 = Curve(
+    "bls12_381", 2,
+    p=0x1a0111ea397fe69a4b1ba7b6434bacd764774b84f38512bf6730d2a0f6b0f6241eabfffeb153ffffb9feffffffffaaab,
+    a=0,
+    b=4,
+    n=0x73eda753299d7d483339d80809a1d80553bda402fffe5bfeffffffff00000001,
+    gx=0x17f1d3a73197d7942695638c4fa9ac0fc3688c4f9774b905a14e3a3f171bac586c55e83ff97a1aeffb3af00adb22c6bb,
+    gy=0x08b3f481e3aaa0f1a09e30ed741d8ae4fcf5e095d5d00af600db18cb2c04b3edd03cc744a2888ae40caa232946c5e7e1,
+)
+
+CURVES = {0: SM2, 1: SECP256K1, 2: BLS12_381, "sm2": SM2, "secp256k1": SECP256K1, "bls12_381": BLS12_381}
 
 INF = None  # point at infinity
 

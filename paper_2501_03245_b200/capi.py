@@ -16,7 +16,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libgecc_b200.so")
 
-SM2, SECP256K1 = 0, 1
+SM2, SECP256K1, BLS12_381 = 0, 1, 2
 FIELD_P, FIELD_N = 0, 1
 STATUS = {0: "ok", 1: "invalid argument", 2: "malformed input", 3: "invalid peer point",
           4: "degenerate result", 5: "nonce retries exhausted", 6: "cost model has no crossover",
@@ -78,10 +78,12 @@ def set_msm_form(form: str):
     lib().gecc_set_msm_form(MSM_FORMS[form])
 
 
-def cols_from_ints(vals) -> np.ndarray:
+def cols_from_ints(vals, limbs: int = 8) -> np.ndarray:
+    """ints -> column buffer [limbs, n] (limb k of element i at [k, i]; 8 limbs = 256 bits,
+    12 limbs = the 381-bit coordinates of BLS12-381)"""
     n = len(vals)
-    raw = b"".join(int(v).to_bytes(32, "little") for v in vals)
-    return np.ascontiguousarray(np.frombuffer(raw, dtype="<u4").reshape(n, 8).T)
+    raw = b"".join(int(v).to_bytes(4 * limbs, "little") for v in vals)
+    return np.ascontiguousarray(np.frombuffer(raw, dtype="<u4").reshape(n, limbs).T)
 
 
 def ints_from_cols(cols: np.ndarray):
@@ -116,6 +118,7 @@ class Context:
                             "(libgecc_b200 has no CPU path)")
         self.h = C.c_void_p(h)
         self.curve = self.l.gecc_ctx_curve(self.h)
+        self.limbs = 12 if self.curve == BLS12_381 else 8  # 32-bit limbs per coordinate
 
     def close(self):
         if getattr(self, "h", None):
@@ -164,7 +167,7 @@ class Context:
     # -- field layer
     def field_op(self, field: int, op: str, a: np.ndarray, b: np.ndarray | None = None):
         n = a.shape[1]
-        out = np.zeros((8, n), np.uint32)
+        out = np.zeros((self.limbs if field == 0 else 8, n), np.uint32)
         rc = self.l.gecc_field_op(self.h, field, FIELD_OPS[op], C.c_size_t(n), _vp(a), _vp(b), _vp(out))
         if self._check(rc, "gecc_field_op"):
             raise ValueError(f"gecc_field_op rc={rc}")
@@ -196,15 +199,14 @@ class Context:
     # -- batch layer (host column buffers)
     def batch_invert(self, field: int, a: np.ndarray):
         n = a.shape[1]
-        out = np.zeros((8, n), np.uint32)
+        out = np.zeros((self.limbs if field == 0 else 8, n), np.uint32)
         rc = self.l.gecc_batch_invert(self.h, field, C.c_size_t(n), _vp(a), _vp(out))
         if self._check(rc, "gecc_batch_invert"):
             raise ValueError(f"gecc_batch_invert rc={rc}")
         return out
 
-    @staticmethod
-    def _pts_out(n):
-        return np.zeros((8, n), np.uint32), np.zeros((8, n), np.uint32), np.zeros(n, np.uint8)
+    def _pts_out(self, n):
+        return np.zeros((self.limbs, n), np.uint32), np.zeros((self.limbs, n), np.uint32), np.zeros(n, np.uint8)
 
     def batch_padd(self, P, T):
         if P[0].shape != T[0].shape:

@@ -56,6 +56,7 @@ struct sm2b_ctx {
     uint32_t* gtab = nullptr;   // fixed-base table (Montgomery form), built on the GPU at creation
     uint32_t* gtab_rec = nullptr;  // table of the byte-record kernels (== gtab on SM2, plain form on secp256k1)
     uint32_t* flags = nullptr;  // device word: malformed-call flag of sign / ecdh
+    int limbs = 8;              // 32-bit limbs per coordinate (12 on BLS12-381)
 };
 
 namespace {
@@ -80,6 +81,9 @@ sm2b_status fail_msg(sm2b_ctx* ctx, const char* what) {
     ctx->last_error = what;
     return SM2B_ERROR_INTERNAL;
 }
+
+// limbs per element of a column buffer: coordinates follow the curve, scalars are 256-bit
+size_t field_limbs(const sm2b_ctx* ctx, int field) { return field == 0 ? (size_t)ctx->limbs : 8; }
 
 #define CU(ctx, call)                                        \
     do {                                                     \
@@ -106,7 +110,8 @@ struct Carver {
 extern "C" {
 
 sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device) {
-    if (curve != GECC_CURVE_SM2 && curve != GECC_CURVE_SECP256K1) return nullptr;
+    if (curve != GECC_CURVE_SM2 && curve != GECC_CURVE_SECP256K1 && curve != GECC_CURVE_BLS12_381)
+        return nullptr;
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
         fprintf(stderr, "gecc_b200: no usable CUDA device (this library has no CPU path)\n");
@@ -118,7 +123,8 @@ sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device) {
     if (device >= count) return nullptr;
     sm2b_ctx* ctx = new (std::nothrow) sm2b_ctx();
     if (!ctx) return nullptr;
-    ctx->curve = curve == GECC_CURVE_SM2 ? CURVE_SM2 : CURVE_SECP;
+    ctx->curve = curve == GECC_CURVE_SM2 ? CURVE_SM2 : curve == GECC_CURVE_SECP256K1 ? CURVE_SECP : CURVE_BLS381;
+    ctx->limbs = curve_limbs(ctx->curve);
     ctx->device = device;
     DeviceGuard g(device);
     cudaDeviceProp prop;
@@ -131,6 +137,13 @@ sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device) {
     }
     ctx->sm_count = prop.multiProcessorCount;
     ctx->stream = ctx->own_stream;
+    if (ctx->curve == CURVE_BLS381) {  // field / batch / MSM layer only: no ECDSA, no fixed-base table
+        if (cudaMalloc(&ctx->flags, 256) != cudaSuccess) {
+            sm2b_ctx_free(ctx);
+            return nullptr;
+        }
+        return ctx;
+    }
     // fixed-base table (sm2b_ctx_new builds sm2_base_table() eagerly too, capi.cpp:101)
     uint32_t* bases = nullptr;
     bool ok = cudaMalloc(&ctx->gtab, gtable_words() * 4) == cudaSuccess &&
@@ -217,7 +230,7 @@ sm2b_status sm2b_crossover_n(uint64_t cost_add, uint64_t cost_mul, uint64_t cost
 }
 
 int gecc_ctx_curve(const sm2b_ctx* ctx) {
-    return ctx ? (ctx->curve == CURVE_SM2 ? GECC_CURVE_SM2 : GECC_CURVE_SECP256K1) : -1;
+    return ctx ? ctx->curve : -1;  // internal ids equal the public enum
 }
 int gecc_ctx_device(const sm2b_ctx* ctx) { return ctx ? ctx->device : -1; }
 const char* gecc_last_error(const sm2b_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
@@ -253,12 +266,12 @@ sm2b_status gecc_field_op(sm2b_ctx* ctx, gecc_field field, gecc_field_opcode op,
     {
         std::lock_guard<std::mutex> lk(ctx->mu);
         DeviceGuard g(ctx->device);
-        const size_t bytes = 32 * n;
+        const size_t bytes = 4 * field_limbs(ctx, field) * n;
         CU(ctx, ctx->in.ensure(2 * Carver::need(bytes)));
         CU(ctx, ctx->out.ensure(Carver::need(bytes)));
         Carver ci(ctx->in.p);
-        da = ci.take<uint32_t>(8 * n);
-        db = ci.take<uint32_t>(8 * n);
+        da = ci.take<uint32_t>(bytes / 4);
+        db = ci.take<uint32_t>(bytes / 4);
         dout = (uint32_t*)ctx->out.p;
         CU(ctx, cudaMemcpyAsync(da, a, bytes, cudaMemcpyHostToDevice, ctx->stream));
         if (b) CU(ctx, cudaMemcpyAsync(db, b, bytes, cudaMemcpyHostToDevice, ctx->stream));
@@ -267,7 +280,7 @@ sm2b_status gecc_field_op(sm2b_ctx* ctx, gecc_field field, gecc_field_opcode op,
     if (st != SM2B_OK) return st;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
-    CU(ctx, cudaMemcpyAsync(out, dout, 32 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(out, dout, 4 * field_limbs(ctx, field) * n, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     return SM2B_OK;
 }
@@ -377,6 +390,7 @@ extern "C" {
 sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
                             const uint8_t* publics, const uint8_t* signatures,
                             uint8_t* results) {
+    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (count > 0 && (!digests || !publics || !signatures || !results)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -395,6 +409,7 @@ sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
 
 sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
                         const uint8_t* publics, const uint8_t* signatures, uint8_t* results) {
+    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (count > 0 && (!digests || !publics || !signatures || !results)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     if (count == 0) return SM2B_OK;
@@ -442,6 +457,7 @@ sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
 sm2b_status gecc_sign_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
                           const uint8_t* secrets, uint64_t nonce_seed, uint64_t lane_base,
                           uint8_t* signatures, int32_t* lane_status) {
+    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (count > 0 && (!digests || !secrets || !signatures || !lane_status)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     if (nonce_seed == 0) return fail_msg(ctx, "device signing needs a non-zero nonce seed");
@@ -484,6 +500,7 @@ sm2b_status report_lanes(const int32_t* st, size_t n, int32_t* lane_status) {
 sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const uint8_t* secrets,
                       uint64_t nonce_seed, uint64_t lane_base, uint8_t* signatures,
                       int32_t* lane_status) {
+    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (count > 0 && (!digests || !secrets || !signatures)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     if (count == 0) return SM2B_OK;
@@ -550,6 +567,7 @@ sm2b_status sm2b_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const
 
 sm2b_status gecc_keygen(sm2b_ctx* ctx, uint64_t seed, uint64_t lane_base, size_t count,
                         uint8_t* secrets, uint8_t* publics) {
+    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (count > 0 && (!secrets || !publics))) return SM2B_ERROR_INVALID_ARGUMENT;
     if (count == 0) return SM2B_OK;
     if (seed == 0) seed = system_seed();
@@ -574,6 +592,7 @@ sm2b_status sm2b_keygen(sm2b_ctx* ctx, uint64_t seed, size_t count, uint8_t* sec
 
 sm2b_status sm2b_ecdh(sm2b_ctx* ctx, size_t count, const uint8_t* secrets, const uint8_t* peers,
                       uint8_t* shared, int32_t* lane_status) {
+    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (count > 0 && (!secrets || !peers || !shared))) return SM2B_ERROR_INVALID_ARGUMENT;
     if (count == 0) return SM2B_OK;
     std::vector<int32_t> hst(count);
@@ -643,6 +662,7 @@ sm2b_status gecc_batch_pdbl_dev(sm2b_ctx* ctx, size_t n, const uint32_t* px, con
 }
 sm2b_status gecc_batch_fpmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, uint32_t* ox,
                                  uint32_t* oy, uint8_t* oinf) {
+    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (n > 0 && (!scalars || !ox || !oy || !oinf))) return SM2B_ERROR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
@@ -654,6 +674,7 @@ sm2b_status gecc_batch_fpmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalar
 sm2b_status gecc_batch_upmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars,
                                  const uint32_t* px, const uint32_t* py, const uint8_t* pinf,
                                  uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (n > 0 && (!scalars || !px || !py || !ox || !oy || !oinf)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -679,7 +700,8 @@ struct HostPoints {
 template <class Body>
 sm2b_status run_points(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const HostPoints* p,
                        const HostPoints* t, uint32_t* ox, uint32_t* oy, uint8_t* oinf, Body body) {
-    const size_t cb = Carver::need(32 * n), mb = Carver::need(n);
+    const size_t L = (size_t)ctx->limbs, pb = 4 * L * n;  // bytes per coordinate column buffer
+    const size_t cb = Carver::need(pb), mb = Carver::need(n);
     uint32_t *dk = nullptr, *dpx = nullptr, *dpy = nullptr, *dtx = nullptr, *dty = nullptr;
     uint8_t *dpi = nullptr, *dti = nullptr;
     uint32_t *dox, *doy;
@@ -690,21 +712,21 @@ sm2b_status run_points(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const H
         CU(ctx, ctx->in.ensure(5 * cb + 2 * mb));
         CU(ctx, ctx->out.ensure(2 * cb + mb));
         Carver ci(ctx->in.p), co(ctx->out.p);
-        dox = co.take<uint32_t>(8 * n);
-        doy = co.take<uint32_t>(8 * n);
+        dox = co.take<uint32_t>(L * n);
+        doy = co.take<uint32_t>(L * n);
         doi = co.take<uint8_t>(n);
         auto up = [&](const void* h, size_t bytes, void* d) {
             return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream);
         };
         if (scalars) { dk = ci.take<uint32_t>(8 * n); CU(ctx, up(scalars, 32 * n, dk)); }
         if (p) {
-            dpx = ci.take<uint32_t>(8 * n); dpy = ci.take<uint32_t>(8 * n);
-            CU(ctx, up(p->x, 32 * n, dpx)); CU(ctx, up(p->y, 32 * n, dpy));
+            dpx = ci.take<uint32_t>(L * n); dpy = ci.take<uint32_t>(L * n);
+            CU(ctx, up(p->x, pb, dpx)); CU(ctx, up(p->y, pb, dpy));
             if (p->inf) { dpi = ci.take<uint8_t>(n); CU(ctx, up(p->inf, n, dpi)); }
         }
         if (t) {
-            dtx = ci.take<uint32_t>(8 * n); dty = ci.take<uint32_t>(8 * n);
-            CU(ctx, up(t->x, 32 * n, dtx)); CU(ctx, up(t->y, 32 * n, dty));
+            dtx = ci.take<uint32_t>(L * n); dty = ci.take<uint32_t>(L * n);
+            CU(ctx, up(t->x, pb, dtx)); CU(ctx, up(t->y, pb, dty));
             if (t->inf) { dti = ci.take<uint8_t>(n); CU(ctx, up(t->inf, n, dti)); }
         }
     }
@@ -712,8 +734,8 @@ sm2b_status run_points(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const H
     if (st != SM2B_OK) return st;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
-    CU(ctx, cudaMemcpyAsync(ox, dox, 32 * n, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaMemcpyAsync(oy, doy, 32 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(ox, dox, pb, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(oy, doy, pb, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaMemcpyAsync(oinf, doi, n, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     return SM2B_OK;
@@ -729,17 +751,18 @@ sm2b_status gecc_batch_invert(sm2b_ctx* ctx, gecc_field field, size_t n, const u
     {
         std::lock_guard<std::mutex> lk(ctx->mu);
         DeviceGuard g(ctx->device);
-        CU(ctx, ctx->in.ensure(32 * n));
-        CU(ctx, ctx->out.ensure(32 * n));
+        const size_t bytes = 4 * field_limbs(ctx, field) * n;
+        CU(ctx, ctx->in.ensure(bytes));
+        CU(ctx, ctx->out.ensure(bytes));
         din = (uint32_t*)ctx->in.p;
         dout = (uint32_t*)ctx->out.p;
-        CU(ctx, cudaMemcpyAsync(din, in, 32 * n, cudaMemcpyHostToDevice, ctx->stream));
+        CU(ctx, cudaMemcpyAsync(din, in, bytes, cudaMemcpyHostToDevice, ctx->stream));
     }
     sm2b_status st = gecc_batch_invert_dev(ctx, field, n, din, dout);
     if (st != SM2B_OK) return st;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
-    CU(ctx, cudaMemcpyAsync(out, dout, 32 * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(out, dout, 4 * field_limbs(ctx, field) * n, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     return SM2B_OK;
 }
@@ -770,6 +793,7 @@ sm2b_status gecc_batch_pdbl(sm2b_ctx* ctx, size_t n, const uint32_t* px, const u
 }
 sm2b_status gecc_batch_fpmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, uint32_t* ox,
                              uint32_t* oy, uint8_t* oinf) {
+    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (n > 0 && (!scalars || !ox || !oy || !oinf))) return SM2B_ERROR_INVALID_ARGUMENT;
     if (n == 0) return SM2B_OK;
     return run_points(ctx, n, scalars, nullptr, nullptr, ox, oy, oinf,
@@ -781,6 +805,7 @@ sm2b_status gecc_batch_fpmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, u
 sm2b_status gecc_batch_upmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uint32_t* px,
                              const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
                              uint8_t* oinf) {
+    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (n > 0 && (!scalars || !px || !py || !ox || !oy || !oinf)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     if (n == 0) return SM2B_OK;
@@ -812,6 +837,7 @@ extern "C" {
 sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, size_t n,
                            size_t lanes, uint32_t workers, uint64_t seed, uint32_t repeats,
                            sm2b_bench_report* out) {
+    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || !op || !strategy || !out) return SM2B_ERROR_INVALID_ARGUMENT;
     static const char* const ops[] = {"padd", "fpmul", "upmul", "sign", "verify"};
     int opi = -1;
@@ -958,12 +984,12 @@ sm2b_status gecc_msm_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
     if (n == 0) {  // empty sum = point at infinity
-        CU(ctx, cudaMemsetAsync(ox, 0, 32, ctx->stream));
-        CU(ctx, cudaMemsetAsync(oy, 0, 32, ctx->stream));
+        CU(ctx, cudaMemsetAsync(ox, 0, 4 * ctx->limbs, ctx->stream));
+        CU(ctx, cudaMemsetAsync(oy, 0, 4 * ctx->limbs, ctx->stream));
         CU(ctx, cudaMemsetAsync(oinf, 1, 1, ctx->stream));
         return SM2B_OK;
     }
-    CU(ctx, ctx->scratch.ensure(msm_scratch_bytes(n)));
+    CU(ctx, ctx->scratch.ensure(msm_scratch_bytes(n, ctx->curve)));
     int launches = 0;
     CU(ctx, launch_msm(ctx->curve, n, scalars, px, py, pinf, ox, oy, oinf, ctx->scratch.p, ctx->stream,
                        &launches));
@@ -981,20 +1007,21 @@ sm2b_status gecc_msm(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uin
     {
         std::lock_guard<std::mutex> lk(ctx->mu);
         DeviceGuard g(ctx->device);
-        const size_t cb = Carver::need(32 * n), mb = Carver::need(n);
+        const size_t L = (size_t)ctx->limbs;
+        const size_t cb = Carver::need(4 * L * n), mb = Carver::need(n);
         CU(ctx, ctx->in.ensure(3 * cb + mb + 256));
         CU(ctx, ctx->out.ensure(1024));
         Carver ci(ctx->in.p), co(ctx->out.p);
-        dox = co.take<uint32_t>(8);
-        doy = co.take<uint32_t>(8);
+        dox = co.take<uint32_t>(L);
+        doy = co.take<uint32_t>(L);
         doi = co.take<uint8_t>(1);
         if (n) {
             dk = ci.take<uint32_t>(8 * n);
-            dpx = ci.take<uint32_t>(8 * n);
-            dpy = ci.take<uint32_t>(8 * n);
+            dpx = ci.take<uint32_t>(L * n);
+            dpy = ci.take<uint32_t>(L * n);
             CU(ctx, cudaMemcpyAsync(dk, scalars, 32 * n, cudaMemcpyHostToDevice, ctx->stream));
-            CU(ctx, cudaMemcpyAsync(dpx, px, 32 * n, cudaMemcpyHostToDevice, ctx->stream));
-            CU(ctx, cudaMemcpyAsync(dpy, py, 32 * n, cudaMemcpyHostToDevice, ctx->stream));
+            CU(ctx, cudaMemcpyAsync(dpx, px, 4 * L * n, cudaMemcpyHostToDevice, ctx->stream));
+            CU(ctx, cudaMemcpyAsync(dpy, py, 4 * L * n, cudaMemcpyHostToDevice, ctx->stream));
             if (pinf) {
                 dpi = ci.take<uint8_t>(n);
                 CU(ctx, cudaMemcpyAsync(dpi, pinf, n, cudaMemcpyHostToDevice, ctx->stream));
@@ -1005,8 +1032,8 @@ sm2b_status gecc_msm(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uin
     if (st != SM2B_OK) return st;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
-    CU(ctx, cudaMemcpyAsync(ox, dox, 32, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaMemcpyAsync(oy, doy, 32, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(ox, dox, 4 * ctx->limbs, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(oy, doy, 4 * ctx->limbs, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaMemcpyAsync(oinf, doi, 1, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     return SM2B_OK;

@@ -13,8 +13,8 @@ enum : uint32_t { K_GENERIC = 0, K_TANGENT, K_INFINITY, K_COPY_LEFT, K_COPY_RIGH
 
 // classification + denominator of one pair (batch_point.cpp:91-111)
 template <class C>
-__device__ __forceinline__ uint32_t classify_pair(const fe& px, const fe& py, bool pinf,
-                                                  const fe& tx, const fe& ty, bool tinf, fe* d) {
+__device__ __forceinline__ uint32_t classify_pair(const cfe<C>& px, const cfe<C>& py, bool pinf,
+                                                  const cfe<C>& tx, const cfe<C>& ty, bool tinf, cfe<C>* d) {
     const typename C::Fp f{};
     if (pinf && tinf) return K_INFINITY;
     if (pinf) return K_COPY_RIGHT;
@@ -31,37 +31,47 @@ __device__ __forceinline__ uint32_t classify_pair(const fe& px, const fe& py, bo
 }
 
 template <class C>
-__device__ __forceinline__ void finish_lambda(const fe& lam, const fe& x1, const fe& x2,
-                                              const fe& y1, fe* xr, fe* yr) {
+__device__ __forceinline__ void finish_lambda(const cfe<C>& lam, const cfe<C>& x1, const cfe<C>& x2,
+                                              const cfe<C>& y1, cfe<C>* xr, cfe<C>* yr) {
     const typename C::Fp f{};
     *xr = fe_sub(f, fe_sub(f, fe_sqr(f, lam), x1), x2);
     *yr = fe_sub(f, fe_mul(f, lam, fe_sub(f, x1, *xr)), y1);
 }
 template <class C>
-__device__ __forceinline__ fe tangent_numerator(const fe& x) {  // 3x^2 + a
+__device__ __forceinline__ cfe<C> tangent_numerator(const cfe<C>& x) {  // 3x^2 + a
     const typename C::Fp f{};
-    fe x2 = fe_sqr(f, x);
-    fe num = fe_add(f, fe_dbl(f, x2), x2);
+    cfe<C> x2 = fe_sqr(f, x);
+    cfe<C> num = fe_add(f, fe_dbl(f, x2), x2);
     if (C::a_kind == A_ZERO) return num;
     return fe_add(f, num, curve_a<C>());
 }
 
-__device__ __forceinline__ fe fe_shfl_up(const fe& v, int d) {
-    fe r;
+template <int N>
+__device__ __forceinline__ feN<N> fe_shfl_up(const feN<N>& v, int d) {
+    feN<N> r;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r.w[i] = __shfl_up_sync(0xFFFFFFFFu, v.w[i], d);
+    for (int i = 0; i < N; ++i) r.w[i] = __shfl_up_sync(0xFFFFFFFFu, v.w[i], d);
     return r;
 }
-__device__ __forceinline__ fe fe_shfl_down(const fe& v, int d) {
-    fe r;
+template <int N>
+__device__ __forceinline__ feN<N> fe_shfl_down(const feN<N>& v, int d) {
+    feN<N> r;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r.w[i] = __shfl_down_sync(0xFFFFFFFFu, v.w[i], d);
+    for (int i = 0; i < N; ++i) r.w[i] = __shfl_down_sync(0xFFFFFFFFu, v.w[i], d);
+    return r;
+}
+template <int N>
+__device__ __forceinline__ feN<N> fe_shfl(const feN<N>& v, int src) {
+    feN<N> r;
+#pragma unroll
+    for (int i = 0; i < N; ++i) r.w[i] = __shfl_sync(0xFFFFFFFFu, v.w[i], src);
     return r;
 }
 // inclusive prefix product P and inclusive suffix product Q of t over the 32 lanes of a warp
 template <class F>
-__device__ __forceinline__ void warp_scan_products(const F& f, const fe& t, int lane, int width,
-                                                   fe* P, fe* Q) {
+__device__ __forceinline__ void warp_scan_products(const F& f, const fel<F>& t, int lane, int width,
+                                                   fel<F>* P, fel<F>* Q) {
+    using fe = fel<F>;
     *P = t;
     *Q = t;
 #pragma unroll 1
@@ -73,9 +83,12 @@ __device__ __forceinline__ void warp_scan_products(const F& f, const fe& t, int 
     }
 }
 // t != 0 on every thread of the block (all COOP_THREADS threads must call).  Returns t^-1.
-// sm: 2 * (COOP_THREADS / 32) field elements of shared memory, word-major.
+// sm: 2 * (COOP_THREADS / 32) field elements (2 * F::N * COOP_THREADS / 32 words) of shared
+// memory, word-major.
 template <class F, int COOP_THREADS>
-__device__ fe coop_block_inverse(const F& f, const fe& t, uint32_t* sm) {
+__device__ fel<F> coop_block_inverse(const F& f, const fel<F>& t, uint32_t* sm) {
+    using fe = fel<F>;
+    constexpr int NL = F::N;
     constexpr int NW = COOP_THREADS / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const fe one = fe_one(f);
@@ -86,45 +99,47 @@ __device__ fe coop_block_inverse(const F& f, const fe& t, uint32_t* sm) {
     if constexpr (NW == 1) {  // a block of one warp: the warp total is inverted directly
         fe total;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) total.w[i] = __shfl_sync(0xFFFFFFFFu, P.w[i], 31);
+        for (int i = 0; i < NL; ++i) total.w[i] = __shfl_sync(0xFFFFFFFFu, P.w[i], 31);
         return fe_mul(f, fe_mul(f, fe_inv(f, total), E), S);
     }
     if (lane == 31) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) sm[i * NW + warp] = P.w[i];
+        for (int i = 0; i < NL; ++i) sm[i * NW + warp] = P.w[i];
     }
     __syncthreads();
     if (warp == 0) {
         fe w = one;
         if (lane < NW) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) w.w[i] = sm[i * NW + lane];
+            for (int i = 0; i < NL; ++i) w.w[i] = sm[i * NW + lane];
         }
         fe PP, QQ;
         warp_scan_products(f, w, lane, NW, &PP, &QQ);  // lanes >= NW hold one
         fe total;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) total.w[i] = __shfl_sync(0xFFFFFFFFu, PP.w[i], NW - 1);
+        for (int i = 0; i < NL; ++i) total.w[i] = __shfl_sync(0xFFFFFFFFu, PP.w[i], NW - 1);
         const fe inv = fe_inv(f, total);  // the block's single inversion
         fe EE = fe_select(lane == 0, one, fe_shfl_up(PP, 1));
         fe SS = fe_select(lane == 31, one, fe_shfl_down(QQ, 1));
         fe wi = fe_mul(f, fe_mul(f, inv, EE), SS);
         if (lane < NW) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) sm[(8 + i) * NW + lane] = wi.w[i];
+            for (int i = 0; i < NL; ++i) sm[(NL + i) * NW + lane] = wi.w[i];
         }
     }
     __syncthreads();
     fe wi;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) wi.w[i] = sm[(8 + i) * NW + warp];
+    for (int i = 0; i < NL; ++i) wi.w[i] = sm[(NL + i) * NW + warp];
     return fe_mul(f, fe_mul(f, wi, E), S);
 }
 
 // product of every other thread's t in the block (returned) and the block total (*total, valid
-// on thread 0 only).  sm: 16 * (THREADS / 32) words.
+// on thread 0 only).  sm: 2 * F::N * (THREADS / 32) words.
 template <class F, int THREADS>
-__device__ fe block_others_product(const F& f, const fe& t, uint32_t* sm, fe* total) {
+__device__ fel<F> block_others_product(const F& f, const fel<F>& t, uint32_t* sm, fel<F>* total) {
+    using fe = fel<F>;
+    constexpr int NL = F::N;
     constexpr int NW = THREADS / 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const fe one = fe_one(f);
@@ -134,14 +149,14 @@ __device__ fe block_others_product(const F& f, const fe& t, uint32_t* sm, fe* to
     fe S = fe_select(lane == 31, one, fe_shfl_down(Q, 1));
     if (lane == 31) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) sm[i * NW + warp] = P.w[i];
+        for (int i = 0; i < NL; ++i) sm[i * NW + warp] = P.w[i];
     }
     __syncthreads();
     if (warp == 0) {
         fe w = one;
         if (lane < NW) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) w.w[i] = sm[i * NW + lane];
+            for (int i = 0; i < NL; ++i) w.w[i] = sm[i * NW + lane];
         }
         fe PP, QQ;
         warp_scan_products(f, w, lane, NW, &PP, &QQ);
@@ -150,14 +165,14 @@ __device__ fe block_others_product(const F& f, const fe& t, uint32_t* sm, fe* to
         fe ab = fe_mul(f, EE, SS);  // product of the other warps' totals
         if (lane < NW) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i) sm[(8 + i) * NW + lane] = ab.w[i];
+            for (int i = 0; i < NL; ++i) sm[(NL + i) * NW + lane] = ab.w[i];
         }
         if (lane == 0) *total = QQ;  // lane 0's inclusive suffix = all warps
     }
     __syncthreads();
     fe ab;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) ab.w[i] = sm[(8 + i) * NW + warp];
+    for (int i = 0; i < NL; ++i) ab.w[i] = sm[(NL + i) * NW + warp];
     return fe_mul(f, fe_mul(f, ab, E), S);
 }
 

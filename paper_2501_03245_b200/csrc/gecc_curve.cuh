@@ -19,47 +19,57 @@
 
 namespace gecc {
 
-struct jac {
-    fe X, Y, Z;  // Z == 0 <=> point at infinity
+template <int N>
+struct jacN {
+    feN<N> X, Y, Z;  // Z == 0 <=> point at infinity
 };
-struct aff {
-    fe x, y;
+template <int N>
+struct affN {
+    feN<N> x, y;
 };
+using jac = jacN<8>;
+using aff = affN<8>;
+template <class C>
+using cfe = feN<C::Fp::N>;   // coordinate type of curve C
+template <class C>
+using cjac = jacN<C::Fp::N>;
+template <class C>
+using caff = affN<C::Fp::N>;
 
 template <class C>
-GECC_HD jac jac_infinity() {
-    jac r;
+GECC_HD cjac<C> jac_infinity() {
+    cjac<C> r;
     r.X = fe_one(typename C::Fp{});
     r.Y = r.X;
-    r.Z = fe_zero();
+    r.Z = fe_zero_n<C::Fp::N>();
     return r;
 }
 // Z == 0 (mod q).  Infinity is always *written* as the exact zero, but a weakly reduced
 // field may also hold q itself, so the test is the field's own.
 template <class C>
-GECC_HD bool jac_is_inf(const jac& p) {
+GECC_HD bool jac_is_inf(const cjac<C>& p) {
     return fe_is_zero(typename C::Fp{}, p.Z);
 }
 
 template <class C>
-GECC_HD fe curve_a() {
-    fe r;
+GECC_HD cfe<C> curve_a() {
+    cfe<C> r;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r.w[i] = C::a(i);
+    for (int i = 0; i < C::Fp::N; ++i) r.w[i] = C::a(i);
     return r;
 }
 template <class C>
-GECC_HD fe curve_b() {
-    fe r;
+GECC_HD cfe<C> curve_b() {
+    cfe<C> r;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r.w[i] = C::b(i);
+    for (int i = 0; i < C::Fp::N; ++i) r.w[i] = C::b(i);
     return r;
 }
 template <class C>
-GECC_HD aff curve_g() {
-    aff g;
+GECC_HD caff<C> curve_g() {
+    caff<C> g;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < C::Fp::N; ++i) {
         g.x.w[i] = C::gx(i);
         g.y.w[i] = C::gy(i);
     }
@@ -68,7 +78,8 @@ GECC_HD aff curve_g() {
 
 // y^2 == x^3 + a x + b (curve.cpp:62-70)
 template <class C>
-GECC_HD bool aff_on_curve(const aff& p) {
+GECC_HD bool aff_on_curve(const caff<C>& p) {
+    using fe = cfe<C>;
     const typename C::Fp f{};
     fe lhs = fe_sqr(f, p.y);
     fe rhs = fe_mul(f, fe_sqr(f, p.x), p.x);
@@ -83,9 +94,10 @@ GECC_HD bool aff_on_curve(const aff& p) {
 }
 
 template <class C>
-GECC_HD_CALL jac jac_dbl(const jac& p) {
+GECC_HD_CALL cjac<C> jac_dbl(const cjac<C>& p) {
+    using fe = cfe<C>;
     const typename C::Fp f{};
-    jac r;
+    cjac<C> r;
     if (C::a_kind == A_ZERO) {
         fe A = fe_sqr(f, p.X);
         fe B = fe_sqr(f, p.Y);
@@ -132,7 +144,9 @@ GECC_HD_CALL jac jac_dbl(const jac& p) {
 // p + (x2, y2), (x2, y2) finite.  Handles p = infinity, p = q (doubling) and
 // p = -q (infinity) -- curve.cpp:129-167 with t.Z == 1.
 template <class C>
-GECC_HD_CALL jac jac_madd(const jac& p, const aff& q) {
+GECC_HD_CALL cjac<C> jac_madd(const cjac<C>& p, const caff<C>& q) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
     const typename C::Fp f{};
     if (jac_is_inf<C>(p)) {
         jac r;
@@ -162,7 +176,9 @@ GECC_HD_CALL jac jac_madd(const jac& p, const aff& q) {
 
 // complete Jacobian + Jacobian (curve.cpp:142-166)
 template <class C>
-GECC_HD_CALL jac jac_add(const jac& p, const jac& q) {
+GECC_HD_CALL cjac<C> jac_add(const cjac<C>& p, const cjac<C>& q) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
     const typename C::Fp f{};
     if (jac_is_inf<C>(p)) return q;
     if (jac_is_inf<C>(q)) return p;
@@ -190,7 +206,9 @@ GECC_HD_CALL jac jac_add(const jac& p, const jac& q) {
 
 // (X/Z^2, Y/Z^3) given zinv = Z^-1 (curve.cpp:169-174)
 template <class C>
-GECC_HD aff jac_to_aff_with(const jac& p, const fe& zinv) {
+GECC_HD caff<C> jac_to_aff_with(const cjac<C>& p, const cfe<C>& zinv) {
+    using fe = cfe<C>;
+    using aff = caff<C>;
     const typename C::Fp f{};
     fe zi2 = fe_sqr(f, zinv);
     aff r;
@@ -200,8 +218,8 @@ GECC_HD aff jac_to_aff_with(const jac& p, const fe& zinv) {
 }
 
 template <class C>
-GECC_HD aff aff_neg(const aff& p) {
-    aff r;
+GECC_HD caff<C> aff_neg(const caff<C>& p) {
+    caff<C> r;
     r.x = p.x;
     r.y = fe_neg(typename C::Fp{}, p.y);
     return r;

@@ -7,15 +7,17 @@
 namespace gecc {
 
 // limb k of element i at cols[k*n + i]: a warp reads 32 consecutive words per limb.
-GECC_HD fe col_load(const uint32_t* __restrict__ cols, size_t n, size_t i) {
-    fe v;
+template <int N = 8>
+GECC_HD feN<N> col_load(const uint32_t* __restrict__ cols, size_t n, size_t i) {
+    feN<N> v;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v.w[k] = cols[(size_t)k * n + i];
+    for (int k = 0; k < N; ++k) v.w[k] = cols[(size_t)k * n + i];
     return v;
 }
-GECC_HD void col_store(uint32_t* __restrict__ cols, size_t n, size_t i, const fe& v) {
+template <int N>
+GECC_HD void col_store(uint32_t* __restrict__ cols, size_t n, size_t i, const feN<N>& v) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) cols[(size_t)k * n + i] = v.w[k];
+    for (int k = 0; k < N; ++k) cols[(size_t)k * n + i] = v.w[k];
 }
 
 // 32 big-endian bytes -> limbs (limbs.cpp:5-14).  p need not be aligned.

@@ -23,9 +23,15 @@
 
 namespace gecc {
 
-struct fe {
-    uint32_t w[8];
+// N x 32-bit limbs, least significant first.  fe (8 limbs) is the 256-bit element every
+// reference-facing kernel uses; 12 limbs carry the 381-bit base field of BLS12-381.
+template <int N>
+struct feN {
+    uint32_t w[N];
 };
+using fe = feN<8>;
+template <class F>
+using fel = feN<F::N>;  // element type of field F
 
 struct FieldRT {
     static constexpr int N = 8;
@@ -43,53 +49,59 @@ struct FieldRT {
 };
 
 // ---------------------------------------------------------------- basics
-GECC_HD fe fe_zero() {
-    fe r;
+template <int N>
+GECC_HD feN<N> fe_zero_n() {
+    feN<N> r;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r.w[i] = 0;
+    for (int i = 0; i < N; ++i) r.w[i] = 0;
+    return r;
+}
+GECC_HD fe fe_zero() { return fe_zero_n<8>(); }
+template <class F>
+GECC_HD fel<F> fe_one(const F& f) {  // Montgomery one = R mod q
+    fel<F> r;
+#pragma unroll
+    for (int i = 0; i < F::N; ++i) r.w[i] = f.r(i);
     return r;
 }
 template <class F>
-GECC_HD fe fe_one(const F& f) {  // Montgomery one = R mod q
-    fe r;
+GECC_HD fel<F> fe_modulus(const F& f) {
+    fel<F> r;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r.w[i] = f.r(i);
+    for (int i = 0; i < F::N; ++i) r.w[i] = f.q(i);
     return r;
 }
-template <class F>
-GECC_HD fe fe_modulus(const F& f) {
-    fe r;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) r.w[i] = f.q(i);
-    return r;
-}
-GECC_HD bool fe_is_zero(const fe& a) {
+template <int N>
+GECC_HD bool fe_is_zero(const feN<N>& a) {
     uint32_t acc = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc |= a.w[i];
+    for (int i = 0; i < N; ++i) acc |= a.w[i];
     return acc == 0;
 }
-GECC_HD bool fe_eq(const fe& a, const fe& b) {
+template <int N>
+GECC_HD bool fe_eq(const feN<N>& a, const feN<N>& b) {
     uint32_t acc = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) acc |= a.w[i] ^ b.w[i];
+    for (int i = 0; i < N; ++i) acc |= a.w[i] ^ b.w[i];
     return acc == 0;
 }
-GECC_HD fe fe_select(bool c, const fe& a, const fe& b) {  // c ? a : b
-    fe r;
+template <int N>
+GECC_HD feN<N> fe_select(bool c, const feN<N>& a, const feN<N>& b) {  // c ? a : b
+    feN<N> r;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r.w[i] = c ? a.w[i] : b.w[i];
+    for (int i = 0; i < N; ++i) r.w[i] = c ? a.w[i] : b.w[i];
     return r;
 }
-// a < b as 256-bit integers (limbs.hpp:115-122)
-GECC_HD bool u256_lt(const fe& a, const fe& b) {
+// a < b as unsigned integers (limbs.hpp:115-122)
+template <int N>
+GECC_HD bool u256_lt(const feN<N>& a, const feN<N>& b) {
     sub_cc(a.w[0], b.w[0]);
 #pragma unroll
-    for (int i = 1; i < 8; ++i) subc_cc(a.w[i], b.w[i]);
+    for (int i = 1; i < N; ++i) subc_cc(a.w[i], b.w[i]);
     return subc(0, 0) != 0;
 }
 template <class F>
-GECC_HD bool fe_lt_modulus(const F& f, const fe& a) {
+GECC_HD bool fe_lt_modulus(const F& f, const fel<F>& a) {
     return u256_lt(a, fe_modulus(f));
 }
 
@@ -217,51 +229,53 @@ GECC_HD fe redc_secp_lazy(const uint32_t* t) {
 
 // field-aware predicates: canonical fields compare limbs, the lazy field compares mod q
 template <class F>
-GECC_HD bool fe_is_zero(const F& f, const fe& a) {
+GECC_HD bool fe_is_zero(const F& f, const fel<F>& a) {
     if constexpr (F::kind == KIND_SECP_LAZY) return lazy_is_zero(f, a);
     else return fe_is_zero(a);
 }
 
 // ---------------------------------------------------------------- add / sub
 template <class F>
-GECC_HD fe fe_add(const F& f, const fe& a, const fe& b) {
+GECC_HD fel<F> fe_add(const F& f, const fel<F>& a, const fel<F>& b) {
     if constexpr (F::kind == KIND_SECP_LAZY) return lazy_add(a, b);
-    fe s, d;
+    constexpr int N = F::N;
+    fel<F> s, d;
     s.w[0] = add_cc(a.w[0], b.w[0]);
 #pragma unroll
-    for (int i = 1; i < 8; ++i) s.w[i] = addc_cc(a.w[i], b.w[i]);
+    for (int i = 1; i < N; ++i) s.w[i] = addc_cc(a.w[i], b.w[i]);
     uint32_t top = addc(0, 0);
     d.w[0] = sub_cc(s.w[0], f.q(0));
 #pragma unroll
-    for (int i = 1; i < 8; ++i) d.w[i] = subc_cc(s.w[i], f.q(i));
+    for (int i = 1; i < N; ++i) d.w[i] = subc_cc(s.w[i], f.q(i));
     uint32_t borrow = subc(0, 0);  // 0xFFFFFFFF when s < q
-    // s >= q  <=>  carried out of 2^256, or no borrow
+    // s >= q  <=>  carried out of 2^(32N), or no borrow
     return fe_select(top != 0 || borrow == 0, d, s);
 }
 template <class F>
-GECC_HD fe fe_sub(const F& f, const fe& a, const fe& b) {
+GECC_HD fel<F> fe_sub(const F& f, const fel<F>& a, const fel<F>& b) {
     if constexpr (F::kind == KIND_SECP_LAZY) return lazy_sub(a, b);
-    fe d, e;
+    constexpr int N = F::N;
+    fel<F> d, e;
     d.w[0] = sub_cc(a.w[0], b.w[0]);
 #pragma unroll
-    for (int i = 1; i < 8; ++i) d.w[i] = subc_cc(a.w[i], b.w[i]);
+    for (int i = 1; i < N; ++i) d.w[i] = subc_cc(a.w[i], b.w[i]);
     uint32_t borrow = subc(0, 0);
     e.w[0] = add_cc(d.w[0], f.q(0));
 #pragma unroll
-    for (int i = 1; i < 8; ++i) e.w[i] = addc_cc(d.w[i], f.q(i));
+    for (int i = 1; i < N; ++i) e.w[i] = addc_cc(d.w[i], f.q(i));
     return fe_select(borrow != 0, e, d);
 }
 template <class F>
-GECC_HD bool fe_eq(const F& f, const fe& a, const fe& b) {
+GECC_HD bool fe_eq(const F& f, const fel<F>& a, const fel<F>& b) {
     if constexpr (F::kind == KIND_SECP_LAZY) return lazy_is_zero(f, lazy_sub(a, b));
     else return fe_eq(a, b);
 }
 template <class F>
-GECC_HD fe fe_neg(const F& f, const fe& a) {
-    return fe_sub(f, fe_zero(), a);
+GECC_HD fel<F> fe_neg(const F& f, const fel<F>& a) {
+    return fe_sub(f, fe_zero_n<F::N>(), a);
 }
 template <class F>
-GECC_HD fe fe_dbl(const F& f, const fe& a) {
+GECC_HD fel<F> fe_dbl(const F& f, const fel<F>& a) {
     return fe_add(f, a, a);
 }
 
@@ -270,8 +284,9 @@ GECC_HD fe fe_dbl(const F& f, const fe& a) {
 // accumulated in e[], odd ones in o[] (o is one limb to the left), so that every
 // lo/hi pair sits on an aligned register pair and each row is two carry chains of
 // IMAD.WIDE.U32(.X).  64 wide multiply-adds + 8 carry folds + 15 merge adds.
-GECC_HD void mul_wide8(uint32_t* t, const uint32_t* a, const uint32_t* b) {
-    constexpr int N = 8;
+template <int N>
+GECC_HD void mul_wide_n(uint32_t* t, const uint32_t* a, const uint32_t* b) {
+    static_assert(N % 2 == 0, "even/odd layout needs an even limb count");
     uint32_t e[2 * N], o[2 * N];
 #pragma unroll
     for (int k = 0; k < 2 * N; ++k) e[k] = o[k] = 0;
@@ -318,9 +333,11 @@ GECC_HD void mul_wide8(uint32_t* t, const uint32_t* a, const uint32_t* b) {
     for (int k = 2; k < 2 * N; ++k) t[k] = addc_cc(e[k], o[k - 1]);
 }
 
-// Low 8 limbs of a*b (used only by the generic REDC).
-GECC_HD void mul_low8(uint32_t* r, const uint32_t* a, const uint32_t* b) {
-    constexpr int N = 8;
+GECC_HD void mul_wide8(uint32_t* t, const uint32_t* a, const uint32_t* b) { mul_wide_n<8>(t, a, b); }
+
+// Low N limbs of a*b (used only by the generic REDC).
+template <int N>
+GECC_HD void mul_low_n(uint32_t* r, const uint32_t* a, const uint32_t* b) {
 #pragma unroll
     for (int k = 0; k < N; ++k) r[k] = 0;
 #pragma unroll
@@ -337,11 +354,13 @@ GECC_HD void mul_low8(uint32_t* r, const uint32_t* a, const uint32_t* b) {
     }
 }
 
-// Full 16-limb square: the 28 off-diagonal products once (same even/odd carry-chain
+GECC_HD void mul_low8(uint32_t* r, const uint32_t* a, const uint32_t* b) { mul_low_n<8>(r, a, b); }
+
+// Full 2N-limb square: the N(N-1)/2 off-diagonal products once (same even/odd carry-chain
 // layout as mul_wide8), doubled by a one-bit funnel shift, plus the 8 diagonal
 // squares in one chain: 36 wide multiply-adds instead of 64.
-GECC_HD void sqr_wide8(uint32_t* t, const uint32_t* a) {
-    constexpr int N = 8;
+template <int N>
+GECC_HD void sqr_wide_n(uint32_t* t, const uint32_t* a) {
     uint32_t e[2 * N], o[2 * N];
 #pragma unroll
     for (int k = 0; k < 2 * N; ++k) e[k] = o[k] = 0;
@@ -394,14 +413,16 @@ GECC_HD void sqr_wide8(uint32_t* t, const uint32_t* a) {
     }
 }
 
+GECC_HD void sqr_wide8(uint32_t* t, const uint32_t* a) { sqr_wide_n<8>(t, a); }
+
 // ---------------------------------------------------------------- reductions
 // r = (top:r) - q if (top:r) >= q
 template <class F>
-GECC_HD fe final_sub(const F& f, const fe& r, uint32_t top) {
-    fe d;
+GECC_HD fel<F> final_sub(const F& f, const fel<F>& r, uint32_t top) {
+    fel<F> d;
     d.w[0] = sub_cc(r.w[0], f.q(0));
 #pragma unroll
-    for (int i = 1; i < 8; ++i) d.w[i] = subc_cc(r.w[i], f.q(i));
+    for (int i = 1; i < F::N; ++i) d.w[i] = subc_cc(r.w[i], f.q(i));
     uint32_t borrow = subc(0, 0);
     return fe_select(top != 0 || borrow == 0, d, r);
 }
@@ -411,23 +432,24 @@ GECC_HD fe final_sub(const F& f, const fe& r, uint32_t top) {
 // subtraction.  Two more products instead of a word-serial sweep: no dependent
 // chain of 8 multiplier words.
 template <class F>
-GECC_HD fe redc_generic(const F& f, const uint32_t* t) {
-    uint32_t ninv[8], q[8], m[8], u[16];
+GECC_HD fel<F> redc_generic(const F& f, const uint32_t* t) {
+    constexpr int N = F::N;
+    uint32_t ninv[N], q[N], m[N], u[2 * N];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < N; ++i) {
         ninv[i] = f.ninv(i);
         q[i] = f.q(i);
     }
-    mul_low8(m, t, ninv);
-    mul_wide8(u, m, q);
-    // t_lo + u_lo == 0 mod 2^256: it carries exactly when t_lo != 0
+    mul_low_n<N>(m, t, ninv);
+    mul_wide_n<N>(u, m, q);
+    // t_lo + u_lo == 0 mod 2^(32N): it carries exactly when t_lo != 0
     uint32_t nz = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) nz |= t[i];
+    for (int i = 0; i < N; ++i) nz |= t[i];
     add_cc(nz != 0 ? 1u : 0u, 0xFFFFFFFFu);
-    fe r;
+    fel<F> r;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r.w[i] = addc_cc(t[8 + i], u[8 + i]);
+    for (int i = 0; i < N; ++i) r.w[i] = addc_cc(t[N + i], u[N + i]);
     uint32_t top = addc(0, 0);
     return final_sub(f, r, top);
 }
@@ -514,7 +536,7 @@ GECC_HD fe redc_sm2(const F& f, const uint32_t* tin) {
 }
 
 template <class F>
-GECC_HD fe redc(const F& f, const uint32_t* t) {
+GECC_HD fel<F> redc(const F& f, const uint32_t* t) {
     if constexpr (F::kind == KIND_SECP_P) return redc_secp(f, t);
     else if constexpr (F::kind == KIND_SECP_LAZY) return redc_secp_lazy(t);
     else if constexpr (F::kind == KIND_SM2_P) return redc_sm2(f, t);
@@ -538,17 +560,17 @@ inline OpCounters& op_counters() {
 #endif
 
 template <class F>
-GECC_HD fe fe_mul_inl(const F& f, const fe& a, const fe& b) {
+GECC_HD fel<F> fe_mul_inl(const F& f, const fel<F>& a, const fel<F>& b) {
     GECC_COUNT(mul, F);
-    uint32_t t[16];
-    mul_wide8(t, a.w, b.w);
+    uint32_t t[2 * F::N];
+    mul_wide_n<F::N>(t, a.w, b.w);
     return redc(f, t);
 }
 template <class F>
-GECC_HD fe fe_sqr_inl(const F& f, const fe& a) {
+GECC_HD fel<F> fe_sqr_inl(const F& f, const fel<F>& a) {
     GECC_COUNT(sqr, F);
-    uint32_t t[16];
-    sqr_wide8(t, a.w);
+    uint32_t t[2 * F::N];
+    sqr_wide_n<F::N>(t, a.w);
     return redc(f, t);
 }
 // On the device the two products are real functions with by-value arguments: the
@@ -558,49 +580,49 @@ GECC_HD fe fe_sqr_inl(const F& f, const fe& a) {
 // top stall of k_verify was no_instruction).  Runtime fields stay inline.
 #if defined(__CUDA_ARCH__) && !defined(GECC_INLINE_FIELD)
 template <class F>
-__device__ __noinline__ fe fe_mul_call(fe a, fe b) {
+__device__ __noinline__ fel<F> fe_mul_call(fel<F> a, fel<F> b) {
     return fe_mul_inl(F{}, a, b);
 }
 template <class F>
-__device__ __noinline__ fe fe_sqr_call(fe a) {
+__device__ __noinline__ fel<F> fe_sqr_call(fel<F> a) {
     return fe_sqr_inl(F{}, a);
 }
 template <class F>
-GECC_HD fe fe_mul(const F& f, const fe& a, const fe& b) {
+GECC_HD fel<F> fe_mul(const F& f, const fel<F>& a, const fel<F>& b) {
     if constexpr (std::is_empty<F>::value) return fe_mul_call<F>(a, b);
     else return fe_mul_inl(f, a, b);
 }
 template <class F>
-GECC_HD fe fe_sqr(const F& f, const fe& a) {
+GECC_HD fel<F> fe_sqr(const F& f, const fel<F>& a) {
     if constexpr (std::is_empty<F>::value) return fe_sqr_call<F>(a);
     else return fe_sqr_inl(f, a);
 }
 #else
 template <class F>
-GECC_HD fe fe_mul(const F& f, const fe& a, const fe& b) {
+GECC_HD fel<F> fe_mul(const F& f, const fel<F>& a, const fel<F>& b) {
     return fe_mul_inl(f, a, b);
 }
 template <class F>
-GECC_HD fe fe_sqr(const F& f, const fe& a) {
+GECC_HD fel<F> fe_sqr(const F& f, const fel<F>& a) {
     return fe_sqr_inl(f, a);
 }
 #endif
 template <class F>
-GECC_HD fe fe_to_mont(const F& f, const fe& a) {  // a * R
+GECC_HD fel<F> fe_to_mont(const F& f, const fel<F>& a) {  // a * R
     if constexpr (F::kind == KIND_SECP_LAZY) return a;  // plain representation: R = 1
-    fe r2;
+    fel<F> r2;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r2.w[i] = f.r2(i);
+    for (int i = 0; i < F::N; ++i) r2.w[i] = f.r2(i);
     return fe_mul(f, a, r2);
 }
 template <class F>
-GECC_HD fe fe_from_mont(const F& f, const fe& a) {  // a * R^-1
+GECC_HD fel<F> fe_from_mont(const F& f, const fel<F>& a) {  // a * R^-1
     if constexpr (F::kind == KIND_SECP_LAZY) return lazy_canon(f, a);  // leaves the field layer: canonical
-    uint32_t t[16];
+    uint32_t t[2 * F::N];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < F::N; ++i) {
         t[i] = a.w[i];
-        t[8 + i] = 0;
+        t[F::N + i] = 0;
     }
     return redc(f, t);
 }
@@ -608,15 +630,15 @@ GECC_HD fe fe_from_mont(const F& f, const fe& a) {  // a * R^-1
 // a^(q-2) in Montgomery form, 4-bit fixed window: 256 squarings + 64 + 14 products.
 // Not unrolled on purpose (code size).  Zero maps to zero.
 template <class F>
-GECC_HD_CALL fe fe_inv_fermat(const F& f, const fe& a) {
-    fe tab[16];
+GECC_HD_CALL fel<F> fe_inv_fermat(const F& f, const fel<F>& a) {
+    fel<F> tab[16];
     tab[0] = fe_one(f);
     tab[1] = a;
 #pragma unroll 1
     for (int i = 2; i < 16; ++i) tab[i] = fe_mul(f, tab[i - 1], a);
-    fe r = fe_one(f);
+    fel<F> r = fe_one(f);
 #pragma unroll 1
-    for (int k = 63; k >= 0; --k) {
+    for (int k = 8 * F::N - 1; k >= 0; --k) {
         r = fe_sqr(f, r);
         r = fe_sqr(f, r);
         r = fe_sqr(f, r);

@@ -11,7 +11,8 @@
 
 namespace gecc {
 
-enum { CURVE_SM2 = 0, CURVE_SECP = 1 };
+enum { CURVE_SM2 = 0, CURVE_SECP = 1, CURVE_BLS381 = 2 };  // BLS12-381 G1: 12-limb coordinates
+inline int curve_limbs(int curve) { return curve == CURVE_BLS381 ? 12 : 8; }
 
 cudaError_t launch_field_op(int curve, int field, int op, size_t n, const uint32_t* a,
                             const uint32_t* b, uint32_t* out, cudaStream_t s);
@@ -71,7 +72,7 @@ cudaError_t launch_pmul_serial(int curve, size_t n, const uint32_t* k, const uin
                                uint8_t* oinf, cudaStream_t s);
 
 // MSM: scratch must hold msm_scratch_bytes(n) bytes of device memory
-size_t msm_scratch_bytes(size_t n);
+size_t msm_scratch_bytes(size_t n, int curve);
 void set_msm_form(int form);  // 0 default (batch-affine), 1 mixed-Jacobian slices, 2 batch-affine tree
 cudaError_t launch_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px,
                        const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,

@@ -18,37 +18,40 @@
 
 namespace gecc {
 
-struct s30 {
-    int32_t v[9];  // value = sum v[i] 2^(30 i); limbs in (-2^30, 2^30) except v[8]
+template <int L>
+struct s30n {
+    int32_t v[L];  // value = sum v[i] 2^(30 i); limbs in (-2^30, 2^30) except the top one
 };
+using s30 = s30n<9>;  // 256-bit fields; the 381-bit field uses 13 limbs
 struct trans2x2 {
     int32_t u, v, q, r;
 };
 
-GECC_HD s30 s30_from_u256(const uint32_t* w) {
-    s30 r;
+// N 32-bit limbs -> L 30-bit limbs (the shifts are compile-time constants after unrolling)
+template <int N, int L>
+GECC_HD s30n<L> s30_from_limbs(const uint32_t* w) {
+    s30n<L> r;
     const uint32_t M30 = 0x3FFFFFFFu;
-    r.v[0] = (int32_t)(w[0] & M30);
-    r.v[1] = (int32_t)(((w[0] >> 30) | (w[1] << 2)) & M30);
-    r.v[2] = (int32_t)(((w[1] >> 28) | (w[2] << 4)) & M30);
-    r.v[3] = (int32_t)(((w[2] >> 26) | (w[3] << 6)) & M30);
-    r.v[4] = (int32_t)(((w[3] >> 24) | (w[4] << 8)) & M30);
-    r.v[5] = (int32_t)(((w[4] >> 22) | (w[5] << 10)) & M30);
-    r.v[6] = (int32_t)(((w[5] >> 20) | (w[6] << 12)) & M30);
-    r.v[7] = (int32_t)(((w[6] >> 18) | (w[7] << 14)) & M30);
-    r.v[8] = (int32_t)(w[7] >> 16);
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        const int bit = 30 * i, wi = bit >> 5, sh = bit & 31;
+        uint32_t v = w[wi] >> sh;
+        if (sh > 2 && wi + 1 < N) v |= w[wi + 1] << (32 - sh);
+        r.v[i] = (int32_t)(v & M30);
+    }
     return r;
 }
-GECC_HD void s30_to_u256(uint32_t* w, const s30& a) {  // a normalised: limbs in [0, 2^30)
+template <int N, int L>
+GECC_HD void s30_to_limbs(uint32_t* w, const s30n<L>& a) {  // a normalised: limbs in [0, 2^30)
     const uint32_t* v = reinterpret_cast<const uint32_t*>(a.v);
-    w[0] = v[0] | (v[1] << 30);
-    w[1] = (v[1] >> 2) | (v[2] << 28);
-    w[2] = (v[2] >> 4) | (v[3] << 26);
-    w[3] = (v[3] >> 6) | (v[4] << 24);
-    w[4] = (v[4] >> 8) | (v[5] << 22);
-    w[5] = (v[5] >> 10) | (v[6] << 20);
-    w[6] = (v[6] >> 12) | (v[7] << 18);
-    w[7] = (v[7] >> 14) | (v[8] << 16);
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+        const int bit = 32 * k, li = bit / 30, off = bit % 30;
+        uint32_t x = v[li] >> off;
+        if (li + 1 < L) x |= v[li + 1] << (30 - off);
+        if (60 - off < 32 && li + 2 < L) x |= v[li + 2] << (60 - off);
+        w[k] = x;
+    }
 }
 
 // 30 division steps on the low limbs; zeta = -(delta + 1/2).  Returns the new zeta
@@ -83,7 +86,8 @@ GECC_HD int32_t divsteps_30(int32_t zeta, uint32_t f0, uint32_t g0, trans2x2* t)
 }
 
 // (f, g) <- t * (f, g) / 2^30 (exact)
-GECC_HD void update_fg_30(s30* f, s30* g, const trans2x2& t) {
+template <int L>
+GECC_HD void update_fg_30(s30n<L>* f, s30n<L>* g, const trans2x2& t) {
     const int32_t M30 = 0x3FFFFFFF;
     const int64_t u = t.u, v = t.v, q = t.q, r = t.r;
     int64_t cf = u * f->v[0] + v * g->v[0];
@@ -91,7 +95,7 @@ GECC_HD void update_fg_30(s30* f, s30* g, const trans2x2& t) {
     cf >>= 30;
     cg >>= 30;
 #pragma unroll
-    for (int i = 1; i < 9; ++i) {
+    for (int i = 1; i < L; ++i) {
         const int32_t fi = f->v[i], gi = g->v[i];
         cf += u * fi + v * gi;
         cg += q * fi + r * gi;
@@ -100,17 +104,17 @@ GECC_HD void update_fg_30(s30* f, s30* g, const trans2x2& t) {
         g->v[i - 1] = (int32_t)cg & M30;
         cg >>= 30;
     }
-    f->v[8] = (int32_t)cf;
-    g->v[8] = (int32_t)cg;
+    f->v[L - 1] = (int32_t)cf;
+    g->v[L - 1] = (int32_t)cg;
 }
 
 // (d, e) <- t * (d, e) / 2^30 mod q: a multiple of q is added first so that the
 // low 30 bits vanish and the division is exact.  d, e stay in (-2q, q).
-template <class F>
-GECC_HD void update_de_30(const F& f, s30* d, s30* e, const trans2x2& t) {
+template <class F, int L>
+GECC_HD void update_de_30(const F& f, s30n<L>* d, s30n<L>* e, const trans2x2& t) {
     const int32_t M30 = 0x3FFFFFFF;
     const int64_t u = t.u, v = t.v, q = t.q, r = t.r;
-    const int32_t sd = d->v[8] >> 31, se = e->v[8] >> 31;
+    const int32_t sd = d->v[L - 1] >> 31, se = e->v[L - 1] >> 31;
     int32_t md = (t.u & sd) + (t.v & se);
     int32_t me = (t.q & sd) + (t.r & se);
     int64_t cd = u * d->v[0] + v * e->v[0];
@@ -122,7 +126,7 @@ GECC_HD void update_de_30(const F& f, s30* d, s30* e, const trans2x2& t) {
     cd >>= 30;
     ce >>= 30;
 #pragma unroll
-    for (int i = 1; i < 9; ++i) {
+    for (int i = 1; i < L; ++i) {
         const int32_t di = d->v[i], ei = e->v[i];
         cd += u * di + v * ei;
         ce += q * di + r * ei;
@@ -133,70 +137,73 @@ GECC_HD void update_de_30(const F& f, s30* d, s30* e, const trans2x2& t) {
         e->v[i - 1] = (int32_t)ce & M30;
         ce >>= 30;
     }
-    d->v[8] = (int32_t)cd;
-    e->v[8] = (int32_t)ce;
+    d->v[L - 1] = (int32_t)cd;
+    e->v[L - 1] = (int32_t)ce;
 }
 
 // r in (-2q, q) -> [0, q), negated first when sign < 0
-template <class F>
-GECC_HD void normalize_30(const F& f, s30* r, int32_t sign) {
+template <class F, int L>
+GECC_HD void normalize_30(const F& f, s30n<L>* r, int32_t sign) {
     const int32_t M30 = 0x3FFFFFFF;
-    int32_t cond_add = r->v[8] >> 31;
+    int32_t cond_add = r->v[L - 1] >> 31;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) r->v[i] += (int32_t)f.q30(i) & cond_add;
+    for (int i = 0; i < L; ++i) r->v[i] += (int32_t)f.q30(i) & cond_add;
     const int32_t cond_negate = sign >> 31;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) r->v[i] = (r->v[i] ^ cond_negate) - cond_negate;
+    for (int i = 0; i < L; ++i) r->v[i] = (r->v[i] ^ cond_negate) - cond_negate;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < L - 1; ++i) {
         r->v[i + 1] += r->v[i] >> 30;
         r->v[i] &= M30;
     }
-    cond_add = r->v[8] >> 31;
+    cond_add = r->v[L - 1] >> 31;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) r->v[i] += (int32_t)f.q30(i) & cond_add;
+    for (int i = 0; i < L; ++i) r->v[i] += (int32_t)f.q30(i) & cond_add;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < L - 1; ++i) {
         r->v[i + 1] += r->v[i] >> 30;
         r->v[i] &= M30;
     }
 }
 
-// x^-1 mod q, x a plain residue in [0, q); 0 -> 0.
+// x^-1 mod q, x a plain residue in [0, q); 0 -> 0.  Limb and round counts per field size
+// (half-delta divsteps: 590 suffice for 256-bit moduli, 879 for 381-bit ones; extra rounds
+// leave the result unchanged once g has reached zero).
 template <class F>
-GECC_HD_CALL fe safegcd_inverse(const F& fld, const fe& x) {
+GECC_HD_CALL fel<F> safegcd_inverse(const F& fld, const fel<F>& x) {
     GECC_COUNT(safegcd, F);
-    s30 d, e, f, g;
+    constexpr int N = F::N, L = N == 8 ? 9 : (32 * N + 29) / 30, ROUNDS = N == 8 ? 20 : (49 * N + 16) / 17 + 1;
+    s30n<L> d, e, f, g;
 #pragma unroll
-    for (int i = 0; i < 9; ++i) {
+    for (int i = 0; i < L; ++i) {
         d.v[i] = 0;
         e.v[i] = 0;
         f.v[i] = (int32_t)fld.q30(i);
     }
     e.v[0] = 1;
-    g = s30_from_u256(x.w);
+    g = s30_from_limbs<N, L>(x.w);
     int32_t zeta = -1;
 #pragma unroll 1
-    for (int round = 0; round < 20; ++round) {  // 600 divsteps >= 590 needed for 256 bits
+    for (int round = 0; round < ROUNDS; ++round) {
         trans2x2 t;
         zeta = divsteps_30(zeta, (uint32_t)f.v[0], (uint32_t)g.v[0], &t);
         update_de_30(fld, &d, &e, t);
         update_fg_30(&f, &g, t);
     }
     // g == 0 now and f == +-gcd == +-1 (or f == +-q when x == 0, where d == 0)
-    normalize_30(fld, &d, f.v[8]);
-    fe r;
-    s30_to_u256(r.w, d);
+    normalize_30(fld, &d, f.v[L - 1]);
+    fel<F> r;
+    s30_to_limbs<N, L>(r.w, d);
     return r;
 }
 
 // Montgomery-form inverse of a Montgomery-form element (zero -> zero).
 template <class F>
-GECC_HD fe fe_inv(const F& f, const fe& a) {
+GECC_HD fel<F> fe_inv(const F& f, const fel<F>& a) {
     if constexpr (F::kind == KIND_SECP_LAZY) return safegcd_inverse(f, lazy_canon(f, a));  // plain in, plain out
-    fe r3;
+    fel<F> r3;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) r3.w[i] = f.r3(i);
+    for (int i = 0; i < F::N; ++i) r3.w[i] = f.r3(i);
     return fe_mul(f, safegcd_inverse(f, a), r3);
 }
 

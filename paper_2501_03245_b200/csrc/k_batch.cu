@@ -170,7 +170,9 @@ constexpr int COOP_K = 4;
 template <class F, int COOP_THREADS>
 __global__ void __launch_bounds__(COOP_THREADS)
 k_batch_invert_coop(size_t n, const uint32_t* __restrict__ in, uint32_t* __restrict__ out) {
-    __shared__ uint32_t sm[16 * (COOP_THREADS / 32)];
+    using fe = fel<F>;
+    constexpr int NL = F::N;
+    __shared__ uint32_t sm[2 * NL * (COOP_THREADS / 32)];
     const F f{};
     const size_t tile = (size_t)blockIdx.x * (COOP_THREADS * COOP_K) + threadIdx.x;
     fe lp[COOP_K];
@@ -179,7 +181,7 @@ k_batch_invert_coop(size_t n, const uint32_t* __restrict__ in, uint32_t* __restr
     for (int k = 0; k < COOP_K; ++k) {
         const size_t i = tile + (size_t)k * COOP_THREADS;
         if (i < n) {
-            fe v = col_load(in, n, i);
+            fe v = col_load<NL>(in, n, i);
             if (!fe_is_zero(v)) acc = fe_mul(f, acc, v);
         }
         lp[k] = acc;
@@ -189,11 +191,11 @@ k_batch_invert_coop(size_t n, const uint32_t* __restrict__ in, uint32_t* __restr
     for (int k = COOP_K - 1; k >= 0; --k) {
         const size_t i = tile + (size_t)k * COOP_THREADS;
         if (i < n) {
-            fe v = col_load(in, n, i);
+            fe v = col_load<NL>(in, n, i);
             const bool zero = fe_is_zero(v);
             fe r = k > 0 ? fe_mul(f, inv, lp[k > 0 ? k - 1 : 0]) : inv;
             if (!zero && k > 0) inv = fe_mul(f, inv, v);
-            col_store(out, n, i, zero ? fe_zero() : r);
+            col_store(out, n, i, zero ? fe_zero_n<NL>() : r);
         }
     }
 }
@@ -204,7 +206,9 @@ k_batch_padd_coop(size_t n, const uint32_t* __restrict__ px, const uint32_t* __r
                   const uint8_t* __restrict__ pinf, const uint32_t* __restrict__ tx,
                   const uint32_t* __restrict__ ty, const uint8_t* __restrict__ tinf,
                   uint32_t* __restrict__ ox, uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf) {
-    __shared__ uint32_t sm[16 * (COOP_THREADS / 32)];
+    using fe = cfe<C>;
+    constexpr int NL = C::Fp::N;
+    __shared__ uint32_t sm[2 * NL * (COOP_THREADS / 32)];
     const typename C::Fp f{};
     const size_t tile = (size_t)blockIdx.x * (COOP_THREADS * COOP_K) + threadIdx.x;
     fe lp[COOP_K];
@@ -213,11 +217,11 @@ k_batch_padd_coop(size_t n, const uint32_t* __restrict__ px, const uint32_t* __r
     for (int k = 0; k < COOP_K; ++k) {
         const size_t i = tile + (size_t)k * COOP_THREADS;
         if (i < n) {
-            fe ax = col_load(px, n, i), bx = col_load(tx, n, i);
+            fe ax = col_load<NL>(px, n, i), bx = col_load<NL>(tx, n, i);
             const bool ai = pinf && pinf[i], bi = tinf && tinf[i];
             fe d = fe_one(f);
             if (!ai && !bi && fe_eq(ax, bx)) {
-                fe ay = col_load(py, n, i), by = col_load(ty, n, i);
+                fe ay = col_load<NL>(py, n, i), by = col_load<NL>(ty, n, i);
                 classify_pair<C>(ax, ay, ai, bx, by, bi, &d);
             } else if (!ai && !bi) {
                 d = fe_sub(f, ax, bx);
@@ -231,14 +235,14 @@ k_batch_padd_coop(size_t n, const uint32_t* __restrict__ px, const uint32_t* __r
     for (int k = COOP_K - 1; k >= 0; --k) {
         const size_t i = tile + (size_t)k * COOP_THREADS;
         if (i < n) {
-            fe ax = col_load(px, n, i), ay = col_load(py, n, i);
-            fe bx = col_load(tx, n, i), by = col_load(ty, n, i);
+            fe ax = col_load<NL>(px, n, i), ay = col_load<NL>(py, n, i);
+            fe bx = col_load<NL>(tx, n, i), by = col_load<NL>(ty, n, i);
             const bool ai = pinf && pinf[i], bi = tinf && tinf[i];
             fe d = fe_one(f);
             const uint32_t kind = classify_pair<C>(ax, ay, ai, bx, by, bi, &d);
             fe dinv = k > 0 ? fe_mul(f, inv, lp[k > 0 ? k - 1 : 0]) : inv;
             if (k > 0) inv = fe_mul(f, inv, d);
-            fe xr = fe_zero(), yr = fe_zero();
+            fe xr = fe_zero_n<NL>(), yr = fe_zero_n<NL>();
             uint8_t rinf = 0;
             if (kind == K_GENERIC) {
                 fe lam = fe_mul(f, fe_sub(f, ay, by), dinv);
@@ -265,7 +269,9 @@ __global__ void __launch_bounds__(COOP_THREADS)
 k_batch_pdbl_coop(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
                   const uint8_t* __restrict__ pinf, uint32_t* __restrict__ ox,
                   uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf) {
-    __shared__ uint32_t sm[16 * (COOP_THREADS / 32)];
+    using fe = cfe<C>;
+    constexpr int NL = C::Fp::N;
+    __shared__ uint32_t sm[2 * NL * (COOP_THREADS / 32)];
     const typename C::Fp f{};
     const size_t tile = (size_t)blockIdx.x * (COOP_THREADS * COOP_K) + threadIdx.x;
     fe lp[COOP_K];
@@ -274,7 +280,7 @@ k_batch_pdbl_coop(size_t n, const uint32_t* __restrict__ px, const uint32_t* __r
     for (int k = 0; k < COOP_K; ++k) {
         const size_t i = tile + (size_t)k * COOP_THREADS;
         if (i < n) {
-            fe ay = col_load(py, n, i);
+            fe ay = col_load<NL>(py, n, i);
             const bool degenerate = (pinf && pinf[i]) || fe_is_zero(ay);
             if (!degenerate) acc = fe_mul(f, acc, fe_dbl(f, ay));
         }
@@ -285,10 +291,10 @@ k_batch_pdbl_coop(size_t n, const uint32_t* __restrict__ px, const uint32_t* __r
     for (int k = COOP_K - 1; k >= 0; --k) {
         const size_t i = tile + (size_t)k * COOP_THREADS;
         if (i < n) {
-            fe ax = col_load(px, n, i), ay = col_load(py, n, i);
+            fe ax = col_load<NL>(px, n, i), ay = col_load<NL>(py, n, i);
             const bool degenerate = (pinf && pinf[i]) || fe_is_zero(ay);
             fe dinv = k > 0 ? fe_mul(f, inv, lp[k > 0 ? k - 1 : 0]) : inv;
-            fe xr = fe_zero(), yr = fe_zero();
+            fe xr = fe_zero_n<NL>(), yr = fe_zero_n<NL>();
             if (!degenerate) {
                 if (k > 0) inv = fe_mul(f, inv, fe_dbl(f, ay));
                 fe lam = fe_mul(f, tangent_numerator<C>(ax), dinv);
@@ -438,6 +444,12 @@ static size_t pick_threads(size_t n, int form) {
 cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* in, uint32_t* out,
                                 cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    if (curve == CURVE_BLS381) {  // 381-bit base field (12 limbs) / 255-bit scalar field: cooperative form
+        const unsigned cb = coop_blocks(n, 128);
+        if (field == 0) k_batch_invert_coop<Bls381P, 128><<<cb, 128, 0, s>>>(n, in, out);
+        else k_batch_invert_coop<Bls381R, 128><<<cb, 128, 0, s>>>(n, in, out);
+        return cudaGetLastError();
+    }
     const int form = pick_form(n);
     if (const int ct = coop_threads(form)) {
         if (curve == CURVE_SECP && field == 0) {
@@ -476,6 +488,10 @@ cudaError_t launch_batch_padd(int curve, size_t n, const uint32_t* px, const uin
                               const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
                               cudaStream_t s, void* scratch) {
     if (n == 0) return cudaSuccess;
+    if (curve == CURVE_BLS381) {
+        k_batch_padd_coop<Bls381Curve, 128><<<coop_blocks(n, 128), 128, 0, s>>>(n, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
+        return cudaGetLastError();
+    }
     const int form = pick_form(n, scratch != nullptr);
     if (form >= 6) {
         const int K = form == 6 ? 8 : 4;
@@ -525,6 +541,10 @@ cudaError_t launch_batch_pdbl(int curve, size_t n, const uint32_t* px, const uin
                               const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
                               cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    if (curve == CURVE_BLS381) {
+        k_batch_pdbl_coop<Bls381Curve, 128><<<coop_blocks(n, 128), 128, 0, s>>>(n, px, py, pinf, ox, oy, oinf);
+        return cudaGetLastError();
+    }
     const int form = pick_form(n);
     if (const int ct = coop_threads(form)) {
         if (curve == CURVE_SECP) {

@@ -13,9 +13,10 @@ __global__ void __launch_bounds__(256) k_field_op(int op, size_t n, const uint32
     const F f{};
     for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
          i += (size_t)gridDim.x * blockDim.x) {
-        fe x = col_load(a, n, i);
-        fe y = b ? col_load(b, n, i) : fe_zero();
-        fe r;
+        constexpr int N = F::N;
+        feN<N> x = col_load<N>(a, n, i);
+        feN<N> y = b ? col_load<N>(b, n, i) : fe_zero_n<N>();
+        feN<N> r;
         switch (op) {
             case 0: r = fe_mul(f, x, y); break;
             case 1: r = fe_add(f, x, y); break;
@@ -35,7 +36,10 @@ cudaError_t launch_field_op(int curve, int field, int op, size_t n, const uint32
     const int threads = 256;
     size_t want = (n + threads - 1) / threads;
     const int blocks = (int)(want < 148 * 16 ? want : 148 * 16);
-    if (curve == CURVE_SECP) {
+    if (curve == CURVE_BLS381) {  // base field: 12 limbs per element, scalar field: 8
+        if (field == 0) k_field_op<Bls381P><<<blocks, threads, 0, s>>>(op, n, a, b, out);
+        else k_field_op<Bls381R><<<blocks, threads, 0, s>>>(op, n, a, b, out);
+    } else if (curve == CURVE_SECP) {
         if (field == 0) k_field_op<SecpP><<<blocks, threads, 0, s>>>(op, n, a, b, out);
         else k_field_op<SecpN><<<blocks, threads, 0, s>>>(op, n, a, b, out);
     } else {

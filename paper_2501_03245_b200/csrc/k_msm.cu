@@ -37,7 +37,9 @@ k_msm_digits(size_t n, const uint32_t* __restrict__ scalars, const uint8_t* __re
              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
     const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    fe k = scalar_reduce_once<typename C::Fn>(col_load(scalars, n, i));
+    // any 256-bit scalar is accepted: below 2n for the 256-bit curves (one subtraction), below
+    // 2^256 < 3r for BLS12-381's 255-bit group order (two)
+    fe k = scalar_reduce_once<typename C::Fn>(scalar_reduce_once<typename C::Fn>(col_load<8>(scalars, n, i)));
     const bool skip = pinf && pinf[i];
     // k >= 2^255: use (n - k) * (-P).  A carry window would otherwise collect ~n/2 points in
     // ONE bucket (a single thread adding half a million points).
@@ -69,23 +71,25 @@ __device__ __forceinline__ size_t lower_bound_key(const uint32_t* keys, size_t m
     return lo;
 }
 
-// Jacobian point arrays are stored word-major: word k (0..23: X, Y, Z) of element e at
+// Jacobian point arrays are stored word-major: word k (0..3N-1: X, Y, Z) of element e at
 // buf[k * count + e].
-__device__ __forceinline__ void jac_store(uint32_t* buf, size_t count, size_t e, const jac& p) {
+template <int N>
+__device__ __forceinline__ void jac_store(uint32_t* buf, size_t count, size_t e, const jacN<N>& p) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < N; ++k) {
         buf[(size_t)k * count + e] = p.X.w[k];
-        buf[(size_t)(8 + k) * count + e] = p.Y.w[k];
-        buf[(size_t)(16 + k) * count + e] = p.Z.w[k];
+        buf[(size_t)(N + k) * count + e] = p.Y.w[k];
+        buf[(size_t)(2 * N + k) * count + e] = p.Z.w[k];
     }
 }
-__device__ __forceinline__ jac jac_load(const uint32_t* buf, size_t count, size_t e) {
-    jac p;
+template <int N>
+__device__ __forceinline__ jacN<N> jac_load(const uint32_t* buf, size_t count, size_t e) {
+    jacN<N> p;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
+    for (int k = 0; k < N; ++k) {
         p.X.w[k] = buf[(size_t)k * count + e];
-        p.Y.w[k] = buf[(size_t)(8 + k) * count + e];
-        p.Z.w[k] = buf[(size_t)(16 + k) * count + e];
+        p.Y.w[k] = buf[(size_t)(N + k) * count + e];
+        p.Z.w[k] = buf[(size_t)(2 * N + k) * count + e];
     }
     return p;
 }
@@ -106,6 +110,11 @@ k_msm_buckets(size_t n, size_t m, const uint32_t* __restrict__ keys, const uint3
               const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
               uint32_t* __restrict__ buckets, uint32_t* __restrict__ edge, uint32_t* __restrict__ edge_key,
               size_t slices) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (t >= slices) return;
     const typename C::Fp f{};
@@ -124,16 +133,16 @@ k_msm_buckets(size_t n, size_t m, const uint32_t* __restrict__ keys, const uint3
                 const bool open_left = first_run && cur == prev_key;
                 const bool open_right = p == hi && cur == next_key;
                 if (open_left) {
-                    jac_store(edge, 2 * slices, 2 * t, acc);
+                    jac_store<NL>(edge, 2 * slices, 2 * t, acc);
                     edge_key[2 * t] = cur;
                     // the whole slice lies inside one bucket: mark "continues to the right"
                     // (no point is stored in the right edge; the high bit says so)
                     if (open_right) edge_key[2 * t + 1] = cur | 0x80000000u;
                 } else if (open_right) {
-                    jac_store(edge, 2 * slices, 2 * t + 1, acc);
+                    jac_store<NL>(edge, 2 * slices, 2 * t + 1, acc);
                     edge_key[2 * t + 1] = cur;
                 } else {
-                    jac_store(buckets, MSM_NB, cur, acc);
+                    jac_store<NL>(buckets, MSM_NB, cur, acc);
                 }
             }
             first_run = false;
@@ -143,7 +152,7 @@ k_msm_buckets(size_t n, size_t m, const uint32_t* __restrict__ keys, const uint3
         if (p < hi && key < MSM_NB) {
             const uint32_t v = vals[p];
             const size_t idx = v & 0x7FFFFFFFu;
-            aff q{col_load(px, n, idx), col_load(py, n, idx)};
+            aff q{col_load<NL>(px, n, idx), col_load<NL>(py, n, idx)};
             if (v >> 31) q.y = fe_neg(f, q.y);
             acc = jac_madd<C>(acc, q);
         }
@@ -158,17 +167,22 @@ template <class C>
 __global__ void __launch_bounds__(128)
 k_msm_bucket_edges(uint32_t* __restrict__ buckets, const uint32_t* __restrict__ edge,
                    const uint32_t* __restrict__ edge_key, size_t slices) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     const size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (t >= slices) return;
     const uint32_t key = edge_key[2 * t + 1];
     if (key >= MSM_NB) return;  // this slice's last run does not continue to the right
-    jac acc = jac_load(edge, 2 * slices, 2 * t + 1);
+    jac acc = jac_load<NL>(edge, 2 * slices, 2 * t + 1);
 #pragma unroll 1
     for (size_t u = t + 1; u < slices && edge_key[2 * u] == key; ++u) {
-        acc = jac_add<C>(acc, jac_load(edge, 2 * slices, 2 * u));
+        acc = jac_add<C>(acc, jac_load<NL>(edge, 2 * slices, 2 * u));
         if (edge_key[2 * u + 1] != (key | 0x80000000u)) break;  // the run ended inside slice u
     }
-    jac_store(buckets, MSM_NB, key, acc);
+    jac_store<NL>(buckets, MSM_NB, key, acc);
 }
 
 // ---------------------------------------------------------------- batch-affine bucket accumulation
@@ -191,37 +205,66 @@ k_msm_bucket_edges(uint32_t* __restrict__ buckets, const uint32_t* __restrict__ 
 constexpr int MSM_TREE_LEVELS = 6;
 constexpr int MSM_TREE_THREADS = 128;
 
-struct rec4 {
-    uint4 a, b, c, d;  // x limbs 0-3, 4-7, y limbs 0-3, 4-7
-};
-__device__ __forceinline__ fe fe_from_u4(const uint4& lo, const uint4& hi) {
-    fe r;
-    r.w[0] = lo.x; r.w[1] = lo.y; r.w[2] = lo.z; r.w[3] = lo.w;
-    r.w[4] = hi.x; r.w[5] = hi.y; r.w[6] = hi.z; r.w[7] = hi.w;
+// A record is x | y, 2N limbs = N/2 16-byte words (64 B for 256-bit, 96 B for 381-bit curves).
+enum { LD_PLAIN = 0, LD_STREAM = 1, LD_KEEP = 2 };
+template <int N, int MODE>
+__device__ __forceinline__ feN<N> fe_load_u4(const uint4* p) {
+    feN<N> r;
+#pragma unroll
+    for (int q = 0; q < N / 4; ++q) {
+        const uint4 v = MODE == LD_STREAM ? __ldcs(p + q) : MODE == LD_KEEP ? __ldg(p + q) : p[q];
+        r.w[4 * q] = v.x; r.w[4 * q + 1] = v.y; r.w[4 * q + 2] = v.z; r.w[4 * q + 3] = v.w;
+    }
     return r;
 }
-__device__ __forceinline__ void rec_store(uint4* rec, size_t i, const fe& x, const fe& y) {
-    uint4* p = rec + 4 * i;
-    p[0] = make_uint4(x.w[0], x.w[1], x.w[2], x.w[3]);
-    p[1] = make_uint4(x.w[4], x.w[5], x.w[6], x.w[7]);
-    p[2] = make_uint4(y.w[0], y.w[1], y.w[2], y.w[3]);
-    p[3] = make_uint4(y.w[4], y.w[5], y.w[6], y.w[7]);
+template <int N, bool STREAM>
+__device__ __forceinline__ void fe_store_u4(uint4* p, const feN<N>& v) {
+#pragma unroll
+    for (int q = 0; q < N / 4; ++q) {
+        const uint4 t = make_uint4(v.w[4 * q], v.w[4 * q + 1], v.w[4 * q + 2], v.w[4 * q + 3]);
+        if (STREAM) __stcs(p + q, t);
+        else p[q] = t;
+    }
 }
-__device__ __forceinline__ fe rec_x(const uint4* rec, size_t i) {
-    return fe_from_u4(rec[4 * i], rec[4 * i + 1]);
+// Cache policy: the input records (64 MiB at 2^20) are gathered at random and re-read by every
+// window, so they should stay in L2; slots, prefix products and thread totals are written once
+// and read once per level, far apart -- they go through with streaming (evict-first) accesses.
+template <int N>
+__device__ __forceinline__ void rec_store(uint4* rec, size_t i, const feN<N>& x, const feN<N>& y) {
+    fe_store_u4<N, true>(rec + (N / 2) * i, x);
+    fe_store_u4<N, true>(rec + (N / 2) * i + N / 4, y);
 }
-__device__ __forceinline__ fe rec_y(const uint4* rec, size_t i) {
-    return fe_from_u4(rec[4 * i + 2], rec[4 * i + 3]);
+template <int N>
+__device__ __forceinline__ feN<N> rec_x(const uint4* rec, size_t i) {  // slots: streaming
+    return fe_load_u4<N, LD_STREAM>(rec + (N / 2) * i);
 }
+template <int N>
+__device__ __forceinline__ feN<N> rec_y(const uint4* rec, size_t i) {
+    return fe_load_u4<N, LD_STREAM>(rec + (N / 2) * i + N / 4);
+}
+template <int N>
+__device__ __forceinline__ feN<N> pt_x(const uint4* __restrict__ rec, size_t i) {  // input points: keep
+    return fe_load_u4<N, LD_KEEP>(rec + (N / 2) * i);
+}
+template <int N>
+__device__ __forceinline__ feN<N> pt_y(const uint4* __restrict__ rec, size_t i) {
+    return fe_load_u4<N, LD_KEEP>(rec + (N / 2) * i + N / 4);
+}
+template <int N>
+__device__ __forceinline__ void fe_store_cs(uint4* p, const feN<N>& v) { fe_store_u4<N, true>(p, v); }
+template <int N>
+__device__ __forceinline__ feN<N> fe_load_cs(const uint4* p) { return fe_load_u4<N, LD_STREAM>(p); }
 
 // column-major coordinates -> 64-byte records (one gather of a point = two 32-byte sectors
 // instead of sixteen)
+template <int N>
 __global__ void __launch_bounds__(256)
 k_msm_aos(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
           uint4* __restrict__ rec) {
     const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    rec_store(rec, i, col_load(px, n, i), col_load(py, n, i));
+    fe_store_u4<N, false>(rec + (N / 2) * i, col_load<N>(px, n, i));
+    fe_store_u4<N, false>(rec + (N / 2) * i + N / 4, col_load<N>(py, n, i));
 }
 
 // first position of every bucket's run in the sorted keys (0xFFFFFFFF: empty bucket; memset)
@@ -286,28 +329,32 @@ __device__ __forceinline__ TreeJoin<C, LEVEL0> tree_locate(size_t j, int level, 
 }
 
 template <class C>
-__device__ __forceinline__ aff msm_point(const uint4* __restrict__ rec, uint32_t v) {
+__device__ __forceinline__ caff<C> msm_point(const uint4* __restrict__ rec, uint32_t v) {
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
     const size_t idx = v & 0x7FFFFFFFu;
-    aff q{rec_x(rec, idx), rec_y(rec, idx)};
+    aff q{pt_x<NL>(rec, idx), pt_y<NL>(rec, idx)};
     if (v >> 31) q.y = fe_neg(typename C::Fp{}, q.y);
     return q;
 }
 
 // denominator of a join (one when nothing is inverted for it)
 template <class C, bool LEVEL0>
-__device__ __forceinline__ fe tree_denominator(const TreeJoin<C, LEVEL0>& t, const uint4* __restrict__ rec,
-                                               const uint4* slots, const uint8_t* sinf) {
+__device__ __forceinline__ cfe<C> tree_denominator(const TreeJoin<C, LEVEL0>& t, const uint4* __restrict__ rec,
+                                                   const uint4* slots, const uint8_t* sinf) {
+    using fe = cfe<C>;
+    constexpr int NL = C::Fp::N;
     const typename C::Fp f{};
     fe d = fe_one(f);
     if (!t.active) return d;
     fe ax, bx;
     bool ai = false, bi = false;
     if (LEVEL0) {
-        ax = rec_x(rec, t.v0 & 0x7FFFFFFFu);
-        bx = rec_x(rec, t.v1 & 0x7FFFFFFFu);
+        ax = pt_x<NL>(rec, t.v0 & 0x7FFFFFFFu);
+        bx = pt_x<NL>(rec, t.v1 & 0x7FFFFFFFu);
     } else {
-        ax = rec_x(slots, t.dst);
-        bx = rec_x(slots, t.src);
+        ax = rec_x<NL>(slots, t.dst);
+        bx = rec_x<NL>(slots, t.src);
         ai = sinf[t.dst] != 0;
         bi = sinf[t.src] != 0;
     }
@@ -318,8 +365,8 @@ __device__ __forceinline__ fe tree_denominator(const TreeJoin<C, LEVEL0>& t, con
             ay = msm_point<C>(rec, t.v0).y;
             by = msm_point<C>(rec, t.v1).y;
         } else {
-            ay = rec_y(slots, t.dst);
-            by = rec_y(slots, t.src);
+            ay = rec_y<NL>(slots, t.dst);
+            by = rec_y<NL>(slots, t.src);
         }
         classify_pair<C>(ax, ay, false, bx, by, false, &d);
         return d;
@@ -330,16 +377,19 @@ __device__ __forceinline__ fe tree_denominator(const TreeJoin<C, LEVEL0>& t, con
 // backward step of Montgomery's trick for one join: inv holds the inverse of the product of
 // the denominators up to and including this join's; prev the product before it.
 template <class C, bool LEVEL0>
-__device__ __forceinline__ void tree_apply(const TreeJoin<C, LEVEL0>& t, fe& inv, const fe& prev, bool first,
+__device__ __forceinline__ void tree_apply(const TreeJoin<C, LEVEL0>& t, cfe<C>& inv, const cfe<C>& prev, bool first,
                                            const uint4* __restrict__ rec, uint4* slots, uint8_t* sinf) {
+    using fe = cfe<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
     const typename C::Fp f{};
     if (LEVEL0 && t.copy2) {
         const aff p0 = msm_point<C>(rec, t.v0);
-        rec_store(slots, t.dst, p0.x, p0.y);
+        rec_store<NL>(slots, t.dst, p0.x, p0.y);
         sinf[t.dst] = 0;
         if (t.src != (size_t)-1) {
             const aff p1 = msm_point<C>(rec, t.v1);
-            rec_store(slots, t.src, p1.x, p1.y);
+            rec_store<NL>(slots, t.src, p1.x, p1.y);
             sinf[t.src] = 0;
         }
         return;
@@ -351,8 +401,8 @@ __device__ __forceinline__ void tree_apply(const TreeJoin<C, LEVEL0>& t, fe& inv
         A = msm_point<C>(rec, t.v0);
         B = msm_point<C>(rec, t.v1);
     } else {
-        A.x = rec_x(slots, t.dst); A.y = rec_y(slots, t.dst);
-        B.x = rec_x(slots, t.src); B.y = rec_y(slots, t.src);
+        A.x = rec_x<NL>(slots, t.dst); A.y = rec_y<NL>(slots, t.dst);
+        B.x = rec_x<NL>(slots, t.src); B.y = rec_y<NL>(slots, t.src);
         ai = sinf[t.dst] != 0;
         bi = sinf[t.src] != 0;
     }
@@ -363,7 +413,7 @@ __device__ __forceinline__ void tree_apply(const TreeJoin<C, LEVEL0>& t, fe& inv
         dinv = fe_mul(f, inv, prev);
         inv = fe_mul(f, inv, d);
     }
-    fe xr = fe_zero(), yr = fe_zero();
+    fe xr = fe_zero_n<NL>(), yr = fe_zero_n<NL>();
     uint8_t rinf = 0;
     if (kind == K_GENERIC) {
         fe lam = fe_mul(f, fe_sub(f, A.y, B.y), dinv);
@@ -378,7 +428,7 @@ __device__ __forceinline__ void tree_apply(const TreeJoin<C, LEVEL0>& t, fe& inv
     } else {
         rinf = 1;
     }
-    rec_store(slots, t.dst, xr, yr);
+    rec_store<NL>(slots, t.dst, xr, yr);
     sinf[t.dst] = rinf;
 }
 
@@ -389,8 +439,13 @@ __global__ void __launch_bounds__(MSM_TREE_THREADS)
 k_msm_tree(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
            const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
            uint4* slots, uint8_t* sinf) {
-    __shared__ uint32_t sm_scan[16 * (MSM_TREE_THREADS / 32)];
-    __shared__ uint32_t sm_pref[K * 8 * MSM_TREE_THREADS];
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
+    __shared__ uint32_t sm_scan[2 * NL * (MSM_TREE_THREADS / 32)];
+    __shared__ uint32_t sm_pref[K * NL * MSM_TREE_THREADS];
     const typename C::Fp f{};
     const size_t j0 = (size_t)blockIdx.x * (MSM_TREE_THREADS * K) + threadIdx.x;
     fe acc = fe_one(f);
@@ -402,7 +457,7 @@ k_msm_tree(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
             if (t.active) acc = fe_mul(f, acc, tree_denominator<C, LEVEL0>(t, rec, slots, sinf));
         }
 #pragma unroll
-        for (int w = 0; w < 8; ++w) sm_pref[(k * 8 + w) * MSM_TREE_THREADS + threadIdx.x] = acc.w[w];
+        for (int w = 0; w < NL; ++w) sm_pref[(k * NL + w) * MSM_TREE_THREADS + threadIdx.x] = acc.w[w];
     }
     fe inv = coop_block_inverse<decltype(f), MSM_TREE_THREADS>(f, acc, sm_scan);
 #pragma unroll 1
@@ -413,7 +468,7 @@ k_msm_tree(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
         fe prev = fe_one(f);
         if (k > 0) {
 #pragma unroll
-            for (int w = 0; w < 8; ++w) prev.w[w] = sm_pref[((k - 1) * 8 + w) * MSM_TREE_THREADS + threadIdx.x];
+            for (int w = 0; w < NL; ++w) prev.w[w] = sm_pref[((k - 1) * NL + w) * MSM_TREE_THREADS + threadIdx.x];
         }
         tree_apply<C, LEVEL0>(t, inv, prev, k == 0, rec, slots, sinf);
     }
@@ -433,7 +488,12 @@ k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
                const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
                uint4* __restrict__ pref, uint4* __restrict__ others, uint32_t* __restrict__ totals,
                size_t tiles) {
-    __shared__ uint32_t sm_scan[16 * (MSM_TREE_THREADS / 32)];
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
+    __shared__ uint32_t sm_scan[2 * NL * (MSM_TREE_THREADS / 32)];
     const typename C::Fp f{};
     const size_t j0 = (size_t)blockIdx.x * (MSM_TREE_THREADS * K) + threadIdx.x;
     fe acc = fe_one(f);
@@ -443,14 +503,12 @@ k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
         if (j >= joins) break;
         const TreeJoin<C, LEVEL0> t = tree_locate<C, LEVEL0>(j, level, m, keys, vals);
         if (t.active) acc = fe_mul(f, acc, tree_denominator<C, LEVEL0>(t, rec, slots, sinf));
-        pref[2 * j] = make_uint4(acc.w[0], acc.w[1], acc.w[2], acc.w[3]);
-        pref[2 * j + 1] = make_uint4(acc.w[4], acc.w[5], acc.w[6], acc.w[7]);
+        fe_store_cs<NL>(pref + (NL / 4) * j, acc);
     }
     fe total;
     const fe oth = block_others_product<decltype(f), MSM_TREE_THREADS>(f, acc, sm_scan, &total);
     const size_t tid = (size_t)blockIdx.x * MSM_TREE_THREADS + threadIdx.x;
-    others[2 * tid] = make_uint4(oth.w[0], oth.w[1], oth.w[2], oth.w[3]);
-    others[2 * tid + 1] = make_uint4(oth.w[4], oth.w[5], oth.w[6], oth.w[7]);
+    fe_store_cs<NL>(others + (NL / 4) * tid, oth);
     if (threadIdx.x == 0) col_store(totals, tiles, blockIdx.x, total);
 }
 
@@ -460,11 +518,16 @@ k_msm_tree_bwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
                const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
                uint4* slots, uint8_t* sinf, const uint4* __restrict__ pref,
                const uint4* __restrict__ others, const uint32_t* __restrict__ total_inv, size_t tiles) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     const typename C::Fp f{};
     const size_t j0 = (size_t)blockIdx.x * (MSM_TREE_THREADS * K) + threadIdx.x;
     if (j0 >= joins) return;
     const size_t tid = (size_t)blockIdx.x * MSM_TREE_THREADS + threadIdx.x;
-    fe inv = fe_mul(f, col_load(total_inv, tiles, blockIdx.x), fe_from_u4(others[2 * tid], others[2 * tid + 1]));
+    fe inv = fe_mul(f, col_load<NL>(total_inv, tiles, blockIdx.x), fe_load_cs<NL>(others + (NL / 4) * tid));
 #pragma unroll 1
     for (int k = K - 1; k >= 0; --k) {
         const size_t j = j0 + (size_t)k * MSM_TREE_THREADS;
@@ -473,38 +536,10 @@ k_msm_tree_bwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
         fe prev = fe_one(f);
         if (k > 0) {
             const size_t jp = j - MSM_TREE_THREADS;
-            prev = fe_from_u4(pref[2 * jp], pref[2 * jp + 1]);
+            prev = fe_load_cs<NL>(pref + (NL / 4) * jp);
         }
         tree_apply<C, LEVEL0>(t, inv, prev, k == 0, rec, slots, sinf);
     }
-}
-
-// one thread per bucket: slot[start] + the slots at multiples of 2^MSM_TREE_LEVELS inside the run
-template <class C>
-__global__ void __launch_bounds__(128)
-k_msm_tail(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ starts,
-           const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
-           uint32_t* __restrict__ buckets) {
-    const uint32_t b = blockIdx.x * blockDim.x + threadIdx.x;
-    if (b >= MSM_NB) return;
-    const typename C::Fp f{};
-    jac acc = jac_infinity<C>();
-    const size_t s = starts[b];
-    if (s != 0xFFFFFFFFu) {
-        if (!sinf[s]) {
-            acc.X = rec_x(slots, s);
-            acc.Y = rec_y(slots, s);
-            acc.Z = fe_one(f);
-        }
-        const size_t step = (size_t)1 << MSM_TREE_LEVELS;
-#pragma unroll 1
-        for (size_t a = (s / step + 1) * step; a < m && keys[a] == b; a += step) {
-            if (sinf[a]) continue;
-            aff q{rec_x(slots, a), rec_y(slots, a)};
-            acc = jac_madd<C>(acc, q);
-        }
-    }
-    jac_store(buckets, MSM_NB, b, acc);
 }
 
 // marginal sums, stage 1: thread (w, k, e, part) adds the 32 buckets of window w whose
@@ -512,6 +547,11 @@ k_msm_tail(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restri
 template <class C>
 __global__ void __launch_bounds__(128)
 k_msm_marginal_parts(const uint32_t* __restrict__ buckets, uint32_t* __restrict__ parts) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= MSM_WINDOWS * 3 * 32 * 32) return;
     const uint32_t part = t & 31, e = (t >> 5) & 31, k = (t >> 10) % 3, w = t / (3 * 1024);
@@ -522,26 +562,36 @@ k_msm_marginal_parts(const uint32_t* __restrict__ buckets, uint32_t* __restrict_
         if (k == 0) b = e + 32 * part + 1024 * v;        // lo = e
         else if (k == 1) b = part + 32 * e + 1024 * v;   // mid = e
         else b = part + 32 * v + 1024 * e;               // top = e
-        acc = jac_add<C>(acc, jac_load(buckets, MSM_NB, (size_t)w * MSM_BUCKETS + b));
+        acc = jac_add<C>(acc, jac_load<NL>(buckets, MSM_NB, (size_t)w * MSM_BUCKETS + b));
     }
-    jac_store(parts, (size_t)MSM_WINDOWS * 3 * 1024, t, acc);
+    jac_store<NL>(parts, (size_t)MSM_WINDOWS * 3 * 1024, t, acc);
 }
 // stage 2: thread (w, k, e) folds its 32 parts
 template <class C>
 __global__ void __launch_bounds__(128)
 k_msm_marginal_fold(const uint32_t* __restrict__ parts, uint32_t* __restrict__ marg) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= MSM_WINDOWS * 3 * 32) return;
     jac acc = jac_infinity<C>();
 #pragma unroll 1
     for (uint32_t p = 0; p < 32; ++p)
-        acc = jac_add<C>(acc, jac_load(parts, (size_t)MSM_WINDOWS * 3 * 1024, (size_t)t * 32 + p));
-    jac_store(marg, (size_t)MSM_WINDOWS * 3 * 32, t, acc);
+        acc = jac_add<C>(acc, jac_load<NL>(parts, (size_t)MSM_WINDOWS * 3 * 1024, (size_t)t * 32 + p));
+    jac_store<NL>(marg, (size_t)MSM_WINDOWS * 3 * 32, t, acc);
 }
 // stage 3: thread (w, j): j < 3 -> sum_e e * C^j_e (running sums); j == 3 -> sum_e C^0_e
 template <class C>
 __global__ void __launch_bounds__(128)
 k_msm_weighted(const uint32_t* __restrict__ marg, uint32_t* __restrict__ wsum) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= MSM_WINDOWS * 4) return;
     const uint32_t w = t >> 2, j = t & 3;
@@ -549,16 +599,16 @@ k_msm_weighted(const uint32_t* __restrict__ marg, uint32_t* __restrict__ wsum) {
     jac acc = jac_infinity<C>();
     if (j == 3) {
 #pragma unroll 1
-        for (uint32_t e = 0; e < 32; ++e) acc = jac_add<C>(acc, jac_load(marg, cnt, (size_t)(w * 3) * 32 + e));
+        for (uint32_t e = 0; e < 32; ++e) acc = jac_add<C>(acc, jac_load<NL>(marg, cnt, (size_t)(w * 3) * 32 + e));
     } else {
         jac run = jac_infinity<C>();
 #pragma unroll 1
         for (int e = 31; e >= 1; --e) {
-            run = jac_add<C>(run, jac_load(marg, cnt, (size_t)(w * 3 + j) * 32 + e));
+            run = jac_add<C>(run, jac_load<NL>(marg, cnt, (size_t)(w * 3 + j) * 32 + e));
             acc = jac_add<C>(acc, run);
         }
     }
-    jac_store(wsum, (size_t)MSM_WINDOWS * 4, t, acc);
+    jac_store<NL>(wsum, (size_t)MSM_WINDOWS * 4, t, acc);
 }
 // stage 4 (one block of 32 threads): thread w forms S_w = (sum B) + W0 + 32 W1 + 1024 W2
 // (weights b + 1), shifts it by 2^(16 w); thread 0 adds the windows and converts to affine.
@@ -566,31 +616,36 @@ template <class C>
 __global__ void __launch_bounds__(32)
 k_msm_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, uint32_t* __restrict__ oy,
               uint8_t* __restrict__ oinf) {
-    __shared__ uint32_t win[24 * MSM_WINDOWS];
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
+    __shared__ uint32_t win[3 * NL * MSM_WINDOWS];
     const uint32_t w = threadIdx.x;
     const size_t cnt = (size_t)MSM_WINDOWS * 4;
     if (w < MSM_WINDOWS) {
-        jac s = jac_load(wsum, cnt, w * 4 + 2);
+        jac s = jac_load<NL>(wsum, cnt, w * 4 + 2);
 #pragma unroll 1
         for (int i = 0; i < 5; ++i) s = jac_dbl<C>(s);
-        s = jac_add<C>(s, jac_load(wsum, cnt, w * 4 + 1));
+        s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 1));
 #pragma unroll 1
         for (int i = 0; i < 5; ++i) s = jac_dbl<C>(s);
-        s = jac_add<C>(s, jac_load(wsum, cnt, w * 4 + 0));
-        s = jac_add<C>(s, jac_load(wsum, cnt, w * 4 + 3));
+        s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 0));
+        s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 3));
 #pragma unroll 1
         for (uint32_t i = 0; i < MSM_C * w; ++i) s = jac_dbl<C>(s);
-        jac_store(win, MSM_WINDOWS, w, s);
+        jac_store<NL>(win, MSM_WINDOWS, w, s);
     }
     __syncthreads();
     if (w == 0) {
         const typename C::Fp f{};
         jac acc = jac_infinity<C>();
 #pragma unroll 1
-        for (int i = 0; i < MSM_WINDOWS; ++i) acc = jac_add<C>(acc, jac_load(win, MSM_WINDOWS, i));
+        for (int i = 0; i < MSM_WINDOWS; ++i) acc = jac_add<C>(acc, jac_load<NL>(win, MSM_WINDOWS, i));
         if (jac_is_inf<C>(acc)) {
-            col_store(ox, 1, 0, fe_zero());
-            col_store(oy, 1, 0, fe_zero());
+            col_store(ox, 1, 0, fe_zero_n<NL>());
+            col_store(oy, 1, 0, fe_zero_n<NL>());
             oinf[0] = 1;
         } else {
             aff a = jac_to_aff_with<C>(acc, fe_inv(f, acc.Z));
@@ -615,10 +670,11 @@ k_msm_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, uint
 //   k_msm_red_combine  : lane w forms S_w, shifts it by 2^(16 w); shuffle tree over the windows.
 constexpr uint32_t MSM_RED_PARTS = MSM_WINDOWS * 3 * 32 * 32 * 4;
 
-__device__ __forceinline__ jac jac_shfl_down(const jac& p, int d) {
-    jac r;
+template <int N>
+__device__ __forceinline__ jacN<N> jac_shfl_down(const jacN<N>& p, int d) {
+    jacN<N> r;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < N; ++i) {
         r.X.w[i] = __shfl_down_sync(0xFFFFFFFFu, p.X.w[i], d);
         r.Y.w[i] = __shfl_down_sync(0xFFFFFFFFu, p.Y.w[i], d);
         r.Z.w[i] = __shfl_down_sync(0xFFFFFFFFu, p.Z.w[i], d);
@@ -627,7 +683,8 @@ __device__ __forceinline__ jac jac_shfl_down(const jac& p, int d) {
 }
 // lane 0 ends with the sum of all 32 lanes' points
 template <class C>
-__device__ __forceinline__ jac warp_sum_points(jac acc, int lane) {
+__device__ __forceinline__ cjac<C> warp_sum_points(cjac<C> acc, int lane) {
+    using jac = cjac<C>;
 #pragma unroll 1
     for (int d = 16; d >= 1; d >>= 1) {
         const jac other = jac_shfl_down(acc, d);
@@ -641,6 +698,11 @@ __global__ void __launch_bounds__(128)
 k_msm_red_parts(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ starts,
                 const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
                 uint32_t* __restrict__ parts) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= MSM_RED_PARTS) return;
     const uint32_t sub = t & 3, part = (t >> 2) & 31, e = (t >> 7) & 31, k = (t >> 12) % 3, w = t / (3 * 4096);
@@ -655,62 +717,77 @@ k_msm_red_parts(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __r
         const uint32_t id = w * MSM_BUCKETS + b;
         const size_t s = starts[id];
         if (s == 0xFFFFFFFFu) continue;
-        if (!sinf[s]) acc = jac_madd<C>(acc, aff{rec_x(slots, s), rec_y(slots, s)});
+        if (!sinf[s]) acc = jac_madd<C>(acc, aff{rec_x<NL>(slots, s), rec_y<NL>(slots, s)});
 #pragma unroll 1
         for (size_t a = (s / step + 1) * step; a < m && keys[a] == id; a += step)
-            if (!sinf[a]) acc = jac_madd<C>(acc, aff{rec_x(slots, a), rec_y(slots, a)});
+            if (!sinf[a]) acc = jac_madd<C>(acc, aff{rec_x<NL>(slots, a), rec_y<NL>(slots, a)});
     }
-    jac_store(parts, MSM_RED_PARTS, t, acc);
+    jac_store<NL>(parts, MSM_RED_PARTS, t, acc);
 }
 
 template <class C>
 __global__ void __launch_bounds__(128)
 k_msm_red_fold(const uint32_t* __restrict__ parts, uint32_t* __restrict__ marg) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (gw >= MSM_WINDOWS * 3 * 32) return;  // whole warps leave together
     const size_t base = ((size_t)gw * 32 + lane) * 4;
-    jac acc = jac_load(parts, MSM_RED_PARTS, base);
+    jac acc = jac_load<NL>(parts, MSM_RED_PARTS, base);
 #pragma unroll 1
-    for (int sub = 1; sub < 4; ++sub) acc = jac_add<C>(acc, jac_load(parts, MSM_RED_PARTS, base + sub));
+    for (int sub = 1; sub < 4; ++sub) acc = jac_add<C>(acc, jac_load<NL>(parts, MSM_RED_PARTS, base + sub));
     acc = warp_sum_points<C>(acc, lane);
-    if (lane == 0) jac_store(marg, (size_t)MSM_WINDOWS * 3 * 32, gw, acc);
+    if (lane == 0) jac_store<NL>(marg, (size_t)MSM_WINDOWS * 3 * 32, gw, acc);
 }
 
 template <class C>
 __global__ void __launch_bounds__(128)
 k_msm_red_weighted(const uint32_t* __restrict__ marg, uint32_t* __restrict__ wsum) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (gw >= MSM_WINDOWS * 3) return;
     const uint32_t w = gw / 3, k = gw % 3;
-    jac S = jac_load(marg, (size_t)MSM_WINDOWS * 3 * 32, (size_t)gw * 32 + lane);
+    jac S = jac_load<NL>(marg, (size_t)MSM_WINDOWS * 3 * 32, (size_t)gw * 32 + lane);
 #pragma unroll 1
     for (int d = 1; d < 32; d <<= 1) {  // inclusive suffix sums
         const jac other = jac_shfl_down(S, d);
         if (lane + d < 32) S = jac_add<C>(S, other);
     }
     const size_t cnt = (size_t)MSM_WINDOWS * 4;
-    if (lane == 0 && k == 0) jac_store(wsum, cnt, w * 4 + 3, S);  // S_0 = sum_e C_e
+    if (lane == 0 && k == 0) jac_store<NL>(wsum, cnt, w * 4 + 3, S);  // S_0 = sum_e C_e
     jac R = lane == 0 ? jac_infinity<C>() : S;
     R = warp_sum_points<C>(R, lane);                              // sum_{e >= 1} S_e = sum_e e C_e
-    if (lane == 0) jac_store(wsum, cnt, w * 4 + k, R);
+    if (lane == 0) jac_store<NL>(wsum, cnt, w * 4 + k, R);
 }
 
 template <class C>
 __global__ void __launch_bounds__(32)
 k_msm_red_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, uint32_t* __restrict__ oy,
                   uint8_t* __restrict__ oinf) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     const uint32_t w = threadIdx.x;
     const size_t cnt = (size_t)MSM_WINDOWS * 4;
     jac s = jac_infinity<C>();
     if (w < MSM_WINDOWS) {
-        s = jac_load(wsum, cnt, w * 4 + 2);
+        s = jac_load<NL>(wsum, cnt, w * 4 + 2);
 #pragma unroll 1
         for (int i = 0; i < 5; ++i) s = jac_dbl<C>(s);
-        s = jac_add<C>(s, jac_load(wsum, cnt, w * 4 + 1));
+        s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 1));
 #pragma unroll 1
         for (int i = 0; i < 5; ++i) s = jac_dbl<C>(s);
-        s = jac_add<C>(s, jac_load(wsum, cnt, w * 4 + 0));
-        s = jac_add<C>(s, jac_load(wsum, cnt, w * 4 + 3));
+        s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 0));
+        s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 3));
 #pragma unroll 1
         for (uint32_t i = 0; i < MSM_C * w; ++i) s = jac_dbl<C>(s);
     }
@@ -718,8 +795,8 @@ k_msm_red_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, 
     if (w == 0) {
         const typename C::Fp f{};
         if (jac_is_inf<C>(s)) {
-            col_store(ox, 1, 0, fe_zero());
-            col_store(oy, 1, 0, fe_zero());
+            col_store(ox, 1, 0, fe_zero_n<NL>());
+            col_store(oy, 1, 0, fe_zero_n<NL>());
             oinf[0] = 1;
         } else {
             aff a = jac_to_aff_with<C>(s, fe_inv(f, s.Z));
@@ -747,8 +824,9 @@ void set_msm_form(int form) { g_msm_form = form; }
 static bool msm_affine() { return g_msm_form != 1; }
 constexpr int MSM_TREE_KMIN = 2;  // fewest joins per thread any level uses
 
-static MsmPlan msm_plan(size_t n) {
+static MsmPlan msm_plan(size_t n, int limbs) {
     MsmPlan p{};
+    const size_t jb = (size_t)12 * limbs, rb = (size_t)8 * limbs, fb = (size_t)4 * limbs;  // bytes: Jacobian point, record, element
     p.pairs = n * MSM_WINDOWS;
     cub::DeviceRadixSort::SortPairs(nullptr, p.sort_temp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                     (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)p.pairs, 0, 20);
@@ -759,30 +837,30 @@ static MsmPlan msm_plan(size_t n) {
     p.off_keys2 = take(4 * p.pairs);
     p.off_vals2 = take(4 * p.pairs);
     p.slices = (p.pairs + MSM_SLICE - 1) / MSM_SLICE;
-    p.off_buckets = take((size_t)96 * MSM_NB);
-    p.off_parts = take((size_t)96 * MSM_RED_PARTS);
-    p.off_marg = take((size_t)96 * MSM_WINDOWS * 3 * 32);
-    p.off_wsum = take((size_t)96 * MSM_WINDOWS * 4);
+    p.off_buckets = take(jb * MSM_NB);
+    p.off_parts = take(jb * MSM_RED_PARTS);
+    p.off_marg = take(jb * MSM_WINDOWS * 3 * 32);
+    p.off_wsum = take(jb * MSM_WINDOWS * 4);
     p.off_temp = take(p.sort_temp);
     // the two accumulation forms never run in the same call: their scratch overlaps
     const size_t fork = at;
-    p.off_edge = take((size_t)96 * 2 * p.slices);
+    p.off_edge = take(jb * 2 * p.slices);
     p.off_edge_key = take((size_t)4 * 2 * p.slices);
     const size_t end_jac = at;
     at = fork;
-    p.off_rec = take((size_t)64 * n);
-    p.off_slots = take((size_t)64 * p.pairs);
+    p.off_rec = take(rb * n);
+    p.off_slots = take(rb * p.pairs);
     p.off_sinf = take(p.pairs);
     p.off_starts = take((size_t)4 * MSM_NB);
     const size_t joins0 = (p.pairs + 1) / 2;
-    p.off_pref = take((size_t)32 * joins0);
+    p.off_pref = take(fb * joins0);
     p.max_tiles = (joins0 + (size_t)MSM_TREE_THREADS * MSM_TREE_KMIN - 1) / ((size_t)MSM_TREE_THREADS * MSM_TREE_KMIN);
-    p.off_others = take((size_t)32 * MSM_TREE_THREADS * p.max_tiles);
-    p.off_totals = take((size_t)2 * 32 * (p.max_tiles + 64));
+    p.off_others = take(fb * MSM_TREE_THREADS * p.max_tiles);
+    p.off_totals = take(2 * fb * (p.max_tiles + 64));
     p.total = at > end_jac ? at : end_jac;
     return p;
 }
-size_t msm_scratch_bytes(size_t n) { return n ? msm_plan(n).total : 0; }
+size_t msm_scratch_bytes(size_t n, int curve) { return n ? msm_plan(n, curve_limbs(curve)).total : 0; }
 
 struct TreeBufs {
     const uint32_t *keys, *vals;
@@ -800,13 +878,13 @@ static cudaError_t launch_tree(int curve, size_t m, int level, const TreeBufs& b
     const size_t per_block = (size_t)MSM_TREE_THREADS * K;
     const size_t tiles = (joins + per_block - 1) / per_block;
     const unsigned blocks = (unsigned)tiles;
-    if constexpr (K <= 8) {
+    if constexpr (K * C::Fp::N <= 64) {  // the single-launch form parks K prefixes per thread in shared memory
         if (!split) {
             k_msm_tree<C, K, LEVEL0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots, b.sinf);
             return cudaGetLastError();
         }
     }
-    uint32_t* total_inv = b.totals + 8 * (b.max_tiles + 64);
+    uint32_t* total_inv = b.totals + (size_t)C::Fp::N * (b.max_tiles + 64);
     k_msm_tree_fwd<C, K, LEVEL0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots,
                                                                       b.sinf, b.pref, b.others, b.totals, tiles);
     if (cudaError_t e = launch_batch_invert(curve, 0, tiles, b.totals, total_inv, s)) return e;
@@ -819,7 +897,8 @@ template <class C>
 static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px, const uint32_t* py,
                            const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
                            void* scratch, cudaStream_t s, int* launches) {
-    MsmPlan p = msm_plan(n);
+    constexpr int NL = C::Fp::N;
+    MsmPlan p = msm_plan(n, NL);
     uint8_t* base = (uint8_t*)scratch;
     uint32_t *keys = (uint32_t*)(base + p.off_keys), *vals = (uint32_t*)(base + p.off_vals);
     uint32_t *keys2 = (uint32_t*)(base + p.off_keys2), *vals2 = (uint32_t*)(base + p.off_vals2);
@@ -838,7 +917,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
         e = cudaMemsetAsync(starts, 0xFF, (size_t)4 * MSM_NB, s);
         if (e != cudaSuccess) return e;
         k_msm_starts<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, keys2, starts);
-        k_msm_aos<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, px, py, rec);
+        k_msm_aos<NL><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, px, py, rec);
         // K joins per thread; thin levels take fewer per thread so that the chip stays filled
         const bool split = g_msm_form != 3;
         TreeBufs tb{keys2, vals2, rec, slots, sinf, (uint4*)(base + p.off_pref), (uint4*)(base + p.off_others),
@@ -866,7 +945,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
         return cudaGetLastError();
     } else {
         uint32_t *edge = (uint32_t*)(base + p.off_edge), *edge_key = (uint32_t*)(base + p.off_edge_key);
-        e = cudaMemsetAsync(buckets, 0, (size_t)96 * MSM_NB, s);  // empty buckets = infinity (Z = 0)
+        e = cudaMemsetAsync(buckets, 0, (size_t)12 * NL * MSM_NB, s);  // empty buckets = infinity (Z = 0)
         if (e != cudaSuccess) return e;
         const unsigned sb = (unsigned)((p.slices + 127) / 128);
         k_msm_buckets<C><<<sb, 128, 0, s>>>(n, p.pairs, keys2, vals2, px, py, buckets, edge, edge_key, p.slices);
@@ -884,6 +963,8 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
 cudaError_t launch_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px,
                        const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
                        uint8_t* oinf, void* scratch, cudaStream_t s, int* launches) {
+    if (curve == CURVE_BLS381)
+        return run_msm<Bls381Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
     if (curve == CURVE_SECP)
         return run_msm<SecpCurve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
     return run_msm<Sm2Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);

@@ -11,19 +11,22 @@
 using namespace gecc;
 
 namespace {
-fe col_get(const uint32_t* c, size_t n, size_t i) {
-    fe v;
-    for (int k = 0; k < 8; ++k) v.w[k] = c[k * n + i];
+template <int N = 8>
+feN<N> col_get(const uint32_t* c, size_t n, size_t i) {
+    feN<N> v;
+    for (int k = 0; k < N; ++k) v.w[k] = c[k * n + i];
     return v;
 }
-void col_set(uint32_t* c, size_t n, size_t i, const fe& v) {
-    for (int k = 0; k < 8; ++k) c[k * n + i] = v.w[k];
+template <int N>
+void col_set(uint32_t* c, size_t n, size_t i, const feN<N>& v) {
+    for (int k = 0; k < N; ++k) c[k * n + i] = v.w[k];
 }
 
 template <class F>
 int field_op_t(const F& f, int op, size_t n, const uint32_t* a, const uint32_t* b, uint32_t* out) {
+    constexpr int N = F::N;
     for (size_t i = 0; i < n; ++i) {
-        fe x = col_get(a, n, i), y = b ? col_get(b, n, i) : fe_zero(), r = fe_zero();
+        feN<N> x = col_get<N>(a, n, i), y = b ? col_get<N>(b, n, i) : fe_zero_n<N>(), r = fe_zero_n<N>();
         switch (op) {
             case 0: r = fe_mul(f, x, y); break;
             case 1: r = fe_add(f, x, y); break;
@@ -54,11 +57,62 @@ int hs_field_op(int field, const FieldRT* rt, int op, size_t n, const uint32_t* 
         case 3: return field_op_t(Sm2N{}, op, n, a, b, out);
         case 4: return field_op_t(*rt, op, n, a, b, out);
         case 5: return field_op_t(SecpPL{}, op, n, a, b, out);  // lazy plain secp256k1 (outputs weakly reduced)
+        case 6: return field_op_t(Bls381P{}, op, n, a, b, out);  // 12 limbs
+        case 7: return field_op_t(Bls381R{}, op, n, a, b, out);
     }
     return 1;
 }
 
 }  // extern "C"
+
+// BLS12-381 G1 point formulas (12-limb coordinates): op 0 = P + Q through jac_madd / jac_add,
+// 1 = 2P, 2 = k * P by double-and-add with mixed additions; affine Montgomery in and out.
+#include "gecc_curve.cuh"
+extern "C" int hs_bls_point_op(int op, size_t n, const uint32_t* k, const uint32_t* px, const uint32_t* py,
+                               const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty, const uint8_t* tinf,
+                               uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    using C = Bls381Curve;
+    const Bls381P f{};
+    for (size_t i = 0; i < n; ++i) {
+        caff<C> p{col_get<12>(px, n, i), col_get<12>(py, n, i)};
+        cjac<C> P = jac_infinity<C>();
+        if (!pinf[i]) { P.X = p.x; P.Y = p.y; P.Z = fe_one(f); }
+        cjac<C> r = jac_infinity<C>();
+        if (op == 0) {
+            caff<C> t{col_get<12>(tx, n, i), col_get<12>(ty, n, i)};
+            cjac<C> T = jac_infinity<C>();
+            if (!tinf[i]) { T.X = t.x; T.Y = t.y; T.Z = fe_one(f); }
+            // exercise both routes: mixed when T is finite, and the general addition of two doubled-up points
+            cjac<C> m = tinf[i] ? P : jac_madd<C>(P, t);
+            cjac<C> g = jac_add<C>(jac_add<C>(P, T), jac_infinity<C>());
+            if (jac_is_inf<C>(m) != jac_is_inf<C>(g)) return 2;
+            r = g;
+            if (!jac_is_inf<C>(m)) {  // the two routes must agree as affine points
+                caff<C> am = jac_to_aff_with<C>(m, fe_inv(f, m.Z)), ag = jac_to_aff_with<C>(g, fe_inv(f, g.Z));
+                if (!fe_eq(am.x, ag.x) || !fe_eq(am.y, ag.y)) return 3;
+            }
+        } else if (op == 1) {
+            r = jac_dbl<C>(P);
+        } else {
+            feN<8> s = col_get<8>(k, n, i);
+            for (int b = 255; b >= 0; --b) {
+                r = jac_dbl<C>(r);
+                if (!pinf[i] && ((s.w[b >> 5] >> (b & 31)) & 1)) r = jac_madd<C>(r, p);
+            }
+        }
+        if (jac_is_inf<C>(r)) {
+            col_set(ox, n, i, fe_zero_n<12>());
+            col_set(oy, n, i, fe_zero_n<12>());
+            oinf[i] = 1;
+        } else {
+            caff<C> a = jac_to_aff_with<C>(r, fe_inv(f, r.Z));
+            col_set(ox, n, i, a.x);
+            col_set(oy, n, i, a.y);
+            oinf[i] = 0;
+        }
+    }
+    return 0;
+}
 
 // ---------------------------------------------------------------------------
 // ECDSA / point-multiplication lanes (gecc_ecdsa.cuh) run as plain host loops.

@@ -35,9 +35,12 @@ SECP_LAZY_CURVE = 2   # secp256k1 in the lazy plain representation (ECDSA kernel
 SECP_LAZY_FIELD = 5
 
 
+BLS_P_FIELD, BLS_R_FIELD = 6, 7   # BLS12-381 base field (12 limbs) and scalar field (8 limbs)
+
+
 def field_op(curve, which, op, a, b=None, field_id=None):
     n = a.shape[1]
-    out = np.zeros((8, n), np.uint32)
+    out = np.zeros((a.shape[0], n), np.uint32)
     fid = FIELD_IDS[(curve, which)] if field_id is None else field_id
     rc = lib().hs_field_op(fid, None, OPS[op], C.c_size_t(n), _p(a), _p(b), _p(out))
     assert rc == 0
@@ -98,3 +101,14 @@ def glv_split(k):
     m1, m2, sg = np.zeros((8, n), np.uint32), np.zeros((8, n), np.uint32), np.zeros(2 * n, np.uint8)
     assert lib().hs_glv_split(C.c_size_t(n), _p(k), _p(m1), _p(m2), _p(sg)) == 0
     return m1, m2, sg
+
+
+def bls_point_op(op, P, T=None, k=None):
+    """BLS12-381 G1 (12-limb Montgomery coordinates): op 'add' | 'dbl' | 'mul'."""
+    n = P[0].shape[1]
+    o = np.zeros((12, n), np.uint32), np.zeros((12, n), np.uint32), np.zeros(n, np.uint8)
+    T = T if T is not None else P
+    rc = lib().hs_bls_point_op({"add": 0, "dbl": 1, "mul": 2}[op], C.c_size_t(n), _p(k), _p(P[0]), _p(P[1]),
+                               _p(P[2]), _p(T[0]), _p(T[1]), _p(T[2]), _p(o[0]), _p(o[1]), _p(o[2]))
+    assert rc == 0, rc
+    return o
