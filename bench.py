@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="verify", choices=["verify", "sign", "padd", "msm"])
     ap.add_argument("--log2n", type=int, default=20)
+    ap.add_argument("--curve", default="secp256k1", choices=["secp256k1", "bls12_381"],
+                    help="bls12_381 (381-bit coordinates) is served by --workload msm only")
     ap.add_argument("--cpu-sample-log2", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -56,13 +58,28 @@ def parse():
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled DURING the timed region: NVML polled every 5 ms from a
+    thread (short timed regions still get samples), `nvidia-smi -lms` (the profiling recipe's
+    line) when the NVML binding is missing."""
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
-        self.rows, self.proc = [], None
+        self.rows, self.proc, self.nv = [], None, None
+        self.sm, self.mx, self.reasons, self.stop_flag = [], None, set(), False
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            self.h = nv.nvmlDeviceGetHandleByIndex(index)
+            self.mx = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.nv = nv
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
+        except Exception:
+            self.nv = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -72,11 +89,32 @@ class ClockSampler:
         except OSError:
             self.proc = None
 
+    def _poll(self):
+        nv = self.nv
+        get = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons")
+        bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
+        while not self.stop_flag:
+            try:
+                self.sm.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                r = int(get(self.h))
+                for nm, b in bits.items():
+                    if r & b:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
     def _read(self):
         for line in self.proc.stdout:
             self.rows.append([c.strip() for c in line.split(",")])
 
     def stop(self):
+        if self.nv is not None:
+            self.stop_flag = True
+            self.t.join(timeout=1)
+            return {"sm_mhz": statistics.median(self.sm) if self.sm else None, "sm_max_mhz": self.mx,
+                    "samples": len(self.sm), "reasons": sorted(self.reasons), "source": "nvml, 5 ms period"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -85,18 +123,17 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for r in self.rows:
             try:
                 sm.append(float(r[0]))
                 mx = float(r[1])
-                for nm, v in zip(names, r[3:7]):
+                for nm, v in zip(self.NAMES, r[3:7]):
                     if v.lower().startswith("active"):
                         reasons.add(nm)
             except (ValueError, IndexError):
                 pass
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "samples": len(sm), "reasons": sorted(reasons), "source": "nvidia-smi -lms 100"}
 
 
 # ----------------------------------------------------------------------------- CPU arm
@@ -187,13 +224,24 @@ SLOTS = {
 }
 
 
+def msm_products_per_point(kind):
+    """Executed field products per input point of the batch-affine MSM at 2^20 points (c = 16):
+    17 windows x (1 - 1/32) tree joins, each 5 mul + 1 sqr (denominator product, two unwind
+    products, lambda, lambda^2, y) plus its share of the block scan (14 products per thread of
+    16 / 16 / 8 / 4 / 2 / 2 joins on levels 0..5: 1.2 per join on average); then the three marginal
+    sums: 3 x 1.5 mixed Jacobian additions (8M + 3S) per BUCKET, 17 x 2^15 buckets."""
+    joins = 17 * (1 - 1 / 32)
+    madds = 3 * 1.5 * 17 * 2**15 / 2**20
+    return {f"mul_{kind}": joins * (5 + 1.2) + madds * 8, f"sqr_{kind}": joins * 1 + madds * 3}
+
+
 def work_per_lane(workload):
     with open(os.path.join(ROOT, "tools", "op_counts.json")) as f:
         counts = json.load(f)["secp256k1"]
     if workload == "padd":   # compress 1 + scatter 2 + chord 3 (one a square) + inversion share
         c = {"mul_special": 5 + 2 / 16, "sqr_special": 1, "safegcd_special": 1 / 16}
-    elif workload == "msm":  # 16 signed windows: one mixed addition (8M + 3S) per window and point
-        c = {"mul_special": 16 * 8.0, "sqr_special": 16 * 3.0}
+    elif workload == "msm":
+        c = msm_products_per_point("special")
     else:
         c = counts[workload]
     slots = sum(SLOTS[k] * v for k, v in c.items())
@@ -208,6 +256,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if args.impl == "reference":
         run_reference_arm(args, rank)
+        return
+    if args.curve == "bls12_381":
+        if args.workload != "msm":
+            raise SystemExit("bench.py: --curve bls12_381 serves --workload msm only")
+        bench_msm_bls(args, rank, local_rank, world)
         return
 
     import numpy as np
@@ -359,7 +412,7 @@ def main():
     achieved = mads / per_launch_s
     io_bytes = {"verify": 162, "sign": 132, "padd": 194, "msm": 96}[wl] * n
     roofline = {
-        "bound": "imad", "kernel": {"verify": "k_verify", "sign": "k_sign", "padd": "k_batch_padd", "msm": "k_msm_buckets"}[wl],
+        "bound": "imad", "kernel": {"verify": "k_verify", "sign": "k_sign", "padd": "k_batch_padd", "msm": "k_msm_tree_fwd/bwd"}[wl],
         "achieved": achieved / 1e12, "peak": peak_mad_per_s / 1e12, "unit": "T IMAD.WIDE-slot/s",
         "frac": achieved / peak_mad_per_s,
         "peak_source": "measured live: gecc_microbench(dependent IMAD.WIDE.U32), "
@@ -406,7 +459,7 @@ def main():
             "config": {"workload": {"verify": f"secp256k1 ECDSA verify, batch 2^{args.log2n} per GPU",
                                     "sign": f"secp256k1 ECDSA sign, batch 2^{args.log2n} per GPU",
                                     "padd": f"secp256k1 batched affine point addition, 2^{args.log2n} pairs per GPU",
-                                    "msm": f"secp256k1 Pippenger MSM, 2^{args.log2n} points per GPU (c = 16)"}[wl],
+                                    "msm": f"secp256k1 Pippenger MSM, 2^{args.log2n} points per GPU (c = 16, batch-affine buckets)"}[wl],
                        "curve": "secp256k1", "lanes_per_gpu": n, "sharding": f"lane ranges x{world}, no collective",
                        "l2": "inputs larger than L2 (records 161 B/lane x 2^20 = 169 MB > 126 MB)"
                        if wl == "verify" and args.log2n >= 20 else "no L2 flush; kernel is IMAD-bound, records read once"},
@@ -414,6 +467,120 @@ def main():
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def bench_msm_bls(args, rank, local_rank, world):
+    """BLS12-381 G1 MSM (12-limb coordinates, 255-bit scalars), device-resident.  Points are
+    i * G for i = 1 .. n, built on the GPU by doubling-and-adding whole arrays (batch_padd /
+    batch_pdbl); the gate before timing checks sum_i k_i (i G) = (sum_i k_i i mod r) G against
+    Python integers."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    import paper_2501_03245_b200 as gecc
+    from oracle import pyec as E   # equivalence gate only
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    B = E.BLS12_381
+    n = 1 << args.log2n
+    ctx = gecc.Context(gecc.BLS12_381, local_rank)
+    l = gecc.lib()
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    vp = lambda t: C.c_void_p(t.data_ptr())
+    R12 = 1 << 384
+    g = (gecc.cols_from_ints([B.gx * R12 % B.p], 12), gecc.cols_from_ints([B.gy * R12 % B.p], 12), np.zeros(1, np.uint8))
+    # [1..2^k - 1] G  ->  [1..2^(k+1) - 1] G  =  old, 2^k G, old + 2^k G
+    px, py = torch.from_numpy(g[0]).cuda().view(torch.int32), torch.from_numpy(g[1]).cuda().view(torch.int32)
+    base = (px.clone(), py.clone())
+    zero = lambda m: torch.zeros(m, dtype=torch.uint8, device="cuda")
+    col = lambda m: torch.empty((12, m), dtype=torch.int32, device="cuda")
+    for _ in range(args.log2n - 1):
+        m = px.shape[1]
+        bx, by = base[0].expand(12, m).contiguous(), base[1].expand(12, m).contiguous()
+        ox, oy, oi = col(m), col(m), zero(m)
+        assert l.gecc_batch_padd_dev(ctx.h, C.c_size_t(m), vp(px), vp(py), None, vp(bx), vp(by), None,
+                                     vp(ox), vp(oy), vp(oi)) == 0
+        px, py = torch.cat([px, base[0], ox], 1).contiguous(), torch.cat([py, base[1], oy], 1).contiguous()
+        nbx, nby, nbi = col(1), col(1), zero(1)
+        assert l.gecc_batch_pdbl_dev(ctx.h, C.c_size_t(1), vp(base[0]), vp(base[1]), None, vp(nbx), vp(nby), vp(nbi)) == 0
+        base = (nbx, nby)
+    torch.cuda.synchronize()
+    # the order above is not 1..n: recover each point's multiplier the same way
+    mult = np.array([1], dtype=object)
+    for k in range(args.log2n - 1):
+        mult = np.concatenate([mult, np.array([1 << k], dtype=object), mult + (1 << k)])
+    px = torch.cat([px, px[:, :1]], 1).contiguous()   # n - 1 points so far: repeat the first
+    py = torch.cat([py, py[:, :1]], 1).contiguous()
+    mult = np.concatenate([mult, mult[:1]])
+    assert px.shape[1] == n
+    rs = np.random.RandomState(4321 + rank)
+    hk = rs.randint(0, 2**32, size=(8, n), dtype=np.uint64).astype(np.uint32)
+    k = torch.from_numpy(hk).cuda()
+    pinf = zero(n)
+    ox, oy, oi = col(1), col(1), zero(1)
+    step = lambda: l.gecc_msm_dev(ctx.h, C.c_size_t(n), vp(k), vp(px), vp(py), vp(pinf), vp(ox), vp(oy), vp(oi))
+    assert step() == 0
+    torch.cuda.synchronize()
+    ks = gecc.ints_from_cols(hk)
+    total = sum((a % B.n) * int(b) for a, b in zip(ks, mult)) % B.n
+    want = E.ec_mul(B, total, B.G)
+    rinv = pow(R12, -1, B.p)
+    got = (gecc.ints_from_cols(ox.cpu().numpy().view(np.uint32))[0] * rinv % B.p,
+           gecc.ints_from_cols(oy.cpu().numpy().view(np.uint32))[0] * rinv % B.p)
+    assert int(oi.item()) == 0 and got == want, "BLS12-381 MSM gate failed"
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    sctx = gecc.Context(gecc.SECP256K1, local_rank)
+    peak = sctx.microbench(1, 3000)
+    sctx.close()
+    peak_mad_per_s = peak["total_ops"] / peak["seconds"]
+    for _ in range(args.warmup):
+        assert step() == 0
+    barrier()
+    sampler = ClockSampler(local_rank)
+    launches0 = ctx.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        assert step() == 0
+    ev1.record(stream)
+    barrier()
+    dev_s = ev0.elapsed_time(ev1) * 1e-3
+    if world > 1:
+        t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_s = float(t.item())
+    clocks = sampler.stop()
+    per = dev_s / args.steps
+    counts = msm_products_per_point("generic12")
+    # 12-limb generic Montgomery product: 144 (product) + 78 (low product) + 144 (m * q) wide multiplies
+    slots = {"mul_generic12": 144 + 78 + 144, "sqr_generic12": 78 + 78 + 144}
+    mads = n * sum(slots[kk] * v for kk, v in counts.items())
+    if rank == 0:
+        print(json.dumps({
+            "metric": "msm_time", "value": per * 1e3, "unit": "ms per MSM", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u32 limbs (381-bit modular integer, 12 limbs)", "data": "synthetic",
+            "config": {"workload": f"BLS12-381 G1 Pippenger MSM, 2^{args.log2n} points per GPU (c = 16, batch-affine buckets)",
+                       "curve": "bls12_381", "lanes_per_gpu": n, "sharding": f"point ranges x{world}",
+                       "l2": "no L2 flush; scalars + points 2^20 x 128 B = 134 MB > 126 MB L2"},
+            "clocks": clocks, "e2e": None, "gpu_launches": ctx.launches - launches0,
+            "roofline": {"bound": "imad", "kernel": "k_msm_tree_fwd/bwd", "achieved": mads / per / 1e12,
+                         "peak": peak_mad_per_s / 1e12, "unit": "T IMAD.WIDE-slot/s", "frac": mads / per / peak_mad_per_s,
+                         "work_per_lane": {"executed": counts, "slots_per_op": slots}, "traffic": None},
+            "cpu_baseline": None}), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
