@@ -405,6 +405,33 @@ def main():
                "ms_per_step": e2e_s / args.steps * 1e3,
                "api": "sm2b_verify" if wl == "verify" else "gecc_sign", "host_buffers": "pinned"}
 
+    if wl in ("padd", "msm"):
+        hP = tuple(pin(np.ascontiguousarray(t.cpu().numpy().view(np.uint32 if i < 2 else np.uint8))) for i, t in enumerate(P))
+        hT = tuple(pin(np.ascontiguousarray(t.cpu().numpy().view(np.uint32 if i < 2 else np.uint8))) for i, t in enumerate(T))
+        hk = pin(k2.cpu().numpy())
+        m_out = n if wl == "padd" else 1
+        hO = (torch.empty((8, m_out), dtype=torch.int32).pin_memory(), torch.empty((8, m_out), dtype=torch.int32).pin_memory(),
+              torch.empty(m_out, dtype=torch.uint8).pin_memory())
+        if wl == "padd":
+            call = lambda: l.gecc_batch_padd(ctx.h, C.c_size_t(n), vp(hP[0]), vp(hP[1]), vp(hP[2]), vp(hT[0]), vp(hT[1]),
+                                             vp(hT[2]), vp(hO[0]), vp(hO[1]), vp(hO[2]))
+            h2d, d2h, api = 130 * n, 65 * n, "gecc_batch_padd"
+        else:
+            call = lambda: l.gecc_msm(ctx.h, C.c_size_t(n), vp(hk), vp(hP[0]), vp(hP[1]), vp(hP[2]),
+                                      vp(hO[0]), vp(hO[1]), vp(hO[2]))
+            h2d, d2h, api = 97 * n, 65, "gecc_msm"
+        for _ in range(max(1, args.warmup // 2)):
+            assert call() == 0
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            assert call() == 0
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": world * n * args.steps / e2e_s if wl == "padd" else e2e_s / args.steps * 1e3, "unit": UNIT[wl],
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s / args.steps * 1e3,
+               "api": api, "host_buffers": "pinned"}
+
     # ---- roofline of the dominant kernel (the only kernel in the step)
     per_launch_s = dev_s / args.steps
     counts, slots_per_lane, products_per_lane = work_per_lane(wl)
@@ -449,6 +476,32 @@ def main():
         cpu = {"value": m / dt, "unit": UNIT[wl], "cores": cores, "kind": kind,
                "sample": f"first {m} lanes of the timed batch, one call, outputs compared with the GPU's",
                "seconds": dt}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and wl in ("padd", "msm"):
+        from oracle import refshim as R
+        if R.available():
+            m = min(n, 1 << (16 if wl == "padd" else 11))
+            cut = lambda t, w: np.ascontiguousarray(t.cpu().numpy().view(w)[..., :m])
+            cP = (cut(P[0], np.uint32), cut(P[1], np.uint32), cut(P[2], np.uint8))
+            if wl == "padd":   # the reference's batch_padd on all host threads, 2^16 pairs, median of 5
+                cT = (cut(T[0], np.uint32), cut(T[1], np.uint32), cut(T[2], np.uint8))
+                dt = R.batch_padd_timed(SECP, cP, cT, lanes=0, workers=0, repeats=5)
+                want = R.batch_padd(SECP, cP, cT, lanes=0, workers=0)
+                got = (cut(S[0], np.uint32), cut(S[1], np.uint32), cut(S[2], np.uint8)) if e2e is None else \
+                    tuple(np.ascontiguousarray(t.numpy().view(w)[..., :m]) for t, w in zip(hO, (np.uint32, np.uint32, np.uint8)))
+                assert all((a == b).all() for a, b in zip(want, got)), "CPU reference batch_padd differs from the GPU's"
+                cpu = {"value": m / dt, "unit": UNIT[wl], "cores": os.cpu_count(), "kind": "reference",
+                       "sample": f"first {m} pairs of the timed batch, median of 5, outputs compared with the GPU's",
+                       "seconds": dt}
+            else:   # the reference has no MSM: its serial scalar multiplication (pmul_serial) summed, 2^11 terms
+                ck = np.ascontiguousarray(k2.cpu().numpy()[..., :m])
+                t0 = time.perf_counter()
+                R.pmul_serial(SECP, ck, cP)
+                dt = time.perf_counter() - t0
+                cpu = {"value": dt * (n / m) * 1e3, "unit": UNIT[wl], "cores": 1, "kind": "reference",
+                       "sample": f"reference pmul_serial over the first {m} terms ({dt:.2f} s), scaled by {n // m} to 2^{args.log2n} "
+                                 "terms; the reference has no MSM, this is the definition it would run",
+                       "seconds": dt}
 
     if rank == 0:
         line = {
