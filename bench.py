@@ -645,7 +645,8 @@ def _ncu_traffic(wl):
     For k_verify it is well above the 170 MB of records: the excess is per-thread stack
     (2 KB x 2^20 lanes of local memory written back from L1), not re-reads of the inputs."""
     import csv
-    name = {"verify": "r01e_verify_globaltab", "padd": "r01_padd", "msm": "r01_msm"}.get(wl)
+    name, kernel = {"verify": ("r01i_verify", "k_verify_gtab"), "padd": ("r01_padd", "k_batch_padd"),
+                    "msm": ("r01g_msm_tree", "k_msm_tree_bwd")}.get(wl, (None, None))  # msm: the level-0 unwind kernel
     if not name:
         return None
     try:
@@ -653,9 +654,9 @@ def _ncu_traffic(wl):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         with open(os.path.join(ROOT, "profiles", name + "_metrics.csv")) as f:
             for r in csv.reader(f):
-                if len(r) >= 4 and r[1] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                if len(r) >= 4 and kernel in r[0] and r[1] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                     tot += float(r[3]) * scale.get(r[2], 1)
-        return {"bytes_per_launch": tot, "source": f"profiles/{name}_metrics.csv"} if tot else None
+        return {"bytes_per_launch": tot, "kernel": kernel, "source": f"profiles/{name}_metrics.csv"} if tot else None
     except OSError:
         return None
 
