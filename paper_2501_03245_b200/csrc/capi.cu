@@ -57,6 +57,7 @@ struct sm2b_ctx {
     uint32_t* gtab_rec = nullptr;  // table of the byte-record kernels (== gtab on SM2, plain form on secp256k1)
     uint32_t* flags = nullptr;  // device word: malformed-call flag of sign / ecdh
     int limbs = 8;              // 32-bit limbs per coordinate (12 on BLS12-381)
+    uint32_t* hflag = nullptr;  // pinned host word: the flag comes back without blocking the enqueueing thread
 };
 
 namespace {
@@ -137,6 +138,10 @@ sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device) {
     }
     ctx->sm_count = prop.multiProcessorCount;
     ctx->stream = ctx->own_stream;
+    if (cudaHostAlloc((void**)&ctx->hflag, 64, cudaHostAllocDefault) != cudaSuccess) {
+        sm2b_ctx_free(ctx);
+        return nullptr;
+    }
     if (ctx->curve == CURVE_BLS381) {  // field / batch / MSM layer only: no ECDSA, no fixed-base table
         if (cudaMalloc(&ctx->flags, 256) != cudaSuccess) {
             sm2b_ctx_free(ctx);
@@ -188,6 +193,7 @@ void sm2b_ctx_free(sm2b_ctx* ctx) {
         if (ctx->gtab_rec && ctx->gtab_rec != ctx->gtab) cudaFree(ctx->gtab_rec);
         if (ctx->gtab) cudaFree(ctx->gtab);
         if (ctx->flags) cudaFree(ctx->flags);
+        if (ctx->hflag) cudaFreeHost(ctx->hflag);
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
         if (ctx->h2d_stream) cudaStreamDestroy(ctx->h2d_stream);
         if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
@@ -519,41 +525,62 @@ sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const
     cudaEvent_t idle = pool.get();
     CU(ctx, cudaEventRecord(idle, ctx->stream));
     CU(ctx, cudaStreamWaitEvent(ctx->h2d_stream, idle, 0));
+    CU(ctx, cudaStreamWaitEvent(ctx->d2h_stream, idle, 0));
     CU(ctx, cudaMemsetAsync(ctx->flags, 0, 4, ctx->h2d_stream));
     // A zero or oversize secret must fail the whole call before any output is written
-    // (capi.cpp:181-184), so signatures are only copied out after every chunk's kernel has
-    // run and the flag is known; the uploads and kernels still overlap chunk by chunk.
+    // (capi.cpp:181-184).  Chunk 0 goes up first and starts signing; all remaining secrets follow
+    // and are range-checked by a tiny kernel while chunk 0 runs, so the verdict is known about
+    // when the first signatures are ready.  From then on it is a three-stream pipeline: H2D of
+    // the digests of chunk c+1, the kernel of chunk c, D2H of the signatures of chunk c-1.
+    std::vector<cudaEvent_t> done(ch.n);
+    cudaEvent_t verdict = pool.get();
+    *ctx->hflag = 0;
     for (int c = 0; c < ch.n; ++c) {
         const size_t b = ch.begin(c), m = ch.len(c);
-        CU(ctx, cudaMemcpyAsync(dsec + 32 * b, secrets + 32 * b, 32 * m, cudaMemcpyHostToDevice, ctx->h2d_stream));
+        if (c == 0) CU(ctx, cudaMemcpyAsync(dsec, secrets, 32 * m, cudaMemcpyHostToDevice, ctx->h2d_stream));
         CU(ctx, cudaMemcpyAsync(dd + 32 * b, digests + 32 * b, 32 * m, cudaMemcpyHostToDevice, ctx->h2d_stream));
         cudaEvent_t up = pool.get();
         CU(ctx, cudaEventRecord(up, ctx->h2d_stream));
         CU(ctx, cudaStreamWaitEvent(ctx->stream, up, 0));
         CU(ctx, launch_sign(ctx->curve, m, dd + 32 * b, dsec + 32 * b, nonce_seed, lane_base + b, ctx->gtab_rec,
                             dsig + 64 * b, dst + b, ctx->flags, ctx->stream));
+        done[c] = pool.get();
+        CU(ctx, cudaEventRecord(done[c], ctx->stream));
+        if (c == 0) {  // the rest of the secrets, their check, the verdict
+            if (count > m) {
+                CU(ctx, cudaMemcpyAsync(dsec + 32 * m, secrets + 32 * m, 32 * (count - m), cudaMemcpyHostToDevice,
+                                        ctx->h2d_stream));
+                cudaEvent_t sec_up = pool.get();
+                CU(ctx, cudaEventRecord(sec_up, ctx->h2d_stream));
+                CU(ctx, cudaStreamWaitEvent(ctx->stream, sec_up, 0));
+                CU(ctx, launch_secret_range(ctx->curve, count - m, dsec + 32 * m, ctx->flags, ctx->stream));
+            }
+            CU(ctx, cudaMemcpyAsync(ctx->hflag, ctx->flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
+            CU(ctx, cudaEventRecord(verdict, ctx->stream));
+        }
     }
-    ctx->launches += ch.n;
+    ctx->launches += ch.n + 1;
     led_fpmul(ledger_of(ctx), count);
     led_invert(ledger_of(ctx), count);
     led(ledger_of(ctx), 2 * count, count, 0, 0);
-    uint32_t flag = 0;
-    CU(ctx, cudaMemcpyAsync(&flag, ctx->flags, 4, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaStreamSynchronize(ctx->stream));
-    if (flag) return SM2B_ERROR_MALFORMED_INPUT;
-    // two copy streams keep the D2H engine busy with large transfers; per-lane statuses go
-    // straight into the caller's array (no host-side pass over the lanes)
-    const size_t half = count / 2;
+    CU(ctx, cudaEventSynchronize(verdict));
+    if (*ctx->hflag) {  // nothing has been copied out; let the queued kernels drain
+        CU(ctx, cudaStreamSynchronize(ctx->stream));
+        return SM2B_ERROR_MALFORMED_INPUT;
+    }
+    // per-lane statuses go straight into the caller's array (no host-side pass over the lanes)
     std::vector<int32_t> hst;
     int32_t* st_dst = lane_status;
     if (!st_dst) {
         hst.resize(count);
         st_dst = hst.data();
     }
-    CU(ctx, cudaMemcpyAsync(signatures, dsig, 64 * half, cudaMemcpyDeviceToHost, ctx->d2h_stream));
-    CU(ctx, cudaMemcpyAsync(signatures + 64 * half, dsig + 64 * half, 64 * (count - half), cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    CU(ctx, cudaMemcpyAsync(st_dst, dst, 4 * count, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    for (int c = 0; c < ch.n; ++c) {
+        const size_t b = ch.begin(c), m = ch.len(c);
+        CU(ctx, cudaStreamWaitEvent(ctx->d2h_stream, done[c], 0));
+        CU(ctx, cudaMemcpyAsync(signatures + 64 * b, dsig + 64 * b, 64 * m, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+        CU(ctx, cudaMemcpyAsync(st_dst + b, dst + b, 4 * m, cudaMemcpyDeviceToHost, ctx->d2h_stream));
+    }
     CU(ctx, cudaStreamSynchronize(ctx->d2h_stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     if (lane_status) return SM2B_OK;  // report_lanes (capi.cpp:64-73): statuses delivered, call is OK

@@ -31,6 +31,7 @@ size_t verify_scratch_bytes(size_t lanes);
 cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t* pub,
                           const uint8_t* sig, const uint32_t* gtab, uint8_t* res,
                           uint32_t* lane_scratch, size_t scratch_lanes, cudaStream_t s);
+cudaError_t launch_secret_range(int curve, size_t n, const uint8_t* sec, uint32_t* flags, cudaStream_t s);
 cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed,
                         uint64_t lane_base, const uint32_t* gtab, uint8_t* sig, int32_t* status,
                         uint32_t* flags, cudaStream_t s);

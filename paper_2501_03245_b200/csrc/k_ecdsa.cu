@@ -84,6 +84,17 @@ k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ se
     }
 }
 
+// Range check of all secrets of a call (capi.cpp:181-184: one bad secret fails the WHOLE call
+// before any output is written).  Run right after the secrets are uploaded, so that the host
+// knows the verdict early and can stream the signatures out while later chunks still sign.
+template <class C>
+__global__ void __launch_bounds__(256)
+k_secret_range(size_t n, const uint8_t* __restrict__ sec, uint32_t* __restrict__ flags) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (!scalar_in_range<typename C::Fn>(be32_load(sec + 32 * i))) atomicOr(flags, 1u);
+}
+
 // capi.cpp:145-169: secret = nonce stream (lane, attempt 0), public = secret * G
 template <class C>
 __global__ void __launch_bounds__(SIGN_THREADS)
@@ -299,6 +310,14 @@ cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t
         }
 #undef VERIFY_GTAB_
     }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_secret_range(int curve, size_t n, const uint8_t* sec, uint32_t* flags, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    const unsigned b = (unsigned)((n + 255) / 256);
+    if (curve == CURVE_SECP) k_secret_range<SecpEcdsaCurve><<<b, 256, 0, s>>>(n, sec, flags);
+    else k_secret_range<Sm2Curve><<<b, 256, 0, s>>>(n, sec, flags);
     return cudaGetLastError();
 }
 
