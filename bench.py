@@ -325,6 +325,12 @@ def main():
         l.gecc_batch_fpmul_dev(ctx.h, C.c_size_t(n), vp(k2), vp(T[0]), vp(T[1]), vp(T[2]))
         torch.cuda.synchronize()
 
+    if wl == "msm" and world > 1:
+        msm_parts = torch.empty(world * 17, dtype=torch.int32, device="cuda")
+        one = lambda: (torch.empty((8, 1), dtype=torch.int32, device="cuda"),
+                       torch.empty((8, 1), dtype=torch.int32, device="cuda"), u8(1))
+        msm_acc, msm_out = one(), one()
+
     def step_dev():
         if wl == "verify":
             return l.gecc_verify_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_pub), vp(d_sig), vp(d_res))
@@ -332,8 +338,28 @@ def main():
             return l.gecc_sign_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_sec), C.c_uint64(7),
                                    C.c_uint64(lane_base), vp(d_sig), vp(d_st))
         if wl == "msm":   # sum_i k2_i * P_i, one point out
-            return l.gecc_msm_dev(ctx.h, C.c_size_t(n), vp(k2), vp(P[0]), vp(P[1]), vp(P[2]),
-                                  vp(S[0]), vp(S[1]), vp(S[2]))
+            rc = l.gecc_msm_dev(ctx.h, C.c_size_t(n), vp(k2), vp(P[0]), vp(P[1]), vp(P[2]),
+                                vp(S[0]), vp(S[1]), vp(S[2]))
+            if world == 1 or rc != 0:
+                return rc
+            # sharded MSM: every rank summed its own point range; ONE small all_gather of
+            # the partial sums (17 words per rank over NVLink), then world-1 local additions
+            # (EC addition is not an NCCL reduction operator)
+            mine = torch.cat([S[0].view(-1)[:8], S[1].view(-1)[:8], S[2].view(-1)[:1].to(torch.int32)])
+            dist.all_gather_into_tensor(msm_parts, mine)
+            parts = msm_parts.view(world, 17)
+            ax, ay, ai = msm_acc
+            ax.copy_(parts[0, :8].view(8, 1)); ay.copy_(parts[0, 8:16].view(8, 1)); ai.copy_(parts[0, 16:].to(torch.uint8))
+            for r in range(1, world):
+                bx = parts[r, :8].contiguous().view(8, 1)
+                by = parts[r, 8:16].contiguous().view(8, 1)
+                bi = parts[r, 16:].to(torch.uint8)
+                rc = l.gecc_batch_padd_dev(ctx.h, C.c_size_t(1), vp(ax), vp(ay), vp(ai), vp(bx), vp(by), vp(bi),
+                                           vp(msm_out[0]), vp(msm_out[1]), vp(msm_out[2]))
+                if rc != 0:
+                    return rc
+                ax.copy_(msm_out[0]); ay.copy_(msm_out[1]); ai.copy_(msm_out[2])
+            return 0
         return l.gecc_batch_padd_dev(ctx.h, C.c_size_t(n), vp(P[0]), vp(P[1]), vp(P[2]), vp(T[0]),
                                      vp(T[1]), vp(T[2]), vp(S[0]), vp(S[1]), vp(S[2]))
 
@@ -513,7 +539,9 @@ def main():
                                     "sign": f"secp256k1 ECDSA sign, batch 2^{args.log2n} per GPU",
                                     "padd": f"secp256k1 batched affine point addition, 2^{args.log2n} pairs per GPU",
                                     "msm": f"secp256k1 Pippenger MSM, 2^{args.log2n} points per GPU (c = 16, batch-affine buckets)"}[wl],
-                       "curve": "secp256k1", "lanes_per_gpu": n, "sharding": f"lane ranges x{world}, no collective",
+                       "curve": "secp256k1", "lanes_per_gpu": n,
+                       "sharding": (f"point ranges x{world}, one all_gather of the partial sums + {world - 1} local additions"
+                                    if wl == "msm" and world > 1 else f"lane ranges x{world}, no collective"),
                        "l2": "inputs larger than L2 (records 161 B/lane x 2^20 = 169 MB > 126 MB)"
                        if wl == "verify" and args.log2n >= 20 else "no L2 flush; kernel is IMAD-bound, records read once"},
             "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,

@@ -108,7 +108,7 @@ GECC_HD_CALL cjac<C> jac_dbl(const cjac<C>& p) {
         fe E = fe_add(f, fe_dbl(f, A), A);      // 3A
         fe F = fe_sqr(f, E);
         r.X = fe_sub(f, F, fe_dbl(f, D));
-        fe C8 = fe_dbl(f, fe_dbl(f, fe_dbl(f, Cc)));
+        fe C8 = fe_mul8(f, Cc);
         r.Y = fe_sub(f, fe_mul(f, E, fe_sub(f, D, r.X)), C8);
         r.Z = fe_dbl(f, fe_mul(f, p.Y, p.Z));
     } else if (C::a_kind == A_MINUS3) {
@@ -122,7 +122,7 @@ GECC_HD_CALL cjac<C> jac_dbl(const cjac<C>& p) {
         fe yz = fe_add(f, p.Y, p.Z);
         r.Z = fe_sub(f, fe_sub(f, fe_sqr(f, yz), gamma), delta);
         fe g2 = fe_sqr(f, gamma);
-        fe g8 = fe_dbl(f, fe_dbl(f, fe_dbl(f, g2)));
+        fe g8 = fe_mul8(f, g2);
         r.Y = fe_sub(f, fe_mul(f, alpha, fe_sub(f, beta4, r.X)), g8);
     } else {
         fe yy = fe_sqr(f, p.Y);

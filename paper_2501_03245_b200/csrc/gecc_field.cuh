@@ -132,19 +132,50 @@ GECC_HD bool lazy_is_zero(const F& f, const fe& a) {
     }
     return z == 0 || e == 0;
 }
-// r = (carry : a) folded once more: a + carry * c, with the (rare) second wrap handled
+// r = (carry : a) folded once more: a + carry * c (carry is 0 or 1).  Only the two low limbs
+// change unless the addition carries out of limb 1 (probability ~2^-31): the ripple through
+// limbs 2..7 and the (rarer still) second wrap sit behind a branch no warp normally takes.
 GECC_HD fe lazy_fold_carry(const fe& a, uint32_t carry) {
-    fe r;
-    r.w[0] = add_cc(a.w[0], carry * 977u);
+    fe r = a;
+    const uint32_t m = 0u - carry;
+    r.w[0] = add_cc(a.w[0], m & 977u);
     r.w[1] = addc_cc(a.w[1], carry);
+    if (addc(0, 0)) {
+        r.w[2] = add_cc(a.w[2], 1u);
 #pragma unroll
-    for (int i = 2; i < 8; ++i) r.w[i] = addc_cc(a.w[i], 0);
-    const uint32_t again = addc(0, 0);
-    if (again) {  // only when a >= 2^256 - c: the wrapped value is below c, adding c cannot wrap
-        r.w[0] = add_cc(r.w[0], 977u);
-        r.w[1] = addc_cc(r.w[1], 1u);
+        for (int i = 3; i < 8; ++i) r.w[i] = addc_cc(a.w[i], 0);
+        if (addc(0, 0)) {  // only when a >= 2^256 - c: the wrapped value is below c, adding c cannot wrap
+            r.w[0] = add_cc(r.w[0], 977u);
+            r.w[1] = addc_cc(r.w[1], 1u);
 #pragma unroll
-        for (int i = 2; i < 8; ++i) r.w[i] = addc_cc(r.w[i], 0);
+            for (int i = 2; i < 8; ++i) r.w[i] = addc_cc(r.w[i], 0);
+        }
+    }
+    return r;
+}
+// (a << K) mod q for K = 1..3, weakly reduced: funnel shifts (no carry chain) and the K bits
+// shifted out folded back as t * c, t < 8.
+template <int K>
+GECC_HD fe lazy_shl(const fe& a) {
+    static_assert(K >= 1 && K <= 3, "small shifts only");
+    const uint32_t t = a.w[7] >> (32 - K);
+    fe r;
+    r.w[0] = a.w[0] << K;
+#pragma unroll
+    for (int i = 1; i < 8; ++i) r.w[i] = (a.w[i] << K) | (a.w[i - 1] >> (32 - K));
+    const uint32_t lo = r.w[0], hi = r.w[1];
+    r.w[0] = add_cc(lo, t * 977u);
+    r.w[1] = addc_cc(hi, t);
+    if (addc(0, 0)) {  // carry out of limb 1: rare
+        r.w[2] = add_cc(r.w[2], 1u);
+#pragma unroll
+        for (int i = 3; i < 8; ++i) r.w[i] = addc_cc(r.w[i], 0);
+        if (addc(0, 0)) {  // wrapped past 2^256: what is left is below t * c, one more c cannot wrap
+            r.w[0] = add_cc(r.w[0], 977u);
+            r.w[1] = addc_cc(r.w[1], 1u);
+#pragma unroll
+            for (int i = 2; i < 8; ++i) r.w[i] = addc_cc(r.w[i], 0);
+        }
     }
     return r;
 }
@@ -161,17 +192,19 @@ GECC_HD fe lazy_sub(const fe& a, const fe& b) {
 #pragma unroll
     for (int i = 1; i < 8; ++i) d.w[i] = subc_cc(a.w[i], b.w[i]);
     const uint32_t k = subc(0, 0) & 1u;  // borrowed: d = a - b + 2^256 == a - b + c, so take c off
-    fe r;
-    r.w[0] = sub_cc(d.w[0], k * 977u);
+    fe r = d;
+    r.w[0] = sub_cc(d.w[0], (0u - k) & 977u);
     r.w[1] = subc_cc(d.w[1], k);
+    if (subc(0, 0)) {  // borrow out of limb 1 (probability ~2^-31): ripple, and the rarer second wrap
+        r.w[2] = sub_cc(d.w[2], 1u);
 #pragma unroll
-    for (int i = 2; i < 8; ++i) r.w[i] = subc_cc(d.w[i], 0);
-    const uint32_t again = subc(0, 0);
-    if (again) {  // only when d < c: wrapped once more, take c off again (cannot wrap a third time)
-        r.w[0] = sub_cc(r.w[0], 977u);
-        r.w[1] = subc_cc(r.w[1], 1u);
+        for (int i = 3; i < 8; ++i) r.w[i] = subc_cc(d.w[i], 0);
+        if (subc(0, 0)) {  // only when d < c: wrapped once more, take c off again (cannot wrap a third time)
+            r.w[0] = sub_cc(r.w[0], 977u);
+            r.w[1] = subc_cc(r.w[1], 1u);
 #pragma unroll
-        for (int i = 2; i < 8; ++i) r.w[i] = subc_cc(r.w[i], 0);
+            for (int i = 2; i < 8; ++i) r.w[i] = subc_cc(r.w[i], 0);
+        }
     }
     return r;
 }
@@ -219,11 +252,11 @@ GECC_HD fe redc_secp_lazy(const uint32_t* t) {
 #pragma unroll
     for (int i = 2; i < 8; ++i) r.w[i] = addc_cc(r.w[i], 0);
     carry = addc(carry, 0);  // total carry is 0 or 1 (w < 2^256 + 2^67)
-    // w >= 2^256 leaves a tiny remainder, so adding c cannot wrap again
-    r.w[0] = add_cc(r.w[0], carry * 977u);
+    // w >= 2^256 leaves a tiny remainder (below 2^67), so adding c touches limbs 0..2 only and
+    // cannot wrap again
+    r.w[0] = add_cc(r.w[0], (0u - carry) & 977u);
     r.w[1] = addc_cc(r.w[1], carry);
-#pragma unroll
-    for (int i = 2; i < 8; ++i) r.w[i] = addc_cc(r.w[i], 0);
+    r.w[2] = addc(r.w[2], 0);
     return r;
 }
 
@@ -276,7 +309,13 @@ GECC_HD fel<F> fe_neg(const F& f, const fel<F>& a) {
 }
 template <class F>
 GECC_HD fel<F> fe_dbl(const F& f, const fel<F>& a) {
-    return fe_add(f, a, a);
+    if constexpr (F::kind == KIND_SECP_LAZY) return lazy_shl<1>(a);
+    else return fe_add(f, a, a);
+}
+template <class F>
+GECC_HD fel<F> fe_mul8(const F& f, const fel<F>& a) {  // 8 a
+    if constexpr (F::kind == KIND_SECP_LAZY) return lazy_shl<3>(a);
+    else return fe_dbl(f, fe_dbl(f, fe_dbl(f, a)));
 }
 
 // ---------------------------------------------------------------- products

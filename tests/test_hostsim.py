@@ -130,6 +130,28 @@ def test_hostsim_lazy_secp_field():
         assert all(g % p == fn(x, y) % p for g, x, y in zip(got, a, b)), op
     canon = O.cols_to_ints(H.field_op(1, 0, "from_mont", A, field_id=H.SECP_LAZY_FIELD))
     assert canon == [x % p for x in a]
+    # doubling / x8 by funnel shifts: edge values whose shifted-out bits and low limbs hit the
+    # rare carry branches, on the lazy field and (as add chains) on the Montgomery field
+    sh = edge_vals = special + [2**256 - 2**32, 2**255 + 2**64 - 1, (7 << 253) | (2**64 - 1), (7 << 253) | (2**64 - 978),
+                                2**256 - 2**61, (1 << 253) - 1, 0xFFFFFFFF << 32, (0xE0000000 << 224) | (2**256 - 1) >> 35]
+    sh = sh + [rng.randrange(1 << 256) for _ in range(2000)]
+    SH = O.ints_to_cols(sh)
+    for op, kk in (("dbl", 2), ("mul8", 8)):
+        got = O.cols_to_ints(H.field_op(1, 0, op, SH, field_id=H.SECP_LAZY_FIELD))
+        assert all(g % p == kk * x % p and g < (1 << 256) for g, x in zip(got, sh)), op
+        canon_in = O.ints_to_cols([x % p for x in sh])
+        got = O.cols_to_ints(H.field_op(1, 0, op, canon_in))
+        assert got == [kk * x % p for x in sh], op
+    # every pair of edge values: drives the rare branches of the folds (carry / borrow rippling
+    # out of limb 1, and the second wrap at a >= 2^256 - c or d < c)
+    edge = special + [2**64 - 1, 2**64, 2**64 - 977, 2**256 - 2**64, 2**256 - 2**64 + 1, 977, 976, 2**32 + 977,
+                      2**32 + 976, 2**256 - 2**32 - 978, (1 << 256) - (1 << 33), 2**96 - 1]
+    xa = [x for x in edge for _ in edge]
+    xb = [y for _ in edge for y in edge]
+    XA, XB = O.ints_to_cols(xa), O.ints_to_cols(xb)
+    for op, fn in (("mont_mul", lambda x, y: x * y), ("mod_add", lambda x, y: x + y), ("mod_sub", lambda x, y: x - y)):
+        got = O.cols_to_ints(H.field_op(1, 0, op, XA, XB, field_id=H.SECP_LAZY_FIELD))
+        assert all(g % p == fn(x, y) % p for g, x, y in zip(got, xa, xb)), op
     inv = O.cols_to_ints(H.field_op(1, 0, "inv_safegcd", np.ascontiguousarray(A[:, :400]), field_id=H.SECP_LAZY_FIELD))
     assert all((g * x) % p == 1 if x % p else g == 0 for g, x in zip(inv, a[:400]))
 
