@@ -329,8 +329,19 @@ GECC_HD void mul_wide_n(uint32_t* t, const uint32_t* a, const uint32_t* b) {
     uint32_t e[2 * N], o[2 * N];
 #pragma unroll
     for (int k = 0; k < 2 * N; ++k) e[k] = o[k] = 0;
+    {   // row 0 meets only zeros: plain wide products, no carry chain
+        const uint32_t b0 = b[0];
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
+        for (int j = 0; j < N; j += 2) {
+            const uint64_t pe = (uint64_t)a[j] * b0, po = (uint64_t)a[j + 1] * b0;
+            e[j] = (uint32_t)pe;
+            e[j + 1] = (uint32_t)(pe >> 32);
+            o[j] = (uint32_t)po;
+            o[j + 1] = (uint32_t)(po >> 32);
+        }
+    }
+#pragma unroll
+    for (int i = 1; i < N; ++i) {
         const uint32_t bi = b[i];
         if ((i & 1) == 0) {
             e[i] = mad_lo_cc(a[0], bi, e[i]);
