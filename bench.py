@@ -34,7 +34,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-SECP = 1
+SECP = 1          # curve id of the oracle / reference shim; --curve sm2 switches it to 0 (the reference's own curve)
 METRIC = {"verify": "ecdsa_verify_throughput", "sign": "ecdsa_sign_throughput",
           "padd": "batch_padd_throughput", "msm": "msm_time"}
 UNIT = {"verify": "verifications/s", "sign": "signatures/s", "padd": "point additions/s",
@@ -49,8 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="verify", choices=["verify", "sign", "padd", "msm"])
     ap.add_argument("--log2n", type=int, default=20)
-    ap.add_argument("--curve", default="secp256k1", choices=["secp256k1", "bls12_381"],
-                    help="bls12_381 (381-bit coordinates) is served by --workload msm only")
+    ap.add_argument("--curve", default="secp256k1", choices=["secp256k1", "sm2", "bls12_381"],
+                    help="sm2 = the reference's own curve; bls12_381 (381-bit coordinates) is served by --workload msm only")
     ap.add_argument("--cpu-sample-log2", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -169,7 +169,13 @@ def make_records_cpu(n, seed=1):
     return dig, sec, pub, sig
 
 
+def set_curve(args):
+    global SECP
+    SECP = 0 if args.curve == "sm2" else 1
+
+
 def run_reference_arm(args, rank):
+    set_curve(args)
     if rank != 0:
         return
     wl = args.workload if args.workload != "padd" else "verify"
@@ -196,12 +202,13 @@ def run_reference_arm(args, rank):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u32 limbs (256-bit modular integer)", "data": "synthetic",
-        "config": {"workload": f"secp256k1 ECDSA {wl}, batch 2^{args.log2n} per GPU",
-                   "curve": "secp256k1", "cpu_sample_lanes_per_step": n},
+        "config": {"workload": f"{args.curve} ECDSA {wl}, batch 2^{args.log2n} per GPU",
+                   "curve": args.curve, "cpu_sample_lanes_per_step": n},
         "cpu_baseline": {"value": value, "unit": UNIT[wl], "cores": cores, "kind": kind,
                          "sample": f"2^{log2} lanes per step of the same synthetic recipe; "
-                                   "reference batch kernels (batch_fpmul/upmul/padd/invert) "
-                                   "driven by the restated secp256k1 protocol glue"},
+                                   "reference batch kernels (batch_fpmul/upmul/padd/invert) driven by "
+                                   + ("the protocol glue that is checked equal to the reference's sm2b_sign / sm2b_verify"
+                                      if args.curve == "sm2" else "the restated secp256k1 protocol glue")},
         "e2e": {"value": value, "unit": UNIT[wl], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -235,16 +242,19 @@ def msm_products_per_point(kind):
     return {f"mul_{kind}": joins * (5 + 1.2) + madds * 8, f"sqr_{kind}": joins * 1 + madds * 3}
 
 
-def work_per_lane(workload):
+def work_per_lane(workload, curve="secp256k1"):
     with open(os.path.join(ROOT, "tools", "op_counts.json")) as f:
-        counts = json.load(f)["secp256k1"]
+        counts = json.load(f)[curve]
     if workload == "padd":   # compress 1 + scatter 2 + chord 3 (one a square) + inversion share
         c = {"mul_special": 5 + 2 / 16, "sqr_special": 1, "safegcd_special": 1 / 16}
     elif workload == "msm":
         c = msm_products_per_point("special")
     else:
         c = counts[workload]
-    slots = sum(SLOTS[k] * v for k, v in c.items())
+    table = dict(SLOTS)
+    if curve == "sm2":   # SM2 p: the reduction is additions and subtractions only (field.cpp:88-128)
+        table.update(mul_special=64, sqr_special=36)
+    slots = sum(table[k] * v for k, v in c.items())
     products = sum(v for k, v in c.items() if not k.startswith("safegcd"))
     return c, slots, products
 
@@ -257,6 +267,7 @@ def main():
     if args.impl == "reference":
         run_reference_arm(args, rank)
         return
+    set_curve(args)
     if args.curve == "bls12_381":
         if args.workload != "msm":
             raise SystemExit("bench.py: --curve bls12_381 serves --workload msm only")
@@ -277,7 +288,7 @@ def main():
     n = 1 << args.log2n
     lane_base = rank * n
     wl = args.workload
-    ctx = gecc.Context(gecc.SECP256K1, local_rank)
+    ctx = gecc.Context(gecc.SM2 if args.curve == "sm2" else gecc.SECP256K1, local_rank)
     l = gecc.lib()
     stream = torch.cuda.Stream()          # all timed work and its events share this stream
     torch.cuda.set_stream(stream)
@@ -460,7 +471,7 @@ def main():
 
     # ---- roofline of the dominant kernel (the only kernel in the step)
     per_launch_s = dev_s / args.steps
-    counts, slots_per_lane, products_per_lane = work_per_lane(wl)
+    counts, slots_per_lane, products_per_lane = work_per_lane(wl, args.curve)
     mads = n * slots_per_lane
     achieved = mads / per_launch_s
     io_bytes = {"verify": 162, "sign": 132, "padd": 194, "msm": 96}[wl] * n
@@ -475,7 +486,7 @@ def main():
         "modmul_per_s": n * products_per_lane / per_launch_s,
         "hbm": {"algorithmic_bytes_per_launch": io_bytes, "achieved_gbs": io_bytes / per_launch_s / 1e9,
                 "peak_gbs": _measured_peaks().get("hbm_gbs"), "note": "records only; not the bound"},
-        "traffic": _ncu_traffic(wl),
+        "traffic": _ncu_traffic(wl) if args.curve == "secp256k1" else None,
     }
 
     # ---- CPU baseline on this box's host cores (rank 0, N = 1 only)
@@ -535,11 +546,11 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_launch_s * 1e3,
             "higher_is_better": wl != "msm", "scaling": "weak", "vs_baseline": None,
             "dtype": "u32 limbs (256-bit modular integer)", "data": "synthetic",
-            "config": {"workload": {"verify": f"secp256k1 ECDSA verify, batch 2^{args.log2n} per GPU",
-                                    "sign": f"secp256k1 ECDSA sign, batch 2^{args.log2n} per GPU",
-                                    "padd": f"secp256k1 batched affine point addition, 2^{args.log2n} pairs per GPU",
-                                    "msm": f"secp256k1 Pippenger MSM, 2^{args.log2n} points per GPU (c = 16, batch-affine buckets)"}[wl],
-                       "curve": "secp256k1", "lanes_per_gpu": n,
+            "config": {"workload": {"verify": f"{args.curve} ECDSA verify, batch 2^{args.log2n} per GPU",
+                                    "sign": f"{args.curve} ECDSA sign, batch 2^{args.log2n} per GPU",
+                                    "padd": f"{args.curve} batched affine point addition, 2^{args.log2n} pairs per GPU",
+                                    "msm": f"{args.curve} Pippenger MSM, 2^{args.log2n} points per GPU (c = 16, batch-affine buckets)"}[wl],
+                       "curve": args.curve, "lanes_per_gpu": n,
                        "sharding": (f"point ranges x{world}, one all_gather of the partial sums + {world - 1} local additions"
                                     if wl == "msm" and world > 1 else f"lane ranges x{world}, no collective"),
                        "l2": "inputs larger than L2 (records 161 B/lane x 2^20 = 169 MB > 126 MB)"
