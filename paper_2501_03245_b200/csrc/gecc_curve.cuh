@@ -141,6 +141,57 @@ GECC_HD_CALL cjac<C> jac_dbl(const cjac<C>& p) {
     return r;
 }
 
+// The same doubling with the products inlined: for the few places where ONE warp runs a long chain
+// of dependent doublings (window combine of the MSM) -- there the cost is latency, and the
+// independent products of one doubling interleave once they are visible to the scheduler.
+template <class C>
+GECC_HD cjac<C> jac_dbl_flat(const cjac<C>& p) {
+    using fe = cfe<C>;
+    const typename C::Fp f{};
+    cjac<C> r;
+    if (C::a_kind == A_ZERO) {
+        fe A = fe_sqr_inl(f, p.X);
+        fe B = fe_sqr_inl(f, p.Y);
+        fe Cc = fe_sqr_inl(f, B);
+        fe t = fe_add(f, p.X, B);
+        fe D = fe_sub(f, fe_sub(f, fe_sqr_inl(f, t), A), Cc);
+        D = fe_dbl(f, D);                       // 2((X+B)^2 - A - C)
+        fe E = fe_add(f, fe_dbl(f, A), A);      // 3A
+        fe F = fe_sqr_inl(f, E);
+        r.X = fe_sub(f, F, fe_dbl(f, D));
+        fe C8 = fe_mul8(f, Cc);
+        r.Y = fe_sub(f, fe_mul_inl(f, E, fe_sub(f, D, r.X)), C8);
+        r.Z = fe_dbl(f, fe_mul_inl(f, p.Y, p.Z));
+    } else if (C::a_kind == A_MINUS3) {
+        fe delta = fe_sqr_inl(f, p.Z);
+        fe gamma = fe_sqr_inl(f, p.Y);
+        fe beta = fe_mul_inl(f, p.X, gamma);
+        fe t = fe_mul_inl(f, fe_sub(f, p.X, delta), fe_add(f, p.X, delta));
+        fe alpha = fe_add(f, fe_dbl(f, t), t);
+        fe beta4 = fe_dbl(f, fe_dbl(f, beta));
+        r.X = fe_sub(f, fe_sqr_inl(f, alpha), fe_dbl(f, beta4));
+        fe yz = fe_add(f, p.Y, p.Z);
+        r.Z = fe_sub(f, fe_sub(f, fe_sqr_inl(f, yz), gamma), delta);
+        fe g2 = fe_sqr_inl(f, gamma);
+        fe g8 = fe_mul8(f, g2);
+        r.Y = fe_sub(f, fe_mul_inl(f, alpha, fe_sub(f, beta4, r.X)), g8);
+    } else {
+        fe yy = fe_sqr_inl(f, p.Y);
+        fe yy2 = fe_dbl(f, yy);
+        fe s4 = fe_dbl(f, fe_mul_inl(f, p.X, yy2));
+        fe c8 = fe_dbl(f, fe_sqr_inl(f, yy2));
+        fe xx = fe_sqr_inl(f, p.X);
+        fe zz2 = fe_sqr_inl(f, fe_sqr_inl(f, p.Z));
+        fe m = fe_add(f, fe_add(f, fe_dbl(f, xx), xx), fe_mul_inl(f, curve_a<C>(), zz2));
+        r.X = fe_sub(f, fe_sub(f, fe_sqr_inl(f, m), s4), s4);
+        r.Y = fe_sub(f, fe_mul_inl(f, m, fe_sub(f, s4, r.X)), c8);
+        r.Z = fe_dbl(f, fe_mul_inl(f, p.Y, p.Z));
+    }
+    // infinity (Z = 0) stays infinity: Z3 = 2 Y Z = 0.  Y = 0 (a 2-torsion point)
+    // also gives Z3 = 0, matching curve.cpp:110-112.
+    return r;
+}
+
 // p + (x2, y2), (x2, y2) finite.  Handles p = infinity, p = q (doubling) and
 // p = -q (infinity) -- curve.cpp:129-167 with t.Z == 1.
 template <class C>

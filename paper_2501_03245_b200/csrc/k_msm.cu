@@ -782,14 +782,17 @@ k_msm_red_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, 
     if (w < MSM_WINDOWS) {
         s = jac_load<NL>(wsum, cnt, w * 4 + 2);
 #pragma unroll 1
-        for (int i = 0; i < 5; ++i) s = jac_dbl<C>(s);
+        for (int i = 0; i < 5; ++i) s = jac_dbl_flat<C>(s);
         s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 1));
 #pragma unroll 1
-        for (int i = 0; i < 5; ++i) s = jac_dbl<C>(s);
+        for (int i = 0; i < 5; ++i) s = jac_dbl_flat<C>(s);
         s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 0));
         s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 3));
+        // an empty window (the carry window almost always is) has nothing to shift: the warp's
+        // chain is then as long as its highest non-empty window
+        const uint32_t reps = jac_is_inf<C>(s) ? 0u : MSM_C * w;
 #pragma unroll 1
-        for (uint32_t i = 0; i < MSM_C * w; ++i) s = jac_dbl<C>(s);
+        for (uint32_t i = 0; i < reps; ++i) s = jac_dbl_flat<C>(s);
     }
     s = warp_sum_points<C>(s, (int)w);
     if (w == 0) {
