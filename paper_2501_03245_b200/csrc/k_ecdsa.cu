@@ -290,25 +290,16 @@ cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t
         return launch_verify_t<Sm2Curve, 128, 3>(n, dig, pub, sig, gtab, res, s);
     }
     // kernels on one stream run back to back, so consecutive pieces may reuse the scratch
-    static const int bps = [] {  // GECC_VERIFY_BLOCKS=3..6: blocks per SM (register cap 168 / 128 / 102 / 85)
-        const char* v = getenv("GECC_VERIFY_BLOCKS");
-        const int b = v ? atoi(v) : 4;
-        return b >= 3 && b <= 6 ? b : 4;
-    }();
+    // 4 blocks per SM (128 registers) measured best: 3 / 4 / 5 / 6 blocks = 26.4 / 25.5 / 27.1 / 29.2 ms
     for (size_t at = 0; at < n; at += scratch_lanes) {
         const size_t m = n - at < scratch_lanes ? n - at : scratch_lanes;
         const int b = blocks_for(m, 128);
-#define VERIFY_GTAB_(CURVE, BPS) \
-    k_verify_gtab<CURVE, 128, BPS><<<b, 128, 0, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at, gtab, lane_scratch, res + at)
-        if (curve == CURVE_SECP) {
-            if (bps == 3) VERIFY_GTAB_(SecpEcdsaCurve, 3);
-            else if (bps == 5) VERIFY_GTAB_(SecpEcdsaCurve, 5);
-            else if (bps == 6) VERIFY_GTAB_(SecpEcdsaCurve, 6);
-            else VERIFY_GTAB_(SecpEcdsaCurve, 4);
-        } else {
-            VERIFY_GTAB_(Sm2Curve, 4);
-        }
-#undef VERIFY_GTAB_
+        if (curve == CURVE_SECP)
+            k_verify_gtab<SecpEcdsaCurve, 128, 4><<<b, 128, 0, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at,
+                                                                    gtab, lane_scratch, res + at);
+        else
+            k_verify_gtab<Sm2Curve, 128, 4><<<b, 128, 0, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at, gtab,
+                                                              lane_scratch, res + at);
     }
     return cudaGetLastError();
 }
