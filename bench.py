@@ -49,8 +49,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="verify", choices=["verify", "sign", "padd", "msm"])
     ap.add_argument("--log2n", type=int, default=20)
-    ap.add_argument("--curve", default="secp256k1", choices=["secp256k1", "sm2", "bls12_381"],
-                    help="sm2 = the reference's own curve; bls12_381 (381-bit coordinates) is served by --workload msm only")
+    ap.add_argument("--curve", default="secp256k1", choices=["secp256k1", "sm2", "bls12_381", "bls12_377"],
+                    help="sm2 = the reference's own curve; bls12_381 / bls12_377 (12-limb coordinates) are served by --workload msm only")
     ap.add_argument("--cpu-sample-log2", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -268,9 +268,9 @@ def main():
         run_reference_arm(args, rank)
         return
     set_curve(args)
-    if args.curve == "bls12_381":
+    if args.curve.startswith("bls"):
         if args.workload != "msm":
-            raise SystemExit("bench.py: --curve bls12_381 serves --workload msm only")
+            raise SystemExit("bench.py: the BLS curves serve --workload msm only")
         bench_msm_bls(args, rank, local_rank, world)
         return
 
@@ -565,7 +565,7 @@ def main():
 
 
 def bench_msm_bls(args, rank, local_rank, world):
-    """BLS12-381 G1 MSM (12-limb coordinates, 255-bit scalars), device-resident.  Points are
+    """BLS12-381 / BLS12-377 G1 MSM (12-limb coordinates, 255 / 253-bit group order), device-resident.  Points are
     i * G for i = 1 .. n, built on the GPU by doubling-and-adding whole arrays (batch_padd /
     batch_pdbl); the gate before timing checks sum_i k_i (i G) = (sum_i k_i i mod r) G against
     Python integers."""
@@ -578,9 +578,9 @@ def bench_msm_bls(args, rank, local_rank, world):
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    B = E.BLS12_381
+    B = E.CURVES[args.curve]
     n = 1 << args.log2n
-    ctx = gecc.Context(gecc.BLS12_381, local_rank)
+    ctx = gecc.Context(gecc.BLS12_381 if args.curve == "bls12_381" else gecc.BLS12_377, local_rank)
     l = gecc.lib()
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
@@ -589,7 +589,7 @@ def bench_msm_bls(args, rank, local_rank, world):
     R12 = 1 << 384
     g = (gecc.cols_from_ints([B.gx * R12 % B.p], 12), gecc.cols_from_ints([B.gy * R12 % B.p], 12), np.zeros(1, np.uint8))
     # [1..2^k - 1] G  ->  [1..2^(k+1) - 1] G  =  old, 2^k G, old + 2^k G
-    px, py = torch.from_numpy(g[0]).cuda().view(torch.int32), torch.from_numpy(g[1]).cuda().view(torch.int32)
+    px, py = torch.from_numpy(g[0].copy()).cuda().view(torch.int32), torch.from_numpy(g[1].copy()).cuda().view(torch.int32)
     base = (px.clone(), py.clone())
     zero = lambda m: torch.zeros(m, dtype=torch.uint8, device="cuda")
     col = lambda m: torch.empty((12, m), dtype=torch.int32, device="cuda")
@@ -626,7 +626,7 @@ def bench_msm_bls(args, rank, local_rank, world):
     rinv = pow(R12, -1, B.p)
     got = (gecc.ints_from_cols(ox.cpu().numpy().view(np.uint32))[0] * rinv % B.p,
            gecc.ints_from_cols(oy.cpu().numpy().view(np.uint32))[0] * rinv % B.p)
-    assert int(oi.item()) == 0 and got == want, "BLS12-381 MSM gate failed"
+    assert int(oi.item()) == 0 and got == want, "BLS MSM gate failed"
 
     def barrier():
         torch.cuda.synchronize()
@@ -664,9 +664,9 @@ def bench_msm_bls(args, rank, local_rank, world):
         print(json.dumps({
             "metric": "msm_time", "value": per * 1e3, "unit": "ms per MSM", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u32 limbs (381-bit modular integer, 12 limbs)", "data": "synthetic",
-            "config": {"workload": f"BLS12-381 G1 Pippenger MSM, 2^{args.log2n} points per GPU (c = 16, batch-affine buckets)",
-                       "curve": "bls12_381", "lanes_per_gpu": n, "sharding": f"point ranges x{world}",
+            "vs_baseline": None, "dtype": f"u32 limbs ({B.p.bit_length()}-bit modular integer, 12 limbs)", "data": "synthetic",
+            "config": {"workload": f"{args.curve} G1 Pippenger MSM, 2^{args.log2n} points per GPU (c = 16, batch-affine buckets)",
+                       "curve": args.curve, "lanes_per_gpu": n, "sharding": f"point ranges x{world}",
                        "l2": "no L2 flush; scalars + points 2^20 x 128 B = 134 MB > 126 MB L2"},
             "clocks": clocks, "e2e": None, "gpu_launches": ctx.launches - launches0,
             "roofline": {"bound": "imad", "kernel": "k_msm_tree_fwd/bwd", "achieved": mads / per / 1e12,

@@ -113,12 +113,15 @@ sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, 
 
 /* ========================== Part 2: extensions ========================== */
 
-/* GECC_CURVE_BLS12_381 (G1: y^2 = x^3 + 4 over the 381-bit prime) serves the field, batch and MSM
+/* GECC_CURVE_BLS12_381 (G1: y^2 = x^3 + 4 over the 381-bit prime) and GECC_CURVE_BLS12_377 (G1:
+ * y^2 = x^3 + 1 over the 377-bit prime, 253-bit group order) serve the field, batch and MSM
  * layer only -- the reference is 256-bit (limbs.hpp:17) and has no counterpart.  Its coordinate
  * column buffers hold 12 limbs per element (limb k of element i at cols[k*n + i], Montgomery
  * form with R = 2^384); scalars and GECC_FIELD_N elements stay 8 limbs (255-bit group order).
  * The ECDSA / fixed-base / variable-base entry points return SM2B_ERROR_INVALID_ARGUMENT on it. */
-typedef enum gecc_curve { GECC_CURVE_SM2 = 0, GECC_CURVE_SECP256K1 = 1, GECC_CURVE_BLS12_381 = 2 } gecc_curve;
+typedef enum gecc_curve {
+    GECC_CURVE_SM2 = 0, GECC_CURVE_SECP256K1 = 1, GECC_CURVE_BLS12_381 = 2, GECC_CURVE_BLS12_377 = 3
+} gecc_curve;
 typedef enum gecc_field { GECC_FIELD_P = 0, GECC_FIELD_N = 1 } gecc_field;
 /* same numbering as the oracle's field ops */
 typedef enum gecc_field_opcode {

@@ -66,7 +66,20 @@ BLS12_381 = Curve(
     gy=0x08b3f481e3aaa0f1a09e30ed741d8ae4fcf5e095d5d00af600db18cb2c04b3edd03cc744a2888ae40caa232946c5e7e1,
 )
 
-CURVES = {0: SM2, 1: SECP256K1, 2: BLS12_381, "sm2": SM2, "secp256k1": SECP256K1, "bls12_381": BLS12_381}
+# BLS12-377 G1 (BASELINE.json config 4 names it): y^2 = x^3 + 1 over the 377-bit prime, group order
+# the 253-bit n, the arkworks / Zexe generator.
+BLS12_377 = Curve(
+    "bls12_377", 3,
+    p=0x01ae3a4617c510eac63b05c06ca1493b1a22d9f300f5138f1ef3622fba094800170b5d44300000008508c00000000001,
+    a=0,
+    b=1,
+    n=0x12ab655e9a2ca55660b44d1e5c37b00159aa76fed00000010a11800000000001,
+    gx=0x008848defe740a67c8fc6225bf87ff5485951e2caa9d41bb188282c8bd37cb5cd5481512ffcd394eeab9b16eb21be9ef,
+    gy=0x01914a69c5102eff1f674f5d30afeec4bd7fb348ca3e52d96d182ad44fb82305c2fe3d3634a9591afd82de55559c8ea6,
+)
+
+CURVES = {0: SM2, 1: SECP256K1, 2: BLS12_381, 3: BLS12_377, "sm2": SM2, "secp256k1": SECP256K1,
+          "bls12_381": BLS12_381, "bls12_377": BLS12_377}
 
 INF = None  # point at infinity
 

@@ -16,7 +16,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libgecc_b200.so")
 
-SM2, SECP256K1, BLS12_381 = 0, 1, 2
+SM2, SECP256K1, BLS12_381, BLS12_377 = 0, 1, 2, 3
 FIELD_P, FIELD_N = 0, 1
 STATUS = {0: "ok", 1: "invalid argument", 2: "malformed input", 3: "invalid peer point",
           4: "degenerate result", 5: "nonce retries exhausted", 6: "cost model has no crossover",
@@ -118,7 +118,7 @@ class Context:
                             "(libgecc_b200 has no CPU path)")
         self.h = C.c_void_p(h)
         self.curve = self.l.gecc_ctx_curve(self.h)
-        self.limbs = 12 if self.curve == BLS12_381 else 8  # 32-bit limbs per coordinate
+        self.limbs = 12 if self.curve in (BLS12_381, BLS12_377) else 8  # 32-bit limbs per coordinate
 
     def close(self):
         if getattr(self, "h", None):

@@ -111,8 +111,7 @@ struct Carver {
 extern "C" {
 
 sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device) {
-    if (curve != GECC_CURVE_SM2 && curve != GECC_CURVE_SECP256K1 && curve != GECC_CURVE_BLS12_381)
-        return nullptr;
+    if ((unsigned)curve > GECC_CURVE_BLS12_377) return nullptr;
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
         fprintf(stderr, "gecc_b200: no usable CUDA device (this library has no CPU path)\n");
@@ -124,7 +123,7 @@ sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device) {
     if (device >= count) return nullptr;
     sm2b_ctx* ctx = new (std::nothrow) sm2b_ctx();
     if (!ctx) return nullptr;
-    ctx->curve = curve == GECC_CURVE_SM2 ? CURVE_SM2 : curve == GECC_CURVE_SECP256K1 ? CURVE_SECP : CURVE_BLS381;
+    ctx->curve = (int)curve;  // the internal ids equal the public enum
     ctx->limbs = curve_limbs(ctx->curve);
     ctx->device = device;
     DeviceGuard g(device);
@@ -142,7 +141,7 @@ sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device) {
         sm2b_ctx_free(ctx);
         return nullptr;
     }
-    if (ctx->curve == CURVE_BLS381) {  // field / batch / MSM layer only: no ECDSA, no fixed-base table
+    if (curve_is_bls(ctx->curve)) {  // field / batch / MSM layer only: no ECDSA, no fixed-base table
         if (cudaMalloc(&ctx->flags, 256) != cudaSuccess) {
             sm2b_ctx_free(ctx);
             return nullptr;
@@ -396,7 +395,7 @@ extern "C" {
 sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
                             const uint8_t* publics, const uint8_t* signatures,
                             uint8_t* results) {
-    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
+    if (ctx && curve_is_bls(ctx->curve)) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (count > 0 && (!digests || !publics || !signatures || !results)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -415,7 +414,7 @@ sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
 
 sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
                         const uint8_t* publics, const uint8_t* signatures, uint8_t* results) {
-    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
+    if (ctx && curve_is_bls(ctx->curve)) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (count > 0 && (!digests || !publics || !signatures || !results)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     if (count == 0) return SM2B_OK;
@@ -463,7 +462,7 @@ sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
 sm2b_status gecc_sign_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
                           const uint8_t* secrets, uint64_t nonce_seed, uint64_t lane_base,
                           uint8_t* signatures, int32_t* lane_status) {
-    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
+    if (ctx && curve_is_bls(ctx->curve)) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (count > 0 && (!digests || !secrets || !signatures || !lane_status)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     if (nonce_seed == 0) return fail_msg(ctx, "device signing needs a non-zero nonce seed");
@@ -506,7 +505,7 @@ sm2b_status report_lanes(const int32_t* st, size_t n, int32_t* lane_status) {
 sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const uint8_t* secrets,
                       uint64_t nonce_seed, uint64_t lane_base, uint8_t* signatures,
                       int32_t* lane_status) {
-    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
+    if (ctx && curve_is_bls(ctx->curve)) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (count > 0 && (!digests || !secrets || !signatures)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     if (count == 0) return SM2B_OK;
@@ -594,7 +593,7 @@ sm2b_status sm2b_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const
 
 sm2b_status gecc_keygen(sm2b_ctx* ctx, uint64_t seed, uint64_t lane_base, size_t count,
                         uint8_t* secrets, uint8_t* publics) {
-    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
+    if (ctx && curve_is_bls(ctx->curve)) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (count > 0 && (!secrets || !publics))) return SM2B_ERROR_INVALID_ARGUMENT;
     if (count == 0) return SM2B_OK;
     if (seed == 0) seed = system_seed();
@@ -619,7 +618,7 @@ sm2b_status sm2b_keygen(sm2b_ctx* ctx, uint64_t seed, size_t count, uint8_t* sec
 
 sm2b_status sm2b_ecdh(sm2b_ctx* ctx, size_t count, const uint8_t* secrets, const uint8_t* peers,
                       uint8_t* shared, int32_t* lane_status) {
-    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
+    if (ctx && curve_is_bls(ctx->curve)) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (count > 0 && (!secrets || !peers || !shared))) return SM2B_ERROR_INVALID_ARGUMENT;
     if (count == 0) return SM2B_OK;
     std::vector<int32_t> hst(count);
@@ -689,7 +688,7 @@ sm2b_status gecc_batch_pdbl_dev(sm2b_ctx* ctx, size_t n, const uint32_t* px, con
 }
 sm2b_status gecc_batch_fpmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, uint32_t* ox,
                                  uint32_t* oy, uint8_t* oinf) {
-    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
+    if (ctx && curve_is_bls(ctx->curve)) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (n > 0 && (!scalars || !ox || !oy || !oinf))) return SM2B_ERROR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
@@ -701,7 +700,7 @@ sm2b_status gecc_batch_fpmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalar
 sm2b_status gecc_batch_upmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars,
                                  const uint32_t* px, const uint32_t* py, const uint8_t* pinf,
                                  uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
-    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
+    if (ctx && curve_is_bls(ctx->curve)) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (n > 0 && (!scalars || !px || !py || !ox || !oy || !oinf)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -820,7 +819,7 @@ sm2b_status gecc_batch_pdbl(sm2b_ctx* ctx, size_t n, const uint32_t* px, const u
 }
 sm2b_status gecc_batch_fpmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, uint32_t* ox,
                              uint32_t* oy, uint8_t* oinf) {
-    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
+    if (ctx && curve_is_bls(ctx->curve)) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (n > 0 && (!scalars || !ox || !oy || !oinf))) return SM2B_ERROR_INVALID_ARGUMENT;
     if (n == 0) return SM2B_OK;
     return run_points(ctx, n, scalars, nullptr, nullptr, ox, oy, oinf,
@@ -832,7 +831,7 @@ sm2b_status gecc_batch_fpmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, u
 sm2b_status gecc_batch_upmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uint32_t* px,
                              const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
                              uint8_t* oinf) {
-    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
+    if (ctx && curve_is_bls(ctx->curve)) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || (n > 0 && (!scalars || !px || !py || !ox || !oy || !oinf)))
         return SM2B_ERROR_INVALID_ARGUMENT;
     if (n == 0) return SM2B_OK;
@@ -864,7 +863,7 @@ extern "C" {
 sm2b_status sm2b_bench_run(sm2b_ctx* ctx, const char* op, const char* strategy, size_t n,
                            size_t lanes, uint32_t workers, uint64_t seed, uint32_t repeats,
                            sm2b_bench_report* out) {
-    if (ctx && ctx->curve == CURVE_BLS381) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
+    if (ctx && curve_is_bls(ctx->curve)) return SM2B_ERROR_INVALID_ARGUMENT;  // ECDSA layer: 256-bit curves only
     if (!ctx || !op || !strategy || !out) return SM2B_ERROR_INVALID_ARGUMENT;
     static const char* const ops[] = {"padd", "fpmul", "upmul", "sign", "verify"};
     int opi = -1;

@@ -11,8 +11,9 @@
 
 namespace gecc {
 
-enum { CURVE_SM2 = 0, CURVE_SECP = 1, CURVE_BLS381 = 2 };  // BLS12-381 G1: 12-limb coordinates
-inline int curve_limbs(int curve) { return curve == CURVE_BLS381 ? 12 : 8; }
+enum { CURVE_SM2 = 0, CURVE_SECP = 1, CURVE_BLS381 = 2, CURVE_BLS377 = 3 };  // BLS12-381 / BLS12-377 G1: 12-limb coordinates
+inline bool curve_is_bls(int curve) { return curve == CURVE_BLS381 || curve == CURVE_BLS377; }
+inline int curve_limbs(int curve) { return curve_is_bls(curve) ? 12 : 8; }
 
 cudaError_t launch_field_op(int curve, int field, int op, size_t n, const uint32_t* a,
                             const uint32_t* b, uint32_t* out, cudaStream_t s);

@@ -444,10 +444,15 @@ static size_t pick_threads(size_t n, int form) {
 cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* in, uint32_t* out,
                                 cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    if (curve == CURVE_BLS381) {  // 381-bit base field (12 limbs) / 255-bit scalar field: cooperative form
+    if (curve_is_bls(curve)) {  // 12-limb base fields / their 8-limb scalar fields: cooperative form
         const unsigned cb = coop_blocks(n, 128);
-        if (field == 0) k_batch_invert_coop<Bls381P, 128><<<cb, 128, 0, s>>>(n, in, out);
-        else k_batch_invert_coop<Bls381R, 128><<<cb, 128, 0, s>>>(n, in, out);
+        if (curve == CURVE_BLS381) {
+            if (field == 0) k_batch_invert_coop<Bls381P, 128><<<cb, 128, 0, s>>>(n, in, out);
+            else k_batch_invert_coop<Bls381R, 128><<<cb, 128, 0, s>>>(n, in, out);
+        } else {
+            if (field == 0) k_batch_invert_coop<Bls377P, 128><<<cb, 128, 0, s>>>(n, in, out);
+            else k_batch_invert_coop<Bls377R, 128><<<cb, 128, 0, s>>>(n, in, out);
+        }
         return cudaGetLastError();
     }
     const int form = pick_form(n);
@@ -490,6 +495,10 @@ cudaError_t launch_batch_padd(int curve, size_t n, const uint32_t* px, const uin
     if (n == 0) return cudaSuccess;
     if (curve == CURVE_BLS381) {
         k_batch_padd_coop<Bls381Curve, 128><<<coop_blocks(n, 128), 128, 0, s>>>(n, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
+        return cudaGetLastError();
+    }
+    if (curve == CURVE_BLS377) {
+        k_batch_padd_coop<Bls377Curve, 128><<<coop_blocks(n, 128), 128, 0, s>>>(n, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
         return cudaGetLastError();
     }
     const int form = pick_form(n, scratch != nullptr);
@@ -543,6 +552,10 @@ cudaError_t launch_batch_pdbl(int curve, size_t n, const uint32_t* px, const uin
     if (n == 0) return cudaSuccess;
     if (curve == CURVE_BLS381) {
         k_batch_pdbl_coop<Bls381Curve, 128><<<coop_blocks(n, 128), 128, 0, s>>>(n, px, py, pinf, ox, oy, oinf);
+        return cudaGetLastError();
+    }
+    if (curve == CURVE_BLS377) {
+        k_batch_pdbl_coop<Bls377Curve, 128><<<coop_blocks(n, 128), 128, 0, s>>>(n, px, py, pinf, ox, oy, oinf);
         return cudaGetLastError();
     }
     const int form = pick_form(n);

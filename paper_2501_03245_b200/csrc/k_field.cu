@@ -39,6 +39,9 @@ cudaError_t launch_field_op(int curve, int field, int op, size_t n, const uint32
     if (curve == CURVE_BLS381) {  // base field: 12 limbs per element, scalar field: 8
         if (field == 0) k_field_op<Bls381P><<<blocks, threads, 0, s>>>(op, n, a, b, out);
         else k_field_op<Bls381R><<<blocks, threads, 0, s>>>(op, n, a, b, out);
+    } else if (curve == CURVE_BLS377) {
+        if (field == 0) k_field_op<Bls377P><<<blocks, threads, 0, s>>>(op, n, a, b, out);
+        else k_field_op<Bls377R><<<blocks, threads, 0, s>>>(op, n, a, b, out);
     } else if (curve == CURVE_SECP) {
         if (field == 0) k_field_op<SecpP><<<blocks, threads, 0, s>>>(op, n, a, b, out);
         else k_field_op<SecpN><<<blocks, threads, 0, s>>>(op, n, a, b, out);

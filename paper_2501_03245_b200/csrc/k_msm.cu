@@ -38,8 +38,12 @@ k_msm_digits(size_t n, const uint32_t* __restrict__ scalars, const uint8_t* __re
     const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     // any 256-bit scalar is accepted: below 2n for the 256-bit curves (one subtraction), below
-    // 2^256 < 3r for BLS12-381's 255-bit group order (two)
-    fe k = scalar_reduce_once<typename C::Fn>(scalar_reduce_once<typename C::Fn>(col_load<8>(scalars, n, i)));
+    // 3r for BLS12-381's 255-bit group order (two), below 14r for BLS12-377's 253-bit one (13)
+    constexpr uint32_t top = C::Fn::q(7);
+    constexpr int subs = top >= 0x80000000u ? 1 : (int)(0xFFFFFFFFu / top);
+    fe k = col_load<8>(scalars, n, i);
+#pragma unroll 1
+    for (int it = 0; it < subs; ++it) k = scalar_reduce_once<typename C::Fn>(k);
     const bool skip = pinf && pinf[i];
     // k >= 2^255: use (n - k) * (-P).  A carry window would otherwise collect ~n/2 points in
     // ONE bucket (a single thread adding half a million points).
@@ -968,6 +972,8 @@ cudaError_t launch_msm(int curve, size_t n, const uint32_t* scalars, const uint3
                        uint8_t* oinf, void* scratch, cudaStream_t s, int* launches) {
     if (curve == CURVE_BLS381)
         return run_msm<Bls381Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
+    if (curve == CURVE_BLS377)
+        return run_msm<Bls377Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
     if (curve == CURVE_SECP)
         return run_msm<SecpCurve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
     return run_msm<Sm2Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);

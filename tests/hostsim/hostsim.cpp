@@ -61,6 +61,8 @@ int hs_field_op(int field, const FieldRT* rt, int op, size_t n, const uint32_t* 
         case 5: return field_op_t(SecpPL{}, op, n, a, b, out);  // lazy plain secp256k1 (outputs weakly reduced)
         case 6: return field_op_t(Bls381P{}, op, n, a, b, out);  // 12 limbs
         case 7: return field_op_t(Bls381R{}, op, n, a, b, out);
+        case 8: return field_op_t(Bls377P{}, op, n, a, b, out);  // 12 limbs
+        case 9: return field_op_t(Bls377R{}, op, n, a, b, out);
     }
     return 1;
 }
@@ -70,11 +72,11 @@ int hs_field_op(int field, const FieldRT* rt, int op, size_t n, const uint32_t* 
 // BLS12-381 G1 point formulas (12-limb coordinates): op 0 = P + Q through jac_madd / jac_add,
 // 1 = 2P, 2 = k * P by double-and-add with mixed additions; affine Montgomery in and out.
 #include "gecc_curve.cuh"
-extern "C" int hs_bls_point_op(int op, size_t n, const uint32_t* k, const uint32_t* px, const uint32_t* py,
-                               const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty, const uint8_t* tinf,
-                               uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
-    using C = Bls381Curve;
-    const Bls381P f{};
+template <class C>
+static int bls_point_op_t(int op, size_t n, const uint32_t* k, const uint32_t* px, const uint32_t* py,
+                          const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty, const uint8_t* tinf,
+                          uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    const typename C::Fp f{};
     for (size_t i = 0; i < n; ++i) {
         caff<C> p{col_get<12>(px, n, i), col_get<12>(py, n, i)};
         cjac<C> P = jac_infinity<C>();
@@ -114,6 +116,13 @@ extern "C" int hs_bls_point_op(int op, size_t n, const uint32_t* k, const uint32
         }
     }
     return 0;
+}
+// curve: 2 = BLS12-381, 3 = BLS12-377
+extern "C" int hs_bls_point_op(int curve, int op, size_t n, const uint32_t* k, const uint32_t* px, const uint32_t* py,
+                               const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty, const uint8_t* tinf,
+                               uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
+    if (curve == 3) return bls_point_op_t<Bls377Curve>(op, n, k, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
+    return bls_point_op_t<Bls381Curve>(op, n, k, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
 }
 
 // ---------------------------------------------------------------------------

@@ -36,6 +36,7 @@ SECP_LAZY_FIELD = 5
 
 
 BLS_P_FIELD, BLS_R_FIELD = 6, 7   # BLS12-381 base field (12 limbs) and scalar field (8 limbs)
+BLS_FIELDS = {2: (6, 7), 3: (8, 9)}  # curve id -> (base field, scalar field) hostsim ids; 3 = BLS12-377
 
 
 def field_op(curve, which, op, a, b=None, field_id=None):
@@ -103,12 +104,12 @@ def glv_split(k):
     return m1, m2, sg
 
 
-def bls_point_op(op, P, T=None, k=None):
-    """BLS12-381 G1 (12-limb Montgomery coordinates): op 'add' | 'dbl' | 'mul'."""
+def bls_point_op(op, P, T=None, k=None, curve=2):
+    """BLS12-381 / BLS12-377 G1 (12-limb Montgomery coordinates): op 'add' | 'dbl' | 'mul'."""
     n = P[0].shape[1]
     o = np.zeros((12, n), np.uint32), np.zeros((12, n), np.uint32), np.zeros(n, np.uint8)
     T = T if T is not None else P
-    rc = lib().hs_bls_point_op({"add": 0, "dbl": 1, "mul": 2}[op], C.c_size_t(n), _p(k), _p(P[0]), _p(P[1]),
+    rc = lib().hs_bls_point_op(curve, {"add": 0, "dbl": 1, "mul": 2}[op], C.c_size_t(n), _p(k), _p(P[0]), _p(P[1]),
                                _p(P[2]), _p(T[0]), _p(T[1]), _p(T[2]), _p(o[0]), _p(o[1]), _p(o[2]))
     assert rc == 0, rc
     return o

@@ -1,4 +1,4 @@
-"""GPU parity of the 381-bit layer (BLS12-381 G1 context): field kernels, batched affine
+"""GPU parity of the 12-limb layer (BLS12-381 and BLS12-377 G1 contexts): field kernels, batched affine
 addition / doubling / inversion over 12-limb column buffers, and MSM -- against Python
 integers (oracle/pyec.py).  The reference is 256-bit only, so parity is against the definition;
 the same device code is also checked on the CPU by tests/test_hostsim_bls.py."""
@@ -11,34 +11,40 @@ import paper_2501_03245_b200 as gecc
 from oracle import pyec as E
 
 pytestmark = pytest.mark.gpu
-B = E.BLS12_381
 R12 = 1 << 384
-RINV = pow(R12, -1, B.p)
 
 
-@pytest.fixture(scope="module")
-def ctx():
-    c = gecc.Context(gecc.BLS12_381)
-    yield c
-    c.close()
+class Env:
+    """one curve: its oracle parameters, a GPU context, Montgomery conversions"""
+
+    def __init__(self, curve, gid):
+        self.B, self.ctx, self.rinv = curve, gecc.Context(gid), pow(R12, -1, curve.p)
+
+
+@pytest.fixture(scope="module", params=["bls12_381", "bls12_377"])
+def env(request):
+    e = Env(E.CURVES[request.param], {"bls12_381": gecc.BLS12_381, "bls12_377": gecc.BLS12_377}[request.param])
+    yield e
+    e.ctx.close()
 
 
 def cols(v, limbs=12):
     return gecc.cols_from_ints(v, limbs)
 
 
-def mont_pts(pts):
+def mont_pts(B, pts):
     xs = [0 if p is None else p[0] * R12 % B.p for p in pts]
     ys = [0 if p is None else p[1] * R12 % B.p for p in pts]
     return cols(xs), cols(ys), np.array([p is None for p in pts], np.uint8)
 
 
-def from_mont_pts(P):
+def from_mont_pts(B, P):
+    rinv = pow(R12, -1, B.p)
     xs, ys = gecc.ints_from_cols(P[0]), gecc.ints_from_cols(P[1])
-    return [None if P[2][i] else (xs[i] * RINV % B.p, ys[i] * RINV % B.p) for i in range(len(xs))]
+    return [None if P[2][i] else (xs[i] * rinv % B.p, ys[i] * rinv % B.p) for i in range(len(xs))]
 
 
-def rand_points(rng, n):
+def rand_points(B, rng, n):
     """n random multiples of G, built from a few oracle points by cheap additions"""
     seeds = [E.ec_mul(B, rng.randrange(1, B.n), B.G) for _ in range(6)]
     pts, cur = [], seeds[0]
@@ -48,10 +54,11 @@ def rand_points(rng, n):
     return pts
 
 
-def test_field12_kernels(ctx):
+def test_field12_kernels(env):
+    B, ctx, RINV = env.B, env.ctx, env.rinv
     q = B.p
     rng = random.Random(3811)
-    a = [0, 1, 2, q - 1, q - 2, (q + 1) // 2, (1 << 380) % q] + [rng.randrange(q) for _ in range(5000)]
+    a = [0, 1, 2, q - 1, q - 2, (q + 1) // 2, (1 << 376) % q] + [rng.randrange(q) for _ in range(5000)]
     b = list(reversed(a))
     A, Bc = cols(a), cols(b)
     ints = gecc.ints_from_cols
@@ -75,31 +82,33 @@ def test_field12_kernels(ctx):
     assert ints(ctx.batch_invert(1, S)) == [pow(x * rinv % r, -1, r) * (1 << 256) % r if x else 0 for x in s]
 
 
-def test_batch_padd_pdbl_g1(ctx):
+def test_batch_padd_pdbl_g1(env):
+    B, ctx = env.B, env.ctx
     rng = random.Random(3812)
     n = 700  # more than one block; ragged tail
-    P = rand_points(rng, n)
-    T = list(reversed(rand_points(rng, n)))
+    P = rand_points(B, rng, n)
+    T = list(reversed(rand_points(B, rng, n)))
     # exceptional lanes (test_batch_point.cpp:70-100): P == T, P == -T, infinities
     for i in (3, 7, 11):
         T[i] = P[i]
     for i in (19, 23):
         T[i] = (P[i][0], B.p - P[i][1])
     P[31], T[47], P[48], T[48] = None, None, None, None
-    got = from_mont_pts(ctx.batch_padd(mont_pts(P), mont_pts(T)))
+    got = from_mont_pts(B, ctx.batch_padd(mont_pts(B, P), mont_pts(B, T)))
     assert got == [E.ec_add(B, a, b) for a, b in zip(P, T)]
-    got = from_mont_pts(ctx.batch_pdbl(mont_pts(P)))
+    got = from_mont_pts(B, ctx.batch_pdbl(mont_pts(B, P)))
     assert got == [E.ec_add(B, a, a) for a in P]
     assert all(E.on_curve(B, p) for p in got)
 
 
 @pytest.mark.parametrize("form", ["affine", "jacobian"])
-def test_msm_g1(ctx, form):
+def test_msm_g1(env, form):
+    B, ctx = env.B, env.ctx
     gecc.set_msm_form(form)
     try:
         rng = random.Random(3813)
         for n in (1, 2, 33, 300):
-            pts = rand_points(rng, n)
+            pts = rand_points(B, rng, n)
             ks = [rng.randrange(1 << 256) for _ in range(n)]
             if n == 300:  # duplicates, opposite points, zero / order / all-ones scalars, an infinity input
                 for i in range(10, 40):
@@ -112,18 +121,19 @@ def test_msm_g1(ctx, form):
             want = None
             for k, p in zip(ks, pts):
                 want = E.ec_add(B, want, E.ec_mul(B, k % B.n, p) if p is not None else None)
-            got = from_mont_pts(ctx.msm(cols(ks, 8), mont_pts(pts)))
+            got = from_mont_pts(B, ctx.msm(cols(ks, 8), mont_pts(B, pts)))
             assert got == [want], n
         # everything cancels / empty sum
-        pts = rand_points(rng, 4)
-        assert ctx.msm(cols([0] * 4, 8), mont_pts(pts))[2][0] == 1
+        pts = rand_points(B, rng, 4)
+        assert ctx.msm(cols([0] * 4, 8), mont_pts(B, pts))[2][0] == 1
         empty = (np.zeros((12, 0), np.uint32), np.zeros((12, 0), np.uint32), np.zeros(0, np.uint8))
         assert ctx.msm(np.zeros((8, 0), np.uint32), empty)[2][0] == 1
     finally:
         gecc.set_msm_form("auto")
 
 
-def test_msm_g1_identity_2_16(ctx):
+def test_msm_g1_identity_2_16(env):
+    B, ctx = env.B, env.ctx
     """sum_i s_i (t_i G) = (sum_i s_i t_i mod r) G at 2^16 points whose discrete logs t_i are
     known by construction (chains of batch_padd steps from oracle points, ends re-checked)."""
     rng = random.Random(3814)
@@ -134,8 +144,8 @@ def test_msm_g1_identity_2_16(ctx):
     lanes = 256
     per = n // lanes
     starts_log = [rng.randrange(1, B.n) for _ in range(lanes)]
-    cur_pts = mont_pts([E.ec_mul(B, x, B.G) for x in starts_log])
-    incs = [mont_pts([seeds[1 + k]] * lanes) for k in range(5)]
+    cur_pts = mont_pts(B, [E.ec_mul(B, x, B.G) for x in starts_log])
+    incs = [mont_pts(B, [seeds[1 + k]] * lanes) for k in range(5)]
     all_x, all_y, all_logs = [], [], []
     cur_logs = list(starts_log)
     for step in range(per):
@@ -145,9 +155,9 @@ def test_msm_g1_identity_2_16(ctx):
     PX = np.ascontiguousarray(np.concatenate(all_x, axis=1))
     PY = np.ascontiguousarray(np.concatenate(all_y, axis=1))
     PI = np.zeros(n, np.uint8)
-    end = from_mont_pts(cur_pts)
+    end = from_mont_pts(B, cur_pts)
     assert end[0] == E.ec_mul(B, cur_logs[0], B.G) and end[-1] == E.ec_mul(B, cur_logs[-1], B.G)
     ks = [rng.randrange(1 << 256) for _ in range(n)]
-    got = from_mont_pts(ctx.msm(cols(ks, 8), (PX, PY, PI)))
+    got = from_mont_pts(B, ctx.msm(cols(ks, 8), (PX, PY, PI)))
     total = sum((k % B.n) * l for k, l in zip(ks, all_logs)) % B.n
     assert got == [E.ec_mul(B, total, B.G)]
