@@ -224,8 +224,8 @@ def run_reference_arm(args, rank):
 SLOTS = {
     "mul_special": 64 + 8 + 8 * 0.5,            # product + word-serial secp256k1 REDC
     "sqr_special": 36 + 8 + 8 * 0.5,
-    "mul_generic": 64 + (28 + 36 * 0.5) + 64,   # product + low product + m*q product
-    "sqr_generic": 36 + (28 + 36 * 0.5) + 64,
+    "mul_generic": 64 + 64 + 8 * 0.5,           # product + word-serial Montgomery rows (m_i * q) + the 8 m_i
+    "sqr_generic": 36 + 64 + 8 * 0.5,
     "safegcd_special": 20 * (36 + 54),          # 20 rounds of two 2x2 matrix updates
     "safegcd_generic": 20 * (36 + 54),
 }
@@ -657,8 +657,8 @@ def bench_msm_bls(args, rank, local_rank, world):
     clocks = sampler.stop()
     per = dev_s / args.steps
     counts = msm_products_per_point("generic12")
-    # 12-limb generic Montgomery product: 144 (product) + 78 (low product) + 144 (m * q) wide multiplies
-    slots = {"mul_generic12": 144 + 78 + 144, "sqr_generic12": 78 + 78 + 144}
+    # 12-limb Montgomery product: 144 (product) + 144 (word-serial rows m_i * q) wide multiplies + 12 m_i
+    slots = {"mul_generic12": 144 + 144 + 12 * 0.5, "sqr_generic12": 78 + 144 + 12 * 0.5}
     mads = n * sum(slots[kk] * v for kk, v in counts.items())
     if rank == 0:
         print(json.dumps({

@@ -323,10 +323,10 @@ GECC_HD fel<F> fe_mul8(const F& f, const fel<F>& a) {  // 8 a
 // accumulated in e[], odd ones in o[] (o is one limb to the left), so that every
 // lo/hi pair sits on an aligned register pair and each row is two carry chains of
 // IMAD.WIDE.U32(.X).  64 wide multiply-adds + 8 carry folds + 15 merge adds.
+// unmerged form: a*b = sum e[k] 2^(32k) + sum o[k] 2^(32(k+1))
 template <int N>
-GECC_HD void mul_wide_n(uint32_t* t, const uint32_t* a, const uint32_t* b) {
+GECC_HD void mul_wide_eo(uint32_t* e, uint32_t* o, const uint32_t* a, const uint32_t* b) {
     static_assert(N % 2 == 0, "even/odd layout needs an even limb count");
-    uint32_t e[2 * N], o[2 * N];
 #pragma unroll
     for (int k = 0; k < 2 * N; ++k) e[k] = o[k] = 0;
     {   // row 0 meets only zeros: plain wide products, no carry chain
@@ -377,6 +377,11 @@ GECC_HD void mul_wide_n(uint32_t* t, const uint32_t* a, const uint32_t* b) {
             }
         }
     }
+}
+template <int N>
+GECC_HD void mul_wide_n(uint32_t* t, const uint32_t* a, const uint32_t* b) {
+    uint32_t e[2 * N], o[2 * N];
+    mul_wide_eo<N>(e, o, a, b);
     t[0] = e[0];
     t[1] = add_cc(e[1], o[0]);
 #pragma unroll
@@ -475,6 +480,95 @@ GECC_HD fel<F> final_sub(const F& f, const fel<F>& r, uint32_t top) {
     for (int i = 1; i < F::N; ++i) d.w[i] = subc_cc(r.w[i], f.q(i));
     uint32_t borrow = subc(0, 0);
     return fe_select(top != 0 || borrow == 0, d, r);
+}
+
+// Word-serial Montgomery reduction for any odd q on the UNMERGED even/odd product (reference:
+// reduce_generic_raw, field.cpp:50-78 -- the same word-by-word elimination and the same value).
+// Step i takes the low word of what is left at position i, L = e[i] + o[i-1] + carry, the
+// multiplier m = L * (-q^-1 mod 2^32), and adds m * q * 2^(32 i) with the SAME two aligned
+// IMAD.WIDE carry chains a product row uses (row i of "q times m"), so the reduction costs N^2
+// wide multiplies + N 32-bit ones instead of the N(N+1)/2 + N^2 of a two-product REDC.  The
+// chains end in words that may already be full, so their carry-outs are collected in cc[] (by
+// position) and enter the final merge of the high half.
+template <class F>
+GECC_HD fel<F> redc_ws_eo(const F& f, uint32_t* e, uint32_t* o) {
+    constexpr int N = F::N;
+    uint32_t cc[N + 1];  // cc[k]: carries into position N + k
+#pragma unroll
+    for (int k = 0; k <= N; ++k) cc[k] = 0;
+    uint32_t c = 0;      // carry into position i from the eliminated positions below
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const uint32_t below = i ? o[i - 1] : 0u;
+        const uint32_t m = (e[i] + below + c) * f.qinv32;
+        if ((i & 1) == 0) {
+            e[i] = mad_lo_cc(f.q(0), m, e[i]);
+            e[i + 1] = madc_hi_cc(f.q(0), m, e[i + 1]);
+#pragma unroll
+            for (int j = 2; j < N; j += 2) {
+                e[i + j] = madc_lo_cc(f.q(j), m, e[i + j]);
+                e[i + j + 1] = madc_hi_cc(f.q(j), m, e[i + j + 1]);
+            }
+            cc[i] = addc(cc[i], 0);
+            o[i] = mad_lo_cc(f.q(1), m, o[i]);
+            o[i + 1] = madc_hi_cc(f.q(1), m, o[i + 1]);
+#pragma unroll
+            for (int j = 3; j < N; j += 2) {
+                o[i + j - 1] = madc_lo_cc(f.q(j), m, o[i + j - 1]);
+                o[i + j] = madc_hi_cc(f.q(j), m, o[i + j]);
+            }
+            cc[i + 1] = addc(cc[i + 1], 0);
+        } else {
+            o[i - 1] = mad_lo_cc(f.q(0), m, o[i - 1]);
+            o[i] = madc_hi_cc(f.q(0), m, o[i]);
+#pragma unroll
+            for (int j = 2; j < N; j += 2) {
+                o[i + j - 1] = madc_lo_cc(f.q(j), m, o[i + j - 1]);
+                o[i + j] = madc_hi_cc(f.q(j), m, o[i + j]);
+            }
+            cc[i] = addc(cc[i], 0);
+            e[i + 1] = mad_lo_cc(f.q(1), m, e[i + 1]);
+            e[i + 2] = madc_hi_cc(f.q(1), m, e[i + 2]);
+#pragma unroll
+            for (int j = 3; j < N; j += 2) {
+                e[i + j] = madc_lo_cc(f.q(j), m, e[i + j]);
+                e[i + j + 1] = madc_hi_cc(f.q(j), m, e[i + j + 1]);
+            }
+            cc[i + 1] = addc(cc[i + 1], 0);
+        }
+        // position i now sums to 0 mod 2^32; what it carries into position i + 1:
+        const uint32_t s1 = add_cc(e[i], i ? o[i - 1] : 0u);
+        const uint32_t k1 = addc(0, 0);
+        add_cc(s1, c);
+        c = addc(k1, 0);
+    }
+    // high half: e[N + k] + o[N + k - 1] + cc[k] (+ c at k = 0)
+    fel<F> r;
+    r.w[0] = add_cc(e[N], o[N - 1]);
+#pragma unroll
+    for (int k = 1; k < N; ++k) r.w[k] = addc_cc(e[N + k], o[N + k - 1]);
+    uint32_t top = addc(cc[N], 0);
+    r.w[0] = add_cc(r.w[0], c);
+#pragma unroll
+    for (int k = 1; k < N; ++k) r.w[k] = addc_cc(r.w[k], 0);
+    top = addc(top, 0);
+    r.w[0] = add_cc(r.w[0], cc[0]);
+#pragma unroll
+    for (int k = 1; k < N; ++k) r.w[k] = addc_cc(r.w[k], cc[k]);
+    top = addc(top, 0);
+    return final_sub(f, r, top);
+}
+// the same from a merged 2N-limb value
+template <class F>
+GECC_HD fel<F> redc_ws(const F& f, const uint32_t* t) {
+    constexpr int N = F::N;
+    uint32_t e[2 * N], o[2 * N];
+#pragma unroll
+    for (int k = 0; k < 2 * N; ++k) {
+        e[k] = t[k];
+        o[k] = 0;
+    }
+    return redc_ws_eo(f, e, o);
 }
 
 // Generic REDC for any odd q (reference: reduce_generic_raw, field.cpp:50-78, same
@@ -590,7 +684,7 @@ GECC_HD fel<F> redc(const F& f, const uint32_t* t) {
     if constexpr (F::kind == KIND_SECP_P) return redc_secp(f, t);
     else if constexpr (F::kind == KIND_SECP_LAZY) return redc_secp_lazy(t);
     else if constexpr (F::kind == KIND_SM2_P) return redc_sm2(f, t);
-    else return redc_generic(f, t);
+    else return redc_ws(f, t);
 }
 
 // ---------------------------------------------------------------- mul / sqr
@@ -612,6 +706,11 @@ inline OpCounters& op_counters() {
 template <class F>
 GECC_HD fel<F> fe_mul_inl(const F& f, const fel<F>& a, const fel<F>& b) {
     GECC_COUNT(mul, F);
+    if constexpr (F::kind == KIND_GENERIC) {  // reduce the unmerged product: no merge pass in between
+        uint32_t e[2 * F::N], o[2 * F::N];
+        mul_wide_eo<F::N>(e, o, a.w, b.w);
+        return redc_ws_eo(f, e, o);
+    }
     uint32_t t[2 * F::N];
     mul_wide_n<F::N>(t, a.w, b.w);
     return redc(f, t);
