@@ -771,8 +771,73 @@ k_msm_red_weighted(const uint32_t* __restrict__ marg, uint32_t* __restrict__ wsu
     if (lane == 0) jac_store<NL>(wsum, cnt, w * 4 + k, R);
 }
 
+// Doubling of one point by a GROUP of four adjacent lanes: the seven products of dbl-2009-l
+// (a = 0) have depth three, the eight of dbl-2001-b (a = -3) depth four, so the lanes run one
+// product each per level and exchange the
+// results with shuffles; every lane of the group holds the whole point before and after.  A
+// chain of dependent doublings run by a single warp is pure latency: three products per
+// doubling instead of seven.  All 32 lanes of the warp must call (full-mask shuffles).
+template <int N>
+__device__ __forceinline__ feN<N> fe_from_lane(const feN<N>& v, int src) {
+    feN<N> r;
+#pragma unroll
+    for (int i = 0; i < N; ++i) r.w[i] = __shfl_sync(0xFFFFFFFFu, v.w[i], src);
+    return r;
+}
 template <class C>
-__global__ void __launch_bounds__(32)
+__device__ __forceinline__ cjac<C> jac_dbl_group4(const cjac<C>& p, int lane) {
+    static_assert(C::a_kind == A_ZERO || C::a_kind == A_MINUS3, "group doubling: a = 0 or a = -3");
+    using fe = cfe<C>;
+    const typename C::Fp f{};
+    const int r = lane & 3, base = lane & ~3;
+    if constexpr (C::a_kind == A_MINUS3) {  // dbl-2001-b: eight products in four levels
+        // level 1: Z^2 | Y^2 | (Y + Z)^2
+        fe u = fe_select(r == 0, p.Z, fe_select(r == 1, p.Y, fe_add(f, p.Y, p.Z)));
+        const fe l1 = fe_mul_inl(f, u, u);
+        const fe delta = fe_from_lane(l1, base), gamma = fe_from_lane(l1, base + 1), yz2 = fe_from_lane(l1, base + 2);
+        // level 2: X gamma | (X - delta)(X + delta)
+        u = fe_select(r == 0, p.X, fe_sub(f, p.X, delta));
+        fe v = fe_select(r == 0, gamma, fe_add(f, p.X, delta));
+        const fe l2 = fe_mul_inl(f, u, v);
+        const fe beta = fe_from_lane(l2, base), t = fe_from_lane(l2, base + 1);
+        const fe alpha = fe_add(f, fe_dbl(f, t), t);
+        // level 3: alpha^2 | gamma^2
+        u = fe_select(r == 0, alpha, gamma);
+        const fe l3 = fe_mul_inl(f, u, u);
+        const fe alpha2 = fe_from_lane(l3, base), gamma2 = fe_from_lane(l3, base + 1);
+        const fe beta4 = fe_dbl(f, fe_dbl(f, beta));
+        cjac<C> o;
+        o.X = fe_sub(f, alpha2, fe_dbl(f, beta4));
+        o.Z = fe_sub(f, fe_sub(f, yz2, gamma), delta);
+        // level 4: alpha (4 beta - X3), the same on every lane
+        o.Y = fe_sub(f, fe_mul_inl(f, alpha, fe_sub(f, beta4, o.X)), fe_mul8(f, gamma2));
+        return o;
+    }
+    // level 1: X^2 | Y^2 | Y Z
+    fe u = fe_select(r == 1 || r == 2, p.Y, p.X);
+    fe v = fe_select(r == 2, p.Z, u);
+    const fe l1 = fe_mul_inl(f, u, v);
+    const fe A = fe_from_lane(l1, base), B = fe_from_lane(l1, base + 1), YZ = fe_from_lane(l1, base + 2);
+    // level 2: B^2 | (X + B)^2 | (3A)^2
+    const fe E = fe_add(f, fe_dbl(f, A), A);
+    u = fe_select(r == 1, fe_add(f, p.X, B), fe_select(r == 2, E, B));
+    const fe l2 = fe_mul_inl(f, u, u);
+    const fe Cc = fe_from_lane(l2, base), T = fe_from_lane(l2, base + 1), F = fe_from_lane(l2, base + 2);
+    fe D = fe_dbl(f, fe_sub(f, fe_sub(f, T, A), Cc));
+    cjac<C> o;
+    o.X = fe_sub(f, F, fe_dbl(f, D));
+    // level 3: E (D - X3), the same on every lane
+    o.Y = fe_sub(f, fe_mul_inl(f, E, fe_sub(f, D, o.X)), fe_mul8(f, Cc));
+    o.Z = fe_dbl(f, YZ);
+    return o;
+}
+
+// Window combine.  Groups of four lanes own one window each (17 windows -> 3 warps): S_w by
+// Horner over its three weighted marginals, then the shift by 2^(16 w) -- doublings by the lane
+// group; warp 0 then tree-sums the windows.
+constexpr int MSM_COMBINE_THREADS = 96;
+template <class C>
+__global__ void __launch_bounds__(MSM_COMBINE_THREADS)
 k_msm_red_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, uint32_t* __restrict__ oy,
                   uint8_t* __restrict__ oinf) {
     using fe = cfe<C>;
@@ -780,33 +845,54 @@ k_msm_red_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, 
     using aff = caff<C>;
     constexpr int NL = C::Fp::N;
     (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
-    const uint32_t w = threadIdx.x;
+    static_assert(MSM_WINDOWS * 4 <= MSM_COMBINE_THREADS, "one lane group per window");
+    __shared__ uint32_t win[3 * NL * 32];
+    const int lane = threadIdx.x & 31;
+    const uint32_t w = threadIdx.x >> 2;  // window of this lane group
     const size_t cnt = (size_t)MSM_WINDOWS * 4;
+    const bool live = w < MSM_WINDOWS;
+    auto dbl = [&](const jac& p) -> jac {
+        if constexpr (C::a_kind == A_ZERO || C::a_kind == A_MINUS3) return jac_dbl_group4<C>(p, lane);
+        else return jac_dbl_flat<C>(p);
+    };
     jac s = jac_infinity<C>();
-    if (w < MSM_WINDOWS) {
-        s = jac_load<NL>(wsum, cnt, w * 4 + 2);
+    if (live) s = jac_load<NL>(wsum, cnt, w * 4 + 2);
 #pragma unroll 1
-        for (int i = 0; i < 5; ++i) s = jac_dbl_flat<C>(s);
-        s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 1));
+    for (int i = 0; i < 5; ++i) s = dbl(s);
+    if (live) s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 1));
 #pragma unroll 1
-        for (int i = 0; i < 5; ++i) s = jac_dbl_flat<C>(s);
+    for (int i = 0; i < 5; ++i) s = dbl(s);
+    if (live) {
         s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 0));
         s = jac_add<C>(s, jac_load<NL>(wsum, cnt, w * 4 + 3));
-        // an empty window (the carry window almost always is) has nothing to shift: the warp's
-        // chain is then as long as its highest non-empty window
-        const uint32_t reps = jac_is_inf<C>(s) ? 0u : MSM_C * w;
-#pragma unroll 1
-        for (uint32_t i = 0; i < reps; ++i) s = jac_dbl_flat<C>(s);
     }
-    s = warp_sum_points<C>(s, (int)w);
-    if (w == 0) {
+    // an empty window (the carry window almost always is) has nothing to shift; the loop runs as
+    // long as the warp's highest non-empty window needs (uniform trip count: shuffles inside)
+    uint32_t reps = live && !jac_is_inf<C>(s) ? MSM_C * w : 0u;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, reps, d);
+        reps = other > reps ? other : reps;
+    }
+    const uint32_t mine = live && !jac_is_inf<C>(s) ? MSM_C * w : 0u;
+#pragma unroll 1
+    for (uint32_t i = 0; i < reps; ++i) {
+        const jac t = dbl(s);
+        if (i < mine) s = t;
+    }
+    if ((threadIdx.x & 3) == 0) jac_store<NL>(win, 32, threadIdx.x >> 2, s);  // groups 0..23
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+    jac acc = lane < MSM_WINDOWS ? jac_load<NL>(win, 32, lane) : jac_infinity<C>();
+    acc = warp_sum_points<C>(acc, lane);
+    if (lane == 0) {
         const typename C::Fp f{};
-        if (jac_is_inf<C>(s)) {
+        if (jac_is_inf<C>(acc)) {
             col_store(ox, 1, 0, fe_zero_n<NL>());
             col_store(oy, 1, 0, fe_zero_n<NL>());
             oinf[0] = 1;
         } else {
-            aff a = jac_to_aff_with<C>(s, fe_inv(f, s.Z));
+            aff a = jac_to_aff_with<C>(acc, fe_inv(f, acc.Z));
             col_store(ox, 1, 0, a.x);
             col_store(oy, 1, 0, a.y);
             oinf[0] = 0;
@@ -947,7 +1033,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
         k_msm_red_parts<C><<<(MSM_RED_PARTS + 127) / 128, 128, 0, s>>>(m, keys2, starts, slots, sinf, parts);
         k_msm_red_fold<C><<<(MSM_WINDOWS * 3 * 32 * 32 + 127) / 128, 128, 0, s>>>(parts, marg);
         k_msm_red_weighted<C><<<(MSM_WINDOWS * 3 * 32 + 127) / 128, 128, 0, s>>>(marg, wsum);
-        k_msm_red_combine<C><<<1, 32, 0, s>>>(wsum, ox, oy, oinf);
+        k_msm_red_combine<C><<<1, MSM_COMBINE_THREADS, 0, s>>>(wsum, ox, oy, oinf);
         *launches = 3 + (split ? 3 : 1) * MSM_TREE_LEVELS + 4 + 4;  // + the sort's passes
         return cudaGetLastError();
     } else {
