@@ -47,6 +47,7 @@ struct sm2b_ctx {
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
     cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;  // copy engines of the pipelined host API
+    cudaStream_t aux_stream = nullptr;  // second compute stream: consecutive chunk kernels overlap their tails
     sm2b_op_counts ledger{0, 0, 0, 0};
     uint64_t launches = 0;
     std::string last_error;
@@ -131,7 +132,8 @@ sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device) {
     if (cudaGetDeviceProperties(&prop, device) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking) != cudaSuccess) {
         delete ctx;
         return nullptr;
     }
@@ -196,6 +198,7 @@ void sm2b_ctx_free(sm2b_ctx* ctx) {
         if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
         if (ctx->h2d_stream) cudaStreamDestroy(ctx->h2d_stream);
         if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
+        if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
     }
     delete ctx;
 }
@@ -350,20 +353,32 @@ Ledger ledger_of(sm2b_ctx* ctx) { return Ledger{&ctx->ledger, ctx->lanes, ctx->w
 } // extern "C"
 namespace {
 constexpr size_t PIPE_MIN_CHUNK = (size_t)1 << 17;
+constexpr size_t PIPE_HEAD_CHUNK = (size_t)1 << 16;
 constexpr int PIPE_MAX_CHUNKS = 4;
 
+// Up to PIPE_MAX_CHUNKS equal chunks of at least PIPE_MIN_CHUNK records, preceded -- when the
+// batch is large enough -- by a short head chunk: only the first upload is exposed (nothing
+// can run before it), so it should be small; the chunk kernels overlap on two streams, so a
+// small head does not cost a wave of its own.
 struct Chunks {
-    size_t count, size;
+    size_t count, size;  // size: the largest chunk
     int n;
-    explicit Chunks(size_t total) : count(total) {
-        n = (int)(total / PIPE_MIN_CHUNK);
-        if (n < 1) n = 1;
-        if (n > PIPE_MAX_CHUNKS) n = PIPE_MAX_CHUNKS;
-        size = (total + n - 1) / n;
-        n = (int)((total + size - 1) / size);
+    size_t off[PIPE_MAX_CHUNKS + 2];
+    explicit Chunks(size_t total, bool with_head = true) : count(total) {
+        size_t head = with_head && total >= 4 * PIPE_MIN_CHUNK ? PIPE_HEAD_CHUNK : 0;
+        const size_t rest = total - head;
+        int k = (int)(rest / PIPE_MIN_CHUNK);
+        if (k < 1) k = 1;
+        if (k > PIPE_MAX_CHUNKS) k = PIPE_MAX_CHUNKS;
+        size = (rest + k - 1) / k;
+        n = 0;
+        off[0] = 0;
+        if (head) off[++n] = head;
+        for (size_t at = head; at < total; at += size) off[++n] = at + size < total ? at + size : total;
+        if (n == 0) off[++n] = total;  // total == 0 never reaches here; keeps the invariant anyway
     }
-    size_t begin(int c) const { return (size_t)c * size; }
-    size_t len(int c) const { return begin(c) + size <= count ? size : count - begin(c); }
+    size_t begin(int c) const { return off[c]; }
+    size_t len(int c) const { return off[c + 1] - off[c]; }
 };
 
 struct EventPool {  // events of one pipelined call; destroyed at scope exit
@@ -428,12 +443,15 @@ sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
     uint8_t* ds = ci.take<uint8_t>(64 * count);
     uint8_t* dr = (uint8_t*)ctx->out.p;
     const Chunks ch(count);
-    const size_t tab_lanes = ensure_lane_tabs(ctx, ch.size);
+    // chunk kernels alternate between two compute streams (the tail of one chunk overlaps the
+    // head of the next), each with its own half of the lane-table scratch
+    const size_t tab_half = ensure_lane_tabs(ctx, 2 * ch.size) / 2;
     EventPool pool;
     // the arenas may still be in use by earlier work on the compute stream
     cudaEvent_t idle = pool.get();
     CU(ctx, cudaEventRecord(idle, ctx->stream));
     CU(ctx, cudaStreamWaitEvent(ctx->h2d_stream, idle, 0));
+    CU(ctx, cudaStreamWaitEvent(ctx->aux_stream, idle, 0));
     for (int c = 0; c < ch.n; ++c) {
         const size_t b = ch.begin(c), m = ch.len(c);
         CU(ctx, cudaMemcpyAsync(dd + 32 * b, digests + 32 * b, 32 * m, cudaMemcpyHostToDevice, ctx->h2d_stream));
@@ -441,10 +459,12 @@ sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
         CU(ctx, cudaMemcpyAsync(ds + 64 * b, signatures + 64 * b, 64 * m, cudaMemcpyHostToDevice, ctx->h2d_stream));
         cudaEvent_t up = pool.get(), done = pool.get();
         CU(ctx, cudaEventRecord(up, ctx->h2d_stream));
-        CU(ctx, cudaStreamWaitEvent(ctx->stream, up, 0));
-        CU(ctx, launch_verify(ctx->curve, m, dd + 32 * b, dp + 65 * b, ds + 64 * b, ctx->gtab_rec, dr + b,
-                              (uint32_t*)ctx->lane_tabs.p, tab_lanes, ctx->stream));
-        CU(ctx, cudaEventRecord(done, ctx->stream));
+        cudaStream_t ks = (c & 1) ? ctx->aux_stream : ctx->stream;
+        uint32_t* tabs = (uint32_t*)ctx->lane_tabs.p + (size_t)(c & 1) * tab_half * 128;  // 512 B per lane
+        CU(ctx, cudaStreamWaitEvent(ks, up, 0));
+        CU(ctx, launch_verify(ctx->curve, m, dd + 32 * b, dp + 65 * b, ds + 64 * b, ctx->gtab_rec, dr + b, tabs,
+                              tab_half, ks));
+        CU(ctx, cudaEventRecord(done, ks));
         CU(ctx, cudaStreamWaitEvent(ctx->d2h_stream, done, 0));
         CU(ctx, cudaMemcpyAsync(results + b, dr + b, m, cudaMemcpyDeviceToHost, ctx->d2h_stream));
     }
@@ -455,6 +475,7 @@ sm2b_status sm2b_verify(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
     led_upmul(ledger_of(ctx), count);
     led_padd(ledger_of(ctx), count);
     CU(ctx, cudaStreamSynchronize(ctx->d2h_stream));
+    CU(ctx, cudaStreamSynchronize(ctx->aux_stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     return SM2B_OK;
 }
@@ -519,12 +540,13 @@ sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const
     uint8_t* dsec = ci.take<uint8_t>(32 * count);
     uint8_t* dsig = co.take<uint8_t>(64 * count);
     int32_t* dst = co.take<int32_t>(count);
-    const Chunks ch(count);
+    const Chunks ch(count, false);  // all secrets follow chunk 0 anyway: a short head would only idle the GPU
     EventPool pool;
     cudaEvent_t idle = pool.get();
     CU(ctx, cudaEventRecord(idle, ctx->stream));
     CU(ctx, cudaStreamWaitEvent(ctx->h2d_stream, idle, 0));
     CU(ctx, cudaStreamWaitEvent(ctx->d2h_stream, idle, 0));
+    CU(ctx, cudaStreamWaitEvent(ctx->aux_stream, idle, 0));
     CU(ctx, cudaMemsetAsync(ctx->flags, 0, 4, ctx->h2d_stream));
     // A zero or oversize secret must fail the whole call before any output is written
     // (capi.cpp:181-184).  Chunk 0 goes up first and starts signing; all remaining secrets follow
@@ -540,11 +562,14 @@ sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const
         CU(ctx, cudaMemcpyAsync(dd + 32 * b, digests + 32 * b, 32 * m, cudaMemcpyHostToDevice, ctx->h2d_stream));
         cudaEvent_t up = pool.get();
         CU(ctx, cudaEventRecord(up, ctx->h2d_stream));
-        CU(ctx, cudaStreamWaitEvent(ctx->stream, up, 0));
+        // chunk kernels alternate between two streams: a chunk is a fraction of a wave short of
+        // filling the chip, and the next chunk's blocks take the free slots
+        cudaStream_t ks = (c & 1) ? ctx->aux_stream : ctx->stream;
+        CU(ctx, cudaStreamWaitEvent(ks, up, 0));
         CU(ctx, launch_sign(ctx->curve, m, dd + 32 * b, dsec + 32 * b, nonce_seed, lane_base + b, ctx->gtab_rec,
-                            dsig + 64 * b, dst + b, ctx->flags, ctx->stream));
+                            dsig + 64 * b, dst + b, ctx->flags, ks));
         done[c] = pool.get();
-        CU(ctx, cudaEventRecord(done[c], ctx->stream));
+        CU(ctx, cudaEventRecord(done[c], ks));
         if (c == 0) {  // the rest of the secrets, their check, the verdict
             if (count > m) {
                 CU(ctx, cudaMemcpyAsync(dsec + 32 * m, secrets + 32 * m, 32 * (count - m), cudaMemcpyHostToDevice,
@@ -565,6 +590,7 @@ sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const
     CU(ctx, cudaEventSynchronize(verdict));
     if (*ctx->hflag) {  // nothing has been copied out; let the queued kernels drain
         CU(ctx, cudaStreamSynchronize(ctx->stream));
+        CU(ctx, cudaStreamSynchronize(ctx->aux_stream));
         return SM2B_ERROR_MALFORMED_INPUT;
     }
     // per-lane statuses go straight into the caller's array (no host-side pass over the lanes)
@@ -581,6 +607,7 @@ sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests, const
         CU(ctx, cudaMemcpyAsync(st_dst + b, dst + b, 4 * m, cudaMemcpyDeviceToHost, ctx->d2h_stream));
     }
     CU(ctx, cudaStreamSynchronize(ctx->d2h_stream));
+    CU(ctx, cudaStreamSynchronize(ctx->aux_stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     if (lane_status) return SM2B_OK;  // report_lanes (capi.cpp:64-73): statuses delivered, call is OK
     return report_lanes(hst.data(), count, nullptr);
