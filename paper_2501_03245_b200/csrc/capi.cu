@@ -59,6 +59,8 @@ struct sm2b_ctx {
     uint32_t* flags = nullptr;  // device word: malformed-call flag of sign / ecdh
     int limbs = 8;              // 32-bit limbs per coordinate (12 on BLS12-381)
     uint32_t* hflag = nullptr;  // pinned host word: the flag comes back without blocking the enqueueing thread
+    bool ledger_hold = false;   // a pipelined host call runs its chunks with the ledger held and accounts once
+    sm2b_op_counts ledger_sink{0, 0, 0, 0};
 };
 
 namespace {
@@ -342,7 +344,9 @@ void led_fpmul(const Ledger& L, uint64_t n) {
 void led_upmul(const Ledger& L, uint64_t n) {
     if (n) led(L, 256 * (14 * n + 3 * (eff_lanes(L, n) - 1)), 256 * 5 * n, 256 * 11 * n, 256);
 }
-Ledger ledger_of(sm2b_ctx* ctx) { return Ledger{&ctx->ledger, ctx->lanes, ctx->workers}; }
+Ledger ledger_of(sm2b_ctx* ctx) {
+    return Ledger{ctx->ledger_hold ? &ctx->ledger_sink : &ctx->ledger, ctx->lanes, ctx->workers};
+}
 }  // namespace
 
 // ------------------------------------------------------------------ host-API pipeline
@@ -750,47 +754,90 @@ struct HostPoints {
     const uint32_t* y;
     const uint8_t* inf;
 };
-template <class Body>
+// `body(m, ...)` enqueues the kernel for m elements on ctx->stream; `account()` advances the
+// ledger once for the whole call.  Large batches are cut into chunks: every chunk has its own
+// compact column buffers on the device (count = chunk length, so the kernels are unchanged),
+// filled and drained with strided 2-D copies, and upload / kernel / download of successive
+// chunks overlap on three streams (PCIe is full duplex).
+template <class Body, class Account>
 sm2b_status run_points(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const HostPoints* p,
-                       const HostPoints* t, uint32_t* ox, uint32_t* oy, uint8_t* oinf, Body body) {
+                       const HostPoints* t, uint32_t* ox, uint32_t* oy, uint8_t* oinf, Body body,
+                       Account account) {
     const size_t L = (size_t)ctx->limbs, pb = 4 * L * n;  // bytes per coordinate column buffer
     const size_t cb = Carver::need(pb), mb = Carver::need(n);
     uint32_t *dk = nullptr, *dpx = nullptr, *dpy = nullptr, *dtx = nullptr, *dty = nullptr;
     uint8_t *dpi = nullptr, *dti = nullptr;
     uint32_t *dox, *doy;
     uint8_t* doi;
-    {
-        std::lock_guard<std::mutex> lk(ctx->mu);
-        DeviceGuard g(ctx->device);
-        CU(ctx, ctx->in.ensure(5 * cb + 2 * mb));
-        CU(ctx, ctx->out.ensure(2 * cb + mb));
-        Carver ci(ctx->in.p), co(ctx->out.p);
-        dox = co.take<uint32_t>(L * n);
-        doy = co.take<uint32_t>(L * n);
-        doi = co.take<uint8_t>(n);
-        auto up = [&](const void* h, size_t bytes, void* d) {
-            return cudaMemcpyAsync(d, h, bytes, cudaMemcpyHostToDevice, ctx->stream);
-        };
-        if (scalars) { dk = ci.take<uint32_t>(8 * n); CU(ctx, up(scalars, 32 * n, dk)); }
-        if (p) {
-            dpx = ci.take<uint32_t>(L * n); dpy = ci.take<uint32_t>(L * n);
-            CU(ctx, up(p->x, pb, dpx)); CU(ctx, up(p->y, pb, dpy));
-            if (p->inf) { dpi = ci.take<uint8_t>(n); CU(ctx, up(p->inf, n, dpi)); }
-        }
-        if (t) {
-            dtx = ci.take<uint32_t>(L * n); dty = ci.take<uint32_t>(L * n);
-            CU(ctx, up(t->x, pb, dtx)); CU(ctx, up(t->y, pb, dty));
-            if (t->inf) { dti = ci.take<uint8_t>(n); CU(ctx, up(t->inf, n, dti)); }
-        }
-    }
-    sm2b_status st = body(dk, dpx, dpy, dpi, dtx, dty, dti, dox, doy, doi);
-    if (st != SM2B_OK) return st;
-    std::lock_guard<std::mutex> lk(ctx->mu);
+    const Chunks ch(n >= ((size_t)1 << 19) ? n : 1, false);  // small batches: one chunk, one copy each
+    const int chunks = n >= ((size_t)1 << 19) ? ch.n : 1;
+    std::unique_lock<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
-    CU(ctx, cudaMemcpyAsync(ox, dox, pb, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaMemcpyAsync(oy, doy, pb, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaMemcpyAsync(oinf, doi, n, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaStreamSynchronize(ctx->stream));
+    CU(ctx, ctx->in.ensure(5 * cb + 2 * mb));
+    CU(ctx, ctx->out.ensure(2 * cb + mb));
+    Carver ci(ctx->in.p), co(ctx->out.p);
+    dox = co.take<uint32_t>(L * n);
+    doy = co.take<uint32_t>(L * n);
+    doi = co.take<uint8_t>(n);
+    if (scalars) dk = ci.take<uint32_t>(8 * n);
+    if (p) {
+        dpx = ci.take<uint32_t>(L * n); dpy = ci.take<uint32_t>(L * n);
+        if (p->inf) dpi = ci.take<uint8_t>(n);
+    }
+    if (t) {
+        dtx = ci.take<uint32_t>(L * n); dty = ci.take<uint32_t>(L * n);
+        if (t->inf) dti = ci.take<uint8_t>(n);
+    }
+    EventPool pool;
+    cudaEvent_t idle = pool.get();
+    CU(ctx, cudaEventRecord(idle, ctx->stream));
+    CU(ctx, cudaStreamWaitEvent(ctx->h2d_stream, idle, 0));
+    CU(ctx, cudaStreamWaitEvent(ctx->d2h_stream, idle, 0));
+    ctx->ledger_hold = true;
+    sm2b_status st = SM2B_OK;
+    for (int c = 0; c < chunks && st == SM2B_OK; ++c) {
+        const size_t b = chunks == 1 ? 0 : ch.begin(c), m = chunks == 1 ? n : ch.len(c);
+        // rows x m block of a host column buffer (row pitch n) -> compact device block (row pitch m)
+        auto up = [&](const uint32_t* h, uint32_t* d, size_t rows) {
+            return cudaMemcpy2DAsync(d + rows * b, 4 * m, h + b, 4 * n, 4 * m, rows, cudaMemcpyHostToDevice,
+                                     ctx->h2d_stream);
+        };
+        auto upm = [&](const uint8_t* h, uint8_t* d) {
+            return cudaMemcpyAsync(d + b, h + b, m, cudaMemcpyHostToDevice, ctx->h2d_stream);
+        };
+        cudaError_t e = cudaSuccess;
+        if (scalars && e == cudaSuccess) e = up(scalars, dk, 8);
+        if (p && e == cudaSuccess) e = up(p->x, dpx, L);
+        if (p && e == cudaSuccess) e = up(p->y, dpy, L);
+        if (p && p->inf && e == cudaSuccess) e = upm(p->inf, dpi);
+        if (t && e == cudaSuccess) e = up(t->x, dtx, L);
+        if (t && e == cudaSuccess) e = up(t->y, dty, L);
+        if (t && t->inf && e == cudaSuccess) e = upm(t->inf, dti);
+        cudaEvent_t upe = pool.get(), done = pool.get();
+        if (e == cudaSuccess) e = cudaEventRecord(upe, ctx->h2d_stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->stream, upe, 0);
+        if (e != cudaSuccess) { ctx->ledger_hold = false; return fail(ctx, "run_points upload", e); }
+        lk.unlock();  // the _dev entry points take the lock themselves
+        st = body(m, dk ? dk + 8 * b : nullptr, dpx ? dpx + L * b : nullptr, dpy ? dpy + L * b : nullptr,
+                  dpi ? dpi + b : nullptr, dtx ? dtx + L * b : nullptr, dty ? dty + L * b : nullptr,
+                  dti ? dti + b : nullptr, dox + L * b, doy + L * b, doi + b);
+        lk.lock();
+        if (st != SM2B_OK) break;
+        e = cudaEventRecord(done, ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(ctx->d2h_stream, done, 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(ox + b, 4 * n, dox + L * b, 4 * m, 4 * m, L, cudaMemcpyDeviceToHost, ctx->d2h_stream);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(oy + b, 4 * n, doy + L * b, 4 * m, 4 * m, L, cudaMemcpyDeviceToHost, ctx->d2h_stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(oinf + b, doi + b, m, cudaMemcpyDeviceToHost, ctx->d2h_stream);
+        if (e != cudaSuccess) { ctx->ledger_hold = false; return fail(ctx, "run_points download", e); }
+    }
+    ctx->ledger_hold = false;
+    cudaError_t e1 = cudaStreamSynchronize(ctx->d2h_stream), e2 = cudaStreamSynchronize(ctx->stream);
+    if (st != SM2B_OK) return st;
+    if (e1 != cudaSuccess) return fail(ctx, "run_points sync", e1);
+    if (e2 != cudaSuccess) return fail(ctx, "run_points sync", e2);
+    account();
     return SM2B_OK;
 }
 }  // namespace
@@ -828,10 +875,11 @@ sm2b_status gecc_batch_padd(sm2b_ctx* ctx, size_t n, const uint32_t* px, const u
     if (n == 0) return SM2B_OK;
     HostPoints p{px, py, pinf}, t{tx, ty, tinf};
     return run_points(ctx, n, nullptr, &p, &t, ox, oy, oinf,
-                      [&](uint32_t*, uint32_t* dpx, uint32_t* dpy, uint8_t* dpi, uint32_t* dtx,
+                      [&](size_t m, uint32_t*, uint32_t* dpx, uint32_t* dpy, uint8_t* dpi, uint32_t* dtx,
                           uint32_t* dty, uint8_t* dti, uint32_t* dox, uint32_t* doy, uint8_t* doi) {
-                          return gecc_batch_padd_dev(ctx, n, dpx, dpy, dpi, dtx, dty, dti, dox, doy, doi);
-                      });
+                          return gecc_batch_padd_dev(ctx, m, dpx, dpy, dpi, dtx, dty, dti, dox, doy, doi);
+                      },
+                      [&] { led_padd(ledger_of(ctx), n); });
 }
 sm2b_status gecc_batch_pdbl(sm2b_ctx* ctx, size_t n, const uint32_t* px, const uint32_t* py,
                             const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
@@ -839,10 +887,11 @@ sm2b_status gecc_batch_pdbl(sm2b_ctx* ctx, size_t n, const uint32_t* px, const u
     if (n == 0) return SM2B_OK;
     HostPoints p{px, py, pinf};
     return run_points(ctx, n, nullptr, &p, nullptr, ox, oy, oinf,
-                      [&](uint32_t*, uint32_t* dpx, uint32_t* dpy, uint8_t* dpi, uint32_t*, uint32_t*,
+                      [&](size_t m, uint32_t*, uint32_t* dpx, uint32_t* dpy, uint8_t* dpi, uint32_t*, uint32_t*,
                           uint8_t*, uint32_t* dox, uint32_t* doy, uint8_t* doi) {
-                          return gecc_batch_pdbl_dev(ctx, n, dpx, dpy, dpi, dox, doy, doi);
-                      });
+                          return gecc_batch_pdbl_dev(ctx, m, dpx, dpy, dpi, dox, doy, doi);
+                      },
+                      [&] { led(ledger_of(ctx), 7 * n - 3, 4 * n, 4 * n, 1); });
 }
 sm2b_status gecc_batch_fpmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, uint32_t* ox,
                              uint32_t* oy, uint8_t* oinf) {
@@ -850,10 +899,11 @@ sm2b_status gecc_batch_fpmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, u
     if (!ctx || (n > 0 && (!scalars || !ox || !oy || !oinf))) return SM2B_ERROR_INVALID_ARGUMENT;
     if (n == 0) return SM2B_OK;
     return run_points(ctx, n, scalars, nullptr, nullptr, ox, oy, oinf,
-                      [&](uint32_t* dk, uint32_t*, uint32_t*, uint8_t*, uint32_t*, uint32_t*, uint8_t*,
+                      [&](size_t m, uint32_t* dk, uint32_t*, uint32_t*, uint8_t*, uint32_t*, uint32_t*, uint8_t*,
                           uint32_t* dox, uint32_t* doy, uint8_t* doi) {
-                          return gecc_batch_fpmul_dev(ctx, n, dk, dox, doy, doi);
-                      });
+                          return gecc_batch_fpmul_dev(ctx, m, dk, dox, doy, doi);
+                      },
+                      [&] { led_fpmul(ledger_of(ctx), n); });
 }
 sm2b_status gecc_batch_upmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uint32_t* px,
                              const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
@@ -864,10 +914,11 @@ sm2b_status gecc_batch_upmul(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, c
     if (n == 0) return SM2B_OK;
     HostPoints p{px, py, pinf};
     return run_points(ctx, n, scalars, &p, nullptr, ox, oy, oinf,
-                      [&](uint32_t* dk, uint32_t* dpx, uint32_t* dpy, uint8_t* dpi, uint32_t*, uint32_t*,
+                      [&](size_t m, uint32_t* dk, uint32_t* dpx, uint32_t* dpy, uint8_t* dpi, uint32_t*, uint32_t*,
                           uint8_t*, uint32_t* dox, uint32_t* doy, uint8_t* doi) {
-                          return gecc_batch_upmul_dev(ctx, n, dk, dpx, dpy, dpi, dox, doy, doi);
-                      });
+                          return gecc_batch_upmul_dev(ctx, m, dk, dpx, dpy, dpi, dox, doy, doi);
+                      },
+                      [&] { led_upmul(ledger_of(ctx), n); });
 }
 
 // ------------------------------------------------------------------ sm2b_bench_run
