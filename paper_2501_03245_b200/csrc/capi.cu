@@ -1106,38 +1106,46 @@ sm2b_status gecc_msm(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uin
                      uint8_t* oinf) {
     if (!ctx || !ox || !oy || !oinf || (n > 0 && (!scalars || !px || !py)))
         return SM2B_ERROR_INVALID_ARGUMENT;
-    uint32_t *dk = nullptr, *dpx = nullptr, *dpy = nullptr, *dox, *doy;
-    uint8_t *dpi = nullptr, *doi;
-    {
-        std::lock_guard<std::mutex> lk(ctx->mu);
-        DeviceGuard g(ctx->device);
-        const size_t L = (size_t)ctx->limbs;
-        const size_t cb = Carver::need(4 * L * n), mb = Carver::need(n);
-        CU(ctx, ctx->in.ensure(3 * cb + mb + 256));
-        CU(ctx, ctx->out.ensure(1024));
-        Carver ci(ctx->in.p), co(ctx->out.p);
-        dox = co.take<uint32_t>(L);
-        doy = co.take<uint32_t>(L);
-        doi = co.take<uint8_t>(1);
-        if (n) {
-            dk = ci.take<uint32_t>(8 * n);
-            dpx = ci.take<uint32_t>(L * n);
-            dpy = ci.take<uint32_t>(L * n);
-            CU(ctx, cudaMemcpyAsync(dk, scalars, 32 * n, cudaMemcpyHostToDevice, ctx->stream));
-            CU(ctx, cudaMemcpyAsync(dpx, px, 4 * L * n, cudaMemcpyHostToDevice, ctx->stream));
-            CU(ctx, cudaMemcpyAsync(dpy, py, 4 * L * n, cudaMemcpyHostToDevice, ctx->stream));
-            if (pinf) {
-                dpi = ci.take<uint8_t>(n);
-                CU(ctx, cudaMemcpyAsync(dpi, pinf, n, cudaMemcpyHostToDevice, ctx->stream));
-            }
-        }
-    }
-    sm2b_status st = gecc_msm_dev(ctx, n, dk, dpx, dpy, dpi, dox, doy, doi);
-    if (st != SM2B_OK) return st;
+    if (n >= ((size_t)1 << 31)) return SM2B_ERROR_INVALID_ARGUMENT;  // point index is 31 bits
     std::lock_guard<std::mutex> lk(ctx->mu);
     DeviceGuard g(ctx->device);
-    CU(ctx, cudaMemcpyAsync(ox, dox, 4 * ctx->limbs, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(ctx, cudaMemcpyAsync(oy, doy, 4 * ctx->limbs, cudaMemcpyDeviceToHost, ctx->stream));
+    const size_t L = (size_t)ctx->limbs;
+    const size_t cb = Carver::need(4 * L * n), mb = Carver::need(n);
+    CU(ctx, ctx->in.ensure(Carver::need(32 * n) + 2 * cb + mb + 256));
+    CU(ctx, ctx->out.ensure(1024));
+    Carver ci(ctx->in.p), co(ctx->out.p);
+    uint32_t* dox = co.take<uint32_t>(L);
+    uint32_t* doy = co.take<uint32_t>(L);
+    uint8_t* doi = co.take<uint8_t>(1);
+    if (n == 0) {  // empty sum = point at infinity
+        memset(ox, 0, 4 * L);
+        memset(oy, 0, 4 * L);
+        *oinf = 1;
+        return SM2B_OK;
+    }
+    uint32_t* dk = ci.take<uint32_t>(8 * n);
+    uint32_t* dpx = ci.take<uint32_t>(L * n);
+    uint32_t* dpy = ci.take<uint32_t>(L * n);
+    uint8_t* dpi = pinf ? ci.take<uint8_t>(n) : nullptr;
+    // scalars (and the mask) first: digit extraction and the sort run while the points upload
+    EventPool pool;
+    cudaEvent_t idle = pool.get(), scalars_up = pool.get(), points_up = pool.get();
+    CU(ctx, cudaEventRecord(idle, ctx->stream));
+    CU(ctx, cudaStreamWaitEvent(ctx->h2d_stream, idle, 0));
+    CU(ctx, cudaMemcpyAsync(dk, scalars, 32 * n, cudaMemcpyHostToDevice, ctx->h2d_stream));
+    if (pinf) CU(ctx, cudaMemcpyAsync(dpi, pinf, n, cudaMemcpyHostToDevice, ctx->h2d_stream));
+    CU(ctx, cudaEventRecord(scalars_up, ctx->h2d_stream));
+    CU(ctx, cudaMemcpyAsync(dpx, px, 4 * L * n, cudaMemcpyHostToDevice, ctx->h2d_stream));
+    CU(ctx, cudaMemcpyAsync(dpy, py, 4 * L * n, cudaMemcpyHostToDevice, ctx->h2d_stream));
+    CU(ctx, cudaEventRecord(points_up, ctx->h2d_stream));
+    CU(ctx, cudaStreamWaitEvent(ctx->stream, scalars_up, 0));
+    CU(ctx, ctx->scratch.ensure(msm_scratch_bytes(n, ctx->curve)));
+    int launches = 0;
+    CU(ctx, launch_msm(ctx->curve, n, dk, dpx, dpy, dpi, dox, doy, doi, ctx->scratch.p, ctx->stream, &launches,
+                       points_up));
+    ctx->launches += launches;
+    CU(ctx, cudaMemcpyAsync(ox, dox, 4 * L, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(ctx, cudaMemcpyAsync(oy, doy, 4 * L, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaMemcpyAsync(oinf, doi, 1, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaStreamSynchronize(ctx->stream));
     return SM2B_OK;

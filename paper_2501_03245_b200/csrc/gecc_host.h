@@ -78,6 +78,7 @@ size_t msm_scratch_bytes(size_t n, int curve);
 void set_msm_form(int form);  // 0 default (batch-affine), 1 mixed-Jacobian slices, 2 batch-affine tree
 cudaError_t launch_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px,
                        const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
-                       uint8_t* oinf, void* scratch, cudaStream_t s, int* launches);
+                       uint8_t* oinf, void* scratch, cudaStream_t s, int* launches,
+                       cudaEvent_t points_ready = nullptr);  // waited for before the first read of px / py
 
 }  // namespace gecc

@@ -989,7 +989,7 @@ static cudaError_t launch_tree(int curve, size_t m, int level, const TreeBufs& b
 template <class C>
 static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px, const uint32_t* py,
                            const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
-                           void* scratch, cudaStream_t s, int* launches) {
+                           void* scratch, cudaStream_t s, int* launches, cudaEvent_t points_ready) {
     constexpr int NL = C::Fp::N;
     MsmPlan p = msm_plan(n, NL);
     uint8_t* base = (uint8_t*)scratch;
@@ -1002,6 +1002,9 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
     cudaError_t e = cub::DeviceRadixSort::SortPairs(base + p.off_temp, temp, keys, keys2, vals, vals2,
                                                     (int64_t)p.pairs, 0, 20, s);
     if (e != cudaSuccess) return e;
+    // digits and sort need the scalars (and the infinity mask) only: a host caller uploads the
+    // points meanwhile and hands over the event that says they have arrived
+    if (points_ready && (e = cudaStreamWaitEvent(s, points_ready, 0)) != cudaSuccess) return e;
     if (msm_affine()) {
         uint4 *rec = (uint4*)(base + p.off_rec), *slots = (uint4*)(base + p.off_slots);
         uint8_t* sinf = base + p.off_sinf;
@@ -1055,14 +1058,14 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
 
 cudaError_t launch_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px,
                        const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
-                       uint8_t* oinf, void* scratch, cudaStream_t s, int* launches) {
+                       uint8_t* oinf, void* scratch, cudaStream_t s, int* launches, cudaEvent_t points_ready) {
     if (curve == CURVE_BLS381)
-        return run_msm<Bls381Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
+        return run_msm<Bls381Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready);
     if (curve == CURVE_BLS377)
-        return run_msm<Bls377Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
+        return run_msm<Bls377Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready);
     if (curve == CURVE_SECP)
-        return run_msm<SecpCurve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
-    return run_msm<Sm2Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches);
+        return run_msm<SecpCurve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready);
+    return run_msm<Sm2Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready);
 }
 
 }  // namespace gecc
