@@ -486,7 +486,7 @@ k_msm_tree(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
 //   k_msm_tree_bwd : thread total^-1 = block total^-1 * others, unwind, chord / tangent.
 // (6K + 8) / K products per addition.
 template <class C, int K, bool LEVEL0>
-__global__ void __launch_bounds__(MSM_TREE_THREADS)
+__global__ void __launch_bounds__(MSM_TREE_THREADS, 4)
 k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
                const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
                const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
@@ -517,7 +517,7 @@ k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
 }
 
 template <class C, int K, bool LEVEL0>
-__global__ void __launch_bounds__(MSM_TREE_THREADS)
+__global__ void __launch_bounds__(MSM_TREE_THREADS, 4)
 k_msm_tree_bwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
                const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
                uint4* slots, uint8_t* sinf, const uint4* __restrict__ pref,
@@ -698,7 +698,7 @@ __device__ __forceinline__ cjac<C> warp_sum_points(cjac<C> acc, int lane) {
 }
 
 template <class C>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 4)
 k_msm_red_parts(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ starts,
                 const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
                 uint32_t* __restrict__ parts) {
