@@ -19,8 +19,8 @@ __device__ __forceinline__ uint32_t classify_pair(const cfe<C>& px, const cfe<C>
     if (pinf && tinf) return K_INFINITY;
     if (pinf) return K_COPY_RIGHT;
     if (tinf) return K_COPY_LEFT;
-    if (fe_eq(px, tx)) {
-        if (fe_eq(py, ty) && !fe_is_zero(py)) {
+    if (fe_eq(f, px, tx)) {  // field-aware: a weakly reduced field compares mod q
+        if (fe_eq(f, py, ty) && !fe_is_zero(f, py)) {
             *d = fe_dbl(f, py);
             return K_TANGENT;
         }

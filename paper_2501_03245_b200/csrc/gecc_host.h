@@ -52,6 +52,7 @@ cudaError_t launch_upmul(int curve, size_t n, const uint32_t* k, const uint32_t*
 void set_batch_form(int form);
 cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* in, uint32_t* out,
                                 cudaStream_t s);
+cudaError_t launch_batch_invert_secp_lazy(size_t n, const uint32_t* in, uint32_t* out, cudaStream_t s);
 cudaError_t launch_batch_padd(int curve, size_t n, const uint32_t* px, const uint32_t* py,
                               const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty,
                               const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,

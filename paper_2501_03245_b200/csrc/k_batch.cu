@@ -182,7 +182,7 @@ k_batch_invert_coop(size_t n, const uint32_t* __restrict__ in, uint32_t* __restr
         const size_t i = tile + (size_t)k * COOP_THREADS;
         if (i < n) {
             fe v = col_load<NL>(in, n, i);
-            if (!fe_is_zero(v)) acc = fe_mul(f, acc, v);
+            if (!fe_is_zero(f, v)) acc = fe_mul(f, acc, v);
         }
         lp[k] = acc;
     }
@@ -192,7 +192,7 @@ k_batch_invert_coop(size_t n, const uint32_t* __restrict__ in, uint32_t* __restr
         const size_t i = tile + (size_t)k * COOP_THREADS;
         if (i < n) {
             fe v = col_load<NL>(in, n, i);
-            const bool zero = fe_is_zero(v);
+            const bool zero = fe_is_zero(f, v);
             fe r = k > 0 ? fe_mul(f, inv, lp[k > 0 ? k - 1 : 0]) : inv;
             if (!zero && k > 0) inv = fe_mul(f, inv, v);
             col_store(out, n, i, zero ? fe_zero_n<NL>() : r);
@@ -485,6 +485,13 @@ cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* 
         if (field == 0) k_batch_invert<Sm2P><<<b, BATCH_THREADS, 0, s>>>(n, T, in, out);
         else k_batch_invert<Sm2N><<<b, BATCH_THREADS, 0, s>>>(n, T, in, out);
     }
+    return cudaGetLastError();
+}
+
+// block totals of the MSM tree when it runs on the lazy plain secp256k1 field (plain in, plain out)
+cudaError_t launch_batch_invert_secp_lazy(size_t n, const uint32_t* in, uint32_t* out, cudaStream_t s) {
+    if (n == 0) return cudaSuccess;
+    k_batch_invert_coop<SecpPL, 128><<<coop_blocks(n, 128), 128, 0, s>>>(n, in, out);
     return cudaGetLastError();
 }
 

@@ -15,6 +15,8 @@
 //      three marginal sums C^k_e (each over 1024 buckets, done as 32 x 32).
 //   5. k_msm_combine  : sum_w 2^(16 w) S_w, one affine point out.
 // Bucket ids: window w, magnitude m = 1..2^15  ->  w * 2^15 + (m - 1).
+#include <type_traits>
+
 #include <cub/device/device_radix_sort.cuh>
 
 #include "gecc_batch.cuh"
@@ -261,14 +263,29 @@ __device__ __forceinline__ feN<N> fe_load_cs(const uint4* p) { return fe_load_u4
 
 // column-major coordinates -> 64-byte records (one gather of a point = two 32-byte sectors
 // instead of sixteen)
-template <int N>
+// CE: the curve of the caller's column buffers (Montgomery form); CI: the curve the accumulation
+// computes on.  They differ on secp256k1 only, where the tree and the reduction run on the lazy
+// plain field of the ECDSA kernels (a product is 145 instead of 204 instructions): coordinates
+// are taken out of Montgomery form once here and put back once at the very end.
+template <class CE, class CI>
+__device__ __forceinline__ cfe<CI> msm_to_internal(const cfe<CE>& v) {
+    if constexpr (std::is_same<CE, CI>::value) return v;
+    else return fe_from_mont(typename CE::Fp{}, v);   // canonical plain residue: a valid lazy element
+}
+template <class CE, class CI>
+__device__ __forceinline__ cfe<CE> msm_to_external(const cfe<CI>& v) {
+    if constexpr (std::is_same<CE, CI>::value) return v;
+    else return fe_to_mont(typename CE::Fp{}, fe_from_mont(typename CI::Fp{}, v));  // canonicalise, then x R
+}
+template <class CE, class CI>
 __global__ void __launch_bounds__(256)
 k_msm_aos(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
           uint4* __restrict__ rec) {
+    constexpr int N = CE::Fp::N;
     const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    fe_store_u4<N, false>(rec + (N / 2) * i, col_load<N>(px, n, i));
-    fe_store_u4<N, false>(rec + (N / 2) * i + N / 4, col_load<N>(py, n, i));
+    fe_store_u4<N, false>(rec + (N / 2) * i, msm_to_internal<CE, CI>(col_load<N>(px, n, i)));
+    fe_store_u4<N, false>(rec + (N / 2) * i + N / 4, msm_to_internal<CE, CI>(col_load<N>(py, n, i)));
 }
 
 // first position of every bucket's run in the sorted keys (0xFFFFFFFF: empty bucket; memset)
@@ -363,7 +380,7 @@ __device__ __forceinline__ cfe<C> tree_denominator(const TreeJoin<C, LEVEL0>& t,
         bi = sinf[t.src] != 0;
     }
     if (ai || bi) return d;
-    if (fe_eq(ax, bx)) {  // y is only needed when the x's collide
+    if (fe_eq(f, ax, bx)) {  // y is only needed when the x's collide
         fe ay, by;
         if (LEVEL0) {
             ay = msm_point<C>(rec, t.v0).y;
@@ -836,7 +853,7 @@ __device__ __forceinline__ cjac<C> jac_dbl_group4(const cjac<C>& p, int lane) {
 // Horner over its three weighted marginals, then the shift by 2^(16 w) -- doublings by the lane
 // group; warp 0 then tree-sums the windows.
 constexpr int MSM_COMBINE_THREADS = 96;
-template <class C>
+template <class C, class CE>
 __global__ void __launch_bounds__(MSM_COMBINE_THREADS)
 k_msm_red_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, uint32_t* __restrict__ oy,
                   uint8_t* __restrict__ oinf) {
@@ -893,8 +910,8 @@ k_msm_red_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, 
             oinf[0] = 1;
         } else {
             aff a = jac_to_aff_with<C>(acc, fe_inv(f, acc.Z));
-            col_store(ox, 1, 0, a.x);
-            col_store(oy, 1, 0, a.y);
+            col_store(ox, 1, 0, msm_to_external<CE, C>(a.x));
+            col_store(oy, 1, 0, msm_to_external<CE, C>(a.y));
             oinf[0] = 0;
         }
     }
@@ -980,13 +997,17 @@ static cudaError_t launch_tree(int curve, size_t m, int level, const TreeBufs& b
     uint32_t* total_inv = b.totals + (size_t)C::Fp::N * (b.max_tiles + 64);
     k_msm_tree_fwd<C, K, LEVEL0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots,
                                                                       b.sinf, b.pref, b.others, b.totals, tiles);
-    if (cudaError_t e = launch_batch_invert(curve, 0, tiles, b.totals, total_inv, s)) return e;
+    if constexpr (C::Fp::kind == KIND_SECP_LAZY) {
+        if (cudaError_t e = launch_batch_invert_secp_lazy(tiles, b.totals, total_inv, s)) return e;
+    } else {
+        if (cudaError_t e = launch_batch_invert(curve, 0, tiles, b.totals, total_inv, s)) return e;
+    }
     k_msm_tree_bwd<C, K, LEVEL0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots,
                                                                       b.sinf, b.pref, b.others, total_inv, tiles);
     return cudaGetLastError();
 }
 
-template <class C>
+template <class C, class CI = C>
 static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px, const uint32_t* py,
                            const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
                            void* scratch, cudaStream_t s, int* launches, cudaEvent_t points_ready) {
@@ -1013,7 +1034,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
         e = cudaMemsetAsync(starts, 0xFF, (size_t)4 * MSM_NB, s);
         if (e != cudaSuccess) return e;
         k_msm_starts<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, keys2, starts);
-        k_msm_aos<NL><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, px, py, rec);
+        k_msm_aos<C, CI><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, px, py, rec);
         // K joins per thread; thin levels take fewer per thread so that the chip stays filled
         const bool split = g_msm_form != 3;
         TreeBufs tb{keys2, vals2, rec, slots, sinf, (uint4*)(base + p.off_pref), (uint4*)(base + p.off_others),
@@ -1022,21 +1043,21 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
         // products per join).  The single-launch form parks prefixes in shared memory: K <= 8.
         const size_t fill = (size_t)148 * 8 * MSM_TREE_THREADS;
         const size_t joins0 = (m + 1) / 2;
-        if (split && joins0 >= 16 * fill) e = launch_tree<C, 16, true>(curve, m, 0, tb, split, s);
-        else e = launch_tree<C, 8, true>(curve, m, 0, tb, split, s);
+        if (split && joins0 >= 16 * fill) e = launch_tree<CI, 16, true>(curve, m, 0, tb, split, s);
+        else e = launch_tree<CI, 8, true>(curve, m, 0, tb, split, s);
         if (e != cudaSuccess) return e;
         for (int l = 1; l < MSM_TREE_LEVELS; ++l) {
             const size_t joins = (m + ((size_t)2 << l) - 1) / ((size_t)2 << l);
-            if (split && joins >= 16 * fill) e = launch_tree<C, 16, false>(curve, m, l, tb, split, s);
-            else if (joins >= 8 * fill) e = launch_tree<C, 8, false>(curve, m, l, tb, split, s);
-            else if (joins >= 4 * fill) e = launch_tree<C, 4, false>(curve, m, l, tb, split, s);
-            else e = launch_tree<C, MSM_TREE_KMIN, false>(curve, m, l, tb, split, s);
+            if (split && joins >= 16 * fill) e = launch_tree<CI, 16, false>(curve, m, l, tb, split, s);
+            else if (joins >= 8 * fill) e = launch_tree<CI, 8, false>(curve, m, l, tb, split, s);
+            else if (joins >= 4 * fill) e = launch_tree<CI, 4, false>(curve, m, l, tb, split, s);
+            else e = launch_tree<CI, MSM_TREE_KMIN, false>(curve, m, l, tb, split, s);
             if (e != cudaSuccess) return e;
         }
-        k_msm_red_parts<C><<<(MSM_RED_PARTS + 127) / 128, 128, 0, s>>>(m, keys2, starts, slots, sinf, parts);
-        k_msm_red_fold<C><<<(MSM_WINDOWS * 3 * 32 * 32 + 127) / 128, 128, 0, s>>>(parts, marg);
-        k_msm_red_weighted<C><<<(MSM_WINDOWS * 3 * 32 + 127) / 128, 128, 0, s>>>(marg, wsum);
-        k_msm_red_combine<C><<<1, MSM_COMBINE_THREADS, 0, s>>>(wsum, ox, oy, oinf);
+        k_msm_red_parts<CI><<<(MSM_RED_PARTS + 127) / 128, 128, 0, s>>>(m, keys2, starts, slots, sinf, parts);
+        k_msm_red_fold<CI><<<(MSM_WINDOWS * 3 * 32 * 32 + 127) / 128, 128, 0, s>>>(parts, marg);
+        k_msm_red_weighted<CI><<<(MSM_WINDOWS * 3 * 32 + 127) / 128, 128, 0, s>>>(marg, wsum);
+        k_msm_red_combine<CI, C><<<1, MSM_COMBINE_THREADS, 0, s>>>(wsum, ox, oy, oinf);
         *launches = 3 + (split ? 3 : 1) * MSM_TREE_LEVELS + 4 + 4;  // + the sort's passes
         return cudaGetLastError();
     } else {
@@ -1064,7 +1085,7 @@ cudaError_t launch_msm(int curve, size_t n, const uint32_t* scalars, const uint3
     if (curve == CURVE_BLS377)
         return run_msm<Bls377Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready);
     if (curve == CURVE_SECP)
-        return run_msm<SecpCurve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready);
+        return run_msm<SecpCurve, SecpLCurve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready);
     return run_msm<Sm2Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready);
 }
 
