@@ -684,7 +684,7 @@ def _ncu_traffic(wl):
     For k_verify it is well above the 170 MB of records: the excess is per-thread stack
     (2 KB x 2^20 lanes of local memory written back from L1), not re-reads of the inputs."""
     import csv
-    name, kernel = {"verify": ("r01i_verify", "k_verify_gtab"), "padd": ("r01_padd", "k_batch_padd"),
+    name, kernel = {"verify": ("r01m_verify", "k_verify_gtab"), "padd": ("r01_padd", "k_batch_padd"),
                     "msm": ("r01g_msm_tree", "k_msm_tree_bwd")}.get(wl, (None, None))  # msm: the level-0 unwind kernel
     if not name:
         return None
