@@ -437,6 +437,9 @@ def main():
         e2e_s = max_over_ranks(time.perf_counter() - t0)
         if wl == "verify":
             assert int(p_res.sum()) == n
+        else:   # deterministic nonces: the pipelined host path must reproduce the device path's bytes
+            assert bytes(p_out.numpy()[:4096]) == h_sig[:4096].tobytes() and int(p_st.abs().sum()) == 0
+            assert bytes(p_out.numpy()[-4096:]) == h_sig[-4096:].tobytes()
         e2e = {"value": world * n * args.steps / e2e_s, "unit": UNIT[wl],
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": e2e_s / args.steps * 1e3,

@@ -94,3 +94,55 @@ def test_dev_entry_points_match_host_api(cid):
         assert int(d_res.sum()) == n and int(d_st.abs().sum()) == 0
         # device signing refuses seed 0 (system entropy is a host-side service)
         assert l.gecc_sign_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_sec), C.c_uint64(0), C.c_uint64(0), vp(d_sig), vp(d_st)) == 7
+
+
+def test_pipelined_host_api_matches_dev_api_on_a_large_ragged_batch():
+    """The host entry points cut large batches into chunks (short head chunk, two compute streams,
+    strided 2-D copies for column buffers); every byte must equal the single-launch device path.
+    Size chosen to exercise the head chunk, unequal last chunk and a ragged tail."""
+    n = (1 << 19) + (1 << 16) + 3
+    l = gecc.lib()
+    with gecc.Context(gecc.SECP256K1, 0) as ctx:
+        rc, sec, pub = ctx.keygen(9, n)
+        assert rc == 0
+        dig = np.random.RandomState(5).bytes(32 * n)
+        u8 = lambda b: torch.from_numpy(np.frombuffer(b, np.uint8).copy()).cuda()
+        d_dig, d_sec, d_pub = u8(dig), u8(sec), u8(pub)
+        d_sig = torch.empty(64 * n, dtype=torch.uint8, device="cuda")
+        d_st = torch.empty(n, dtype=torch.int32, device="cuda")
+        assert l.gecc_sign_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_sec), C.c_uint64(3), C.c_uint64(0), vp(d_sig), vp(d_st)) == 0
+        torch.cuda.synchronize()
+        rc, sig, st = ctx.sign(dig, sec, 3)
+        assert rc == 0 and sig == d_sig.cpu().numpy().tobytes() and not any(st)
+        # verify: flip a few lanes so that both outcomes travel through every chunk
+        bad = bytearray(sig)
+        flipped = [0, 1, 65535, 65536, 65537, n // 2, n - 1]
+        for i in flipped:
+            bad[64 * i + 40] ^= 1
+        d_res = torch.empty(n, dtype=torch.uint8, device="cuda")
+        assert l.gecc_verify_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_pub), vp(u8(bytes(bad))), vp(d_res)) == 0
+        torch.cuda.synchronize()
+        rc, res = ctx.verify(dig, pub, bytes(bad))
+        assert rc == 0 and res == d_res.cpu().numpy().tobytes()
+        assert sum(res) == n - len(flipped) and all(res[i] == 0 for i in flipped)
+        # a malformed secret in the LAST chunk fails the whole call before any output is written
+        broken = bytearray(sec)
+        broken[32 * (n - 2):32 * (n - 1)] = bytes(32)
+        rc, sig2, _ = ctx.sign(dig, bytes(broken), 3)
+        assert rc == 2 and sig2 == bytes(64 * n)
+        # column buffers: padd through the chunked host path vs the device path
+        k = np.random.RandomState(6).randint(0, 2**32, size=(8, n), dtype=np.uint64).astype(np.uint32)
+        P = ctx.batch_fpmul(k)
+        T = ctx.batch_fpmul(np.ascontiguousarray(k[::-1]))
+        S = ctx.batch_padd(P, T)
+        dP, dT = tuple(dev(a) for a in P), tuple(dev(a) for a in T)
+        dS = (torch.empty((8, n), dtype=torch.int32, device="cuda"), torch.empty((8, n), dtype=torch.int32, device="cuda"),
+              torch.empty(n, dtype=torch.uint8, device="cuda"))
+        assert l.gecc_batch_padd_dev(ctx.h, C.c_size_t(n), vp(dP[0]), vp(dP[1]), vp(dP[2]), vp(dT[0]), vp(dT[1]), vp(dT[2]),
+                                     vp(dS[0]), vp(dS[1]), vp(dS[2])) == 0
+        torch.cuda.synchronize()
+        assert (S[0] == host_u32(dS[0])).all() and (S[1] == host_u32(dS[1])).all() and (S[2] == dS[2].cpu().numpy()).all()
+        led0 = ctx.ledger()
+        ctx.batch_padd(P, T)
+        led1 = ctx.ledger()
+        assert led1["modinv"] - led0["modinv"] == 1 and led1["modmul"] - led0["modmul"] == 6 * n - 3  # one call, one closed form
