@@ -503,7 +503,7 @@ k_msm_tree(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
 //   k_msm_tree_bwd : thread total^-1 = block total^-1 * others, unwind, chord / tangent.
 // (6K + 8) / K products per addition.
 template <class C, int K, bool LEVEL0>
-__global__ void __launch_bounds__(MSM_TREE_THREADS, 4)
+__global__ void __launch_bounds__(MSM_TREE_THREADS, C::Fp::N > 8 ? 4 : 5)
 k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
                const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
                const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
@@ -534,7 +534,7 @@ k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
 }
 
 template <class C, int K, bool LEVEL0>
-__global__ void __launch_bounds__(MSM_TREE_THREADS, 4)
+__global__ void __launch_bounds__(MSM_TREE_THREADS, C::Fp::N > 8 ? 4 : 5)
 k_msm_tree_bwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
                const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
                uint4* slots, uint8_t* sinf, const uint4* __restrict__ pref,
