@@ -336,7 +336,12 @@ def main():
         l.gecc_batch_fpmul_dev(ctx.h, C.c_size_t(n), vp(k2), vp(T[0]), vp(T[1]), vp(T[2]))
         torch.cuda.synchronize()
 
-    if wl == "msm" and world > 1:
+    # GECC_BENCH_FORCE_EXCHANGE=1 runs the exchange code with a one-rank process group (torchrun
+    # --nproc-per-node 1): the only way to execute it on a single-GPU box
+    msm_exchange = wl == "msm" and (world > 1 or (os.environ.get("GECC_BENCH_FORCE_EXCHANGE") == "1" and "RANK" in os.environ))
+    if msm_exchange and world == 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    if msm_exchange:
         msm_parts = torch.empty(world * 17, dtype=torch.int32, device="cuda")
         one = lambda: (torch.empty((8, 1), dtype=torch.int32, device="cuda"),
                        torch.empty((8, 1), dtype=torch.int32, device="cuda"), u8(1))
@@ -351,7 +356,7 @@ def main():
         if wl == "msm":   # sum_i k2_i * P_i, one point out
             rc = l.gecc_msm_dev(ctx.h, C.c_size_t(n), vp(k2), vp(P[0]), vp(P[1]), vp(P[2]),
                                 vp(S[0]), vp(S[1]), vp(S[2]))
-            if world == 1 or rc != 0:
+            if not msm_exchange or rc != 0:
                 return rc
             # sharded MSM: every rank summed its own point range; ONE small all_gather of
             # the partial sums (17 words per rank over NVLink), then world-1 local additions
@@ -563,7 +568,7 @@ def main():
         }
         print(json.dumps(line), flush=True)
     ctx.close()
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
