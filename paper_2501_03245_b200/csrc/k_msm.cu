@@ -4,16 +4,25 @@
 // definition, checked against the oracle's sum of pmul_serial results and against
 // the identity  sum_i s_i (t_i G) = (sum_i s_i t_i) G  at full size.
 //
-//   1. k_msm_digits   : every scalar (folded below 2^255) is recoded into 16 signed 16-bit digits
-//                       plus a rarely non-zero carry digit
-//                       (same offset recoding as the fixed-base path); one
-//                       (bucket id, point index | sign) pair per non-zero digit.
+//   1. k_msm_digits   : every scalar (reduced mod the group order, folded below 2^255) is recoded
+//                       into 16 signed 16-bit digits plus a rarely non-zero carry digit (same
+//                       offset recoding as the fixed-base path); one (bucket id, point index |
+//                       sign) pair per non-zero digit.
 //   2. radix sort of the pairs by bucket id (CUB, plumbing only).
-//   3. k_msm_buckets  : one thread per bucket sums its points (mixed Jacobian adds).
+//   3. bucket accumulation, selectable with gecc_set_msm_form:
+//        batch-affine (default) : segmented pairwise tree over the sorted pairs, affine additions
+//                                 sharing one inversion per thread block -- "batch-affine bucket
+//                                 accumulation" below; three launches per level, or one;
+//        mixed Jacobian         : k_msm_buckets, fixed slices of the sorted pairs per thread.
 //   4. bucket reduction  S_w = sum_b (b+1) B_w[b]  without any long serial chain:
 //      b = lo + 32 mid + 1024 top, so S_w = sum B + sum_k 32^k sum_e e * C^k_e with the
-//      three marginal sums C^k_e (each over 1024 buckets, done as 32 x 32).
-//   5. k_msm_combine  : sum_w 2^(16 w) S_w, one affine point out.
+//      three marginal sums C^k_e (each over 1024 buckets): k_msm_red_* (warp-shuffle trees,
+//      reads the tree's slots directly) after the batch-affine form, k_msm_marginal_* /
+//      k_msm_weighted after the Jacobian one.
+//   5. window combine : sum_w 2^(16 w) S_w, one affine point out (k_msm_red_combine: the
+//      doubling chain is run by groups of four lanes).
+// All of it is a template over the curve: 8-limb SM2 / secp256k1 (the latter accumulates on its
+// lazy plain field), 12-limb BLS12-381 / BLS12-377 G1.
 // Bucket ids: window w, magnitude m = 1..2^15  ->  w * 2^15 + (m - 1).
 #include <type_traits>
 
