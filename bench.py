@@ -174,11 +174,60 @@ def set_curve(args):
     SECP = 0 if args.curve == "sm2" else 1
 
 
+def reference_arm_points(args, wl):
+    """padd: the reference's batch_padd (all host threads) on 2^16 pairs per step.  msm: the
+    reference has none -- its serial scalar multiplication over 2^11 terms per step, scaled to
+    the 2^log2n terms of the workload (what a caller of the reference would have to run)."""
+    import numpy as np
+    from oracle import refshim as R
+    if not R.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref is not built"}), flush=True)
+        return
+    cores = os.cpu_count()
+    m = 1 << (args.cpu_sample_log2 or (16 if wl == "padd" else 11))
+    rs = np.random.RandomState(99)
+    k1 = rs.randint(0, 2**32, size=(8, m), dtype=np.uint64).astype(np.uint32)
+    k2 = rs.randint(0, 2**32, size=(8, m), dtype=np.uint64).astype(np.uint32)
+    P = R.batch_fpmul(SECP, k1, workers=0)
+    if wl == "padd":
+        T = R.batch_fpmul(SECP, k2, workers=0)
+        step = lambda: R.batch_padd(SECP, P, T, lanes=0, workers=0)
+        used = cores
+    else:
+        step = lambda: R.pmul_serial(SECP, k2, P)
+        used = 1
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    n = 1 << args.log2n
+    value = m / dt if wl == "padd" else dt * (n / m) * 1e3
+    sample = (f"2^{m.bit_length() - 1} pairs per step, reference batch_padd" if wl == "padd" else
+              f"reference pmul_serial over 2^{m.bit_length() - 1} terms per step, scaled by {n // m} to 2^{args.log2n} terms (the reference has no MSM)")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC[wl], "value": value, "unit": UNIT[wl], "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": wl != "msm",
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32 limbs (256-bit modular integer)", "data": "synthetic",
+        "config": {"workload": f"{args.curve} {'batched affine point addition' if wl == 'padd' else 'Pippenger MSM'}, 2^{args.log2n} per GPU",
+                   "curve": args.curve, "cpu_sample_per_step": m},
+        "cpu_baseline": {"value": value, "unit": UNIT[wl], "cores": used, "kind": "reference", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT[wl], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0}), flush=True)
+
+
 def run_reference_arm(args, rank):
     set_curve(args)
     if rank != 0:
         return
-    wl = args.workload if args.workload != "padd" else "verify"
+    wl = args.workload
+    if wl in ("padd", "msm") and args.curve in ("secp256k1", "sm2"):
+        reference_arm_points(args, wl)
+        return
+    if wl not in ("verify", "sign"):
+        print(json.dumps({"impl": "reference", "unavailable": f"the reference has no {args.curve} {wl}"}), flush=True)
+        return
     log2 = args.cpu_sample_log2 or (13 if wl == "verify" else 14)
     n = 1 << log2
     dig, sec, pub, sig = make_records_cpu(n)
