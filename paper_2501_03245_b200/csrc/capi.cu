@@ -59,6 +59,7 @@ struct sm2b_ctx {
     uint32_t* flags = nullptr;  // device word: malformed-call flag of sign / ecdh
     int limbs = 8;              // 32-bit limbs per coordinate (12 on BLS12-381)
     uint32_t* hflag = nullptr;  // pinned host word: the flag comes back without blocking the enqueueing thread
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // fork / join of the two-stream MSM tree levels
     bool ledger_hold = false;   // a pipelined host call runs its chunks with the ledger held and accounts once
     sm2b_op_counts ledger_sink{0, 0, 0, 0};
 };
@@ -135,7 +136,9 @@ sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device) {
         cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->h2d_stream, cudaStreamNonBlocking) != cudaSuccess ||
         cudaStreamCreateWithFlags(&ctx->d2h_stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking) != cudaSuccess) {
+        cudaStreamCreateWithFlags(&ctx->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming) != cudaSuccess) {
         delete ctx;
         return nullptr;
     }
@@ -201,6 +204,8 @@ void sm2b_ctx_free(sm2b_ctx* ctx) {
         if (ctx->h2d_stream) cudaStreamDestroy(ctx->h2d_stream);
         if (ctx->d2h_stream) cudaStreamDestroy(ctx->d2h_stream);
         if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
+        if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+        if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     }
     delete ctx;
 }
@@ -1096,7 +1101,7 @@ sm2b_status gecc_msm_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const
     CU(ctx, ctx->scratch.ensure(msm_scratch_bytes(n, ctx->curve)));
     int launches = 0;
     CU(ctx, launch_msm(ctx->curve, n, scalars, px, py, pinf, ox, oy, oinf, ctx->scratch.p, ctx->stream,
-                       &launches));
+                       &launches, nullptr, MsmAux{ctx->aux_stream, ctx->ev_fork, ctx->ev_join}));
     ctx->launches += launches;
     return SM2B_OK;
 }
@@ -1142,7 +1147,7 @@ sm2b_status gecc_msm(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uin
     CU(ctx, ctx->scratch.ensure(msm_scratch_bytes(n, ctx->curve)));
     int launches = 0;
     CU(ctx, launch_msm(ctx->curve, n, dk, dpx, dpy, dpi, dox, doy, doi, ctx->scratch.p, ctx->stream, &launches,
-                       points_up));
+                       points_up, MsmAux{ctx->aux_stream, ctx->ev_fork, ctx->ev_join}));
     ctx->launches += launches;
     CU(ctx, cudaMemcpyAsync(ox, dox, 4 * L, cudaMemcpyDeviceToHost, ctx->stream));
     CU(ctx, cudaMemcpyAsync(oy, doy, 4 * L, cudaMemcpyDeviceToHost, ctx->stream));

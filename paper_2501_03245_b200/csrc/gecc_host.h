@@ -77,9 +77,15 @@ cudaError_t launch_pmul_serial(int curve, size_t n, const uint32_t* k, const uin
 // MSM: scratch must hold msm_scratch_bytes(n) bytes of device memory
 size_t msm_scratch_bytes(size_t n, int curve);
 void set_msm_form(int form);  // 0 default (batch-affine), 1 mixed-Jacobian slices, 2 batch-affine tree
+// optional second stream + two events: the tree levels run as two overlapping halves when given
+struct MsmAux {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
 cudaError_t launch_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px,
                        const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
                        uint8_t* oinf, void* scratch, cudaStream_t s, int* launches,
-                       cudaEvent_t points_ready = nullptr);  // waited for before the first read of px / py
+                       cudaEvent_t points_ready = nullptr,  // waited for before the first read of px / py
+                       MsmAux aux = MsmAux());
 
 }  // namespace gecc

@@ -517,7 +517,7 @@ k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
                const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
                const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
                uint4* __restrict__ pref, uint4* __restrict__ others, uint32_t* __restrict__ totals,
-               size_t tiles) {
+               size_t tiles, size_t tile0) {
     using fe = cfe<C>;
     using jac = cjac<C>;
     using aff = caff<C>;
@@ -525,7 +525,8 @@ k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
     (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     __shared__ uint32_t sm_scan[2 * NL * (MSM_TREE_THREADS / 32)];
     const typename C::Fp f{};
-    const size_t j0 = (size_t)blockIdx.x * (MSM_TREE_THREADS * K) + threadIdx.x;
+    const size_t tile = tile0 + blockIdx.x;  // tiles [tile0, tile0 + gridDim.x) of the level; totals / tiles are local to this launch
+    const size_t j0 = tile * (MSM_TREE_THREADS * K) + threadIdx.x;
     fe acc = fe_one(f);
 #pragma unroll 1
     for (int k = 0; k < K; ++k) {
@@ -537,7 +538,7 @@ k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
     }
     fe total;
     const fe oth = block_others_product<decltype(f), MSM_TREE_THREADS>(f, acc, sm_scan, &total);
-    const size_t tid = (size_t)blockIdx.x * MSM_TREE_THREADS + threadIdx.x;
+    const size_t tid = tile * MSM_TREE_THREADS + threadIdx.x;
     fe_store_cs<NL>(others + (NL / 4) * tid, oth);
     if (threadIdx.x == 0) col_store(totals, tiles, blockIdx.x, total);
 }
@@ -547,16 +548,18 @@ __global__ void __launch_bounds__(MSM_TREE_THREADS, C::Fp::N > 8 ? 4 : 5)
 k_msm_tree_bwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
                const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
                uint4* slots, uint8_t* sinf, const uint4* __restrict__ pref,
-               const uint4* __restrict__ others, const uint32_t* __restrict__ total_inv, size_t tiles) {
+               const uint4* __restrict__ others, const uint32_t* __restrict__ total_inv, size_t tiles,
+               size_t tile0) {
     using fe = cfe<C>;
     using jac = cjac<C>;
     using aff = caff<C>;
     constexpr int NL = C::Fp::N;
     (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     const typename C::Fp f{};
-    const size_t j0 = (size_t)blockIdx.x * (MSM_TREE_THREADS * K) + threadIdx.x;
+    const size_t tile = tile0 + blockIdx.x;
+    const size_t j0 = tile * (MSM_TREE_THREADS * K) + threadIdx.x;
     if (j0 >= joins) return;
-    const size_t tid = (size_t)blockIdx.x * MSM_TREE_THREADS + threadIdx.x;
+    const size_t tid = tile * MSM_TREE_THREADS + threadIdx.x;
     fe inv = fe_mul(f, col_load<NL>(total_inv, tiles, blockIdx.x), fe_load_cs<NL>(others + (NL / 4) * tid));
 #pragma unroll 1
     for (int k = K - 1; k >= 0; --k) {
@@ -989,6 +992,8 @@ struct TreeBufs {
     uint4 *pref, *others;
     uint32_t* totals;
     size_t max_tiles;
+    cudaStream_t aux;           // second stream + fork / join events (may be null: one stream then)
+    cudaEvent_t fork, join;
 };
 template <class C, int K, bool LEVEL0>
 static cudaError_t launch_tree(int curve, size_t m, int level, const TreeBufs& b, bool split, cudaStream_t s) {
@@ -1003,23 +1008,43 @@ static cudaError_t launch_tree(int curve, size_t m, int level, const TreeBufs& b
             return cudaGetLastError();
         }
     }
-    uint32_t* total_inv = b.totals + (size_t)C::Fp::N * (b.max_tiles + 64);
-    k_msm_tree_fwd<C, K, LEVEL0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots,
-                                                                      b.sinf, b.pref, b.others, b.totals, tiles);
-    if constexpr (C::Fp::kind == KIND_SECP_LAZY) {
-        if (cudaError_t e = launch_batch_invert_secp_lazy(tiles, b.totals, total_inv, s)) return e;
-    } else {
-        if (cudaError_t e = launch_batch_invert(curve, 0, tiles, b.totals, total_inv, s)) return e;
+    // The totals' inversion is ~40 us of pure latency (one warp per 512 totals runs safegcd).  A level
+    // is therefore cut into parts that alternate between two streams: while one part inverts, the
+    // forward pass or the unwind of another runs.
+    constexpr int NL = C::Fp::N;
+    const size_t parts = b.aux && tiles >= 64 ? 2 : 1;  // four parts measured slower (two inversions in a row per stream)
+    const size_t cap = b.max_tiles + 64;  // totals | inverses: `parts` regions of cap / parts elements each
+    if (parts > 1) {
+        if (cudaError_t e = cudaEventRecord(b.fork, s)) return e;
+        if (cudaError_t e = cudaStreamWaitEvent(b.aux, b.fork, 0)) return e;
     }
-    k_msm_tree_bwd<C, K, LEVEL0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots,
-                                                                      b.sinf, b.pref, b.others, total_inv, tiles);
+    for (size_t h = 0; h < parts; ++h) {
+        const size_t t0 = tiles * h / parts, cnt = tiles * (h + 1) / parts - t0;
+        cudaStream_t hs = (h & 1) ? b.aux : s;
+        uint32_t* tot = b.totals + (size_t)NL * (cap / parts) * h;
+        uint32_t* inv = b.totals + (size_t)NL * (cap + (cap / parts) * h);
+        k_msm_tree_fwd<C, K, LEVEL0><<<(unsigned)cnt, MSM_TREE_THREADS, 0, hs>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots,
+                                                                               b.sinf, b.pref, b.others, tot, cnt, t0);
+        if constexpr (C::Fp::kind == KIND_SECP_LAZY) {
+            if (cudaError_t e = launch_batch_invert_secp_lazy(cnt, tot, inv, hs)) return e;
+        } else {
+            if (cudaError_t e = launch_batch_invert(curve, 0, cnt, tot, inv, hs)) return e;
+        }
+        k_msm_tree_bwd<C, K, LEVEL0><<<(unsigned)cnt, MSM_TREE_THREADS, 0, hs>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots,
+                                                                               b.sinf, b.pref, b.others, inv, cnt, t0);
+    }
+    if (parts > 1) {
+        if (cudaError_t e = cudaEventRecord(b.join, b.aux)) return e;
+        if (cudaError_t e = cudaStreamWaitEvent(s, b.join, 0)) return e;
+    }
     return cudaGetLastError();
 }
 
 template <class C, class CI = C>
 static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px, const uint32_t* py,
                            const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
-                           void* scratch, cudaStream_t s, int* launches, cudaEvent_t points_ready) {
+                           void* scratch, cudaStream_t s, int* launches, cudaEvent_t points_ready,
+                           const MsmAux& aux) {
     constexpr int NL = C::Fp::N;
     MsmPlan p = msm_plan(n, NL);
     uint8_t* base = (uint8_t*)scratch;
@@ -1047,7 +1072,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
         // K joins per thread; thin levels take fewer per thread so that the chip stays filled
         const bool split = g_msm_form != 3;
         TreeBufs tb{keys2, vals2, rec, slots, sinf, (uint4*)(base + p.off_pref), (uint4*)(base + p.off_others),
-                    (uint32_t*)(base + p.off_totals), p.max_tiles};
+                    (uint32_t*)(base + p.off_totals), p.max_tiles, aux.stream, aux.fork, aux.join};
         // joins per thread: as many as keep >= ~8 blocks per SM in flight (the scan share is 14 / K
         // products per join).  The single-launch form parks prefixes in shared memory: K <= 8.
         const size_t fill = (size_t)148 * 8 * MSM_TREE_THREADS;
@@ -1088,14 +1113,15 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
 
 cudaError_t launch_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px,
                        const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
-                       uint8_t* oinf, void* scratch, cudaStream_t s, int* launches, cudaEvent_t points_ready) {
+                       uint8_t* oinf, void* scratch, cudaStream_t s, int* launches, cudaEvent_t points_ready,
+                       MsmAux aux) {
     if (curve == CURVE_BLS381)
-        return run_msm<Bls381Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready);
+        return run_msm<Bls381Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready, aux);
     if (curve == CURVE_BLS377)
-        return run_msm<Bls377Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready);
+        return run_msm<Bls377Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready, aux);
     if (curve == CURVE_SECP)
-        return run_msm<SecpCurve, SecpLCurve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready);
-    return run_msm<Sm2Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready);
+        return run_msm<SecpCurve, SecpLCurve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready, aux);
+    return run_msm<Sm2Curve>(curve, n, scalars, px, py, pinf, ox, oy, oinf, scratch, s, launches, points_ready, aux);
 }
 
 }  // namespace gecc
