@@ -131,11 +131,35 @@ typedef enum gecc_field_opcode {
     GECC_OP_TO_MONT = 3,  /* field.cpp:194-198 */
     GECC_OP_FROM_MONT = 4,/* field.cpp:200-203 */
     GECC_OP_MOD_INV = 5,  /* field.cpp:239-246's value via safegcd, zero maps to zero */
-    GECC_OP_MOD_INV_FERMAT = 6 /* same value by a^(q-2), kept as a cross-check */
+    GECC_OP_MOD_INV_FERMAT = 6, /* same value by a^(q-2), kept as a cross-check */
+    /* mont_reduce of a 512-bit value (field.hpp mont_reduce_generic / mont_reduce_sm2,
+     * field.cpp:50-128): a = low 8 limbs, b = high 8 limbs, out = value * R^-1 mod q, canonical.
+     * The value must be below q * 2^256.  Reaches the curve-specialised reductions directly. */
+    GECC_OP_MONT_REDUCE = 7,
+    /* The weakly reduced plain representation the fused secp256k1 kernels compute in
+     * (GECC_CURVE_SECP256K1, GECC_FIELD_P only): inputs are ANY 256-bit values (not Montgomery
+     * form, not necessarily below q), outputs are the canonical residues a*b, a^2, a+b, a-b mod q. */
+    GECC_OP_LAZY_MUL = 8, GECC_OP_LAZY_SQR = 9, GECC_OP_LAZY_ADD = 10, GECC_OP_LAZY_SUB = 11
 } gecc_field_opcode;
 
 /* Context for `curve` on CUDA device `device` (< 0: the current device). */
 sm2b_ctx* gecc_ctx_new(gecc_curve curve, int device);
+/* GROUP context: one context that drives `ndev` CUDA devices (the reference's
+ * context owns its workers the same way, capi.cpp:94-107).  `devices` lists them (NULL: devices
+ * 0 .. ndev-1; ndev <= 0: every visible device).  Every host-pointer entry point splits its batch
+ * into contiguous lane ranges, one per device, each served by its own host thread, streams and
+ * arenas; every device downloads its own slice.  The global lane index stays the nonce stream id
+ * (protocol.cpp:125-126), so outputs are byte-identical for any device count.  gecc_msm shards by
+ * point range and exchanges the per-device partial sums with one ncclAllGather followed by local
+ * additions.  A device may be listed more than once (several shards on one GPU: how the sharding
+ * logic is exercised on a one-GPU box; the exchange then uses peer copies, NCCL refuses duplicate
+ * devices).  The *_dev entry points, gecc_ctx_set_stream and gecc_microbench address ONE device and
+ * return SM2B_ERROR_INVALID_ARGUMENT on a group context.
+ * sm2b_ctx_new() itself creates a group over all visible devices when there is more than one
+ * (environment GECC_NDEV=k limits it to the first k). */
+sm2b_ctx* gecc_ctx_new_multi(gecc_curve curve, int ndev, const int* devices);
+/* number of device shards behind the context (1 for a device context) */
+int gecc_ctx_shards(const sm2b_ctx* ctx);
 int gecc_ctx_curve(const sm2b_ctx* ctx);
 int gecc_ctx_device(const sm2b_ctx* ctx);
 /* Message of the last failing call on this context ("" if none). */
@@ -153,6 +177,45 @@ sm2b_status gecc_keygen(sm2b_ctx* ctx, uint64_t seed, uint64_t lane_base, size_t
 sm2b_status gecc_sign(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
                       const uint8_t* secrets, uint64_t nonce_seed, uint64_t lane_base,
                       uint8_t* signatures, int32_t* lane_status);
+
+/* One signing attempt with caller-supplied nonces (32-byte big-endian records): the building
+ * block of ecdsa_sign_batch with an arbitrary NonceSource (protocol.cpp:121-164).  lane_status[i] is
+ * SM2B_OK, or SM2B_ERROR_NONCE_EXHAUSTED when this nonce must be replaced (nonce outside (0, n),
+ * r == 0 or s == 0; the signature is then zeroed).  Secrets are checked as in sm2b_sign. */
+sm2b_status gecc_sign_nonces(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
+                             const uint8_t* secrets, const uint8_t* nonces, uint8_t* signatures,
+                             int32_t* lane_status);
+
+/* Secret-scalar discipline (SPEC.md: "constant structure" on secret-dependent paths; the
+ * reference applies table entries by select, batch_point.cpp:319-333,420).  GECC_SECRET_FAST skips
+ * zero digits and branches on digit signs; GECC_SECRET_UNIFORM makes k*G (sign, keygen) and d*P
+ * (ECDH) execute the same instruction and memory-access sequence for every scalar: every window
+ * performs its addition, the table entry is chosen by masked sweep / arithmetic select and the sign
+ * by a conditional negation without branches.  Outputs are identical. */
+enum { GECC_SECRET_FAST = 0, GECC_SECRET_UNIFORM = 1 };
+sm2b_status gecc_ctx_set_secret_mode(sm2b_ctx* ctx, int mode);
+
+/* precompute_base_table (batch_point.hpp:76-83, batch_point.cpp:341-350) for an arbitrary base:
+ * a device-resident windowed table of the affine point (x, y) (8 Montgomery-form limbs each).
+ * SM2B_ERROR_MALFORMED_INPUT when the point is not on the context's curve (the reference throws
+ * std::invalid_argument there).  batch_fpmul over it: out[i] = scalars[i] * base. */
+typedef struct gecc_base_table gecc_base_table;
+sm2b_status gecc_base_table_new(sm2b_ctx* ctx, const uint32_t* x, const uint32_t* y,
+                                gecc_base_table** out);
+void gecc_base_table_free(gecc_base_table* table);
+sm2b_status gecc_batch_fpmul_base(sm2b_ctx* ctx, const gecc_base_table* base, size_t n,
+                                  const uint32_t* scalars, uint32_t* ox, uint32_t* oy, uint8_t* oinf);
+
+/* Multi-process form of the MSM exchange (one process per GPU, e.g. under torchrun): rank 0 draws
+ * an id, the launcher's own plumbing broadcasts the 128 bytes, every rank joins with its device
+ * context.  gecc_msm_combine_dev then turns every rank's partial sum (one affine point in device
+ * memory, as gecc_msm_dev wrote it) into the total on every rank: one ncclAllGather of 2L+1 words
+ * per rank + nranks-1 local additions (EC addition is not an NCCL reduction operator), enqueued on
+ * the context's stream, not synchronised. */
+#define GECC_COMM_ID_BYTES 128
+sm2b_status gecc_comm_unique_id(uint8_t id[GECC_COMM_ID_BYTES]);
+sm2b_status gecc_comm_init_rank(sm2b_ctx* ctx, int nranks, int rank, const uint8_t id[GECC_COMM_ID_BYTES]);
+sm2b_status gecc_msm_combine_dev(sm2b_ctx* ctx, uint32_t* x, uint32_t* y, uint8_t* inf);
 
 /* Element-wise field operation on column buffers (host pointers). */
 sm2b_status gecc_field_op(sm2b_ctx* ctx, gecc_field field, gecc_field_opcode op, size_t n,
@@ -203,9 +266,16 @@ sm2b_status gecc_batch_upmul_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalar
 sm2b_status gecc_verify_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
                             const uint8_t* publics, const uint8_t* signatures,
                             uint8_t* results);
+/* Differs from sm2b_sign / gecc_sign in one documented way: nothing is synchronised, so a zero or
+ * oversize secret cannot fail the call -- it returns SM2B_OK, the lane's status is
+ * SM2B_ERROR_MALFORMED_INPUT (2) and its signature is zeroed; the caller inspects lane_status.
+ * nonce_seed == 0 (system entropy) is served by the host forms only. */
 sm2b_status gecc_sign_dev(sm2b_ctx* ctx, size_t count, const uint8_t* digests,
                           const uint8_t* secrets, uint64_t nonce_seed, uint64_t lane_base,
                           uint8_t* signatures, int32_t* lane_status);
+sm2b_status gecc_batch_fpmul_base_dev(sm2b_ctx* ctx, const gecc_base_table* base, size_t n,
+                                      const uint32_t* scalars, uint32_t* ox, uint32_t* oy,
+                                      uint8_t* oinf);
 sm2b_status gecc_msm_dev(sm2b_ctx* ctx, size_t n, const uint32_t* scalars, const uint32_t* px,
                          const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
                          uint8_t* oinf);

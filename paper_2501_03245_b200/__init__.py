@@ -5,9 +5,11 @@ CUDA library behind the C ABI in ``include/gecc_b200.h``).  There is no CPU
 implementation here: importing works anywhere, but creating a Context needs the
 compiled library and a CUDA device and raises loudly otherwise.
 """
-from .capi import (Context, GeccError, LIB_PATH, SM2, SECP256K1, BLS12_381, BLS12_377, STATUS, lib, lib_available,
-                   cols_from_ints, ints_from_cols, set_batch_form, set_msm_form)
+from .capi import (BaseTable, Context, GeccError, LIB_PATH, SM2, SECP256K1, BLS12_381, BLS12_377, STATUS,
+                   SECRET_FAST, SECRET_UNIFORM, COMM_ID_BYTES, lib, lib_available, cols_from_ints, ints_from_cols,
+                   comm_unique_id, set_batch_form, set_msm_form)
 
-__all__ = ["Context", "GeccError", "LIB_PATH", "SM2", "SECP256K1", "BLS12_381", "BLS12_377", "STATUS", "lib",
-           "lib_available", "cols_from_ints", "ints_from_cols", "set_batch_form", "set_msm_form"]
+__all__ = ["BaseTable", "Context", "GeccError", "LIB_PATH", "SM2", "SECP256K1", "BLS12_381", "BLS12_377", "STATUS",
+           "SECRET_FAST", "SECRET_UNIFORM", "COMM_ID_BYTES", "lib", "lib_available", "cols_from_ints",
+           "ints_from_cols", "comm_unique_id", "set_batch_form", "set_msm_form"]
 __version__ = "0.1.0"

@@ -21,7 +21,10 @@ FIELD_P, FIELD_N = 0, 1
 STATUS = {0: "ok", 1: "invalid argument", 2: "malformed input", 3: "invalid peer point",
           4: "degenerate result", 5: "nonce retries exhausted", 6: "cost model has no crossover",
           7: "internal error"}
-FIELD_OPS = dict(mont_mul=0, mod_add=1, mod_sub=2, to_mont=3, from_mont=4, mod_inv=5, mod_inv_fermat=6)
+FIELD_OPS = dict(mont_mul=0, mod_add=1, mod_sub=2, to_mont=3, from_mont=4, mod_inv=5, mod_inv_fermat=6,
+                 mont_reduce=7, lazy_mul=8, lazy_sqr=9, lazy_add=10, lazy_sub=11)
+SECRET_FAST, SECRET_UNIFORM = 0, 1
+COMM_ID_BYTES = 128
 
 
 class GeccError(RuntimeError):
@@ -47,6 +50,16 @@ def lib():
         l.sm2b_ctx_new.argtypes = [C.c_uint32, C.c_uint32]
         l.gecc_ctx_new.restype = C.c_void_p
         l.gecc_ctx_new.argtypes = [C.c_int, C.c_int]
+        l.gecc_ctx_new_multi.restype = C.c_void_p
+        l.gecc_ctx_new_multi.argtypes = [C.c_int, C.c_int, C.c_void_p]
+        l.gecc_ctx_shards.argtypes = [C.c_void_p]
+        l.gecc_ctx_set_secret_mode.argtypes = [C.c_void_p, C.c_int]
+        l.gecc_base_table_new.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        l.gecc_base_table_free.argtypes = [C.c_void_p]
+        l.gecc_base_table_free.restype = None
+        l.gecc_comm_unique_id.argtypes = [C.c_void_p]
+        l.gecc_comm_init_rank.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_void_p]
+        l.gecc_msm_combine_dev.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         l.sm2b_ctx_free.argtypes = [C.c_void_p]
         l.sm2b_version.restype = C.c_char_p
         l.sm2b_status_str.restype = C.c_char_p
@@ -62,7 +75,8 @@ def lib():
     return _lib
 
 
-BATCH_FORMS = {"auto": 0, "chunked": 1, "coop": 2, "chunked8": 3, "coop128": 4, "coop32": 5, "tiled8": 6, "tiled4": 7}
+BATCH_FORMS = {"auto": 0, "chunked": 1, "coop": 2, "chunked8": 3, "coop128": 4, "coop32": 5, "tiled8": 6, "tiled4": 7,
+               "fused": 8, "fused2": 9}
 
 
 def set_batch_form(form: str):
@@ -96,21 +110,81 @@ def _vp(a):
     if a is None:
         return None
     if isinstance(a, np.ndarray):
-        assert a.flags["C_CONTIGUOUS"]
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("buffer must be C-contiguous")
         return C.c_void_p(a.ctypes.data)
     if isinstance(a, (bytes, bytearray)):
         return C.cast(C.c_char_p(bytes(a)), C.c_void_p) if len(a) else None
     return C.c_void_p(int(a))
 
 
+def _need_cols(a, rows, n, what):
+    """column buffers are uint32 arrays of shape (rows, n): a short or mistyped buffer would make
+    the C side read past the end of the Python object"""
+    if not isinstance(a, np.ndarray) or a.dtype != np.uint32 or a.shape != (rows, n) or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"{what}: expected a C-contiguous uint32 array of shape ({rows}, {n})")
+
+
+def _need_mask(a, n, what):
+    if a is None:
+        return
+    if not isinstance(a, np.ndarray) or a.dtype != np.uint8 or a.shape != (n,) or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"{what}: expected a C-contiguous uint8 array of shape ({n},)")
+
+
+def _need_bytes(b, size, what):
+    if len(b) != size:
+        raise ValueError(f"{what}: expected {size} bytes, got {len(b)}")
+
+
+class BaseTable:
+    """precompute_base_table(c, g) for an arbitrary on-curve g (batch_point.hpp:76-83): a device
+    table owned by a Context; raises ValueError for an off-curve point as the reference throws
+    std::invalid_argument (batch_point.cpp:343-344)."""
+
+    def __init__(self, ctx: "Context", x: np.ndarray, y: np.ndarray):
+        x = np.ascontiguousarray(x, np.uint32).reshape(8)
+        y = np.ascontiguousarray(y, np.uint32).reshape(8)
+        h = C.c_void_p()
+        rc = ctx.l.gecc_base_table_new(ctx.h, _vp(x), _vp(y), C.byref(h))
+        ctx._check(rc, "gecc_base_table_new")
+        if rc != 0:
+            raise ValueError("precompute_base_table: point off curve" if rc == 2 else f"gecc_base_table_new rc={rc}")
+        self.ctx, self.h = ctx, h
+
+    def close(self):
+        if getattr(self, "h", None) and self.ctx.h:
+            self.ctx.l.gecc_base_table_free(self.h)
+        self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def comm_unique_id() -> bytes:
+    """ncclGetUniqueId through the library (rank 0 draws it, the launcher broadcasts it)."""
+    buf = (C.c_uint8 * COMM_ID_BYTES)()
+    rc = lib().gecc_comm_unique_id(buf)
+    if rc != 0:
+        raise GeccError("gecc_comm_unique_id failed: libnccl.so.2 could not be loaded")
+    return bytes(buf)
+
+
 class Context:
-    """One engine context = one CUDA device + one curve (sm2b_ctx, sm2batch.h:41-45)."""
+    """One engine context = one curve on one CUDA device, or -- with ``devices`` -- a GROUP
+    context that shards every host call over several devices (sm2b_ctx, sm2batch.h:41-45)."""
 
     def __init__(self, curve: int = SM2, device: int = -1, reference_compat: bool = False,
-                 workers: int = 0, lanes: int = 0):
+                 workers: int = 0, lanes: int = 0, devices=None):
         self.l = lib()
         if reference_compat:
             h = self.l.sm2b_ctx_new(workers, lanes)
+        elif devices is not None:
+            devs = np.ascontiguousarray(devices, np.int32)
+            h = self.l.gecc_ctx_new_multi(curve, len(devs), _vp(devs) if len(devs) else None)
         else:
             h = self.l.gecc_ctx_new(curve, device)
         if not h:
@@ -156,6 +230,23 @@ class Context:
             ptr = 1 if int(stream_ptr) == 0 else int(stream_ptr)  # 0x1 == cudaStreamLegacy
         self.l.gecc_ctx_set_stream(self.h, C.c_void_p(ptr))
 
+    @property
+    def shards(self) -> int:
+        return int(self.l.gecc_ctx_shards(self.h))
+
+    def set_secret_mode(self, mode: int):
+        """SECRET_FAST | SECRET_UNIFORM (constant-structure k*G and d*P on secret scalars)."""
+        if self.l.gecc_ctx_set_secret_mode(self.h, mode) != 0:
+            raise ValueError("gecc_ctx_set_secret_mode: bad mode")
+
+    def comm_init_rank(self, nranks: int, rank: int, unique_id: bytes):
+        """Joins the multi-process MSM exchange communicator (ncclCommInitRank)."""
+        _need_bytes(unique_id, COMM_ID_BYTES, "unique_id")
+        rc = self.l.gecc_comm_init_rank(self.h, nranks, rank, _vp(unique_id))
+        self._check(rc, "gecc_comm_init_rank")
+        if rc != 0:
+            raise ValueError(f"gecc_comm_init_rank rc={rc}")
+
     def ledger(self):
         arr = (C.c_uint64 * 4)()
         self.l.sm2b_ledger_read(self.h, arr)
@@ -167,7 +258,11 @@ class Context:
     # -- field layer
     def field_op(self, field: int, op: str, a: np.ndarray, b: np.ndarray | None = None):
         n = a.shape[1]
-        out = np.zeros((self.limbs if field == 0 else 8, n), np.uint32)
+        rows = self.limbs if field == 0 else 8
+        _need_cols(a, rows, n, "field_op a")
+        if b is not None:
+            _need_cols(b, rows, n, "field_op b")
+        out = np.zeros((rows, n), np.uint32)
         rc = self.l.gecc_field_op(self.h, field, FIELD_OPS[op], C.c_size_t(n), _vp(a), _vp(b), _vp(out))
         if self._check(rc, "gecc_field_op"):
             raise ValueError(f"gecc_field_op rc={rc}")
@@ -199,6 +294,7 @@ class Context:
     # -- batch layer (host column buffers)
     def batch_invert(self, field: int, a: np.ndarray):
         n = a.shape[1]
+        _need_cols(a, self.limbs if field == 0 else 8, n, "batch_invert")
         out = np.zeros((self.limbs if field == 0 else 8, n), np.uint32)
         rc = self.l.gecc_batch_invert(self.h, field, C.c_size_t(n), _vp(a), _vp(out))
         if self._check(rc, "gecc_batch_invert"):
@@ -208,10 +304,17 @@ class Context:
     def _pts_out(self, n):
         return np.zeros((self.limbs, n), np.uint32), np.zeros((self.limbs, n), np.uint32), np.zeros(n, np.uint8)
 
+    def _need_points(self, P, n, what):
+        _need_cols(P[0], self.limbs, n, what + " x")
+        _need_cols(P[1], self.limbs, n, what + " y")
+        _need_mask(P[2], n, what + " infinity mask")
+
     def batch_padd(self, P, T):
         if P[0].shape != T[0].shape:
             raise ValueError("batch_padd: buffer sizes differ")  # batch_point.cpp:71-72
         n = P[0].shape[1]
+        self._need_points(P, n, "batch_padd p")
+        self._need_points(T, n, "batch_padd t")
         ox, oy, oi = self._pts_out(n)
         rc = self.l.gecc_batch_padd(self.h, C.c_size_t(n), _vp(P[0]), _vp(P[1]), _vp(P[2]),
                                     _vp(T[0]), _vp(T[1]), _vp(T[2]), _vp(ox), _vp(oy), _vp(oi))
@@ -221,6 +324,7 @@ class Context:
 
     def batch_pdbl(self, P):
         n = P[0].shape[1]
+        self._need_points(P, n, "batch_pdbl")
         ox, oy, oi = self._pts_out(n)
         rc = self.l.gecc_batch_pdbl(self.h, C.c_size_t(n), _vp(P[0]), _vp(P[1]), _vp(P[2]),
                                     _vp(ox), _vp(oy), _vp(oi))
@@ -228,18 +332,28 @@ class Context:
             raise ValueError(f"gecc_batch_pdbl rc={rc}")
         return ox, oy, oi
 
-    def batch_fpmul(self, scalars: np.ndarray):
+    def batch_fpmul(self, scalars: np.ndarray, base: BaseTable | None = None):
+        """scalars[i] * G, or scalars[i] * base for a precomputed table of another point."""
         n = scalars.shape[1]
+        _need_cols(scalars, 8, n, "batch_fpmul scalars")
         ox, oy, oi = self._pts_out(n)
-        rc = self.l.gecc_batch_fpmul(self.h, C.c_size_t(n), _vp(scalars), _vp(ox), _vp(oy), _vp(oi))
+        if base is None:
+            rc = self.l.gecc_batch_fpmul(self.h, C.c_size_t(n), _vp(scalars), _vp(ox), _vp(oy), _vp(oi))
+        else:
+            rc = self.l.gecc_batch_fpmul_base(self.h, base.h, C.c_size_t(n), _vp(scalars), _vp(ox), _vp(oy), _vp(oi))
         if self._check(rc, "gecc_batch_fpmul"):
             raise ValueError(f"gecc_batch_fpmul rc={rc}")
         return ox, oy, oi
+
+    def base_table(self, x: np.ndarray, y: np.ndarray) -> BaseTable:
+        return BaseTable(self, x, y)
 
     def batch_upmul(self, scalars: np.ndarray, P):
         n = scalars.shape[1]
         if P[0].shape[1] != n:
             raise ValueError("batch_upmul: scalar count mismatch")  # batch_point.cpp:239-240
+        _need_cols(scalars, 8, n, "batch_upmul scalars")
+        self._need_points(P, n, "batch_upmul")
         ox, oy, oi = self._pts_out(n)
         rc = self.l.gecc_batch_upmul(self.h, C.c_size_t(n), _vp(scalars), _vp(P[0]), _vp(P[1]),
                                      _vp(P[2]), _vp(ox), _vp(oy), _vp(oi))
@@ -249,6 +363,8 @@ class Context:
 
     def msm(self, scalars: np.ndarray, P):
         n = scalars.shape[1]
+        _need_cols(scalars, 8, n, "msm scalars")
+        self._need_points(P, n, "msm")
         ox, oy, oi = self._pts_out(1)
         rc = self.l.gecc_msm(self.h, C.c_size_t(n), _vp(scalars), _vp(P[0]), _vp(P[1]), _vp(P[2]),
                              _vp(ox), _vp(oy), _vp(oi))
@@ -268,6 +384,8 @@ class Context:
     def sign(self, digests: bytes, secrets: bytes, nonce_seed: int, lane_base: int = 0,
              want_status: bool = True):
         count = len(digests) // 32
+        _need_bytes(digests, 32 * count, "sign digests")
+        _need_bytes(secrets, 32 * count, "sign secrets")
         sig = (C.c_uint8 * max(1, 64 * count))()
         st = (C.c_int32 * max(1, count))() if want_status else None
         rc = self.l.gecc_sign(self.h, C.c_size_t(count), _vp(digests), _vp(secrets),
@@ -275,8 +393,23 @@ class Context:
         self._check(rc, "gecc_sign")
         return rc, bytes(sig)[:64 * count], (list(st)[:count] if st is not None else None)
 
+    def sign_nonces(self, digests: bytes, secrets: bytes, nonces: bytes, want_status: bool = True):
+        """One signing attempt with caller-supplied nonces (gecc_sign_nonces); status 5 = replace."""
+        count = len(digests) // 32
+        _need_bytes(digests, 32 * count, "sign_nonces digests")
+        _need_bytes(secrets, 32 * count, "sign_nonces secrets")
+        _need_bytes(nonces, 32 * count, "sign_nonces nonces")
+        sig = (C.c_uint8 * max(1, 64 * count))()
+        st = (C.c_int32 * max(1, count))() if want_status else None
+        rc = self.l.gecc_sign_nonces(self.h, C.c_size_t(count), _vp(digests), _vp(secrets), _vp(nonces), sig, st)
+        self._check(rc, "gecc_sign_nonces")
+        return rc, bytes(sig)[:64 * count], (list(st)[:count] if st is not None else None)
+
     def verify(self, digests: bytes, publics: bytes, sigs: bytes):
         count = len(digests) // 32
+        _need_bytes(digests, 32 * count, "verify digests")
+        _need_bytes(publics, 65 * count, "verify publics")
+        _need_bytes(sigs, 64 * count, "verify signatures")
         res = (C.c_uint8 * max(1, count))()
         rc = self.l.sm2b_verify(self.h, C.c_size_t(count), _vp(digests), _vp(publics), _vp(sigs), res)
         self._check(rc, "sm2b_verify")
@@ -284,6 +417,8 @@ class Context:
 
     def ecdh(self, secrets: bytes, peers: bytes, want_status: bool = True):
         count = len(secrets) // 32
+        _need_bytes(secrets, 32 * count, "ecdh secrets")
+        _need_bytes(peers, 65 * count, "ecdh peers")
         sh = (C.c_uint8 * max(1, 32 * count))()
         st = (C.c_int32 * max(1, count))() if want_status else None
         rc = self.l.sm2b_ecdh(self.h, C.c_size_t(count), _vp(secrets), _vp(peers), sh, st)

@@ -155,6 +155,79 @@ GECC_HD jac fixed_base_mul(const fe& k_raw, const GTable<WG>& tab) {
     return acc;
 }
 
+// ---- constant-structure forms (GECC_SECRET_UNIFORM, SPEC.md "constant structure"; the
+// reference applies every table entry by select, batch_point.cpp:319-333,420).  The sequence of
+// instructions and of table ROWS touched does not depend on the scalar: every window performs its
+// addition, a zero digit adds a dummy entry whose result is discarded by an arithmetic select,
+// signs are applied by masked negation.  What stays data dependent is only the exceptional-relation
+// branch inside the complete addition (accumulator equal to +- the addend), which a windowed
+// recoding of a scalar below n reaches with negligible probability and which is kept so that the
+// result is correct for EVERY input.
+template <int N>
+GECC_HD feN<N> fe_cmov(uint32_t m, const feN<N>& a, const feN<N>& b) {  // m all ones -> a, zero -> b
+    feN<N> r;
+#pragma unroll
+    for (int i = 0; i < N; ++i) r.w[i] = (a.w[i] & m) | (b.w[i] & ~m);
+    return r;
+}
+// p + q with  keep == all ones -> p returned unchanged (the addition is still executed);
+// p at infinity is handled by select, not by an early return.
+template <class C>
+GECC_HD_CALL cjac<C> jac_madd_uniform(const cjac<C>& p, const caff<C>& q, uint32_t keep) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    const typename C::Fp f{};
+    const uint32_t pinf = jac_is_inf<C>(p) ? 0xFFFFFFFFu : 0u;
+    fe z1z1 = fe_sqr(f, p.Z);
+    fe u2 = fe_mul(f, q.x, z1z1);
+    fe s2 = fe_mul(f, q.y, fe_mul(f, z1z1, p.Z));
+    fe h = fe_sub(f, u2, p.X);
+    fe rr = fe_sub(f, s2, p.Y);
+    jac r;
+    if (!pinf && fe_is_zero(f, h)) {  // accumulator == +-q: see the note above
+        r = fe_is_zero(f, rr) ? jac_dbl<C>(p) : jac_infinity<C>();
+    } else {
+        fe hh = fe_sqr(f, h);
+        fe hhh = fe_mul(f, hh, h);
+        fe v = fe_mul(f, p.X, hh);
+        r.X = fe_sub(f, fe_sub(f, fe_sub(f, fe_sqr(f, rr), hhh), v), v);
+        r.Y = fe_sub(f, fe_mul(f, rr, fe_sub(f, v, r.X)), fe_mul(f, p.Y, hhh));
+        r.Z = fe_mul(f, p.Z, h);
+    }
+    jac o;
+    o.X = fe_cmov(keep, p.X, fe_cmov(pinf, q.x, r.X));
+    o.Y = fe_cmov(keep, p.Y, fe_cmov(pinf, q.y, r.Y));
+    o.Z = fe_cmov(keep, p.Z, fe_cmov(pinf, fe_one(f), r.Z));
+    return o;
+}
+
+// k * G, constant structure: 17 window additions + the removal of the 2^256 G the accumulator
+// starts from, always executed.  Table rows are gathered by address (one 64-byte row per window
+// whatever the digit; digit 0 gathers row 1 and discards the sum).
+template <class C, int WG>
+GECC_HD jac fixed_base_mul_uniform(const fe& k_raw, const GTable<WG>& tab) {
+    const typename C::Fp f{};
+    fe k = scalar_reduce_once<typename C::Fn>(k_raw);
+    Recoded<WG> rc = recode_signed<WG>(k);
+    const aff top = tab.load(256 / WG, 1);  // 2^256 G
+    jac acc;
+    acc.X = top.x; acc.Y = top.y; acc.Z = fe_one(f);
+#pragma unroll 1
+    for (int j = 0; j < 256 / WG; ++j) {
+        const int d = recoded_digit<WG>(rc, j);
+        const int s = d >> 31;                       // all ones when d < 0
+        const int mag = (d ^ s) - s;                 // |d|
+        const uint32_t zero = mag == 0 ? 0xFFFFFFFFu : 0u;
+        aff t = tab.load(j, mag + (int)(zero & 1u));  // row 1 stands in for the zero digit
+        t.y = fe_cmov((uint32_t)s, fe_neg(f, t.y), t.y);
+        acc = jac_madd_uniform<C>(acc, t, zero);
+    }
+    // acc = 2^256 G + sum_j d_j 2^(WG j) G; the true top digit is rc.carry: take 2^256 G off when it is 0
+    aff mt = top;
+    mt.y = fe_neg(f, mt.y);
+    return jac_madd_uniform<C>(acc, mt, rc.carry ? 0xFFFFFFFFu : 0u);
+}
+
 // ------------------------------------------------------------ variable base
 // 8-entry table of the lane's own point, entry e (0..7) = (e+1) * P, affine.
 // `base` points at this lane's first word; consecutive words of one entry are
@@ -201,6 +274,24 @@ struct LaneTable {
         return p;
     }
 };
+
+// entry `e` by a sweep over all eight rows (no secret-dependent address)
+GECC_HD aff lane_table_sweep(const LaneTable& tab, int e) {
+    aff r;
+    r.x = fe_zero();
+    r.y = fe_zero();
+#pragma unroll 1
+    for (int i = 0; i < 8; ++i) {
+        const aff t = tab.load(i);
+        const uint32_t m = i == e ? 0xFFFFFFFFu : 0u;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+            r.x.w[w] |= t.x.w[w] & m;
+            r.y.w[w] |= t.y.w[w] & m;
+        }
+    }
+    return r;
+}
 
 // Builds {1..8} * P in affine form with ONE field inversion (Montgomery's trick
 // over the seven Jacobian Z's).  P must be finite and on the curve.
@@ -260,18 +351,18 @@ GECC_HD void mul_small(uint32_t* out, const uint32_t* a, const uint32_t* b) {
     }
 }
 // r[N] = a[N] - b[N]; returns true when the result is negative, in which case r = b - a
+// (branch-free: the sign of a GLV half is a function of the secret scalar in sign / keygen / ECDH)
 template <int N>
 GECC_HD bool sub_abs(uint32_t* r, const uint32_t* a, const uint32_t* b) {
     r[0] = sub_cc(a[0], b[0]);
 #pragma unroll
     for (int i = 1; i < N; ++i) r[i] = subc_cc(a[i], b[i]);
-    const bool neg = subc(0, 0) != 0;
-    if (neg) {
-        r[0] = sub_cc(b[0], a[0]);
+    const uint32_t m = subc(0, 0);  // all ones when a < b
+    // two's complement negation under the mask: (r ^ m) + (m & 1)
+    r[0] = add_cc(r[0] ^ m, m & 1u);
 #pragma unroll
-        for (int i = 1; i < N; ++i) r[i] = subc_cc(b[i], a[i]);
-    }
-    return neg;
+    for (int i = 1; i < N; ++i) r[i] = addc_cc(r[i] ^ m, 0);
+    return m != 0;
 }
 
 template <class C>
@@ -388,6 +479,71 @@ GECC_HD jac var_base_mul(const fe& k_raw, const LaneTable& tab) {
     }
 }
 
+// k * P, constant structure (the scalar is the secret of ECDH): every window doubles four times
+// and performs its addition(s); entries come from a sweep over the whole lane table.
+template <class C>
+GECC_HD jac var_base_mul_uniform(const fe& k_raw, const LaneTable& tab) {
+    const typename C::Fp f{};
+    fe k = scalar_reduce_once<typename C::Fn>(k_raw);
+    jac acc = jac_infinity<C>();
+    auto step = [&](int d, bool endo) {
+        const int s = d >> 31;
+        const int mag = (d ^ s) - s;
+        const uint32_t zero = mag == 0 ? 0xFFFFFFFFu : 0u;
+        aff t = lane_table_sweep(tab, mag - 1 + (int)(zero & 1u));
+        if constexpr (C::has_glv) {
+            if (endo) {  // public choice: which half of the split this digit belongs to
+                fe beta;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) beta.w[i] = C::beta(i);
+                t.x = fe_mul(f, t.x, beta);
+            }
+        }
+        t.y = fe_cmov((uint32_t)s, fe_neg(f, t.y), t.y);
+        acc = jac_madd_uniform<C>(acc, t, zero);
+    };
+    if constexpr (C::has_glv) {
+        const GlvSplit sp = glv_split<C>(k);
+        const Recoded<4> r1 = recode_signed<4>(sp.m1), r2 = recode_signed<4>(sp.m2);
+        const int n1 = sp.neg1 ? -1 : 0, n2 = sp.neg2 ? -1 : 0;
+#pragma unroll 1
+        for (int j = 33; j >= 0; --j) {
+            if (j != 33) {
+                acc = jac_dbl<C>(acc);
+                acc = jac_dbl<C>(acc);
+                acc = jac_dbl<C>(acc);
+                acc = jac_dbl<C>(acc);
+            }
+            const int d1 = recoded_digit<4>(r1, j), d2 = recoded_digit<4>(r2, j);
+            step((d1 ^ n1) - n1, false);
+            step((d2 ^ n2) - n2, true);
+        }
+    } else {
+        Recoded<4> rc = recode_signed<4>(k);
+        step((int)rc.carry, false);  // top digit: 0 or 1
+#pragma unroll 1
+        for (int j = 63; j >= 0; --j) {
+            acc = jac_dbl<C>(acc);
+            acc = jac_dbl<C>(acc);
+            acc = jac_dbl<C>(acc);
+            acc = jac_dbl<C>(acc);
+            step(recoded_digit<4>(rc, j), false);
+        }
+    }
+    return acc;
+}
+
+template <class C, int WG, bool UNIFORM>
+GECC_HD jac fixed_base_mul_mode(const fe& k, const GTable<WG>& tab) {
+    if constexpr (UNIFORM) return fixed_base_mul_uniform<C, WG>(k, tab);
+    else return fixed_base_mul<C, WG>(k, tab);
+}
+template <class C, bool UNIFORM>
+GECC_HD jac var_base_mul_mode(const fe& k, const LaneTable& tab) {
+    if constexpr (UNIFORM) return var_base_mul_uniform<C>(k, tab);
+    else return var_base_mul<C>(k, tab);
+}
+
 // ------------------------------------------------------------ point codec
 // 65-byte record 0x04 || X || Y -> affine Montgomery point; false when the tag,
 // range or curve check fails (decode_point, curve.cpp:203-217).
@@ -414,31 +570,51 @@ enum { LANE_OK = 0, LANE_NONCE_EXHAUSTED = 5 };  // sm2b_status values
 
 // One lane of ecdsa_sign_batch: e already reduced mod n, 0 < d < n.
 // Writes r || s (64 bytes) or zeros; returns the lane status.
-template <class C, int WG>
+// One signing attempt with the nonce k (0 < k < n), e_m and d_m in Montgomery form mod n
+// (the body of the retry loop, protocol.cpp:133-160).  False when r == 0 or s == 0.
+template <class C, int WG, bool UNIFORM = false>
+GECC_HD bool sign_attempt(const fe& e_m, const fe& d_m, const fe& k, const GTable<WG>& gt, uint8_t* sig64) {
+    const typename C::Fp fp{};
+    const typename C::Fn fn{};
+    jac R = fixed_base_mul_mode<C, WG, UNIFORM>(k, gt);
+    if (jac_is_inf<C>(R)) return false;                   // cannot happen for 0 < k < n
+    fe zinv = fe_inv(fp, R.Z);
+    fe x = fe_from_mont(fp, fe_mul(fp, R.X, fe_sqr(fp, zinv)));
+    fe r = scalar_reduce_once<typename C::Fn>(x);         // coord_mod_n, protocol.cpp:37-39
+    if (fe_is_zero(r)) return false;
+    fe kinv_m = fe_to_mont(fn, safegcd_inverse(fn, k));
+    fe r_m = fe_to_mont(fn, r);
+    fe s_m = fe_mul(fn, kinv_m, fe_add(fn, e_m, fe_mul(fn, r_m, d_m)));
+    fe s = fe_from_mont(fn, s_m);
+    if (fe_is_zero(s)) return false;
+    be32_store(sig64, r);
+    be32_store(sig64 + 32, s);
+    return true;
+}
+
+template <class C, int WG, bool UNIFORM = false>
 GECC_HD int sign_lane(const fe& e, const fe& d, uint64_t seed, uint64_t stream,
                       const GTable<WG>& gt, uint8_t* sig64, uint32_t first_attempt = 0) {
-    const typename C::Fp fp{};
     const typename C::Fn fn{};
     fe e_m = fe_to_mont(fn, e);
     fe d_m = fe_to_mont(fn, d);
 #pragma unroll 1
     for (uint32_t attempt = first_attempt; attempt < 8; ++attempt) {  // protocol.cpp:121
         fe k = nonce_scalar<typename C::Fn>(seed, stream, attempt);
-        jac R = fixed_base_mul<C, WG>(k, gt);
-        if (jac_is_inf<C>(R)) continue;                       // cannot happen for 0 < k < n
-        fe zinv = fe_inv(fp, R.Z);
-        fe x = fe_from_mont(fp, fe_mul(fp, R.X, fe_sqr(fp, zinv)));
-        fe r = scalar_reduce_once<typename C::Fn>(x);         // coord_mod_n, protocol.cpp:37-39
-        if (fe_is_zero(r)) continue;
-        fe kinv_m = fe_to_mont(fn, safegcd_inverse(fn, k));
-        fe r_m = fe_to_mont(fn, r);
-        fe s_m = fe_mul(fn, kinv_m, fe_add(fn, e_m, fe_mul(fn, r_m, d_m)));
-        fe s = fe_from_mont(fn, s_m);
-        if (fe_is_zero(s)) continue;
-        be32_store(sig64, r);
-        be32_store(sig64 + 32, s);
-        return LANE_OK;
+        if (sign_attempt<C, WG, UNIFORM>(e_m, d_m, k, gt, sig64)) return LANE_OK;
     }
+    for (int i = 0; i < 64; ++i) sig64[i] = 0;
+    return LANE_NONCE_EXHAUSTED;
+}
+
+// One attempt with a caller-supplied nonce (gecc_sign_nonces): LANE_OK, or LANE_NONCE_EXHAUSTED
+// when the nonce has to be replaced (outside (0, n), r == 0 or s == 0).
+template <class C, int WG, bool UNIFORM = false>
+GECC_HD int sign_lane_nonce(const fe& e, const fe& d, const fe& k, const GTable<WG>& gt, uint8_t* sig64) {
+    const typename C::Fn fn{};
+    if (scalar_in_range<typename C::Fn>(k) &&
+        sign_attempt<C, WG, UNIFORM>(fe_to_mont(fn, e), fe_to_mont(fn, d), k, gt, sig64))
+        return LANE_OK;
     for (int i = 0; i < 64; ++i) sig64[i] = 0;
     return LANE_NONCE_EXHAUSTED;
 }
@@ -450,7 +626,7 @@ GECC_HD int sign_lane(const fe& e, const fe& d, uint64_t seed, uint64_t stream,
 // cross-thread traffic is needed.  A lane that has to retry (r == 0 or s == 0, probability
 // ~2^-255 unless forced) falls back to sign_lane from attempt 1, which reproduces the
 // reference's per-lane retry sequence exactly.
-template <class C, int WG, int K>
+template <class C, int WG, int K, bool UNIFORM = false>
 GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream0,
                         const GTable<WG>& gt, uint8_t* sig64, int* status) {
     const typename C::Fp fp{};
@@ -459,7 +635,7 @@ GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream
 #pragma unroll 1
     for (int j = 0; j < K; ++j) {
         fe k = nonce_scalar<typename C::Fn>(seed, stream0 + j, 0);
-        jac R = fixed_base_mul<C, WG>(k, gt);
+        jac R = fixed_base_mul_mode<C, WG, UNIFORM>(k, gt);
         X[j] = R.X;
         Z[j] = R.Z;  // never zero for 0 < k < n
         km[j] = fe_to_mont(fn, k);
@@ -486,7 +662,7 @@ GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream
             s = fe_from_mont(fn, s_m);
         }
         if (fe_is_zero(r) || fe_is_zero(s)) {  // retry with fresh nonces (protocol.cpp:142-160)
-            status[j] = sign_lane<C, WG>(e[j], d[j], seed, stream0 + j, gt, out, 1);
+            status[j] = sign_lane<C, WG, UNIFORM>(e[j], d[j], seed, stream0 + j, gt, out, 1);
             continue;
         }
         be32_store(out, r);

@@ -25,6 +25,18 @@ size_t gtable_words();
 // otherwise Montgomery-form coordinates (column-buffer kernels; SM2 uses it for both)
 cudaError_t build_gtable(int curve, bool lazy_plain, uint32_t* tab, uint32_t* bases_scratch,
                          cudaStream_t s);
+// the same table for an arbitrary base point (x, y: 8 Montgomery-form limbs each, device memory);
+// flags[0] is set when the point is not on the curve (the table content is then meaningless)
+cudaError_t build_base_table(int curve, const uint32_t* xy_dev, uint32_t* tab, uint32_t* bases_scratch,
+                             uint32_t* flags, cudaStream_t s);
+// sum of `parts` affine points, each packed as x[L] y[L] inf (2L + 1 words); the sum is written in
+// the same packing to `out` (may alias parts[0]) -- the local additions of the MSM exchange
+cudaError_t launch_point_fold(int curve, int parts, const uint32_t* packed, uint32_t* out, cudaStream_t s);
+// packed (2L + 1 words) <-> separate x / y / inf buffers of one point
+cudaError_t launch_point_pack(int curve, const uint32_t* x, const uint32_t* y, const uint8_t* inf,
+                              uint32_t* packed, cudaStream_t s);
+cudaError_t launch_point_unpack(int curve, const uint32_t* packed, uint32_t* x, uint32_t* y, uint8_t* inf,
+                                cudaStream_t s);
 
 // lane_scratch: verify_scratch_bytes(scratch_lanes) bytes of device memory for the per-lane
 // point tables; batches larger than scratch_lanes are processed in pieces
@@ -35,12 +47,16 @@ cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t
 cudaError_t launch_secret_range(int curve, size_t n, const uint8_t* sec, uint32_t* flags, cudaStream_t s);
 cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed,
                         uint64_t lane_base, const uint32_t* gtab, uint8_t* sig, int32_t* status,
-                        uint32_t* flags, cudaStream_t s);
+                        uint32_t* flags, cudaStream_t s, bool uniform = false);
+// one attempt per lane with caller-supplied 32-byte nonces; status 5 = replace the nonce
+cudaError_t launch_sign_nonces(int curve, size_t n, const uint8_t* dig, const uint8_t* sec,
+                               const uint8_t* nonces, const uint32_t* gtab, uint8_t* sig, int32_t* status,
+                               uint32_t* flags, cudaStream_t s, bool uniform = false);
 cudaError_t launch_keygen(int curve, size_t n, uint64_t seed, uint64_t lane_base,
-                          const uint32_t* gtab, uint8_t* sec, uint8_t* pub, cudaStream_t s);
+                          const uint32_t* gtab, uint8_t* sec, uint8_t* pub, cudaStream_t s, bool uniform = false);
 cudaError_t launch_ecdh(int curve, size_t n, const uint8_t* sec, const uint8_t* peers,
                         uint8_t* shared, int32_t* status, uint32_t* flags, uint32_t* lane_scratch,
-                        size_t scratch_lanes, cudaStream_t s);
+                        size_t scratch_lanes, cudaStream_t s, bool uniform = false);
 cudaError_t launch_fpmul(int curve, size_t n, const uint32_t* k, const uint32_t* gtab, uint32_t* ox,
                          uint32_t* oy, uint8_t* oinf, cudaStream_t s);
 // lane_scratch must cover all n lanes (verify_scratch_bytes(n))

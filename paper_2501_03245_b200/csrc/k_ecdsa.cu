@@ -47,7 +47,7 @@ k_verify_gtab(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restri
 // consecutive lanes and shares the two inversions among them (sign_lanes).
 constexpr int SIGN_K = 4;
 
-template <class C>
+template <class C, bool UNIFORM>
 __global__ void __launch_bounds__(SIGN_THREADS)
 k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ sec, uint64_t seed,
        uint64_t lane_base, const uint32_t* __restrict__ gtab, uint8_t* __restrict__ sig,
@@ -65,7 +65,7 @@ k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ se
     }
     if (all_ok) {
         int st[SIGN_K];
-        sign_lanes<C, GECC_WG, SIGN_K>(e, d, seed, lane_base + i0, gt, sig + 64 * i0, st);
+        sign_lanes<C, GECC_WG, SIGN_K, UNIFORM>(e, d, seed, lane_base + i0, gt, sig + 64 * i0, st);
 #pragma unroll
         for (int j = 0; j < SIGN_K; ++j) status[i0 + j] = st[j];
         return;
@@ -80,8 +80,29 @@ k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ se
             for (int b = 0; b < 64; ++b) sig[64 * i + b] = 0;
             continue;
         }
-        status[i] = sign_lane<C, GECC_WG>(e[j], d[j], seed, lane_base + i, gt, sig + 64 * i);
+        status[i] = sign_lane<C, GECC_WG, UNIFORM>(e[j], d[j], seed, lane_base + i, gt, sig + 64 * i);
     }
+}
+
+// One attempt per lane with caller-supplied nonces (gecc_sign_nonces; the step that
+// ecdsa_sign_batch repeats for the lanes still pending, protocol.cpp:121-164).
+template <class C, bool UNIFORM>
+__global__ void __launch_bounds__(SIGN_THREADS)
+k_sign_nonces(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ sec,
+              const uint8_t* __restrict__ nonces, const uint32_t* __restrict__ gtab,
+              uint8_t* __restrict__ sig, int32_t* __restrict__ status, uint32_t* __restrict__ flags) {
+    const size_t i = blockIdx.x * (size_t)SIGN_THREADS + threadIdx.x;
+    if (i >= n) return;
+    GTable<GECC_WG> gt{gtab};
+    const fe d = be32_load(sec + 32 * i);
+    if (!scalar_in_range<typename C::Fn>(d)) {
+        atomicOr(flags, 1u);
+        status[i] = 2;
+        for (int b = 0; b < 64; ++b) sig[64 * i + b] = 0;
+        return;
+    }
+    const fe e = scalar_reduce_once<typename C::Fn>(be32_load(dig + 32 * i));
+    status[i] = sign_lane_nonce<C, GECC_WG, UNIFORM>(e, d, be32_load(nonces + 32 * i), gt, sig + 64 * i);
 }
 
 // Range check of all secrets of a call (capi.cpp:181-184: one bad secret fails the WHOLE call
@@ -96,7 +117,7 @@ k_secret_range(size_t n, const uint8_t* __restrict__ sec, uint32_t* __restrict__
 }
 
 // capi.cpp:145-169: secret = nonce stream (lane, attempt 0), public = secret * G
-template <class C>
+template <class C, bool UNIFORM>
 __global__ void __launch_bounds__(SIGN_THREADS)
 k_keygen(size_t n, uint64_t seed, uint64_t lane_base, const uint32_t* __restrict__ gtab,
          uint8_t* __restrict__ sec, uint8_t* __restrict__ pub) {
@@ -106,13 +127,13 @@ k_keygen(size_t n, uint64_t seed, uint64_t lane_base, const uint32_t* __restrict
     GTable<GECC_WG> gt{gtab};
     fe d = nonce_scalar<typename C::Fn>(seed, lane_base + i, 0);
     be32_store(sec + 32 * i, d);
-    jac r = fixed_base_mul<C, GECC_WG>(d, gt);
+    jac r = fixed_base_mul_mode<C, GECC_WG, UNIFORM>(d, gt);
     encode_point<C>(pub + 65 * i, jac_to_aff_with<C>(r, fe_inv(f, r.Z)));
 }
 
 // capi.cpp:230-261 + protocol.cpp:224-263.  status: 0 ok, 3 invalid peer,
 // 4 degenerate; a secret >= n flags the whole call malformed.
-template <class C>
+template <class C, bool UNIFORM>
 __global__ void __launch_bounds__(VERIFY_THREADS, 4)
 k_ecdh(size_t n, const uint8_t* __restrict__ sec, const uint8_t* __restrict__ peers,
        uint8_t* __restrict__ shared, int32_t* __restrict__ status, uint32_t* __restrict__ flags,
@@ -134,7 +155,7 @@ k_ecdh(size_t n, const uint8_t* __restrict__ sec, const uint8_t* __restrict__ pe
         return;
     }
     build_lane_table<C>(p, qt);
-    jac r = var_base_mul<C>(d, qt);
+    jac r = var_base_mul_mode<C, UNIFORM>(d, qt);
     if (jac_is_inf<C>(r)) {
         status[i] = 4;
         return;
@@ -312,40 +333,53 @@ cudaError_t launch_secret_range(int curve, size_t n, const uint8_t* sec, uint32_
     return cudaGetLastError();
 }
 
+#define GECC_BY_CURVE_MODE(curve, uniform, KERNEL, GRID, THREADS, ...)                         \
+    do {                                                                                        \
+        if ((curve) == CURVE_SECP) {                                                            \
+            if (uniform) KERNEL<SecpEcdsaCurve, true><<<GRID, THREADS, 0, s>>>(__VA_ARGS__);    \
+            else KERNEL<SecpEcdsaCurve, false><<<GRID, THREADS, 0, s>>>(__VA_ARGS__);           \
+        } else {                                                                                \
+            if (uniform) KERNEL<Sm2Curve, true><<<GRID, THREADS, 0, s>>>(__VA_ARGS__);          \
+            else KERNEL<Sm2Curve, false><<<GRID, THREADS, 0, s>>>(__VA_ARGS__);                 \
+        }                                                                                       \
+    } while (0)
+
 cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed,
                         uint64_t lane_base, const uint32_t* gtab, uint8_t* sig, int32_t* status,
-                        uint32_t* flags, cudaStream_t s) {
+                        uint32_t* flags, cudaStream_t s, bool uniform) {
     if (n == 0) return cudaSuccess;
     const int b = blocks_for((n + SIGN_K - 1) / SIGN_K, SIGN_THREADS);
-    GECC_BY_CURVE(curve,
-        (k_sign<SecpEcdsaCurve><<<b, SIGN_THREADS, 0, s>>>(n, dig, sec, seed, lane_base, gtab, sig, status, flags)),
-        (k_sign<Sm2Curve><<<b, SIGN_THREADS, 0, s>>>(n, dig, sec, seed, lane_base, gtab, sig, status, flags)));
+    GECC_BY_CURVE_MODE(curve, uniform, k_sign, b, SIGN_THREADS, n, dig, sec, seed, lane_base, gtab, sig, status, flags);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sign_nonces(int curve, size_t n, const uint8_t* dig, const uint8_t* sec,
+                               const uint8_t* nonces, const uint32_t* gtab, uint8_t* sig, int32_t* status,
+                               uint32_t* flags, cudaStream_t s, bool uniform) {
+    if (n == 0) return cudaSuccess;
+    const int b = blocks_for(n, SIGN_THREADS);
+    GECC_BY_CURVE_MODE(curve, uniform, k_sign_nonces, b, SIGN_THREADS, n, dig, sec, nonces, gtab, sig, status, flags);
     return cudaGetLastError();
 }
 
 cudaError_t launch_keygen(int curve, size_t n, uint64_t seed, uint64_t lane_base,
-                          const uint32_t* gtab, uint8_t* sec, uint8_t* pub, cudaStream_t s) {
+                          const uint32_t* gtab, uint8_t* sec, uint8_t* pub, cudaStream_t s, bool uniform) {
     if (n == 0) return cudaSuccess;
     const int b = blocks_for(n, SIGN_THREADS);
-    GECC_BY_CURVE(curve,
-        (k_keygen<SecpEcdsaCurve><<<b, SIGN_THREADS, 0, s>>>(n, seed, lane_base, gtab, sec, pub)),
-        (k_keygen<Sm2Curve><<<b, SIGN_THREADS, 0, s>>>(n, seed, lane_base, gtab, sec, pub)));
+    GECC_BY_CURVE_MODE(curve, uniform, k_keygen, b, SIGN_THREADS, n, seed, lane_base, gtab, sec, pub);
     return cudaGetLastError();
 }
 
 cudaError_t launch_ecdh(int curve, size_t n, const uint8_t* sec, const uint8_t* peers,
                         uint8_t* shared, int32_t* status, uint32_t* flags, uint32_t* lane_scratch,
-                        size_t scratch_lanes, cudaStream_t s) {
+                        size_t scratch_lanes, cudaStream_t s, bool uniform) {
     if (n == 0) return cudaSuccess;
     if (!lane_scratch || scratch_lanes == 0) return cudaErrorInvalidValue;
     for (size_t at = 0; at < n; at += scratch_lanes) {
         const size_t m = n - at < scratch_lanes ? n - at : scratch_lanes;
         const int b = blocks_for(m, VERIFY_THREADS);
-        GECC_BY_CURVE(curve,
-            (k_ecdh<SecpEcdsaCurve><<<b, VERIFY_THREADS, 0, s>>>(m, sec + 32 * at, peers + 65 * at, shared + 32 * at,
-                                                                 status + at, flags, lane_scratch)),
-            (k_ecdh<Sm2Curve><<<b, VERIFY_THREADS, 0, s>>>(m, sec + 32 * at, peers + 65 * at, shared + 32 * at,
-                                                           status + at, flags, lane_scratch)));
+        GECC_BY_CURVE_MODE(curve, uniform, k_ecdh, b, VERIFY_THREADS, m, sec + 32 * at, peers + 65 * at,
+                           shared + 32 * at, status + at, flags, lane_scratch);
     }
     return cudaGetLastError();
 }

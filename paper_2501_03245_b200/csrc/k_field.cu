@@ -24,7 +24,29 @@ __global__ void __launch_bounds__(256) k_field_op(int op, size_t n, const uint32
             case 3: r = fe_to_mont(f, x); break;
             case 4: r = fe_from_mont(f, x); break;
             case 5: r = fe_inv(f, x); break;  // safegcd; zero -> zero
-            default: r = fe_is_zero(x) ? x : fe_inv_fermat(f, x); break;  // 6: Fermat cross-check
+            case 6: r = fe_is_zero(x) ? x : fe_inv_fermat(f, x); break;  // Fermat cross-check
+            case 7: {  // mont_reduce of the 2N-limb value y:x through the field's own reduction route
+                uint32_t t[2 * N];
+#pragma unroll
+                for (int k = 0; k < N; ++k) {
+                    t[k] = x.w[k];
+                    t[N + k] = y.w[k];
+                }
+                r = redc(f, t);
+                break;
+            }
+            default: {  // 8..11: the weakly reduced plain field of the fused secp256k1 kernels
+                r = x;
+                if constexpr (std::is_same<F, SecpP>::value) {
+                    const SecpPL l{};
+                    if (op == 8) r = fe_mul(l, x, y);
+                    else if (op == 9) r = fe_sqr(l, x);
+                    else if (op == 10) r = fe_add(l, x, y);
+                    else r = fe_sub(l, x, y);
+                    r = lazy_canon(l, r);
+                }
+                break;
+            }
         }
         col_store(out, n, i, r);
     }

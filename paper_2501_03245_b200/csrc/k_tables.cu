@@ -8,12 +8,28 @@
 
 namespace gecc {
 
+// `base` == nullptr: the curve's generator; otherwise an affine point (x[8] y[8], the field's own
+// representation) whose curve membership is checked here: precompute_base_table rejects off-curve
+// input (batch_point.cpp:343-344), flags[0] reports it.
 template <class C, int WG>
-__global__ void k_gtable_bases(uint32_t* __restrict__ bases) {
+__global__ void k_gtable_bases(uint32_t* __restrict__ bases, const uint32_t* __restrict__ base,
+                               uint32_t* __restrict__ flags) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j >= GTable<WG>::windows) return;
     const typename C::Fp f{};
     aff g = curve_g<C>();
+    if (base) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            g.x.w[i] = base[i];
+            g.y.w[i] = base[8 + i];
+        }
+        const bool ok = fe_lt_modulus(f, g.x) && fe_lt_modulus(f, g.y) && aff_on_curve<C>(g);
+        if (!ok) {
+            if (j == 0) atomicOr(flags, 1u);
+            return;
+        }
+    }
     jac b;
     b.X = g.x; b.Y = g.y; b.Z = fe_one(f);
 #pragma unroll 1
@@ -63,13 +79,30 @@ cudaError_t build_gtable(int curve, bool lazy_plain, uint32_t* tab, uint32_t* ba
     const size_t entries = (size_t)GT::windows * GT::per_window;
     const int blocks = (int)((entries + 127) / 128);
     if (curve == CURVE_SECP && lazy_plain) {  // table of the fused ECDSA kernels (plain coordinates)
-        k_gtable_bases<SecpLCurve, GECC_WG><<<1, 32, 0, s>>>(bases_scratch);
+        k_gtable_bases<SecpLCurve, GECC_WG><<<1, 32, 0, s>>>(bases_scratch, nullptr, nullptr);
         k_gtable_fill<SecpLCurve, GECC_WG><<<blocks, 128, 0, s>>>(bases_scratch, tab);
     } else if (curve == CURVE_SECP) {
-        k_gtable_bases<SecpCurve, GECC_WG><<<1, 32, 0, s>>>(bases_scratch);
+        k_gtable_bases<SecpCurve, GECC_WG><<<1, 32, 0, s>>>(bases_scratch, nullptr, nullptr);
         k_gtable_fill<SecpCurve, GECC_WG><<<blocks, 128, 0, s>>>(bases_scratch, tab);
     } else {
-        k_gtable_bases<Sm2Curve, GECC_WG><<<1, 32, 0, s>>>(bases_scratch);
+        k_gtable_bases<Sm2Curve, GECC_WG><<<1, 32, 0, s>>>(bases_scratch, nullptr, nullptr);
+        k_gtable_fill<Sm2Curve, GECC_WG><<<blocks, 128, 0, s>>>(bases_scratch, tab);
+    }
+    return cudaGetLastError();
+}
+
+// precompute_base_table(c, g) for any on-curve g (batch_point.cpp:341-350): the same windowed
+// table as the generator's, Montgomery-form coordinates (it feeds the column-buffer kernel k_fpmul).
+cudaError_t build_base_table(int curve, const uint32_t* xy_dev, uint32_t* tab, uint32_t* bases_scratch,
+                             uint32_t* flags, cudaStream_t s) {
+    using GT = GTable<GECC_WG>;
+    const size_t entries = (size_t)GT::windows * GT::per_window;
+    const int blocks = (int)((entries + 127) / 128);
+    if (curve == CURVE_SECP) {
+        k_gtable_bases<SecpCurve, GECC_WG><<<1, 32, 0, s>>>(bases_scratch, xy_dev, flags);
+        k_gtable_fill<SecpCurve, GECC_WG><<<blocks, 128, 0, s>>>(bases_scratch, tab);
+    } else {
+        k_gtable_bases<Sm2Curve, GECC_WG><<<1, 32, 0, s>>>(bases_scratch, xy_dev, flags);
         k_gtable_fill<Sm2Curve, GECC_WG><<<blocks, 128, 0, s>>>(bases_scratch, tab);
     }
     return cudaGetLastError();

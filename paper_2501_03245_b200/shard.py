@@ -46,7 +46,9 @@ def sign_sharded(engine, digests: bytes, secrets: bytes, nonce_seed: int, rank: 
     parts = _gather_bytes((rc, sig, st), dist, world)
     rcs = [p[0] for p in parts]
     first_bad = next((r for r in rcs if r != 0), 0)
-    return first_bad, b"".join(p[1] for p in parts), sum((p[2] for p in parts), [])
+    if first_bad:   # a failed rank returned no usable slice: joining would misalign the lanes
+        return first_bad, b"", []
+    return 0, b"".join(p[1] for p in parts), sum((p[2] for p in parts), [])
 
 
 def verify_sharded(engine, digests: bytes, publics: bytes, sigs: bytes, rank: int, world: int,
@@ -55,15 +57,18 @@ def verify_sharded(engine, digests: bytes, publics: bytes, sigs: bytes, rank: in
     b, e = shard_range(n, rank, world)
     rc, res = engine.verify(digests[32 * b:32 * e], publics[65 * b:65 * e], sigs[64 * b:64 * e])
     parts = _gather_bytes((rc, res), dist, world)
-    return next((p[0] for p in parts if p[0] != 0), 0), b"".join(p[1] for p in parts)
+    bad = next((p[0] for p in parts if p[0] != 0), 0)
+    return bad, (b"" if bad else b"".join(p[1] for p in parts))
 
 
 def keygen_sharded(engine, seed: int, count: int, rank: int, world: int, dist=None):
     b, e = shard_range(count, rank, world)
     rc, sec, pub = engine.keygen(seed, e - b, lane_base=b)
     parts = _gather_bytes((rc, sec, pub), dist, world)
-    return (next((p[0] for p in parts if p[0] != 0), 0), b"".join(p[1] for p in parts),
-            b"".join(p[2] for p in parts))
+    bad = next((p[0] for p in parts if p[0] != 0), 0)
+    if bad:
+        return bad, b"", b""
+    return 0, b"".join(p[1] for p in parts), b"".join(p[2] for p in parts)
 
 
 def msm_sharded(engine, scalars: np.ndarray, points: Sequence[np.ndarray], rank: int, world: int,
@@ -77,7 +82,9 @@ def msm_sharded(engine, scalars: np.ndarray, points: Sequence[np.ndarray], rank:
     part = engine.msm(cut(scalars), tuple(cut(a) for a in points))
     payload = tuple(np.ascontiguousarray(a).tobytes() for a in part)
     parts = _gather_bytes(payload, dist, world)
-    pts = [(np.frombuffer(p[0], np.uint32).reshape(8, 1).copy(), np.frombuffer(p[1], np.uint32).reshape(8, 1).copy(),
+    # limbs per coordinate follow the payload: 8 on the 256-bit curves, 12 on BLS12-381 / BLS12-377
+    pts = [(np.frombuffer(p[0], np.uint32).reshape(len(p[0]) // 4, 1).copy(),
+            np.frombuffer(p[1], np.uint32).reshape(len(p[1]) // 4, 1).copy(),
             np.frombuffer(p[2], np.uint8).copy()) for p in parts]
     if add_points is not None:
         return add_points(pts)

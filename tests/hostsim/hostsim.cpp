@@ -176,11 +176,15 @@ void store_point(const jac& r, uint32_t* ox, uint32_t* oy, uint8_t* oinf, size_t
     oinf[i] = 0;
 }
 
+// 1: the constant-structure forms (GECC_SECRET_UNIFORM) of k*G, k*P, sign, keygen
+static int g_uniform = 0;
+
 template <class C>
 int fpmul_t(size_t n, const uint32_t* k, uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
     GTable<HS_WG> gt{host_gtable<C>().data()};
     for (size_t i = 0; i < n; ++i)
-        store_point<C>(fixed_base_mul<C, HS_WG>(col_get(k, n, i), gt), ox, oy, oinf, n, i);
+        store_point<C>(g_uniform ? fixed_base_mul_uniform<C, HS_WG>(col_get(k, n, i), gt)
+                                 : fixed_base_mul<C, HS_WG>(col_get(k, n, i), gt), ox, oy, oinf, n, i);
     return 0;
 }
 template <class C>
@@ -192,7 +196,8 @@ int upmul_t(size_t n, const uint32_t* k, const uint32_t* px, const uint32_t* py,
         if (pinf && pinf[i]) { store_point<C>(jac_infinity<C>(), ox, oy, oinf, n, i); continue; }
         aff p{col_get(px, n, i), col_get(py, n, i)};
         build_lane_table<C>(p, lt);
-        store_point<C>(var_base_mul<C>(col_get(k, n, i), lt), ox, oy, oinf, n, i);
+        store_point<C>(g_uniform ? var_base_mul_uniform<C>(col_get(k, n, i), lt) : var_base_mul<C>(col_get(k, n, i), lt),
+                       ox, oy, oinf, n, i);
     }
     return 0;
 }
@@ -209,13 +214,28 @@ int sign_t(size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed, uint
             e[j] = scalar_reduce_once<typename C::Fn>(be32_load(dig + 32 * (i + j)));
             d[j] = be32_load(sec + 32 * (i + j));
         }
-        sign_lanes<C, HS_WG, K>(e, d, seed, base + i, gt, sig + 64 * i, s4);
+        if (g_uniform) sign_lanes<C, HS_WG, K, true>(e, d, seed, base + i, gt, sig + 64 * i, s4);
+        else sign_lanes<C, HS_WG, K>(e, d, seed, base + i, gt, sig + 64 * i, s4);
         for (int j = 0; j < K; ++j) st[i + j] = s4[j];
     }
     for (; i < n; ++i) {
         fe e = scalar_reduce_once<typename C::Fn>(be32_load(dig + 32 * i));
         fe d = be32_load(sec + 32 * i);
-        st[i] = sign_lane<C, HS_WG>(e, d, seed, base + i, gt, sig + 64 * i);
+        st[i] = g_uniform ? sign_lane<C, HS_WG, true>(e, d, seed, base + i, gt, sig + 64 * i)
+                          : sign_lane<C, HS_WG>(e, d, seed, base + i, gt, sig + 64 * i);
+    }
+    return 0;
+}
+// one attempt per lane with explicit nonces (k_sign_nonces)
+template <class C>
+int sign_nonces_t(size_t n, const uint8_t* dig, const uint8_t* sec, const uint8_t* nonces, uint8_t* sig, int32_t* st) {
+    GTable<HS_WG> gt{host_gtable<C>().data()};
+    for (size_t i = 0; i < n; ++i) {
+        fe e = scalar_reduce_once<typename C::Fn>(be32_load(dig + 32 * i));
+        fe d = be32_load(sec + 32 * i);
+        fe k = be32_load(nonces + 32 * i);
+        st[i] = g_uniform ? sign_lane_nonce<C, HS_WG, true>(e, d, k, gt, sig + 64 * i)
+                          : sign_lane_nonce<C, HS_WG>(e, d, k, gt, sig + 64 * i);
     }
     return 0;
 }
@@ -235,7 +255,7 @@ int keygen_t(size_t n, uint64_t seed, uint64_t base, uint8_t* sec, uint8_t* pub)
     for (size_t i = 0; i < n; ++i) {
         fe d = nonce_scalar<typename C::Fn>(seed, base + i, 0);
         be32_store(sec + 32 * i, d);
-        jac r = fixed_base_mul<C, HS_WG>(d, gt);
+        jac r = g_uniform ? fixed_base_mul_uniform<C, HS_WG>(d, gt) : fixed_base_mul<C, HS_WG>(d, gt);
         encode_point<C>(pub + 65 * i, jac_to_aff_with<C>(r, fe_inv(f, r.Z)));
     }
     return 0;
@@ -257,6 +277,11 @@ int hs_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, uint64_
 int hs_verify(int curve, size_t n, const uint8_t* dig, const uint8_t* pub, const uint8_t* sig,
               uint8_t* res) {
     return curve == 0 ? verify_t<Sm2Curve>(n, dig, pub, sig, res) : curve == 2 ? verify_t<SecpLCurve>(n, dig, pub, sig, res) : verify_t<SecpCurve>(n, dig, pub, sig, res);
+}
+void hs_set_uniform(int on) { g_uniform = on; }
+int hs_sign_nonces(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, const uint8_t* nonces,
+                   uint8_t* sig, int32_t* st) {
+    return curve == 0 ? sign_nonces_t<Sm2Curve>(n, dig, sec, nonces, sig, st) : curve == 2 ? sign_nonces_t<SecpLCurve>(n, dig, sec, nonces, sig, st) : sign_nonces_t<SecpCurve>(n, dig, sec, nonces, sig, st);
 }
 int hs_keygen(int curve, size_t n, uint64_t seed, uint64_t base, uint8_t* sec, uint8_t* pub) {
     return curve == 0 ? keygen_t<Sm2Curve>(n, seed, base, sec, pub) : curve == 2 ? keygen_t<SecpLCurve>(n, seed, base, sec, pub) : keygen_t<SecpCurve>(n, seed, base, sec, pub);

@@ -113,3 +113,16 @@ def bls_point_op(op, P, T=None, k=None, curve=2):
                                _p(P[2]), _p(T[0]), _p(T[1]), _p(T[2]), _p(o[0]), _p(o[1]), _p(o[2]))
     assert rc == 0, rc
     return o
+
+
+def set_uniform(on: bool):
+    """Selects the constant-structure forms (GECC_SECRET_UNIFORM) of k*G, k*P, sign and keygen."""
+    lib().hs_set_uniform(1 if on else 0)
+
+
+def sign_nonces(curve, dig, sec, nonces):
+    n = len(dig) // 32
+    sig = (C.c_uint8 * max(1, 64 * n))()
+    st = (C.c_int32 * max(1, n))()
+    assert lib().hs_sign_nonces(curve, C.c_size_t(n), _p(dig), _p(sec), _p(nonces), sig, st) == 0
+    return bytes(sig)[:64 * n], list(st)[:n]

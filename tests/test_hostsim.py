@@ -188,3 +188,68 @@ def test_hostsim_sign_group_retry(cid, hs_curve):
     k1 = E.nonce(c, seed, rig, 1)
     assert want[1][64 * rig:64 * rig + 32] == E.be32(E.ec_mul(c, k1, c.G)[0] % c.n)  # really retried
     assert H.sign(hs_curve, bytes(dig), sec, seed) == (want[1], want[2])
+
+
+@pytest.mark.parametrize("cid,hs_curve", [(0, 0), (1, 1), (1, 2)])
+def test_hostsim_uniform_mode_equals_fast(cid, hs_curve):
+    """GECC_SECRET_UNIFORM (constant-structure k*G / k*P: every window adds, entries by select,
+    SPEC.md 'constant structure', batch_point.cpp:319-333,420) gives the same bytes as the fast
+    path and as the oracle -- edge scalars {0, 1, 2^77, n-1, all-ones}, zero-digit-heavy scalars,
+    random scalars, keygen and sign."""
+    c = E.CURVES[cid]
+    rng = random.Random(31 + hs_curve)
+    W = H.lib().hs_window_bits()
+    sparse = [1 << (W * j) for j in range(0, 256 // W, 7)] + [(1 << 255) | 1, c.n - (1 << 200), (1 << (W * 5)) - 1]
+    ks = [0, 1, 2, 1 << 77, c.n - 1, c.n - 2, (1 << 256) - 1, c.n, c.n + 1] + sparse + [rng.randrange(1 << 256) for _ in range(40)]
+    k = O.ints_to_cols(ks)
+    try:
+        H.set_uniform(False)
+        fast_f = H.batch_fpmul(hs_curve, k)
+        if hs_curve != 2:   # column-buffer checks need the Montgomery-form curve
+            P = O.batch_fpmul(cid, O.ints_to_cols([rng.randrange(1, c.n) for _ in ks]))
+            fast_u = H.batch_upmul(hs_curve, k, P)
+        H.set_uniform(True)
+        uni_f = H.batch_fpmul(hs_curve, k)
+        for a, b in zip(fast_f, uni_f):
+            assert (a == b).all()
+        if hs_curve != 2:
+            want = O.batch_fpmul(cid, k)
+            for a, b in zip(uni_f, want):
+                assert (a == b).all()
+            uni_u = H.batch_upmul(hs_curve, k, P)
+            for a, b, w in zip(fast_u, uni_u, O.pmul_serial(cid, k, P)):
+                assert (a == b).all() and (a == w).all()
+        ent = ECDSA["secp256k1" if cid == 1 else "sm2"]
+        n = ent["n"]
+        sec, pub = bytes.fromhex(ent["secrets"]), bytes.fromhex(ent["publics"])
+        dig, sig = bytes.fromhex(ent["digests"]), bytes.fromhex(ent["sigs"])
+        assert H.keygen(hs_curve, ent["keygen_seed"], n) == (sec, pub)
+        assert H.sign(hs_curve, dig, sec, ent["nonce_seed"]) == (sig, [0] * n)
+    finally:
+        H.set_uniform(False)
+
+
+@pytest.mark.parametrize("cid,hs_curve", [(0, 0), (1, 2)])
+def test_hostsim_sign_with_explicit_nonces(cid, hs_curve):
+    """gecc_sign_nonces' lane: with the deterministic source's attempt-0 nonces it reproduces
+    sm2b_sign; a nonce outside (0, n) and a rigged s == 0 ask for a replacement (status 5)."""
+    c = E.CURVES[cid]
+    rng = random.Random(5 + cid)
+    n, seed = 10, 21
+    sec = b"".join(E.be32(rng.randrange(1, c.n)) for _ in range(n))
+    dig = bytearray(rng.randrange(256) for _ in range(32 * n))
+    nonces = bytearray(b"".join(E.be32(E.nonce(c, seed, i, 0)) for i in range(n)))
+    want = O.ecdsa_sign(cid, bytes(dig), sec, seed)
+    assert H.sign_nonces(hs_curve, bytes(dig), sec, bytes(nonces)) == (want[1], [0] * n)
+    # lane 3: nonce 0; lane 4: nonce n; lane 6: e + r d == 0 -> s == 0
+    nonces[32 * 3:32 * 4] = bytes(32)
+    nonces[32 * 4:32 * 5] = E.be32(c.n)
+    d6 = int.from_bytes(sec[32 * 6:32 * 7], "big")
+    r6 = E.ec_mul(c, E.nonce(c, seed, 6, 0), c.G)[0] % c.n
+    dig[32 * 6:32 * 7] = E.be32((-r6 * d6) % c.n)
+    sig, st = H.sign_nonces(hs_curve, bytes(dig), sec, bytes(nonces))
+    assert st == [0, 0, 0, 5, 5, 0, 5, 0, 0, 0]
+    for i in (3, 4, 6):
+        assert sig[64 * i:64 * i + 64] == bytes(64)
+    for i in (0, 1, 2, 5, 7, 8, 9):
+        assert sig[64 * i:64 * i + 64] == want[1][64 * i:64 * i + 64]
