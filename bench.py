@@ -53,6 +53,8 @@ def parse():
                     help="sm2 = the reference's own curve; bls12_381 / bls12_377 (12-limb coordinates) are served by --workload msm only")
     ap.add_argument("--cpu-sample-log2", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="headline leg only (default: the verify headline also carries sign / MSM / padd legs in `extra`)")
     return ap.parse_args()
 
 
@@ -228,7 +230,9 @@ def run_reference_arm(args, rank):
     if wl not in ("verify", "sign"):
         print(json.dumps({"impl": "reference", "unavailable": f"the reference has no {args.curve} {wl}"}), flush=True)
         return
-    log2 = args.cpu_sample_log2 or (13 if wl == "verify" else 14)
+    # 2^16 lanes per step: the reference's throughput is flat beyond 2^12 but a 2^13 sample under-reports
+    # it by ~28 % (BENCH_r01: 12.9 k/s at 2^13 against 17.9 k/s at 2^16 on the same box)
+    log2 = args.cpu_sample_log2 or 16
     n = 1 << log2
     dig, sec, pub, sig = make_records_cpu(n)
     if wl == "verify":
@@ -268,36 +272,39 @@ def run_reference_arm(args, rank):
 # Executed field products per lane of OUR kernels: counted by running the product's own
 # lane code on the host with instrumented multiply / square / safegcd
 # (tools/count_ops.py -> tools/op_counts.json; method in DESIGN.md "work per lane").
-# Multiply-pipe issue slots per product, in IMAD.WIDE units (IMAD.WIDE and IMAD.HI = 1,
-# 32-bit IMAD = 1/2: measured issue rates are 32 and 64 per clk per SM):
+# Roofline unit = one IMAD.WIDE (32 x 32 -> 64 multiply-add), the instruction whose issue rate
+# (32 per clk per SM) bounds the path.  ONLY IMAD.WIDE is counted per product -- the 32-bit IMAD
+# / IMAD.HI a reduction also issues are overhead, not work -- so the figure can be checked
+# against the ncu opcode mix (profiles/*_opmix.csv: IMAD.WIDE warp instructions x active lanes).
 SLOTS = {
-    "mul_special": 64 + 8 + 8 * 0.5,            # product + word-serial secp256k1 REDC
-    "sqr_special": 36 + 8 + 8 * 0.5,
-    "mul_generic": 64 + 64 + 8 * 0.5,           # product + word-serial Montgomery rows (m_i * q) + the 8 m_i
-    "sqr_generic": 36 + 64 + 8 * 0.5,
-    "safegcd_special": 20 * (36 + 54),          # 20 rounds of two 2x2 matrix updates
+    "mul_special": 64 + 8,             # 8 x 8 product + the 8 wide multiplies of the pseudo-Mersenne fold
+    "sqr_special": 36 + 8,
+    "mul_generic": 64 + 64,            # product + word-serial Montgomery rows (m_i * q)
+    "sqr_generic": 36 + 64,
+    "safegcd_special": 20 * (36 + 54),  # 20 rounds of two 2x2 matrix updates on 9 limbs
     "safegcd_generic": 20 * (36 + 54),
 }
+IO_BYTES = {"verify": 162, "sign": 132, "padd": 194, "msm": 96}   # algorithmic bytes per unit
+KERNEL = {"verify": "k_verify_gtab", "sign": "k_sign", "padd": "k_batch_padd", "msm": "k_msm_*"}
 
 
-def msm_products_per_point(kind):
-    """Executed field products per input point of the batch-affine MSM at 2^20 points (c = 16):
-    17 windows x (1 - 1/32) tree joins, each 5 mul + 1 sqr (denominator product, two unwind
-    products, lambda, lambda^2, y) plus its share of the block scan (14 products per thread of
-    16 / 16 / 8 / 4 / 2 / 2 joins on levels 0..5: 1.2 per join on average); then the three marginal
-    sums: 3 x 1.5 mixed Jacobian additions (8M + 3S) per BUCKET, 17 x 2^15 buckets."""
-    joins = 17 * (1 - 1 / 32)
-    madds = 3 * 1.5 * 17 * 2**15 / 2**20
+def msm_products_per_point(kind, log2n=20, windows=17, bucket_bits=15):
+    """Executed field products per input point of the batch-affine MSM: `windows` x (1 - 1/32)
+    tree joins, each 5 mul + 1 sqr (denominator product, two unwind products, lambda, lambda^2, y)
+    plus its share of the block scan (1.2 per join on average); then the three marginal sums:
+    3 x 1.5 mixed Jacobian additions (8M + 3S) per BUCKET, windows x 2^bucket_bits buckets."""
+    joins = windows * (1 - 1 / 32)
+    madds = 3 * 1.5 * windows * 2**bucket_bits / 2**log2n
     return {f"mul_{kind}": joins * (5 + 1.2) + madds * 8, f"sqr_{kind}": joins * 1 + madds * 3}
 
 
-def work_per_lane(workload, curve="secp256k1"):
+def work_per_lane(workload, curve="secp256k1", log2n=20, msm_shape=None):
     with open(os.path.join(ROOT, "tools", "op_counts.json")) as f:
         counts = json.load(f)[curve]
-    if workload == "padd":   # compress 1 + scatter 2 + chord 3 (one a square) + inversion share
-        c = {"mul_special": 5 + 2 / 16, "sqr_special": 1, "safegcd_special": 1 / 16}
+    if workload == "padd":   # ALGORITHMIC work of one affine addition under Montgomery's trick (SURVEY.md 8d):
+        c = {"mul_special": 5, "sqr_special": 1}   # 6 products per pair; the shared inversion is not counted
     elif workload == "msm":
-        c = msm_products_per_point("special")
+        c = msm_products_per_point("special", log2n, *(msm_shape or (17, 15)))
     else:
         c = counts[workload]
     table = dict(SLOTS)
@@ -306,6 +313,319 @@ def work_per_lane(workload, curve="secp256k1"):
     slots = sum(table[k] * v for k, v in c.items())
     products = sum(v for k, v in c.items() if not k.startswith("safegcd"))
     return c, slots, products
+
+
+class GpuArm:
+    """Synthetic records + device buffers of one rank, and the timed legs over them."""
+
+    def __init__(self, args, rank, local_rank, world):
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+        import paper_2501_03245_b200 as gecc
+        self.np, self.torch, self.dist, self.gecc = np, torch, dist, gecc
+        self.args, self.rank, self.local_rank, self.world = args, rank, local_rank, world
+        if not torch.cuda.is_available():
+            raise SystemExit("bench.py: no CUDA device; the product has no CPU path "
+                             "(use --impl reference for the CPU arm)")
+        torch.cuda.set_device(local_rank)
+        if world > 1 or (os.environ.get("GECC_BENCH_FORCE_EXCHANGE") == "1" and "RANK" in os.environ):
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        self.ctx = gecc.Context(gecc.SM2 if args.curve == "sm2" else gecc.SECP256K1, local_rank)
+        self.l = gecc.lib()
+        self.stream = torch.cuda.Stream()          # all timed work and its events share this stream
+        torch.cuda.set_stream(self.stream)
+        self.ctx.set_stream(self.stream.cuda_stream)
+        peak = self.ctx.microbench(1, 3000)        # dependent IMAD.WIDE chain, 8 warps per scheduler
+        self.peak = peak
+        self.peak_mad_per_s = peak["total_ops"] / peak["seconds"]
+        self.records = {}
+        self.points = {}
+        self.comm_ready = False
+
+    # ---- plumbing
+    def vp(self, t):
+        return C.c_void_p(t.data_ptr())
+
+    def barrier(self):
+        self.torch.cuda.synchronize()
+        if self.world > 1:
+            self.dist.barrier()
+            self.torch.cuda.synchronize()
+
+    def max_over_ranks(self, x):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device="cuda")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def pin(self, a):
+        return self.torch.from_numpy(a).pin_memory()
+
+    # ---- synthetic inputs, generated on the GPU by our own keygen / sign / fpmul (not timed)
+    def ensure_records(self, n):
+        if n in self.records:
+            return self.records[n]
+        np, torch, l, ctx, vp = self.np, self.torch, self.l, self.ctx, self.vp
+        lane_base = self.rank * n
+        h_sec, h_pub = np.empty(32 * n, np.uint8), np.empty(65 * n, np.uint8)
+        rc = l.gecc_keygen(ctx.h, C.c_uint64(1), C.c_uint64(lane_base), C.c_size_t(n),
+                           C.c_void_p(h_sec.ctypes.data), C.c_void_p(h_pub.ctypes.data))
+        assert rc == 0, l.gecc_last_error(ctx.h)
+        h_dig = np.frombuffer(np.random.RandomState(1234 + self.rank).bytes(32 * n), np.uint8).copy()
+        d_dig, d_sec, d_pub = (torch.from_numpy(a).cuda() for a in (h_dig, h_sec, h_pub))
+        d_sig = torch.empty(64 * n, dtype=torch.uint8, device="cuda")
+        d_res = torch.empty(n, dtype=torch.uint8, device="cuda")
+        d_st = torch.empty(n, dtype=torch.int32, device="cuda")
+        rc = l.gecc_sign_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_sec), C.c_uint64(7),
+                             C.c_uint64(lane_base), vp(d_sig), vp(d_st))
+        assert rc == 0
+        torch.cuda.synchronize()
+        assert int(d_st.abs().sum()) == 0
+        h_sig = d_sig.cpu().numpy()
+        # equivalence gate before timing (bench.cpp:253-256): spot lanes vs the oracle
+        from oracle import coracle as O
+        rs = np.random.RandomState(99)
+        idx = [int(i) for i in rs.choice(n, 24, replace=False)]
+        pick = lambda a, w: b"".join(a[w * i:w * i + w].tobytes() for i in idx)
+        for i in idx[:8]:
+            want = O.ecdsa_sign(SECP, h_dig[32 * i:32 * i + 32].tobytes(), h_sec[32 * i:32 * i + 32].tobytes(),
+                                7, lane_base=lane_base + i)[1]
+            assert want == h_sig[64 * i:64 * i + 64].tobytes(), "sign parity gate failed"
+        bad = bytearray(pick(h_sig, 64))
+        bad[64 * 3 + 9] ^= 4
+        want = O.ecdsa_verify(SECP, pick(h_dig, 32), pick(h_pub, 65), bytes(bad))[1]
+        got = ctx.verify(pick(h_dig, 32), pick(h_pub, 65), bytes(bad))[1]
+        assert want == got and sum(want) == 23, "verify parity gate failed"
+        r = dict(n=n, lane_base=lane_base, h_dig=h_dig, h_sec=h_sec, h_pub=h_pub, h_sig=h_sig, d_dig=d_dig,
+                 d_sec=d_sec, d_pub=d_pub, d_sig=d_sig, d_res=d_res, d_st=d_st)
+        self.records[n] = r
+        return r
+
+    def ensure_points(self, n):
+        if n in self.points:
+            return self.points[n]
+        np, torch, l, ctx, vp = self.np, self.torch, self.l, self.ctx, self.vp
+        rs = np.random.RandomState(99 + self.rank)
+        k1 = torch.from_numpy(rs.randint(0, 2**32, size=(8, n), dtype=np.uint64).astype(np.uint32)).cuda()
+        k2 = torch.from_numpy(rs.randint(0, 2**32, size=(8, n), dtype=np.uint64).astype(np.uint32)).cuda()
+        col = lambda m=n: torch.empty((8, m), dtype=torch.int32, device="cuda")
+        u8 = lambda m: torch.empty(m, dtype=torch.uint8, device="cuda")
+        P = (col(), col(), u8(n)); T = (col(), col(), u8(n)); S = (col(), col(), u8(n))
+        assert l.gecc_batch_fpmul_dev(ctx.h, C.c_size_t(n), vp(k1), vp(P[0]), vp(P[1]), vp(P[2])) == 0
+        assert l.gecc_batch_fpmul_dev(ctx.h, C.c_size_t(n), vp(k2), vp(T[0]), vp(T[1]), vp(T[2])) == 0
+        torch.cuda.synchronize()
+        M = (col(1), col(1), u8(1))
+        p = dict(n=n, k1=k1, k2=k2, P=P, T=T, S=S, M=M)
+        self.points[n] = p
+        return p
+
+    def ensure_comm(self):
+        """MSM exchange communicator in the library (ncclCommInitRank); torch.distributed only
+        carries the 128-byte id from rank 0."""
+        if self.comm_ready:
+            return
+        uid = [self.gecc.comm_unique_id() if self.rank == 0 else None]
+        if self.world > 1:
+            self.dist.broadcast_object_list(uid, src=0)
+        self.ctx.comm_init_rank(self.world, self.rank, uid[0])
+        self.comm_ready = True
+
+    # ---- one leg: device-resident value, e2e through the host API, roofline, CPU baseline
+    def run(self, wl, log2n, with_cpu=True):
+        np, torch, l, ctx, vp, args = self.np, self.torch, self.l, self.ctx, self.vp, self.args
+        n = 1 << log2n
+        world, rank = self.world, self.rank
+        stream = self.stream
+        msm_exchange = wl == "msm" and (world > 1 or os.environ.get("GECC_BENCH_FORCE_EXCHANGE") == "1")
+        if wl in ("verify", "sign"):
+            r = self.ensure_records(n)
+            lane_base = r["lane_base"]
+        else:
+            p = self.ensure_points(n)
+            P, T, S, M = p["P"], p["T"], p["S"], p["M"]
+            if msm_exchange:
+                self.ensure_comm()
+
+        def step_dev():
+            if wl == "verify":
+                return l.gecc_verify_dev(ctx.h, C.c_size_t(n), vp(r["d_dig"]), vp(r["d_pub"]), vp(r["d_sig"]), vp(r["d_res"]))
+            if wl == "sign":
+                return l.gecc_sign_dev(ctx.h, C.c_size_t(n), vp(r["d_dig"]), vp(r["d_sec"]), C.c_uint64(7),
+                                       C.c_uint64(lane_base), vp(r["d_sig"]), vp(r["d_st"]))
+            if wl == "msm":   # sum_i k2_i * P_i, one point out
+                rc = l.gecc_msm_dev(ctx.h, C.c_size_t(n), vp(p["k2"]), vp(P[0]), vp(P[1]), vp(P[2]),
+                                    vp(M[0]), vp(M[1]), vp(M[2]))
+                if not msm_exchange or rc != 0:
+                    return rc
+                # sharded MSM (SURVEY 8e): every rank summed its own point range; the library
+                # all-gathers the partial sums over NCCL and adds them locally, in C++
+                return l.gecc_msm_combine_dev(ctx.h, vp(M[0]), vp(M[1]), vp(M[2]))
+            return l.gecc_batch_padd_dev(ctx.h, C.c_size_t(n), vp(P[0]), vp(P[1]), vp(P[2]), vp(T[0]),
+                                         vp(T[1]), vp(T[2]), vp(S[0]), vp(S[1]), vp(S[2]))
+
+        # ---- value: device-resident
+        for _ in range(args.warmup):
+            assert step_dev() == 0
+        self.barrier()
+        sampler = ClockSampler(self.local_rank)
+        launches0 = ctx.launches
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            assert step_dev() == 0
+        ev1.record(stream)
+        self.barrier()
+        launches = ctx.launches - launches0
+        dev_s = self.max_over_ranks(ev0.elapsed_time(ev1) * 1e-3)
+        clocks = sampler.stop()
+        if wl == "verify":
+            assert int(r["d_res"].sum()) == n, "timed verify produced rejects"
+        per_launch_s = dev_s / args.steps
+        value = world * n * args.steps / dev_s
+        if wl == "msm":   # time-like metric: ms per 2^log2n-point MSM (per GPU; ranks run their own range)
+            value = per_launch_s * 1e3
+
+        # ---- e2e: reference-facing C ABI, pinned host buffers, copies inside the timed region
+        pin = self.pin
+        if wl in ("verify", "sign"):
+            p_dig, p_pub, p_sig, p_sec = pin(r["h_dig"]), pin(r["h_pub"]), pin(r["h_sig"].copy()), pin(r["h_sec"])
+            p_res = torch.empty(n, dtype=torch.uint8).pin_memory()
+            p_out = torch.empty(64 * n, dtype=torch.uint8).pin_memory()
+            p_st = torch.empty(n, dtype=torch.int32).pin_memory()
+            if wl == "verify":
+                call = lambda: l.sm2b_verify(ctx.h, C.c_size_t(n), vp(p_dig), vp(p_pub), vp(p_sig), vp(p_res))
+                h2d, d2h, api = 161 * n, n, "sm2b_verify"
+            else:
+                call = lambda: l.gecc_sign(ctx.h, C.c_size_t(n), vp(p_dig), vp(p_sec), C.c_uint64(7),
+                                           C.c_uint64(lane_base), vp(p_out), vp(p_st))
+                h2d, d2h, api = 64 * n, 68 * n, "gecc_sign"
+        else:
+            h = lambda t, i: pin(np.ascontiguousarray(t.cpu().numpy().view(np.uint32 if i < 2 else np.uint8)))
+            hP = tuple(h(t, i) for i, t in enumerate(P))
+            hT = tuple(h(t, i) for i, t in enumerate(T))
+            hk = pin(p["k2"].cpu().numpy())
+            m_out = n if wl == "padd" else 1
+            hO = (torch.empty((8, m_out), dtype=torch.int32).pin_memory(), torch.empty((8, m_out), dtype=torch.int32).pin_memory(),
+                  torch.empty(m_out, dtype=torch.uint8).pin_memory())
+            if wl == "padd":
+                call = lambda: l.gecc_batch_padd(ctx.h, C.c_size_t(n), vp(hP[0]), vp(hP[1]), vp(hP[2]), vp(hT[0]), vp(hT[1]),
+                                                 vp(hT[2]), vp(hO[0]), vp(hO[1]), vp(hO[2]))
+                h2d, d2h, api = 130 * n, 65 * n, "gecc_batch_padd"
+            else:
+                call = lambda: l.gecc_msm(ctx.h, C.c_size_t(n), vp(hk), vp(hP[0]), vp(hP[1]), vp(hP[2]),
+                                          vp(hO[0]), vp(hO[1]), vp(hO[2]))
+                h2d, d2h, api = 97 * n, 65, "gecc_msm"
+        for _ in range(max(1, args.warmup // 2)):
+            assert call() == 0
+        self.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            assert call() == 0  # synchronous: returns after the D2H copy completed
+        torch.cuda.synchronize()
+        e2e_s = self.max_over_ranks(time.perf_counter() - t0)
+        if wl == "verify":
+            assert int(p_res.sum()) == n
+        elif wl == "sign":   # deterministic nonces: the pipelined host path must reproduce the device path's bytes
+            assert bytes(p_out.numpy()[:4096]) == r["h_sig"][:4096].tobytes() and int(p_st.abs().sum()) == 0
+            assert bytes(p_out.numpy()[-4096:]) == r["h_sig"][-4096:].tobytes()
+        e2e = {"value": (e2e_s / args.steps * 1e3) if wl == "msm" else world * n * args.steps / e2e_s, "unit": UNIT[wl],
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s / args.steps * 1e3,
+               "api": api, "host_buffers": "pinned"}
+
+        # ---- roofline of the dominant kernel
+        counts, slots_per_lane, products_per_lane = work_per_lane(wl, args.curve, log2n)
+        achieved = n * slots_per_lane / per_launch_s
+        io_bytes = IO_BYTES[wl] * n
+        hbm_peak = _measured_peaks().get("hbm_gbs")
+        roofline = {
+            "bound": "imad", "kernel": KERNEL[wl],
+            "achieved": achieved / 1e12, "peak": self.peak_mad_per_s / 1e12, "unit": "T IMAD.WIDE/s",
+            "frac": achieved / self.peak_mad_per_s,
+            "peak_source": "measured live: gecc_microbench(dependent IMAD.WIDE.U32), "
+                           f"{self.peak['ops_per_clk_per_sm']:.1f} per clk per SM (MEASURED_PEAKS.json has no integer peak)",
+            "work_per_unit": {"executed": counts, "imad_wide": slots_per_lane, "imad_wide_per_op": SLOTS,
+                              "source": "tools/op_counts.json (host-sim counted)" if wl in ("verify", "sign")
+                              else "algorithmic count (DESIGN.md section 4)"},
+            "modmul_per_s": n * products_per_lane / per_launch_s,
+            "hbm": {"algorithmic_bytes_per_launch": io_bytes, "achieved_gbs": io_bytes / per_launch_s / 1e9,
+                    "peak_gbs": hbm_peak, "frac": (io_bytes / per_launch_s / 1e9 / hbm_peak) if hbm_peak else None,
+                    "note": "records only" + ("; near the compute / HBM ridge" if wl == "padd" else "; not the bound")},
+            "traffic": _ncu_traffic(wl, log2n) if args.curve == "secp256k1" else None,
+        }
+
+        # ---- CPU baseline on this box's host cores (rank 0, N = 1 only): the compiled reference on a
+        # bounded sample of the SAME inputs, outputs compared with the GPU's
+        cpu = None
+        if with_cpu and rank == 0 and world == 1 and not args.no_cpu_baseline:
+            cpu = self.cpu_baseline(wl, n, log2n, locals())
+        return {"metric": METRIC[wl], "value": value, "unit": UNIT[wl], "ms_per_step": per_launch_s * 1e3,
+                "higher_is_better": wl != "msm", "lanes_per_gpu": n, "clocks": clocks, "e2e": e2e,
+                "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu}
+
+    def cpu_baseline(self, wl, n, log2n, env):
+        np, args = self.np, self.args
+        if wl in ("verify", "sign"):
+            r = env["r"]
+            log2 = args.cpu_sample_log2 or (16 if wl == "verify" else 17)
+            m = min(n, 1 << log2)
+            if wl == "verify":
+                kind, cores, fn = cpu_verify_runner()
+                if kind == "port":
+                    m = min(m, 1 << 12)
+                t0 = time.perf_counter()
+                out = fn(r["h_dig"][:32 * m].tobytes(), r["h_pub"][:65 * m].tobytes(), r["h_sig"][:64 * m].tobytes())
+                dt = time.perf_counter() - t0
+                assert out == b"\x01" * m, "CPU reference rejected GPU-made signatures"
+            else:
+                kind, cores, fn = cpu_sign_runner()
+                if kind == "port":
+                    m = min(m, 1 << 13)
+                t0 = time.perf_counter()
+                out = fn(r["h_dig"][:32 * m].tobytes(), r["h_sec"][:32 * m].tobytes(), 7)
+                dt = time.perf_counter() - t0
+                assert out == r["h_sig"][:64 * m].tobytes(), "CPU reference signatures differ from the GPU's"
+            return {"value": m / dt, "unit": UNIT[wl], "cores": cores, "kind": kind,
+                    "sample": f"first {m} lanes of the timed batch, one call, outputs compared with the GPU's",
+                    "seconds": dt}
+        from oracle import refshim as R
+        if not R.available():
+            return None
+        P, T, hO, k2 = env["P"], env["T"], env["hO"], env["p"]["k2"]
+        m = min(n, 1 << (16 if wl == "padd" else 11))
+        cut = lambda t, w: np.ascontiguousarray(t.cpu().numpy().view(w)[..., :m])
+        cP = (cut(P[0], np.uint32), cut(P[1], np.uint32), cut(P[2], np.uint8))
+        if wl == "padd":   # the reference's batch_padd on all host threads, up to 2^16 pairs, median of 5
+            cT = (cut(T[0], np.uint32), cut(T[1], np.uint32), cut(T[2], np.uint8))
+            dt = R.batch_padd_timed(SECP, cP, cT, lanes=0, workers=0, repeats=5)
+            want = R.batch_padd(SECP, cP, cT, lanes=0, workers=0)
+            got = tuple(np.ascontiguousarray(t.numpy().view(w)[..., :m]) for t, w in zip(hO, (np.uint32, np.uint32, np.uint8)))
+            assert all((a == b).all() for a, b in zip(want, got)), "CPU reference batch_padd differs from the GPU's"
+            return {"value": m / dt, "unit": UNIT[wl], "cores": os.cpu_count(), "kind": "reference",
+                    "sample": f"first {m} pairs of the timed batch, median of 5, ALL outputs compared with the GPU's",
+                    "seconds": dt}
+        # the reference has no MSM: its serial scalar multiplication (pmul_serial) summed, 2^11 terms
+        ck = np.ascontiguousarray(k2.cpu().numpy()[..., :m])
+        t0 = time.perf_counter()
+        R.pmul_serial(SECP, ck, cP)
+        dt = time.perf_counter() - t0
+        return {"value": dt * (n / m) * 1e3, "unit": UNIT[wl], "cores": 1, "kind": "reference",
+                "sample": f"reference pmul_serial over the first {m} terms ({dt:.2f} s), scaled by {n // m} to 2^{log2n} "
+                          "terms; the reference has no MSM, this is the definition it would run",
+                "seconds": dt}
+
+    def close(self):
+        self.ctx.close()
+        if self.dist.is_initialized():
+            self.dist.destroy_process_group()
+
+
+WORKLOAD_TEXT = {"verify": "{c} ECDSA verify, batch 2^{k} per GPU", "sign": "{c} ECDSA sign, batch 2^{k} per GPU",
+                 "padd": "{c} batched affine point addition, 2^{k} pairs per GPU",
+                 "msm": "{c} Pippenger MSM, 2^{k} points per GPU (batch-affine buckets)"}
+# the other legs of BASELINE.json's metric ("ECDSA sign & verify ops/s ...; MSM 2^20 ms") and config 1
+EXTRA_LEGS = [("sign_2^20", "sign", 20), ("msm_2^20", "msm", 20), ("padd_2^16", "padd", 16), ("padd_2^20", "padd", 20)]
 
 
 def main():
@@ -322,303 +642,37 @@ def main():
             raise SystemExit("bench.py: the BLS curves serve --workload msm only")
         bench_msm_bls(args, rank, local_rank, world)
         return
-
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-    import paper_2501_03245_b200 as gecc
-
-    if not torch.cuda.is_available():
-        raise SystemExit("bench.py: no CUDA device; the product has no CPU path "
-                         "(use --impl reference for the CPU arm)")
-    torch.cuda.set_device(local_rank)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    n = 1 << args.log2n
-    lane_base = rank * n
+    arm = GpuArm(args, rank, local_rank, world)
     wl = args.workload
-    ctx = gecc.Context(gecc.SM2 if args.curve == "sm2" else gecc.SECP256K1, local_rank)
-    l = gecc.lib()
-    stream = torch.cuda.Stream()          # all timed work and its events share this stream
-    torch.cuda.set_stream(stream)
-    ctx.set_stream(stream.cuda_stream)
-    vp = lambda t: C.c_void_p(t.data_ptr())
-
-    # ---- synthetic records, generated on the GPU by our own keygen/sign (not timed)
-    u8 = lambda m: torch.empty(m, dtype=torch.uint8, device="cuda")
-    h_sec, h_pub = np.empty(32 * n, np.uint8), np.empty(65 * n, np.uint8)
-    rc = l.gecc_keygen(ctx.h, C.c_uint64(1), C.c_uint64(lane_base), C.c_size_t(n),
-                       C.c_void_p(h_sec.ctypes.data), C.c_void_p(h_pub.ctypes.data))
-    assert rc == 0, ctx.l.gecc_last_error(ctx.h)
-    h_dig = np.frombuffer(np.random.RandomState(1234 + rank).bytes(32 * n), np.uint8).copy()
-    d_dig, d_sec, d_pub = (torch.from_numpy(a).cuda() for a in (h_dig, h_sec, h_pub))
-    d_sig, d_res = u8(64 * n), u8(n)
-    d_st = torch.empty(n, dtype=torch.int32, device="cuda")
-    rc = l.gecc_sign_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_sec), C.c_uint64(7),
-                         C.c_uint64(lane_base), vp(d_sig), vp(d_st))
-    assert rc == 0
-    torch.cuda.synchronize()
-    assert int(d_st.abs().sum()) == 0
-    h_sig = d_sig.cpu().numpy()
-
-    # ---- equivalence gate before timing (bench.cpp:253-256): spot lanes vs the oracle
-    from oracle import coracle as O
-    rs = np.random.RandomState(99)
-    idx = [int(i) for i in rs.choice(n, 24, replace=False)]
-    pick = lambda a, w: b"".join(a[w * i:w * i + w].tobytes() for i in idx)
-    for i in idx[:8]:
-        want = O.ecdsa_sign(SECP, h_dig[32 * i:32 * i + 32].tobytes(), h_sec[32 * i:32 * i + 32].tobytes(),
-                            7, lane_base=lane_base + i)[1]
-        assert want == h_sig[64 * i:64 * i + 64].tobytes(), "sign parity gate failed"
-    bad = bytearray(pick(h_sig, 64))
-    bad[64 * 3 + 9] ^= 4
-    want = O.ecdsa_verify(SECP, pick(h_dig, 32), pick(h_pub, 65), bytes(bad))[1]
-    got = ctx.verify(pick(h_dig, 32), pick(h_pub, 65), bytes(bad))[1]
-    assert want == got and sum(want) == 23, "verify parity gate failed"
-
-    if wl in ("padd", "msm"):
-        k1 = torch.from_numpy(rs.randint(0, 2**32, size=(8, n), dtype=np.uint64).astype(np.uint32)).cuda()
-        k2 = torch.from_numpy(rs.randint(0, 2**32, size=(8, n), dtype=np.uint64).astype(np.uint32)).cuda()
-        col = lambda: torch.empty((8, n), dtype=torch.int32, device="cuda")
-        P = (col(), col(), u8(n)); T = (col(), col(), u8(n)); S = (col(), col(), u8(n))
-        l.gecc_batch_fpmul_dev(ctx.h, C.c_size_t(n), vp(k1), vp(P[0]), vp(P[1]), vp(P[2]))
-        l.gecc_batch_fpmul_dev(ctx.h, C.c_size_t(n), vp(k2), vp(T[0]), vp(T[1]), vp(T[2]))
-        torch.cuda.synchronize()
-
-    # GECC_BENCH_FORCE_EXCHANGE=1 runs the exchange code with a one-rank process group (torchrun
-    # --nproc-per-node 1): the only way to execute it on a single-GPU box
-    msm_exchange = wl == "msm" and (world > 1 or (os.environ.get("GECC_BENCH_FORCE_EXCHANGE") == "1" and "RANK" in os.environ))
-    if msm_exchange and world == 1 and not dist.is_initialized():
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    if msm_exchange:
-        msm_parts = torch.empty(world * 17, dtype=torch.int32, device="cuda")
-        one = lambda: (torch.empty((8, 1), dtype=torch.int32, device="cuda"),
-                       torch.empty((8, 1), dtype=torch.int32, device="cuda"), u8(1))
-        msm_acc, msm_out = one(), one()
-
-    def step_dev():
-        if wl == "verify":
-            return l.gecc_verify_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_pub), vp(d_sig), vp(d_res))
-        if wl == "sign":
-            return l.gecc_sign_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_sec), C.c_uint64(7),
-                                   C.c_uint64(lane_base), vp(d_sig), vp(d_st))
-        if wl == "msm":   # sum_i k2_i * P_i, one point out
-            rc = l.gecc_msm_dev(ctx.h, C.c_size_t(n), vp(k2), vp(P[0]), vp(P[1]), vp(P[2]),
-                                vp(S[0]), vp(S[1]), vp(S[2]))
-            if not msm_exchange or rc != 0:
-                return rc
-            # sharded MSM: every rank summed its own point range; ONE small all_gather of
-            # the partial sums (17 words per rank over NVLink), then world-1 local additions
-            # (EC addition is not an NCCL reduction operator)
-            mine = torch.cat([S[0].view(-1)[:8], S[1].view(-1)[:8], S[2].view(-1)[:1].to(torch.int32)])
-            dist.all_gather_into_tensor(msm_parts, mine)
-            parts = msm_parts.view(world, 17)
-            ax, ay, ai = msm_acc
-            ax.copy_(parts[0, :8].view(8, 1)); ay.copy_(parts[0, 8:16].view(8, 1)); ai.copy_(parts[0, 16:].to(torch.uint8))
-            for r in range(1, world):
-                bx = parts[r, :8].contiguous().view(8, 1)
-                by = parts[r, 8:16].contiguous().view(8, 1)
-                bi = parts[r, 16:].to(torch.uint8)
-                rc = l.gecc_batch_padd_dev(ctx.h, C.c_size_t(1), vp(ax), vp(ay), vp(ai), vp(bx), vp(by), vp(bi),
-                                           vp(msm_out[0]), vp(msm_out[1]), vp(msm_out[2]))
-                if rc != 0:
-                    return rc
-                ax.copy_(msm_out[0]); ay.copy_(msm_out[1]); ai.copy_(msm_out[2])
-            return 0
-        return l.gecc_batch_padd_dev(ctx.h, C.c_size_t(n), vp(P[0]), vp(P[1]), vp(P[2]), vp(T[0]),
-                                     vp(T[1]), vp(T[2]), vp(S[0]), vp(S[1]), vp(S[2]))
-
-    def barrier():
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-            torch.cuda.synchronize()
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    # ---- integer-pipe peak, measured live (rank 0's device is representative)
-    peak = ctx.microbench(1, 3000)  # dependent IMAD.WIDE chain, 8 warps/scheduler
-    peak_mad_per_s = peak["total_ops"] / peak["seconds"]
-
-    # ---- value: device-resident
-    for _ in range(args.warmup):
-        assert step_dev() == 0
-    barrier()
-    sampler = ClockSampler(local_rank)
-    launches0 = ctx.launches
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record(stream)
-    for _ in range(args.steps):
-        assert step_dev() == 0
-    ev1.record(stream)
-    barrier()
-    launches = ctx.launches - launches0
-    dev_s = max_over_ranks(ev0.elapsed_time(ev1) * 1e-3)
-    clocks = sampler.stop()
-    if wl == "verify":
-        assert int(d_res.sum()) == n, "timed verify produced rejects"
-    value = world * n * args.steps / dev_s
-    if wl == "msm":   # time-like metric: ms per 2^log2n-point MSM (per GPU; ranks run their own range)
-        value = dev_s / args.steps * 1e3
-
-    # ---- e2e: reference-facing C ABI, pinned host buffers, copies inside the timed region
-    pin = lambda a: torch.from_numpy(a).pin_memory()
-    e2e = None
-    if wl in ("verify", "sign"):
-        p_dig, p_pub, p_sig, p_sec = pin(h_dig), pin(h_pub), pin(h_sig.copy()), pin(h_sec)
-        p_res = torch.empty(n, dtype=torch.uint8).pin_memory()
-        p_out = torch.empty(64 * n, dtype=torch.uint8).pin_memory()
-        p_st = torch.empty(n, dtype=torch.int32).pin_memory()
-        if wl == "verify":
-            call = lambda: l.sm2b_verify(ctx.h, C.c_size_t(n), vp(p_dig), vp(p_pub), vp(p_sig), vp(p_res))
-            h2d, d2h = 161 * n, n
-        else:
-            call = lambda: l.gecc_sign(ctx.h, C.c_size_t(n), vp(p_dig), vp(p_sec), C.c_uint64(7),
-                                       C.c_uint64(lane_base), vp(p_out), vp(p_st))
-            h2d, d2h = 64 * n, 68 * n
-        for _ in range(max(1, args.warmup // 2)):
-            assert call() == 0
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            assert call() == 0  # synchronous: returns after the D2H copy completed
-        torch.cuda.synchronize()
-        e2e_s = max_over_ranks(time.perf_counter() - t0)
-        if wl == "verify":
-            assert int(p_res.sum()) == n
-        else:   # deterministic nonces: the pipelined host path must reproduce the device path's bytes
-            assert bytes(p_out.numpy()[:4096]) == h_sig[:4096].tobytes() and int(p_st.abs().sum()) == 0
-            assert bytes(p_out.numpy()[-4096:]) == h_sig[-4096:].tobytes()
-        e2e = {"value": world * n * args.steps / e2e_s, "unit": UNIT[wl],
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": e2e_s / args.steps * 1e3,
-               "api": "sm2b_verify" if wl == "verify" else "gecc_sign", "host_buffers": "pinned"}
-
-    if wl in ("padd", "msm"):
-        hP = tuple(pin(np.ascontiguousarray(t.cpu().numpy().view(np.uint32 if i < 2 else np.uint8))) for i, t in enumerate(P))
-        hT = tuple(pin(np.ascontiguousarray(t.cpu().numpy().view(np.uint32 if i < 2 else np.uint8))) for i, t in enumerate(T))
-        hk = pin(k2.cpu().numpy())
-        m_out = n if wl == "padd" else 1
-        hO = (torch.empty((8, m_out), dtype=torch.int32).pin_memory(), torch.empty((8, m_out), dtype=torch.int32).pin_memory(),
-              torch.empty(m_out, dtype=torch.uint8).pin_memory())
-        if wl == "padd":
-            call = lambda: l.gecc_batch_padd(ctx.h, C.c_size_t(n), vp(hP[0]), vp(hP[1]), vp(hP[2]), vp(hT[0]), vp(hT[1]),
-                                             vp(hT[2]), vp(hO[0]), vp(hO[1]), vp(hO[2]))
-            h2d, d2h, api = 130 * n, 65 * n, "gecc_batch_padd"
-        else:
-            call = lambda: l.gecc_msm(ctx.h, C.c_size_t(n), vp(hk), vp(hP[0]), vp(hP[1]), vp(hP[2]),
-                                      vp(hO[0]), vp(hO[1]), vp(hO[2]))
-            h2d, d2h, api = 97 * n, 65, "gecc_msm"
-        for _ in range(max(1, args.warmup // 2)):
-            assert call() == 0
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            assert call() == 0
-        torch.cuda.synchronize()
-        e2e_s = max_over_ranks(time.perf_counter() - t0)
-        e2e = {"value": world * n * args.steps / e2e_s if wl == "padd" else e2e_s / args.steps * 1e3, "unit": UNIT[wl],
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": e2e_s / args.steps * 1e3,
-               "api": api, "host_buffers": "pinned"}
-
-    # ---- roofline of the dominant kernel (the only kernel in the step)
-    per_launch_s = dev_s / args.steps
-    counts, slots_per_lane, products_per_lane = work_per_lane(wl, args.curve)
-    mads = n * slots_per_lane
-    achieved = mads / per_launch_s
-    io_bytes = {"verify": 162, "sign": 132, "padd": 194, "msm": 96}[wl] * n
-    roofline = {
-        "bound": "imad", "kernel": {"verify": "k_verify", "sign": "k_sign", "padd": "k_batch_padd", "msm": "k_msm_tree_fwd/bwd"}[wl],
-        "achieved": achieved / 1e12, "peak": peak_mad_per_s / 1e12, "unit": "T IMAD.WIDE-slot/s",
-        "frac": achieved / peak_mad_per_s,
-        "peak_source": "measured live: gecc_microbench(dependent IMAD.WIDE.U32), "
-                       f"{peak['ops_per_clk_per_sm']:.1f} per clk per SM",
-        "work_per_lane": {"executed": counts, "imad_wide_slots": slots_per_lane,
-                          "slots_per_op": SLOTS, "source": "tools/op_counts.json"},
-        "modmul_per_s": n * products_per_lane / per_launch_s,
-        "hbm": {"algorithmic_bytes_per_launch": io_bytes, "achieved_gbs": io_bytes / per_launch_s / 1e9,
-                "peak_gbs": _measured_peaks().get("hbm_gbs"), "note": "records only; not the bound"},
-        "traffic": _ncu_traffic(wl) if args.curve == "secp256k1" else None,
-    }
-
-    # ---- CPU baseline on this box's host cores (rank 0, N = 1 only)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and wl in ("verify", "sign"):
-        log2 = args.cpu_sample_log2 or (16 if wl == "verify" else 17)
-        m = min(n, 1 << log2)
-        if wl == "verify":
-            kind, cores, fn = cpu_verify_runner()
-            if kind == "port":
-                m = min(m, 1 << 12)
-            t0 = time.perf_counter()
-            out = fn(h_dig[:32 * m].tobytes(), h_pub[:65 * m].tobytes(), h_sig[:64 * m].tobytes())
-            dt = time.perf_counter() - t0
-            assert out == b"\x01" * m, "CPU reference rejected GPU-made signatures"
-        else:
-            kind, cores, fn = cpu_sign_runner()
-            if kind == "port":
-                m = min(m, 1 << 13)
-            t0 = time.perf_counter()
-            out = fn(h_dig[:32 * m].tobytes(), h_sec[:32 * m].tobytes(), 7)
-            dt = time.perf_counter() - t0
-            assert out == h_sig[:64 * m].tobytes(), "CPU reference signatures differ from the GPU's"
-        cpu = {"value": m / dt, "unit": UNIT[wl], "cores": cores, "kind": kind,
-               "sample": f"first {m} lanes of the timed batch, one call, outputs compared with the GPU's",
-               "seconds": dt}
-
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and wl in ("padd", "msm"):
-        from oracle import refshim as R
-        if R.available():
-            m = min(n, 1 << (16 if wl == "padd" else 11))
-            cut = lambda t, w: np.ascontiguousarray(t.cpu().numpy().view(w)[..., :m])
-            cP = (cut(P[0], np.uint32), cut(P[1], np.uint32), cut(P[2], np.uint8))
-            if wl == "padd":   # the reference's batch_padd on all host threads, 2^16 pairs, median of 5
-                cT = (cut(T[0], np.uint32), cut(T[1], np.uint32), cut(T[2], np.uint8))
-                dt = R.batch_padd_timed(SECP, cP, cT, lanes=0, workers=0, repeats=5)
-                want = R.batch_padd(SECP, cP, cT, lanes=0, workers=0)
-                got = (cut(S[0], np.uint32), cut(S[1], np.uint32), cut(S[2], np.uint8)) if e2e is None else \
-                    tuple(np.ascontiguousarray(t.numpy().view(w)[..., :m]) for t, w in zip(hO, (np.uint32, np.uint32, np.uint8)))
-                assert all((a == b).all() for a, b in zip(want, got)), "CPU reference batch_padd differs from the GPU's"
-                cpu = {"value": m / dt, "unit": UNIT[wl], "cores": os.cpu_count(), "kind": "reference",
-                       "sample": f"first {m} pairs of the timed batch, median of 5, outputs compared with the GPU's",
-                       "seconds": dt}
-            else:   # the reference has no MSM: its serial scalar multiplication (pmul_serial) summed, 2^11 terms
-                ck = np.ascontiguousarray(k2.cpu().numpy()[..., :m])
-                t0 = time.perf_counter()
-                R.pmul_serial(SECP, ck, cP)
-                dt = time.perf_counter() - t0
-                cpu = {"value": dt * (n / m) * 1e3, "unit": UNIT[wl], "cores": 1, "kind": "reference",
-                       "sample": f"reference pmul_serial over the first {m} terms ({dt:.2f} s), scaled by {n // m} to 2^{args.log2n} "
-                                 "terms; the reference has no MSM, this is the definition it would run",
-                       "seconds": dt}
-
+    leg = arm.run(wl, args.log2n)
+    extra = None
+    if wl == "verify" and args.log2n == 20 and not args.no_extra:
+        extra = {}
+        for name, w, k in EXTRA_LEGS:
+            e = arm.run(w, k)
+            e["config"] = {"workload": WORKLOAD_TEXT[w].format(c=args.curve, k=k)}
+            extra[name] = e
     if rank == 0:
         line = {
-            "metric": METRIC[wl], "value": value, "unit": UNIT[wl], "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_launch_s * 1e3,
-            "higher_is_better": wl != "msm", "scaling": "weak", "vs_baseline": None,
+            "metric": leg["metric"], "value": leg["value"], "unit": leg["unit"], "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": leg["ms_per_step"],
+            "higher_is_better": leg["higher_is_better"], "scaling": "weak", "vs_baseline": None,
             "dtype": "u32 limbs (256-bit modular integer)", "data": "synthetic",
-            "config": {"workload": {"verify": f"{args.curve} ECDSA verify, batch 2^{args.log2n} per GPU",
-                                    "sign": f"{args.curve} ECDSA sign, batch 2^{args.log2n} per GPU",
-                                    "padd": f"{args.curve} batched affine point addition, 2^{args.log2n} pairs per GPU",
-                                    "msm": f"{args.curve} Pippenger MSM, 2^{args.log2n} points per GPU (c = 16, batch-affine buckets)"}[wl],
-                       "curve": args.curve, "lanes_per_gpu": n,
-                       "sharding": (f"point ranges x{world}, one all_gather of the partial sums + {world - 1} local additions"
+            "config": {"workload": WORKLOAD_TEXT[wl].format(c=args.curve, k=args.log2n),
+                       "curve": args.curve, "lanes_per_gpu": 1 << args.log2n,
+                       "sharding": (f"point ranges x{world}, one ncclAllGather of the partial sums + {world - 1} local additions (in the library)"
                                     if wl == "msm" and world > 1 else f"lane ranges x{world}, no collective"),
                        "l2": "inputs larger than L2 (records 161 B/lane x 2^20 = 169 MB > 126 MB)"
-                       if wl == "verify" and args.log2n >= 20 else "no L2 flush; kernel is IMAD-bound, records read once"},
-            "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
-            "cpu_baseline": cpu,
+                       if wl == "verify" and args.log2n >= 20 else "no L2 flush; kernel is IMAD-bound, records read once",
+                       "parity": "secp256k1 ECDSA: pinned to reference kernels + restated protocol glue + Python ints; "
+                                 "MSM: definition only (the reference has none)"},
+            "clocks": leg["clocks"], "e2e": leg["e2e"], "gpu_launches": leg["gpu_launches"],
+            "roofline": leg["roofline"], "cpu_baseline": leg["cpu_baseline"],
         }
+        if extra is not None:
+            line["extra"] = extra
         print(json.dumps(line), flush=True)
-    ctx.close()
-    if dist.is_initialized():
-        dist.destroy_process_group()
+    arm.close()
 
 
 def bench_msm_bls(args, rank, local_rank, world):
@@ -715,7 +769,7 @@ def bench_msm_bls(args, rank, local_rank, world):
     per = dev_s / args.steps
     counts = msm_products_per_point("generic12")
     # 12-limb Montgomery product: 144 (product) + 144 (word-serial rows m_i * q) wide multiplies + 12 m_i
-    slots = {"mul_generic12": 144 + 144 + 12 * 0.5, "sqr_generic12": 78 + 144 + 12 * 0.5}
+    slots = {"mul_generic12": 144 + 144, "sqr_generic12": 78 + 144}   # IMAD.WIDE only
     mads = n * sum(slots[kk] * v for kk, v in counts.items())
     if rank == 0:
         print(json.dumps({
@@ -735,24 +789,25 @@ def bench_msm_bls(args, rank, local_rank, world):
         dist.destroy_process_group()
 
 
-def _ncu_traffic(wl):
+def _ncu_traffic(wl, log2n=20):
     """dram__bytes_read.sum + dram__bytes_write.sum of the dominant kernel, per launch, from the
-    committed `ncu --set full` capture of this same command (profiles/, tools/ncu_summary.py).
-    For k_verify it is well above the 170 MB of records: the excess is per-thread stack
-    (2 KB x 2^20 lanes of local memory written back from L1), not re-reads of the inputs."""
+    committed `ncu --set full` capture of this round's kernels (profiles/r02_*, tools/ncu_summary.py);
+    None when this round has no capture for the leg (stale captures are not quoted)."""
     import csv
-    name, kernel = {"verify": ("r01m_verify", "k_verify_gtab"), "padd": ("r01_padd", "k_batch_padd"),
-                    "msm": ("r01g_msm_tree", "k_msm_tree_bwd")}.get(wl, (None, None))  # msm: the level-0 unwind kernel
+    name, kernel = {"verify": ("r02_verify", "k_verify"), "sign": ("r02_sign", "k_sign"),
+                    "padd": ("r02_padd" + ("16" if log2n <= 16 else ""), "k_"),
+                    "msm": ("r02_msm", "k_msm")}.get(wl, (None, None))
     if not name:
         return None
     try:
-        tot = 0.0
+        tot, names = 0.0, set()
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         with open(os.path.join(ROOT, "profiles", name + "_metrics.csv")) as f:
             for r in csv.reader(f):
                 if len(r) >= 4 and kernel in r[0] and r[1] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                     tot += float(r[3]) * scale.get(r[2], 1)
-        return {"bytes_per_launch": tot, "kernel": kernel, "source": f"profiles/{name}_metrics.csv"} if tot else None
+                    names.add(r[0])
+        return {"bytes_per_launch": tot, "kernels": sorted(names), "source": f"profiles/{name}_metrics.csv"} if tot else None
     except OSError:
         return None
 

@@ -72,3 +72,48 @@ def test_product_never_imports_the_oracle():
                 txt = open(os.path.join(dirpath, fn), errors="ignore").read()
                 assert "import oracle" not in txt and "from oracle" not in txt, fn
                 assert "gecc_oracle" not in txt and "libgecc_ref" not in txt, fn
+
+
+def test_sm2batch_h_is_a_drop_in(tmp_path):
+    """include/sm2batch.h: a C consumer of the reference's header name compiles against it and
+    sees the reference's enum values and struct layouts (sm2batch.h:27-36,51-56,89-96)."""
+    import subprocess
+    src = tmp_path / "use.c"
+    src.write_text(r'''
+#include <stddef.h>
+#include <stdio.h>
+#include <sm2batch.h>
+int main(void) {
+    sm2b_bench_report r;
+    sm2b_op_counts c;
+    sm2b_status (*verify)(sm2b_ctx*, size_t, const uint8_t*, const uint8_t*, const uint8_t*, uint8_t*) = sm2b_verify;
+    sm2b_status (*sign)(sm2b_ctx*, size_t, const uint8_t*, const uint8_t*, uint64_t, uint8_t*, int32_t*) = sm2b_sign;
+    sm2b_status (*keygen)(sm2b_ctx*, uint64_t, size_t, uint8_t*, uint8_t*) = sm2b_keygen;
+    sm2b_status (*ecdh)(sm2b_ctx*, size_t, const uint8_t*, const uint8_t*, uint8_t*, int32_t*) = sm2b_ecdh;
+    sm2b_ctx* (*mk)(uint32_t, uint32_t) = sm2b_ctx_new;
+    (void)verify; (void)sign; (void)keygen; (void)ecdh; (void)mk; (void)r; (void)c;
+    printf("%d %d %d %d %d %d %d %d\n", SM2B_OK, SM2B_ERROR_INVALID_ARGUMENT, SM2B_ERROR_MALFORMED_INPUT,
+           SM2B_ERROR_INVALID_PEER, SM2B_ERROR_DEGENERATE, SM2B_ERROR_NONCE_EXHAUSTED, SM2B_ERROR_NO_CROSSOVER,
+           SM2B_ERROR_INTERNAL);
+    printf("%zu %zu %zu %zu %zu\n", sizeof(sm2b_op_counts), offsetof(sm2b_op_counts, modinv), sizeof(sm2b_bench_report),
+           offsetof(sm2b_bench_report, ops), offsetof(sm2b_bench_report, equivalence_checked));
+    printf("%s\n", sm2b_version());
+    return 0;
+}
+''')
+    exe = tmp_path / "use"
+    lib = os.path.join(ROOT, "paper_2501_03245_b200", "lib")
+    subprocess.check_call(["gcc", "-std=c11", "-Wall", "-Werror", "-I" + os.path.join(ROOT, "include"), str(src), "-o", str(exe),
+                           "-L" + lib, "-lgecc_b200", "-Wl,-rpath," + lib])
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
+    assert out[0] == "0 1 2 3 4 5 6 7"
+    assert out[1] == "32 24 72 24 64"     # u64 x4; {u64, double, double, 4 x u64, u64, int + pad}
+    assert out[2] == "1.0.0"
+    # where the reference lies beside us: the same translation unit against ITS header and library
+    ref_inc = "/root/reference/proj/include"
+    ref_lib = os.path.join(ROOT, "oracle", "_ref")
+    if os.path.exists(os.path.join(ref_inc, "sm2batch.h")) and os.path.exists(os.path.join(ref_lib, "libgecc_ref.so")):
+        exe2 = tmp_path / "use_ref"
+        subprocess.check_call(["gcc", "-std=c11", "-Wall", "-Werror", "-I" + ref_inc, str(src), "-o", str(exe2),
+                               "-L" + ref_lib, "-lgecc_ref", "-Wl,-rpath," + ref_lib])
+        assert subprocess.run([str(exe2)], capture_output=True, text=True, check=True).stdout.split("\n") == out
