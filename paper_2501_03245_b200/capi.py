@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libgecc_b200.so")
+# GECC_LIB selects an experiment build of the same library (csrc/Makefile VARIANT=...), for A/B timing
+LIB_PATH = os.environ.get("GECC_LIB") or os.path.join(HERE, "lib", "libgecc_b200.so")
 
 SM2, SECP256K1, BLS12_381, BLS12_377 = 0, 1, 2, 3
 FIELD_P, FIELD_N = 0, 1

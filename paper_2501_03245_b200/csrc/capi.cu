@@ -790,7 +790,7 @@ sm2b_status points_locked(sm2b_ctx* ctx, int op, size_t n, const uint32_t* k, co
         case OP_PADD:
             CU(ctx, ctx->batch_tmp.ensure(batch_padd_scratch_bytes(n)));
             CU(ctx, launch_batch_padd(ctx->curve, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, ctx->stream,
-                                      ctx->batch_tmp.p));
+                                      ctx->batch_tmp.p, BatchAux{ctx->aux_stream, ctx->ev_fork, ctx->ev_join}));
             break;
         case OP_PDBL:
             CU(ctx, launch_batch_pdbl(ctx->curve, n, px, py, pinf, ox, oy, oinf, ctx->stream));

@@ -3,6 +3,7 @@
 // chord / tangent finish (batch_point.cpp:124-170) and the block-level Montgomery
 // trick (warp-shuffle scans + shared memory, one inversion per thread block).
 #pragma once
+#include <type_traits>
 #include "gecc_curve.cuh"
 #include "gecc_dev.cuh"
 #include "gecc_modinv.cuh"
@@ -10,6 +11,40 @@
 namespace gecc {
 
 enum : uint32_t { K_GENERIC = 0, K_TANGENT, K_INFINITY, K_COPY_LEFT, K_COPY_RIGHT };
+
+// secp256k1 column buffers hold Montgomery representatives x~ = x R (the reference's I/O contract),
+// but R = 2^256 = c (mod p) is tiny, so the affine formulas can run on the PLAIN weakly reduced
+// field directly on the representatives, without ever converting:
+//   lambda   = (y1~ - y2~) / (x1~ - x2~)            the factors R cancel: the plain slope
+//   x3~      = c lambda^2 - x1~ - x2~                 one multiplication by c = 2^32 + 977 (a fold)
+//   y3~      = lambda (x1~ - x3~) - y1~               already scaled
+//   tangent  : lambda = 3 (x~^2 R^-1) / (2 y~)        one more product, on doubling lanes only
+// Montgomery's trick runs on the plain denominators d~ (their plain inverses are what lambda
+// needs).  Products cost 72 wide multiplies with a shallow fold instead of the word-serial
+// Montgomery reduction, additions fold a carry instead of compare-and-select; results are made
+// canonical when they are stored.
+struct SecpMLCurve : SecpLCurve {
+    static constexpr bool mont_reps = true;
+    GECC_HD static constexpr uint32_t rinv(int i) {  // (2^256)^-1 mod p
+        constexpr uint32_t t[8] = {0x0868192Au, 0xD838091Du, 0xDC24A059u, 0xBCB223FEu, 0x95F2B761u, 0x9C46C2C2u, 0x15538399u, 0xC9BD1905u};
+        return t[i];
+    }
+};
+template <class C, class = void>
+struct curve_mont_reps : std::false_type {};
+template <class C>
+struct curve_mont_reps<C, std::void_t<decltype(C::mont_reps)>> : std::bool_constant<C::mont_reps> {};
+
+// a * 2^256 mod p = a * c, weakly reduced: the product fold applied to (a : 0)
+__device__ __forceinline__ fe lazy_times_r(const fe& a) {
+    uint32_t t[16];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        t[i] = 0;
+        t[8 + i] = a.w[i];
+    }
+    return redc_secp_lazy(t);
+}
 
 // classification + denominator of one pair (batch_point.cpp:91-111)
 template <class C>
@@ -34,13 +69,25 @@ template <class C>
 __device__ __forceinline__ void finish_lambda(const cfe<C>& lam, const cfe<C>& x1, const cfe<C>& x2,
                                               const cfe<C>& y1, cfe<C>* xr, cfe<C>* yr) {
     const typename C::Fp f{};
-    *xr = fe_sub(f, fe_sub(f, fe_sqr(f, lam), x1), x2);
-    *yr = fe_sub(f, fe_mul(f, lam, fe_sub(f, x1, *xr)), y1);
+    if constexpr (curve_mont_reps<C>::value) {
+        cfe<C> x3 = fe_sub(f, fe_sub(f, lazy_times_r(fe_sqr(f, lam)), x1), x2);
+        *yr = lazy_canon(f, fe_sub(f, fe_mul(f, lam, fe_sub(f, x1, x3)), y1));
+        *xr = lazy_canon(f, x3);
+    } else {
+        *xr = fe_sub(f, fe_sub(f, fe_sqr(f, lam), x1), x2);
+        *yr = fe_sub(f, fe_mul(f, lam, fe_sub(f, x1, *xr)), y1);
+    }
 }
 template <class C>
 __device__ __forceinline__ cfe<C> tangent_numerator(const cfe<C>& x) {  // 3x^2 + a
     const typename C::Fp f{};
     cfe<C> x2 = fe_sqr(f, x);
+    if constexpr (curve_mont_reps<C>::value) {  // x~^2 R^-1 = x^2 R
+        cfe<C> ri;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ri.w[i] = C::rinv(i);
+        x2 = fe_mul(f, x2, ri);
+    }
     cfe<C> num = fe_add(f, fe_dbl(f, x2), x2);
     if (C::a_kind == A_ZERO) return num;
     return fe_add(f, num, curve_a<C>());

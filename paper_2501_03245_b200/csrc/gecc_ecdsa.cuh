@@ -139,11 +139,13 @@ struct GTable {
 // k * G for any 256-bit k (the value of k mod n times G, like the reference's
 // bit ladder on an unreduced scalar, acceptance.cpp:288-291).
 template <class C, int WG>
-GECC_HD jac fixed_base_mul(const fe& k_raw, const GTable<WG>& tab) {
+GECC_HD jac fixed_base_mul(const fe& k_raw, const GTable<WG>& tab, const jac* start = nullptr) {
     const typename C::Fp f{};
     fe k = scalar_reduce_once<typename C::Fn>(k_raw);
     Recoded<WG> rc = recode_signed<WG>(k);
-    jac acc = jac_infinity<C>();
+    // `start`: the additions continue into an existing accumulator (start + k G): the verify
+    // lane adds u1 G onto u2 Q this way, which saves the separate complete addition at the end
+    jac acc = start ? *start : jac_infinity<C>();
 #pragma unroll 1
     for (int j = 0; j <= 256 / WG; ++j) {
         int d = j == 256 / WG ? (int)rc.carry : recoded_digit<WG>(rc, j);
@@ -685,10 +687,9 @@ GECC_HD uint8_t verify_lane(const uint8_t* digest32, const uint8_t* pub65, const
     fe w_m = fe_to_mont(fn, safegcd_inverse(fn, s));                   // s^-1 (Montgomery form)
     fe u1 = fe_mul(fn, e, w_m);                                        // e * w, plain
     fe u2 = fe_mul(fn, r, w_m);
-    jac A = fixed_base_mul<C, WG>(u1, gt);
     build_lane_table<C>(Q, qt);
     jac B = var_base_mul<C>(u2, qt);
-    jac R = jac_add<C>(A, B);
+    jac R = fixed_base_mul<C, WG>(u1, gt, &B);   // u2 Q + u1 G: mixed additions are complete
     if (jac_is_inf<C>(R)) return 0;
     // x(R) mod n == r  <=>  X == r Z^2  or  (r + n < p and X == (r + n) Z^2)
     fe zz = fe_sqr(fp, R.Z);

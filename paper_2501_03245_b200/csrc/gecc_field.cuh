@@ -744,6 +744,29 @@ GECC_HD fel<F> fe_sqr_inl(const F& f, const fel<F>& a) {
 // keeps it inside the instruction caches (round-1 ncu: with everything inlined the
 // top stall of k_verify was no_instruction).  Runtime fields stay inline.
 #if defined(__CUDA_ARCH__) && !defined(GECC_INLINE_FIELD)
+#if defined(GECC_PRODUCTS_BY_REF)
+// experiment: operands and result through local memory (LSU pipe) instead of register moves
+template <class F>
+__device__ __noinline__ void fe_mul_ref(fel<F>* r, const fel<F>* a, const fel<F>* b) {
+    *r = fe_mul_inl(F{}, *a, *b);
+}
+template <class F>
+__device__ __noinline__ void fe_sqr_ref(fel<F>* r, const fel<F>* a) {
+    *r = fe_sqr_inl(F{}, *a);
+}
+template <class F>
+__device__ __forceinline__ fel<F> fe_mul_call(const fel<F>& a, const fel<F>& b) {
+    fel<F> r;
+    fe_mul_ref<F>(&r, &a, &b);
+    return r;
+}
+template <class F>
+__device__ __forceinline__ fel<F> fe_sqr_call(const fel<F>& a) {
+    fel<F> r;
+    fe_sqr_ref<F>(&r, &a);
+    return r;
+}
+#else
 template <class F>
 __device__ __noinline__ fel<F> fe_mul_call(fel<F> a, fel<F> b) {
     return fe_mul_inl(F{}, a, b);
@@ -752,6 +775,7 @@ template <class F>
 __device__ __noinline__ fel<F> fe_sqr_call(fel<F> a) {
     return fe_sqr_inl(F{}, a);
 }
+#endif
 template <class F>
 GECC_HD fel<F> fe_mul(const F& f, const fel<F>& a, const fel<F>& b) {
     if constexpr (std::is_empty<F>::value) return fe_mul_call<F>(a, b);

@@ -69,10 +69,15 @@ void set_batch_form(int form);
 cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* in, uint32_t* out,
                                 cudaStream_t s);
 cudaError_t launch_batch_invert_secp_lazy(size_t n, const uint32_t* in, uint32_t* out, cudaStream_t s);
+// optional second stream + two events: large batches run as two overlapping halves when given
+struct BatchAux {
+    cudaStream_t stream = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
 cudaError_t launch_batch_padd(int curve, size_t n, const uint32_t* px, const uint32_t* py,
                               const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty,
                               const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
-                              cudaStream_t s, void* scratch = nullptr);
+                              cudaStream_t s, void* scratch = nullptr, BatchAux aux = BatchAux());
 // scratch of the tiled batch_padd form (tile totals); without it the single-launch forms run
 size_t batch_padd_scratch_bytes(size_t n);
 cudaError_t launch_batch_pdbl(int curve, size_t n, const uint32_t* px, const uint32_t* py,

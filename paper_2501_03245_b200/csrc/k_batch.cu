@@ -402,6 +402,145 @@ k_padd_bwd(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict
     }
 }
 
+// ---------------------------------------------------------------- fused form (three launches, recompute)
+// The tiled form above parks every prefix product in the output buffer (64 B written and 64 B read
+// back per pair) and re-reads both x coordinates a third time.  Here the forward launch keeps
+// nothing but the tile total and each thread's "product of all other totals"; the backward launch
+// RECOMPUTES the thread's K prefix products (one more product per pair instead of 128 B of HBM
+// traffic), holds them in shared memory (word-interleaved by thread: conflict-free), and unwinds.
+//   fwd : 1 + 14/K products per pair, reads x1, x2 (64 B per pair)
+//   bwd : 1 + 1/K + 2 + 3 products per pair, reads x1, x2 (L2), y1, y2, writes x3, y3, flag
+// HBM traffic ~ 257 B per pair against 385 B for the tiled form.  Elements [begin, end) of column
+// buffers with row pitch n: large batches run as two halves on two streams, so that the inversion
+// of one half's tile totals (one warp, pure latency) hides behind the other half's launches.
+template <int NL>
+__device__ __forceinline__ void prefetch_cols(const uint32_t* __restrict__ cols, size_t n, size_t i) {
+#pragma unroll
+    for (int k = 0; k < NL; ++k) asm volatile("prefetch.global.L1 [%0];" ::"l"(cols + (size_t)k * n + i));
+}
+
+template <class C>
+__device__ __forceinline__ cfe<C> padd_denominator(size_t n, size_t i, const uint32_t* __restrict__ px,
+                                                   const uint32_t* __restrict__ py, const uint8_t* __restrict__ pinf,
+                                                   const uint32_t* __restrict__ tx, const uint32_t* __restrict__ ty,
+                                                   const uint8_t* __restrict__ tinf) {
+    using fe = cfe<C>;
+    constexpr int NL = C::Fp::N;
+    const typename C::Fp f{};
+    fe ax = col_load<NL>(px, n, i), bx = col_load<NL>(tx, n, i);
+    const bool ai = pinf && pinf[i], bi = tinf && tinf[i];
+    fe d = fe_one(f);
+    if (!ai && !bi && fe_eq(ax, bx)) {  // y is only needed when the x's collide
+        fe ay = col_load<NL>(py, n, i), by = col_load<NL>(ty, n, i);
+        classify_pair<C>(ax, ay, ai, bx, by, bi, &d);
+    } else if (!ai && !bi) {
+        d = fe_sub(f, ax, bx);
+    }
+    return d;
+}
+
+template <class C, int K, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+k_padd_fused_fwd(size_t n, size_t begin, size_t end, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
+                 const uint8_t* __restrict__ pinf, const uint32_t* __restrict__ tx, const uint32_t* __restrict__ ty,
+                 const uint8_t* __restrict__ tinf, uint32_t* __restrict__ totals, uint32_t* __restrict__ others,
+                 size_t tiles) {
+    using fe = cfe<C>;
+    constexpr int NL = C::Fp::N;
+    __shared__ uint32_t sm[2 * NL * (THREADS / 32)];
+    const typename C::Fp f{};
+    const size_t first = begin + (size_t)blockIdx.x * (THREADS * K) + threadIdx.x;
+    fe acc = fe_one(f);
+    if (first < end) acc = padd_denominator<C>(n, first, px, py, pinf, tx, ty, tinf);
+#pragma unroll 1
+    for (int k = 1; k < K; ++k) {
+        const size_t i = first + (size_t)k * THREADS;
+        if (i + THREADS < end) {  // the next pair's lines are requested before this pair's product
+            prefetch_cols<NL>(px, n, i + THREADS);
+            prefetch_cols<NL>(tx, n, i + THREADS);
+        }
+        if (i < end) acc = fe_mul(f, acc, padd_denominator<C>(n, i, px, py, pinf, tx, ty, tinf));
+    }
+    fe total;
+    fe oth = block_others_product<decltype(f), THREADS>(f, acc, sm, &total);
+    col_store(others, tiles * THREADS, (size_t)blockIdx.x * THREADS + threadIdx.x, oth);
+    if (threadIdx.x == 0) col_store(totals, tiles, blockIdx.x, total);
+}
+
+template <class C, int K, int THREADS, int MINB>
+__global__ void __launch_bounds__(THREADS, MINB)
+k_padd_fused_bwd(size_t n, size_t begin, size_t end, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
+                 const uint8_t* __restrict__ pinf, const uint32_t* __restrict__ tx, const uint32_t* __restrict__ ty,
+                 const uint8_t* __restrict__ tinf, uint32_t* __restrict__ ox, uint32_t* __restrict__ oy,
+                 uint8_t* __restrict__ oinf, const uint32_t* __restrict__ total_inv,
+                 const uint32_t* __restrict__ others, size_t tiles) {
+    using fe = cfe<C>;
+    constexpr int NL = C::Fp::N;
+    extern __shared__ uint32_t pre[];  // prefix products 0 .. K-2: word (k * NL + w) of thread t at [(k * NL + w) * THREADS + t]
+    const typename C::Fp f{};
+    const size_t first = begin + (size_t)blockIdx.x * (THREADS * K) + threadIdx.x;
+    if (first >= end) return;
+    fe inv = fe_mul(f, col_load<NL>(total_inv, tiles, blockIdx.x),
+                    col_load<NL>(others, tiles * THREADS, (size_t)blockIdx.x * THREADS + threadIdx.x));
+    int last = K - 1;
+    while (first + (size_t)last * THREADS >= end) --last;
+    {   // recompute the prefix products of this thread's denominators
+        fe acc = padd_denominator<C>(n, first, px, py, pinf, tx, ty, tinf);
+#pragma unroll 1
+        for (int k = 0; k < last; ++k) {
+            if (k + 2 <= last) {
+                prefetch_cols<NL>(px, n, first + (size_t)(k + 2) * THREADS);
+                prefetch_cols<NL>(tx, n, first + (size_t)(k + 2) * THREADS);
+            } else {  // the unwind starts at the last pair: its y coordinates come from HBM
+                prefetch_cols<NL>(py, n, first + (size_t)last * THREADS);
+                prefetch_cols<NL>(ty, n, first + (size_t)last * THREADS);
+            }
+#pragma unroll
+            for (int w = 0; w < NL; ++w) pre[(size_t)(k * NL + w) * THREADS + threadIdx.x] = acc.w[w];
+            acc = fe_mul(f, acc, padd_denominator<C>(n, first + (size_t)(k + 1) * THREADS, px, py, pinf, tx, ty, tinf));
+        }
+    }
+#pragma unroll 1
+    for (int k = last; k >= 0; --k) {
+        const size_t i = first + (size_t)k * THREADS;
+        if (k > 0) {
+            prefetch_cols<NL>(py, n, i - THREADS);
+            prefetch_cols<NL>(ty, n, i - THREADS);
+        }
+        fe ax = col_load<NL>(px, n, i), ay = col_load<NL>(py, n, i);
+        fe bx = col_load<NL>(tx, n, i), by = col_load<NL>(ty, n, i);
+        const bool ai = pinf && pinf[i], bi = tinf && tinf[i];
+        fe d = fe_one(f);
+        const uint32_t kind = classify_pair<C>(ax, ay, ai, bx, by, bi, &d);
+        fe dinv = inv;
+        if (k > 0) {
+            fe prev;
+#pragma unroll
+            for (int w = 0; w < NL; ++w) prev.w[w] = pre[(size_t)((k - 1) * NL + w) * THREADS + threadIdx.x];
+            dinv = fe_mul(f, inv, prev);
+            inv = fe_mul(f, inv, d);
+        }
+        fe xr = fe_zero_n<NL>(), yr = fe_zero_n<NL>();
+        uint8_t rinf = 0;
+        if (kind == K_GENERIC) {
+            fe lam = fe_mul(f, fe_sub(f, ay, by), dinv);
+            finish_lambda<C>(lam, ax, bx, ay, &xr, &yr);
+        } else if (kind == K_TANGENT) {
+            fe lam = fe_mul(f, tangent_numerator<C>(ax), dinv);
+            finish_lambda<C>(lam, ax, ax, ay, &xr, &yr);
+        } else if (kind == K_COPY_LEFT) {
+            xr = ax; yr = ay;
+        } else if (kind == K_COPY_RIGHT) {
+            xr = bx; yr = by;
+        } else {
+            rinf = 1;
+        }
+        col_store(ox, n, i, xr);
+        col_store(oy, n, i, yr);
+        oinf[i] = rinf;
+    }
+}
+
 // Form selection: the cooperative kernels while 16-element chunks would leave the chip
 // under-filled, the chunked kernels beyond.  gecc_set_batch_form pins one form (tests, sweeps):
 // 0 auto, 1 chunked (16 per thread), 2 cooperative 256 threads, 3 chunked at 6 blocks per SM,
@@ -414,12 +553,29 @@ static int pick_form(size_t n, bool tiled_ok = false) {
     if (g_batch_form >= 6) return tiled_ok ? g_batch_form : (n <= g_coop_max_n ? 4 : 1);
     if (g_batch_form) return g_batch_form;
     // measured on B200 (profiles/r01f_sweep.json): cooperative/128 wins up to 2^18 pairs
-    // (0.054 ms vs 0.083 ms), chunked and tiled are within 7 % of each other beyond
-    return n <= g_coop_max_n ? 4 : 1;
+    // (0.054 ms vs 0.083 ms); beyond, the fused three-launch form (batch_padd with scratch only)
+    if (n <= g_coop_max_n) return 4;
+    return tiled_ok ? 8 : 1;
 }
-size_t batch_padd_scratch_bytes(size_t n) {  // tile totals and their inverses (K = 4 is the larger)
+// fused form: K pairs per thread, FUSED_THREADS threads per tile
+#ifndef GECC_FUSED_THREADS
+#define GECC_FUSED_THREADS 128
+#endif
+#ifndef GECC_FUSED_MINB
+#define GECC_FUSED_MINB 4
+#endif
+constexpr int FUSED_THREADS = GECC_FUSED_THREADS;
+constexpr int FUSED_MINB = GECC_FUSED_MINB;
+static size_t fused_tiles(size_t n, int K) { return (n + (size_t)FUSED_THREADS * K - 1) / ((size_t)FUSED_THREADS * K); }
+// tile totals, their inverses (tiled / fused forms) and the per-thread "others" products (fused)
+size_t batch_padd_scratch_bytes(size_t n) {
     const size_t tiles = (n + (size_t)TILED_THREADS * 4 - 1) / ((size_t)TILED_THREADS * 4);
-    return 2 * tiles * 32 + 512;
+    // fused form: two sets (the two halves) of totals | inverses | others; K = 8 has the most tiles
+    const size_t half_tiles = fused_tiles(n, 8) / 2 + 2;
+    const size_t tot_words = (half_tiles * 8 + 63) & ~(size_t)63;
+    const size_t fused = 2 * (2 * tot_words + half_tiles * FUSED_THREADS * 8) * 4;
+    const size_t tiled = 2 * tiles * 32 + 512;
+    return (fused > tiled ? fused : tiled) + 1024;
 }
 static int coop_threads(int form) { return form == 2 ? 256 : form == 4 ? 128 : form == 5 ? 32 : 0; }
 static unsigned coop_blocks(size_t n, int threads) {
@@ -495,10 +651,65 @@ cudaError_t launch_batch_invert_secp_lazy(size_t n, const uint32_t* in, uint32_t
     return cudaGetLastError();
 }
 
+// one range [begin, end) of the fused form on stream s
+template <class C, int K>
+static cudaError_t fused_range(int curve, size_t n, size_t begin, size_t end, const uint32_t* px, const uint32_t* py,
+                               const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty, const uint8_t* tinf,
+                               uint32_t* ox, uint32_t* oy, uint8_t* oinf, uint32_t* totals, uint32_t* total_inv,
+                               uint32_t* others, cudaStream_t s) {
+    const size_t m = end - begin;
+    const size_t tiles = fused_tiles(m, K);
+    const size_t smem = (size_t)(K - 1) * 8 * FUSED_THREADS * sizeof(uint32_t);
+    if (smem > 48 * 1024)  // per device: set on every launch (a context may be one of several devices')
+        cudaFuncSetAttribute(k_padd_fused_bwd<C, K, FUSED_THREADS, FUSED_MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_padd_fused_fwd<C, K, FUSED_THREADS><<<(unsigned)tiles, FUSED_THREADS, 0, s>>>(n, begin, end, px, py, pinf, tx, ty, tinf,
+                                                                                  totals, others, tiles);
+    // tile totals: plain residues on the lazy secp256k1 field, Montgomery form otherwise
+    if (cudaError_t e = curve_mont_reps<C>::value ? launch_batch_invert_secp_lazy(tiles, totals, total_inv, s)
+                                                  : launch_batch_invert(curve, 0, tiles, totals, total_inv, s))
+        return e;
+    k_padd_fused_bwd<C, K, FUSED_THREADS, FUSED_MINB><<<(unsigned)tiles, FUSED_THREADS, smem, s>>>(
+        n, begin, end, px, py, pinf, tx, ty, tinf, ox, oy, oinf, total_inv, others, tiles);
+    return cudaGetLastError();
+}
+
+template <class C, int K>
+static cudaError_t fused_padd(int curve, size_t n, const uint32_t* px, const uint32_t* py, const uint8_t* pinf,
+                              const uint32_t* tx, const uint32_t* ty, const uint8_t* tinf, uint32_t* ox, uint32_t* oy,
+                              uint8_t* oinf, void* scratch, cudaStream_t s, const BatchAux& aux) {
+    // scratch: two sets (one per half) of totals | total_inv | others
+    const size_t half_tiles = fused_tiles(n, K) / 2 + 2;
+    const size_t tot_words = (half_tiles * 8 + 63) & ~(size_t)63;
+    const size_t oth_words = half_tiles * FUSED_THREADS * 8;
+    uint32_t* base = (uint32_t*)scratch;
+    uint32_t* set0 = base;
+    uint32_t* set1 = base + 2 * tot_words + oth_words;
+    const bool split = aux.stream && aux.fork && aux.join && n >= ((size_t)1 << 18);
+    if (!split) {  // one range: the whole scratch is one set, sized by the full tile count
+        const size_t all_words = (fused_tiles(n, K) * 8 + 63) & ~(size_t)63;
+        return fused_range<C, K>(curve, n, 0, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, base, base + all_words,
+                                 base + 2 * all_words, s);
+    }
+    // two halves on two streams: each half is fwd -> invert -> bwd; the inversion of one half (a
+    // single warp's latency) overlaps the other half's launches
+    const size_t mid = (n / 2 + (size_t)FUSED_THREADS * K - 1) / ((size_t)FUSED_THREADS * K) * ((size_t)FUSED_THREADS * K);
+    cudaError_t e = cudaEventRecord(aux.fork, s);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(aux.stream, aux.fork, 0);
+    if (e == cudaSuccess)
+        e = fused_range<C, K>(curve, n, 0, mid, px, py, pinf, tx, ty, tinf, ox, oy, oinf, set0, set0 + tot_words,
+                              set0 + 2 * tot_words, s);
+    if (e == cudaSuccess)
+        e = fused_range<C, K>(curve, n, mid, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, set1, set1 + tot_words,
+                              set1 + 2 * tot_words, aux.stream);
+    if (e == cudaSuccess) e = cudaEventRecord(aux.join, aux.stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(s, aux.join, 0);
+    return e;
+}
+
 cudaError_t launch_batch_padd(int curve, size_t n, const uint32_t* px, const uint32_t* py,
                               const uint8_t* pinf, const uint32_t* tx, const uint32_t* ty,
                               const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
-                              cudaStream_t s, void* scratch) {
+                              cudaStream_t s, void* scratch, BatchAux aux) {
     if (n == 0) return cudaSuccess;
     if (curve == CURVE_BLS381) {
         k_batch_padd_coop<Bls381Curve, 128><<<coop_blocks(n, 128), 128, 0, s>>>(n, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
@@ -509,6 +720,14 @@ cudaError_t launch_batch_padd(int curve, size_t n, const uint32_t* px, const uin
         return cudaGetLastError();
     }
     const int form = pick_form(n, scratch != nullptr);
+    if (form >= 8) {  // fused: 8 = eight pairs per thread, 9 = sixteen
+        if (curve == CURVE_SECP) {
+            if (form == 8) return fused_padd<SecpMLCurve, 8>(curve, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, scratch, s, aux);
+            return fused_padd<SecpMLCurve, 16>(curve, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, scratch, s, aux);
+        }
+        if (form == 8) return fused_padd<Sm2Curve, 8>(curve, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, scratch, s, aux);
+        return fused_padd<Sm2Curve, 16>(curve, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, scratch, s, aux);
+    }
     if (form >= 6) {
         const int K = form == 6 ? 8 : 4;
         const size_t tiles = (n + (size_t)TILED_THREADS * K - 1) / ((size_t)TILED_THREADS * K);

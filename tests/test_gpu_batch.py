@@ -24,7 +24,7 @@ def ctxs():
         x.close()
 
 
-@pytest.fixture(params=["chunked", "coop", "coop32", "tiled8", "tiled4"])
+@pytest.fixture(params=["chunked", "coop", "coop32", "tiled8", "tiled4", "fused", "fused2"])
 def form(request):
     """Both forms of the batch kernels (one inversion per thread / one per block) must agree
     with the reference bit for bit (results are grouping-invariant, batch_invert.hpp:59-60)."""
