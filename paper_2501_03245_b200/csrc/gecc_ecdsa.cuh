@@ -19,6 +19,11 @@
 #include "gecc_dev.cuh"
 #include "gecc_modinv.cuh"
 
+// lanes signed by one thread of k_sign (they share one inversion mod p and one mod n)
+#ifndef GECC_SIGN_K
+#define GECC_SIGN_K 8
+#endif
+
 namespace gecc {
 
 // ------------------------------------------------------------ scalars
@@ -116,6 +121,17 @@ struct GTable {
     const uint32_t* tab;
     static constexpr int windows = 256 / WG + 1;
     static constexpr int per_window = 1 << (WG - 1);
+    // requests the 64-byte row (j, d) ahead of its use: the rows are gathered at random from a
+    // table that lives in L2, one per window, and each gather otherwise sits in the dependency chain
+    GECC_HD void prefetch(int j, int d) const {
+#if defined(__CUDA_ARCH__)
+        const uint32_t* p = tab + ((size_t)j * per_window + (size_t)(d - 1)) * 16;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(p + 8));
+#else
+        (void)j; (void)d;
+#endif
+    }
     GECC_HD aff load(int j, int d) const {  // d >= 1
         const uint32_t* p = tab + ((size_t)j * per_window + (size_t)(d - 1)) * 16;
         aff r;
@@ -146,9 +162,14 @@ GECC_HD jac fixed_base_mul(const fe& k_raw, const GTable<WG>& tab, const jac* st
     // `start`: the additions continue into an existing accumulator (start + k G): the verify
     // lane adds u1 G onto u2 Q this way, which saves the separate complete addition at the end
     jac acc = start ? *start : jac_infinity<C>();
+    auto digit = [&](int j) { return j == 256 / WG ? (int)rc.carry : recoded_digit<WG>(rc, j); };
 #pragma unroll 1
     for (int j = 0; j <= 256 / WG; ++j) {
-        int d = j == 256 / WG ? (int)rc.carry : recoded_digit<WG>(rc, j);
+        if (j < 256 / WG) {  // the next window's row is on its way while this window's addition runs
+            const int dn = digit(j + 1);
+            if (dn != 0) tab.prefetch(j + 1, dn < 0 ? -dn : dn);
+        }
+        int d = digit(j);
         if (d == 0) continue;
         aff t = tab.load(j, d < 0 ? -d : d);
         if (d < 0) t.y = fe_neg(f, t.y);
@@ -575,7 +596,8 @@ enum { LANE_OK = 0, LANE_NONCE_EXHAUSTED = 5 };  // sm2b_status values
 // One signing attempt with the nonce k (0 < k < n), e_m and d_m in Montgomery form mod n
 // (the body of the retry loop, protocol.cpp:133-160).  False when r == 0 or s == 0.
 template <class C, int WG, bool UNIFORM = false>
-GECC_HD bool sign_attempt(const fe& e_m, const fe& d_m, const fe& k, const GTable<WG>& gt, uint8_t* sig64) {
+GECC_HD bool sign_attempt(const fe& e_m, const fe& d_m, const fe& k, const GTable<WG>& gt, uint8_t* sig64,
+                          bool aligned = false) {
     const typename C::Fp fp{};
     const typename C::Fn fn{};
     jac R = fixed_base_mul_mode<C, WG, UNIFORM>(k, gt);
@@ -589,8 +611,8 @@ GECC_HD bool sign_attempt(const fe& e_m, const fe& d_m, const fe& k, const GTabl
     fe s_m = fe_mul(fn, kinv_m, fe_add(fn, e_m, fe_mul(fn, r_m, d_m)));
     fe s = fe_from_mont(fn, s_m);
     if (fe_is_zero(s)) return false;
-    be32_store(sig64, r);
-    be32_store(sig64 + 32, s);
+    be32_store_a(sig64, r, aligned);
+    be32_store_a(sig64 + 32, s, aligned);
     return true;
 }
 
@@ -630,7 +652,7 @@ GECC_HD int sign_lane_nonce(const fe& e, const fe& d, const fe& k, const GTable<
 // reference's per-lane retry sequence exactly.
 template <class C, int WG, int K, bool UNIFORM = false>
 GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream0,
-                        const GTable<WG>& gt, uint8_t* sig64, int* status) {
+                        const GTable<WG>& gt, uint8_t* sig64, int* status, bool aligned = false) {
     const typename C::Fp fp{};
     const typename C::Fn fn{};
     fe X[K], Z[K], km[K], pz[K], pk[K];
@@ -667,8 +689,8 @@ GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream
             status[j] = sign_lane<C, WG, UNIFORM>(e[j], d[j], seed, stream0 + j, gt, out, 1);
             continue;
         }
-        be32_store(out, r);
-        be32_store(out + 32, s);
+        be32_store_a(out, r, aligned);
+        be32_store_a(out + 32, s, aligned);
         status[j] = LANE_OK;
     }
 }

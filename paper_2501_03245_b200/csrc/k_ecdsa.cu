@@ -45,7 +45,7 @@ k_verify_gtab(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restri
 // flags[0] is set when any secret is zero or >= n: the whole call is malformed
 // (capi.cpp:181-184) and the host discards the outputs.  Each thread signs SIGN_K
 // consecutive lanes and shares the two inversions among them (sign_lanes).
-constexpr int SIGN_K = 4;
+constexpr int SIGN_K = GECC_SIGN_K;  // gecc_ecdsa.cuh: measured 4 / 8 / 16 lanes per thread = 2.87 / 2.76 / 3.09 ms per 2^20
 
 template <class C, bool UNIFORM>
 __global__ void __launch_bounds__(SIGN_THREADS)
@@ -57,15 +57,17 @@ k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ se
     GTable<GECC_WG> gt{gtab};
     fe e[SIGN_K], d[SIGN_K];
     bool all_ok = i0 + SIGN_K <= n;
+    // 32- and 64-byte records on 16-byte boundaries: vector loads / stores (uniform over the launch)
+    const bool al_in = ptr_aligned16(dig) && ptr_aligned16(sec), al_out = ptr_aligned16(sig);
 #pragma unroll 1
     for (int j = 0; j < SIGN_K && i0 + j < n; ++j) {
-        d[j] = be32_load(sec + 32 * (i0 + j));
-        e[j] = scalar_reduce_once<typename C::Fn>(be32_load(dig + 32 * (i0 + j)));
+        d[j] = be32_load_a(sec + 32 * (i0 + j), al_in);
+        e[j] = scalar_reduce_once<typename C::Fn>(be32_load_a(dig + 32 * (i0 + j), al_in));
         if (!scalar_in_range<typename C::Fn>(d[j])) all_ok = false;
     }
     if (all_ok) {
         int st[SIGN_K];
-        sign_lanes<C, GECC_WG, SIGN_K, UNIFORM>(e, d, seed, lane_base + i0, gt, sig + 64 * i0, st);
+        sign_lanes<C, GECC_WG, SIGN_K, UNIFORM>(e, d, seed, lane_base + i0, gt, sig + 64 * i0, st, al_out);
 #pragma unroll
         for (int j = 0; j < SIGN_K; ++j) status[i0 + j] = st[j];
         return;

@@ -205,7 +205,7 @@ template <class C>
 int sign_t(size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed, uint64_t base,
            uint8_t* sig, int32_t* st) {
     GTable<HS_WG> gt{host_gtable<C>().data()};
-    constexpr int K = 4;  // same grouping as k_sign: shared inversions inside a group
+    constexpr int K = GECC_SIGN_K;  // same grouping as k_sign: shared inversions inside a group
     size_t i = 0;
     for (; i + K <= n; i += K) {
         fe e[K], d[K];
