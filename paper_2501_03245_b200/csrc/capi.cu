@@ -1274,7 +1274,7 @@ namespace {
 sm2b_status msm_args(const sm2b_ctx* ctx, size_t n, const void* scalars, const void* px, const void* py,
                      const void* ox, const void* oy, const void* oinf) {
     if (!ctx || !ox || !oy || !oinf || (n > 0 && (!scalars || !px || !py))) return SM2B_ERROR_INVALID_ARGUMENT;
-    if (n >= ((size_t)1 << 31)) return SM2B_ERROR_INVALID_ARGUMENT;  // point index is 31 bits
+    if (n >= ((size_t)1 << 27)) return SM2B_ERROR_INVALID_ARGUMENT;  // 17 n pair positions are 32-bit, the point index 31
     return SM2B_OK;
 }
 }  // namespace

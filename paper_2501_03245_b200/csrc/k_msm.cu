@@ -26,8 +26,6 @@
 // Bucket ids: window w, magnitude m = 1..2^15  ->  w * 2^15 + (m - 1).
 #include <type_traits>
 
-#include <cub/device/device_radix_sort.cuh>
-
 #include "gecc_batch.cuh"
 #include "gecc_ecdsa.cuh"
 #include "gecc_host.h"
@@ -42,37 +40,160 @@ constexpr int MSM_BUCKETS = 1 << (MSM_C - 1);      // 32768 per window
 constexpr uint32_t MSM_NB = MSM_WINDOWS * MSM_BUCKETS;
 constexpr uint32_t MSM_KEY_NONE = 0xFFFFFu;        // sorts behind every real bucket (20-bit keys)
 
+// The (bucket, point | sign) pair of scalar i in window w; key == MSM_KEY_NONE when the digit is zero.
+template <class C>
+struct MsmDigits {
+    Recoded<MSM_C> rc;
+    bool flip, skip;
+    uint32_t index;
+    __device__ __forceinline__ MsmDigits(size_t n, size_t i, const uint32_t* __restrict__ scalars,
+                                         const uint8_t* __restrict__ pinf) {
+        // any 256-bit scalar is accepted: below 2n for the 256-bit curves (one subtraction), below
+        // 3r for BLS12-381's 255-bit group order (two), below 14r for BLS12-377's 253-bit one (13)
+        constexpr uint32_t top = C::Fn::q(7);
+        constexpr int subs = top >= 0x80000000u ? 1 : (int)(0xFFFFFFFFu / top);
+        fe k = col_load<8>(scalars, n, i);
+#pragma unroll 1
+        for (int it = 0; it < subs; ++it) k = scalar_reduce_once<typename C::Fn>(k);
+        skip = pinf && pinf[i];
+        // k >= 2^255: use (n - k) * (-P).  A carry window would otherwise collect ~n/2 points in
+        // ONE bucket (a single thread adding half a million points).
+        flip = (k.w[7] >> 31) != 0;
+        if (flip) k = u256_sub(fe_modulus(typename C::Fn{}), k);
+        rc = recode_signed<MSM_C>(k);  // k < 2^255: rc.carry is 1 only for 0x7FFF8... tops
+        index = (uint32_t)i;
+    }
+    __device__ __forceinline__ void pair(int w, uint32_t* key, uint32_t* val) const {
+        const int d = w == MSM_WINDOWS - 1 ? (int)rc.carry : recoded_digit<MSM_C>(rc, w);
+        *key = MSM_KEY_NONE;
+        *val = 0;
+        if (d != 0 && !skip) {
+            const uint32_t mag = (uint32_t)(d < 0 ? -d : d);
+            *key = (uint32_t)w * MSM_BUCKETS + (mag - 1);
+            *val = index | (((d < 0) != flip) ? 0x80000000u : 0u);
+        }
+    }
+};
+
 template <class C>
 __global__ void __launch_bounds__(256)
 k_msm_digits(size_t n, const uint32_t* __restrict__ scalars, const uint8_t* __restrict__ pinf,
              uint32_t* __restrict__ keys, uint32_t* __restrict__ vals) {
     const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
-    // any 256-bit scalar is accepted: below 2n for the 256-bit curves (one subtraction), below
-    // 3r for BLS12-381's 255-bit group order (two), below 14r for BLS12-377's 253-bit one (13)
-    constexpr uint32_t top = C::Fn::q(7);
-    constexpr int subs = top >= 0x80000000u ? 1 : (int)(0xFFFFFFFFu / top);
-    fe k = col_load<8>(scalars, n, i);
-#pragma unroll 1
-    for (int it = 0; it < subs; ++it) k = scalar_reduce_once<typename C::Fn>(k);
-    const bool skip = pinf && pinf[i];
-    // k >= 2^255: use (n - k) * (-P).  A carry window would otherwise collect ~n/2 points in
-    // ONE bucket (a single thread adding half a million points).
-    const bool flip = (k.w[7] >> 31) != 0;
-    if (flip) k = u256_sub(fe_modulus(typename C::Fn{}), k);
-    Recoded<MSM_C> rc = recode_signed<MSM_C>(k);  // k < 2^255: rc.carry is 1 only for 0x7FFF8... tops
+    const MsmDigits<C> dg(n, i, scalars, pinf);
 #pragma unroll
     for (int w = 0; w < MSM_WINDOWS; ++w) {
-        int d = w == MSM_WINDOWS - 1 ? (int)rc.carry : recoded_digit<MSM_C>(rc, w);
-        uint32_t key = MSM_KEY_NONE, val = 0;
-        if (d != 0 && !skip) {
-            const uint32_t mag = (uint32_t)(d < 0 ? -d : d);
-            key = (uint32_t)w * MSM_BUCKETS + (mag - 1);
-            val = (uint32_t)i | (((d < 0) != flip) ? 0x80000000u : 0u);
-        }
+        uint32_t key, val;
+        dg.pair(w, &key, &val);
         keys[(size_t)w * n + i] = key;   // window-major: coalesced writes
         vals[(size_t)w * n + i] = val;
     }
+}
+
+// ---------------------------------------------------------------- bucket sort (counting sort)
+// The pairs have to be grouped by bucket; nothing else about their order matters (a bucket's sum
+// does not depend on the order of its points).  Keys are w * 2^15 + m - 1 < 17 * 2^15, so this is
+// a counting sort over 557 056 counters -- no general radix sort is needed:
+//   k_msm_hist    : recodes every scalar and counts its 17 buckets (atomics on L2-resident words);
+//   k_msm_scan_*  : the counts become first positions (`starts`, 0xFFFFFFFF for an empty bucket --
+//                   the array the bucket reduction reads) and scatter cursors; the unused tail of
+//                   the pair arrays is marked;
+//   k_msm_scatter : recodes again (cheaper than parking 142 MB of unsorted pairs) and writes every
+//                   pair at cursor[bucket]++.  Threads walk window by window, so at any time the
+//                   scattered writes fall into one window's 8 MB of the output and merge in L2.
+template <class C>
+__global__ void __launch_bounds__(256)
+k_msm_hist(size_t n, const uint32_t* __restrict__ scalars, const uint8_t* __restrict__ pinf,
+           uint32_t* __restrict__ counts) {
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const MsmDigits<C> dg(n, i, scalars, pinf);
+#pragma unroll
+    for (int w = 0; w < MSM_WINDOWS; ++w) {
+        uint32_t key, val;
+        dg.pair(w, &key, &val);
+        if (key != MSM_KEY_NONE) atomicAdd(counts + key, 1u);
+    }
+}
+
+// exclusive scan of the 557 056 counts in three small launches: per-block scans (coalesced, one
+// counter per thread), a scan of the 544 block totals, and the pass that adds the block offsets
+constexpr int MSM_SCAN_THREADS = 1024;
+constexpr unsigned MSM_SCAN_BLOCKS = (MSM_NB + MSM_SCAN_THREADS - 1) / MSM_SCAN_THREADS;
+static_assert(MSM_SCAN_BLOCKS <= MSM_SCAN_THREADS, "the block totals are scanned by one block");
+
+// inclusive scan of v over the block; returns this thread's inclusive value, *total = block sum
+__device__ __forceinline__ uint32_t block_scan_inclusive(uint32_t v, uint32_t* sh, uint32_t* total) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, inc, d);
+        if (lane >= (uint32_t)d) inc += o;
+    }
+    if (lane == 31) sh[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t ws = sh[lane];
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t o = __shfl_up_sync(0xFFFFFFFFu, ws, d);
+            if (lane >= (uint32_t)d) ws += o;
+        }
+        sh[lane] = ws;
+    }
+    __syncthreads();
+    *total = sh[31];
+    return inc + (warp ? sh[warp - 1] : 0u);
+}
+__global__ void __launch_bounds__(MSM_SCAN_THREADS)
+k_msm_scan_blocks(const uint32_t* __restrict__ counts, uint32_t* __restrict__ local, uint32_t* __restrict__ block_totals) {
+    __shared__ uint32_t sh[32];
+    const uint32_t b = blockIdx.x * MSM_SCAN_THREADS + threadIdx.x;
+    const uint32_t c = b < MSM_NB ? counts[b] : 0u;
+    uint32_t total;
+    const uint32_t inc = block_scan_inclusive(c, sh, &total);
+    if (b < MSM_NB) local[b] = inc - c;  // exclusive, local to the block
+    if (threadIdx.x == 0) block_totals[blockIdx.x] = total;
+}
+__global__ void __launch_bounds__(MSM_SCAN_THREADS)
+k_msm_scan_tops(uint32_t* __restrict__ block_totals, uint32_t* __restrict__ keys_sorted, size_t pairs) {
+    __shared__ uint32_t sh[32];
+    const uint32_t t = threadIdx.x;
+    const uint32_t c = t < MSM_SCAN_BLOCKS ? block_totals[t] : 0u;
+    uint32_t total;
+    const uint32_t inc = block_scan_inclusive(c, sh, &total);
+    if (t < MSM_SCAN_BLOCKS) block_totals[t] = inc - c;  // exclusive block offsets
+    // positions behind the last pair hold "no bucket" (zero digits, points at infinity)
+    for (size_t p = (size_t)total + t; p < pairs; p += MSM_SCAN_THREADS) keys_sorted[p] = MSM_KEY_NONE;
+}
+__global__ void __launch_bounds__(MSM_SCAN_THREADS)
+k_msm_scan_finish(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ block_totals,
+                  uint32_t* __restrict__ starts /* in: local prefixes */, uint32_t* __restrict__ cursor) {
+    const uint32_t b = blockIdx.x * MSM_SCAN_THREADS + threadIdx.x;
+    if (b >= MSM_NB) return;
+    const uint32_t at = starts[b] + block_totals[blockIdx.x];
+    cursor[b] = at;
+    starts[b] = counts[b] ? at : 0xFFFFFFFFu;  // first position of the bucket's run; none for an empty bucket
+}
+
+template <class C>
+__global__ void __launch_bounds__(256)
+k_msm_scatter(size_t n, const uint32_t* __restrict__ scalars, const uint8_t* __restrict__ pinf,
+              uint32_t* __restrict__ cursor, uint32_t* __restrict__ keys_sorted, uint32_t* __restrict__ vals_sorted) {
+    // block b serves window b / blocks_per_window: the grid runs through the windows in order
+    const unsigned bpw = (unsigned)((n + 255) / 256);
+    const int w = (int)(blockIdx.x / bpw);
+    const size_t i = (size_t)(blockIdx.x % bpw) * 256 + threadIdx.x;
+    if (i >= n) return;
+    const MsmDigits<C> dg(n, i, scalars, pinf);
+    uint32_t key, val;
+    dg.pair(w, &key, &val);
+    if (key == MSM_KEY_NONE) return;
+    const uint32_t pos = atomicAdd(cursor + key, 1u);
+    keys_sorted[pos] = key;
+    vals_sorted[pos] = val;
 }
 
 // first position whose key is >= bucket (sorted keys)
@@ -295,15 +416,6 @@ k_msm_aos(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict_
     if (i >= n) return;
     fe_store_u4<N, false>(rec + (N / 2) * i, msm_to_internal<CE, CI>(col_load<N>(px, n, i)));
     fe_store_u4<N, false>(rec + (N / 2) * i + N / 4, msm_to_internal<CE, CI>(col_load<N>(py, n, i)));
-}
-
-// first position of every bucket's run in the sorted keys (0xFFFFFFFF: empty bucket; memset)
-__global__ void __launch_bounds__(256)
-k_msm_starts(size_t m, const uint32_t* __restrict__ keys, uint32_t* __restrict__ starts) {
-    const size_t p = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-    if (p >= m) return;
-    const uint32_t k = keys[p];
-    if (k < MSM_NB && (p == 0 || keys[p - 1] != k)) starts[k] = (uint32_t)p;
 }
 
 // One join (see above).  LEVEL0: the operands are input points fetched through vals.
@@ -950,12 +1062,10 @@ static MsmPlan msm_plan(size_t n, int limbs) {
     MsmPlan p{};
     const size_t jb = (size_t)12 * limbs, rb = (size_t)8 * limbs, fb = (size_t)4 * limbs;  // bytes: Jacobian point, record, element
     p.pairs = n * MSM_WINDOWS;
-    cub::DeviceRadixSort::SortPairs(nullptr, p.sort_temp, (const uint32_t*)nullptr, (uint32_t*)nullptr,
-                                    (const uint32_t*)nullptr, (uint32_t*)nullptr, (int64_t)p.pairs, 0, 20);
+    p.sort_temp = (size_t)2 * 4 * MSM_NB + 4 * 1024;  // bucket counts | scatter cursors | block totals of the scan
     size_t at = 0;
     auto take = [&](size_t bytes) { size_t o = at; at += align256(bytes); return o; };
-    p.off_keys = take(4 * p.pairs);
-    p.off_vals = take(4 * p.pairs);
+    p.off_keys = p.off_vals = 0;  // unsorted pairs are never stored (the counting sort recodes)
     p.off_keys2 = take(4 * p.pairs);
     p.off_vals2 = take(4 * p.pairs);
     p.slices = (p.pairs + MSM_SLICE - 1) / MSM_SLICE;
@@ -964,6 +1074,7 @@ static MsmPlan msm_plan(size_t n, int limbs) {
     p.off_marg = take(jb * MSM_WINDOWS * 3 * 32);
     p.off_wsum = take(jb * MSM_WINDOWS * 4);
     p.off_temp = take(p.sort_temp);
+    p.off_starts = take((size_t)4 * MSM_NB);
     // the two accumulation forms never run in the same call: their scratch overlaps
     const size_t fork = at;
     p.off_edge = take(jb * 2 * p.slices);
@@ -973,7 +1084,6 @@ static MsmPlan msm_plan(size_t n, int limbs) {
     p.off_rec = take(rb * n);
     p.off_slots = take(rb * p.pairs);
     p.off_sinf = take(p.pairs);
-    p.off_starts = take((size_t)4 * MSM_NB);
     const size_t joins0 = (p.pairs + 1) / 2;
     p.off_pref = take(fb * joins0);
     p.max_tiles = (joins0 + (size_t)MSM_TREE_THREADS * MSM_TREE_KMIN - 1) / ((size_t)MSM_TREE_THREADS * MSM_TREE_KMIN);
@@ -1052,22 +1162,27 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
     uint32_t *keys2 = (uint32_t*)(base + p.off_keys2), *vals2 = (uint32_t*)(base + p.off_vals2);
     uint32_t *buckets = (uint32_t*)(base + p.off_buckets), *parts = (uint32_t*)(base + p.off_parts);
     uint32_t *marg = (uint32_t*)(base + p.off_marg), *wsum = (uint32_t*)(base + p.off_wsum);
-    k_msm_digits<C><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, scalars, pinf, keys, vals);
-    size_t temp = p.sort_temp;
-    cudaError_t e = cub::DeviceRadixSort::SortPairs(base + p.off_temp, temp, keys, keys2, vals, vals2,
-                                                    (int64_t)p.pairs, 0, 20, s);
+    (void)keys; (void)vals;  // the unsorted pairs are never stored: the scatter pass recodes
+    uint32_t* counts = (uint32_t*)(base + p.off_temp);
+    uint32_t* cursor = counts + MSM_NB;
+    uint32_t* starts = (uint32_t*)(base + p.off_starts);
+    cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)4 * MSM_NB, s);
     if (e != cudaSuccess) return e;
+    const unsigned bpw = (unsigned)((n + 255) / 256);
+    k_msm_hist<C><<<bpw, 256, 0, s>>>(n, scalars, pinf, counts);
+    uint32_t* block_totals = cursor + MSM_NB;
+    k_msm_scan_blocks<<<MSM_SCAN_BLOCKS, MSM_SCAN_THREADS, 0, s>>>(counts, starts, block_totals);
+    k_msm_scan_tops<<<1, MSM_SCAN_THREADS, 0, s>>>(block_totals, keys2, p.pairs);
+    k_msm_scan_finish<<<MSM_SCAN_BLOCKS, MSM_SCAN_THREADS, 0, s>>>(counts, block_totals, starts, cursor);
+    k_msm_scatter<C><<<bpw * MSM_WINDOWS, 256, 0, s>>>(n, scalars, pinf, cursor, keys2, vals2);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // digits and sort need the scalars (and the infinity mask) only: a host caller uploads the
     // points meanwhile and hands over the event that says they have arrived
     if (points_ready && (e = cudaStreamWaitEvent(s, points_ready, 0)) != cudaSuccess) return e;
     if (msm_affine()) {
         uint4 *rec = (uint4*)(base + p.off_rec), *slots = (uint4*)(base + p.off_slots);
         uint8_t* sinf = base + p.off_sinf;
-        uint32_t* starts = (uint32_t*)(base + p.off_starts);
         const size_t m = p.pairs;
-        e = cudaMemsetAsync(starts, 0xFF, (size_t)4 * MSM_NB, s);
-        if (e != cudaSuccess) return e;
-        k_msm_starts<<<(unsigned)((m + 255) / 256), 256, 0, s>>>(m, keys2, starts);
         k_msm_aos<C, CI><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, px, py, rec);
         // K joins per thread; thin levels take fewer per thread so that the chip stays filled
         const bool split = g_msm_form != 3;
@@ -1092,7 +1207,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
         k_msm_red_fold<CI><<<(MSM_WINDOWS * 3 * 32 * 32 + 127) / 128, 128, 0, s>>>(parts, marg);
         k_msm_red_weighted<CI><<<(MSM_WINDOWS * 3 * 32 + 127) / 128, 128, 0, s>>>(marg, wsum);
         k_msm_red_combine<CI, C><<<1, MSM_COMBINE_THREADS, 0, s>>>(wsum, ox, oy, oinf);
-        *launches = 3 + (split ? 3 : 1) * MSM_TREE_LEVELS + 4 + 4;  // + the sort's passes
+        *launches = 6 + (split ? 3 : 1) * MSM_TREE_LEVELS * (split ? 2 : 1) + 4;  // sort (5) + records + tree + reduction
         return cudaGetLastError();
     } else {
         uint32_t *edge = (uint32_t*)(base + p.off_edge), *edge_key = (uint32_t*)(base + p.off_edge_key);
@@ -1101,13 +1216,13 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
         const unsigned sb = (unsigned)((p.slices + 127) / 128);
         k_msm_buckets<C><<<sb, 128, 0, s>>>(n, p.pairs, keys2, vals2, px, py, buckets, edge, edge_key, p.slices);
         k_msm_bucket_edges<C><<<sb, 128, 0, s>>>(buckets, edge, edge_key, p.slices);
-        *launches = 3;
+        *launches = 5 + 2;
     }
     k_msm_marginal_parts<C><<<(MSM_WINDOWS * 3 * 1024 + 127) / 128, 128, 0, s>>>(buckets, parts);
     k_msm_marginal_fold<C><<<(MSM_WINDOWS * 3 * 32 + 127) / 128, 128, 0, s>>>(parts, marg);
     k_msm_weighted<C><<<1, 128, 0, s>>>(marg, wsum);
     k_msm_combine<C><<<1, 32, 0, s>>>(wsum, ox, oy, oinf);
-    *launches += 4 + 4;  // reduction + the sort's passes (approximate; CUB picks the pass count)
+    *launches += 4;  // reduction
     return cudaGetLastError();
 }
 
