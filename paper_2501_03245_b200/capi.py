@@ -72,6 +72,11 @@ def lib():
         l.gecc_set_batch_form.restype = None
         l.gecc_set_msm_form.argtypes = [C.c_int]
         l.gecc_set_msm_form.restype = None
+        # A/B timing knobs (tools/, bench.py): pin a kernel form for the whole process
+        if os.environ.get("GECC_MSM_FORM"):
+            l.gecc_set_msm_form(int(os.environ["GECC_MSM_FORM"]))
+        if os.environ.get("GECC_BATCH_FORM"):
+            l.gecc_set_batch_form(int(os.environ["GECC_BATCH_FORM"]))
         _lib = l
     return _lib
 

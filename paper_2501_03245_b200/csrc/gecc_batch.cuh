@@ -147,7 +147,7 @@ __device__ fel<F> coop_block_inverse(const F& f, const fel<F>& t, uint32_t* sm) 
         fe total;
 #pragma unroll
         for (int i = 0; i < NL; ++i) total.w[i] = __shfl_sync(0xFFFFFFFFu, P.w[i], 31);
-        return fe_mul(f, fe_mul(f, fe_inv(f, total), E), S);
+        return fe_mul(f, fe_mul(f, fe_inv_var(f, total), E), S);  // warp-uniform public value
     }
     if (lane == 31) {
 #pragma unroll
@@ -165,7 +165,7 @@ __device__ fel<F> coop_block_inverse(const F& f, const fel<F>& t, uint32_t* sm) 
         fe total;
 #pragma unroll
         for (int i = 0; i < NL; ++i) total.w[i] = __shfl_sync(0xFFFFFFFFu, PP.w[i], NW - 1);
-        const fe inv = fe_inv(f, total);  // the block's single inversion
+        const fe inv = fe_inv_var(f, total);  // the block's single inversion (warp-uniform, public)
         fe EE = fe_select(lane == 0, one, fe_shfl_up(PP, 1));
         fe SS = fe_select(lane == 31, one, fe_shfl_down(QQ, 1));
         fe wi = fe_mul(f, fe_mul(f, inv, EE), SS);

@@ -744,7 +744,63 @@ GECC_HD fel<F> fe_sqr_inl(const F& f, const fel<F>& a) {
 // keeps it inside the instruction caches (round-1 ncu: with everything inlined the
 // top stall of k_verify was no_instruction).  Runtime fields stay inline.
 #if defined(__CUDA_ARCH__) && !defined(GECC_INLINE_FIELD)
-#if defined(GECC_PRODUCTS_BY_REF)
+#if defined(GECC_PRODUCTS_SMEM)
+// experiment: operands and result travel through per-thread shared-memory slots (16-byte granules,
+// granule g of thread t at [g * 256 + t]: conflict-free LDS.128 / STS.128) instead of the register
+// ABI -- no argument / result register moves around the call.  1-D blocks of <= 256 threads, N = 8.
+template <class F>
+__device__ __forceinline__ uint4* product_slots() {
+    __shared__ uint4 slots[6 * 256];
+    return slots + threadIdx.x;
+}
+__device__ __forceinline__ void slot_store(uint4* s, int g, const uint32_t* w) {
+    s[g * 256] = make_uint4(w[0], w[1], w[2], w[3]);
+    s[(g + 1) * 256] = make_uint4(w[4], w[5], w[6], w[7]);
+}
+__device__ __forceinline__ void slot_load(const uint4* s, int g, uint32_t* w) {
+    const uint4 a = s[g * 256], b = s[(g + 1) * 256];
+    w[0] = a.x; w[1] = a.y; w[2] = a.z; w[3] = a.w;
+    w[4] = b.x; w[5] = b.y; w[6] = b.z; w[7] = b.w;
+}
+template <class F>
+__device__ __noinline__ void fe_mul_smem() {
+    uint4* s = product_slots<F>();
+    fel<F> a, b;
+    slot_load(s, 0, a.w);
+    slot_load(s, 2, b.w);
+    const fel<F> r = fe_mul_inl(F{}, a, b);
+    slot_store(s, 4, r.w);
+}
+template <class F>
+__device__ __noinline__ void fe_sqr_smem() {
+    uint4* s = product_slots<F>();
+    fel<F> a;
+    slot_load(s, 0, a.w);
+    const fel<F> r = fe_sqr_inl(F{}, a);
+    slot_store(s, 4, r.w);
+}
+template <class F>
+__device__ __forceinline__ fel<F> fe_mul_call(const fel<F>& a, const fel<F>& b) {
+    if constexpr (F::N != 8) return fe_mul_inl(F{}, a, b);
+    uint4* s = product_slots<F>();
+    slot_store(s, 0, a.w);
+    slot_store(s, 2, b.w);
+    fe_mul_smem<F>();
+    fel<F> r;
+    slot_load(s, 4, r.w);
+    return r;
+}
+template <class F>
+__device__ __forceinline__ fel<F> fe_sqr_call(const fel<F>& a) {
+    if constexpr (F::N != 8) return fe_sqr_inl(F{}, a);
+    uint4* s = product_slots<F>();
+    slot_store(s, 0, a.w);
+    fe_sqr_smem<F>();
+    fel<F> r;
+    slot_load(s, 4, r.w);
+    return r;
+}
+#elif defined(GECC_PRODUCTS_BY_REF)
 // experiment: operands and result through local memory (LSU pipe) instead of register moves
 template <class F>
 __device__ __noinline__ void fe_mul_ref(fel<F>* r, const fel<F>* a, const fel<F>* b) {

@@ -197,6 +197,96 @@ GECC_HD_CALL fel<F> safegcd_inverse(const F& fld, const fel<F>& x) {
     return r;
 }
 
+// ---------------------------------------------------------------- variable-time form
+// The same recurrence run for LATENCY instead of uniformity, for the places where one warp inverts
+// one PUBLIC value that all of its lanes share (the block total of Montgomery's trick: every lane
+// holds the same number, so data-dependent control flow does not diverge): whole runs of zero bits
+// of g are shifted out at once (count-trailing-zeros), up to six low bits of g are cancelled per
+// iteration with w = -g / f mod 2^k (f (f^2 - 2) == -1/f mod 64 for odd f), and the rounds stop as
+// soon as g is zero.  Classic divsteps (delta starts at 1; eta = -delta).  Never used on secrets.
+GECC_HD int ctz32_nz(uint32_t x) {  // x != 0
+#if defined(__CUDA_ARCH__)
+    return __ffs((int)x) - 1;
+#else
+    return __builtin_ctz(x);
+#endif
+}
+GECC_HD int32_t divsteps_30_var(int32_t eta, uint32_t f0, uint32_t g0, trans2x2* t) {
+    uint32_t u = 1, v = 0, q = 0, r = 1;
+    uint32_t f = f0, g = g0;
+    uint32_t nf = f * (f * f - 2u);  // -1/f mod 64
+    int i = 30;
+    for (;;) {
+        const int zeros = ctz32_nz(g | (0xFFFFFFFFu << i));  // sentinel: at most i
+        g >>= zeros;
+        u <<= zeros;
+        v <<= zeros;
+        eta -= zeros;
+        i -= zeros;
+        if (i == 0) break;
+        if (eta < 0) {  // g is odd here: (f, g) <- (g, -f)
+            eta = -eta;
+            uint32_t tmp = f; f = g; g = 0u - tmp;
+            tmp = u; u = q; q = 0u - tmp;
+            tmp = v; v = r; r = 0u - tmp;
+            nf = f * (f * f - 2u);
+        }
+        // cancel the low min(eta + 1, i, 6) bits of g: no more than i are left in this round and the
+        // sign of eta flips after eta + 1
+        const int limit = (eta + 1) > i ? i : (eta + 1);
+        const uint32_t m = (0xFFFFFFFFu >> (32 - limit)) & 63u;
+        const uint32_t w = (g * nf) & m;
+        g += f * w;
+        q += u * w;
+        r += v * w;
+    }
+    t->u = (int32_t)u;
+    t->v = (int32_t)v;
+    t->q = (int32_t)q;
+    t->r = (int32_t)r;
+    return eta;
+}
+template <class F>
+GECC_HD_CALL fel<F> safegcd_inverse_var(const F& fld, const fel<F>& x) {
+    GECC_COUNT(safegcd, F);
+    constexpr int N = F::N, L = N == 8 ? 9 : (32 * N + 29) / 30;
+    constexpr int MAX_ROUNDS = N == 8 ? 25 : 37;  // 724 / 1086 classic divsteps bound the worst case
+    s30n<L> d, e, f, g;
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        d.v[i] = 0;
+        e.v[i] = 0;
+        f.v[i] = (int32_t)fld.q30(i);
+    }
+    e.v[0] = 1;
+    g = s30_from_limbs<N, L>(x.w);
+    int32_t eta = -1;
+#pragma unroll 1
+    for (int round = 0; round < MAX_ROUNDS; ++round) {
+        int32_t nz = 0;
+#pragma unroll
+        for (int i = 0; i < L; ++i) nz |= g.v[i];
+        if (nz == 0) break;
+        trans2x2 t;
+        eta = divsteps_30_var(eta, (uint32_t)f.v[0], (uint32_t)g.v[0], &t);
+        update_de_30(fld, &d, &e, t);
+        update_fg_30(&f, &g, t);
+    }
+    normalize_30(fld, &d, f.v[L - 1]);
+    fel<F> r;
+    s30_to_limbs<N, L>(r.w, d);
+    return r;
+}
+// Montgomery-form inverse, variable time: for warp-uniform public values only (see above)
+template <class F>
+GECC_HD fel<F> fe_inv_var(const F& f, const fel<F>& a) {
+    if constexpr (F::kind == KIND_SECP_LAZY) return safegcd_inverse_var(f, lazy_canon(f, a));
+    fel<F> r3;
+#pragma unroll
+    for (int i = 0; i < F::N; ++i) r3.w[i] = f.r3(i);
+    return fe_mul(f, safegcd_inverse_var(f, a), r3);
+}
+
 // Montgomery-form inverse of a Montgomery-form element (zero -> zero).
 template <class F>
 GECC_HD fel<F> fe_inv(const F& f, const fel<F>& a) {

@@ -32,7 +32,7 @@ __global__ void k_point_fold(int parts, const uint32_t* __restrict__ packed, uin
         out[2 * L] = 1;
         return;
     }
-    const caff<C> a = jac_to_aff_with<C>(acc, fe_inv(f, acc.Z));
+    const caff<C> a = jac_to_aff_with<C>(acc, fe_inv_var(f, acc.Z));
 #pragma unroll
     for (int i = 0; i < L; ++i) {
         out[i] = a.x.w[i];

@@ -793,7 +793,7 @@ k_msm_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, uint
             col_store(oy, 1, 0, fe_zero_n<NL>());
             oinf[0] = 1;
         } else {
-            aff a = jac_to_aff_with<C>(acc, fe_inv(f, acc.Z));
+            aff a = jac_to_aff_with<C>(acc, fe_inv_var(f, acc.Z));
             col_store(ox, 1, 0, a.x);
             col_store(oy, 1, 0, a.y);
             oinf[0] = 0;
@@ -1033,7 +1033,7 @@ k_msm_red_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, 
             col_store(oy, 1, 0, fe_zero_n<NL>());
             oinf[0] = 1;
         } else {
-            aff a = jac_to_aff_with<C>(acc, fe_inv(f, acc.Z));
+            aff a = jac_to_aff_with<C>(acc, fe_inv_var(f, acc.Z));
             col_store(ox, 1, 0, msm_to_external<CE, C>(a.x));
             col_store(oy, 1, 0, msm_to_external<CE, C>(a.y));
             oinf[0] = 0;

@@ -39,6 +39,8 @@ int field_op_t(const F& f, int op, size_t n, const uint32_t* a, const uint32_t* 
             case 8: r = safegcd_inverse(f, x); break;   // safegcd, plain in/out
             case 9: r = fe_dbl(f, x); break;            // 2x (shift form on the lazy field)
             case 10: r = fe_mul8(f, x); break;          // 8x
+            case 11: r = fe_inv_var(f, x); break;       // variable-time safegcd, Montgomery in/out
+            case 12: r = safegcd_inverse_var(f, x); break;  // variable-time safegcd, plain in/out
             default: return 1;
         }
         col_set(out, n, i, r);

@@ -57,6 +57,9 @@ def test_hostsim_inverse_and_glv():
             assert (H.field_op(cid, which, "inv_safegcd", a) == O.field_op(cid, which, "mod_inv", a)).all()
             plain = O.cols_to_ints(H.field_op(cid, which, "inv_plain", a))
             assert all(g == (pow(v, -1, q) if v else 0) for g, v in zip(plain, vals))
+            # the variable-time form (block totals of Montgomery's trick) gives the same residues
+            assert (H.field_op(cid, which, "inv_var", a) == O.field_op(cid, which, "mod_inv", a)).all()
+            assert O.cols_to_ints(H.field_op(cid, which, "inv_var_plain", a)) == plain
     n = E.SECP256K1.n
     lam = 0x5363AD4CC05C30E0A5261C028812645A122E22EA20816678DF02967C1B23BD72
     ks = [0, 1, 2, n - 1, n - 2, lam, n - lam, (n - 1) // 2, 1 << 255] + [rng.randrange(n) for _ in range(5000)]
@@ -153,6 +156,8 @@ def test_hostsim_lazy_secp_field():
         got = O.cols_to_ints(H.field_op(1, 0, op, XA, XB, field_id=H.SECP_LAZY_FIELD))
         assert all(g % p == fn(x, y) % p for g, x, y in zip(got, xa, xb)), op
     inv = O.cols_to_ints(H.field_op(1, 0, "inv_safegcd", np.ascontiguousarray(A[:, :400]), field_id=H.SECP_LAZY_FIELD))
+    assert all((g * x) % p == 1 if x % p else g == 0 for g, x in zip(inv, a[:400]))
+    inv = O.cols_to_ints(H.field_op(1, 0, "inv_var", np.ascontiguousarray(A[:, :400]), field_id=H.SECP_LAZY_FIELD))
     assert all((g * x) % p == 1 if x % p else g == 0 for g, x in zip(inv, a[:400]))
 
 

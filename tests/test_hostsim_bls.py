@@ -50,6 +50,8 @@ def test_field12_ops_vs_python_ints(B):
     assert ints(H.field_op(0, 0, "inv_plain", A, field_id=f)) == want_plain
     want_mont = [pow(x * rinv % q, -1, q) * R12 % q if x else 0 for x in a]
     assert ints(H.field_op(0, 0, "inv_safegcd", A, field_id=f)) == want_mont
+    assert ints(H.field_op(0, 0, "inv_var_plain", A, field_id=f)) == want_plain
+    assert ints(H.field_op(0, 0, "inv_var", A, field_id=f)) == want_mont
     small = cols(a[:40])
     assert ints(H.field_op(0, 0, "mod_inv", small, field_id=f)) == want_mont[:40]
 
@@ -65,6 +67,7 @@ def test_scalar_field_bls_r(B):
     f = H.BLS_FIELDS[B.cid][1]
     assert ints(H.field_op(0, 0, "mont_mul", A, Bc, field_id=f)) == [x * y * rinv % q for x, y in zip(a, b)]
     assert ints(H.field_op(0, 0, "inv_plain", A, field_id=f)) == [pow(x, -1, q) if x else 0 for x in a]
+    assert ints(H.field_op(0, 0, "inv_var_plain", A, field_id=f)) == [pow(x, -1, q) if x else 0 for x in a]
 
 
 def mont_pts(B, pts):

@@ -3,16 +3,19 @@
 #include "../../paper_2501_03245_b200/csrc/gecc_modinv.cuh"
 using namespace gecc;
 
+#ifndef UNIFORM
+#define UNIFORM 1
+#endif
 template <class F, int MODE>
 __global__ void k(uint32_t seed, uint64_t* cycles, uint32_t* out) {
     const F f{};
     fel<F> x;
-    for (int k = 0; k < F::N; ++k) x.w[k] = seed * (k + 3) + threadIdx.x * 7 + 1;
+    for (int k = 0; k < F::N; ++k) x.w[k] = seed * (k + 3) * 2654435761u + (UNIFORM ? 0 : threadIdx.x * 7) + 1;
     x.w[F::N - 1] &= 0x00FFFFFFu;
     fel<F> r;
     long long t0 = clock64();
     if (MODE == 0) r = safegcd_inverse(f, x);
-    else if (MODE == 4) r = safegcd_inverse_pipelined(f, x);
+    else if (MODE == 4) r = safegcd_inverse_var(f, x);
     else if (MODE == 1) r = fe_inv_fermat(f, x);
     else if (MODE == 2) r = fe_mul(f, x, x);
     else {
@@ -48,10 +51,10 @@ void run(const char* name, int threads) {
 
 int main() {
     run<SecpP, 0>("safegcd SecpP", 32);
-    run<SecpP, 4>("safegcd pipelined SecpP", 32);
-    run<SecpPL, 4>("safegcd pipelined lazy", 32);
+    run<SecpP, 4>("safegcd var SecpP", 32);
+    run<SecpPL, 4>("safegcd var lazy", 32);
     run<Bls381P, 0>("safegcd BLS381", 32);
-    run<Bls381P, 4>("safegcd pipelined BLS381", 32);
+    run<Bls381P, 4>("safegcd var BLS381", 32);
     run<SecpP, 0>("safegcd SecpP", 1);
     run<SecpN, 0>("safegcd SecpN", 32);
     run<SecpP, 1>("fermat SecpP", 32);

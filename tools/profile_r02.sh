@@ -31,4 +31,11 @@ for leg in $LEGS; do
         python bench.py --workload msm --steps 1 --warmup 1 --no-cpu-baseline > $OUT/${TAG}_msm.log 2>&1 ;;
   esac
 done
-ls -la $OUT | tail -20
+# the .ncu-rep files (source imported) are far beyond what gpurun brings back (64 MiB for the whole
+# directory): summarise them ON the box and keep only the CSVs
+for rep in $OUT/${TAG}_*.ncu-rep; do
+  [ -f "$rep" ] || continue
+  python tools/ncu_summary.py "$rep" "${rep%.ncu-rep}" > /dev/null 2>&1
+  rm -f "$rep"
+done
+ls -la $OUT | tail -30
