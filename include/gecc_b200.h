@@ -139,7 +139,10 @@ typedef enum gecc_field_opcode {
     /* The weakly reduced plain representation the fused secp256k1 kernels compute in
      * (GECC_CURVE_SECP256K1, GECC_FIELD_P only): inputs are ANY 256-bit values (not Montgomery
      * form, not necessarily below q), outputs are the canonical residues a*b, a^2, a+b, a-b mod q. */
-    GECC_OP_LAZY_MUL = 8, GECC_OP_LAZY_SQR = 9, GECC_OP_LAZY_ADD = 10, GECC_OP_LAZY_SUB = 11
+    GECC_OP_LAZY_MUL = 8, GECC_OP_LAZY_SQR = 9, GECC_OP_LAZY_ADD = 10, GECC_OP_LAZY_SUB = 11,
+    /* GECC_OP_MOD_INV's value computed by the warp-cooperative inversion the block-level Montgomery
+     * trick uses for its one shared inversion (every element is inverted by a whole warp) */
+    GECC_OP_MOD_INV_WARP = 12
 } gecc_field_opcode;
 
 /* Context for `curve` on CUDA device `device` (< 0: the current device). */

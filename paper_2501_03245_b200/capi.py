@@ -23,7 +23,7 @@ STATUS = {0: "ok", 1: "invalid argument", 2: "malformed input", 3: "invalid peer
           4: "degenerate result", 5: "nonce retries exhausted", 6: "cost model has no crossover",
           7: "internal error"}
 FIELD_OPS = dict(mont_mul=0, mod_add=1, mod_sub=2, to_mont=3, from_mont=4, mod_inv=5, mod_inv_fermat=6,
-                 mont_reduce=7, lazy_mul=8, lazy_sqr=9, lazy_add=10, lazy_sub=11)
+                 mont_reduce=7, lazy_mul=8, lazy_sqr=9, lazy_add=10, lazy_sub=11, mod_inv_warp=12)
 SECRET_FAST, SECRET_UNIFORM = 0, 1
 COMM_ID_BYTES = 128
 
@@ -90,7 +90,7 @@ def set_batch_form(form: str):
     lib().gecc_set_batch_form(BATCH_FORMS[form])
 
 
-MSM_FORMS = {"auto": 0, "jacobian": 1, "affine": 2, "affine1": 3}
+MSM_FORMS = {"auto": 0, "jacobian": 1, "affine": 2, "affine1": 3, "fused16": 4, "fused8": 5}
 
 
 def set_msm_form(form: str):

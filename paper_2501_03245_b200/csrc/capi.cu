@@ -339,12 +339,12 @@ sm2b_status gecc_ctx_set_secret_mode(sm2b_ctx* ctx, int mode) {
 // ------------------------------------------------------------------ field ops
 namespace {
 bool field_args_ok(const sm2b_ctx* ctx, int field, int op, size_t n, const void* a, const void* b, const void* out) {
-    if (!ctx || (n > 0 && (!a || !out)) || (unsigned)op > GECC_OP_LAZY_SUB || (unsigned)field > 1) return false;
+    if (!ctx || (n > 0 && (!a || !out)) || (unsigned)op > GECC_OP_MOD_INV_WARP || (unsigned)field > 1) return false;
     const bool binary = op <= GECC_OP_MOD_SUB || op == GECC_OP_MONT_REDUCE || op == GECC_OP_LAZY_MUL ||
                         op == GECC_OP_LAZY_ADD || op == GECC_OP_LAZY_SUB;
     if (n > 0 && binary && !b) return false;
     // the weakly reduced representation exists for the secp256k1 base field only
-    if (op >= GECC_OP_LAZY_MUL && !(ctx->curve == CURVE_SECP && field == 0)) return false;
+    if (op >= GECC_OP_LAZY_MUL && op <= GECC_OP_LAZY_SUB && !(ctx->curve == CURVE_SECP && field == 0)) return false;
     return true;
 }
 }  // namespace
@@ -394,7 +394,7 @@ sm2b_status gecc_field_op(sm2b_ctx* ctx, gecc_field field, gecc_field_opcode op,
 }
 
 void gecc_set_batch_form(int form) { set_batch_form(form < 0 || form > 9 ? 0 : form); }
-void gecc_set_msm_form(int form) { set_msm_form(form < 0 || form > 3 ? 0 : form); }
+void gecc_set_msm_form(int form) { set_msm_form(form < 0 || form > 5 ? 0 : form); }
 
 sm2b_status gecc_microbench(sm2b_ctx* ctx, int which, int iters, double* ops_per_clk_per_sm,
                             double* seconds, double* total_ops) {

@@ -147,14 +147,17 @@ __device__ fel<F> coop_block_inverse(const F& f, const fel<F>& t, uint32_t* sm) 
         fe total;
 #pragma unroll
         for (int i = 0; i < NL; ++i) total.w[i] = __shfl_sync(0xFFFFFFFFu, P.w[i], 31);
-        return fe_mul(f, fe_mul(f, fe_inv_var(f, total), E), S);  // warp-uniform public value
+        return fe_mul(f, fe_mul(f, fe_inv_warp(f, total), E), S);  // all 32 lanes hold the total: cooperative inversion
     }
     if (lane == 31) {
 #pragma unroll
         for (int i = 0; i < NL; ++i) sm[i * NW + warp] = P.w[i];
     }
     __syncthreads();
-    if (warp == 0) {
+    // the block's one inversion is run by a warp that ROTATES with the block index: warp w always
+    // sits on sub-partition w % 4, and with several blocks per SM the inversions (long chains of
+    // dependent instructions) would otherwise all queue on sub-partition 0
+    if (warp == (int)(blockIdx.x % NW)) {
         fe w = one;
         if (lane < NW) {
 #pragma unroll
@@ -165,7 +168,7 @@ __device__ fel<F> coop_block_inverse(const F& f, const fel<F>& t, uint32_t* sm) 
         fe total;
 #pragma unroll
         for (int i = 0; i < NL; ++i) total.w[i] = __shfl_sync(0xFFFFFFFFu, PP.w[i], NW - 1);
-        const fe inv = fe_inv_var(f, total);  // the block's single inversion (warp-uniform, public)
+        const fe inv = fe_inv_warp(f, total);  // the block's single inversion: warp 0 runs it cooperatively
         fe EE = fe_select(lane == 0, one, fe_shfl_up(PP, 1));
         fe SS = fe_select(lane == 31, one, fe_shfl_down(QQ, 1));
         fe wi = fe_mul(f, fe_mul(f, inv, EE), SS);

@@ -85,20 +85,32 @@ GECC_HD int32_t divsteps_30(int32_t zeta, uint32_t f0, uint32_t g0, trans2x2* t)
     return zeta;
 }
 
+// c + a * b, signed 32 x 32 -> 64: ONE instruction on the device (IMAD.WIDE); the C expression
+// (int64)a * b + c compiles to an unsigned wide multiply plus two sign corrections.
+GECC_HD int64_t mac_s32(int32_t a, int32_t b, int64_t c) {
+#if defined(__CUDA_ARCH__)
+    int64_t r;
+    asm("mad.wide.s32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(c));
+    return r;
+#else
+    return (int64_t)a * b + c;
+#endif
+}
+
 // (f, g) <- t * (f, g) / 2^30 (exact)
 template <int L>
 GECC_HD void update_fg_30(s30n<L>* f, s30n<L>* g, const trans2x2& t) {
     const int32_t M30 = 0x3FFFFFFF;
-    const int64_t u = t.u, v = t.v, q = t.q, r = t.r;
-    int64_t cf = u * f->v[0] + v * g->v[0];
-    int64_t cg = q * f->v[0] + r * g->v[0];
+    const int32_t u = t.u, v = t.v, q = t.q, r = t.r;
+    int64_t cf = mac_s32(u, f->v[0], mac_s32(v, g->v[0], 0));
+    int64_t cg = mac_s32(q, f->v[0], mac_s32(r, g->v[0], 0));
     cf >>= 30;
     cg >>= 30;
 #pragma unroll
     for (int i = 1; i < L; ++i) {
         const int32_t fi = f->v[i], gi = g->v[i];
-        cf += u * fi + v * gi;
-        cg += q * fi + r * gi;
+        cf = mac_s32(u, fi, mac_s32(v, gi, cf));
+        cg = mac_s32(q, fi, mac_s32(r, gi, cg));
         f->v[i - 1] = (int32_t)cf & M30;
         cf >>= 30;
         g->v[i - 1] = (int32_t)cg & M30;
@@ -113,25 +125,23 @@ GECC_HD void update_fg_30(s30n<L>* f, s30n<L>* g, const trans2x2& t) {
 template <class F, int L>
 GECC_HD void update_de_30(const F& f, s30n<L>* d, s30n<L>* e, const trans2x2& t) {
     const int32_t M30 = 0x3FFFFFFF;
-    const int64_t u = t.u, v = t.v, q = t.q, r = t.r;
+    const int32_t u = t.u, v = t.v, q = t.q, r = t.r;
     const int32_t sd = d->v[L - 1] >> 31, se = e->v[L - 1] >> 31;
     int32_t md = (t.u & sd) + (t.v & se);
     int32_t me = (t.q & sd) + (t.r & se);
-    int64_t cd = u * d->v[0] + v * e->v[0];
-    int64_t ce = q * d->v[0] + r * e->v[0];
+    int64_t cd = mac_s32(u, d->v[0], mac_s32(v, e->v[0], 0));
+    int64_t ce = mac_s32(q, d->v[0], mac_s32(r, e->v[0], 0));
     md -= (int32_t)((f.qinv30() * (uint32_t)cd + (uint32_t)md) & (uint32_t)M30);
     me -= (int32_t)((f.qinv30() * (uint32_t)ce + (uint32_t)me) & (uint32_t)M30);
-    cd += (int64_t)f.q30(0) * md;
-    ce += (int64_t)f.q30(0) * me;
+    cd = mac_s32((int32_t)f.q30(0), md, cd);
+    ce = mac_s32((int32_t)f.q30(0), me, ce);
     cd >>= 30;
     ce >>= 30;
 #pragma unroll
     for (int i = 1; i < L; ++i) {
         const int32_t di = d->v[i], ei = e->v[i];
-        cd += u * di + v * ei;
-        ce += q * di + r * ei;
-        cd += (int64_t)f.q30(i) * md;
-        ce += (int64_t)f.q30(i) * me;
+        cd = mac_s32(u, di, mac_s32(v, ei, mac_s32((int32_t)f.q30(i), md, cd)));
+        ce = mac_s32(q, di, mac_s32(r, ei, mac_s32((int32_t)f.q30(i), me, ce)));
         d->v[i - 1] = (int32_t)cd & M30;
         cd >>= 30;
         e->v[i - 1] = (int32_t)ce & M30;
@@ -277,6 +287,225 @@ GECC_HD_CALL fel<F> safegcd_inverse_var(const F& fld, const fel<F>& x) {
     s30_to_limbs<N, L>(r.w, d);
     return r;
 }
+// ---------------------------------------------------------------- latency-scheduled form
+// One warp inverting one value is a chain of dependent instructions: 30 divsteps (each ~5 dependent
+// operations on g) and then the matrix applied to 4 x L limbs, round after round.  Only the LOW TWO
+// limbs of f and g decide the next round's matrix, so the rounds are software-pipelined: the next
+// matrix is computed from the freshly updated low limbs in the SAME straight-line block as the rest
+// of this round's update of f, g, d, e -- two independent instruction streams that the scheduler
+// interleaves.  Same branch-free recurrence and round count as safegcd_inverse (one extra, unused,
+// divsteps block at the end); EARLY_EXIT additionally stops once g is zero (data-dependent: for
+// warp-uniform public values only).
+GECC_HD int32_t divsteps_30_flat(int32_t zeta, uint32_t f0, uint32_t g0, trans2x2* t) {
+    uint32_t u = 1, v = 0, q = 0, r = 1;
+    uint32_t f = f0, g = g0;
+#pragma unroll
+    for (int i = 0; i < 30; ++i) {
+        uint32_t c1 = (uint32_t)(zeta >> 31);
+        uint32_t c2 = 0u - (g & 1u);
+        uint32_t x = (f ^ c1) - c1;
+        uint32_t y = (u ^ c1) - c1;
+        uint32_t z = (v ^ c1) - c1;
+        g += x & c2;
+        q += y & c2;
+        r += z & c2;
+        c1 &= c2;
+        zeta = (int32_t)(((uint32_t)zeta ^ c1) - 1u);
+        f += g & c1;
+        u += q & c1;
+        v += r & c1;
+        g >>= 1;
+        u <<= 1;
+        v <<= 1;
+    }
+    t->u = (int32_t)u;
+    t->v = (int32_t)v;
+    t->q = (int32_t)q;
+    t->r = (int32_t)r;
+    return zeta;
+}
+template <bool EARLY_EXIT, class F>
+GECC_HD_CALL fel<F> safegcd_inverse_sched(const F& fld, const fel<F>& x) {
+    GECC_COUNT(safegcd, F);
+    constexpr int N = F::N, L = N == 8 ? 9 : (32 * N + 29) / 30, ROUNDS = N == 8 ? 20 : (49 * N + 16) / 17 + 1;
+    const int32_t M30 = 0x3FFFFFFF;
+    s30n<L> d, e, f, g;
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+        d.v[i] = 0;
+        e.v[i] = 0;
+        f.v[i] = (int32_t)fld.q30(i);
+    }
+    e.v[0] = 1;
+    g = s30_from_limbs<N, L>(x.w);
+    trans2x2 t;
+    int32_t zeta = divsteps_30_flat(-1, (uint32_t)f.v[0], (uint32_t)g.v[0], &t);
+#pragma unroll 1
+    for (int round = 0; round < ROUNDS; ++round) {
+        // limb 0 of t * (f, g) / 2^30 from limbs 0 and 1 (the same arithmetic update_fg_30 does)
+        const int64_t u = t.u, v = t.v, q = t.q, r = t.r;
+        int64_t cf = u * f.v[0] + v * g.v[0];
+        int64_t cg = q * f.v[0] + r * g.v[0];
+        cf >>= 30;
+        cg >>= 30;
+        cf += u * f.v[1] + v * g.v[1];
+        cg += q * f.v[1] + r * g.v[1];
+        trans2x2 tn;
+        const int32_t zn = divsteps_30_flat(zeta, (uint32_t)((int32_t)cf & M30), (uint32_t)((int32_t)cg & M30), &tn);
+        update_de_30(fld, &d, &e, t);
+        update_fg_30(&f, &g, t);
+        t = tn;
+        zeta = zn;
+        if (EARLY_EXIT) {
+            int32_t nz = 0;
+#pragma unroll
+            for (int i = 0; i < L; ++i) nz |= g.v[i];
+            if (nz == 0) break;
+        }
+    }
+    normalize_30(fld, &d, f.v[L - 1]);
+    fel<F> res;
+    s30_to_limbs<N, L>(res.w, d);
+    return res;
+}
+
+#if defined(__CUDACC__)
+#ifndef GECC_WARP_INV_VAR
+#define GECC_WARP_INV_VAR false
+#endif
+// ---------------------------------------------------------------- warp-cooperative form
+// One value inverted by a whole warp (every lane passes the SAME x; all 32 lanes must call).  A
+// single thread's inversion is ~24 000 dependent-ish instructions; here the two halves of the warp
+// split the work that does not sit on the critical chain:
+//   * the transition matrix: lanes 0-15 track its first column (u, q), lanes 16-31 the second
+//     (v, r) -- the same recurrence from different start values, 7 operations per divstep instead
+//     of 14 -- and swap the columns with four shuffles per round;
+//   * the big updates: lanes 0-15 hold (f, g), lanes 16-31 hold (d, e).  Both run the ONE routine
+//     "(A, B) <- t (A, B) + (md, me) q, shifted down 30 bits" (md = me = 0 on the f, g half), with
+//     signed wide multiply-adds (mad.wide.s32: one instruction per product; the C form compiles to
+//     three);
+//   * the next round's f0, g0 come back from lane 0 by shuffle; the rounds stop when g is zero
+//     (uniform: the value is shared), the result leaves lanes 16-31 by shuffle.
+// Same recurrence, same value as safegcd_inverse.  Public values only (early exit).
+// VAR: the divsteps of a round by count-trailing-zeros runs and 6-bit cancellation (divsteps_30_var)
+// instead of 30 branch-free steps -- a third of the instructions, data-dependent trip count.
+template <bool VAR, class F>
+__device__ __noinline__ fel<F> safegcd_inverse_warp(const F& fld, const fel<F>& x) {
+    constexpr int N = F::N, L = N == 8 ? 9 : (32 * N + 29) / 30;
+    constexpr int ROUNDS = VAR ? (N == 8 ? 25 : 37) : (N == 8 ? 20 : (49 * N + 16) / 17 + 1);
+    const int32_t M30 = 0x3FFFFFFF;
+    const unsigned FULL = 0xFFFFFFFFu;
+    const bool de = (threadIdx.x & 16) != 0;  // this lane's half: (d, e) / second column
+    s30n<L> A, B;                             // (f, g) or (d, e)
+    {
+        const s30n<L> g = s30_from_limbs<N, L>(x.w);
+#pragma unroll
+        for (int i = 0; i < L; ++i) {
+            A.v[i] = de ? 0 : (int32_t)fld.q30(i);
+            B.v[i] = de ? (i == 0 ? 1 : 0) : g.v[i];
+        }
+    }
+    int32_t zeta = -1;
+    uint32_t f0 = fld.q30(0), g0 = (uint32_t)__shfl_sync(FULL, B.v[0], 0);
+#pragma unroll 1
+    for (int round = 0; round < ROUNDS; ++round) {
+        // 30 divsteps; this lane's column (a, b) of the matrix
+        uint32_t a = de ? 0u : 1u, b = de ? 1u : 0u;
+        uint32_t f = f0, g = g0;
+        if constexpr (VAR) {  // zeta holds eta = -delta of the classic divsteps here
+            uint32_t nf = f * (f * f - 2u);
+            int i = 30;
+            for (;;) {
+                const int zeros = ctz32_nz(g | (0xFFFFFFFFu << i));
+                g >>= zeros;
+                a <<= zeros;
+                zeta -= zeros;
+                i -= zeros;
+                if (i == 0) break;
+                if (zeta < 0) {
+                    zeta = -zeta;
+                    uint32_t tmp = f; f = g; g = 0u - tmp;
+                    tmp = a; a = b; b = 0u - tmp;
+                    nf = f * (f * f - 2u);
+                }
+                const int limit = (zeta + 1) > i ? i : (zeta + 1);
+                const uint32_t w = (g * nf) & (0xFFFFFFFFu >> (32 - limit)) & 63u;
+                g += f * w;
+                b += a * w;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < 30; ++i) {
+                uint32_t c1 = (uint32_t)(zeta >> 31);
+                const uint32_t c2 = 0u - (g & 1u);
+                const uint32_t xx = (f ^ c1) - c1;
+                const uint32_t yy = (a ^ c1) - c1;
+                g += xx & c2;
+                b += yy & c2;
+                c1 &= c2;
+                zeta = (int32_t)(((uint32_t)zeta ^ c1) - 1u);
+                f += g & c1;
+                a += b & c1;
+                g >>= 1;
+                a <<= 1;
+            }
+        }
+        const int32_t u = (int32_t)__shfl_sync(FULL, a, 0), q = (int32_t)__shfl_sync(FULL, b, 0);
+        const int32_t v = (int32_t)__shfl_sync(FULL, a, 16), r = (int32_t)__shfl_sync(FULL, b, 16);
+        // (A, B) <- (t (A, B) + (md, me) q) / 2^30; md = me = 0 on the (f, g) half (update_fg_30),
+        // the modular correction of update_de_30 on the other
+        const int32_t sa = A.v[L - 1] >> 31, sb = B.v[L - 1] >> 31;
+        int32_t md = (u & sa) + (v & sb);
+        int32_t me = (q & sa) + (r & sb);
+        int64_t ca = mac_s32(u, A.v[0], mac_s32(v, B.v[0], 0));
+        int64_t cb = mac_s32(q, A.v[0], mac_s32(r, B.v[0], 0));
+        md -= (int32_t)((fld.qinv30() * (uint32_t)ca + (uint32_t)md) & (uint32_t)M30);
+        me -= (int32_t)((fld.qinv30() * (uint32_t)cb + (uint32_t)me) & (uint32_t)M30);
+        md = de ? md : 0;
+        me = de ? me : 0;
+        ca = mac_s32((int32_t)fld.q30(0), md, ca);
+        cb = mac_s32((int32_t)fld.q30(0), me, cb);
+        ca >>= 30;
+        cb >>= 30;
+#pragma unroll
+        for (int i = 1; i < L; ++i) {
+            const int32_t ai = A.v[i], bi = B.v[i];
+            ca = mac_s32(u, ai, mac_s32(v, bi, mac_s32((int32_t)fld.q30(i), md, ca)));
+            cb = mac_s32(q, ai, mac_s32(r, bi, mac_s32((int32_t)fld.q30(i), me, cb)));
+            A.v[i - 1] = (int32_t)ca & M30;
+            ca >>= 30;
+            B.v[i - 1] = (int32_t)cb & M30;
+            cb >>= 30;
+        }
+        A.v[L - 1] = (int32_t)ca;
+        B.v[L - 1] = (int32_t)cb;
+        int32_t nz = 0;
+#pragma unroll
+        for (int i = 0; i < L; ++i) nz |= B.v[i];
+        f0 = (uint32_t)__shfl_sync(FULL, A.v[0], 0);
+        g0 = (uint32_t)__shfl_sync(FULL, B.v[0], 0);
+        if (__shfl_sync(FULL, nz, 0) == 0) break;  // g == 0: uniform over the warp
+    }
+    // d (lanes 16-31), negated when f (lanes 0-15) ended at -1
+    const int32_t fsign = __shfl_sync(FULL, A.v[L - 1], 0);
+    normalize_30(fld, &A, fsign);
+    fel<F> res;
+    s30_to_limbs<N, L>(res.w, A);
+#pragma unroll
+    for (int i = 0; i < N; ++i) res.w[i] = __shfl_sync(FULL, res.w[i], 16);
+    return res;
+}
+// Montgomery-form inverse of a value shared by the whole warp (all 32 lanes call with the same a)
+template <class F>
+__device__ __forceinline__ fel<F> fe_inv_warp(const F& f, const fel<F>& a) {
+    if constexpr (F::kind == KIND_SECP_LAZY) return safegcd_inverse_warp<GECC_WARP_INV_VAR>(f, lazy_canon(f, a));
+    fel<F> r3;
+#pragma unroll
+    for (int i = 0; i < F::N; ++i) r3.w[i] = f.r3(i);
+    return fe_mul(f, safegcd_inverse_warp<GECC_WARP_INV_VAR>(f, a), r3);
+}
+#endif
+
 // Montgomery-form inverse, variable time: for warp-uniform public values only (see above)
 template <class F>
 GECC_HD fel<F> fe_inv_var(const F& f, const fel<F>& a) {

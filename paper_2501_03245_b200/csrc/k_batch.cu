@@ -165,10 +165,10 @@ k_batch_pdbl(size_t n, size_t T, const uint32_t* __restrict__ px, const uint32_t
 // tile + k * COOP_THREADS + tid), so every limb load of a warp is one 128-byte line.
 // Compared with the chunked kernels above this exposes n / COOP_K threads instead of n / 16:
 // it is the form used while the batch is too small to fill the chip with 16-element chunks.
-constexpr int COOP_K = 4;
+constexpr int COOP_K = 4;  // elements per thread of the default form; small batches take fewer (coop_k)
 
-template <class F, int COOP_THREADS>
-__global__ void __launch_bounds__(COOP_THREADS)
+template <class F, int COOP_THREADS, int COOP_K = 4>
+__global__ void __launch_bounds__(COOP_THREADS, COOP_THREADS == 128 ? 4 : 1)
 k_batch_invert_coop(size_t n, const uint32_t* __restrict__ in, uint32_t* __restrict__ out) {
     using fe = fel<F>;
     constexpr int NL = F::N;
@@ -200,8 +200,8 @@ k_batch_invert_coop(size_t n, const uint32_t* __restrict__ in, uint32_t* __restr
     }
 }
 
-template <class C, int COOP_THREADS>
-__global__ void __launch_bounds__(COOP_THREADS)
+template <class C, int COOP_THREADS, int COOP_K = 4>
+__global__ void __launch_bounds__(COOP_THREADS, COOP_THREADS == 128 ? 4 : 1)
 k_batch_padd_coop(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
                   const uint8_t* __restrict__ pinf, const uint32_t* __restrict__ tx,
                   const uint32_t* __restrict__ ty, const uint8_t* __restrict__ tinf,
@@ -264,8 +264,8 @@ k_batch_padd_coop(size_t n, const uint32_t* __restrict__ px, const uint32_t* __r
     }
 }
 
-template <class C, int COOP_THREADS>
-__global__ void __launch_bounds__(COOP_THREADS)
+template <class C, int COOP_THREADS, int COOP_K = 4>
+__global__ void __launch_bounds__(COOP_THREADS, COOP_THREADS == 128 ? 4 : 1)
 k_batch_pdbl_coop(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
                   const uint8_t* __restrict__ pinf, uint32_t* __restrict__ ox,
                   uint32_t* __restrict__ oy, uint8_t* __restrict__ oinf) {
@@ -578,9 +578,12 @@ size_t batch_padd_scratch_bytes(size_t n) {
     return (fused > tiled ? fused : tiled) + 1024;
 }
 static int coop_threads(int form) { return form == 2 ? 256 : form == 4 ? 128 : form == 5 ? 32 : 0; }
-static unsigned coop_blocks(size_t n, int threads) {
-    return (unsigned)((n + (size_t)threads * COOP_K - 1) / ((size_t)threads * COOP_K));
+static unsigned coop_blocks(size_t n, int threads, int k = COOP_K) {
+    return (unsigned)((n + (size_t)threads * k - 1) / ((size_t)threads * k));
 }
+// elements per thread: small batches spread over more blocks (the chain of dependent products and
+// memory round trips per thread is what their time consists of)
+static int coop_k(size_t n) { return n <= ((size_t)1 << 15) ? 1 : n <= ((size_t)1 << 17) ? 2 : 4; }
 // threads: enough to fill the chip, at most one element short of ~CHUNK per thread
 static size_t pick_threads(size_t n, int form) {
     const size_t CHUNK = 16, cap = (size_t)148 * (form == 3 ? 24 : 16) * BATCH_THREADS;
@@ -589,12 +592,15 @@ static size_t pick_threads(size_t n, int form) {
     if (T < 1) T = 1;
     return (T + BATCH_THREADS - 1) / BATCH_THREADS * BATCH_THREADS;
 }
-#define COOP_DISPATCH(threads, KERNEL, ...)                                             \
-    do {                                                                                \
-        const unsigned cb__ = coop_blocks(n, threads);                                  \
-        if (threads == 256) KERNEL(256)<<<cb__, 256, 0, s>>>(__VA_ARGS__);              \
-        else if (threads == 128) KERNEL(128)<<<cb__, 128, 0, s>>>(__VA_ARGS__);         \
-        else KERNEL(32)<<<cb__, 32, 0, s>>>(__VA_ARGS__);                               \
+#define COOP_DISPATCH(threads, KERNEL, ...)                                                       \
+    do {                                                                                          \
+        const int ck__ = threads == 128 ? coop_k(n) : COOP_K;                                     \
+        const unsigned cb__ = coop_blocks(n, threads, ck__);                                      \
+        if (threads == 256) KERNEL(256, 4)<<<cb__, 256, 0, s>>>(__VA_ARGS__);                     \
+        else if (threads == 128 && ck__ == 1) KERNEL(128, 1)<<<cb__, 128, 0, s>>>(__VA_ARGS__);   \
+        else if (threads == 128 && ck__ == 2) KERNEL(128, 2)<<<cb__, 128, 0, s>>>(__VA_ARGS__);   \
+        else if (threads == 128) KERNEL(128, 4)<<<cb__, 128, 0, s>>>(__VA_ARGS__);                \
+        else KERNEL(32, 4)<<<cb__, 32, 0, s>>>(__VA_ARGS__);                                      \
     } while (0)
 
 cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* in, uint32_t* out,
@@ -614,19 +620,19 @@ cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* 
     const int form = pick_form(n);
     if (const int ct = coop_threads(form)) {
         if (curve == CURVE_SECP && field == 0) {
-#define KT_(t) k_batch_invert_coop<SecpP, t>
+#define KT_(t, k) k_batch_invert_coop<SecpP, t, k>
             COOP_DISPATCH(ct, KT_, n, in, out);
 #undef KT_
         } else if (curve == CURVE_SECP) {
-#define KT_(t) k_batch_invert_coop<SecpN, t>
+#define KT_(t, k) k_batch_invert_coop<SecpN, t, k>
             COOP_DISPATCH(ct, KT_, n, in, out);
 #undef KT_
         } else if (field == 0) {
-#define KT_(t) k_batch_invert_coop<Sm2P, t>
+#define KT_(t, k) k_batch_invert_coop<Sm2P, t, k>
             COOP_DISPATCH(ct, KT_, n, in, out);
 #undef KT_
         } else {
-#define KT_(t) k_batch_invert_coop<Sm2N, t>
+#define KT_(t, k) k_batch_invert_coop<Sm2N, t, k>
             COOP_DISPATCH(ct, KT_, n, in, out);
 #undef KT_
         }
@@ -748,11 +754,11 @@ cudaError_t launch_batch_padd(int curve, size_t n, const uint32_t* px, const uin
     }
     if (const int ct = coop_threads(form)) {
         if (curve == CURVE_SECP) {
-#define KT_(t) k_batch_padd_coop<SecpCurve, t>
+#define KT_(t, k) k_batch_padd_coop<SecpMLCurve, t, k>
             COOP_DISPATCH(ct, KT_, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
 #undef KT_
         } else {
-#define KT_(t) k_batch_padd_coop<Sm2Curve, t>
+#define KT_(t, k) k_batch_padd_coop<Sm2Curve, t, k>
             COOP_DISPATCH(ct, KT_, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf);
 #undef KT_
         }
@@ -787,11 +793,11 @@ cudaError_t launch_batch_pdbl(int curve, size_t n, const uint32_t* px, const uin
     const int form = pick_form(n);
     if (const int ct = coop_threads(form)) {
         if (curve == CURVE_SECP) {
-#define KT_(t) k_batch_pdbl_coop<SecpCurve, t>
+#define KT_(t, k) k_batch_pdbl_coop<SecpMLCurve, t, k>
             COOP_DISPATCH(ct, KT_, n, px, py, pinf, ox, oy, oinf);
 #undef KT_
         } else {
-#define KT_(t) k_batch_pdbl_coop<Sm2Curve, t>
+#define KT_(t, k) k_batch_pdbl_coop<Sm2Curve, t, k>
             COOP_DISPATCH(ct, KT_, n, px, py, pinf, ox, oy, oinf);
 #undef KT_
         }

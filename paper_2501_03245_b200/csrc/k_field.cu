@@ -52,9 +52,48 @@ __global__ void __launch_bounds__(256) k_field_op(int op, size_t n, const uint32
     }
 }
 
+// op 12: every element inverted by a whole warp (the inversion of coop_block_inverse).  Lane e's
+// element is broadcast, inverted by all 32 lanes together, and kept by lane e.
+template <class F>
+__global__ void __launch_bounds__(128) k_field_inv_warp(size_t n, const uint32_t* __restrict__ a,
+                                                        uint32_t* __restrict__ out) {
+    const F f{};
+    constexpr int N = F::N;
+    const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;  // whole warps stay in the loop
+    const int lane = threadIdx.x & 31;
+    feN<N> x = i < n ? col_load<N>(a, n, i) : fe_zero_n<N>();
+    feN<N> r = x;
+#pragma unroll 1
+    for (int e = 0; e < 32; ++e) {
+        feN<N> xe;
+#pragma unroll
+        for (int k = 0; k < N; ++k) xe.w[k] = __shfl_sync(0xFFFFFFFFu, x.w[k], e);
+        const feN<N> re = fe_inv_warp(f, xe);
+        if (lane == e) r = re;
+    }
+    if (i < n) col_store(out, n, i, r);
+}
+
 cudaError_t launch_field_op(int curve, int field, int op, size_t n, const uint32_t* a,
                             const uint32_t* b, uint32_t* out, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
+    if (op == 12) {
+        const unsigned wb = (unsigned)((n + 127) / 128);
+        if (curve == CURVE_BLS381) {
+            if (field == 0) k_field_inv_warp<Bls381P><<<wb, 128, 0, s>>>(n, a, out);
+            else k_field_inv_warp<Bls381R><<<wb, 128, 0, s>>>(n, a, out);
+        } else if (curve == CURVE_BLS377) {
+            if (field == 0) k_field_inv_warp<Bls377P><<<wb, 128, 0, s>>>(n, a, out);
+            else k_field_inv_warp<Bls377R><<<wb, 128, 0, s>>>(n, a, out);
+        } else if (curve == CURVE_SECP) {
+            if (field == 0) k_field_inv_warp<SecpP><<<wb, 128, 0, s>>>(n, a, out);
+            else k_field_inv_warp<SecpN><<<wb, 128, 0, s>>>(n, a, out);
+        } else {
+            if (field == 0) k_field_inv_warp<Sm2P><<<wb, 128, 0, s>>>(n, a, out);
+            else k_field_inv_warp<Sm2N><<<wb, 128, 0, s>>>(n, a, out);
+        }
+        return cudaGetLastError();
+    }
     const int threads = 256;
     size_t want = (n + threads - 1) / threads;
     const int blocks = (int)(want < 148 * 16 ? want : 148 * 16);

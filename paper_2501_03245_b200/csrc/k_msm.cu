@@ -24,6 +24,7 @@
 // All of it is a template over the curve: 8-limb SM2 / secp256k1 (the latter accumulates on its
 // lazy plain field), 12-limb BLS12-381 / BLS12-377 G1.
 // Bucket ids: window w, magnitude m = 1..2^15  ->  w * 2^15 + (m - 1).
+#include <cstdlib>
 #include <type_traits>
 
 #include "gecc_batch.cuh"
@@ -157,21 +158,42 @@ k_msm_scan_blocks(const uint32_t* __restrict__ counts, uint32_t* __restrict__ lo
     if (b < MSM_NB) local[b] = inc - c;  // exclusive, local to the block
     if (threadIdx.x == 0) block_totals[blockIdx.x] = total;
 }
+// Window w owns the positions [w * region, (w + 1) * region) of the sorted pair arrays (region =
+// n rounded up to the tree's largest node): the windows are then independent sub-problems whose
+// trees and reductions run as a pipeline on two streams.  block_totals[b] becomes the first
+// position of scan block b (32 blocks per window), block_totals[MSM_SCAN_BLOCKS + w] the number
+// of pairs of window w.
+constexpr unsigned MSM_SCAN_BLOCKS_PER_WINDOW = MSM_BUCKETS / MSM_SCAN_THREADS;
+static_assert(MSM_BUCKETS % MSM_SCAN_THREADS == 0, "whole scan blocks per window");
 __global__ void __launch_bounds__(MSM_SCAN_THREADS)
-k_msm_scan_tops(uint32_t* __restrict__ block_totals, uint32_t* __restrict__ keys_sorted, size_t pairs) {
+k_msm_scan_tops(uint32_t* __restrict__ block_totals, uint32_t region) {
     __shared__ uint32_t sh[32];
+    __shared__ uint32_t inc_all[MSM_SCAN_THREADS];
     const uint32_t t = threadIdx.x;
     const uint32_t c = t < MSM_SCAN_BLOCKS ? block_totals[t] : 0u;
     uint32_t total;
     const uint32_t inc = block_scan_inclusive(c, sh, &total);
-    if (t < MSM_SCAN_BLOCKS) block_totals[t] = inc - c;  // exclusive block offsets
-    // positions behind the last pair hold "no bucket" (zero digits, points at infinity)
-    for (size_t p = (size_t)total + t; p < pairs; p += MSM_SCAN_THREADS) keys_sorted[p] = MSM_KEY_NONE;
+    inc_all[t] = inc;
+    __syncthreads();
+    if (t < MSM_SCAN_BLOCKS) {
+        const uint32_t w = t / MSM_SCAN_BLOCKS_PER_WINDOW, first = w * MSM_SCAN_BLOCKS_PER_WINDOW;
+        const uint32_t before = first ? inc_all[first - 1] : 0u;      // pairs of the windows below
+        block_totals[t] = (inc - c) - before + w * region;
+        if (t == first) block_totals[MSM_SCAN_BLOCKS + w] = inc_all[first + MSM_SCAN_BLOCKS_PER_WINDOW - 1] - before;
+    }
 }
 __global__ void __launch_bounds__(MSM_SCAN_THREADS)
 k_msm_scan_finish(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ block_totals,
-                  uint32_t* __restrict__ starts /* in: local prefixes */, uint32_t* __restrict__ cursor) {
+                  uint32_t* __restrict__ starts /* in: local prefixes */, uint32_t* __restrict__ cursor,
+                  uint32_t* __restrict__ keys_sorted, uint32_t region) {
     const uint32_t b = blockIdx.x * MSM_SCAN_THREADS + threadIdx.x;
+    // the positions of a window's region behind its last pair hold "no bucket" (zero digits, points
+    // at infinity, the rounding of the region; the carry window is almost all of that kind)
+    for (uint32_t w = 0; w < MSM_WINDOWS; ++w) {
+        const size_t end = (size_t)(w + 1) * region;
+        for (size_t p = (size_t)w * region + block_totals[MSM_SCAN_BLOCKS + w] + b; p < end; p += (size_t)gridDim.x * MSM_SCAN_THREADS)
+            keys_sorted[p] = MSM_KEY_NONE;
+    }
     if (b >= MSM_NB) return;
     const uint32_t at = starts[b] + block_totals[blockIdx.x];
     cursor[b] = at;
@@ -687,6 +709,87 @@ k_msm_tree_bwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
     }
 }
 
+// Fused form: ALL levels of the tree in one launch.  A block owns the aligned chunk of
+// 2 * THREADS * K0 positions: its level-l joins touch only slots of that chunk, so the levels run one
+// after the other inside the block (slots go through L2; __syncthreads orders them) and nothing is
+// parked in global memory: prefix products live in shared memory, every level does ONE block-level
+// (or, on the thin upper levels, warp-level) inversion -- the variable-time one, ~7 us of one warp's
+// time while the other resident blocks compute.  Level l has THREADS * K0 / 2^l joins per block:
+// K0 / 2^l per thread while that is >= FUSED_KMIN, then warp 0 alone takes them all (K = count / 32),
+// so that the scan share (12-14 products per thread and level) stays small against the joins.
+// One launch instead of 36, and 8 (keys) + 64 (gather) + ~130 (slots, L2) bytes per addition
+// instead of ~320.
+constexpr int MSM_FUSED_KMIN = 4;
+
+template <class C, bool LEVEL0, int THREADS_ACTIVE, int NSM>
+__device__ __forceinline__ void tree_level_in_block(size_t m, int level, size_t j_first, int K, size_t joins,
+                                                    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                                    const uint4* __restrict__ rec, uint4* slots, uint8_t* sinf,
+                                                    uint32_t* sm_pref, uint32_t* sm_scan) {
+    // the THREADS_ACTIVE calling threads (the whole block, or warp 0) take K joins each:
+    // j = j_first + k * THREADS_ACTIVE + tid.  sm_pref is word-interleaved over NSM threads.
+    using fe = cfe<C>;
+    constexpr int NL = C::Fp::N;
+    const typename C::Fp f{};
+    const int tid = threadIdx.x;
+    fe acc = fe_one(f);
+#pragma unroll 1
+    for (int k = 0; k < K; ++k) {
+        const size_t j = j_first + (size_t)k * THREADS_ACTIVE + tid;
+        if (j < joins) {
+            const TreeJoin<C, LEVEL0> t = tree_locate<C, LEVEL0>(j, level, m, keys, vals);
+            if (t.active) acc = fe_mul(f, acc, tree_denominator<C, LEVEL0>(t, rec, slots, sinf));
+        }
+#pragma unroll
+        for (int w = 0; w < NL; ++w) sm_pref[(k * NL + w) * NSM + tid] = acc.w[w];
+    }
+    fe inv = coop_block_inverse<decltype(f), THREADS_ACTIVE>(f, acc, sm_scan);
+#pragma unroll 1
+    for (int k = K - 1; k >= 0; --k) {
+        const size_t j = j_first + (size_t)k * THREADS_ACTIVE + tid;
+        if (j >= joins) continue;
+        const TreeJoin<C, LEVEL0> t = tree_locate<C, LEVEL0>(j, level, m, keys, vals);
+        fe prev = fe_one(f);
+        if (k > 0) {
+#pragma unroll
+            for (int w = 0; w < NL; ++w) prev.w[w] = sm_pref[((k - 1) * NL + w) * NSM + tid];
+        }
+        tree_apply<C, LEVEL0>(t, inv, prev, k == 0, rec, slots, sinf);
+    }
+}
+
+template <class C, int K0>
+__global__ void __launch_bounds__(MSM_TREE_THREADS, K0 * C::Fp::N > 128 ? 2 : K0 * C::Fp::N > 64 ? 3 : 5)
+k_msm_tree_fused(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                 const uint4* __restrict__ rec, uint4* slots, uint8_t* sinf) {
+    constexpr int NL = C::Fp::N;
+    constexpr int T = MSM_TREE_THREADS;
+    static_assert((T * K0) >> (MSM_TREE_LEVELS - 1) >= 32, "the last level still fills a warp");
+    static_assert(K0 >= 2 * MSM_FUSED_KMIN, "warp 0 takes at most K0 joins per lane on the thin levels");
+    extern __shared__ uint32_t sm_dyn[];
+    uint32_t* sm_pref = sm_dyn;                       // K0 * NL * T words
+    uint32_t* sm_scan = sm_dyn + K0 * NL * T;         // 2 * NL * (T / 32) words
+    {
+        const size_t joins = (m + 1) / 2;
+        tree_level_in_block<C, true, T, T>(m, 0, (size_t)blockIdx.x * (T * K0), K0, joins, keys, vals, rec, slots, sinf,
+                                           sm_pref, sm_scan);
+    }
+#pragma unroll 1
+    for (int level = 1; level < MSM_TREE_LEVELS; ++level) {
+        __syncthreads();  // the slots of the level below are complete (and sm_pref / sm_scan are free)
+        const size_t span = (size_t)2 << level;
+        const size_t joins = (m + span - 1) / span;
+        const int count = (T * K0) >> level;          // joins of this block on this level
+        const size_t j_first = (size_t)blockIdx.x * count;
+        if (j_first >= joins) continue;               // uniform over the block
+        if (count >= T * MSM_FUSED_KMIN) {
+            tree_level_in_block<C, false, T, T>(m, level, j_first, count / T, joins, keys, vals, rec, slots, sinf, sm_pref, sm_scan);
+        } else if (threadIdx.x < 32) {                // warp 0 alone: K = count / 32 <= 4 * KMIN
+            tree_level_in_block<C, false, 32, T>(m, level, j_first, count / 32, joins, keys, vals, rec, slots, sinf, sm_pref, sm_scan);
+        }
+    }
+}
+
 // marginal sums, stage 1: thread (w, k, e, part) adds the 32 buckets of window w whose
 // k-th base-32 digit is e and whose next digit (cyclically) is `part`.
 template <class C>
@@ -842,13 +945,13 @@ template <class C>
 __global__ void __launch_bounds__(128, 4)
 k_msm_red_parts(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ starts,
                 const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
-                uint32_t* __restrict__ parts) {
+                uint32_t* __restrict__ parts, uint32_t w0) {
     using fe = cfe<C>;
     using jac = cjac<C>;
     using aff = caff<C>;
     constexpr int NL = C::Fp::N;
     (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x + w0 * (3 * 4096);  // windows [w0, w0 + gridDim.x / 96)
     if (t >= MSM_RED_PARTS) return;
     const uint32_t sub = t & 3, part = (t >> 2) & 31, e = (t >> 7) & 31, k = (t >> 12) % 3, w = t / (3 * 4096);
     const size_t step = (size_t)1 << MSM_TREE_LEVELS;
@@ -872,13 +975,13 @@ k_msm_red_parts(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __r
 
 template <class C>
 __global__ void __launch_bounds__(128)
-k_msm_red_fold(const uint32_t* __restrict__ parts, uint32_t* __restrict__ marg) {
+k_msm_red_fold(const uint32_t* __restrict__ parts, uint32_t* __restrict__ marg, uint32_t w0) {
     using fe = cfe<C>;
     using jac = cjac<C>;
     using aff = caff<C>;
     constexpr int NL = C::Fp::N;
     (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
-    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    const uint32_t gw = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) + w0 * 96, lane = threadIdx.x & 31;
     if (gw >= MSM_WINDOWS * 3 * 32) return;  // whole warps leave together
     const size_t base = ((size_t)gw * 32 + lane) * 4;
     jac acc = jac_load<NL>(parts, MSM_RED_PARTS, base);
@@ -890,14 +993,14 @@ k_msm_red_fold(const uint32_t* __restrict__ parts, uint32_t* __restrict__ marg) 
 
 template <class C>
 __global__ void __launch_bounds__(128)
-k_msm_red_weighted(const uint32_t* __restrict__ marg, uint32_t* __restrict__ wsum) {
+k_msm_red_weighted(const uint32_t* __restrict__ marg, uint32_t* __restrict__ wsum, uint32_t w0, uint32_t w1) {
     using fe = cfe<C>;
     using jac = cjac<C>;
     using aff = caff<C>;
     constexpr int NL = C::Fp::N;
     (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
-    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (gw >= MSM_WINDOWS * 3) return;
+    const uint32_t gw = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) + w0 * 3, lane = threadIdx.x & 31;
+    if (gw >= w1 * 3) return;
     const uint32_t w = gw / 3, k = gw % 3;
     jac S = jac_load<NL>(marg, (size_t)MSM_WINDOWS * 3 * 32, (size_t)gw * 32 + lane);
 #pragma unroll 1
@@ -973,25 +1076,25 @@ __device__ __forceinline__ cjac<C> jac_dbl_group4(const cjac<C>& p, int lane) {
     return o;
 }
 
-// Window combine.  Groups of four lanes own one window each (17 windows -> 3 warps): S_w by
-// Horner over its three weighted marginals, then the shift by 2^(16 w) -- doublings by the lane
-// group; warp 0 then tree-sums the windows.
+// Window combine, two kernels.  k_msm_red_shift: groups of four lanes own one window each of
+// [w0, w1): S_w by Horner over its three weighted marginals, then the shift by 2^(16 w) --
+// doublings by the lane group -- and the shifted window sum goes to `win`.  k_msm_red_final: one
+// warp tree-sums the windows and converts to affine.  (Split so that the window groups of the
+// pipeline shift independently, the long chains of the high windows behind other groups' trees.)
 constexpr int MSM_COMBINE_THREADS = 96;
-template <class C, class CE>
+template <class C>
 __global__ void __launch_bounds__(MSM_COMBINE_THREADS)
-k_msm_red_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, uint32_t* __restrict__ oy,
-                  uint8_t* __restrict__ oinf) {
+k_msm_red_shift(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ win, uint32_t w0, uint32_t w1) {
     using fe = cfe<C>;
     using jac = cjac<C>;
     using aff = caff<C>;
     constexpr int NL = C::Fp::N;
     (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
     static_assert(MSM_WINDOWS * 4 <= MSM_COMBINE_THREADS, "one lane group per window");
-    __shared__ uint32_t win[3 * NL * 32];
     const int lane = threadIdx.x & 31;
-    const uint32_t w = threadIdx.x >> 2;  // window of this lane group
+    const uint32_t w = w0 + (threadIdx.x >> 2);  // window of this lane group
     const size_t cnt = (size_t)MSM_WINDOWS * 4;
-    const bool live = w < MSM_WINDOWS;
+    const bool live = w < w1;
     auto dbl = [&](const jac& p) -> jac {
         if constexpr (C::a_kind == A_ZERO || C::a_kind == A_MINUS3) return jac_dbl_group4<C>(p, lane);
         else return jac_dbl_flat<C>(p);
@@ -1021,10 +1124,19 @@ k_msm_red_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, 
         const jac t = dbl(s);
         if (i < mine) s = t;
     }
-    if ((threadIdx.x & 3) == 0) jac_store<NL>(win, 32, threadIdx.x >> 2, s);  // groups 0..23
-    __syncthreads();
-    if (threadIdx.x >= 32) return;
-    jac acc = lane < MSM_WINDOWS ? jac_load<NL>(win, 32, lane) : jac_infinity<C>();
+    if (live && (threadIdx.x & 3) == 0) jac_store<NL>(win, MSM_WINDOWS, w, s);
+}
+template <class C, class CE>
+__global__ void __launch_bounds__(32)
+k_msm_red_final(const uint32_t* __restrict__ win, uint32_t* __restrict__ ox, uint32_t* __restrict__ oy,
+                uint8_t* __restrict__ oinf) {
+    using fe = cfe<C>;
+    using jac = cjac<C>;
+    using aff = caff<C>;
+    constexpr int NL = C::Fp::N;
+    (void)sizeof(fe); (void)sizeof(jac); (void)sizeof(aff);
+    const int lane = threadIdx.x & 31;
+    jac acc = lane < MSM_WINDOWS ? jac_load<NL>(win, MSM_WINDOWS, lane) : jac_infinity<C>();
     acc = warp_sum_points<C>(acc, lane);
     if (lane == 0) {
         const typename C::Fp f{};
@@ -1043,25 +1155,29 @@ k_msm_red_combine(const uint32_t* __restrict__ wsum, uint32_t* __restrict__ ox, 
 
 // ---------------------------------------------------------------- host side
 struct MsmPlan {
-    size_t pairs, sort_temp, total;
+    size_t pairs, region, sort_temp, total;
     size_t slices;
-    size_t off_keys, off_vals, off_keys2, off_vals2, off_buckets, off_edge, off_edge_key, off_parts, off_marg, off_wsum, off_temp;
+    size_t off_keys, off_vals, off_keys2, off_vals2, off_buckets, off_edge, off_edge_key, off_parts, off_marg, off_wsum, off_win, off_temp;
     size_t off_rec, off_slots, off_sinf, off_starts, off_pref, off_others, off_totals;
     size_t max_tiles;
 };
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 // 0 auto (= 2), 1 mixed-Jacobian slices, 2 batch-affine tree with three launches per level,
-// 3 batch-affine tree with one launch per level (inversion inside the block)
+// 3 batch-affine tree with one launch per level (inversion inside the block),
+// 4 / 5 batch-affine tree, all levels fused into one launch (16 / 8 level-0 joins per thread)
 static int g_msm_form = 0;
 void set_msm_form(int form) { g_msm_form = form; }
 static bool msm_affine() { return g_msm_form != 1; }
 constexpr int MSM_TREE_KMIN = 2;  // fewest joins per thread any level uses
+constexpr int MSM_GROUPS = 4;     // most window groups of the two-stream pipeline (scratch is sized for it)
+constexpr int MSM_GROUPS_DEFAULT = 2;  // measured: 4.02 / 3.80 / 4.41 ms with 1 / 2 / 4 groups (secp256k1, 2^20)
 
 static MsmPlan msm_plan(size_t n, int limbs) {
     MsmPlan p{};
     const size_t jb = (size_t)12 * limbs, rb = (size_t)8 * limbs, fb = (size_t)4 * limbs;  // bytes: Jacobian point, record, element
-    p.pairs = n * MSM_WINDOWS;
+    p.region = (n + ((size_t)1 << MSM_TREE_LEVELS) - 1) >> MSM_TREE_LEVELS << MSM_TREE_LEVELS;  // positions per window
+    p.pairs = p.region * MSM_WINDOWS;
     p.sort_temp = (size_t)2 * 4 * MSM_NB + 4 * 1024;  // bucket counts | scatter cursors | block totals of the scan
     size_t at = 0;
     auto take = [&](size_t bytes) { size_t o = at; at += align256(bytes); return o; };
@@ -1073,6 +1189,7 @@ static MsmPlan msm_plan(size_t n, int limbs) {
     p.off_parts = take(jb * MSM_RED_PARTS);
     p.off_marg = take(jb * MSM_WINDOWS * 3 * 32);
     p.off_wsum = take(jb * MSM_WINDOWS * 4);
+    p.off_win = take(jb * MSM_WINDOWS);
     p.off_temp = take(p.sort_temp);
     p.off_starts = take((size_t)4 * MSM_NB);
     // the two accumulation forms never run in the same call: their scratch overlaps
@@ -1086,9 +1203,10 @@ static MsmPlan msm_plan(size_t n, int limbs) {
     p.off_sinf = take(p.pairs);
     const size_t joins0 = (p.pairs + 1) / 2;
     p.off_pref = take(fb * joins0);
-    p.max_tiles = (joins0 + (size_t)MSM_TREE_THREADS * MSM_TREE_KMIN - 1) / ((size_t)MSM_TREE_THREADS * MSM_TREE_KMIN);
+    // tiles of the thinnest level, one rounding tile per window group; totals | inverses per group
+    p.max_tiles = (joins0 + (size_t)MSM_TREE_THREADS * MSM_TREE_KMIN - 1) / ((size_t)MSM_TREE_THREADS * MSM_TREE_KMIN) + 2 * MSM_GROUPS;
     p.off_others = take(fb * MSM_TREE_THREADS * p.max_tiles);
-    p.off_totals = take(2 * fb * (p.max_tiles + 64));
+    p.off_totals = take(2 * fb * (p.max_tiles + 64 * (MSM_GROUPS + 1)));
     p.total = at > end_jac ? at : end_jac;
     return p;
 }
@@ -1150,6 +1268,19 @@ static cudaError_t launch_tree(int curve, size_t m, int level, const TreeBufs& b
     return cudaGetLastError();
 }
 
+template <class C, int K0>
+static cudaError_t launch_tree_fused(size_t m, const TreeBufs& b, cudaStream_t s) {
+    constexpr int NL = C::Fp::N;
+    const size_t per_block = (size_t)2 * MSM_TREE_THREADS * K0;  // positions
+    const unsigned blocks = (unsigned)((m + per_block - 1) / per_block);
+    const size_t smem = ((size_t)K0 * NL * MSM_TREE_THREADS + 2 * NL * (MSM_TREE_THREADS / 32)) * sizeof(uint32_t);
+    if (smem > 48 * 1024)
+        if (cudaError_t e = cudaFuncSetAttribute(k_msm_tree_fused<C, K0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
+            return e;
+    k_msm_tree_fused<C, K0><<<blocks, MSM_TREE_THREADS, smem, s>>>(m, b.keys, b.vals, b.rec, b.slots, b.sinf);
+    return cudaGetLastError();
+}
+
 template <class C, class CI = C>
 static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px, const uint32_t* py,
                            const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
@@ -1172,8 +1303,8 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
     k_msm_hist<C><<<bpw, 256, 0, s>>>(n, scalars, pinf, counts);
     uint32_t* block_totals = cursor + MSM_NB;
     k_msm_scan_blocks<<<MSM_SCAN_BLOCKS, MSM_SCAN_THREADS, 0, s>>>(counts, starts, block_totals);
-    k_msm_scan_tops<<<1, MSM_SCAN_THREADS, 0, s>>>(block_totals, keys2, p.pairs);
-    k_msm_scan_finish<<<MSM_SCAN_BLOCKS, MSM_SCAN_THREADS, 0, s>>>(counts, block_totals, starts, cursor);
+    k_msm_scan_tops<<<1, MSM_SCAN_THREADS, 0, s>>>(block_totals, (uint32_t)p.region);
+    k_msm_scan_finish<<<MSM_SCAN_BLOCKS, MSM_SCAN_THREADS, 0, s>>>(counts, block_totals, starts, cursor, keys2, (uint32_t)p.region);
     k_msm_scatter<C><<<bpw * MSM_WINDOWS, 256, 0, s>>>(n, scalars, pinf, cursor, keys2, vals2);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // digits and sort need the scalars (and the infinity mask) only: a host caller uploads the
@@ -1182,32 +1313,67 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
     if (msm_affine()) {
         uint4 *rec = (uint4*)(base + p.off_rec), *slots = (uint4*)(base + p.off_slots);
         uint8_t* sinf = base + p.off_sinf;
-        const size_t m = p.pairs;
         k_msm_aos<C, CI><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, px, py, rec);
-        // K joins per thread; thin levels take fewer per thread so that the chip stays filled
+        uint32_t* win = (uint32_t*)(base + p.off_win);
+        const bool fused = g_msm_form == 4 || g_msm_form == 5;
         const bool split = g_msm_form != 3;
-        TreeBufs tb{keys2, vals2, rec, slots, sinf, (uint4*)(base + p.off_pref), (uint4*)(base + p.off_others),
-                    (uint32_t*)(base + p.off_totals), p.max_tiles, aux.stream, aux.fork, aux.join};
-        // joins per thread: as many as keep >= ~8 blocks per SM in flight (the scan share is 14 / K
-        // products per join).  The single-launch form parks prefixes in shared memory: K <= 8.
-        const size_t fill = (size_t)148 * 8 * MSM_TREE_THREADS;
-        const size_t joins0 = (m + 1) / 2;
-        if (split && joins0 >= 16 * fill) e = launch_tree<CI, 16, true>(curve, m, 0, tb, split, s);
-        else e = launch_tree<CI, 8, true>(curve, m, 0, tb, split, s);
-        if (e != cudaSuccess) return e;
-        for (int l = 1; l < MSM_TREE_LEVELS; ++l) {
-            const size_t joins = (m + ((size_t)2 << l) - 1) / ((size_t)2 << l);
-            if (split && joins >= 16 * fill) e = launch_tree<CI, 16, false>(curve, m, l, tb, split, s);
-            else if (joins >= 8 * fill) e = launch_tree<CI, 8, false>(curve, m, l, tb, split, s);
-            else if (joins >= 4 * fill) e = launch_tree<CI, 4, false>(curve, m, l, tb, split, s);
-            else e = launch_tree<CI, MSM_TREE_KMIN, false>(curve, m, l, tb, split, s);
-            if (e != cudaSuccess) return e;
+        // Window groups, highest windows first: a group is an independent sub-problem (its own
+        // region of the sorted pairs, its own buckets), so the groups alternate between two streams
+        // and the latency-bound tail of one -- thin tree levels, the totals' inversions, the
+        // marginal folds, the doubling chain of its shift (longest for the high windows) -- runs
+        // behind the wide tree levels of the next.
+        static const int groups_knob = [] { const char* v = getenv("GECC_MSM_GROUPS"); return v ? atoi(v) : 0; }();  // A/B timing
+        const int want_groups = groups_knob >= 1 && groups_knob <= MSM_GROUPS ? groups_knob : MSM_GROUPS_DEFAULT;
+        const int G = (aux.stream && aux.fork && aux.join && split && !fused && n >= ((size_t)1 << 16)) ? want_groups : 1;
+        if (G > 1) {
+            if ((e = cudaEventRecord(aux.fork, s)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(aux.stream, aux.fork, 0)) != cudaSuccess) return e;
         }
-        k_msm_red_parts<CI><<<(MSM_RED_PARTS + 127) / 128, 128, 0, s>>>(m, keys2, starts, slots, sinf, parts);
-        k_msm_red_fold<CI><<<(MSM_WINDOWS * 3 * 32 * 32 + 127) / 128, 128, 0, s>>>(parts, marg);
-        k_msm_red_weighted<CI><<<(MSM_WINDOWS * 3 * 32 + 127) / 128, 128, 0, s>>>(marg, wsum);
-        k_msm_red_combine<CI, C><<<1, MSM_COMBINE_THREADS, 0, s>>>(wsum, ox, oy, oinf);
-        *launches = 6 + (split ? 3 : 1) * MSM_TREE_LEVELS * (split ? 2 : 1) + 4;  // sort (5) + records + tree + reduction
+        size_t tile_base = 0;
+        for (int g = 0; g < G; ++g) {
+            const uint32_t w1 = (uint32_t)(MSM_WINDOWS * (G - g) / G), w0 = (uint32_t)(MSM_WINDOWS * (G - g - 1) / G);
+            const size_t pos0 = (size_t)w0 * p.region, m = (size_t)(w1 - w0) * p.region;
+            cudaStream_t hs = (g & 1) ? aux.stream : s;
+            const size_t tiles_max = ((m + 1) / 2 + (size_t)MSM_TREE_THREADS * MSM_TREE_KMIN - 1) / ((size_t)MSM_TREE_THREADS * MSM_TREE_KMIN) + 1;
+            TreeBufs tb{keys2 + pos0, vals2 + pos0, rec, slots + (NL / 2) * pos0, sinf + pos0,
+                        (uint4*)(base + p.off_pref) + (NL / 4) * (pos0 / 2),
+                        (uint4*)(base + p.off_others) + (size_t)(NL / 4) * MSM_TREE_THREADS * tile_base,
+                        (uint32_t*)(base + p.off_totals) + (size_t)2 * NL * (tile_base + (size_t)64 * g), tiles_max,
+                        G > 1 ? nullptr : aux.stream, aux.fork, aux.join};
+            tile_base += tiles_max;
+            // K joins per thread: as many as keep >= ~8 blocks per SM in flight (the scan share is
+            // 14 / K products per join); thin levels take fewer so that the chip stays filled.  The
+            // single-launch form parks prefixes in shared memory: K <= 8.
+            const size_t fill = (size_t)148 * (G > 1 ? 4 : 8) * MSM_TREE_THREADS;  // two groups share the chip
+            const size_t joins0 = (m + 1) / 2;
+            if (fused) {
+                e = g_msm_form == 4 ? launch_tree_fused<CI, 16>(m, tb, hs) : launch_tree_fused<CI, 8>(m, tb, hs);
+            } else {
+                if (split && joins0 >= 16 * fill) e = launch_tree<CI, 16, true>(curve, m, 0, tb, split, hs);
+                else e = launch_tree<CI, 8, true>(curve, m, 0, tb, split, hs);
+                for (int l = 1; l < MSM_TREE_LEVELS && e == cudaSuccess; ++l) {
+                    const size_t joins = (m + ((size_t)2 << l) - 1) / ((size_t)2 << l);
+                    if (split && joins >= 16 * fill) e = launch_tree<CI, 16, false>(curve, m, l, tb, split, hs);
+                    else if (joins >= 8 * fill) e = launch_tree<CI, 8, false>(curve, m, l, tb, split, hs);
+                    else if (joins >= 4 * fill) e = launch_tree<CI, 4, false>(curve, m, l, tb, split, hs);
+                    else e = launch_tree<CI, MSM_TREE_KMIN, false>(curve, m, l, tb, split, hs);
+                }
+            }
+            if (e != cudaSuccess) return e;
+            const uint32_t nw = w1 - w0;
+            k_msm_red_parts<CI><<<nw * 96, 128, 0, hs>>>(p.pairs, keys2, starts, slots, sinf, parts, w0);
+            k_msm_red_fold<CI><<<nw * 24, 128, 0, hs>>>(parts, marg, w0);
+            k_msm_red_weighted<CI><<<(nw * 3 + 3) / 4, 128, 0, hs>>>(marg, wsum, w0, w1);
+            k_msm_red_shift<CI><<<1, (nw * 4 + 31) / 32 * 32, 0, hs>>>(wsum, win, w0, w1);
+            if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        }
+        if (G > 1) {
+            if ((e = cudaEventRecord(aux.join, aux.stream)) != cudaSuccess) return e;
+            if ((e = cudaStreamWaitEvent(s, aux.join, 0)) != cudaSuccess) return e;
+        }
+        k_msm_red_final<CI, C><<<1, 32, 0, s>>>(win, ox, oy, oinf);
+        const int per_level = fused ? 0 : (split ? 3 : 1) * (G > 1 || !aux.stream ? 1 : 2);
+        *launches = 6 + G * ((fused ? 1 : per_level * MSM_TREE_LEVELS) + 4) + 1;  // sort (5) + records + groups x (tree + reduction) + final
         return cudaGetLastError();
     } else {
         uint32_t *edge = (uint32_t*)(base + p.off_edge), *edge_key = (uint32_t*)(base + p.off_edge_key);

@@ -41,6 +41,8 @@ int field_op_t(const F& f, int op, size_t n, const uint32_t* a, const uint32_t* 
             case 10: r = fe_mul8(f, x); break;          // 8x
             case 11: r = fe_inv_var(f, x); break;       // variable-time safegcd, Montgomery in/out
             case 12: r = safegcd_inverse_var(f, x); break;  // variable-time safegcd, plain in/out
+            case 13: r = safegcd_inverse_sched<false>(f, x); break;  // latency-scheduled, plain in/out
+            case 14: r = safegcd_inverse_sched<true>(f, x); break;   // + early exit
             default: return 1;
         }
         col_set(out, n, i, r);

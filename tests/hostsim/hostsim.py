@@ -28,7 +28,7 @@ def _p(a):
 
 
 FIELD_IDS = {(1, 0): 0, (1, 1): 1, (0, 0): 2, (0, 1): 3}  # (curve, which) -> hostsim field id
-OPS = dict(mont_mul=0, mod_add=1, mod_sub=2, to_mont=3, from_mont=4, mod_inv=5, sqr=6, inv_safegcd=7, inv_plain=8, dbl=9, mul8=10, inv_var=11, inv_var_plain=12)
+OPS = dict(mont_mul=0, mod_add=1, mod_sub=2, to_mont=3, from_mont=4, mod_inv=5, sqr=6, inv_safegcd=7, inv_plain=8, dbl=9, mul8=10, inv_var=11, inv_var_plain=12, inv_sched_plain=13, inv_sched_exit_plain=14)
 
 
 SECP_LAZY_CURVE = 2   # secp256k1 in the lazy plain representation (ECDSA kernels)

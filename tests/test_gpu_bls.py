@@ -70,6 +70,7 @@ def test_field12_kernels(env):
     assert ints(ctx.field_op(0, "from_mont", A)) == [x * RINV % q for x in a]
     want = [pow(x * RINV % q, -1, q) * R12 % q if x else 0 for x in a]
     assert ints(ctx.field_op(0, "mod_inv", A)) == want                      # safegcd, 13 x 30-bit limbs
+    assert ints(ctx.field_op(0, "mod_inv_warp", A)) == want                 # the same by a whole warp per element
     assert ints(ctx.field_op(0, "mod_inv_fermat", cols(a[:64]))) == want[:64]
     # batch inversion (Montgomery's trick, one inversion per block), zeros masked
     assert ints(ctx.batch_invert(0, A)) == want
@@ -101,7 +102,7 @@ def test_batch_padd_pdbl_g1(env):
     assert all(E.on_curve(B, p) for p in got)
 
 
-@pytest.mark.parametrize("form", ["affine", "jacobian"])
+@pytest.mark.parametrize("form", ["affine", "fused16", "fused8", "jacobian"])
 def test_msm_g1(env, form):
     B, ctx = env.B, env.ctx
     gecc.set_msm_form(form)

@@ -50,6 +50,10 @@ def test_field_random_vs_oracle(ctxs, cid, which):
     m = 512
     a2 = np.ascontiguousarray(a[:, :m])
     assert (ctxs[cid].field_op(which, "mod_inv", a2) == O.field_op(cid, which, "mod_inv", a2)).all()
+    # the warp-cooperative inversion (the one shared inversion of the block-level Montgomery trick),
+    # ragged count so that the last warp is partly out of range
+    a3 = np.ascontiguousarray(a[:, :m + 13])
+    assert (ctxs[cid].field_op(which, "mod_inv_warp", a3) == O.field_op(cid, which, "mod_inv", a3)).all()
 
 
 def test_field_properties_large(ctxs):

@@ -21,7 +21,7 @@ def ctxs():
         x.close()
 
 
-@pytest.fixture(params=["affine", "affine1", "jacobian"], autouse=True)
+@pytest.fixture(params=["affine", "affine1", "fused16", "fused8", "jacobian"], autouse=True)
 def msm_form(request):
     """every test runs with both bucket-accumulation forms (results must be identical)"""
     gecc.set_msm_form(request.param)

@@ -60,6 +60,9 @@ def test_hostsim_inverse_and_glv():
             # the variable-time form (block totals of Montgomery's trick) gives the same residues
             assert (H.field_op(cid, which, "inv_var", a) == O.field_op(cid, which, "mod_inv", a)).all()
             assert O.cols_to_ints(H.field_op(cid, which, "inv_var_plain", a)) == plain
+            # the software-pipelined schedule of the same rounds, with and without the early exit
+            assert O.cols_to_ints(H.field_op(cid, which, "inv_sched_plain", a)) == plain
+            assert O.cols_to_ints(H.field_op(cid, which, "inv_sched_exit_plain", a)) == plain
     n = E.SECP256K1.n
     lam = 0x5363AD4CC05C30E0A5261C028812645A122E22EA20816678DF02967C1B23BD72
     ks = [0, 1, 2, n - 1, n - 2, lam, n - lam, (n - 1) // 2, 1 << 255] + [rng.randrange(n) for _ in range(5000)]

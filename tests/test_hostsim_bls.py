@@ -51,6 +51,8 @@ def test_field12_ops_vs_python_ints(B):
     want_mont = [pow(x * rinv % q, -1, q) * R12 % q if x else 0 for x in a]
     assert ints(H.field_op(0, 0, "inv_safegcd", A, field_id=f)) == want_mont
     assert ints(H.field_op(0, 0, "inv_var_plain", A, field_id=f)) == want_plain
+    assert ints(H.field_op(0, 0, "inv_sched_plain", A, field_id=f)) == want_plain
+    assert ints(H.field_op(0, 0, "inv_sched_exit_plain", A, field_id=f)) == want_plain
     assert ints(H.field_op(0, 0, "inv_var", A, field_id=f)) == want_mont
     small = cols(a[:40])
     assert ints(H.field_op(0, 0, "mod_inv", small, field_id=f)) == want_mont[:40]

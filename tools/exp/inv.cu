@@ -16,6 +16,10 @@ __global__ void k(uint32_t seed, uint64_t* cycles, uint32_t* out) {
     long long t0 = clock64();
     if (MODE == 0) r = safegcd_inverse(f, x);
     else if (MODE == 4) r = safegcd_inverse_var(f, x);
+    else if (MODE == 5) r = safegcd_inverse_sched<false>(f, x);
+    else if (MODE == 6) r = safegcd_inverse_sched<true>(f, x);
+    else if (MODE == 7) r = safegcd_inverse_warp<false>(f, x);
+    else if (MODE == 8) r = safegcd_inverse_warp<true>(f, x);
     else if (MODE == 1) r = fe_inv_fermat(f, x);
     else if (MODE == 2) r = fe_mul(f, x, x);
     else {
@@ -25,7 +29,7 @@ __global__ void k(uint32_t seed, uint64_t* cycles, uint32_t* out) {
     }
     long long t1 = clock64();
     for (int k = 0; k < 8; ++k) out[threadIdx.x * 8 + k] = r.w[k];
-    if (MODE == 4) {  // cross-check against the plain rounds
+    if (MODE >= 4) {  // cross-check against the plain rounds
         fel<F> w = safegcd_inverse(f, x);
         for (int k = 0; k < F::N; ++k) if (w.w[k] != r.w[k]) out[0] = 0xDEADBEEF, cycles[1] = 1;
     }
@@ -53,6 +57,15 @@ int main() {
     run<SecpP, 0>("safegcd SecpP", 32);
     run<SecpP, 4>("safegcd var SecpP", 32);
     run<SecpPL, 4>("safegcd var lazy", 32);
+    run<SecpP, 7>("safegcd warp-coop SecpP", 32);
+    run<SecpP, 8>("safegcd warp-coop var SecpP", 32);
+    run<Bls381P, 8>("safegcd warp-coop var BLS381", 32);
+    run<SecpPL, 7>("safegcd warp-coop lazy", 32);
+    run<Bls381P, 7>("safegcd warp-coop BLS381", 32);
+    run<SecpP, 5>("safegcd sched SecpP", 32);
+    run<SecpP, 6>("safegcd sched+exit SecpP", 32);
+    run<Bls381P, 5>("safegcd sched BLS381", 32);
+    run<Bls381P, 6>("safegcd sched+exit BLS381", 32);
     run<Bls381P, 0>("safegcd BLS381", 32);
     run<Bls381P, 4>("safegcd var BLS381", 32);
     run<SecpP, 0>("safegcd SecpP", 1);
