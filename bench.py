@@ -802,11 +802,20 @@ def _ncu_traffic(wl, log2n=20):
     try:
         tot, names = 0.0, set()
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        inside = wl != "msm"   # the MSM capture is a window of launches: one MSM = k_msm_hist .. k_msm_red_final
+        done = False
         with open(os.path.join(ROOT, "profiles", name + "_metrics.csv")) as f:
             for r in csv.reader(f):
-                if len(r) >= 4 and kernel in r[0] and r[1] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                if len(r) < 4 or kernel not in r[0] or done:
+                    continue
+                if wl == "msm":
+                    if not inside and "k_msm_hist" in r[0]:
+                        inside = True
+                if inside and r[1] in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
                     tot += float(r[3]) * scale.get(r[2], 1)
                     names.add(r[0])
+                    if wl == "msm" and "k_msm_red_final" in r[0] and r[1] == "dram__bytes_write.sum":
+                        done = True   # the closing launch's last DRAM row (tools/ncu_summary.py keeps the report's metric order)
         return {"bytes_per_launch": tot, "kernels": sorted(names), "source": f"profiles/{name}_metrics.csv"} if tot else None
     except OSError:
         return None

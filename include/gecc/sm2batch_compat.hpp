@@ -179,9 +179,28 @@ private:
     sm2b_ctx* ctx_;
 };
 
-struct FieldParams {  // handle: which field of which engine
+using MontElement = Limbs256;  // a field element in Montgomery form (field.hpp)
+
+struct FieldParams {  // handle: which field of which engine, or a runtime modulus (make)
     const Engine* engine = nullptr;
     gecc_field which = GECC_FIELD_P;
+    // runtime modulus: FieldParams::make(q) (field.hpp / field.cpp:159-179).  The constants travel
+    // with every call (gecc_*_rt); `engine` only names the device that runs it.
+    std::shared_ptr<gecc_field_params> runtime;
+    Limbs256 q{}, r{}, r2{};
+
+    static FieldParams make(const Limbs256& modulus, const Engine* on = nullptr) {
+        FieldParams f;
+        f.runtime = std::make_shared<gecc_field_params>();
+        if (gecc_field_params_make(modulus.w.data(), f.runtime.get()) != SM2B_OK)
+            throw std::invalid_argument("modulus must be odd");  // field.cpp:160
+        f.engine = on;
+        f.q = modulus;
+        gecc_field_params_get(f.runtime.get(), 1, f.r.w.data());
+        gecc_field_params_get(f.runtime.get(), 2, f.r2.w.data());
+        return f;
+    }
+    bool is_runtime() const { return runtime != nullptr; }
 };
 
 struct CurveParams {
@@ -194,6 +213,28 @@ struct CurveParams {
 
     static const CurveParams& sm2() { return instance(GECC_CURVE_SM2); }
     static const CurveParams& secp256k1() { return instance(GECC_CURVE_SECP256K1); }
+
+    // A user curve y^2 = x^3 + a x + b over F_q (curve.hpp:51-59: CurveParams is a plain aggregate
+    // of a base field and the Montgomery-form coefficients).  batch_invert / batch_padd /
+    // batch_pdbl serve it through the runtime-modulus kernels on the device of `like`'s engine;
+    // the fixed-base, ECDSA and MSM layers need a compiled-in curve.
+    MontElement a{}, b{};
+    bool custom = false;
+    static CurveParams user(const FieldParams& base_field_rt, const Limbs256& a_mont, const Limbs256& b_mont,
+                            const CurveParams& like = sm2()) {
+        if (!base_field_rt.is_runtime()) throw std::invalid_argument("CurveParams::user needs FieldParams::make(q)");
+        CurveParams c;
+        c.engine = like.engine;
+        c.base = base_field_rt;
+        c.base.engine = c.engine.get();
+        c.order = c.base;
+        c.base_field = c.order_field = nullptr;  // (the object is copied by value: use field())
+        c.a = a_mont;
+        c.b = b_mont;
+        c.custom = true;
+        return c;
+    }
+    const FieldParams& field() const { return base; }
 
 private:
     static const CurveParams& instance(gecc_curve id) {
@@ -253,6 +294,11 @@ inline BatchColumnBuffer batch_invert(const BatchColumnBuffer& inputs, const Fie
                                       const LanePlan& plan, WorkerPool* = nullptr) {
     if (plan.total != inputs.n) throw std::invalid_argument("batch_invert: plan does not match batch size");
     BatchColumnBuffer out = BatchColumnBuffer::make(inputs.n);
+    if (field.is_runtime()) {
+        const Engine* e = field.engine ? field.engine : CurveParams::sm2().engine.get();
+        e->check(gecc_batch_invert_rt(e->ctx(), field.runtime.get(), inputs.n, inputs.data(), out.data()), "batch_invert");
+        return out;
+    }
     field.engine->check(gecc_batch_invert(field.engine->ctx(), field.which, inputs.n, inputs.data(), out.data()),
                         "batch_invert");
     return out;
@@ -263,6 +309,13 @@ inline BatchPointBuffer batch_padd(const CurveParams& c, const BatchPointBuffer&
     if (p.n != t.n) throw std::invalid_argument("batch_padd: buffer sizes differ");
     if (plan.total != p.n) throw std::invalid_argument("batch_padd: plan does not match batch");
     BatchPointBuffer out = BatchPointBuffer::make(p.n);
+    if (c.custom) {
+        c.engine->check(gecc_batch_padd_rt(c.engine->ctx(), c.base.runtime.get(), c.a.w.data(), p.n, p.x.data(), p.y.data(),
+                                           p.infinity_mask.data(), t.x.data(), t.y.data(), t.infinity_mask.data(),
+                                           out.x.data(), out.y.data(), out.infinity_mask.data()),
+                        "batch_padd");
+        return out;
+    }
     c.engine->check(gecc_batch_padd(c.engine->ctx(), p.n, p.x.data(), p.y.data(), p.infinity_mask.data(), t.x.data(),
                                     t.y.data(), t.infinity_mask.data(), out.x.data(), out.y.data(),
                                     out.infinity_mask.data()),
@@ -274,6 +327,12 @@ inline BatchPointBuffer batch_pdbl(const CurveParams& c, const BatchPointBuffer&
                                    WorkerPool* = nullptr) {
     if (plan.total != p.n) throw std::invalid_argument("batch_pdbl: plan does not match batch");
     BatchPointBuffer out = BatchPointBuffer::make(p.n);
+    if (c.custom) {
+        c.engine->check(gecc_batch_pdbl_rt(c.engine->ctx(), c.base.runtime.get(), c.a.w.data(), p.n, p.x.data(), p.y.data(),
+                                           p.infinity_mask.data(), out.x.data(), out.y.data(), out.infinity_mask.data()),
+                        "batch_pdbl");
+        return out;
+    }
     c.engine->check(gecc_batch_pdbl(c.engine->ctx(), p.n, p.x.data(), p.y.data(), p.infinity_mask.data(),
                                     out.x.data(), out.y.data(), out.infinity_mask.data()),
                     "batch_pdbl");

@@ -220,6 +220,31 @@ sm2b_status gecc_comm_unique_id(uint8_t id[GECC_COMM_ID_BYTES]);
 sm2b_status gecc_comm_init_rank(sm2b_ctx* ctx, int nranks, int rank, const uint8_t id[GECC_COMM_ID_BYTES]);
 sm2b_status gecc_msm_combine_dev(sm2b_ctx* ctx, uint32_t* x, uint32_t* y, uint8_t* inf);
 
+/* ---- runtime moduli and user curves (the reference's C++ layer is generic in both:
+ * FieldParams::make(q), field.cpp:159-179; CurveParams {base_field, a, b}, curve.hpp:51-59;
+ * batch_invert / batch_padd / batch_pdbl take them as arguments, batch_invert.hpp:61,
+ * batch_point.hpp:47-60).  Elements are 8-limb column buffers, Montgomery form with R = 2^256.
+ * Device contexts only; any context serves (the constants travel with the call). */
+typedef struct gecc_field_params { uint32_t w[64]; } gecc_field_params; /* opaque; fill with gecc_field_params_make */
+/* FieldParams::make(q): q odd and >= 3, else SM2B_ERROR_INVALID_ARGUMENT ("modulus must be odd").
+ * Inversion assumes q prime, as the reference's does. */
+sm2b_status gecc_field_params_make(const uint32_t q[8], gecc_field_params* out);
+/* which: 0 q, 1 R = 2^256 mod q, 2 R^2 mod q, 3 R^3 mod q (FieldParams::r / r2) */
+sm2b_status gecc_field_params_get(const gecc_field_params* params, int which, uint32_t out[8]);
+/* op: GECC_OP_MONT_MUL .. GECC_OP_MOD_INV_FERMAT on the runtime field */
+sm2b_status gecc_field_op_rt(sm2b_ctx* ctx, const gecc_field_params* params, gecc_field_opcode op, size_t n,
+                             const uint32_t* a, const uint32_t* b, uint32_t* out);
+sm2b_status gecc_batch_invert_rt(sm2b_ctx* ctx, const gecc_field_params* params, size_t n, const uint32_t* in,
+                                 uint32_t* out);
+/* batch_padd / batch_pdbl on y^2 = x^3 + a x + b over F_q; a_mont = a R mod q (b is not needed by
+ * the formulas).  Same complete pair classification as gecc_batch_padd. */
+sm2b_status gecc_batch_padd_rt(sm2b_ctx* ctx, const gecc_field_params* params, const uint32_t a_mont[8], size_t n,
+                               const uint32_t* px, const uint32_t* py, const uint8_t* pinf, const uint32_t* tx,
+                               const uint32_t* ty, const uint8_t* tinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf);
+sm2b_status gecc_batch_pdbl_rt(sm2b_ctx* ctx, const gecc_field_params* params, const uint32_t a_mont[8], size_t n,
+                               const uint32_t* px, const uint32_t* py, const uint8_t* pinf, uint32_t* ox, uint32_t* oy,
+                               uint8_t* oinf);
+
 /* Element-wise field operation on column buffers (host pointers). */
 sm2b_status gecc_field_op(sm2b_ctx* ctx, gecc_field field, gecc_field_opcode op, size_t n,
                           const uint32_t* a, const uint32_t* b, uint32_t* out);

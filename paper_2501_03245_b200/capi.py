@@ -68,6 +68,12 @@ def lib():
         l.gecc_last_error.argtypes = [C.c_void_p]
         l.gecc_kernel_launches.restype = C.c_uint64
         l.gecc_kernel_launches.argtypes = [C.c_void_p]
+        l.gecc_field_params_make.argtypes = [C.c_void_p, C.c_void_p]
+        l.gecc_field_params_get.argtypes = [C.c_void_p, C.c_int, C.c_void_p]
+        l.gecc_field_op_rt.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_size_t, C.c_void_p, C.c_void_p, C.c_void_p]
+        l.gecc_batch_invert_rt.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]
+        l.gecc_batch_padd_rt.argtypes = [C.c_void_p] * 3 + [C.c_size_t] + [C.c_void_p] * 9
+        l.gecc_batch_pdbl_rt.argtypes = [C.c_void_p] * 3 + [C.c_size_t] + [C.c_void_p] * 6
         l.gecc_set_batch_form.argtypes = [C.c_int]
         l.gecc_set_batch_form.restype = None
         l.gecc_set_msm_form.argtypes = [C.c_int]
@@ -96,6 +102,26 @@ MSM_FORMS = {"auto": 0, "jacobian": 1, "affine": 2, "affine1": 3, "fused16": 4, 
 def set_msm_form(form: str):
     """Pins gecc_msm's bucket accumulation (gecc_set_msm_form): auto | jacobian | affine."""
     lib().gecc_set_msm_form(MSM_FORMS[form])
+
+
+def field_params_make(q: int):
+    """FieldParams::make(q) (gecc_field_params_make): the opaque parameter block for the *_rt entry
+    points, or ValueError for an even / too small modulus (no GPU needed)."""
+    qa = np.frombuffer(int(q).to_bytes(32, "little"), np.uint32).copy()
+    out = np.zeros(64, np.uint32)
+    rc = lib().gecc_field_params_make(qa.ctypes.data, out.ctypes.data)
+    if rc != 0:
+        raise ValueError(f"gecc_field_params_make rc={rc}")
+    return out
+
+
+def field_params_get(params, which: int) -> int:
+    """0 q, 1 R, 2 R^2, 3 R^3 of a parameter block"""
+    out = np.zeros(8, np.uint32)
+    rc = lib().gecc_field_params_get(params.ctypes.data, which, out.ctypes.data)
+    if rc != 0:
+        raise ValueError(f"gecc_field_params_get rc={rc}")
+    return int.from_bytes(out.tobytes(), "little")
 
 
 def cols_from_ints(vals, limbs: int = 8) -> np.ndarray:
@@ -298,6 +324,52 @@ class Context:
                         modeled_cost=rep.modeled_cost, equivalence_checked=rep.equivalence_checked)
 
     # -- batch layer (host column buffers)
+    # ---- runtime moduli / user curves (gecc_*_rt): params from field_params_make(q)
+    def field_op_rt(self, params, op: str, a: np.ndarray, b: np.ndarray | None = None):
+        n = a.shape[1]
+        _need_cols(a, 8, n, "field_op_rt a")
+        if b is not None:
+            _need_cols(b, 8, n, "field_op_rt b")
+        out = np.zeros((8, n), np.uint32)
+        rc = self.l.gecc_field_op_rt(self.h, params.ctypes.data, FIELD_OPS[op], C.c_size_t(n), _vp(a), _vp(b), _vp(out))
+        if self._check(rc, "gecc_field_op_rt"):
+            raise ValueError(f"gecc_field_op_rt rc={rc}")
+        return out
+
+    def batch_invert_rt(self, params, a: np.ndarray):
+        n = a.shape[1]
+        _need_cols(a, 8, n, "batch_invert_rt")
+        out = np.zeros((8, n), np.uint32)
+        rc = self.l.gecc_batch_invert_rt(self.h, params.ctypes.data, C.c_size_t(n), _vp(a), _vp(out))
+        if self._check(rc, "gecc_batch_invert_rt"):
+            raise ValueError(f"gecc_batch_invert_rt rc={rc}")
+        return out
+
+    def batch_padd_rt(self, params, a_mont: np.ndarray, P, T):
+        n = P[0].shape[1]
+        for X in (P, T):
+            _need_cols(X[0], 8, n, "batch_padd_rt x")
+            _need_cols(X[1], 8, n, "batch_padd_rt y")
+            _need_mask(X[2], n, "batch_padd_rt infinity mask")
+        ox, oy, oi = np.zeros((8, n), np.uint32), np.zeros((8, n), np.uint32), np.zeros(n, np.uint8)
+        rc = self.l.gecc_batch_padd_rt(self.h, params.ctypes.data, a_mont.ctypes.data, C.c_size_t(n), _vp(P[0]), _vp(P[1]),
+                                       _vp(P[2]), _vp(T[0]), _vp(T[1]), _vp(T[2]), _vp(ox), _vp(oy), _vp(oi))
+        if self._check(rc, "gecc_batch_padd_rt"):
+            raise ValueError(f"gecc_batch_padd_rt rc={rc}")
+        return ox, oy, oi
+
+    def batch_pdbl_rt(self, params, a_mont: np.ndarray, P):
+        n = P[0].shape[1]
+        _need_cols(P[0], 8, n, "batch_pdbl_rt x")
+        _need_cols(P[1], 8, n, "batch_pdbl_rt y")
+        _need_mask(P[2], n, "batch_pdbl_rt infinity mask")
+        ox, oy, oi = np.zeros((8, n), np.uint32), np.zeros((8, n), np.uint32), np.zeros(n, np.uint8)
+        rc = self.l.gecc_batch_pdbl_rt(self.h, params.ctypes.data, a_mont.ctypes.data, C.c_size_t(n), _vp(P[0]), _vp(P[1]),
+                                       _vp(P[2]), _vp(ox), _vp(oy), _vp(oi))
+        if self._check(rc, "gecc_batch_pdbl_rt"):
+            raise ValueError(f"gecc_batch_pdbl_rt rc={rc}")
+        return ox, oy, oi
+
     def batch_invert(self, field: int, a: np.ndarray):
         n = a.shape[1]
         _need_cols(a, self.limbs if field == 0 else 8, n, "batch_invert")

@@ -107,6 +107,27 @@ static void run(const CurveParams& C, int curve_id) {
     go_pmul_serial(curve_id, n, kc.data(), ts.x.data(), ts.y.data(), ts.infinity_mask.data(), ser.x.data(),
                    ser.y.data(), ser.infinity_mask.data());
     CHECK(same(C, up, ser));
+    // the same curve given at run time: FieldParams::make(q) + CurveParams::user(field, a, b)
+    // (field.cpp:159-179, curve.hpp:51-59) must give the compiled-in kernels' results
+    {
+        Limbs256 q{}, a_mont{}, b_mont{}, gx{}, gy{}, r{}, r2{};
+        go_field_params(curve_id, 0, q.w.data(), r.w.data(), r2.w.data());
+        FieldParams fq = FieldParams::make(q);
+        CHECK(fq.r == r);
+        CHECK(fq.r2 == r2);
+        go_curve_params(curve_id, a_mont.w.data(), b_mont.w.data(), gx.w.data(), gy.w.data());
+        CurveParams U = CurveParams::user(fq, a_mont, b_mont, C);
+        CHECK(same(C, batch_padd(U, ps, ts, LanePlan::make(n, 4)), out));
+        CHECK(same(C, batch_pdbl(U, ps, LanePlan::make(n, 4)), dbl));
+        auto inv_rt = batch_invert(v, U.field(), LanePlan::make(40, 3));
+        CHECK(inv_rt.cols == want.cols);
+        bool even_threw = false;
+        Limbs256 even = q;
+        even.w[0] &= ~1u;
+        try { (void)FieldParams::make(even); }
+        catch (const std::invalid_argument&) { even_threw = true; }
+        CHECK(even_threw);
+    }
     AffinePoint m = msm(C, ks, ts), mw;
     std::uint8_t winf = 0;
     go_msm(curve_id, n, kc.data(), ts.x.data(), ts.y.data(), ts.infinity_mask.data(), mw.x.w.data(), mw.y.w.data(), &winf);

@@ -21,10 +21,10 @@ for leg in $LEGS; do
       $NCU --set full --import-source on -k regex:k_sign -s 3 -c 1 -f -o $OUT/${TAG}_sign \
         python bench.py --workload sign --steps 2 --warmup 3 --no-cpu-baseline > $OUT/${TAG}_sign.log 2>&1 ;;
     padd)
-      $NCU --set full --import-source on -k regex:'k_batch_padd|k_padd' -s 4 -c 3 -f -o $OUT/${TAG}_padd \
+      $NCU --set full --import-source on -k regex:'k_batch_padd|k_padd' -s 4 -c 4 -f -o $OUT/${TAG}_padd \
         python bench.py --workload padd --steps 2 --warmup 3 --no-cpu-baseline > $OUT/${TAG}_padd.log 2>&1 ;;
     padd16)
-      $NCU --set full --import-source on -k regex:'k_batch_padd|k_padd|k_batch_invert' -s 4 -c 3 -f -o $OUT/${TAG}_padd16 \
+      $NCU --set full --import-source on -k regex:'k_batch_padd|k_padd' -s 4 -c 1 -f -o $OUT/${TAG}_padd16 \
         python bench.py --workload padd --log2n 16 --steps 2 --warmup 3 --no-cpu-baseline > $OUT/${TAG}_padd16.log 2>&1 ;;
     msm)
       $NCU --set full --import-source on -k regex:k_msm -s 60 -c 60 -f -o $OUT/${TAG}_msm \
