@@ -256,9 +256,13 @@ GECC_HD jac fixed_base_mul_uniform(const fe& k_raw, const GTable<WG>& tab) {
 // `base` points at this lane's first word; consecutive words of one entry are
 // `stride` words apart (stride = blockDim.x in shared memory: conflict-free,
 // 1 on the host).
+template <class C>
+struct RowSrc;
 struct LaneTable {
     uint32_t* base;
     int stride;
+    template <class C>
+    GECC_HD RowSrc<C> row(int e, bool neg, bool endo) const;  // entry e as a row source (defined below)
     GECC_HD void store(int e, const aff& p) const {
 #if defined(__CUDA_ARCH__)
         if (stride == 1) {  // table in global memory, 64 B per entry, 16-byte aligned by construction
@@ -275,6 +279,23 @@ struct LaneTable {
             base[(size_t)(e * 16 + i) * stride] = p.x.w[i];
             base[(size_t)(e * 16 + 8 + i) * stride] = p.y.w[i];
         }
+    }
+    GECC_HD fe load_x(int e) const { return load_half(e, 0); }
+    GECC_HD fe load_y(int e) const { return load_half(e, 8); }
+    GECC_HD fe load_half(int e, int off) const {  // one coordinate of entry e
+        fe v;
+#if defined(__CUDA_ARCH__)
+        if (stride == 1) {
+            const uint4* q = reinterpret_cast<const uint4*>(base + e * 16 + off);
+            const uint4 a = q[0], b = q[1];
+            v.w[0] = a.x; v.w[1] = a.y; v.w[2] = a.z; v.w[3] = a.w;
+            v.w[4] = b.x; v.w[5] = b.y; v.w[6] = b.z; v.w[7] = b.w;
+            return v;
+        }
+#endif
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v.w[i] = base[(size_t)(e * 16 + off + i) * stride];
+        return v;
     }
     GECC_HD aff load(int e) const {
         aff p;
@@ -556,10 +577,256 @@ GECC_HD jac var_base_mul_uniform(const fe& k_raw, const LaneTable& tab) {
     return acc;
 }
 
+// ------------------------------------------------------------ accumulator at rest in shared memory
+// The verify ladder (132 doublings + ~80 mixed additions per signature) spends ~13 % of its
+// instructions moving registers around the two product calls and ~4 % spilling the accumulator:
+// every value that lives across a call has to be copied out of the argument registers.  Here the
+// accumulator and the formulas' temporaries REST in per-thread shared-memory slots (16-byte
+// granules, granule g of slot s of thread t at [(2 s + g) * stride + t]: conflict-free LDS.128 /
+// STS.128); an operand is loaded straight into the argument registers where it is consumed and a
+// result is stored straight from the return registers, so nothing is live across a call but
+// addresses.  Same formulas, same values as jac_dbl / jac_madd.
+struct PointSlots {
+    enum { SX = 0, SY, SZ, S1, S2, S3, S4, S5, COUNT };
+#if defined(__CUDA_ARCH__)
+    uint32_t addr;    // shared-window byte address of this thread's granule 0 of slot 0
+    uint32_t pitch;   // bytes between consecutive granules of one thread (16 * threads per block)
+    __device__ __forceinline__ fe ld(int s) const {
+        fe r;
+        const uint32_t a = addr + (uint32_t)(2 * s) * pitch;
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]) : "r"(a));
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(r.w[4]), "=r"(r.w[5]), "=r"(r.w[6]), "=r"(r.w[7]) : "r"(a + pitch));
+        return r;
+    }
+    __device__ __forceinline__ void st(int s, const fe& v) const {
+        const uint32_t a = addr + (uint32_t)(2 * s) * pitch;
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.w[0]), "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]) : "memory");
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a + pitch), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7]) : "memory");
+    }
+#else
+    fe* slots;  // COUNT elements (host-sim)
+    fe ld(int s) const { return slots[s]; }
+    void st(int s, const fe& v) const { slots[s] = v; }
+#endif
+    GECC_HD jac load_point() const { return jac{ld(SX), ld(SY), ld(SZ)}; }
+    GECC_HD void store_point(const jac& p) const {
+        st(SX, p.X);
+        st(SY, p.Y);
+        st(SZ, p.Z);
+    }
+};
+
+template <class C>
+GECC_HD_CALL void jac_dbl_slots(const PointSlots S) {
+    using P = PointSlots;
+    const typename C::Fp f{};
+    if constexpr (C::a_kind == A_ZERO) {  // dbl-2009-l, as jac_dbl
+        S.st(P::S1, fe_sqr(f, S.ld(P::SX)));                                   // A
+        S.st(P::S2, fe_sqr(f, S.ld(P::SY)));                                   // B
+        S.st(P::S3, fe_sqr(f, S.ld(P::S2)));                                   // C
+        {
+            const fe T = fe_sqr(f, fe_add(f, S.ld(P::SX), S.ld(P::S2)));
+            S.st(P::S4, fe_dbl(f, fe_sub(f, fe_sub(f, T, S.ld(P::S1)), S.ld(P::S3))));  // D
+        }
+        S.st(P::SZ, fe_dbl(f, fe_mul(f, S.ld(P::SY), S.ld(P::SZ))));           // Z3 = 2 Y Z
+        {
+            const fe A = S.ld(P::S1);
+            S.st(P::S1, fe_add(f, fe_dbl(f, A), A));                           // E = 3A
+        }
+        {
+            const fe F = fe_sqr(f, S.ld(P::S1));
+            S.st(P::SX, fe_sub(f, F, fe_dbl(f, S.ld(P::S4))));                 // X3 = F - 2D
+        }
+        {
+            const fe M = fe_mul(f, S.ld(P::S1), fe_sub(f, S.ld(P::S4), S.ld(P::SX)));
+            S.st(P::SY, fe_sub(f, M, fe_mul8(f, S.ld(P::S3))));                // Y3 = E (D - X3) - 8C
+        }
+    } else if constexpr (C::a_kind == A_MINUS3) {  // dbl-2001-b, as jac_dbl
+        S.st(P::S1, fe_sqr(f, S.ld(P::SZ)));                                   // delta
+        S.st(P::S2, fe_sqr(f, S.ld(P::SY)));                                   // gamma
+        S.st(P::S3, fe_mul(f, S.ld(P::SX), S.ld(P::S2)));                      // beta
+        {
+            const fe X = S.ld(P::SX), d = S.ld(P::S1);
+            const fe t = fe_mul(f, fe_sub(f, X, d), fe_add(f, X, d));
+            S.st(P::S4, fe_add(f, fe_dbl(f, t), t));                           // alpha
+        }
+        {
+            const fe q = fe_sqr(f, fe_add(f, S.ld(P::SY), S.ld(P::SZ)));
+            S.st(P::SZ, fe_sub(f, fe_sub(f, q, S.ld(P::S2)), S.ld(P::S1)));    // Z3 = (Y + Z)^2 - gamma - delta
+        }
+        {
+            const fe a2 = fe_sqr(f, S.ld(P::S4));
+            const fe beta4 = fe_dbl(f, fe_dbl(f, S.ld(P::S3)));
+            const fe X3 = fe_sub(f, a2, fe_dbl(f, beta4));
+            S.st(P::SX, X3);
+            S.st(P::S3, fe_sub(f, beta4, X3));                                 // 4 beta - X3
+        }
+        S.st(P::S2, fe_mul8(f, fe_sqr(f, S.ld(P::S2))));                       // 8 gamma^2
+        S.st(P::SY, fe_sub(f, fe_mul(f, S.ld(P::S4), S.ld(P::S3)), S.ld(P::S2)));
+    } else {
+        S.store_point(jac_dbl<C>(S.load_point()));
+    }
+}
+
+// A 64-byte table row x[8] y[8] (a lane-table entry or a fixed-base table entry; `stride` words
+// between consecutive words: 1 for rows in global memory), optionally mapped by the endomorphism
+// (x -> beta x) and / or negated.  The coordinates are reloaded where the formulas consume them.
+template <class C>
+struct RowSrc {
+    const uint32_t* row;
+    int stride;
+    bool neg, endo;
+    GECC_HD fe half(int off) const {
+        fe v;
+#if defined(__CUDA_ARCH__)
+        if (stride == 1) {
+            const uint4* q = reinterpret_cast<const uint4*>(row + off);
+            const uint4 a = __ldg(q), b = __ldg(q + 1);
+            v.w[0] = a.x; v.w[1] = a.y; v.w[2] = a.z; v.w[3] = a.w;
+            v.w[4] = b.x; v.w[5] = b.y; v.w[6] = b.z; v.w[7] = b.w;
+            return v;
+        }
+#endif
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v.w[i] = row[(size_t)(off + i) * stride];
+        return v;
+    }
+    GECC_HD fe x() const {
+        fe v = half(0);
+        if constexpr (C::has_glv) {
+            if (endo) {
+                fe beta;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) beta.w[i] = C::beta(i);
+                v = fe_mul(typename C::Fp{}, v, beta);
+            }
+        }
+        return v;
+    }
+    GECC_HD fe y() const {
+        const fe v = half(8);
+        return neg ? fe_neg(typename C::Fp{}, v) : v;
+    }
+    GECC_HD aff point() const { return aff{x(), y()}; }
+};
+
+template <class C>
+GECC_HD RowSrc<C> LaneTable::row(int e, bool neg, bool endo) const {
+    return RowSrc<C>{base + (size_t)e * 16 * stride, stride, neg, endo};
+}
+
+// acc += q, q finite and affine, given as a row source.  Complete, as jac_madd.
+template <class C>
+GECC_HD_CALL void jac_madd_slots(const PointSlots S, const RowSrc<C> src) {
+    using P = PointSlots;
+    const typename C::Fp f{};
+    {
+        const fe Z = S.ld(P::SZ);
+        if (fe_is_zero(f, Z)) {  // accumulator at infinity
+            const aff q = src.point();
+            S.st(P::SX, q.x);
+            S.st(P::SY, q.y);
+            S.st(P::SZ, fe_one(f));
+            return;
+        }
+        S.st(P::S1, fe_sqr(f, Z));                                             // Z^2
+    }
+    bool h_zero;
+    {
+        const fe h = fe_sub(f, fe_mul(f, src.x(), S.ld(P::S1)), S.ld(P::SX));  // u2 - X
+        h_zero = fe_is_zero(f, h);
+        S.st(P::S2, h);
+    }
+    {
+        const fe zzz = fe_mul(f, S.ld(P::S1), S.ld(P::SZ));
+        S.st(P::S3, fe_sub(f, fe_mul(f, src.y(), zzz), S.ld(P::SY)));          // r = s2 - Y
+    }
+    if (h_zero) {  // accumulator == +-q: the complete formulas
+        S.store_point(jac_madd<C>(S.load_point(), src.point()));
+        return;
+    }
+    S.st(P::S1, fe_sqr(f, S.ld(P::S2)));                                       // hh
+    S.st(P::S4, fe_mul(f, S.ld(P::S1), S.ld(P::S2)));                          // hhh
+    S.st(P::S5, fe_mul(f, S.ld(P::SX), S.ld(P::S1)));                          // v = X hh
+    {
+        const fe r2 = fe_sqr(f, S.ld(P::S3));
+        const fe v = S.ld(P::S5);
+        S.st(P::SX, fe_sub(f, fe_sub(f, fe_sub(f, r2, S.ld(P::S4)), v), v));   // X3 = r^2 - hhh - 2v
+    }
+    S.st(P::S4, fe_mul(f, S.ld(P::SY), S.ld(P::S4)));                          // Y hhh
+    S.st(P::SY, fe_sub(f, fe_mul(f, S.ld(P::S3), fe_sub(f, S.ld(P::S5), S.ld(P::SX))), S.ld(P::S4)));
+    S.st(P::SZ, fe_mul(f, S.ld(P::SZ), S.ld(P::S2)));                          // Z3 = Z h
+}
+
+// var_base_mul with the accumulator in the slots (result left there)
+template <class C>
+GECC_HD void var_base_mul_slots(const fe& k_raw, const LaneTable& tab, const PointSlots S) {
+    const typename C::Fp f{};
+    const fe k = scalar_reduce_once<typename C::Fn>(k_raw);
+    S.store_point(jac_infinity<C>());
+    if constexpr (C::has_glv) {
+        const GlvSplit sp = glv_split<C>(k);
+        const Recoded<4> r1 = recode_signed<4>(sp.m1), r2 = recode_signed<4>(sp.m2);
+#pragma unroll 1
+        for (int j = 33; j >= 0; --j) {
+            if (j != 33) {
+                jac_dbl_slots<C>(S);
+                jac_dbl_slots<C>(S);
+                jac_dbl_slots<C>(S);
+                jac_dbl_slots<C>(S);
+            }
+            int d1 = recoded_digit<4>(r1, j), d2 = recoded_digit<4>(r2, j);
+            if (sp.neg1) d1 = -d1;
+            if (sp.neg2) d2 = -d2;
+            if (d1 != 0) jac_madd_slots<C>(S, tab.template row<C>((d1 < 0 ? -d1 : d1) - 1, d1 < 0, false));
+            if (d2 != 0) jac_madd_slots<C>(S, tab.template row<C>((d2 < 0 ? -d2 : d2) - 1, d2 < 0, true));
+        }
+    } else {
+        const Recoded<4> rc = recode_signed<4>(k);
+        if (rc.carry) {
+            const aff t = tab.load(0);
+            S.store_point(jac{t.x, t.y, fe_one(f)});
+        }
+#pragma unroll 1
+        for (int j = 63; j >= 0; --j) {
+            jac_dbl_slots<C>(S);
+            jac_dbl_slots<C>(S);
+            jac_dbl_slots<C>(S);
+            jac_dbl_slots<C>(S);
+            const int d = recoded_digit<4>(rc, j);
+            if (d != 0) jac_madd_slots<C>(S, tab.template row<C>((d < 0 ? -d : d) - 1, d < 0, false));
+        }
+    }
+}
+// the accumulator in the slots += k G (fixed_base_mul with `start`)
+template <class C, int WG>
+GECC_HD void fixed_base_add_slots(const fe& k_raw, const GTable<WG>& tab, const PointSlots S) {
+    const fe k = scalar_reduce_once<typename C::Fn>(k_raw);
+    const Recoded<WG> rc = recode_signed<WG>(k);
+    auto digit = [&](int j) { return j == 256 / WG ? (int)rc.carry : recoded_digit<WG>(rc, j); };
+#pragma unroll 1
+    for (int j = 0; j <= 256 / WG; ++j) {
+        if (j < 256 / WG) {
+            const int dn = digit(j + 1);
+            if (dn != 0) tab.prefetch(j + 1, dn < 0 ? -dn : dn);
+        }
+        const int d = digit(j);
+        if (d == 0) continue;
+        jac_madd_slots<C>(S, RowSrc<C>{tab.tab + ((size_t)j * GTable<WG>::per_window + (size_t)((d < 0 ? -d : d) - 1)) * 16, 1, d < 0, false});
+    }
+}
+
 template <class C, int WG, bool UNIFORM>
-GECC_HD jac fixed_base_mul_mode(const fe& k, const GTable<WG>& tab) {
+GECC_HD jac fixed_base_mul_mode(const fe& k, const GTable<WG>& tab, const PointSlots* slots = nullptr) {
     if constexpr (UNIFORM) return fixed_base_mul_uniform<C, WG>(k, tab);
-    else return fixed_base_mul<C, WG>(k, tab);
+    else {
+        if (slots) {  // accumulator at rest in shared memory (see PointSlots)
+            slots->store_point(jac_infinity<C>());
+            fixed_base_add_slots<C, WG>(k, tab, *slots);
+            return slots->load_point();
+        }
+        return fixed_base_mul<C, WG>(k, tab);
+    }
 }
 template <class C, bool UNIFORM>
 GECC_HD jac var_base_mul_mode(const fe& k, const LaneTable& tab) {
@@ -597,10 +864,10 @@ enum { LANE_OK = 0, LANE_NONCE_EXHAUSTED = 5 };  // sm2b_status values
 // (the body of the retry loop, protocol.cpp:133-160).  False when r == 0 or s == 0.
 template <class C, int WG, bool UNIFORM = false>
 GECC_HD bool sign_attempt(const fe& e_m, const fe& d_m, const fe& k, const GTable<WG>& gt, uint8_t* sig64,
-                          bool aligned = false) {
+                          bool aligned = false, const PointSlots* slots = nullptr) {
     const typename C::Fp fp{};
     const typename C::Fn fn{};
-    jac R = fixed_base_mul_mode<C, WG, UNIFORM>(k, gt);
+    jac R = fixed_base_mul_mode<C, WG, UNIFORM>(k, gt, slots);
     if (jac_is_inf<C>(R)) return false;                   // cannot happen for 0 < k < n
     fe zinv = fe_inv(fp, R.Z);
     fe x = fe_from_mont(fp, fe_mul(fp, R.X, fe_sqr(fp, zinv)));
@@ -618,14 +885,14 @@ GECC_HD bool sign_attempt(const fe& e_m, const fe& d_m, const fe& k, const GTabl
 
 template <class C, int WG, bool UNIFORM = false>
 GECC_HD int sign_lane(const fe& e, const fe& d, uint64_t seed, uint64_t stream,
-                      const GTable<WG>& gt, uint8_t* sig64, uint32_t first_attempt = 0) {
+                      const GTable<WG>& gt, uint8_t* sig64, uint32_t first_attempt = 0, const PointSlots* slots = nullptr) {
     const typename C::Fn fn{};
     fe e_m = fe_to_mont(fn, e);
     fe d_m = fe_to_mont(fn, d);
 #pragma unroll 1
     for (uint32_t attempt = first_attempt; attempt < 8; ++attempt) {  // protocol.cpp:121
         fe k = nonce_scalar<typename C::Fn>(seed, stream, attempt);
-        if (sign_attempt<C, WG, UNIFORM>(e_m, d_m, k, gt, sig64)) return LANE_OK;
+        if (sign_attempt<C, WG, UNIFORM>(e_m, d_m, k, gt, sig64, false, slots)) return LANE_OK;
     }
     for (int i = 0; i < 64; ++i) sig64[i] = 0;
     return LANE_NONCE_EXHAUSTED;
@@ -634,10 +901,11 @@ GECC_HD int sign_lane(const fe& e, const fe& d, uint64_t seed, uint64_t stream,
 // One attempt with a caller-supplied nonce (gecc_sign_nonces): LANE_OK, or LANE_NONCE_EXHAUSTED
 // when the nonce has to be replaced (outside (0, n), r == 0 or s == 0).
 template <class C, int WG, bool UNIFORM = false>
-GECC_HD int sign_lane_nonce(const fe& e, const fe& d, const fe& k, const GTable<WG>& gt, uint8_t* sig64) {
+GECC_HD int sign_lane_nonce(const fe& e, const fe& d, const fe& k, const GTable<WG>& gt, uint8_t* sig64,
+                            const PointSlots* slots = nullptr) {
     const typename C::Fn fn{};
     if (scalar_in_range<typename C::Fn>(k) &&
-        sign_attempt<C, WG, UNIFORM>(fe_to_mont(fn, e), fe_to_mont(fn, d), k, gt, sig64))
+        sign_attempt<C, WG, UNIFORM>(fe_to_mont(fn, e), fe_to_mont(fn, d), k, gt, sig64, false, slots))
         return LANE_OK;
     for (int i = 0; i < 64; ++i) sig64[i] = 0;
     return LANE_NONCE_EXHAUSTED;
@@ -652,14 +920,15 @@ GECC_HD int sign_lane_nonce(const fe& e, const fe& d, const fe& k, const GTable<
 // reference's per-lane retry sequence exactly.
 template <class C, int WG, int K, bool UNIFORM = false>
 GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream0,
-                        const GTable<WG>& gt, uint8_t* sig64, int* status, bool aligned = false) {
+                        const GTable<WG>& gt, uint8_t* sig64, int* status, bool aligned = false,
+                        const PointSlots* slots = nullptr) {
     const typename C::Fp fp{};
     const typename C::Fn fn{};
     fe X[K], Z[K], km[K], pz[K], pk[K];
 #pragma unroll 1
     for (int j = 0; j < K; ++j) {
         fe k = nonce_scalar<typename C::Fn>(seed, stream0 + j, 0);
-        jac R = fixed_base_mul_mode<C, WG, UNIFORM>(k, gt);
+        jac R = fixed_base_mul_mode<C, WG, UNIFORM>(k, gt, slots);
         X[j] = R.X;
         Z[j] = R.Z;  // never zero for 0 < k < n
         km[j] = fe_to_mont(fn, k);
@@ -686,7 +955,7 @@ GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream
             s = fe_from_mont(fn, s_m);
         }
         if (fe_is_zero(r) || fe_is_zero(s)) {  // retry with fresh nonces (protocol.cpp:142-160)
-            status[j] = sign_lane<C, WG, UNIFORM>(e[j], d[j], seed, stream0 + j, gt, out, 1);
+            status[j] = sign_lane<C, WG, UNIFORM>(e[j], d[j], seed, stream0 + j, gt, out, 1, slots);
             continue;
         }
         be32_store_a(out, r, aligned);
@@ -698,7 +967,7 @@ GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream
 // One lane of sm2b_verify: raw records in, 0/1 out.
 template <class C, int WG>
 GECC_HD uint8_t verify_lane(const uint8_t* digest32, const uint8_t* pub65, const uint8_t* sig64,
-                            const GTable<WG>& gt, const LaneTable& qt) {
+                            const GTable<WG>& gt, const LaneTable& qt, const PointSlots* slots = nullptr) {
     const typename C::Fp fp{};
     const typename C::Fn fn{};
     fe r = be32_load(sig64), s = be32_load(sig64 + 32);
@@ -710,8 +979,15 @@ GECC_HD uint8_t verify_lane(const uint8_t* digest32, const uint8_t* pub65, const
     fe u1 = fe_mul(fn, e, w_m);                                        // e * w, plain
     fe u2 = fe_mul(fn, r, w_m);
     build_lane_table<C>(Q, qt);
-    jac B = var_base_mul<C>(u2, qt);
-    jac R = fixed_base_mul<C, WG>(u1, gt, &B);   // u2 Q + u1 G: mixed additions are complete
+    jac R;
+    if (slots) {  // the ladder with its accumulator at rest in shared memory
+        var_base_mul_slots<C>(u2, qt, *slots);
+        fixed_base_add_slots<C, WG>(u1, gt, *slots);
+        R = slots->load_point();
+    } else {
+        jac B = var_base_mul<C>(u2, qt);
+        R = fixed_base_mul<C, WG>(u1, gt, &B);   // u2 Q + u1 G: mixed additions are complete
+    }
     if (jac_is_inf<C>(R)) return 0;
     // x(R) mod n == r  <=>  X == r Z^2  or  (r + n < p and X == (r + n) Z^2)
     fe zz = fe_sqr(fp, R.Z);

@@ -10,6 +10,10 @@
 
 namespace gecc {
 
+#ifndef GECC_VERIFY_BLOCKS
+#define GECC_VERIFY_BLOCKS 6      // blocks per SM (x 128 lanes): measured 4 / 5 / 6 = 22.70 / 22.10 / 22.03 ms per 2^20 (secp256k1)
+#define GECC_VERIFY_BLOCKS_SM2 5  // SM2: 44.85 / 44.32 / 44.80 ms
+#endif
 constexpr int VERIFY_THREADS = 128;  // x 512 B of lane table = 64 KiB shared memory per block
 constexpr int SIGN_THREADS = 128;
 
@@ -39,7 +43,14 @@ k_verify_gtab(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restri
     if (i >= n) return;
     GTable<GECC_WG> gt{gtab};
     LaneTable qt{lane_tables + i * 128, 1};
+#if defined(GECC_VERIFY_REGS)
     res[i] = verify_lane<C, GECC_WG>(dig + 32 * i, pub + 65 * i, sig + 64 * i, gt, qt);
+#else
+    // accumulator and temporaries of the ladder: 8 slots x 32 B per lane of shared memory
+    extern __shared__ uint4 point_slots[];
+    const PointSlots S{(uint32_t)__cvta_generic_to_shared(point_slots + threadIdx.x), 16u * THREADS};
+    res[i] = verify_lane<C, GECC_WG>(dig + 32 * i, pub + 65 * i, sig + 64 * i, gt, qt, &S);
+#endif
 }
 
 // flags[0] is set when any secret is zero or >= n: the whole call is malformed
@@ -55,6 +66,10 @@ k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ se
     const size_t i0 = (blockIdx.x * (size_t)SIGN_THREADS + threadIdx.x) * SIGN_K;
     if (i0 >= n) return;
     GTable<GECC_WG> gt{gtab};
+    // accumulator and temporaries of the fixed-base additions rest in shared memory (PointSlots)
+    extern __shared__ uint4 point_slots[];
+    const PointSlots S{(uint32_t)__cvta_generic_to_shared(point_slots + threadIdx.x), 16u * SIGN_THREADS};
+    const PointSlots* slots = UNIFORM ? nullptr : &S;
     fe e[SIGN_K], d[SIGN_K];
     bool all_ok = i0 + SIGN_K <= n;
     // 32- and 64-byte records on 16-byte boundaries: vector loads / stores (uniform over the launch)
@@ -67,7 +82,7 @@ k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ se
     }
     if (all_ok) {
         int st[SIGN_K];
-        sign_lanes<C, GECC_WG, SIGN_K, UNIFORM>(e, d, seed, lane_base + i0, gt, sig + 64 * i0, st, al_out);
+        sign_lanes<C, GECC_WG, SIGN_K, UNIFORM>(e, d, seed, lane_base + i0, gt, sig + 64 * i0, st, al_out, slots);
 #pragma unroll
         for (int j = 0; j < SIGN_K; ++j) status[i0 + j] = st[j];
         return;
@@ -82,7 +97,7 @@ k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ se
             for (int b = 0; b < 64; ++b) sig[64 * i + b] = 0;
             continue;
         }
-        status[i] = sign_lane<C, GECC_WG, UNIFORM>(e[j], d[j], seed, lane_base + i, gt, sig + 64 * i);
+        status[i] = sign_lane<C, GECC_WG, UNIFORM>(e[j], d[j], seed, lane_base + i, gt, sig + 64 * i, 0, slots);
     }
 }
 
@@ -317,12 +332,17 @@ cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t
     for (size_t at = 0; at < n; at += scratch_lanes) {
         const size_t m = n - at < scratch_lanes ? n - at : scratch_lanes;
         const int b = blocks_for(m, 128);
+#if defined(GECC_VERIFY_REGS)
+        const size_t slot_bytes = 0;
+#else
+        const size_t slot_bytes = (size_t)PointSlots::COUNT * 32 * 128;  // 32 KB per block: 4 blocks per SM
+#endif
         if (curve == CURVE_SECP)
-            k_verify_gtab<SecpEcdsaCurve, 128, 4><<<b, 128, 0, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at,
-                                                                    gtab, lane_scratch, res + at);
+            k_verify_gtab<SecpEcdsaCurve, 128, GECC_VERIFY_BLOCKS><<<b, 128, slot_bytes, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at,
+                                                                             gtab, lane_scratch, res + at);
         else
-            k_verify_gtab<Sm2Curve, 128, 4><<<b, 128, 0, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at, gtab,
-                                                              lane_scratch, res + at);
+            k_verify_gtab<Sm2Curve, 128, GECC_VERIFY_BLOCKS_SM2><<<b, 128, slot_bytes, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at, gtab,
+                                                                       lane_scratch, res + at);
     }
     return cudaGetLastError();
 }
@@ -335,23 +355,27 @@ cudaError_t launch_secret_range(int curve, size_t n, const uint8_t* sec, uint32_
     return cudaGetLastError();
 }
 
-#define GECC_BY_CURVE_MODE(curve, uniform, KERNEL, GRID, THREADS, ...)                         \
-    do {                                                                                        \
-        if ((curve) == CURVE_SECP) {                                                            \
-            if (uniform) KERNEL<SecpEcdsaCurve, true><<<GRID, THREADS, 0, s>>>(__VA_ARGS__);    \
-            else KERNEL<SecpEcdsaCurve, false><<<GRID, THREADS, 0, s>>>(__VA_ARGS__);           \
-        } else {                                                                                \
-            if (uniform) KERNEL<Sm2Curve, true><<<GRID, THREADS, 0, s>>>(__VA_ARGS__);          \
-            else KERNEL<Sm2Curve, false><<<GRID, THREADS, 0, s>>>(__VA_ARGS__);                 \
-        }                                                                                       \
+#define GECC_BY_CURVE_MODE_SMEM(curve, uniform, KERNEL, GRID, THREADS, SMEM, ...)                  \
+    do {                                                                                           \
+        if ((curve) == CURVE_SECP) {                                                               \
+            if (uniform) KERNEL<SecpEcdsaCurve, true><<<GRID, THREADS, SMEM, s>>>(__VA_ARGS__);    \
+            else KERNEL<SecpEcdsaCurve, false><<<GRID, THREADS, SMEM, s>>>(__VA_ARGS__);           \
+        } else {                                                                                   \
+            if (uniform) KERNEL<Sm2Curve, true><<<GRID, THREADS, SMEM, s>>>(__VA_ARGS__);          \
+            else KERNEL<Sm2Curve, false><<<GRID, THREADS, SMEM, s>>>(__VA_ARGS__);                 \
+        }                                                                                          \
     } while (0)
+#define GECC_BY_CURVE_MODE(curve, uniform, KERNEL, GRID, THREADS, ...) \
+    GECC_BY_CURVE_MODE_SMEM(curve, uniform, KERNEL, GRID, THREADS, 0, __VA_ARGS__)
+constexpr size_t SIGN_SLOT_BYTES = (size_t)PointSlots::COUNT * 32 * SIGN_THREADS;  // 32 KB per block
 
 cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed,
                         uint64_t lane_base, const uint32_t* gtab, uint8_t* sig, int32_t* status,
                         uint32_t* flags, cudaStream_t s, bool uniform) {
     if (n == 0) return cudaSuccess;
     const int b = blocks_for((n + SIGN_K - 1) / SIGN_K, SIGN_THREADS);
-    GECC_BY_CURVE_MODE(curve, uniform, k_sign, b, SIGN_THREADS, n, dig, sec, seed, lane_base, gtab, sig, status, flags);
+    GECC_BY_CURVE_MODE_SMEM(curve, uniform, k_sign, b, SIGN_THREADS, SIGN_SLOT_BYTES, n, dig, sec, seed, lane_base, gtab, sig, status,
+                            flags);
     return cudaGetLastError();
 }
 

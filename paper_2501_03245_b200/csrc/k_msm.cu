@@ -1171,6 +1171,7 @@ void set_msm_form(int form) { g_msm_form = form; }
 static bool msm_affine() { return g_msm_form != 1; }
 constexpr int MSM_TREE_KMIN = 2;  // fewest joins per thread any level uses
 constexpr int MSM_GROUPS = 4;     // most window groups of the two-stream pipeline (scratch is sized for it)
+constexpr uint32_t MSM_GROUP_CUT = 8;  // first window of the high group when there are two
 constexpr int MSM_GROUPS_DEFAULT = 2;  // measured: 4.02 / 3.80 / 4.41 ms with 1 / 2 / 4 groups (secp256k1, 2^20)
 
 static MsmPlan msm_plan(size_t n, int limbs) {
@@ -1331,7 +1332,13 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
         }
         size_t tile_base = 0;
         for (int g = 0; g < G; ++g) {
-            const uint32_t w1 = (uint32_t)(MSM_WINDOWS * (G - g) / G), w0 = (uint32_t)(MSM_WINDOWS * (G - g - 1) / G);
+            uint32_t w1 = (uint32_t)(MSM_WINDOWS * (G - g) / G), w0 = (uint32_t)(MSM_WINDOWS * (G - g - 1) / G);
+            if (G == 2) {  // the high group carries the long doubling chain of its shift: it gets fewer windows
+                static const int cut_knob = [] { const char* v = getenv("GECC_MSM_CUT"); return v ? atoi(v) : 0; }();  // A/B timing
+                const uint32_t cut = cut_knob >= 1 && cut_knob < MSM_WINDOWS ? (uint32_t)cut_knob : MSM_GROUP_CUT;
+                w1 = g == 0 ? MSM_WINDOWS : cut;
+                w0 = g == 0 ? cut : 0;
+            }
             const size_t pos0 = (size_t)w0 * p.region, m = (size_t)(w1 - w0) * p.region;
             cudaStream_t hs = (g & 1) ? aux.stream : s;
             const size_t tiles_max = ((m + 1) / 2 + (size_t)MSM_TREE_THREADS * MSM_TREE_KMIN - 1) / ((size_t)MSM_TREE_THREADS * MSM_TREE_KMIN) + 1;

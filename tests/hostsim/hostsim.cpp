@@ -219,7 +219,11 @@ int sign_t(size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed, uint
             d[j] = be32_load(sec + 32 * (i + j));
         }
         if (g_uniform) sign_lanes<C, HS_WG, K, true>(e, d, seed, base + i, gt, sig + 64 * i, s4);
-        else sign_lanes<C, HS_WG, K>(e, d, seed, base + i, gt, sig + 64 * i, s4);
+        else {  // through the shared-memory-slot form of the fixed-base additions, as k_sign runs it
+            fe slot_mem[PointSlots::COUNT];
+            PointSlots S{slot_mem};
+            sign_lanes<C, HS_WG, K>(e, d, seed, base + i, gt, sig + 64 * i, s4, false, &S);
+        }
         for (int j = 0; j < K; ++j) st[i + j] = s4[j];
     }
     for (; i < n; ++i) {
@@ -248,8 +252,14 @@ int verify_t(size_t n, const uint8_t* dig, const uint8_t* pub, const uint8_t* si
     GTable<HS_WG> gt{host_gtable<C>().data()};
     uint32_t lane[8 * 16];
     LaneTable lt{lane, 1};
-    for (size_t i = 0; i < n; ++i)
+    for (size_t i = 0; i < n; ++i) {
         res[i] = verify_lane<C, HS_WG>(dig + 32 * i, pub + 65 * i, sig + 64 * i, gt, lt);
+        // the same lane with the ladder's accumulator at rest in "shared memory" slots (the form the
+        // GPU kernel runs): must agree
+        fe slot_mem[PointSlots::COUNT];
+        PointSlots S{slot_mem};
+        if (verify_lane<C, HS_WG>(dig + 32 * i, pub + 65 * i, sig + 64 * i, gt, lt, &S) != res[i]) return 77;
+    }
     return 0;
 }
 template <class C>
