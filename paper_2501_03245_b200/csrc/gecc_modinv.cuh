@@ -61,19 +61,18 @@ GECC_HD int32_t divsteps_30(int32_t zeta, uint32_t f0, uint32_t g0, trans2x2* t)
     uint32_t f = f0, g = g0;
 #pragma unroll 6
     for (int i = 0; i < 30; ++i) {
-        uint32_t c1 = (uint32_t)(zeta >> 31);  // all ones when zeta < 0
-        uint32_t c2 = 0u - (g & 1u);           // all ones when g is odd
-        uint32_t x = (f ^ c1) - c1;            // +-f
-        uint32_t y = (u ^ c1) - c1;
-        uint32_t z = (v ^ c1) - c1;
-        g += x & c2;
-        q += y & c2;
-        r += z & c2;
-        c1 &= c2;                              // swap happens when zeta < 0 and g odd
-        zeta = (int32_t)(((uint32_t)zeta ^ c1) - 1u);
-        f += g & c1;
-        u += q & c1;
-        v += r & c1;
+        const uint32_t c1 = (uint32_t)(zeta >> 31);  // all ones when zeta < 0
+        const uint32_t c2 = 0u - (g & 1u);           // all ones when g is odd
+        const uint32_t c12 = c1 & c2;                // swap happens when zeta < 0 and g odd
+        // g += (+-f) & c2 with -f = (f ^ c1) - c1:  ((f ^ c1) - c1) & c2 == ((f ^ c1) & c2) - c12, so each
+        // update is one three-input logic operation and one three-input add (21 instead of 27 per step)
+        g = g + ((f ^ c1) & c2) - c12;
+        q = q + ((u ^ c1) & c2) - c12;
+        r = r + ((v ^ c1) & c2) - c12;
+        zeta = (int32_t)(((uint32_t)zeta ^ c12) - 1u);
+        f += g & c12;
+        u += q & c12;
+        v += r & c12;
         g >>= 1;
         u <<= 1;
         v <<= 1;
@@ -436,16 +435,14 @@ __device__ __noinline__ fel<F> safegcd_inverse_warp(const F& fld, const fel<F>& 
         } else {
 #pragma unroll
             for (int i = 0; i < 30; ++i) {
-                uint32_t c1 = (uint32_t)(zeta >> 31);
+                const uint32_t c1 = (uint32_t)(zeta >> 31);
                 const uint32_t c2 = 0u - (g & 1u);
-                const uint32_t xx = (f ^ c1) - c1;
-                const uint32_t yy = (a ^ c1) - c1;
-                g += xx & c2;
-                b += yy & c2;
-                c1 &= c2;
-                zeta = (int32_t)(((uint32_t)zeta ^ c1) - 1u);
-                f += g & c1;
-                a += b & c1;
+                const uint32_t c12 = c1 & c2;
+                g = g + ((f ^ c1) & c2) - c12;   // see divsteps_30
+                b = b + ((a ^ c1) & c2) - c12;
+                zeta = (int32_t)(((uint32_t)zeta ^ c12) - 1u);
+                f += g & c12;
+                a += b & c12;
                 g >>= 1;
                 a <<= 1;
             }

@@ -58,8 +58,11 @@ k_verify_gtab(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restri
 // consecutive lanes and shares the two inversions among them (sign_lanes).
 constexpr int SIGN_K = GECC_SIGN_K;  // gecc_ecdsa.cuh: measured 4 / 8 / 16 lanes per thread = 2.87 / 2.76 / 3.09 ms per 2^20
 
+#ifndef GECC_SIGN_BLOCKS
+#define GECC_SIGN_BLOCKS 4
+#endif
 template <class C, bool UNIFORM>
-__global__ void __launch_bounds__(SIGN_THREADS)
+__global__ void __launch_bounds__(SIGN_THREADS, GECC_SIGN_BLOCKS)
 k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ sec, uint64_t seed,
        uint64_t lane_base, const uint32_t* __restrict__ gtab, uint8_t* __restrict__ sig,
        int32_t* __restrict__ status, uint32_t* __restrict__ flags) {
