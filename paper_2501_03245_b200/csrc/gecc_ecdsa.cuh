@@ -829,10 +829,24 @@ GECC_HD jac fixed_base_mul_mode(const fe& k, const GTable<WG>& tab, const PointS
     }
 }
 template <class C, bool UNIFORM>
-GECC_HD jac var_base_mul_mode(const fe& k, const LaneTable& tab) {
+GECC_HD jac var_base_mul_mode(const fe& k, const LaneTable& tab, const PointSlots* slots = nullptr) {
     if constexpr (UNIFORM) return var_base_mul_uniform<C>(k, tab);
-    else return var_base_mul<C>(k, tab);
+    else {
+        if (slots) {
+            var_base_mul_slots<C>(k, tab, *slots);
+            return slots->load_point();
+        }
+        return var_base_mul<C>(k, tab);
+    }
 }
+#if defined(__CUDACC__)
+// this thread's slots in a static shared array of the calling kernel (1-D blocks of THREADS)
+template <int THREADS>
+__device__ __forceinline__ PointSlots block_point_slots() {
+    __shared__ uint4 mem[2 * PointSlots::COUNT * THREADS];
+    return PointSlots{(uint32_t)__cvta_generic_to_shared(mem + threadIdx.x), 16u * THREADS};
+}
+#endif
 
 // ------------------------------------------------------------ point codec
 // 65-byte record 0x04 || X || Y -> affine Montgomery point; false when the tag,

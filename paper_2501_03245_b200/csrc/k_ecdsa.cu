@@ -47,8 +47,7 @@ k_verify_gtab(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restri
     res[i] = verify_lane<C, GECC_WG>(dig + 32 * i, pub + 65 * i, sig + 64 * i, gt, qt);
 #else
     // accumulator and temporaries of the ladder: 8 slots x 32 B per lane of shared memory
-    extern __shared__ uint4 point_slots[];
-    const PointSlots S{(uint32_t)__cvta_generic_to_shared(point_slots + threadIdx.x), 16u * THREADS};
+    const PointSlots S = block_point_slots<THREADS>();
     res[i] = verify_lane<C, GECC_WG>(dig + 32 * i, pub + 65 * i, sig + 64 * i, gt, qt, &S);
 #endif
 }
@@ -70,8 +69,7 @@ k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ se
     if (i0 >= n) return;
     GTable<GECC_WG> gt{gtab};
     // accumulator and temporaries of the fixed-base additions rest in shared memory (PointSlots)
-    extern __shared__ uint4 point_slots[];
-    const PointSlots S{(uint32_t)__cvta_generic_to_shared(point_slots + threadIdx.x), 16u * SIGN_THREADS};
+    const PointSlots S = block_point_slots<SIGN_THREADS>();
     const PointSlots* slots = UNIFORM ? nullptr : &S;
     fe e[SIGN_K], d[SIGN_K];
     bool all_ok = i0 + SIGN_K <= n;
@@ -147,7 +145,8 @@ k_keygen(size_t n, uint64_t seed, uint64_t lane_base, const uint32_t* __restrict
     GTable<GECC_WG> gt{gtab};
     fe d = nonce_scalar<typename C::Fn>(seed, lane_base + i, 0);
     be32_store(sec + 32 * i, d);
-    jac r = fixed_base_mul_mode<C, GECC_WG, UNIFORM>(d, gt);
+    const PointSlots S = block_point_slots<SIGN_THREADS>();
+    jac r = fixed_base_mul_mode<C, GECC_WG, UNIFORM>(d, gt, UNIFORM ? nullptr : &S);
     encode_point<C>(pub + 65 * i, jac_to_aff_with<C>(r, fe_inv(f, r.Z)));
 }
 
@@ -175,7 +174,8 @@ k_ecdh(size_t n, const uint8_t* __restrict__ sec, const uint8_t* __restrict__ pe
         return;
     }
     build_lane_table<C>(p, qt);
-    jac r = var_base_mul_mode<C, UNIFORM>(d, qt);
+    const PointSlots S = block_point_slots<VERIFY_THREADS>();
+    jac r = var_base_mul_mode<C, UNIFORM>(d, qt, UNIFORM ? nullptr : &S);
     if (jac_is_inf<C>(r)) {
         status[i] = 4;
         return;
@@ -209,7 +209,8 @@ k_fpmul(size_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ g
     const size_t i = blockIdx.x * (size_t)SIGN_THREADS + threadIdx.x;
     if (i >= n) return;
     GTable<GECC_WG> gt{gtab};
-    store_affine<C>(fixed_base_mul<C, GECC_WG>(col_load(k, n, i), gt), ox, oy, oinf, n, i);
+    const PointSlots S = block_point_slots<SIGN_THREADS>();
+    store_affine<C>(fixed_base_mul_mode<C, GECC_WG, false>(col_load(k, n, i), gt, &S), ox, oy, oinf, n, i);
 }
 
 template <class C>
@@ -227,7 +228,8 @@ k_upmul(size_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ p
     }
     aff p{col_load(px, n, i), col_load(py, n, i)};
     build_lane_table<C>(p, qt);
-    store_affine<C>(var_base_mul<C>(col_load(k, n, i), qt), ox, oy, oinf, n, i);
+    const PointSlots S = block_point_slots<VERIFY_THREADS>();
+    store_affine<C>(var_base_mul_mode<C, false>(col_load(k, n, i), qt, &S), ox, oy, oinf, n, i);
 }
 
 // ---- sm2b_bench_run support (bench.cpp:20-62): seeded inputs and the "jacobian-serial"
@@ -335,11 +337,7 @@ cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t
     for (size_t at = 0; at < n; at += scratch_lanes) {
         const size_t m = n - at < scratch_lanes ? n - at : scratch_lanes;
         const int b = blocks_for(m, 128);
-#if defined(GECC_VERIFY_REGS)
-        const size_t slot_bytes = 0;
-#else
-        const size_t slot_bytes = (size_t)PointSlots::COUNT * 32 * 128;  // 32 KB per block: 4 blocks per SM
-#endif
+        const size_t slot_bytes = 0;  // the ladder's slots are a static shared array of the kernel (32 KB per block)
         if (curve == CURVE_SECP)
             k_verify_gtab<SecpEcdsaCurve, 128, GECC_VERIFY_BLOCKS><<<b, 128, slot_bytes, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at,
                                                                              gtab, lane_scratch, res + at);
@@ -370,15 +368,13 @@ cudaError_t launch_secret_range(int curve, size_t n, const uint8_t* sec, uint32_
     } while (0)
 #define GECC_BY_CURVE_MODE(curve, uniform, KERNEL, GRID, THREADS, ...) \
     GECC_BY_CURVE_MODE_SMEM(curve, uniform, KERNEL, GRID, THREADS, 0, __VA_ARGS__)
-constexpr size_t SIGN_SLOT_BYTES = (size_t)PointSlots::COUNT * 32 * SIGN_THREADS;  // 32 KB per block
 
 cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed,
                         uint64_t lane_base, const uint32_t* gtab, uint8_t* sig, int32_t* status,
                         uint32_t* flags, cudaStream_t s, bool uniform) {
     if (n == 0) return cudaSuccess;
     const int b = blocks_for((n + SIGN_K - 1) / SIGN_K, SIGN_THREADS);
-    GECC_BY_CURVE_MODE_SMEM(curve, uniform, k_sign, b, SIGN_THREADS, SIGN_SLOT_BYTES, n, dig, sec, seed, lane_base, gtab, sig, status,
-                            flags);
+    GECC_BY_CURVE_MODE(curve, uniform, k_sign, b, SIGN_THREADS, n, dig, sec, seed, lane_base, gtab, sig, status, flags);
     return cudaGetLastError();
 }
 

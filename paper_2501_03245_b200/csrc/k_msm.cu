@@ -790,6 +790,37 @@ k_msm_tree_fused(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __
     }
 }
 
+// The THIN levels fused: levels [first, MSM_TREE_LEVELS) in one launch.  Level 0 and 1 are wide and
+// bound by memory latency (they want every warp the SM can hold: the three-launch kernels); from
+// level 2 on a level has so few joins that its three launches mostly wait -- for the inversion of
+// the totals and for each other.  Here a block owns 2 * THREADS * K0 << first positions and walks
+// the remaining levels by itself (block-level inversion per level while the level still gives every
+// thread a join, warp 0 alone below that); 16 KB of shared memory per block, so several blocks per
+// SM hide each other's inversions.
+template <class C, int K0>
+__global__ void __launch_bounds__(MSM_TREE_THREADS, C::Fp::N > 8 ? 4 : 5)
+k_msm_tree_upper(size_t m, int first, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                 const uint4* __restrict__ rec, uint4* slots, uint8_t* sinf) {
+    constexpr int NL = C::Fp::N;
+    constexpr int T = MSM_TREE_THREADS;
+    __shared__ uint32_t sm_pref[K0 * NL * T];
+    __shared__ uint32_t sm_scan[2 * NL * (T / 32)];
+#pragma unroll 1
+    for (int level = first; level < MSM_TREE_LEVELS; ++level) {
+        if (level > first) __syncthreads();  // the slots of the level below are complete
+        const size_t span = (size_t)2 << level;
+        const size_t joins = (m + span - 1) / span;
+        const int count = (T * K0) >> (level - first);  // joins of this block on this level
+        const size_t j_first = (size_t)blockIdx.x * count;
+        if (j_first >= joins) continue;                 // uniform over the block
+        if (count >= T) {
+            tree_level_in_block<C, false, T, T>(m, level, j_first, count / T, joins, keys, vals, rec, slots, sinf, sm_pref, sm_scan);
+        } else if (threadIdx.x < 32) {
+            tree_level_in_block<C, false, 32, T>(m, level, j_first, count / 32, joins, keys, vals, rec, slots, sinf, sm_pref, sm_scan);
+        }
+    }
+}
+
 // marginal sums, stage 1: thread (w, k, e, part) adds the 32 buckets of window w whose
 // k-th base-32 digit is e and whose next digit (cyclically) is `part`.
 template <class C>
@@ -1282,6 +1313,15 @@ static cudaError_t launch_tree_fused(size_t m, const TreeBufs& b, cudaStream_t s
     return cudaGetLastError();
 }
 
+template <class C, int K0>
+static cudaError_t launch_tree_upper(size_t m, int first, const TreeBufs& b, cudaStream_t s) {
+    static_assert((MSM_TREE_THREADS * K0) >> (MSM_TREE_LEVELS - 1) >= 8, "warp 0 still has joins on the last level");
+    const size_t per_block = ((size_t)2 * MSM_TREE_THREADS * K0) << first;  // positions
+    const unsigned blocks = (unsigned)((m + per_block - 1) / per_block);
+    k_msm_tree_upper<C, K0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, first, b.keys, b.vals, b.rec, b.slots, b.sinf);
+    return cudaGetLastError();
+}
+
 template <class C, class CI = C>
 static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const uint32_t* px, const uint32_t* py,
                            const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf,
@@ -1358,7 +1398,13 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
             } else {
                 if (split && joins0 >= 16 * fill) e = launch_tree<CI, 16, true>(curve, m, 0, tb, split, hs);
                 else e = launch_tree<CI, 8, true>(curve, m, 0, tb, split, hs);
+                static const int upper_knob = [] { const char* v = getenv("GECC_MSM_UPPER"); return v ? atoi(v) : 0; }();  // A/B timing
+                const int first_fused = upper_knob >= 1 && upper_knob < MSM_TREE_LEVELS ? upper_knob : MSM_TREE_LEVELS;
                 for (int l = 1; l < MSM_TREE_LEVELS && e == cudaSuccess; ++l) {
+                    if (l == first_fused) {  // the remaining levels in one launch
+                        e = launch_tree_upper<CI, 4>(m, l, tb, hs);
+                        break;
+                    }
                     const size_t joins = (m + ((size_t)2 << l) - 1) / ((size_t)2 << l);
                     if (split && joins >= 16 * fill) e = launch_tree<CI, 16, false>(curve, m, l, tb, split, hs);
                     else if (joins >= 8 * fill) e = launch_tree<CI, 8, false>(curve, m, l, tb, split, hs);

@@ -66,6 +66,8 @@ def main():
     l.gecc_batch_fpmul_dev(ctx.h, C.c_size_t(nmax), vp(k2), vp(T[0]), vp(T[1]), vp(T[2]))
     torch.cuda.synchronize()
     rows = []
+    from oracle import refshim as gate_mod   # checker only: the compiled reference, per-size parity gates
+    gate = gate_mod if gate_mod.available() else None
     for lg in range(lo, hi + 1, 2):
         n = 1 << lg
         # column buffers must be contiguous per size: repack the prefix (limb k at k*n + i)
@@ -73,13 +75,42 @@ def main():
         Pn, Tn, Sn = sub(P), sub(T), sub(S)
         ms_v = timed(lambda: l.gecc_verify_dev(ctx.h, C.c_size_t(n), vp(d_dig), vp(d_pub), vp(d_sig), vp(d_res)), stream)
         assert int(d_res[:n].sum()) == n
+        # parity gate of this size (verify): a sample of lanes, two of them forged, through the CPU
+        # reference (oracle/_ref) and the GPU -- the same verdict lane by lane
+        if gate is not None:
+            m = min(n, 256)
+            idx = np.linspace(0, n - 1, m).astype(np.int64)
+            take = lambda d, w: d.view(-1, w)[torch.from_numpy(idx).cuda()].contiguous()
+            g_dig, g_pub, g_sig = take(d_dig[:32 * n], 32), take(d_pub[:65 * n], 65), take(d_sig[:64 * n], 64).clone()
+            g_sig[3, 5] ^= 1
+            g_sig[m - 1, 40] ^= 0x80
+            g_res = u8(m)
+            assert l.gecc_verify_dev(ctx.h, C.c_size_t(m), vp(g_dig), vp(g_pub), vp(g_sig), vp(g_res)) == 0
+            rc, want = gate.ecdsa_verify(1, g_dig.cpu().numpy().tobytes(), g_pub.cpu().numpy().tobytes(),
+                                         g_sig.cpu().numpy().tobytes(), workers=0)
+            assert rc == 0 and g_res.cpu().numpy().tobytes() == want and want.count(b"\x00") == 2, f"verify parity at 2^{lg}"
         padd = lambda: l.gecc_batch_padd_dev(ctx.h, C.c_size_t(n), vp(Pn[0]), vp(Pn[1]), vp(Pn[2]), vp(Tn[0]),
                                              vp(Tn[1]), vp(Tn[2]), vp(Sn[0]), vp(Sn[1]), vp(Sn[2]))
         forms = {}
-        for name in ("chunked", "chunked8", "coop", "coop128", "tiled8", "tiled4", "auto"):  # one inversion per thread / per block / library's pick
+        outs = {}
+        for name in ("chunked", "coop128", "tiled8", "fused", "auto"):  # one inversion per thread / per block / per tile; library's pick
             gecc.set_batch_form(name)
             forms[name] = timed(padd, stream)
+            outs[name] = tuple(t.clone() for t in Sn)
+        gecc.set_batch_form("auto")
         ms_p = forms["auto"]
+        # parity gate of this size (padd): every form gives the same bytes for ALL n pairs, and a sample
+        # of the pairs (all of them up to 2^16) equals the CPU reference's batch_padd
+        for name, o in outs.items():
+            assert all(bool((a == b).all()) for a, b in zip(o, outs["chunked"])), f"padd form {name} differs at 2^{lg}"
+        if gate is not None:
+            m = min(n, 1 << 16)
+            idx = torch.from_numpy(np.linspace(0, n - 1, m).astype(np.int64)).cuda()
+            pick = lambda A: tuple((a[:, idx] if a.dim() == 2 else a[idx]).contiguous().cpu().numpy() for a in A)
+            as_u = lambda A: (A[0].view(np.uint32), A[1].view(np.uint32), A[2])
+            want = gate.batch_padd(1, as_u(pick(Pn)), as_u(pick(Tn)), workers=0)
+            got = as_u(pick(outs["auto"]))
+            assert all((np.asarray(w) == g).all() for w, g in zip(want, got)), f"padd parity at 2^{lg}"
         rows.append(dict(log2n=lg, verify_ms=ms_v, verify_per_s=n / ms_v * 1e3, padd_ms=ms_p, padd_per_s=n / ms_p * 1e3,
                          padd_ms_by_form=forms))
         print(f"2^{lg:2d}  verify {ms_v:9.3f} ms  {n / ms_v / 1e3:8.2f} M/s   padd {ms_p:8.4f} ms  {n / ms_p / 1e6:7.3f} G/s"
@@ -103,7 +134,9 @@ def main():
             print(f"CPU 2^{lg}: verify {n / dt:9.0f}/s  padd {n / tp / 1e6:6.2f} M/s  ({os.cpu_count()} cores)", flush=True)
     os.makedirs("gpurun_out", exist_ok=True)
     with open("gpurun_out/sweep.json", "w") as f:
-        json.dump(dict(gpu=rows, cpu_reference=cpu, curve="secp256k1"), f, indent=1)
+        json.dump(dict(gpu=rows, cpu_reference=cpu, curve="secp256k1",
+                       parity="every size: verify sample (two forged lanes) and padd (all forms equal; sample of <= 2^16 pairs) checked against oracle/_ref"
+                       if gate is not None else "oracle/_ref not built: sizes unchecked"), f, indent=1)
 
 
 def sub_cpu(A, n):
