@@ -392,6 +392,29 @@ __device__ __forceinline__ void rec_store(uint4* rec, size_t i, const feN<N>& x,
     fe_store_u4<N, true>(rec + (N / 2) * i, x);
     fe_store_u4<N, true>(rec + (N / 2) * i + N / 4, y);
 }
+// The point at infinity is the slot whose x is ALL ONES -- never a stored coordinate: the canonical
+// fields stay below their modulus, and the weakly reduced field canonicalises the one value that
+// collides (2^256 - 1 == c - 1).  No separate flag array: a one-byte flag read at random costs a
+// whole DRAM burst, as much as the coordinate it describes (the flags were half of the traffic of
+// the forward passes above level 0).
+template <int N>
+__device__ __forceinline__ bool slot_is_inf(const feN<N>& x) {
+    uint32_t a = 0xFFFFFFFFu;
+#pragma unroll
+    for (int i = 0; i < N; ++i) a &= x.w[i];
+    return a == 0xFFFFFFFFu;
+}
+template <class C>
+__device__ __forceinline__ void slot_store(uint4* slots, size_t i, cfe<C> x, const cfe<C>& y, bool inf) {
+    constexpr int N = C::Fp::N;
+    if (inf) {
+#pragma unroll
+        for (int k = 0; k < N; ++k) x.w[k] = 0xFFFFFFFFu;
+    } else if (slot_is_inf(x)) {
+        if constexpr (C::Fp::kind == KIND_SECP_LAZY) x = lazy_canon(typename C::Fp{}, x);
+    }
+    rec_store<N>(slots, i, x, y);
+}
 template <int N>
 __device__ __forceinline__ feN<N> rec_x(const uint4* rec, size_t i) {  // slots: streaming
     return fe_load_u4<N, LD_STREAM>(rec + (N / 2) * i);
@@ -505,7 +528,7 @@ __device__ __forceinline__ caff<C> msm_point(const uint4* __restrict__ rec, uint
 // denominator of a join (one when nothing is inverted for it)
 template <class C, bool LEVEL0>
 __device__ __forceinline__ cfe<C> tree_denominator(const TreeJoin<C, LEVEL0>& t, const uint4* __restrict__ rec,
-                                                   const uint4* slots, const uint8_t* sinf) {
+                                                   const uint4* slots) {
     using fe = cfe<C>;
     constexpr int NL = C::Fp::N;
     const typename C::Fp f{};
@@ -519,8 +542,8 @@ __device__ __forceinline__ cfe<C> tree_denominator(const TreeJoin<C, LEVEL0>& t,
     } else {
         ax = rec_x<NL>(slots, t.dst);
         bx = rec_x<NL>(slots, t.src);
-        ai = sinf[t.dst] != 0;
-        bi = sinf[t.src] != 0;
+        ai = slot_is_inf(ax);
+        bi = slot_is_inf(bx);
     }
     if (ai || bi) return d;
     if (fe_eq(f, ax, bx)) {  // y is only needed when the x's collide
@@ -542,19 +565,17 @@ __device__ __forceinline__ cfe<C> tree_denominator(const TreeJoin<C, LEVEL0>& t,
 // the denominators up to and including this join's; prev the product before it.
 template <class C, bool LEVEL0>
 __device__ __forceinline__ void tree_apply(const TreeJoin<C, LEVEL0>& t, cfe<C>& inv, const cfe<C>& prev, bool first,
-                                           const uint4* __restrict__ rec, uint4* slots, uint8_t* sinf) {
+                                           const uint4* __restrict__ rec, uint4* slots) {
     using fe = cfe<C>;
     using aff = caff<C>;
     constexpr int NL = C::Fp::N;
     const typename C::Fp f{};
     if (LEVEL0 && t.copy2) {
         const aff p0 = msm_point<C>(rec, t.v0);
-        rec_store<NL>(slots, t.dst, p0.x, p0.y);
-        sinf[t.dst] = 0;
+        slot_store<C>(slots, t.dst, p0.x, p0.y, false);
         if (t.src != (size_t)-1) {
             const aff p1 = msm_point<C>(rec, t.v1);
-            rec_store<NL>(slots, t.src, p1.x, p1.y);
-            sinf[t.src] = 0;
+            slot_store<C>(slots, t.src, p1.x, p1.y, false);
         }
         return;
     }
@@ -567,8 +588,8 @@ __device__ __forceinline__ void tree_apply(const TreeJoin<C, LEVEL0>& t, cfe<C>&
     } else {
         A.x = rec_x<NL>(slots, t.dst); A.y = rec_y<NL>(slots, t.dst);
         B.x = rec_x<NL>(slots, t.src); B.y = rec_y<NL>(slots, t.src);
-        ai = sinf[t.dst] != 0;
-        bi = sinf[t.src] != 0;
+        ai = slot_is_inf(A.x);
+        bi = slot_is_inf(B.x);
     }
     fe d = fe_one(f);
     const uint32_t kind = classify_pair<C>(A.x, A.y, ai, B.x, B.y, bi, &d);
@@ -592,8 +613,7 @@ __device__ __forceinline__ void tree_apply(const TreeJoin<C, LEVEL0>& t, cfe<C>&
     } else {
         rinf = 1;
     }
-    rec_store<NL>(slots, t.dst, xr, yr);
-    sinf[t.dst] = rinf;
+    slot_store<C>(slots, t.dst, xr, yr, rinf != 0);
 }
 
 // Single-launch form of one level: the block's one inversion happens inside the kernel
@@ -602,7 +622,7 @@ template <class C, int K, bool LEVEL0>
 __global__ void __launch_bounds__(MSM_TREE_THREADS)
 k_msm_tree(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
            const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
-           uint4* slots, uint8_t* sinf) {
+           uint4* slots) {
     using fe = cfe<C>;
     using jac = cjac<C>;
     using aff = caff<C>;
@@ -618,7 +638,7 @@ k_msm_tree(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
         const size_t j = j0 + (size_t)k * MSM_TREE_THREADS;
         if (j < joins) {
             const TreeJoin<C, LEVEL0> t = tree_locate<C, LEVEL0>(j, level, m, keys, vals);
-            if (t.active) acc = fe_mul(f, acc, tree_denominator<C, LEVEL0>(t, rec, slots, sinf));
+            if (t.active) acc = fe_mul(f, acc, tree_denominator<C, LEVEL0>(t, rec, slots));
         }
 #pragma unroll
         for (int w = 0; w < NL; ++w) sm_pref[(k * NL + w) * MSM_TREE_THREADS + threadIdx.x] = acc.w[w];
@@ -634,7 +654,7 @@ k_msm_tree(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
 #pragma unroll
             for (int w = 0; w < NL; ++w) prev.w[w] = sm_pref[((k - 1) * NL + w) * MSM_TREE_THREADS + threadIdx.x];
         }
-        tree_apply<C, LEVEL0>(t, inv, prev, k == 0, rec, slots, sinf);
+        tree_apply<C, LEVEL0>(t, inv, prev, k == 0, rec, slots);
     }
 }
 
@@ -649,7 +669,7 @@ template <class C, int K, bool LEVEL0>
 __global__ void __launch_bounds__(MSM_TREE_THREADS, C::Fp::N > 8 ? 4 : 5)
 k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
                const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
-               const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
+               const uint4* __restrict__ slots,
                uint4* __restrict__ pref, uint4* __restrict__ others, uint32_t* __restrict__ totals,
                size_t tiles, size_t tile0) {
     using fe = cfe<C>;
@@ -667,7 +687,7 @@ k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
         const size_t j = j0 + (size_t)k * MSM_TREE_THREADS;
         if (j >= joins) break;
         const TreeJoin<C, LEVEL0> t = tree_locate<C, LEVEL0>(j, level, m, keys, vals);
-        if (t.active) acc = fe_mul(f, acc, tree_denominator<C, LEVEL0>(t, rec, slots, sinf));
+        if (t.active) acc = fe_mul(f, acc, tree_denominator<C, LEVEL0>(t, rec, slots));
         fe_store_cs<NL>(pref + (NL / 4) * j, acc);
     }
     fe total;
@@ -681,7 +701,7 @@ template <class C, int K, bool LEVEL0>
 __global__ void __launch_bounds__(MSM_TREE_THREADS, C::Fp::N > 8 ? 4 : 5)
 k_msm_tree_bwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
                const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
-               uint4* slots, uint8_t* sinf, const uint4* __restrict__ pref,
+               uint4* slots, const uint4* __restrict__ pref,
                const uint4* __restrict__ others, const uint32_t* __restrict__ total_inv, size_t tiles,
                size_t tile0) {
     using fe = cfe<C>;
@@ -705,7 +725,7 @@ k_msm_tree_bwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
             const size_t jp = j - MSM_TREE_THREADS;
             prev = fe_load_cs<NL>(pref + (NL / 4) * jp);
         }
-        tree_apply<C, LEVEL0>(t, inv, prev, k == 0, rec, slots, sinf);
+        tree_apply<C, LEVEL0>(t, inv, prev, k == 0, rec, slots);
     }
 }
 
@@ -724,7 +744,7 @@ constexpr int MSM_FUSED_KMIN = 4;
 template <class C, bool LEVEL0, int THREADS_ACTIVE, int NSM>
 __device__ __forceinline__ void tree_level_in_block(size_t m, int level, size_t j_first, int K, size_t joins,
                                                     const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
-                                                    const uint4* __restrict__ rec, uint4* slots, uint8_t* sinf,
+                                                    const uint4* __restrict__ rec, uint4* slots,
                                                     uint32_t* sm_pref, uint32_t* sm_scan) {
     // the THREADS_ACTIVE calling threads (the whole block, or warp 0) take K joins each:
     // j = j_first + k * THREADS_ACTIVE + tid.  sm_pref is word-interleaved over NSM threads.
@@ -738,7 +758,7 @@ __device__ __forceinline__ void tree_level_in_block(size_t m, int level, size_t 
         const size_t j = j_first + (size_t)k * THREADS_ACTIVE + tid;
         if (j < joins) {
             const TreeJoin<C, LEVEL0> t = tree_locate<C, LEVEL0>(j, level, m, keys, vals);
-            if (t.active) acc = fe_mul(f, acc, tree_denominator<C, LEVEL0>(t, rec, slots, sinf));
+            if (t.active) acc = fe_mul(f, acc, tree_denominator<C, LEVEL0>(t, rec, slots));
         }
 #pragma unroll
         for (int w = 0; w < NL; ++w) sm_pref[(k * NL + w) * NSM + tid] = acc.w[w];
@@ -754,14 +774,14 @@ __device__ __forceinline__ void tree_level_in_block(size_t m, int level, size_t 
 #pragma unroll
             for (int w = 0; w < NL; ++w) prev.w[w] = sm_pref[((k - 1) * NL + w) * NSM + tid];
         }
-        tree_apply<C, LEVEL0>(t, inv, prev, k == 0, rec, slots, sinf);
+        tree_apply<C, LEVEL0>(t, inv, prev, k == 0, rec, slots);
     }
 }
 
 template <class C, int K0>
 __global__ void __launch_bounds__(MSM_TREE_THREADS, K0 * C::Fp::N > 128 ? 2 : K0 * C::Fp::N > 64 ? 3 : 5)
 k_msm_tree_fused(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
-                 const uint4* __restrict__ rec, uint4* slots, uint8_t* sinf) {
+                 const uint4* __restrict__ rec, uint4* slots) {
     constexpr int NL = C::Fp::N;
     constexpr int T = MSM_TREE_THREADS;
     static_assert((T * K0) >> (MSM_TREE_LEVELS - 1) >= 32, "the last level still fills a warp");
@@ -771,7 +791,7 @@ k_msm_tree_fused(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __
     uint32_t* sm_scan = sm_dyn + K0 * NL * T;         // 2 * NL * (T / 32) words
     {
         const size_t joins = (m + 1) / 2;
-        tree_level_in_block<C, true, T, T>(m, 0, (size_t)blockIdx.x * (T * K0), K0, joins, keys, vals, rec, slots, sinf,
+        tree_level_in_block<C, true, T, T>(m, 0, (size_t)blockIdx.x * (T * K0), K0, joins, keys, vals, rec, slots,
                                            sm_pref, sm_scan);
     }
 #pragma unroll 1
@@ -783,9 +803,9 @@ k_msm_tree_fused(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __
         const size_t j_first = (size_t)blockIdx.x * count;
         if (j_first >= joins) continue;               // uniform over the block
         if (count >= T * MSM_FUSED_KMIN) {
-            tree_level_in_block<C, false, T, T>(m, level, j_first, count / T, joins, keys, vals, rec, slots, sinf, sm_pref, sm_scan);
+            tree_level_in_block<C, false, T, T>(m, level, j_first, count / T, joins, keys, vals, rec, slots, sm_pref, sm_scan);
         } else if (threadIdx.x < 32) {                // warp 0 alone: K = count / 32 <= 4 * KMIN
-            tree_level_in_block<C, false, 32, T>(m, level, j_first, count / 32, joins, keys, vals, rec, slots, sinf, sm_pref, sm_scan);
+            tree_level_in_block<C, false, 32, T>(m, level, j_first, count / 32, joins, keys, vals, rec, slots, sm_pref, sm_scan);
         }
     }
 }
@@ -800,7 +820,7 @@ k_msm_tree_fused(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __
 template <class C, int K0>
 __global__ void __launch_bounds__(MSM_TREE_THREADS, C::Fp::N > 8 ? 4 : 5)
 k_msm_tree_upper(size_t m, int first, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
-                 const uint4* __restrict__ rec, uint4* slots, uint8_t* sinf) {
+                 const uint4* __restrict__ rec, uint4* slots) {
     constexpr int NL = C::Fp::N;
     constexpr int T = MSM_TREE_THREADS;
     __shared__ uint32_t sm_pref[K0 * NL * T];
@@ -814,9 +834,9 @@ k_msm_tree_upper(size_t m, int first, const uint32_t* __restrict__ keys, const u
         const size_t j_first = (size_t)blockIdx.x * count;
         if (j_first >= joins) continue;                 // uniform over the block
         if (count >= T) {
-            tree_level_in_block<C, false, T, T>(m, level, j_first, count / T, joins, keys, vals, rec, slots, sinf, sm_pref, sm_scan);
+            tree_level_in_block<C, false, T, T>(m, level, j_first, count / T, joins, keys, vals, rec, slots, sm_pref, sm_scan);
         } else if (threadIdx.x < 32) {
-            tree_level_in_block<C, false, 32, T>(m, level, j_first, count / 32, joins, keys, vals, rec, slots, sinf, sm_pref, sm_scan);
+            tree_level_in_block<C, false, 32, T>(m, level, j_first, count / 32, joins, keys, vals, rec, slots, sm_pref, sm_scan);
         }
     }
 }
@@ -975,7 +995,7 @@ __device__ __forceinline__ cjac<C> warp_sum_points(cjac<C> acc, int lane) {
 template <class C>
 __global__ void __launch_bounds__(128, 4)
 k_msm_red_parts(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ starts,
-                const uint4* __restrict__ slots, const uint8_t* __restrict__ sinf,
+                const uint4* __restrict__ slots,
                 uint32_t* __restrict__ parts, uint32_t w0) {
     using fe = cfe<C>;
     using jac = cjac<C>;
@@ -996,10 +1016,16 @@ k_msm_red_parts(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __r
         const uint32_t id = w * MSM_BUCKETS + b;
         const size_t s = starts[id];
         if (s == 0xFFFFFFFFu) continue;
-        if (!sinf[s]) acc = jac_madd<C>(acc, aff{rec_x<NL>(slots, s), rec_y<NL>(slots, s)});
+        {
+            const fe x = rec_x<NL>(slots, s);
+            if (!slot_is_inf(x)) acc = jac_madd<C>(acc, aff{x, rec_y<NL>(slots, s)});
+        }
 #pragma unroll 1
         for (size_t a = (s / step + 1) * step; a < m && keys[a] == id; a += step)
-            if (!sinf[a]) acc = jac_madd<C>(acc, aff{rec_x<NL>(slots, a), rec_y<NL>(slots, a)});
+        {
+            const fe x = rec_x<NL>(slots, a);
+            if (!slot_is_inf(x)) acc = jac_madd<C>(acc, aff{x, rec_y<NL>(slots, a)});
+        }
     }
     jac_store<NL>(parts, MSM_RED_PARTS, t, acc);
 }
@@ -1189,7 +1215,7 @@ struct MsmPlan {
     size_t pairs, region, sort_temp, total;
     size_t slices;
     size_t off_keys, off_vals, off_keys2, off_vals2, off_buckets, off_edge, off_edge_key, off_parts, off_marg, off_wsum, off_win, off_temp;
-    size_t off_rec, off_slots, off_sinf, off_starts, off_pref, off_others, off_totals;
+    size_t off_rec, off_slots, off_starts, off_pref, off_others, off_totals;
     size_t max_tiles;
 };
 static size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
@@ -1232,7 +1258,6 @@ static MsmPlan msm_plan(size_t n, int limbs) {
     at = fork;
     p.off_rec = take(rb * n);
     p.off_slots = take(rb * p.pairs);
-    p.off_sinf = take(p.pairs);
     const size_t joins0 = (p.pairs + 1) / 2;
     p.off_pref = take(fb * joins0);
     // tiles of the thinnest level, one rounding tile per window group; totals | inverses per group
@@ -1248,7 +1273,6 @@ struct TreeBufs {
     const uint32_t *keys, *vals;
     const uint4* rec;
     uint4* slots;
-    uint8_t* sinf;
     uint4 *pref, *others;
     uint32_t* totals;
     size_t max_tiles;
@@ -1264,7 +1288,7 @@ static cudaError_t launch_tree(int curve, size_t m, int level, const TreeBufs& b
     const unsigned blocks = (unsigned)tiles;
     if constexpr (K * C::Fp::N <= 64) {  // the single-launch form parks K prefixes per thread in shared memory
         if (!split) {
-            k_msm_tree<C, K, LEVEL0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots, b.sinf);
+            k_msm_tree<C, K, LEVEL0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots);
             return cudaGetLastError();
         }
     }
@@ -1284,14 +1308,14 @@ static cudaError_t launch_tree(int curve, size_t m, int level, const TreeBufs& b
         uint32_t* tot = b.totals + (size_t)NL * (cap / parts) * h;
         uint32_t* inv = b.totals + (size_t)NL * (cap + (cap / parts) * h);
         k_msm_tree_fwd<C, K, LEVEL0><<<(unsigned)cnt, MSM_TREE_THREADS, 0, hs>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots,
-                                                                               b.sinf, b.pref, b.others, tot, cnt, t0);
+                                                                               b.pref, b.others, tot, cnt, t0);
         if constexpr (C::Fp::kind == KIND_SECP_LAZY) {
             if (cudaError_t e = launch_batch_invert_secp_lazy(cnt, tot, inv, hs)) return e;
         } else {
             if (cudaError_t e = launch_batch_invert(curve, 0, cnt, tot, inv, hs)) return e;
         }
         k_msm_tree_bwd<C, K, LEVEL0><<<(unsigned)cnt, MSM_TREE_THREADS, 0, hs>>>(m, joins, level, b.keys, b.vals, b.rec, b.slots,
-                                                                               b.sinf, b.pref, b.others, inv, cnt, t0);
+                                                                               b.pref, b.others, inv, cnt, t0);
     }
     if (parts > 1) {
         if (cudaError_t e = cudaEventRecord(b.join, b.aux)) return e;
@@ -1309,7 +1333,7 @@ static cudaError_t launch_tree_fused(size_t m, const TreeBufs& b, cudaStream_t s
     if (smem > 48 * 1024)
         if (cudaError_t e = cudaFuncSetAttribute(k_msm_tree_fused<C, K0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
             return e;
-    k_msm_tree_fused<C, K0><<<blocks, MSM_TREE_THREADS, smem, s>>>(m, b.keys, b.vals, b.rec, b.slots, b.sinf);
+    k_msm_tree_fused<C, K0><<<blocks, MSM_TREE_THREADS, smem, s>>>(m, b.keys, b.vals, b.rec, b.slots);
     return cudaGetLastError();
 }
 
@@ -1318,7 +1342,7 @@ static cudaError_t launch_tree_upper(size_t m, int first, const TreeBufs& b, cud
     static_assert((MSM_TREE_THREADS * K0) >> (MSM_TREE_LEVELS - 1) >= 8, "warp 0 still has joins on the last level");
     const size_t per_block = ((size_t)2 * MSM_TREE_THREADS * K0) << first;  // positions
     const unsigned blocks = (unsigned)((m + per_block - 1) / per_block);
-    k_msm_tree_upper<C, K0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, first, b.keys, b.vals, b.rec, b.slots, b.sinf);
+    k_msm_tree_upper<C, K0><<<blocks, MSM_TREE_THREADS, 0, s>>>(m, first, b.keys, b.vals, b.rec, b.slots);
     return cudaGetLastError();
 }
 
@@ -1353,7 +1377,6 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
     if (points_ready && (e = cudaStreamWaitEvent(s, points_ready, 0)) != cudaSuccess) return e;
     if (msm_affine()) {
         uint4 *rec = (uint4*)(base + p.off_rec), *slots = (uint4*)(base + p.off_slots);
-        uint8_t* sinf = base + p.off_sinf;
         k_msm_aos<C, CI><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, px, py, rec);
         uint32_t* win = (uint32_t*)(base + p.off_win);
         const bool fused = g_msm_form == 4 || g_msm_form == 5;
@@ -1382,7 +1405,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
             const size_t pos0 = (size_t)w0 * p.region, m = (size_t)(w1 - w0) * p.region;
             cudaStream_t hs = (g & 1) ? aux.stream : s;
             const size_t tiles_max = ((m + 1) / 2 + (size_t)MSM_TREE_THREADS * MSM_TREE_KMIN - 1) / ((size_t)MSM_TREE_THREADS * MSM_TREE_KMIN) + 1;
-            TreeBufs tb{keys2 + pos0, vals2 + pos0, rec, slots + (NL / 2) * pos0, sinf + pos0,
+            TreeBufs tb{keys2 + pos0, vals2 + pos0, rec, slots + (NL / 2) * pos0,
                         (uint4*)(base + p.off_pref) + (NL / 4) * (pos0 / 2),
                         (uint4*)(base + p.off_others) + (size_t)(NL / 4) * MSM_TREE_THREADS * tile_base,
                         (uint32_t*)(base + p.off_totals) + (size_t)2 * NL * (tile_base + (size_t)64 * g), tiles_max,
@@ -1414,7 +1437,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
             }
             if (e != cudaSuccess) return e;
             const uint32_t nw = w1 - w0;
-            k_msm_red_parts<CI><<<nw * 96, 128, 0, hs>>>(p.pairs, keys2, starts, slots, sinf, parts, w0);
+            k_msm_red_parts<CI><<<nw * 96, 128, 0, hs>>>(p.pairs, keys2, starts, slots, parts, w0);
             k_msm_red_fold<CI><<<nw * 24, 128, 0, hs>>>(parts, marg, w0);
             k_msm_red_weighted<CI><<<(nw * 3 + 3) / 4, 128, 0, hs>>>(marg, wsum, w0, w1);
             k_msm_red_shift<CI><<<1, (nw * 4 + 31) / 32 * 32, 0, hs>>>(wsum, win, w0, w1);
