@@ -358,7 +358,7 @@ k_msm_bucket_edges(uint32_t* __restrict__ buckets, const uint32_t* __restrict__ 
 // spread over slot s and the slots at multiples of 2^MSM_TREE_LEVELS inside (s, e): the tail
 // kernel (one thread per bucket) adds those few (mean run length is 32) with mixed Jacobian
 // additions and writes the bucket in the layout the reduction kernels read.
-// All formulas are complete: slots carry an infinity flag; equal points take the tangent,
+// All formulas are complete: the point at infinity is a slot whose x is all ones (slot_is_inf); equal points take the tangent,
 // opposite points give infinity (classification as batch_padd, batch_point.cpp:91-111).
 constexpr int MSM_TREE_LEVELS = 6;
 constexpr int MSM_TREE_THREADS = 128;
@@ -1388,7 +1388,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
         // behind the wide tree levels of the next.
         static const int groups_knob = [] { const char* v = getenv("GECC_MSM_GROUPS"); return v ? atoi(v) : 0; }();  // A/B timing
         const int want_groups = groups_knob >= 1 && groups_knob <= MSM_GROUPS ? groups_knob : MSM_GROUPS_DEFAULT;
-        const int G = (aux.stream && aux.fork && aux.join && split && !fused && n >= ((size_t)1 << 16)) ? want_groups : 1;
+        const int G = (aux.stream && aux.fork && aux.join && !fused && n >= ((size_t)1 << 16)) ? want_groups : 1;
         if (G > 1) {
             if ((e = cudaEventRecord(aux.fork, s)) != cudaSuccess) return e;
             if ((e = cudaStreamWaitEvent(aux.stream, aux.fork, 0)) != cudaSuccess) return e;
