@@ -92,6 +92,19 @@ k_msm_digits(size_t n, const uint32_t* __restrict__ scalars, const uint8_t* __re
     }
 }
 
+// The sorted pairs are ONE array of (bucket id, point index | sign) words: the scatter of the sort
+// writes a pair with a single 8-byte store (it is bound by the number of scattered write
+// transactions, not by bytes), and level 0 of the tree reads the two pairs of a join with one
+// 16-byte load.  PairKeys / PairVals are the two views the kernels index.
+struct PairKeys {
+    const uint2* p;
+    __device__ __forceinline__ uint32_t operator[](size_t i) const { return p[i].x; }
+};
+struct PairVals {
+    const uint2* p;
+    __device__ __forceinline__ uint32_t operator[](size_t i) const { return p[i].y; }
+};
+
 // ---------------------------------------------------------------- bucket sort (counting sort)
 // The pairs have to be grouped by bucket; nothing else about their order matters (a bucket's sum
 // does not depend on the order of its points).  Keys are w * 2^15 + m - 1 < 17 * 2^15, so this is
@@ -185,14 +198,14 @@ k_msm_scan_tops(uint32_t* __restrict__ block_totals, uint32_t region) {
 __global__ void __launch_bounds__(MSM_SCAN_THREADS)
 k_msm_scan_finish(const uint32_t* __restrict__ counts, const uint32_t* __restrict__ block_totals,
                   uint32_t* __restrict__ starts /* in: local prefixes */, uint32_t* __restrict__ cursor,
-                  uint32_t* __restrict__ keys_sorted, uint32_t region) {
+                  uint2* __restrict__ pairs_sorted, uint32_t region) {
     const uint32_t b = blockIdx.x * MSM_SCAN_THREADS + threadIdx.x;
     // the positions of a window's region behind its last pair hold "no bucket" (zero digits, points
     // at infinity, the rounding of the region; the carry window is almost all of that kind)
     for (uint32_t w = 0; w < MSM_WINDOWS; ++w) {
         const size_t end = (size_t)(w + 1) * region;
         for (size_t p = (size_t)w * region + block_totals[MSM_SCAN_BLOCKS + w] + b; p < end; p += (size_t)gridDim.x * MSM_SCAN_THREADS)
-            keys_sorted[p] = MSM_KEY_NONE;
+            pairs_sorted[p] = make_uint2(MSM_KEY_NONE, 0u);
     }
     if (b >= MSM_NB) return;
     const uint32_t at = starts[b] + block_totals[blockIdx.x];
@@ -203,7 +216,7 @@ k_msm_scan_finish(const uint32_t* __restrict__ counts, const uint32_t* __restric
 template <class C>
 __global__ void __launch_bounds__(256)
 k_msm_scatter(size_t n, const uint32_t* __restrict__ scalars, const uint8_t* __restrict__ pinf,
-              uint32_t* __restrict__ cursor, uint32_t* __restrict__ keys_sorted, uint32_t* __restrict__ vals_sorted) {
+              uint32_t* __restrict__ cursor, uint2* __restrict__ pairs_sorted) {
     // block b serves window b / blocks_per_window: the grid runs through the windows in order
     const unsigned bpw = (unsigned)((n + 255) / 256);
     const int w = (int)(blockIdx.x / bpw);
@@ -214,8 +227,7 @@ k_msm_scatter(size_t n, const uint32_t* __restrict__ scalars, const uint8_t* __r
     dg.pair(w, &key, &val);
     if (key == MSM_KEY_NONE) return;
     const uint32_t pos = atomicAdd(cursor + key, 1u);
-    keys_sorted[pos] = key;
-    vals_sorted[pos] = val;
+    pairs_sorted[pos] = make_uint2(key, val);
 }
 
 // first position whose key is >= bucket (sorted keys)
@@ -264,7 +276,7 @@ constexpr int MSM_SLICE = 32;
 
 template <class C>
 __global__ void __launch_bounds__(128)
-k_msm_buckets(size_t n, size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+k_msm_buckets(size_t n, size_t m, const PairKeys keys, const PairVals vals,
               const uint32_t* __restrict__ px, const uint32_t* __restrict__ py,
               uint32_t* __restrict__ buckets, uint32_t* __restrict__ edge, uint32_t* __restrict__ edge_key,
               size_t slices) {
@@ -474,8 +486,7 @@ struct TreeJoin {
 
 template <class C, bool LEVEL0>
 __device__ __forceinline__ TreeJoin<C, LEVEL0> tree_locate(size_t j, int level, size_t m,
-                                                           const uint32_t* __restrict__ keys,
-                                                           const uint32_t* __restrict__ vals) {
+                                                           const PairKeys keys, const PairVals vals) {
     TreeJoin<C, LEVEL0> t;
     t.active = t.copy2 = false;
     t.dst = t.src = 0;
@@ -483,17 +494,25 @@ __device__ __forceinline__ TreeJoin<C, LEVEL0> tree_locate(size_t j, int level, 
     if (LEVEL0) {
         const size_t a = 2 * j;
         if (a >= m) return t;
-        const uint32_t k0 = keys[a], k1 = a + 1 < m ? keys[a + 1] : 0xFFFFFFFFu;
+        // the two pairs of the join in one 16-byte load (a is even and the groups start on multiples of 64)
+        uint32_t k0, k1 = 0xFFFFFFFFu, va, vb = 0;
+        if (a + 1 < m) {
+            const uint4 q = *reinterpret_cast<const uint4*>(keys.p + a);
+            k0 = q.x; va = q.y; k1 = q.z; vb = q.w;
+        } else {
+            k0 = keys[a];
+            va = vals[a];
+        }
         if (k0 >= MSM_NB) return t;  // sorted: k1 is not a bucket either
         t.dst = a;
         t.src = a + 1;
-        t.v0 = vals[a];
+        t.v0 = va;
         if (k1 == k0) {
             t.active = true;
-            t.v1 = vals[a + 1];
+            t.v1 = vb;
         } else {
             t.copy2 = true;          // dst gets entry a; src gets entry a + 1 when it is a bucket
-            if (k1 < MSM_NB) t.v1 = vals[a + 1];
+            if (k1 < MSM_NB) t.v1 = vb;
             else t.src = (size_t)-1;
         }
         return t;
@@ -620,8 +639,8 @@ __device__ __forceinline__ void tree_apply(const TreeJoin<C, LEVEL0>& t, cfe<C>&
 // (prefix products in shared memory; the other warps wait while warp 0 inverts).
 template <class C, int K, bool LEVEL0>
 __global__ void __launch_bounds__(MSM_TREE_THREADS)
-k_msm_tree(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
-           const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
+k_msm_tree(size_t m, size_t joins, int level, const PairKeys keys,
+           const PairVals vals, const uint4* __restrict__ rec,
            uint4* slots) {
     using fe = cfe<C>;
     using jac = cjac<C>;
@@ -667,8 +686,8 @@ k_msm_tree(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
 // (6K + 8) / K products per addition.
 template <class C, int K, bool LEVEL0>
 __global__ void __launch_bounds__(MSM_TREE_THREADS, C::Fp::N > 8 ? 4 : 5)
-k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
-               const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
+k_msm_tree_fwd(size_t m, size_t joins, int level, const PairKeys keys,
+               const PairVals vals, const uint4* __restrict__ rec,
                const uint4* __restrict__ slots,
                uint4* __restrict__ pref, uint4* __restrict__ others, uint32_t* __restrict__ totals,
                size_t tiles, size_t tile0) {
@@ -699,8 +718,8 @@ k_msm_tree_fwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ k
 
 template <class C, int K, bool LEVEL0>
 __global__ void __launch_bounds__(MSM_TREE_THREADS, C::Fp::N > 8 ? 4 : 5)
-k_msm_tree_bwd(size_t m, size_t joins, int level, const uint32_t* __restrict__ keys,
-               const uint32_t* __restrict__ vals, const uint4* __restrict__ rec,
+k_msm_tree_bwd(size_t m, size_t joins, int level, const PairKeys keys,
+               const PairVals vals, const uint4* __restrict__ rec,
                uint4* slots, const uint4* __restrict__ pref,
                const uint4* __restrict__ others, const uint32_t* __restrict__ total_inv, size_t tiles,
                size_t tile0) {
@@ -743,7 +762,7 @@ constexpr int MSM_FUSED_KMIN = 4;
 
 template <class C, bool LEVEL0, int THREADS_ACTIVE, int NSM>
 __device__ __forceinline__ void tree_level_in_block(size_t m, int level, size_t j_first, int K, size_t joins,
-                                                    const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                                    const PairKeys keys, const PairVals vals,
                                                     const uint4* __restrict__ rec, uint4* slots,
                                                     uint32_t* sm_pref, uint32_t* sm_scan) {
     // the THREADS_ACTIVE calling threads (the whole block, or warp 0) take K joins each:
@@ -780,7 +799,7 @@ __device__ __forceinline__ void tree_level_in_block(size_t m, int level, size_t 
 
 template <class C, int K0>
 __global__ void __launch_bounds__(MSM_TREE_THREADS, K0 * C::Fp::N > 128 ? 2 : K0 * C::Fp::N > 64 ? 3 : 5)
-k_msm_tree_fused(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+k_msm_tree_fused(size_t m, const PairKeys keys, const PairVals vals,
                  const uint4* __restrict__ rec, uint4* slots) {
     constexpr int NL = C::Fp::N;
     constexpr int T = MSM_TREE_THREADS;
@@ -819,7 +838,7 @@ k_msm_tree_fused(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __
 // SM hide each other's inversions.
 template <class C, int K0>
 __global__ void __launch_bounds__(MSM_TREE_THREADS, C::Fp::N > 8 ? 4 : 5)
-k_msm_tree_upper(size_t m, int first, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+k_msm_tree_upper(size_t m, int first, const PairKeys keys, const PairVals vals,
                  const uint4* __restrict__ rec, uint4* slots) {
     constexpr int NL = C::Fp::N;
     constexpr int T = MSM_TREE_THREADS;
@@ -994,7 +1013,7 @@ __device__ __forceinline__ cjac<C> warp_sum_points(cjac<C> acc, int lane) {
 
 template <class C>
 __global__ void __launch_bounds__(128, 4)
-k_msm_red_parts(size_t m, const uint32_t* __restrict__ keys, const uint32_t* __restrict__ starts,
+k_msm_red_parts(size_t m, const PairKeys keys, const uint32_t* __restrict__ starts,
                 const uint4* __restrict__ slots,
                 uint32_t* __restrict__ parts, uint32_t w0) {
     using fe = cfe<C>;
@@ -1240,8 +1259,8 @@ static MsmPlan msm_plan(size_t n, int limbs) {
     size_t at = 0;
     auto take = [&](size_t bytes) { size_t o = at; at += align256(bytes); return o; };
     p.off_keys = p.off_vals = 0;  // unsorted pairs are never stored (the counting sort recodes)
-    p.off_keys2 = take(4 * p.pairs);
-    p.off_vals2 = take(4 * p.pairs);
+    p.off_keys2 = take(8 * p.pairs);  // (key, val) pairs
+    p.off_vals2 = p.off_keys2;
     p.slices = (p.pairs + MSM_SLICE - 1) / MSM_SLICE;
     p.off_buckets = take(jb * MSM_NB);
     p.off_parts = take(jb * MSM_RED_PARTS);
@@ -1270,7 +1289,8 @@ static MsmPlan msm_plan(size_t n, int limbs) {
 size_t msm_scratch_bytes(size_t n, int curve) { return n ? msm_plan(n, curve_limbs(curve)).total : 0; }
 
 struct TreeBufs {
-    const uint32_t *keys, *vals;
+    PairKeys keys;
+    PairVals vals;
     const uint4* rec;
     uint4* slots;
     uint4 *pref, *others;
@@ -1355,7 +1375,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
     MsmPlan p = msm_plan(n, NL);
     uint8_t* base = (uint8_t*)scratch;
     uint32_t *keys = (uint32_t*)(base + p.off_keys), *vals = (uint32_t*)(base + p.off_vals);
-    uint32_t *keys2 = (uint32_t*)(base + p.off_keys2), *vals2 = (uint32_t*)(base + p.off_vals2);
+    uint2* pairs2 = (uint2*)(base + p.off_keys2);
     uint32_t *buckets = (uint32_t*)(base + p.off_buckets), *parts = (uint32_t*)(base + p.off_parts);
     uint32_t *marg = (uint32_t*)(base + p.off_marg), *wsum = (uint32_t*)(base + p.off_wsum);
     (void)keys; (void)vals;  // the unsorted pairs are never stored: the scatter pass recodes
@@ -1369,8 +1389,8 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
     uint32_t* block_totals = cursor + MSM_NB;
     k_msm_scan_blocks<<<MSM_SCAN_BLOCKS, MSM_SCAN_THREADS, 0, s>>>(counts, starts, block_totals);
     k_msm_scan_tops<<<1, MSM_SCAN_THREADS, 0, s>>>(block_totals, (uint32_t)p.region);
-    k_msm_scan_finish<<<MSM_SCAN_BLOCKS, MSM_SCAN_THREADS, 0, s>>>(counts, block_totals, starts, cursor, keys2, (uint32_t)p.region);
-    k_msm_scatter<C><<<bpw * MSM_WINDOWS, 256, 0, s>>>(n, scalars, pinf, cursor, keys2, vals2);
+    k_msm_scan_finish<<<MSM_SCAN_BLOCKS, MSM_SCAN_THREADS, 0, s>>>(counts, block_totals, starts, cursor, pairs2, (uint32_t)p.region);
+    k_msm_scatter<C><<<bpw * MSM_WINDOWS, 256, 0, s>>>(n, scalars, pinf, cursor, pairs2);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     // digits and sort need the scalars (and the infinity mask) only: a host caller uploads the
     // points meanwhile and hands over the event that says they have arrived
@@ -1405,7 +1425,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
             const size_t pos0 = (size_t)w0 * p.region, m = (size_t)(w1 - w0) * p.region;
             cudaStream_t hs = (g & 1) ? aux.stream : s;
             const size_t tiles_max = ((m + 1) / 2 + (size_t)MSM_TREE_THREADS * MSM_TREE_KMIN - 1) / ((size_t)MSM_TREE_THREADS * MSM_TREE_KMIN) + 1;
-            TreeBufs tb{keys2 + pos0, vals2 + pos0, rec, slots + (NL / 2) * pos0,
+            TreeBufs tb{PairKeys{pairs2 + pos0}, PairVals{pairs2 + pos0}, rec, slots + (NL / 2) * pos0,
                         (uint4*)(base + p.off_pref) + (NL / 4) * (pos0 / 2),
                         (uint4*)(base + p.off_others) + (size_t)(NL / 4) * MSM_TREE_THREADS * tile_base,
                         (uint32_t*)(base + p.off_totals) + (size_t)2 * NL * (tile_base + (size_t)64 * g), tiles_max,
@@ -1437,7 +1457,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
             }
             if (e != cudaSuccess) return e;
             const uint32_t nw = w1 - w0;
-            k_msm_red_parts<CI><<<nw * 96, 128, 0, hs>>>(p.pairs, keys2, starts, slots, parts, w0);
+            k_msm_red_parts<CI><<<nw * 96, 128, 0, hs>>>(p.pairs, PairKeys{pairs2}, starts, slots, parts, w0);
             k_msm_red_fold<CI><<<nw * 24, 128, 0, hs>>>(parts, marg, w0);
             k_msm_red_weighted<CI><<<(nw * 3 + 3) / 4, 128, 0, hs>>>(marg, wsum, w0, w1);
             k_msm_red_shift<CI><<<1, (nw * 4 + 31) / 32 * 32, 0, hs>>>(wsum, win, w0, w1);
@@ -1456,7 +1476,7 @@ static cudaError_t run_msm(int curve, size_t n, const uint32_t* scalars, const u
         e = cudaMemsetAsync(buckets, 0, (size_t)12 * NL * MSM_NB, s);  // empty buckets = infinity (Z = 0)
         if (e != cudaSuccess) return e;
         const unsigned sb = (unsigned)((p.slices + 127) / 128);
-        k_msm_buckets<C><<<sb, 128, 0, s>>>(n, p.pairs, keys2, vals2, px, py, buckets, edge, edge_key, p.slices);
+        k_msm_buckets<C><<<sb, 128, 0, s>>>(n, p.pairs, PairKeys{pairs2}, PairVals{pairs2}, px, py, buckets, edge, edge_key, p.slices);
         k_msm_bucket_edges<C><<<sb, 128, 0, s>>>(buckets, edge, edge_key, p.slices);
         *launches = 5 + 2;
     }
