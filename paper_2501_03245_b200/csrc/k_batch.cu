@@ -607,6 +607,12 @@ cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* 
                                 cudaStream_t s) {
     if (n == 0) return cudaSuccess;
     if (curve_is_bls(curve)) {  // 12-limb base fields / their 8-limb scalar fields: cooperative form
+        if (field == 0 && n <= ((size_t)1 << 15)) {  // small batches (the MSM's level totals): one element per thread
+            const unsigned c1 = coop_blocks(n, 128, 1);
+            if (curve == CURVE_BLS381) k_batch_invert_coop<Bls381P, 128, 1><<<c1, 128, 0, s>>>(n, in, out);
+            else k_batch_invert_coop<Bls377P, 128, 1><<<c1, 128, 0, s>>>(n, in, out);
+            return cudaGetLastError();
+        }
         const unsigned cb = coop_blocks(n, 128);
         if (curve == CURVE_BLS381) {
             if (field == 0) k_batch_invert_coop<Bls381P, 128><<<cb, 128, 0, s>>>(n, in, out);
@@ -653,7 +659,10 @@ cudaError_t launch_batch_invert(int curve, int field, size_t n, const uint32_t* 
 // block totals of the MSM tree when it runs on the lazy plain secp256k1 field (plain in, plain out)
 cudaError_t launch_batch_invert_secp_lazy(size_t n, const uint32_t* in, uint32_t* out, cudaStream_t s) {
     if (n == 0) return cudaSuccess;
-    k_batch_invert_coop<SecpPL, 128><<<coop_blocks(n, 128), 128, 0, s>>>(n, in, out);
+    // the totals of a tree level / a fused batch_padd half: a few thousand elements whose inversion is pure
+    // latency -- one element per thread (the shortest chain) while that still fits one wave
+    if (n <= ((size_t)1 << 15)) k_batch_invert_coop<SecpPL, 128, 1><<<coop_blocks(n, 128, 1), 128, 0, s>>>(n, in, out);
+    else k_batch_invert_coop<SecpPL, 128><<<coop_blocks(n, 128), 128, 0, s>>>(n, in, out);
     return cudaGetLastError();
 }
 
