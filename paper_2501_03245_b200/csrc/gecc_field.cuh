@@ -669,23 +669,32 @@ GECC_HD fe redc_sm2(const F& f, const uint32_t* tin) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) t[i] = tin[i];
     t[16] = 0;
+    // FOUR words per pass (two passes instead of the reference's four two-word passes, same value):
+    // the multipliers of words j+2, j+3 are what words j, j+1 leave there,
+    //   m2 = t[j+2] + m0            (the add chain's first step)
+    //   m3 = t[j+3] + m1 + carry - m0
+    // and from position j+4 on every position receives at most one positive and one negative term of
+    // the four eliminations, so ONE add chain and ONE sub chain apply them all:
+    //   +m0 +m1 +m2 +m3 @ j+2 .. j+5 and @ j+8 .. j+11;  -m0 @ j+3, j+7; -m1 @ j+4, j+8; -m2 @ j+5, j+9; -m3 @ j+6, j+10
+    // 52 chain operations per reduction instead of 92, and half the depth.
 #pragma unroll
-    for (int j = 0; j < 8; j += 2) {
+    for (int j = 0; j < 8; j += 4) {
         const uint32_t m0 = t[j], m1 = t[j + 1];
-        // positive contributions: +m0 @ j+2, +m1 @ j+3, +m0 @ j+8, +m1 @ j+9
-        t[j + 2] = add_cc(t[j + 2], m0);
-        t[j + 3] = addc_cc(t[j + 3], m1);
+        const uint32_t m2 = add_cc(t[j + 2], m0);
+        const uint32_t u3 = addc_cc(t[j + 3], m1);
+        const uint32_t m3 = u3 - m0;  // plain subtraction: leaves the carry flag of the chain alone
+        t[j + 4] = addc_cc(t[j + 4], m2);
+        t[j + 5] = addc_cc(t[j + 5], m3);
 #pragma unroll
-        for (int w = j + 4; w < 17; ++w) {
-            const uint32_t d = (w == j + 8) ? m0 : (w == j + 9) ? m1 : 0u;
+        for (int w = j + 6; w < 17; ++w) {
+            const uint32_t d = (w == j + 8) ? m0 : (w == j + 9) ? m1 : (w == j + 10) ? m2 : (w == j + 11) ? m3 : 0u;
             t[w] = addc_cc(t[w], d);
         }
-        // negative contributions: -m0 @ j+3, -m1 @ j+4, -m0 @ j+7, -m1 @ j+8
-        t[j + 3] = sub_cc(t[j + 3], m0);
-        t[j + 4] = subc_cc(t[j + 4], m1);
+        sub_cc(u3, m0);  // position j+3 again, for its borrow (the word itself is eliminated)
 #pragma unroll
-        for (int w = j + 5; w < 17; ++w) {
-            const uint32_t d = (w == j + 7) ? m0 : (w == j + 8) ? m1 : 0u;
+        for (int w = j + 4; w < 17; ++w) {
+            const uint32_t d = (w == j + 4 || w == j + 8) ? m1 : (w == j + 5 || w == j + 9) ? m2
+                             : (w == j + 6 || w == j + 10) ? m3 : (w == j + 7) ? m0 : 0u;
             t[w] = subc_cc(t[w], d);
         }
     }
