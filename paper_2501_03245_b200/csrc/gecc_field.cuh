@@ -260,10 +260,80 @@ GECC_HD fe redc_secp_lazy(const uint32_t* t) {
     return r;
 }
 
+// ---------------------------------------------------------------- lazy SM2 field
+// KIND_SM2_LAZY: the SM2 prime in MONTGOMERY form (R = 2^256: the constants and tables of Sm2P
+// serve), elements only WEAKLY reduced -- any 256-bit value congruent to the element.  2^256 == c
+// (mod q) with c = 2^256 - q = 2^224 + 2^96 - 2^64 + 1 = limbs {1, 0, 0xFFFFFFFF, 0, 0, 0, 0, 1}: a
+// carry out of an addition is folded back by adding c under a mask and a borrow by subtracting it
+// (one more 8-limb chain instead of a trial subtraction and a select), a second wrap (probability
+// 2^-32) sits behind a branch.  The Montgomery reduction ends with the same fold instead of the
+// conditional subtraction.  Canonical form only where a value leaves the field layer.
+template <class F>
+GECC_HD fe weak_canon(const F& f, const fe& a) {  // a in [0, 2^256) -> a mod q (q > 2^255: one subtraction)
+    fe d;
+    d.w[0] = sub_cc(a.w[0], f.q(0));
+#pragma unroll
+    for (int i = 1; i < 8; ++i) d.w[i] = subc_cc(a.w[i], f.q(i));
+    const uint32_t borrow = subc(0, 0);
+    return fe_select(borrow == 0, d, a);
+}
+GECC_HD fe sm2l_fold_carry(const fe& s, uint32_t k) {  // (k : s) -> s + k c, k = 0 or 1
+    const uint32_t m = 0u - k;
+    fe r;
+    r.w[0] = add_cc(s.w[0], k);
+    r.w[1] = addc_cc(s.w[1], 0);
+    r.w[2] = addc_cc(s.w[2], m);
+#pragma unroll
+    for (int i = 3; i < 7; ++i) r.w[i] = addc_cc(s.w[i], 0);
+    r.w[7] = addc_cc(s.w[7], k);
+    if (addc(0, 0)) {  // s >= q and k: what is left is below c, one more c cannot wrap
+        r.w[0] = add_cc(r.w[0], 1u);
+        r.w[1] = addc_cc(r.w[1], 0);
+        r.w[2] = addc_cc(r.w[2], 0xFFFFFFFFu);
+#pragma unroll
+        for (int i = 3; i < 7; ++i) r.w[i] = addc_cc(r.w[i], 0);
+        r.w[7] = addc_cc(r.w[7], 1u);
+    }
+    return r;
+}
+GECC_HD fe sm2l_add(const fe& a, const fe& b) {
+    fe s;
+    s.w[0] = add_cc(a.w[0], b.w[0]);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) s.w[i] = addc_cc(a.w[i], b.w[i]);
+    return sm2l_fold_carry(s, addc(0, 0));
+}
+GECC_HD fe sm2l_sub(const fe& a, const fe& b) {
+    fe d;
+    d.w[0] = sub_cc(a.w[0], b.w[0]);
+#pragma unroll
+    for (int i = 1; i < 8; ++i) d.w[i] = subc_cc(a.w[i], b.w[i]);
+    const uint32_t k = subc(0, 0) & 1u;  // borrowed: d = a - b + 2^256 == a - b + c, so take c off
+    const uint32_t m = 0u - k;
+    fe r;
+    r.w[0] = sub_cc(d.w[0], k);
+    r.w[1] = subc_cc(d.w[1], 0);
+    r.w[2] = subc_cc(d.w[2], m);
+#pragma unroll
+    for (int i = 3; i < 7; ++i) r.w[i] = subc_cc(d.w[i], 0);
+    r.w[7] = subc_cc(d.w[7], k);
+    if (subc(0, 0)) {  // d < c and k: wrapped once more, take c off again (cannot wrap a third time)
+        r.w[0] = sub_cc(r.w[0], 1u);
+        r.w[1] = subc_cc(r.w[1], 0);
+        r.w[2] = subc_cc(r.w[2], 0xFFFFFFFFu);
+#pragma unroll
+        for (int i = 3; i < 7; ++i) r.w[i] = subc_cc(r.w[i], 0);
+        r.w[7] = subc_cc(r.w[7], 1u);
+    }
+    return r;
+}
+template <class F>
+constexpr bool field_is_weak() { return F::kind == KIND_SECP_LAZY || F::kind == KIND_SM2_LAZY; }
+
 // field-aware predicates: canonical fields compare limbs, the lazy field compares mod q
 template <class F>
 GECC_HD bool fe_is_zero(const F& f, const fel<F>& a) {
-    if constexpr (F::kind == KIND_SECP_LAZY) return lazy_is_zero(f, a);
+    if constexpr (field_is_weak<F>()) return lazy_is_zero(f, a);
     else return fe_is_zero(a);
 }
 
@@ -271,6 +341,7 @@ GECC_HD bool fe_is_zero(const F& f, const fel<F>& a) {
 template <class F>
 GECC_HD fel<F> fe_add(const F& f, const fel<F>& a, const fel<F>& b) {
     if constexpr (F::kind == KIND_SECP_LAZY) return lazy_add(a, b);
+    if constexpr (F::kind == KIND_SM2_LAZY) return sm2l_add(a, b);
     constexpr int N = F::N;
     fel<F> s, d;
     s.w[0] = add_cc(a.w[0], b.w[0]);
@@ -287,6 +358,7 @@ GECC_HD fel<F> fe_add(const F& f, const fel<F>& a, const fel<F>& b) {
 template <class F>
 GECC_HD fel<F> fe_sub(const F& f, const fel<F>& a, const fel<F>& b) {
     if constexpr (F::kind == KIND_SECP_LAZY) return lazy_sub(a, b);
+    if constexpr (F::kind == KIND_SM2_LAZY) return sm2l_sub(a, b);
     constexpr int N = F::N;
     fel<F> d, e;
     d.w[0] = sub_cc(a.w[0], b.w[0]);
@@ -301,6 +373,7 @@ GECC_HD fel<F> fe_sub(const F& f, const fel<F>& a, const fel<F>& b) {
 template <class F>
 GECC_HD bool fe_eq(const F& f, const fel<F>& a, const fel<F>& b) {
     if constexpr (F::kind == KIND_SECP_LAZY) return lazy_is_zero(f, lazy_sub(a, b));
+    else if constexpr (F::kind == KIND_SM2_LAZY) return lazy_is_zero(f, sm2l_sub(a, b));
     else return fe_eq(a, b);
 }
 template <class F>
@@ -701,14 +774,28 @@ GECC_HD fe redc_sm2(const F& f, const uint32_t* tin) {
     fe r;
 #pragma unroll
     for (int i = 0; i < 8; ++i) r.w[i] = t[8 + i];
-    return final_sub(f, r, t[16]);
+    if constexpr (F::kind == KIND_SM2_LAZY) {
+        // weakly reduced inputs: the value is below 2^256 + q, so t[16] is 0 or 1 and folding it
+        // (+ c under a mask) cannot wrap: what is left of a set top word is below q
+        const uint32_t k = t[16], m = 0u - k;
+        fe o;
+        o.w[0] = add_cc(r.w[0], k);
+        o.w[1] = addc_cc(r.w[1], 0);
+        o.w[2] = addc_cc(r.w[2], m);
+#pragma unroll
+        for (int i = 3; i < 7; ++i) o.w[i] = addc_cc(r.w[i], 0);
+        o.w[7] = addc(r.w[7], k);
+        return o;
+    } else {
+        return final_sub(f, r, t[16]);
+    }
 }
 
 template <class F>
 GECC_HD fel<F> redc(const F& f, const uint32_t* t) {
     if constexpr (F::kind == KIND_SECP_P) return redc_secp(f, t);
     else if constexpr (F::kind == KIND_SECP_LAZY) return redc_secp_lazy(t);
-    else if constexpr (F::kind == KIND_SM2_P) return redc_sm2(f, t);
+    else if constexpr (F::kind == KIND_SM2_P || F::kind == KIND_SM2_LAZY) return redc_sm2(f, t);
     else return redc_ws(f, t);
 }
 
@@ -878,7 +965,8 @@ GECC_HD fel<F> fe_from_mont(const F& f, const fel<F>& a) {  // a * R^-1
         t[i] = a.w[i];
         t[F::N + i] = 0;
     }
-    return redc(f, t);
+    if constexpr (F::kind == KIND_SM2_LAZY) return weak_canon(f, redc(f, t));
+    else return redc(f, t);
 }
 
 // a^(q-2) in Montgomery form, 4-bit fixed window: 256 squarings + 64 + 14 products.

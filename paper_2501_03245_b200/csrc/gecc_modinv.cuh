@@ -496,6 +496,12 @@ __device__ __noinline__ fel<F> safegcd_inverse_warp(const F& fld, const fel<F>& 
 template <class F>
 __device__ __forceinline__ fel<F> fe_inv_warp(const F& f, const fel<F>& a) {
     if constexpr (F::kind == KIND_SECP_LAZY) return safegcd_inverse_warp<GECC_WARP_INV_VAR>(f, lazy_canon(f, a));
+    if constexpr (F::kind == KIND_SM2_LAZY) {
+        fe r3l;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r3l.w[i] = f.r3(i);
+        return fe_mul(f, safegcd_inverse_warp<GECC_WARP_INV_VAR>(f, weak_canon(f, a)), r3l);
+    }
     fel<F> r3;
 #pragma unroll
     for (int i = 0; i < F::N; ++i) r3.w[i] = f.r3(i);
@@ -507,6 +513,12 @@ __device__ __forceinline__ fel<F> fe_inv_warp(const F& f, const fel<F>& a) {
 template <class F>
 GECC_HD fel<F> fe_inv_var(const F& f, const fel<F>& a) {
     if constexpr (F::kind == KIND_SECP_LAZY) return safegcd_inverse_var(f, lazy_canon(f, a));
+    if constexpr (F::kind == KIND_SM2_LAZY) {
+        fe r3l;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r3l.w[i] = f.r3(i);
+        return fe_mul(f, safegcd_inverse_var(f, weak_canon(f, a)), r3l);
+    }
     fel<F> r3;
 #pragma unroll
     for (int i = 0; i < F::N; ++i) r3.w[i] = f.r3(i);
@@ -517,6 +529,12 @@ GECC_HD fel<F> fe_inv_var(const F& f, const fel<F>& a) {
 template <class F>
 GECC_HD fel<F> fe_inv(const F& f, const fel<F>& a) {
     if constexpr (F::kind == KIND_SECP_LAZY) return safegcd_inverse(f, lazy_canon(f, a));  // plain in, plain out
+    if constexpr (F::kind == KIND_SM2_LAZY) {  // weakly reduced Montgomery in, Montgomery out
+        fe r3l;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r3l.w[i] = f.r3(i);
+        return fe_mul(f, safegcd_inverse(f, weak_canon(f, a)), r3l);
+    }
     fel<F> r3;
 #pragma unroll
     for (int i = 0; i < F::N; ++i) r3.w[i] = f.r3(i);

@@ -28,6 +28,7 @@ FIELDS = {
     "Sm2P": 2**256 - 2**224 - 2**96 + 2**64 - 1,
     "Sm2N": 0xFFFFFFFEFFFFFFFFFFFFFFFFFFFFFFFF7203DF6B21C6052B53BBF40939D54123,
     "SecpPL": 2**256 - 2**32 - 977,
+    "Sm2PL": 2**256 - 2**224 - 2**96 + 2**64 - 1,
     # BLS12-381: 381-bit base field (12 limbs) and 255-bit scalar field (8 limbs)
     "Bls381P": 0x1a0111ea397fe69a4b1ba7b6434bacd764774b84f38512bf6730d2a0f6b0f6241eabfffeb153ffffb9feffffffffaaab,
     "Bls381R": 0x73eda753299d7d483339d80809a1d80553bda402fffe5bfeffffffff00000001,
@@ -37,11 +38,13 @@ FIELDS = {
 }
 LIMBS = {"Bls381P": 12, "Bls377P": 12}
 KIND = {"SecpP": "KIND_SECP_P", "SecpN": "KIND_GENERIC", "Sm2P": "KIND_SM2_P", "Sm2N": "KIND_GENERIC",
-        "SecpPL": "KIND_SECP_LAZY", "Bls381P": "KIND_GENERIC", "Bls381R": "KIND_GENERIC",
+        "SecpPL": "KIND_SECP_LAZY", "Sm2PL": "KIND_SM2_LAZY", "Bls381P": "KIND_GENERIC", "Bls381R": "KIND_GENERIC",
         "Bls377P": "KIND_GENERIC", "Bls377R": "KIND_GENERIC"}
 # SecpPL: the same prime as SecpP in a plain (non-Montgomery), weakly reduced representation
 # used inside the fused ECDSA kernels: "R" is 1, elements live in [0, 2^256).
 PLAIN = {"SecpPL"}
+# Sm2PL: the SM2 prime in MONTGOMERY form (R = 2^256, the tables and constants of Sm2P serve), weakly
+# reduced: any 256-bit value congruent to the element; used inside the fused ECDSA kernels.
 
 CURVES = {
     "Secp": dict(fp="SecpP", fn="SecpN", a=0, b=7,
@@ -52,6 +55,11 @@ CURVES = {
                   gx=0x79BE667EF9DCBBAC55A06295CE870B07029BFCDB2DCE28D959F2815B16F81798,
                   gy=0x483ADA7726A3C4655DA4FBFC0E1108A8FD17B448A68554199C47D08FFB10D4B8,
                   a_kind="A_ZERO"),
+    "Sm2L": dict(fp="Sm2PL", fn="Sm2N", a=FIELDS["Sm2P"] - 3,
+                 b=0x28E9FA9E9D9F5E344D5A9E4BCF6509A7F39789F515AB8F92DDBCBD414D940E93,
+                 gx=0x32C4AE2C1F1981195F9904466A39C9948FE30BBFF2660BE1715A4589334C74C7,
+                 gy=0xBC3736A2F4F6779C59BDCEE36B692153D0A9877CC62A474002DF32E52139F0A0,
+                 a_kind="A_MINUS3"),
     "Sm2": dict(fp="Sm2P", fn="Sm2N", a=FIELDS["Sm2P"] - 3,
                 b=0x28E9FA9E9D9F5E344D5A9E4BCF6509A7F39789F515AB8F92DDBCBD414D940E93,
                 gx=0x32C4AE2C1F1981195F9904466A39C9948FE30BBFF2660BE1715A4589334C74C7,
@@ -84,7 +92,7 @@ def main():
     w = out.append
     w("// GENERATED by gen_consts.py -- do not edit.\n#pragma once\n#include \"gecc_prims.cuh\"\n")
     w("namespace gecc {\n")
-    w("enum FieldKind { KIND_GENERIC = 0, KIND_SECP_P = 1, KIND_SM2_P = 2, KIND_SECP_LAZY = 3 };")
+    w("enum FieldKind { KIND_GENERIC = 0, KIND_SECP_P = 1, KIND_SM2_P = 2, KIND_SECP_LAZY = 3, KIND_SM2_LAZY = 4 };")
     w("enum CurveA { A_ZERO = 0, A_MINUS3 = 1, A_GENERIC = 2 };\n")
     for name, q in FIELDS.items():
         nl = LIMBS.get(name, 8)

@@ -301,6 +301,10 @@ static int blocks_for(size_t n, int threads) { return (int)((n + threads - 1) / 
 // representation (SecpLCurve, its own fixed-base table); the column-buffer kernels keep
 // the reference's Montgomery form (SecpCurve) because that is their I/O contract.
 using SecpEcdsaCurve = SecpLCurve;
+// SM2 likewise computes on its weakly reduced Montgomery field inside the byte-record kernels
+// (Sm2LCurve: same Montgomery form and the same fixed-base table, carry / borrow folds instead of
+// trial subtractions); the column-buffer kernels keep the canonical field.
+using Sm2EcdsaCurve = Sm2LCurve;
 
 template <class C, int THREADS, int BLOCKS_PER_SM>
 static cudaError_t launch_verify_t(size_t n, const uint8_t* dig, const uint8_t* pub, const uint8_t* sig,
@@ -330,7 +334,7 @@ cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t
     }();
     if (use_smem || !lane_scratch || scratch_lanes == 0) {
         if (curve == CURVE_SECP) return launch_verify_t<SecpEcdsaCurve, 128, 3>(n, dig, pub, sig, gtab, res, s);
-        return launch_verify_t<Sm2Curve, 128, 3>(n, dig, pub, sig, gtab, res, s);
+        return launch_verify_t<Sm2EcdsaCurve, 128, 3>(n, dig, pub, sig, gtab, res, s);
     }
     // kernels on one stream run back to back, so consecutive pieces may reuse the scratch
     // 4 blocks per SM (128 registers) measured best: 3 / 4 / 5 / 6 blocks = 26.4 / 25.5 / 27.1 / 29.2 ms
@@ -342,7 +346,7 @@ cudaError_t launch_verify(int curve, size_t n, const uint8_t* dig, const uint8_t
             k_verify_gtab<SecpEcdsaCurve, 128, GECC_VERIFY_BLOCKS><<<b, 128, slot_bytes, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at,
                                                                              gtab, lane_scratch, res + at);
         else
-            k_verify_gtab<Sm2Curve, 128, GECC_VERIFY_BLOCKS_SM2><<<b, 128, slot_bytes, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at, gtab,
+            k_verify_gtab<Sm2EcdsaCurve, 128, GECC_VERIFY_BLOCKS_SM2><<<b, 128, slot_bytes, s>>>(m, dig + 32 * at, pub + 65 * at, sig + 64 * at, gtab,
                                                                        lane_scratch, res + at);
     }
     return cudaGetLastError();
@@ -362,8 +366,8 @@ cudaError_t launch_secret_range(int curve, size_t n, const uint8_t* sec, uint32_
             if (uniform) KERNEL<SecpEcdsaCurve, true><<<GRID, THREADS, SMEM, s>>>(__VA_ARGS__);    \
             else KERNEL<SecpEcdsaCurve, false><<<GRID, THREADS, SMEM, s>>>(__VA_ARGS__);           \
         } else {                                                                                   \
-            if (uniform) KERNEL<Sm2Curve, true><<<GRID, THREADS, SMEM, s>>>(__VA_ARGS__);          \
-            else KERNEL<Sm2Curve, false><<<GRID, THREADS, SMEM, s>>>(__VA_ARGS__);                 \
+            if (uniform) KERNEL<Sm2EcdsaCurve, true><<<GRID, THREADS, SMEM, s>>>(__VA_ARGS__);     \
+            else KERNEL<Sm2EcdsaCurve, false><<<GRID, THREADS, SMEM, s>>>(__VA_ARGS__);            \
         }                                                                                          \
     } while (0)
 #define GECC_BY_CURVE_MODE(curve, uniform, KERNEL, GRID, THREADS, ...) \

@@ -63,6 +63,7 @@ int hs_field_op(int field, const FieldRT* rt, int op, size_t n, const uint32_t* 
         case 3: return field_op_t(Sm2N{}, op, n, a, b, out);
         case 4: return field_op_t(*rt, op, n, a, b, out);
         case 5: return field_op_t(SecpPL{}, op, n, a, b, out);  // lazy plain secp256k1 (outputs weakly reduced)
+        case 10: return field_op_t(Sm2PL{}, op, n, a, b, out);  // lazy Montgomery SM2 (outputs weakly reduced)
         case 6: return field_op_t(Bls381P{}, op, n, a, b, out);  // 12 limbs
         case 7: return field_op_t(Bls381R{}, op, n, a, b, out);
         case 8: return field_op_t(Bls377P{}, op, n, a, b, out);  // 12 limbs
@@ -278,27 +279,27 @@ int keygen_t(size_t n, uint64_t seed, uint64_t base, uint8_t* sec, uint8_t* pub)
 
 extern "C" {
 int hs_fpmul(int curve, size_t n, const uint32_t* k, uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
-    return curve == 0 ? fpmul_t<Sm2Curve>(n, k, ox, oy, oinf) : curve == 2 ? fpmul_t<SecpLCurve>(n, k, ox, oy, oinf) : fpmul_t<SecpCurve>(n, k, ox, oy, oinf);
+    return curve == 0 ? fpmul_t<Sm2Curve>(n, k, ox, oy, oinf) : curve == 3 ? fpmul_t<Sm2LCurve>(n, k, ox, oy, oinf) : curve == 2 ? fpmul_t<SecpLCurve>(n, k, ox, oy, oinf) : fpmul_t<SecpCurve>(n, k, ox, oy, oinf);
 }
 int hs_upmul(int curve, size_t n, const uint32_t* k, const uint32_t* px, const uint32_t* py,
              const uint8_t* pinf, uint32_t* ox, uint32_t* oy, uint8_t* oinf) {
-    return curve == 0 ? upmul_t<Sm2Curve>(n, k, px, py, pinf, ox, oy, oinf) : curve == 2 ? upmul_t<SecpLCurve>(n, k, px, py, pinf, ox, oy, oinf) : upmul_t<SecpCurve>(n, k, px, py, pinf, ox, oy, oinf);
+    return curve == 0 ? upmul_t<Sm2Curve>(n, k, px, py, pinf, ox, oy, oinf) : curve == 3 ? upmul_t<Sm2LCurve>(n, k, px, py, pinf, ox, oy, oinf) : curve == 2 ? upmul_t<SecpLCurve>(n, k, px, py, pinf, ox, oy, oinf) : upmul_t<SecpCurve>(n, k, px, py, pinf, ox, oy, oinf);
 }
 int hs_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, uint64_t seed,
             uint64_t base, uint8_t* sig, int32_t* st) {
-    return curve == 0 ? sign_t<Sm2Curve>(n, dig, sec, seed, base, sig, st) : curve == 2 ? sign_t<SecpLCurve>(n, dig, sec, seed, base, sig, st) : sign_t<SecpCurve>(n, dig, sec, seed, base, sig, st);
+    return curve == 0 ? sign_t<Sm2Curve>(n, dig, sec, seed, base, sig, st) : curve == 3 ? sign_t<Sm2LCurve>(n, dig, sec, seed, base, sig, st) : curve == 2 ? sign_t<SecpLCurve>(n, dig, sec, seed, base, sig, st) : sign_t<SecpCurve>(n, dig, sec, seed, base, sig, st);
 }
 int hs_verify(int curve, size_t n, const uint8_t* dig, const uint8_t* pub, const uint8_t* sig,
               uint8_t* res) {
-    return curve == 0 ? verify_t<Sm2Curve>(n, dig, pub, sig, res) : curve == 2 ? verify_t<SecpLCurve>(n, dig, pub, sig, res) : verify_t<SecpCurve>(n, dig, pub, sig, res);
+    return curve == 0 ? verify_t<Sm2Curve>(n, dig, pub, sig, res) : curve == 3 ? verify_t<Sm2LCurve>(n, dig, pub, sig, res) : curve == 2 ? verify_t<SecpLCurve>(n, dig, pub, sig, res) : verify_t<SecpCurve>(n, dig, pub, sig, res);
 }
 void hs_set_uniform(int on) { g_uniform = on; }
 int hs_sign_nonces(int curve, size_t n, const uint8_t* dig, const uint8_t* sec, const uint8_t* nonces,
                    uint8_t* sig, int32_t* st) {
-    return curve == 0 ? sign_nonces_t<Sm2Curve>(n, dig, sec, nonces, sig, st) : curve == 2 ? sign_nonces_t<SecpLCurve>(n, dig, sec, nonces, sig, st) : sign_nonces_t<SecpCurve>(n, dig, sec, nonces, sig, st);
+    return curve == 0 ? sign_nonces_t<Sm2Curve>(n, dig, sec, nonces, sig, st) : curve == 3 ? sign_nonces_t<Sm2LCurve>(n, dig, sec, nonces, sig, st) : curve == 2 ? sign_nonces_t<SecpLCurve>(n, dig, sec, nonces, sig, st) : sign_nonces_t<SecpCurve>(n, dig, sec, nonces, sig, st);
 }
 int hs_keygen(int curve, size_t n, uint64_t seed, uint64_t base, uint8_t* sec, uint8_t* pub) {
-    return curve == 0 ? keygen_t<Sm2Curve>(n, seed, base, sec, pub) : curve == 2 ? keygen_t<SecpLCurve>(n, seed, base, sec, pub) : keygen_t<SecpCurve>(n, seed, base, sec, pub);
+    return curve == 0 ? keygen_t<Sm2Curve>(n, seed, base, sec, pub) : curve == 3 ? keygen_t<Sm2LCurve>(n, seed, base, sec, pub) : curve == 2 ? keygen_t<SecpLCurve>(n, seed, base, sec, pub) : keygen_t<SecpCurve>(n, seed, base, sec, pub);
 }
 }  // extern "C"
 

@@ -33,6 +33,8 @@ OPS = dict(mont_mul=0, mod_add=1, mod_sub=2, to_mont=3, from_mont=4, mod_inv=5, 
 
 SECP_LAZY_CURVE = 2   # secp256k1 in the lazy plain representation (ECDSA kernels)
 SECP_LAZY_FIELD = 5
+SM2_LAZY_CURVE = 3    # SM2 in weakly reduced Montgomery form (ECDSA kernels)
+SM2_LAZY_FIELD = 10
 
 
 BLS_P_FIELD, BLS_R_FIELD = 6, 7   # BLS12-381 base field (12 limbs) and scalar field (8 limbs)

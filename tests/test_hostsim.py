@@ -164,9 +164,48 @@ def test_hostsim_lazy_secp_field():
     assert all((g * x) % p == 1 if x % p else g == 0 for g, x in zip(inv, a[:400]))
 
 
-def test_hostsim_lazy_curve_ecdsa_golden():
-    ent = ECDSA["secp256k1"]
-    cid, n = H.SECP_LAZY_CURVE, ent["n"]
+def test_hostsim_lazy_sm2_field():
+    """The weakly reduced Montgomery SM2 field of the fused ECDSA kernels on NON-canonical inputs
+    (q, q + 1, 2^256 - 1, values around c = 2^256 - q ...), against Python integers mod q; every pair
+    of edge values drives the second-wrap branches of the carry / borrow folds."""
+    p = E.SM2.p
+    c = (1 << 256) - p
+    rinv = pow(1 << 256, -1, p)
+    rng = random.Random(12)
+    special = [0, 1, p - 1, p, p + 1, 2**256 - 1, 2**256 - 2, c, c - 1, c + 1, 2 * c, 2**255, p - c, 2**224, 2**96 - 2**64, 5]
+    a = special + [rng.randrange(1 << 256) for _ in range(5000)]
+    b = special[::-1] + [rng.randrange(1 << 256) for _ in range(5000)]
+    A, B = O.ints_to_cols(a), O.ints_to_cols(b)
+    f = H.SM2_LAZY_FIELD
+    for op, fn in (("mont_mul", lambda x, y: x * y * rinv), ("mod_add", lambda x, y: x + y),
+                   ("mod_sub", lambda x, y: x - y), ("sqr", lambda x, y: x * x * rinv), ("dbl", lambda x, y: 2 * x),
+                   ("mul8", lambda x, y: 8 * x)):
+        got = O.cols_to_ints(H.field_op(0, 0, op, A, B, field_id=f))
+        assert all(g % p == fn(x, y) % p and g < (1 << 256) for g, x, y in zip(got, a, b)), op
+    assert O.cols_to_ints(H.field_op(0, 0, "from_mont", A, field_id=f)) == [x * rinv % p for x in a]
+    assert all(g % p == x * (1 << 256) % p for g, x in zip(O.cols_to_ints(H.field_op(0, 0, "to_mont", A, field_id=f)), a))
+    edge = special + [2**64 - 1, 2**64, 2**256 - 2**64, 2**256 - c, 2**256 - c - 1, 2**256 - c + 1, 2**96, 2**224 - 1, (1 << 256) - (1 << 33)]
+    xa = [x for x in edge for _ in edge]
+    xb = [y for _ in edge for y in edge]
+    XA, XB = O.ints_to_cols(xa), O.ints_to_cols(xb)
+    for op, fn in (("mont_mul", lambda x, y: x * y * rinv), ("mod_add", lambda x, y: x + y), ("mod_sub", lambda x, y: x - y)):
+        got = O.cols_to_ints(H.field_op(0, 0, op, XA, XB, field_id=f))
+        assert all(g % p == fn(x, y) % p for g, x, y in zip(got, xa, xb)), op
+    # canonical inputs: the lazy field's values equal the canonical field's mod q
+    ca = O.ints_to_cols([x % p for x in a[:2000]])
+    cb = O.ints_to_cols([x % p for x in b[:2000]])
+    want = O.cols_to_ints(O.field_op(0, 0, "mont_mul", ca, cb))
+    assert [g % p for g in O.cols_to_ints(H.field_op(0, 0, "mont_mul", ca, cb, field_id=f))] == want
+    R = 1 << 256
+    for op in ("inv_safegcd", "inv_var"):
+        inv = O.cols_to_ints(H.field_op(0, 0, op, np.ascontiguousarray(A[:, :400]), field_id=f))
+        assert all((g * x * rinv * rinv) % p == 1 if x % p else g % p == 0 for g, x in zip(inv, a[:400])), op
+
+
+@pytest.mark.parametrize("curve_name,cid", [("secp256k1", H.SECP_LAZY_CURVE), ("sm2", H.SM2_LAZY_CURVE)])
+def test_hostsim_lazy_curve_ecdsa_golden(curve_name, cid):
+    ent = ECDSA[curve_name]
+    n = ent["n"]
     sec, pub = bytes.fromhex(ent["secrets"]), bytes.fromhex(ent["publics"])
     dig, sig = bytes.fromhex(ent["digests"]), bytes.fromhex(ent["sigs"])
     assert H.keygen(cid, ent["keygen_seed"], n) == (sec, pub)
@@ -178,7 +217,7 @@ def test_hostsim_lazy_curve_ecdsa_golden():
     assert H.sign(cid, bytes.fromhex(rt["digests"]), bytes.fromhex(rt["secrets"]), rt["nonce_seed"])[0].hex() == rt["sigs"]
 
 
-@pytest.mark.parametrize("cid,hs_curve", [(0, 0), (1, 1), (1, 2)])
+@pytest.mark.parametrize("cid,hs_curve", [(0, 0), (0, 3), (1, 1), (1, 2)])
 def test_hostsim_sign_group_retry(cid, hs_curve):
     """A forced s == 0 on attempt 0 INSIDE a 4-lane group (shared inversions) must retry that
     lane with a fresh nonce exactly as the reference does (test_protocol.cpp:196-228)."""
