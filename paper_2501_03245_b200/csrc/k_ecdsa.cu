@@ -12,7 +12,9 @@ namespace gecc {
 
 #ifndef GECC_VERIFY_BLOCKS
 #define GECC_VERIFY_BLOCKS 6      // blocks per SM (x 128 lanes): measured 4 / 5 / 6 = 22.70 / 22.10 / 22.03 ms per 2^20 (secp256k1)
-#define GECC_VERIFY_BLOCKS_SM2 5  // SM2: 44.85 / 44.32 / 44.80 ms
+#endif
+#ifndef GECC_VERIFY_BLOCKS_SM2
+#define GECC_VERIFY_BLOCKS_SM2 5  // SM2 (lazy field): 4 / 5 / 6 = 37.4 / 36.6 / 36.6 ms
 #endif
 constexpr int VERIFY_THREADS = 128;  // x 512 B of lane table = 64 KiB shared memory per block
 constexpr int SIGN_THREADS = 128;
