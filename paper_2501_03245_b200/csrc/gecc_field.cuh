@@ -328,12 +328,12 @@ GECC_HD fe sm2l_sub(const fe& a, const fe& b) {
     return r;
 }
 template <class F>
-constexpr bool field_is_weak() { return F::kind == KIND_SECP_LAZY || F::kind == KIND_SM2_LAZY; }
+constexpr bool field_is_weak_v = F::kind == KIND_SECP_LAZY || F::kind == KIND_SM2_LAZY;
 
 // field-aware predicates: canonical fields compare limbs, the lazy field compares mod q
 template <class F>
 GECC_HD bool fe_is_zero(const F& f, const fel<F>& a) {
-    if constexpr (field_is_weak<F>()) return lazy_is_zero(f, a);
+    if constexpr (field_is_weak_v<F>) return lazy_is_zero(f, a);
     else return fe_is_zero(a);
 }
 
