@@ -175,9 +175,15 @@ k_ecdh(size_t n, const uint8_t* __restrict__ sec, const uint8_t* __restrict__ pe
         status[i] = 3;
         return;
     }
-    build_lane_table<C>(p, qt);
     const PointSlots S = block_point_slots<VERIFY_THREADS>();
-    jac r = var_base_mul_mode<C, UNIFORM>(d, qt, UNIFORM ? nullptr : &S);
+    jac r;
+    if constexpr (UNIFORM) {
+        build_lane_table<C>(p, qt);
+        r = var_base_mul_uniform<C>(d, qt);
+    } else {
+        var_base_mul_point_slots<C>(d, p, qt, S);
+        r = S.load_point();
+    }
     if (jac_is_inf<C>(r)) {
         status[i] = 4;
         return;
@@ -229,9 +235,9 @@ k_upmul(size_t n, const uint32_t* __restrict__ k, const uint32_t* __restrict__ p
         return;
     }
     aff p{col_load(px, n, i), col_load(py, n, i)};
-    build_lane_table<C>(p, qt);
     const PointSlots S = block_point_slots<VERIFY_THREADS>();
-    store_affine<C>(var_base_mul_mode<C, false>(col_load(k, n, i), qt, &S), ox, oy, oinf, n, i);
+    var_base_mul_point_slots<C>(col_load(k, n, i), p, qt, S);
+    store_affine<C>(S.load_point(), ox, oy, oinf, n, i);
 }
 
 // ---- sm2b_bench_run support (bench.cpp:20-62): seeded inputs and the "jacobian-serial"

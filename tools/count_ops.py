@@ -55,8 +55,8 @@ def gadds(wg):  # expected fixed-base additions per scalar multiplication
 def main():
     subprocess.check_call(["make", "-C", HS, "count"], stdout=subprocess.DEVNULL)
     result = {}
-    # secp256k1 byte-record kernels run on the lazy plain curve (hostsim curve id 2)
-    for curve, name, hs in ((1, "secp256k1", 2), (0, "sm2", 0)):
+    # the byte-record kernels run on the lazy curves (hostsim curve ids 2 and 3)
+    for curve, name, hs in ((1, "secp256k1", 2), (0, "sm2", 3)):
         r4, r8 = run(4, curve, hs_curve=hs), run(8, curve, hs_curve=hs)
         ent = {}
         for op in r4:
