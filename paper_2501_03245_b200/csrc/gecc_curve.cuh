@@ -9,7 +9,7 @@
 // kernel exit.
 //
 //   jac_dbl   : a = 0    -> 2M + 5S ("dbl-2009-l")
-//               a = -3   -> 3M + 5S ("dbl-2001-b")
+//               a = -3   -> 4M + 4S ("dbl-2001-b" with Z3 = 2 Y Z)
 //               generic  -> the reference's own formula, curve.cpp:109-127
 //   jac_madd  : Jacobian + affine, 8M + 3S, the reference's mixed path
 //               (curve.cpp:136-141,152-166), complete
@@ -119,8 +119,7 @@ GECC_HD_CALL cjac<C> jac_dbl(const cjac<C>& p) {
         fe alpha = fe_add(f, fe_dbl(f, t), t);
         fe beta4 = fe_dbl(f, fe_dbl(f, beta));
         r.X = fe_sub(f, fe_sqr(f, alpha), fe_dbl(f, beta4));
-        fe yz = fe_add(f, p.Y, p.Z);
-        r.Z = fe_sub(f, fe_sub(f, fe_sqr(f, yz), gamma), delta);
+        r.Z = fe_dbl(f, fe_mul(f, p.Y, p.Z));  // 2 Y Z: fewer instructions than (Y + Z)^2 - gamma - delta here
         fe g2 = fe_sqr(f, gamma);
         fe g8 = fe_mul8(f, g2);
         r.Y = fe_sub(f, fe_mul(f, alpha, fe_sub(f, beta4, r.X)), g8);

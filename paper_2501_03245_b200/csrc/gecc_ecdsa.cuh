@@ -687,10 +687,9 @@ GECC_HD_CALL void jac_dbl_slots(const PointSlots S) {
             const fe t = fe_mul(f, fe_sub(f, X, d), fe_add(f, X, d));
             S.st(P::S4, fe_add(f, fe_dbl(f, t), t));                           // alpha
         }
-        {
-            const fe q = fe_sqr(f, fe_add(f, S.ld(P::SY), S.ld(P::SZ)));
-            S.st(P::SZ, fe_sub(f, fe_sub(f, q, S.ld(P::S2)), S.ld(P::S1)));    // Z3 = (Y + Z)^2 - gamma - delta
-        }
+        // Z3 = 2 Y Z as a product: (Y + Z)^2 - gamma - delta trades the multiply for a square and three
+        // additions, which is MORE instructions on a field whose reduction is additions
+        S.st(P::SZ, fe_dbl(f, fe_mul(f, S.ld(P::SY), S.ld(P::SZ))));
         {
             const fe a2 = fe_sqr(f, S.ld(P::S4));
             const fe beta4 = fe_dbl(f, fe_dbl(f, S.ld(P::S3)));
