@@ -55,6 +55,16 @@ GECC_HD bool scalar_in_range(const fe& v) {
     return !fe_is_zero(v) && fe_lt_modulus(Fn{}, v);
 }
 
+// k (already below n) or n - k, whichever is below 2^255 (n > 2^255 on every curve here), and
+// whether it was flipped: k G = -((n - k) G).  A scalar below 2^255 leaves the top window of the
+// signed recoding without a carry, so the fixed-base walk needs no addition of 2^256 G (one in
+// two scalars otherwise): the caller negates every digit instead.
+template <class Fn>
+GECC_HD fe scalar_fold_half(const fe& k, bool* flipped) {
+    *flipped = (k.w[7] >> 31) != 0;
+    return *flipped ? u256_sub(fe_modulus(Fn{}), k) : k;
+}
+
 GECC_HD uint64_t splitmix64(uint64_t* x) {  // protocol.cpp:13-19
     *x += 0x9E3779B97F4A7C15ull;
     uint64_t z = *x;
@@ -157,7 +167,8 @@ struct GTable {
 template <class C, int WG>
 GECC_HD jac fixed_base_mul(const fe& k_raw, const GTable<WG>& tab, const jac* start = nullptr) {
     const typename C::Fp f{};
-    fe k = scalar_reduce_once<typename C::Fn>(k_raw);
+    bool flip;
+    fe k = scalar_fold_half<typename C::Fn>(scalar_reduce_once<typename C::Fn>(k_raw), &flip);
     Recoded<WG> rc = recode_signed<WG>(k);
     // `start`: the additions continue into an existing accumulator (start + k G): the verify
     // lane adds u1 G onto u2 Q this way, which saves the separate complete addition at the end
@@ -172,7 +183,7 @@ GECC_HD jac fixed_base_mul(const fe& k_raw, const GTable<WG>& tab, const jac* st
         int d = digit(j);
         if (d == 0) continue;
         aff t = tab.load(j, d < 0 ? -d : d);
-        if (d < 0) t.y = fe_neg(f, t.y);
+        if ((d < 0) != flip) t.y = fe_neg(f, t.y);
         acc = jac_madd<C>(acc, t);
     }
     return acc;
@@ -850,7 +861,8 @@ GECC_HD void var_base_mul_point_slots(const fe& k, const aff& P, const LaneTable
 // the accumulator in the slots += k G (fixed_base_mul with `start`)
 template <class C, int WG>
 GECC_HD void fixed_base_add_slots(const fe& k_raw, const GTable<WG>& tab, const PointSlots S) {
-    const fe k = scalar_reduce_once<typename C::Fn>(k_raw);
+    bool flip;
+    const fe k = scalar_fold_half<typename C::Fn>(scalar_reduce_once<typename C::Fn>(k_raw), &flip);
     const Recoded<WG> rc = recode_signed<WG>(k);
     auto digit = [&](int j) { return j == 256 / WG ? (int)rc.carry : recoded_digit<WG>(rc, j); };
 #pragma unroll 1
@@ -861,7 +873,7 @@ GECC_HD void fixed_base_add_slots(const fe& k_raw, const GTable<WG>& tab, const 
         }
         const int d = digit(j);
         if (d == 0) continue;
-        jac_madd_slots<C>(S, RowSrc<C>{tab.tab + ((size_t)j * GTable<WG>::per_window + (size_t)((d < 0 ? -d : d) - 1)) * 16, 1, d < 0, false});
+        jac_madd_slots<C>(S, RowSrc<C>{tab.tab + ((size_t)j * GTable<WG>::per_window + (size_t)((d < 0 ? -d : d) - 1)) * 16, 1, (d < 0) != flip, false});
     }
 }
 

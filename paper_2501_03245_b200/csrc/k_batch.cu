@@ -10,6 +10,7 @@
 // until they are consumed, so no extra scratch array exists.  Results do not
 // depend on how elements are grouped (batch_invert.hpp:59-60), so they equal the
 // reference's for any LanePlan.
+#include <cstdlib>
 #include "gecc_batch.cuh"
 #include "gecc_host.h"
 
@@ -413,6 +414,9 @@ k_padd_bwd(size_t n, const uint32_t* __restrict__ px, const uint32_t* __restrict
 // HBM traffic ~ 257 B per pair against 385 B for the tiled form.  Elements [begin, end) of column
 // buffers with row pitch n: large batches run as two halves on two streams, so that the inversion
 // of one half's tile totals (one warp, pure latency) hides behind the other half's launches.
+#ifndef GECC_PADD_PF
+#define GECC_PADD_PF 1  // pairs of prefetch distance in the forward launch
+#endif
 template <int NL>
 __device__ __forceinline__ void prefetch_cols(const uint32_t* __restrict__ cols, size_t n, size_t i) {
 #pragma unroll
@@ -451,13 +455,20 @@ k_padd_fused_fwd(size_t n, size_t begin, size_t end, const uint32_t* __restrict_
     const typename C::Fp f{};
     const size_t first = begin + (size_t)blockIdx.x * (THREADS * K) + threadIdx.x;
     fe acc = fe_one(f);
+#pragma unroll
+    for (int k = 1; k < GECC_PADD_PF; ++k) {
+        if (k < K && first + (size_t)k * THREADS < end) {
+            prefetch_cols<NL>(px, n, first + (size_t)k * THREADS);
+            prefetch_cols<NL>(tx, n, first + (size_t)k * THREADS);
+        }
+    }
     if (first < end) acc = padd_denominator<C>(n, first, px, py, pinf, tx, ty, tinf);
 #pragma unroll 1
     for (int k = 1; k < K; ++k) {
         const size_t i = first + (size_t)k * THREADS;
-        if (i + THREADS < end) {  // the next pair's lines are requested before this pair's product
-            prefetch_cols<NL>(px, n, i + THREADS);
-            prefetch_cols<NL>(tx, n, i + THREADS);
+        if (k + GECC_PADD_PF < K && i + (size_t)GECC_PADD_PF * THREADS < end) {  // lines of the pair GECC_PADD_PF ahead are requested before this pair's product
+            prefetch_cols<NL>(px, n, i + (size_t)GECC_PADD_PF * THREADS);
+            prefetch_cols<NL>(tx, n, i + (size_t)GECC_PADD_PF * THREADS);
         }
         if (i < end) acc = fe_mul(f, acc, padd_denominator<C>(n, i, px, py, pinf, tx, ty, tinf));
     }
@@ -692,30 +703,33 @@ template <class C, int K>
 static cudaError_t fused_padd(int curve, size_t n, const uint32_t* px, const uint32_t* py, const uint8_t* pinf,
                               const uint32_t* tx, const uint32_t* ty, const uint8_t* tinf, uint32_t* ox, uint32_t* oy,
                               uint8_t* oinf, void* scratch, cudaStream_t s, const BatchAux& aux) {
-    // scratch: two sets (one per half) of totals | total_inv | others
-    const size_t half_tiles = fused_tiles(n, K) / 2 + 2;
-    const size_t tot_words = (half_tiles * 8 + 63) & ~(size_t)63;
-    const size_t oth_words = half_tiles * FUSED_THREADS * 8;
+    // scratch: two sets (one per part) of totals | total_inv | others, carved by each part's tile count
+    const size_t tile_pairs = (size_t)FUSED_THREADS * K;
     uint32_t* base = (uint32_t*)scratch;
-    uint32_t* set0 = base;
-    uint32_t* set1 = base + 2 * tot_words + oth_words;
     const bool split = aux.stream && aux.fork && aux.join && n >= ((size_t)1 << 18);
     if (!split) {  // one range: the whole scratch is one set, sized by the full tile count
         const size_t all_words = (fused_tiles(n, K) * 8 + 63) & ~(size_t)63;
         return fused_range<C, K>(curve, n, 0, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, base, base + all_words,
                                  base + 2 * all_words, s);
     }
-    // two halves on two streams: each half is fwd -> invert -> bwd; the inversion of one half (a
-    // single warp's latency) overlaps the other half's launches
-    const size_t mid = (n / 2 + (size_t)FUSED_THREADS * K - 1) / ((size_t)FUSED_THREADS * K) * ((size_t)FUSED_THREADS * K);
+    // two parts on two streams: each part is fwd -> invert -> bwd; the inversion of one part (a
+    // single warp's latency) overlaps the other part's launches
+    static const int split_pct = getenv("GECC_PADD_SPLIT") ? atoi(getenv("GECC_PADD_SPLIT")) : 50;
+    const size_t tiles = fused_tiles(n, K);
+    size_t tiles0 = tiles * (size_t)split_pct / 100;
+    if (tiles0 < 1) tiles0 = 1;
+    if (tiles0 >= tiles) tiles0 = tiles - 1;
+    const size_t mid = tiles0 * tile_pairs;
+    const size_t tot0 = (tiles0 * 8 + 63) & ~(size_t)63, tot1 = ((tiles - tiles0) * 8 + 63) & ~(size_t)63;
+    uint32_t* set0 = base;
+    uint32_t* set1 = base + 2 * tot0 + tiles0 * FUSED_THREADS * 8;
     cudaError_t e = cudaEventRecord(aux.fork, s);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(aux.stream, aux.fork, 0);
     if (e == cudaSuccess)
-        e = fused_range<C, K>(curve, n, 0, mid, px, py, pinf, tx, ty, tinf, ox, oy, oinf, set0, set0 + tot_words,
-                              set0 + 2 * tot_words, s);
+        e = fused_range<C, K>(curve, n, 0, mid, px, py, pinf, tx, ty, tinf, ox, oy, oinf, set0, set0 + tot0, set0 + 2 * tot0, s);
     if (e == cudaSuccess)
-        e = fused_range<C, K>(curve, n, mid, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, set1, set1 + tot_words,
-                              set1 + 2 * tot_words, aux.stream);
+        e = fused_range<C, K>(curve, n, mid, n, px, py, pinf, tx, ty, tinf, ox, oy, oinf, set1, set1 + tot1, set1 + 2 * tot1,
+                              aux.stream);
     if (e == cudaSuccess) e = cudaEventRecord(aux.join, aux.stream);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(s, aux.join, 0);
     return e;
