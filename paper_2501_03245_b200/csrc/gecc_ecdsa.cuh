@@ -833,6 +833,82 @@ GECC_HD_CALL void jac_mmadd_slots(const PointSlots S, const RowSrc<C> src) {
     S.st(P::SZ, S.ld(P::S2));                                                  // Z3 = h
 }
 
+// ---- the same additions on (X, Y, ZZ, ZZZ) = (X, Y, Z^2, Z^3): a walk made of mixed additions only
+// never needs Z itself (ZZ3 = ZZ PP, ZZZ3 = ZZZ PPP), which saves the squaring of Z in every
+// addition: 8M + 2S.  Slots: SX, SY, SZ = ZZ, S1 = ZZZ; infinity is ZZ == 0.  Complete.
+template <class C>
+GECC_HD_CALL void zz_madd_slots(const PointSlots S, const RowSrc<C> src) {
+    using P = PointSlots;
+    const typename C::Fp f{};
+    if (fe_is_zero(f, S.ld(P::SZ))) {  // accumulator at infinity: place the row
+        const aff q = src.point();
+        S.st(P::SX, q.x);
+        S.st(P::SY, q.y);
+        S.st(P::SZ, fe_one(f));
+        S.st(P::S1, fe_one(f));
+        return;
+    }
+    bool p_zero;
+    {
+        const fe p = fe_sub(f, fe_mul(f, src.x(), S.ld(P::SZ)), S.ld(P::SX));  // P = x2 ZZ - X
+        p_zero = fe_is_zero(f, p);
+        S.st(P::S2, p);
+    }
+    S.st(P::S3, fe_sub(f, fe_mul(f, src.y(), S.ld(P::S1)), S.ld(P::SY)));      // R = y2 ZZZ - Y
+    if (p_zero) {  // accumulator == +-q
+        if (fe_is_zero(f, S.ld(P::S3))) {  // == q: the tangent at the affine point
+            const aff q = src.point();
+            const jac d = jac_dbl<C>(jac{q.x, q.y, fe_one(f)});
+            const fe zz = fe_sqr(f, d.Z);
+            S.st(P::SX, d.X);
+            S.st(P::SY, d.Y);
+            S.st(P::SZ, zz);
+            S.st(P::S1, fe_mul(f, zz, d.Z));
+        } else {
+            S.st(P::SZ, fe_zero());
+            S.st(P::S1, fe_zero());
+        }
+        return;
+    }
+    S.st(P::S4, fe_sqr(f, S.ld(P::S2)));                                       // PP
+    S.st(P::S5, fe_mul(f, S.ld(P::S2), S.ld(P::S4)));                          // PPP
+    S.st(P::S2, fe_mul(f, S.ld(P::SX), S.ld(P::S4)));                          // Q = X PP
+    S.st(P::SZ, fe_mul(f, S.ld(P::SZ), S.ld(P::S4)));                          // ZZ3
+    S.st(P::S1, fe_mul(f, S.ld(P::S1), S.ld(P::S5)));                          // ZZZ3
+    {
+        const fe r2 = fe_sqr(f, S.ld(P::S3));
+        const fe q = S.ld(P::S2);
+        S.st(P::SX, fe_sub(f, fe_sub(f, fe_sub(f, r2, S.ld(P::S5)), q), q));   // X3 = R^2 - PPP - 2Q
+    }
+    S.st(P::S4, fe_mul(f, S.ld(P::SY), S.ld(P::S5)));                          // Y PPP
+    S.st(P::SY, fe_sub(f, fe_mul(f, S.ld(P::S3), fe_sub(f, S.ld(P::S2), S.ld(P::SX))), S.ld(P::S4)));
+}
+// the accumulator affine (ZZ == ZZZ == 1, the state right after a row was placed): 4M + 2S
+template <class C>
+GECC_HD_CALL void zz_mmadd_slots(const PointSlots S, const RowSrc<C> src) {
+    using P = PointSlots;
+    const typename C::Fp f{};
+    {
+        const fe p = fe_sub(f, src.x(), S.ld(P::SX));
+        if (fe_is_zero(f, p)) {
+            zz_madd_slots<C>(S, src);
+            return;
+        }
+        S.st(P::S2, p);
+    }
+    S.st(P::S3, fe_sub(f, src.y(), S.ld(P::SY)));                              // R
+    S.st(P::SZ, fe_sqr(f, S.ld(P::S2)));                                       // ZZ3 = PP
+    S.st(P::S1, fe_mul(f, S.ld(P::S2), S.ld(P::SZ)));                          // ZZZ3 = PPP
+    S.st(P::S2, fe_mul(f, S.ld(P::SX), S.ld(P::SZ)));                          // Q = X PP
+    {
+        const fe r2 = fe_sqr(f, S.ld(P::S3));
+        const fe q = S.ld(P::S2);
+        S.st(P::SX, fe_sub(f, fe_sub(f, fe_sub(f, r2, S.ld(P::S1)), q), q));
+    }
+    S.st(P::S4, fe_mul(f, S.ld(P::SY), S.ld(P::S1)));                          // Y PPP
+    S.st(P::SY, fe_sub(f, fe_mul(f, S.ld(P::S3), fe_sub(f, S.ld(P::S2), S.ld(P::SX))), S.ld(P::S4)));
+}
+
 // var_base_mul with the accumulator in the slots (result left there)
 template <class C>
 GECC_HD void var_base_mul_slots(const fe& k_raw, const LaneTable& tab, const PointSlots S) {
@@ -909,6 +985,33 @@ GECC_HD void fixed_base_add_slots(const fe& k_raw, const GTable<WG>& tab, const 
         else jac_madd_slots<C>(S, row);  // places the row while the accumulator is at infinity
         if (placed < 2) ++placed;
     }
+}
+
+// x(k G) as a fraction X / ZZ (what a signature needs of the nonce point): the walk of
+// fixed_base_add_slots from infinity on (X, Y, ZZ, ZZZ).  ZZ == 0 for k == 0 (mod n) only.
+template <class C, int WG>
+GECC_HD void fixed_base_x_slots(const fe& k_raw, const GTable<WG>& tab, const PointSlots S, fe* X, fe* ZZ) {
+    bool flip;
+    const fe k = scalar_fold_half<typename C::Fn>(scalar_reduce_once<typename C::Fn>(k_raw), &flip);
+    const Recoded<WG> rc = recode_signed<WG>(k);
+    auto digit = [&](int j) { return j == 256 / WG ? (int)rc.carry : recoded_digit<WG>(rc, j); };
+    S.st(PointSlots::SZ, fe_zero());
+    int placed = 0;
+#pragma unroll 1
+    for (int j = 0; j <= 256 / WG; ++j) {
+        if (j < 256 / WG) {
+            const int dn = digit(j + 1);
+            if (dn != 0) tab.prefetch(j + 1, dn < 0 ? -dn : dn);
+        }
+        const int d = digit(j);
+        if (d == 0) continue;
+        const RowSrc<C> row{tab.tab + ((size_t)j * GTable<WG>::per_window + (size_t)((d < 0 ? -d : d) - 1)) * 16, 1, (d < 0) != flip, false};
+        if (placed == 1) zz_mmadd_slots<C>(S, row);
+        else zz_madd_slots<C>(S, row);
+        if (placed < 2) ++placed;
+    }
+    *X = S.ld(PointSlots::SX);
+    *ZZ = S.ld(PointSlots::SZ);
 }
 
 template <class C, int WG, bool UNIFORM>
@@ -1034,12 +1137,17 @@ GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream
     const typename C::Fp fp{};
     const typename C::Fn fn{};
     fe X[K], Z[K], km[K], pz[K], pk[K];
+    const bool zz_walk = !UNIFORM && slots != nullptr;
 #pragma unroll 1
     for (int j = 0; j < K; ++j) {
         fe k = nonce_scalar<typename C::Fn>(seed, stream0 + j, 0);
-        jac R = fixed_base_mul_mode<C, WG, UNIFORM>(k, gt, slots);
-        X[j] = R.X;
-        Z[j] = R.Z;  // never zero for 0 < k < n
+        if (zz_walk) {  // only x = X / ZZ is needed: the walk on (X, Y, ZZ, ZZZ), Z[j] holds ZZ
+            fixed_base_x_slots<C, WG>(k, gt, *slots, &X[j], &Z[j]);
+        } else {
+            jac R = fixed_base_mul_mode<C, WG, UNIFORM>(k, gt, slots);
+            X[j] = R.X;
+            Z[j] = R.Z;  // never zero for 0 < k < n
+        }
         km[j] = fe_to_mont(fn, k);
         pz[j] = j ? fe_mul(fp, pz[j - 1], Z[j]) : Z[j];
         pk[j] = j ? fe_mul(fn, pk[j - 1], km[j]) : km[j];
@@ -1055,7 +1163,7 @@ GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream
             ik = fe_mul(fn, ik, km[j]);
         }
         uint8_t* out = sig64 + 64 * j;
-        fe x = fe_from_mont(fp, fe_mul(fp, X[j], fe_sqr(fp, zinv)));
+        fe x = fe_from_mont(fp, fe_mul(fp, X[j], zz_walk ? zinv : fe_sqr(fp, zinv)));
         fe r = scalar_reduce_once<typename C::Fn>(x);
         fe s = fe_zero();
         if (!fe_is_zero(r)) {

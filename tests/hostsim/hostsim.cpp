@@ -326,6 +326,76 @@ int hs_keygen(int curve, size_t n, uint64_t seed, uint64_t base, uint8_t* sec, u
 }
 }  // extern "C"
 
+// The additions on shared-memory slots (jac_madd_slots, jac_mmadd_slots, and the (X, Y, ZZ, ZZZ)
+// forms zz_madd_slots, zz_mmadd_slots) against jac_madd, for every pair (P_i, Q_i) with the
+// accumulator = P_i affine, P_i rescaled by Z = lam_i, and infinity.  Pairs with P == +-Q exercise
+// the exceptional branches.  Returns 0 or the number of the first failing check.
+template <class C>
+static int slot_adds_t(size_t n, const uint32_t* px, const uint32_t* py, const uint32_t* tx, const uint32_t* ty,
+                       const uint32_t* lam) {
+    const typename C::Fp f{};
+    auto same = [&](const jac& a, const jac& b) {  // projective equality
+        if (jac_is_inf<C>(a) || jac_is_inf<C>(b)) return jac_is_inf<C>(a) == jac_is_inf<C>(b);
+        const fe za2 = fe_sqr(f, a.Z), zb2 = fe_sqr(f, b.Z);
+        return fe_eq(f, fe_mul(f, a.X, zb2), fe_mul(f, b.X, za2)) &&
+               fe_eq(f, fe_mul(f, a.Y, fe_mul(f, zb2, b.Z)), fe_mul(f, b.Y, fe_mul(f, za2, a.Z)));
+    };
+    auto same_zz = [&](const PointSlots& S, const jac& b) {  // (X, Y, ZZ, ZZZ) in the slots against b
+        const fe zz = S.ld(PointSlots::SZ), zzz = S.ld(PointSlots::S1);
+        if (fe_is_zero(f, zz) || jac_is_inf<C>(b)) return fe_is_zero(f, zz) == jac_is_inf<C>(b);
+        const fe zb2 = fe_sqr(f, b.Z);
+        return fe_eq(f, fe_mul(f, S.ld(PointSlots::SX), zb2), fe_mul(f, b.X, zz)) &&
+               fe_eq(f, fe_mul(f, S.ld(PointSlots::SY), fe_mul(f, zb2, b.Z)), fe_mul(f, b.Y, zzz));
+    };
+    for (size_t i = 0; i < n; ++i) {
+        const aff P{col_get(px, n, i), col_get(py, n, i)}, Q{col_get(tx, n, i), col_get(ty, n, i)};
+        uint32_t row[16];
+        for (int w = 0; w < 8; ++w) { row[w] = Q.x.w[w]; row[8 + w] = Q.y.w[w]; }
+        const fe l = col_get(lam, n, i), l2 = fe_sqr(f, l);
+        const jac accs[3] = {jac{P.x, P.y, fe_one(f)}, jac{fe_mul(f, P.x, l2), fe_mul(f, P.y, fe_mul(f, l2, l)), l},
+                             jac_infinity<C>()};
+        for (int neg = 0; neg < 2; ++neg) {
+            aff q = Q;
+            if (neg) q.y = fe_neg(f, q.y);
+            const RowSrc<C> src{row, 1, neg != 0, false};
+            for (int a = 0; a < 3; ++a) {
+                const jac want = jac_madd<C>(accs[a], q);
+                fe mem[PointSlots::COUNT];
+                PointSlots S{mem};
+                S.store_point(accs[a]);
+                jac_madd_slots<C>(S, src);
+                if (!same(S.load_point(), want)) return 100 + 10 * a + neg;
+                if (a == 0) {
+                    S.store_point(accs[a]);
+                    jac_mmadd_slots<C>(S, src);
+                    if (!same(S.load_point(), want)) return 200 + neg;
+                }
+                // (X, Y, ZZ, ZZZ)
+                S.st(PointSlots::SX, accs[a].X);
+                S.st(PointSlots::SY, accs[a].Y);
+                S.st(PointSlots::SZ, fe_sqr(f, accs[a].Z));
+                S.st(PointSlots::S1, fe_mul(f, fe_sqr(f, accs[a].Z), accs[a].Z));
+                zz_madd_slots<C>(S, src);
+                if (!same_zz(S, want)) return 300 + 10 * a + neg;
+                if (a == 0) {
+                    S.st(PointSlots::SX, P.x);
+                    S.st(PointSlots::SY, P.y);
+                    S.st(PointSlots::SZ, fe_one(f));
+                    S.st(PointSlots::S1, fe_one(f));
+                    zz_mmadd_slots<C>(S, src);
+                    if (!same_zz(S, want)) return 400 + neg;
+                }
+            }
+        }
+    }
+    return 0;
+}
+extern "C" int hs_slot_adds(int curve, size_t n, const uint32_t* px, const uint32_t* py, const uint32_t* tx,
+                            const uint32_t* ty, const uint32_t* lam) {
+    return curve == 0 ? slot_adds_t<Sm2Curve>(n, px, py, tx, ty, lam) : curve == 3 ? slot_adds_t<Sm2LCurve>(n, px, py, tx, ty, lam)
+         : curve == 2 ? slot_adds_t<SecpLCurve>(n, px, py, tx, ty, lam) : slot_adds_t<SecpCurve>(n, px, py, tx, ty, lam);
+}
+
 // GLV split of secp256k1 scalars: out = m1 (8 limbs) | m2 (8 limbs) per element, signs in sg[2*i..]
 extern "C" int hs_glv_split(size_t n, const uint32_t* k, uint32_t* m1, uint32_t* m2, uint8_t* sg) {
     for (size_t i = 0; i < n; ++i) {

@@ -69,6 +69,12 @@ def batch_upmul(curve, k, P):
     return o
 
 
+def slot_adds(curve, P, Q, lam):
+    """0 when every slot-form addition agrees with jac_madd on the pairs (P_i, Q_i); see hs_slot_adds."""
+    n = P[0].shape[1]
+    return lib().hs_slot_adds(curve, C.c_size_t(n), _p(P[0]), _p(P[1]), _p(Q[0]), _p(Q[1]), _p(lam))
+
+
 def sign(curve, dig, sec, seed, lane_base=0):
     n = len(dig) // 32
     sig = (C.c_uint8 * max(1, 64 * n))()

@@ -300,3 +300,24 @@ def test_hostsim_sign_with_explicit_nonces(cid, hs_curve):
         assert sig[64 * i:64 * i + 64] == bytes(64)
     for i in (0, 1, 2, 5, 7, 8, 9):
         assert sig[64 * i:64 * i + 64] == want[1][64 * i:64 * i + 64]
+
+
+@pytest.mark.parametrize("cid,hs_curve", [(0, 0), (0, 3), (1, 1), (1, 2)])
+def test_hostsim_slot_additions_complete(cid, hs_curve):
+    """jac_madd_slots / jac_mmadd_slots and the (X, Y, ZZ, ZZZ) forms of the fixed-base walk against
+    jac_madd: generic pairs, Q == P (tangent), Q == -P (infinity), accumulator affine, rescaled by a
+    random Z, and at infinity; each pair also with the row negated."""
+    from tests.util import ints_to_cols
+    c = E.CURVES[cid]
+    rng = random.Random(4242 + hs_curve)
+    a = [rng.randrange(1, c.n) for _ in range(12)]
+    b = [rng.randrange(1, c.n) for _ in range(12)]
+    for i in (1, 5):
+        b[i] = a[i]            # same point
+    for i in (2, 7):
+        b[i] = c.n - a[i]      # inverse point
+    P = H.batch_fpmul(hs_curve, ints_to_cols(a))
+    Q = H.batch_fpmul(hs_curve, ints_to_cols(b))
+    assert not P[2].any() and not Q[2].any()
+    lam = ints_to_cols([rng.randrange(2, 1 << 250) for _ in a])
+    assert H.slot_adds(hs_curve, P, Q, lam) == 0

@@ -17,6 +17,7 @@ timeout 2400 bash tools/profile_r02.sh $T lists verify sign padd padd16 msm > $O
 timeout 900 python tools/sweep.py > $O/${T}_sweep.log 2>&1; mv $O/sweep.json $O/${T}_sweep.json 2>/dev/null
 timeout 600 python tools/msm_sweep.py secp256k1 bls12_377 > $O/${T}_msm_sweep.jsonl 2> $O/${T}_msm_sweep.err
 timeout 120 tools/exp/_build/inv_exp > $O/${T}_inversion_latency.txt 2>&1
+timeout 120 tools/exp/_build/padd_timeline > $O/${T}_padd16_timeline.txt 2>&1
 # the launch the driver uses for N > 1, with one rank: torchrun rendezvous, NCCL init, the MSM exchange path
 GECC_BENCH_FORCE_EXCHANGE=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29517 bench.py --gpus 1 --steps 3 --warmup 3 --no-cpu-baseline > $O/${T}_bench_torchrun_1rank.json 2> $O/${T}_bench_torchrun_1rank.err
 (python -c "import __graft_entry__ as g; g.smoke()" > $O/${T}_smoke.log 2>&1; echo "smoke rc $?" >> $O/${T}_smoke.log)
