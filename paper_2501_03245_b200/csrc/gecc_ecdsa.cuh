@@ -1148,12 +1148,16 @@ GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream
             X[j] = R.X;
             Z[j] = R.Z;  // never zero for 0 < k < n
         }
-        km[j] = fe_to_mont(fn, k);
+        // the nonces stay PLAIN in the Montgomery products mod n: p_j = k_0 ... k_j / R^j, so the
+        // inverse of the last one, brought to Montgomery form, is I_j = R^(j+1) / (k_0 ... k_j) for
+        // j = K - 1, and the unwinding below yields k_j^-1 R (Montgomery form) from I_j p_(j-1) / R
+        // and I_(j-1) from I_j k_j / R -- no conversion of the nonces
+        km[j] = k;
         pz[j] = j ? fe_mul(fp, pz[j - 1], Z[j]) : Z[j];
         pk[j] = j ? fe_mul(fn, pk[j - 1], km[j]) : km[j];
     }
     fe iz = fe_inv(fp, pz[K - 1]);                                   // (Z_0 ... Z_{K-1})^-1
-    fe ik = fe_to_mont(fn, safegcd_inverse(fn, fe_from_mont(fn, pk[K - 1])));  // Montgomery form
+    fe ik = fe_to_mont(fn, safegcd_inverse(fn, pk[K - 1]));
 #pragma unroll 1
     for (int j = K - 1; j >= 0; --j) {
         fe zinv = j ? fe_mul(fp, iz, pz[j - 1]) : iz;
@@ -1166,10 +1170,8 @@ GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream
         fe x = fe_from_mont(fp, fe_mul(fp, X[j], zz_walk ? zinv : fe_sqr(fp, zinv)));
         fe r = scalar_reduce_once<typename C::Fn>(x);
         fe s = fe_zero();
-        if (!fe_is_zero(r)) {
-            fe s_m = fe_mul(fn, kinv_m, fe_add(fn, fe_to_mont(fn, e[j]),
-                                               fe_mul(fn, fe_to_mont(fn, r), fe_to_mont(fn, d[j]))));
-            s = fe_from_mont(fn, s_m);
+        if (!fe_is_zero(r)) {  // s = k^-1 (e + r d): (r)(d R) / R is r d plain, (k^-1 R)(e + r d) / R is s plain
+            s = fe_mul(fn, kinv_m, fe_add(fn, e[j], fe_mul(fn, r, fe_to_mont(fn, d[j]))));
         }
         if (fe_is_zero(r) || fe_is_zero(s)) {  // retry with fresh nonces (protocol.cpp:142-160)
             status[j] = sign_lane<C, WG, UNIFORM>(e[j], d[j], seed, stream0 + j, gt, out, 1, slots);
