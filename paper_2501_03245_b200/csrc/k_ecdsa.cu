@@ -57,12 +57,17 @@ k_verify_gtab(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restri
 // flags[0] is set when any secret is zero or >= n: the whole call is malformed
 // (capi.cpp:181-184) and the host discards the outputs.  Each thread signs SIGN_K
 // consecutive lanes and shares the two inversions among them (sign_lanes).
+#ifndef GECC_SIGN_SMALL_LOG2
+#define GECC_SIGN_SMALL_LOG2 18
+#endif
+constexpr int SIGN_K_SMALL = 4;
+constexpr size_t SIGN_SMALL_MAX = (size_t)1 << GECC_SIGN_SMALL_LOG2;
 constexpr int SIGN_K = GECC_SIGN_K;  // gecc_ecdsa.cuh: measured 4 / 8 / 16 lanes per thread = 2.87 / 2.76 / 3.09 ms per 2^20
 
 #ifndef GECC_SIGN_BLOCKS
 #define GECC_SIGN_BLOCKS 4
 #endif
-template <class C, bool UNIFORM>
+template <class C, bool UNIFORM, int SIGN_K = GECC_SIGN_K>
 __global__ void __launch_bounds__(SIGN_THREADS, GECC_SIGN_BLOCKS)
 k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ sec, uint64_t seed,
        uint64_t lane_base, const uint32_t* __restrict__ gtab, uint8_t* __restrict__ sig,
@@ -385,6 +390,16 @@ cudaError_t launch_sign(int curve, size_t n, const uint8_t* dig, const uint8_t* 
                         uint64_t lane_base, const uint32_t* gtab, uint8_t* sig, int32_t* status,
                         uint32_t* flags, cudaStream_t s, bool uniform) {
     if (n == 0) return cudaSuccess;
+    // lanes per thread: SIGN_K (8) shares the two inversions best; a launch that would leave the chip
+    // half empty at 8 (the chunks of the host pipeline, small batches) takes 4 and twice the blocks
+    if (!uniform && n <= SIGN_SMALL_MAX) {
+        const int b = blocks_for((n + SIGN_K_SMALL - 1) / SIGN_K_SMALL, SIGN_THREADS);
+        if (curve == CURVE_SECP)
+            k_sign<SecpEcdsaCurve, false, SIGN_K_SMALL><<<b, SIGN_THREADS, 0, s>>>(n, dig, sec, seed, lane_base, gtab, sig, status, flags);
+        else
+            k_sign<Sm2EcdsaCurve, false, SIGN_K_SMALL><<<b, SIGN_THREADS, 0, s>>>(n, dig, sec, seed, lane_base, gtab, sig, status, flags);
+        return cudaGetLastError();
+    }
     const int b = blocks_for((n + SIGN_K - 1) / SIGN_K, SIGN_THREADS);
     GECC_BY_CURVE_MODE(curve, uniform, k_sign, b, SIGN_THREADS, n, dig, sec, seed, lane_base, gtab, sig, status, flags);
     return cudaGetLastError();
