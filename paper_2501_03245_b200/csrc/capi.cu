@@ -418,7 +418,10 @@ sm2b_status gecc_microbench(sm2b_ctx* ctx, int which, int iters, double* ops_per
 namespace {
 constexpr size_t PIPE_MIN_CHUNK = (size_t)1 << 17;
 constexpr size_t PIPE_HEAD_CHUNK = (size_t)1 << 16;
-constexpr int PIPE_MAX_CHUNKS = 4;
+#ifndef GECC_PIPE_MAX_CHUNKS
+#define GECC_PIPE_MAX_CHUNKS 4
+#endif
+constexpr int PIPE_MAX_CHUNKS = GECC_PIPE_MAX_CHUNKS;
 
 // Up to PIPE_MAX_CHUNKS equal chunks of at least PIPE_MIN_CHUNK records, preceded -- when the
 // batch is large enough -- by a short head chunk: only the first upload is exposed (nothing
