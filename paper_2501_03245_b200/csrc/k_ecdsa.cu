@@ -5,6 +5,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "gecc_batch.cuh"
 #include "gecc_ecdsa.cuh"
 #include "gecc_host.h"
 
@@ -147,14 +148,31 @@ __global__ void __launch_bounds__(SIGN_THREADS)
 k_keygen(size_t n, uint64_t seed, uint64_t lane_base, const uint32_t* __restrict__ gtab,
          uint8_t* __restrict__ sec, uint8_t* __restrict__ pub) {
     const size_t i = blockIdx.x * (size_t)SIGN_THREADS + threadIdx.x;
-    if (i >= n) return;
     const typename C::Fp f{};
     GTable<GECC_WG> gt{gtab};
-    fe d = nonce_scalar<typename C::Fn>(seed, lane_base + i, 0);
-    be32_store(sec + 32 * i, d);
-    const PointSlots S = block_point_slots<SIGN_THREADS>();
-    jac r = fixed_base_mul_mode<C, GECC_WG, UNIFORM>(d, gt, UNIFORM ? nullptr : &S);
-    encode_point<C>(pub + 65 * i, jac_to_aff_with<C>(r, fe_inv(f, r.Z)));
+    if constexpr (UNIFORM) {  // constant structure: every lane inverts its own Z with the branch-free rounds
+        if (i >= n) return;
+        fe d = nonce_scalar<typename C::Fn>(seed, lane_base + i, 0);
+        be32_store(sec + 32 * i, d);
+        jac r = fixed_base_mul_mode<C, GECC_WG, true>(d, gt, nullptr);
+        encode_point<C>(pub + 65 * i, jac_to_aff_with<C>(r, fe_inv(f, r.Z)));
+    } else {
+        // the block's Z coordinates share ONE inversion (warp-shuffle scans + the warp-cooperative
+        // safegcd of coop_block_inverse) instead of one safegcd per lane; lanes past n carry 1
+        __shared__ uint32_t sm_scan[2 * C::Fp::N * (SIGN_THREADS / 32)];
+        const bool live = i < n;
+        jac r = jac_infinity<C>();
+        fe z = fe_one(f);
+        if (live) {
+            fe d = nonce_scalar<typename C::Fn>(seed, lane_base + i, 0);
+            be32_store(sec + 32 * i, d);
+            const PointSlots S = block_point_slots<SIGN_THREADS>();
+            r = fixed_base_mul_mode<C, GECC_WG, false>(d, gt, &S);
+            z = r.Z;  // never zero for 0 < d < n
+        }
+        const fe zinv = coop_block_inverse<decltype(f), SIGN_THREADS>(f, z, sm_scan);
+        if (live) encode_point<C>(pub + 65 * i, jac_to_aff_with<C>(r, zinv));
+    }
 }
 
 // capi.cpp:230-261 + protocol.cpp:224-263.  status: 0 ok, 3 invalid peer,
