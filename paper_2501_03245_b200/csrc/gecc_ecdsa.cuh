@@ -1130,44 +1130,56 @@ GECC_HD int sign_lane_nonce(const fe& e, const fe& d, const fe& k, const GTable<
 // cross-thread traffic is needed.  A lane that has to retry (r == 0 or s == 0, probability
 // ~2^-255 unless forced) falls back to sign_lane from attempt 1, which reproduces the
 // reference's per-lane retry sequence exactly.
+// the state of a group between its two phases: nonce-point fractions, nonces, prefix products
+template <int K>
+struct SignGroup {
+    fe X[K], Z[K], km[K], pz[K], pk[K];
+};
+// phase 1: the K nonce points and the running products of their denominators and of the nonces
 template <class C, int WG, int K, bool UNIFORM = false>
-GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream0,
-                        const GTable<WG>& gt, uint8_t* sig64, int* status, bool aligned = false,
-                        const PointSlots* slots = nullptr) {
+GECC_HD void sign_lanes_walk(uint64_t seed, uint64_t stream0, const GTable<WG>& gt, const PointSlots* slots,
+                             SignGroup<K>& g) {
     const typename C::Fp fp{};
     const typename C::Fn fn{};
-    fe X[K], Z[K], km[K], pz[K], pk[K];
     const bool zz_walk = !UNIFORM && slots != nullptr;
 #pragma unroll 1
     for (int j = 0; j < K; ++j) {
         fe k = nonce_scalar<typename C::Fn>(seed, stream0 + j, 0);
         if (zz_walk) {  // only x = X / ZZ is needed: the walk on (X, Y, ZZ, ZZZ), Z[j] holds ZZ
-            fixed_base_x_slots<C, WG>(k, gt, *slots, &X[j], &Z[j]);
+            fixed_base_x_slots<C, WG>(k, gt, *slots, &g.X[j], &g.Z[j]);
         } else {
             jac R = fixed_base_mul_mode<C, WG, UNIFORM>(k, gt, slots);
-            X[j] = R.X;
-            Z[j] = R.Z;  // never zero for 0 < k < n
+            g.X[j] = R.X;
+            g.Z[j] = R.Z;  // never zero for 0 < k < n
         }
         // the nonces stay PLAIN in the Montgomery products mod n: p_j = k_0 ... k_j / R^j, so the
         // inverse of the last one, brought to Montgomery form, is I_j = R^(j+1) / (k_0 ... k_j) for
-        // j = K - 1, and the unwinding below yields k_j^-1 R (Montgomery form) from I_j p_(j-1) / R
+        // j = K - 1, and the unwinding yields k_j^-1 R (Montgomery form) from I_j p_(j-1) / R
         // and I_(j-1) from I_j k_j / R -- no conversion of the nonces
-        km[j] = k;
-        pz[j] = j ? fe_mul(fp, pz[j - 1], Z[j]) : Z[j];
-        pk[j] = j ? fe_mul(fn, pk[j - 1], km[j]) : km[j];
+        g.km[j] = k;
+        g.pz[j] = j ? fe_mul(fp, g.pz[j - 1], g.Z[j]) : g.Z[j];
+        g.pk[j] = j ? fe_mul(fn, g.pk[j - 1], g.km[j]) : g.km[j];
     }
-    fe iz = fe_inv(fp, pz[K - 1]);                                   // (Z_0 ... Z_{K-1})^-1
-    fe ik = fe_to_mont(fn, safegcd_inverse(fn, pk[K - 1]));
+}
+// phase 2: iz = pz[K-1]^-1 (representation of the field), ik = R / pk[K-1] mod n (the plain inverse
+// of the residue pk[K-1], in Montgomery form); unwinds both and writes the signatures
+template <class C, int WG, int K, bool UNIFORM = false>
+GECC_HD void sign_lanes_finish(const fe* e, const fe* d, uint64_t seed, uint64_t stream0, const GTable<WG>& gt,
+                               uint8_t* sig64, int* status, bool aligned, const PointSlots* slots,
+                               const SignGroup<K>& g, fe iz, fe ik) {
+    const typename C::Fp fp{};
+    const typename C::Fn fn{};
+    const bool zz_walk = !UNIFORM && slots != nullptr;
 #pragma unroll 1
     for (int j = K - 1; j >= 0; --j) {
-        fe zinv = j ? fe_mul(fp, iz, pz[j - 1]) : iz;
-        fe kinv_m = j ? fe_mul(fn, ik, pk[j - 1]) : ik;
+        fe zinv = j ? fe_mul(fp, iz, g.pz[j - 1]) : iz;
+        fe kinv_m = j ? fe_mul(fn, ik, g.pk[j - 1]) : ik;
         if (j) {
-            iz = fe_mul(fp, iz, Z[j]);
-            ik = fe_mul(fn, ik, km[j]);
+            iz = fe_mul(fp, iz, g.Z[j]);
+            ik = fe_mul(fn, ik, g.km[j]);
         }
         uint8_t* out = sig64 + 64 * j;
-        fe x = fe_from_mont(fp, fe_mul(fp, X[j], zz_walk ? zinv : fe_sqr(fp, zinv)));
+        fe x = fe_from_mont(fp, fe_mul(fp, g.X[j], zz_walk ? zinv : fe_sqr(fp, zinv)));
         fe r = scalar_reduce_once<typename C::Fn>(x);
         fe s = fe_zero();
         if (!fe_is_zero(r)) {  // s = k^-1 (e + r d): (r)(d R) / R is r d plain, (k^-1 R)(e + r d) / R is s plain
@@ -1181,6 +1193,18 @@ GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream
         be32_store_a(out + 32, s, aligned);
         status[j] = LANE_OK;
     }
+}
+template <class C, int WG, int K, bool UNIFORM = false>
+GECC_HD void sign_lanes(const fe* e, const fe* d, uint64_t seed, uint64_t stream0,
+                        const GTable<WG>& gt, uint8_t* sig64, int* status, bool aligned = false,
+                        const PointSlots* slots = nullptr) {
+    const typename C::Fp fp{};
+    const typename C::Fn fn{};
+    SignGroup<K> g;
+    sign_lanes_walk<C, WG, K, UNIFORM>(seed, stream0, gt, slots, g);
+    const fe iz = fe_inv(fp, g.pz[K - 1]);                                   // (Z_0 ... Z_{K-1})^-1
+    const fe ik = fe_to_mont(fn, safegcd_inverse(fn, g.pk[K - 1]));
+    sign_lanes_finish<C, WG, K, UNIFORM>(e, d, seed, stream0, gt, sig64, status, aligned, slots, g, iz, ik);
 }
 
 // One lane of sm2b_verify: raw records in, 0/1 out.

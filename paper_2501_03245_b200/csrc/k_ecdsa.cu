@@ -74,7 +74,7 @@ k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ se
        uint64_t lane_base, const uint32_t* __restrict__ gtab, uint8_t* __restrict__ sig,
        int32_t* __restrict__ status, uint32_t* __restrict__ flags) {
     const size_t i0 = (blockIdx.x * (size_t)SIGN_THREADS + threadIdx.x) * SIGN_K;
-    if (i0 >= n) return;
+    if (UNIFORM && i0 >= n) return;  // the fast mode meets block-wide barriers below: no early exit there
     GTable<GECC_WG> gt{gtab};
     // accumulator and temporaries of the fixed-base additions rest in shared memory (PointSlots)
     const PointSlots S = block_point_slots<SIGN_THREADS>();
@@ -89,7 +89,34 @@ k_sign(size_t n, const uint8_t* __restrict__ dig, const uint8_t* __restrict__ se
         e[j] = scalar_reduce_once<typename C::Fn>(be32_load_a(dig + 32 * (i0 + j), al_in));
         if (!scalar_in_range<typename C::Fn>(d[j])) all_ok = false;
     }
-    if (all_ok) {
+    if constexpr (!UNIFORM) {
+        // The two inversions of a group (its denominators mod p, its nonces mod n) are shared by the
+        // whole BLOCK: warp-shuffle scans over the 128 group totals and one warp-cooperative safegcd
+        // each (coop_block_inverse) instead of two safegcd chains per thread.  Every thread of the
+        // block takes part; a thread without a full valid group contributes 1.
+        __shared__ uint32_t sm_scan[2 * 8 * (SIGN_THREADS / 32)];
+        const typename C::Fp fp{};
+        const typename C::Fn fn{};
+        SignGroup<SIGN_K> g;
+        fe tz = fe_one(fp), tk = fe_one(fn);
+        if (all_ok) {
+            sign_lanes_walk<C, GECC_WG, SIGN_K, false>(seed, lane_base + i0, gt, slots, g);
+            tz = g.pz[SIGN_K - 1];
+            tk = g.pk[SIGN_K - 1];
+        }
+        const fe iz = coop_block_inverse<decltype(fp), SIGN_THREADS>(fp, tz, sm_scan);
+        __syncthreads();  // sm_scan is reused
+        // the Montgomery-domain inverse of the residue tk is R^2 / tk; one reduction makes it R / tk
+        const fe ik = fe_from_mont(fn, coop_block_inverse<decltype(fn), SIGN_THREADS>(fn, tk, sm_scan));
+        if (all_ok) {
+            int st[SIGN_K];
+            sign_lanes_finish<C, GECC_WG, SIGN_K, false>(e, d, seed, lane_base + i0, gt, sig + 64 * i0, st, al_out, slots, g, iz, ik);
+#pragma unroll
+            for (int j = 0; j < SIGN_K; ++j) status[i0 + j] = st[j];
+            return;
+        }
+        if (i0 >= n) return;
+    } else if (all_ok) {
         int st[SIGN_K];
         sign_lanes<C, GECC_WG, SIGN_K, UNIFORM>(e, d, seed, lane_base + i0, gt, sig + 64 * i0, st, al_out, slots);
 #pragma unroll
